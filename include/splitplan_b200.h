@@ -1,0 +1,289 @@
+/*
+ * splitplan_b200.h -- C ABI of the B200-native SplitLLM placement engine.
+ *
+ * The reference (`splitplan`, /root/reference/pkg/src/splitplan) is a pure
+ * Python package with no FFI; its "operator API" is the set of module-level
+ * functions.  Each entry point below replaces one of them, batched over many
+ * independent instances (requests / scenarios), and is what a Python (ctypes),
+ * C or C++ host binds.  See INTEGRATION.md for the ctypes stub.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *    unless the name ends in `_host`.  The caller owns every buffer; the
+ *    library never frees caller memory and keeps no allocations between
+ *    calls.  `stream` is a cudaStream_t passed as void*.
+ *  - Every function returns an int status (SP_OK == 0).  Nothing throws across
+ *    the ABI.  On failure `sp_last_error()` (thread-local) describes it.
+ *  - "Infeasible" is a result, not an error (planner.py:104-107): the policy
+ *    is all-server with feasible == 0 and its latency computed.
+ *  - Instances are batched in CSR form over layers (sp_instances).
+ *  - The functions are reentrant across host threads given distinct streams
+ *    and workspaces.
+ */
+#ifndef SPLITPLAN_B200_H
+#define SPLITPLAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+
+enum sp_status {
+  SP_OK = 0,
+  SP_ERR_INVALID = 1,    /* bad argument (wrapper raises ValueError) */
+  SP_ERR_CUDA = 2,       /* CUDA runtime error */
+  SP_ERR_WORKSPACE = 3,  /* workspace too small; see sp_last_required_workspace() */
+  SP_ERR_BACKTRACE = 4,  /* planner.py:168-169/177-178 AssertionError (NaN tables) */
+  SP_ERR_DEADLOCK = 5,   /* throughput_sim.py:243-246 CapacityDeadlockError */
+  SP_ERR_UNSUPPORTED = 6 /* size outside what the engine handles (e.g. W_eff >= 2^31) */
+};
+
+enum sp_prefix_planner { SP_GREEDY = 0, SP_ALL_SERVER = 1, SP_ALL_CLIENT = 2 };
+
+/* A batch of integer placement instances (problem.py:118-185 PlanProblem),
+ * CSR over layers: instance k owns layers [layer_off[k], layer_off[k+1]). */
+typedef struct sp_instances {
+  int64_t n;                      /* number of instances */
+  int64_t total_layers;           /* == layer_off[n] */
+  const int64_t* layer_off;       /* [n+1] */
+  const int64_t* client_units;    /* [total_layers] i_k */
+  const int64_t* server_units;    /* [total_layers] s_k */
+  const int64_t* up_units;        /* [total_layers] u_k */
+  const int64_t* down_units;      /* [total_layers] d_k */
+  const double* r;                /* [total_layers] resource value r_k */
+  const int64_t* budget;          /* [n] integer budget W */
+  const uint8_t* source_at_client;/* [n] 1 = data originates at the client */
+  const int8_t* must_end_at;      /* [n] or NULL: -1 free, 0 server, 1 client */
+} sp_instances;
+
+/* Planner output (planner.py:42-51 PlacementPolicy), one record per instance. */
+typedef struct sp_policies {
+  uint8_t* pi;               /* [total_layers] 1 = client, 0 = server */
+  double* client_value;      /* [n] numpy-order sum of r over client layers */
+  double* server_load;       /* [n] numpy-order sum of r over server layers */
+  int64_t* integer_latency;  /* [n] exact unit latency of pi */
+  uint8_t* feasible;         /* [n] */
+  int32_t* status;           /* [n] SP_OK or SP_ERR_BACKTRACE */
+} sp_policies;
+
+/* ---- library ------------------------------------------------------------ */
+
+int sp_abi_version(void);
+const char* sp_last_error(void);
+/* bytes the last SP_ERR_WORKSPACE call needed */
+size_t sp_last_required_workspace(void);
+
+/* Instrumentation (thread-local, off by default).  While enabled, every
+ * DP-stage kernel launch is bracketed by CUDA events on its stream and every
+ * kernel the library launches is counted. sp_profile_collect synchronises
+ * the recorded events and returns: total DP-stage kernel ms, DP-stage
+ * launches, DP cells and algorithmic DP bytes those launches processed, and
+ * the count of all library kernel launches; then resets the counters. */
+void sp_profile_enable(int on);
+int sp_profile_collect(double* dp_kernel_ms, int64_t* dp_launches, double* dp_cells,
+                       double* dp_bytes, int64_t* all_launches);
+
+/* ---- planner (planner.py) ---------------------------------------------- */
+
+/* W_eff = min(budget, sum_k max(i_k+d_k, s_k+u_k)) per instance.
+ * Replaces planner.py:120-125 `_effective_budget`.  w_eff: device int64[n]. */
+int sp_effective_budget(const sp_instances* in, int64_t* w_eff, void* stream);
+
+/* Optimal DP placement for every instance: cost-table prep, the DP stage
+ * kernel over the integer budget axis, end-side argmax and back-pointer walk.
+ * Replaces planner.py:182-202 `plan_dp` (with :128-143 `build_dp_tables`,
+ * :146-179 `_backtrace`, :88-107 `_finish`/`_infeasible`).
+ * `ws` is scratch of `ws_bytes` bytes (device); instances are processed in
+ * waves that fit it.  SP_ERR_WORKSPACE if a single instance does not fit.
+ * Synchronises `stream` once (to size the waves) before returning. */
+int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes,
+               void* stream);
+
+/* Full DP tables of ONE instance (in->n == 1) as float64, row-major
+ * [(L+1) x (w_eff+1)], unreachable cells = -inf.  Replaces planner.py:128-143
+ * `build_dp_tables`.  w_eff must equal sp_effective_budget()'s value. */
+int sp_build_dp_tables(const sp_instances* in, int64_t w_eff, double* client_table,
+                       double* server_table, void* ws, size_t ws_bytes, void* stream);
+
+/* Prefix planners: greedy longest feasible client prefix, all-server,
+ * all-client.  Replaces planner.py:205-214 `plan_greedy` and :217-225
+ * `plan_trivial`.  `which` is an sp_prefix_planner. */
+int sp_plan_prefix(const sp_instances* in, int32_t which, sp_policies* out, void* stream);
+
+/* Exhaustive planner over all 2^L placements (L <= 24).  Replaces
+ * planner.py:228-268 `plan_oracle`: maximum client value among feasible
+ * masks, ties to the smallest mask with layer 1 as the MSB. */
+int sp_plan_exhaustive(const sp_instances* in, sp_policies* out, void* stream);
+
+/* ---- evaluator (evaluator.py) ------------------------------------------ */
+
+/* Eq. (1) real-valued latency of each policy (evaluator.py:64-78
+ * `latency_of`): per-layer terms x(c + (1-x')d) + (1-x)(s + x'u) summed in
+ * numpy pairwise order.  Times are [total_layers] float64; latency_s [n]. */
+int sp_latency_eq1(const sp_instances* in, const double* client_s, const double* server_s,
+                   const double* up_s, const double* down_s, const uint8_t* pi,
+                   double* latency_s, void* stream);
+
+
+
+/* _finish for caller-supplied placements (planner.py:88-101): fills
+ * client_value / server_load (numpy order), integer_latency and feasible of
+ * each policy pi.  Also evaluator.py:81-102 server_load_of / client_value_of.
+ * ws: >= 4 * total_layers bytes of scratch. */
+int sp_evaluate_policy(const sp_instances* in, const uint8_t* pi, sp_policies* out, void* ws,
+                       size_t ws_bytes, void* stream);
+
+/* Elementwise integerization of times (problem.py:79-104): mode 0 = cost,
+ * conservative (ceil); 1 = paper (floor(q+0.5)), cost or budget; 2 = budget,
+ * conservative (floor).  status[k] is an sp_cost_status. */
+int sp_to_units(const double* seconds, int64_t n, double unit_s, int32_t mode, int64_t* units,
+                int32_t* status, void* stream);
+
+/* ---- cost model + integerization (cost_model.py, problem.py) ------------ */
+
+enum sp_layer_kind {  /* cost_model.py:43-49 LayerKind */
+  SP_EMBEDDING = 0, SP_ATTENTION = 1, SP_FEED_FORWARD = 2,
+  SP_LAYER_NORM = 3, SP_CLASSIFIER = 4, SP_CUSTOM = 5
+};
+
+/* Model specs (cost_model.py:52-106 LayerSpec / ModelSpec), CSR over layer
+ * entries: model m owns entries [layer_off[m], layer_off[m+1]). */
+typedef struct sp_models {
+  int64_t n_models;
+  const int64_t* layer_off;         /* [n_models+1] */
+  const int32_t* kind;              /* [E] sp_layer_kind */
+  const int64_t* hidden_dim;        /* [E] */
+  const int64_t* heads;             /* [E] */
+  const int64_t* ffn_dim;           /* [E] */
+  const int64_t* out_dim;           /* [E] */
+  const int64_t* seq_divisor;       /* [E] */
+  const double* flop_coeffs;        /* [E*3] custom (quad, lin, const) */
+  const double* mem_coeffs;         /* [E*3] custom, valid where has_mem_coeffs */
+  const uint8_t* has_mem_coeffs;    /* [E] */
+  const double* out_bytes_per_token;/* [E] custom, valid where has_out_bytes */
+  const uint8_t* has_out_bytes;     /* [E] */
+} sp_models;
+
+enum sp_request_flags {
+  SP_REQ_PAPER_ROUNDING = 1,  /* problem.py rounding="paper" (else conservative) */
+  SP_REQ_SOURCE_CLIENT = 2,   /* source_at_client */
+  SP_REQ_ZERO_SERVER = 4,     /* build_problem zero_server_time */
+  SP_REQ_METRIC_MEMORY = 8    /* profile metric="memory" (else "flop") */
+};
+
+/* One scenario per request: model x seq_len x devices x link x deadline. */
+typedef struct sp_requests {
+  int64_t n;
+  const int32_t* model;          /* [n] index into sp_models */
+  const int64_t* seq_len;        /* [n] */
+  const double* client_fps;      /* [n] DeviceSpec.flops_per_s */
+  const double* server_fps;      /* [n] */
+  const double* uplink_bps;      /* [n] LinkSpec */
+  const double* downlink_bps;    /* [n] */
+  const double* propagation_s;   /* [n] */
+  const double* deadline_s;      /* [n] */
+  const double* unit_s;          /* [n] */
+  const uint8_t* flags;          /* [n] sp_request_flags */
+} sp_requests;
+
+/* Per-layer profiles supplied directly (build_problem from LayerProfile list). */
+typedef struct sp_profiles {
+  const double* r;               /* [total_layers] */
+  const double* client_time_s;
+  const double* server_time_s;
+  const double* tau_bytes;
+} sp_profiles;
+
+/* Cost-table output, CSR over request layers.  Any per-layer pointer may be
+ * NULL to skip it.  The integer arrays + r + budget + source_at_client form
+ * an sp_instances batch for the planners. */
+typedef struct sp_cost_table {
+  const int64_t* layer_off;   /* [n+1] from sp_request_layer_offsets */
+  int64_t total_layers;
+  double* r;                  /* LayerProfile.r */
+  double* client_time_s;      /* LayerProfile.client_time_s */
+  double* server_time_s;      /* LayerProfile.server_time_s (profiled) */
+  double* tau_bytes;          /* LayerProfile.tau_bytes */
+  double* server_s;           /* PlanProblem.server_s (0 under zero_server_time) */
+  double* up_s;               /* PlanProblem.up_s (problem.py:58-65) */
+  double* down_s;             /* PlanProblem.down_s */
+  int64_t* client_units;      /* problem.py:79-92 to_units */
+  int64_t* server_units;
+  int64_t* up_units;
+  int64_t* down_units;
+  int64_t* budget;            /* [n] problem.py:95-104 budget_units */
+  uint8_t* source_at_client;  /* [n] */
+  int32_t* status;            /* [n] 0 ok, else (array sp_cost_status)
+                                 | (budget sp_cost_status << 8) | (negative r << 16) */
+} sp_cost_table;
+
+enum sp_cost_status {
+  SP_COST_OK = 0,
+  SP_COST_NEGATIVE_TIME = 1,   /* ValueError("times must be >= 0") problem.py:87 */
+  SP_COST_NEGATIVE_R = 2,      /* ValueError("r must be >= 0") problem.py:152 */
+  SP_COST_NAN_TIME = 3,        /* ValueError from round(nan) problem.py:69 */
+  SP_COST_INF_TIME = 4,        /* OverflowError from round(inf) problem.py:69 */
+  SP_COST_OVERFLOW = 5         /* unit count beyond int64 */
+};
+
+/* layer_off[k+1] = layer_off[k] + L(model[k]); layer_off device int64[n+1]. */
+int sp_request_layer_offsets(const sp_models* models, const sp_requests* req,
+                             int64_t* layer_off, void* stream);
+
+/* K1: per (request, layer) profile (cost_model.py:305-329 `profile`), link
+ * transfer times and integerization (problem.py:58-115, 188-222
+ * `build_problem`); integer outputs are skipped when `integerize` == 0. */
+int sp_build_cost_table(const sp_models* models, const sp_requests* req, int32_t integerize,
+                        sp_cost_table* out, void* stream);
+
+/* build_problem over caller-supplied profiles (problem.py:188-222). */
+int sp_integerize_profiles(const sp_profiles* prof, const sp_requests* req,
+                           sp_cost_table* out, void* stream);
+
+/* ---- throughput simulator (throughput_sim.py) --------------------------- */
+
+/* Independent replay runs, CSR over requests: run k owns requests
+ * [run_off[k], run_off[k+1]) in arrival order (throughput_sim.py:98-106 Stream). */
+typedef struct sp_sim_batch {
+  int64_t n_runs;
+  int64_t total_requests;      /* == run_off[n_runs] (host value) */
+  const int64_t* run_off;      /* [n_runs+1] */
+  const double* arrival_ms;    /* [total] non-decreasing within a run */
+  const double* demand;        /* [total] */
+  const double* duration_ms;   /* [total] */
+  const double* capacity;      /* [n_runs] */
+} sp_sim_batch;
+
+typedef struct sp_sim_out {
+  double* admit_ms;      /* [total] */
+  double* wait_ms;       /* [total] or NULL */
+  double* cum_wait_ms;   /* [total] or NULL: np.cumsum of waits */
+  double* max_wait_ms;   /* [n_runs] or NULL */
+  double* mean_wait_ms;  /* [n_runs] or NULL: numpy-order mean */
+  int32_t* status;       /* [n_runs] SP_OK or SP_ERR_DEADLOCK */
+  int64_t* deadlock_req; /* [n_runs] or NULL: FIFO head that can never fit */
+} sp_sim_out;
+
+/* Segmented numpy-order sums: out[k] = np.sum(x[seg_off[k]:seg_off[k+1]])
+ * (0.0 + pairwise).  Backs np.sum / np.mean in evaluator.py:102 total_r and
+ * throughput_sim.py:156,176 (scenario normalisation, capacity). */
+int sp_segment_sum(const double* x, const int64_t* seg_off, int64_t n_seg, double* out,
+                   void* stream);
+
+/* Heap workspace the replay needs (16 bytes per request). */
+size_t sp_sim_workspace_bytes(const sp_sim_batch* b);
+
+/* K4: FIFO admission with a completion min-heap keyed (finish, seq), one
+ * thread per run.  Replaces throughput_sim.py:207-256 `simulate_stream`
+ * (and the per-variant loop of :264-272 `compare_variants`). */
+int sp_sim_replay(const sp_sim_batch* b, sp_sim_out* out, void* ws, size_t ws_bytes,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLITPLAN_B200_H */

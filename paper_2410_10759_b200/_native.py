@@ -1,0 +1,215 @@
+"""ctypes binding of the C ABI declared in include/splitplan_b200.h.
+
+This is the only place Python talks to the CUDA library.  Device memory and
+streams come from PyTorch (plumbing only); every computation on the hot path
+is one of the `sp_*` entry points.  There is no CPU fallback: if the library
+or a CUDA device is missing, calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from ._build import LIB
+
+SP_OK = 0
+SP_ERR_INVALID = 1
+SP_ERR_CUDA = 2
+SP_ERR_WORKSPACE = 3
+SP_ERR_BACKTRACE = 4
+SP_ERR_DEADLOCK = 5
+SP_ERR_UNSUPPORTED = 6
+
+SP_GREEDY, SP_ALL_SERVER, SP_ALL_CLIENT = 0, 1, 2
+
+SP_REQ_PAPER_ROUNDING = 1
+SP_REQ_SOURCE_CLIENT = 2
+SP_REQ_ZERO_SERVER = 4
+SP_REQ_METRIC_MEMORY = 8
+
+KIND_CODE = {"embedding": 0, "attention": 1, "feed_forward": 2,
+             "layer_norm": 3, "classifier": 4, "custom": 5}
+
+P = C.c_void_p
+
+
+class SpInstances(C.Structure):
+    _fields_ = [("n", C.c_int64), ("total_layers", C.c_int64), ("layer_off", P),
+                ("client_units", P), ("server_units", P), ("up_units", P), ("down_units", P),
+                ("r", P), ("budget", P), ("source_at_client", P), ("must_end_at", P)]
+
+
+class SpPolicies(C.Structure):
+    _fields_ = [("pi", P), ("client_value", P), ("server_load", P),
+                ("integer_latency", P), ("feasible", P), ("status", P)]
+
+
+class SpModels(C.Structure):
+    _fields_ = [("n_models", C.c_int64), ("layer_off", P), ("kind", P), ("hidden_dim", P),
+                ("heads", P), ("ffn_dim", P), ("out_dim", P), ("seq_divisor", P),
+                ("flop_coeffs", P), ("mem_coeffs", P), ("has_mem_coeffs", P),
+                ("out_bytes_per_token", P), ("has_out_bytes", P)]
+
+
+class SpRequests(C.Structure):
+    _fields_ = [("n", C.c_int64), ("model", P), ("seq_len", P), ("client_fps", P),
+                ("server_fps", P), ("uplink_bps", P), ("downlink_bps", P),
+                ("propagation_s", P), ("deadline_s", P), ("unit_s", P), ("flags", P)]
+
+
+class SpProfiles(C.Structure):
+    _fields_ = [("r", P), ("client_time_s", P), ("server_time_s", P), ("tau_bytes", P)]
+
+
+class SpCostTable(C.Structure):
+    _fields_ = [("layer_off", P), ("total_layers", C.c_int64), ("r", P), ("client_time_s", P),
+                ("server_time_s", P), ("tau_bytes", P), ("server_s", P), ("up_s", P),
+                ("down_s", P), ("client_units", P), ("server_units", P), ("up_units", P),
+                ("down_units", P), ("budget", P), ("source_at_client", P), ("status", P)]
+
+
+class SpSimBatch(C.Structure):
+    _fields_ = [("n_runs", C.c_int64), ("total_requests", C.c_int64), ("run_off", P),
+                ("arrival_ms", P), ("demand", P), ("duration_ms", P), ("capacity", P)]
+
+
+class SpSimOut(C.Structure):
+    _fields_ = [("admit_ms", P), ("wait_ms", P), ("cum_wait_ms", P), ("max_wait_ms", P),
+                ("mean_wait_ms", P), ("status", P), ("deadlock_req", P)]
+
+
+# name -> (restype, argtypes); the full list the header declares
+SIGNATURES = {
+    "sp_abi_version": (C.c_int, []),
+    "sp_last_error": (C.c_char_p, []),
+    "sp_last_required_workspace": (C.c_size_t, []),
+    "sp_profile_enable": (None, [C.c_int]),
+    "sp_profile_collect": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_int64)]),
+    "sp_effective_budget": (C.c_int, [C.POINTER(SpInstances), P, P]),
+    "sp_plan_dp": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_size_t, P]),
+    "sp_build_dp_tables": (C.c_int, [C.POINTER(SpInstances), C.c_int64, P, P, P, C.c_size_t, P]),
+    "sp_plan_prefix": (C.c_int, [C.POINTER(SpInstances), C.c_int32, C.POINTER(SpPolicies), P]),
+    "sp_plan_exhaustive": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P]),
+    "sp_latency_eq1": (C.c_int, [C.POINTER(SpInstances), P, P, P, P, P, P, P]),
+    "sp_request_layer_offsets": (C.c_int, [C.POINTER(SpModels), C.POINTER(SpRequests), P, P]),
+    "sp_build_cost_table": (C.c_int, [C.POINTER(SpModels), C.POINTER(SpRequests), C.c_int32,
+                                      C.POINTER(SpCostTable), P]),
+    "sp_integerize_profiles": (C.c_int, [C.POINTER(SpProfiles), C.POINTER(SpRequests),
+                                         C.POINTER(SpCostTable), P]),
+    "sp_evaluate_policy": (C.c_int, [C.POINTER(SpInstances), P, C.POINTER(SpPolicies), P,
+                                     C.c_size_t, P]),
+    "sp_to_units": (C.c_int, [P, C.c_int64, C.c_double, C.c_int32, P, P, P]),
+    "sp_segment_sum": (C.c_int, [P, P, C.c_int64, P, P]),
+    "sp_sim_workspace_bytes": (C.c_size_t, [C.POINTER(SpSimBatch)]),
+    "sp_sim_replay": (C.c_int, [C.POINTER(SpSimBatch), C.POINTER(SpSimOut), P, C.c_size_t, P]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library() -> C.CDLL:
+    """Load (never silently rebuild on the GPU box) the in-tree library."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not Path(LIB).exists():
+                raise RuntimeError(f"splitplan-b200 CUDA library missing at {LIB}; "
+                                   "run __graft_entry__.build() first")
+            lib = C.CDLL(str(LIB))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name, None)
+                if fn is None:
+                    continue
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    lib = library()
+    return [n for n in SIGNATURES if hasattr(lib, n)]
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == SP_OK:
+        return
+    msg = library().sp_last_error().decode(errors="replace")
+    if rc == SP_ERR_INVALID:
+        raise ValueError(f"{what}: {msg}")
+    raise NativeError(rc, f"{what}: {msg}")
+
+
+# ---------------------------------------------------------------------------
+# device plumbing
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("splitplan-b200 requires a CUDA device (B200, sm_100a); none is visible")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> P:
+    return P(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> P:
+    if t is None:
+        return P(0)
+    return P(t.data_ptr())
+
+
+def to_dev(a, dtype, dev=None) -> torch.Tensor:
+    dev = dev or device()
+    arr = np.ascontiguousarray(a)
+    t = torch.from_numpy(arr)
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.to(dev, non_blocking=False)
+
+
+_ws: dict[int, torch.Tensor] = {}
+
+
+def workspace(min_bytes: int = 0) -> torch.Tensor:
+    """Per-device cached scratch buffer, grown on demand."""
+    dev = device()
+    key = dev.index
+    cur = _ws.get(key)
+    if cur is None or cur.numel() < min_bytes:
+        if cur is not None:
+            del _ws[key]
+            cur = None
+            torch.cuda.empty_cache()
+        free, _total = torch.cuda.mem_get_info(dev)
+        want = max(min_bytes, min(64 << 30, int(free * 0.45)), 64 << 20)
+        _ws[key] = torch.empty(want, dtype=torch.uint8, device=dev)
+    return _ws[key]
+
+
+def with_workspace(fn, *args):
+    """Call fn(*args, ws_ptr, ws_bytes), growing the workspace on SP_ERR_WORKSPACE."""
+    ws = workspace()
+    rc = fn(*args, ptr(ws), C.c_size_t(ws.numel()))
+    if rc == SP_ERR_WORKSPACE:
+        need = int(library().sp_last_required_workspace())
+        ws = workspace(need + (1 << 20))
+        rc = fn(*args, ptr(ws), C.c_size_t(ws.numel()))
+    return rc

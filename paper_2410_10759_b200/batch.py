@@ -1,0 +1,165 @@
+"""Batched device API: many independent placement instances per call.
+
+`InstanceBatch` is the CSR form of a list of `PlanProblem`s (the C ABI's
+`sp_instances`) held in CUDA tensors; `PolicyBatch` the matching
+`sp_policies`.  The reference-compatible functions in `planner.py` wrap these
+with n == 1; sweeps and benches call them directly with thousands of
+instances.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+
+@dataclass
+class InstanceBatch:
+    layer_off: torch.Tensor      # int64 [n+1]
+    client_units: torch.Tensor   # int64 [T]
+    server_units: torch.Tensor
+    up_units: torch.Tensor
+    down_units: torch.Tensor
+    r: torch.Tensor              # float64 [T]
+    budget: torch.Tensor         # int64 [n]
+    source_at_client: torch.Tensor  # uint8 [n]
+    must_end_at: torch.Tensor | None = None  # int8 [n]
+    n_layers_host: np.ndarray | None = None  # int64 [n] (host copy of lengths, optional)
+
+    @property
+    def n(self) -> int:
+        return int(self.budget.numel())
+
+    @property
+    def total_layers(self) -> int:
+        return int(self.r.numel())
+
+    def struct(self) -> N.SpInstances:
+        return N.SpInstances(self.n, self.total_layers, N.ptr(self.layer_off).value,
+                             N.ptr(self.client_units).value, N.ptr(self.server_units).value,
+                             N.ptr(self.up_units).value, N.ptr(self.down_units).value,
+                             N.ptr(self.r).value, N.ptr(self.budget).value,
+                             N.ptr(self.source_at_client).value,
+                             N.ptr(self.must_end_at).value if self.must_end_at is not None else None)
+
+    @classmethod
+    def from_arrays(cls, layer_off, i, s, u, d, r, budget, sac, must=None) -> "InstanceBatch":
+        dev = N.device()
+        lo = np.asarray(layer_off, dtype=np.int64)
+        return cls(N.to_dev(lo, torch.int64, dev), N.to_dev(i, torch.int64, dev),
+                   N.to_dev(s, torch.int64, dev), N.to_dev(u, torch.int64, dev),
+                   N.to_dev(d, torch.int64, dev), N.to_dev(r, torch.float64, dev),
+                   N.to_dev(budget, torch.int64, dev), N.to_dev(sac, torch.uint8, dev),
+                   None if must is None else N.to_dev(must, torch.int8, dev),
+                   np.diff(lo))
+
+    @classmethod
+    def from_problems(cls, problems, must_end_at=None) -> "InstanceBatch":
+        lens = np.array([p.n_layers for p in problems], dtype=np.int64)
+        off = np.zeros(len(problems) + 1, dtype=np.int64)
+        np.cumsum(lens, out=off[1:])
+        cat = lambda name, dt: (np.concatenate([np.asarray(getattr(p, name), dtype=dt) for p in problems])
+                                if problems else np.zeros(0, dt))
+        must = None
+        if must_end_at is not None:
+            must = np.array([-1 if m is None else (1 if m == "client" else 0) for m in must_end_at],
+                            dtype=np.int8)
+        return cls.from_arrays(off, cat("client_units", np.int64), cat("server_units", np.int64),
+                               cat("up_units", np.int64), cat("down_units", np.int64),
+                               cat("r", np.float64),
+                               np.array([p.budget for p in problems], dtype=np.int64),
+                               np.array([p.source_at_client for p in problems], dtype=np.uint8),
+                               must)
+
+
+@dataclass
+class PolicyBatch:
+    pi: torch.Tensor               # uint8 [T]
+    client_value: torch.Tensor     # float64 [n]
+    server_load: torch.Tensor      # float64 [n]
+    integer_latency: torch.Tensor  # int64 [n]
+    feasible: torch.Tensor         # uint8 [n]
+    status: torch.Tensor           # int32 [n]
+
+    @classmethod
+    def empty(cls, n: int, total: int, dev=None) -> "PolicyBatch":
+        dev = dev or N.device()
+        return cls(torch.zeros(total, dtype=torch.uint8, device=dev),
+                   torch.empty(n, dtype=torch.float64, device=dev),
+                   torch.empty(n, dtype=torch.float64, device=dev),
+                   torch.empty(n, dtype=torch.int64, device=dev),
+                   torch.empty(n, dtype=torch.uint8, device=dev),
+                   torch.zeros(n, dtype=torch.int32, device=dev))
+
+    def struct(self) -> N.SpPolicies:
+        return N.SpPolicies(N.ptr(self.pi).value, N.ptr(self.client_value).value,
+                            N.ptr(self.server_load).value, N.ptr(self.integer_latency).value,
+                            N.ptr(self.feasible).value, N.ptr(self.status).value)
+
+    def to_host(self) -> dict:
+        return dict(pi=self.pi.cpu().numpy(), client_value=self.client_value.cpu().numpy(),
+                    server_load=self.server_load.cpu().numpy(),
+                    integer_latency=self.integer_latency.cpu().numpy(),
+                    feasible=self.feasible.cpu().numpy().astype(bool),
+                    status=self.status.cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# planners
+
+
+def effective_budget(batch: InstanceBatch) -> torch.Tensor:
+    out = torch.empty(batch.n, dtype=torch.int64, device=batch.r.device)
+    s = batch.struct()
+    N.check(N.library().sp_effective_budget(s, N.ptr(out), N.stream_ptr()), "sp_effective_budget")
+    return out
+
+
+def plan_dp(batch: InstanceBatch, out: PolicyBatch | None = None) -> PolicyBatch:
+    """K1-prep + K2 DP stage + K3 backtrack over the whole batch (sp_plan_dp)."""
+    out = out or PolicyBatch.empty(batch.n, batch.total_layers, batch.r.device)
+    s, o = batch.struct(), out.struct()
+    rc = N.with_workspace(lambda ws, nb: N.library().sp_plan_dp(s, o, ws, nb, N.stream_ptr()))
+    N.check(rc, "sp_plan_dp")
+    return out
+
+
+def plan_prefix(batch: InstanceBatch, which: int, out: PolicyBatch | None = None) -> PolicyBatch:
+    out = out or PolicyBatch.empty(batch.n, batch.total_layers, batch.r.device)
+    s, o = batch.struct(), out.struct()
+    N.check(N.library().sp_plan_prefix(s, which, o, N.stream_ptr()), "sp_plan_prefix")
+    return out
+
+
+def plan_exhaustive(batch: InstanceBatch, out: PolicyBatch | None = None) -> PolicyBatch:
+    out = out or PolicyBatch.empty(batch.n, batch.total_layers, batch.r.device)
+    s, o = batch.struct(), out.struct()
+    N.check(N.library().sp_plan_exhaustive(s, o, N.stream_ptr()), "sp_plan_exhaustive")
+    return out
+
+
+def build_dp_tables(batch: InstanceBatch) -> tuple[torch.Tensor, torch.Tensor]:
+    if batch.n != 1:
+        raise ValueError("build_dp_tables takes exactly one instance")
+    w = int(effective_budget(batch).item())
+    L = batch.total_layers
+    C = torch.empty((L + 1, w + 1), dtype=torch.float64, device=batch.r.device)
+    S = torch.empty_like(C)
+    s = batch.struct()
+    rc = N.with_workspace(lambda ws, nb: N.library().sp_build_dp_tables(
+        s, w, N.ptr(C), N.ptr(S), ws, nb, N.stream_ptr()))
+    N.check(rc, "sp_build_dp_tables")
+    return C, S
+
+
+def latency_eq1(batch: InstanceBatch, client_s, server_s, up_s, down_s, pi) -> torch.Tensor:
+    out = torch.empty(batch.n, dtype=torch.float64, device=batch.r.device)
+    s = batch.struct()
+    N.check(N.library().sp_latency_eq1(s, N.ptr(client_s), N.ptr(server_s), N.ptr(up_s),
+                                       N.ptr(down_s), N.ptr(pi), N.ptr(out), N.stream_ptr()),
+            "sp_latency_eq1")
+    return out

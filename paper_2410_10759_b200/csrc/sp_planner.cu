@@ -1,0 +1,951 @@
+// Planner kernels of the B200 placement engine (reference: planner.py).
+//
+//   prep_kernel       per-instance W_eff, value domain, clamped stage shifts
+//   dp_stage_kernel   K2: the two-state DP over the integer budget axis
+//                     (planner.py:128-143) with a uint8 back-pointer per cell
+//   backtrack_kernel  K3: end-side choice + pointer walk + _finish
+//                     (planner.py:88-107, 146-202)
+//   prefix_kernel     greedy / all-server / all-client (planner.py:205-225)
+//   exhaustive_kernel plan_oracle (planner.py:228-268)
+//   eq1_kernel        evaluator latency_of (evaluator.py:64-78)
+//
+// See DESIGN.md for the data layout and the value domains.
+#include <algorithm>
+#include <vector>
+
+#include "sp_internal.cuh"
+
+namespace sp {
+namespace {
+
+constexpr int kStageTile = 128;          // stage records staged in SMEM at a time
+constexpr int kCellsPerThread = 8;       // E: columns per thread per chunk
+constexpr int kMaxThreads = 1024;
+constexpr size_t kSmemCap = 227 * 1024;  // sm_100a max dynamic SMEM per CTA
+constexpr int64_t kMaxCols = (int64_t(1) << 31) - 64;
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------
+// value domains
+
+template <int MODE> struct VT;
+template <> struct VT<VM_INT32> {
+  using T = int32_t;
+  static __device__ __forceinline__ T neg() { return INT32_MIN; }
+};
+template <> struct VT<VM_F64> {
+  using T = double;
+  static __device__ __forceinline__ T neg() { return -INFINITY; }
+};
+template <> struct VT<VM_F64_NAN> {
+  using T = double;
+  static __device__ __forceinline__ T neg() { return -INFINITY; }
+};
+
+__device__ __forceinline__ double to_f64(int32_t v, double g) {
+  return v >= 0 ? dmul((double)v, g) : -INFINITY;
+}
+__device__ __forceinline__ double to_f64(double v, double) { return v; }
+
+__device__ __forceinline__ uint64_t gcd_u64(uint64_t a, uint64_t b) {
+  while (b) {
+    uint64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// ---------------------------------------------------------------------------
+// block reductions (128-thread prep blocks)
+
+template <typename T, typename Op>
+__device__ T block_reduce(T v, Op op, T* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  T r = sh[0];
+  for (int w = 1; w < nw; ++w) r = op(r, sh[w]);
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// W_eff only (planner.py:120-125)
+
+__global__ void weff_kernel(sp_instances in, int64_t* w_eff) {
+  __shared__ int64_t sh64[32];
+  for (int64_t k = blockIdx.x; k < in.n; k += gridDim.x) {
+    const int64_t lo = in.layer_off[k], hi = in.layer_off[k + 1];
+    int64_t worst = 0;
+    for (int64_t l = lo + threadIdx.x; l < hi; l += blockDim.x)
+      worst += max(in.client_units[l] + in.down_units[l], in.server_units[l] + in.up_units[l]);
+    worst = block_reduce(worst, [](int64_t a, int64_t b) { return a + b; }, sh64);
+    if (threadIdx.x == 0) w_eff[k] = min(in.budget[k], worst);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// prep: W_eff, value domain, clamped shifts, scaled values
+
+__global__ void prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts, int64_t* rv) {
+  __shared__ int64_t sh64[32];
+  __shared__ uint64_t shu[32];
+  __shared__ int shi[32];
+  for (int64_t k = blockIdx.x; k < in.n; k += gridDim.x) {
+    const int64_t lo = in.layer_off[k], hi = in.layer_off[k + 1];
+    int64_t worst = 0;
+    int finite = 1, integral = 1;
+    uint64_t isum = 0, g = 0;
+    for (int64_t l = lo + threadIdx.x; l < hi; l += blockDim.x) {
+      worst += max(in.client_units[l] + in.down_units[l], in.server_units[l] + in.up_units[l]);
+      const double r = in.r[l];
+      if (!isfinite(r)) {
+        finite = 0;
+      } else if (r != floor(r) || r >= 9007199254740992.0) {
+        integral = 0;
+      } else {
+        const uint64_t v = (uint64_t)r;  // r >= 0 (problem.py:151-153)
+        isum = min(isum + v, (uint64_t)1 << 62);
+        g = gcd_u64(g, v);
+      }
+    }
+    worst = block_reduce(worst, [](int64_t a, int64_t b) { return a + b; }, sh64);
+    finite = block_reduce(finite, [](int a, int b) { return a & b; }, shi);
+    integral = block_reduce(integral, [](int a, int b) { return a & b; }, shi);
+    isum = block_reduce(isum, [](uint64_t a, uint64_t b) { return min(a + b, (uint64_t)1 << 62); }, shu);
+    g = block_reduce(g, [](uint64_t a, uint64_t b) { return gcd_u64(a, b); }, shu);
+    if (g == 0) g = 1;
+    const int64_t W = min(in.budget[k], worst);
+    int32_t mode;
+    if (!finite) mode = VM_F64_NAN;
+    else if (integral && isum < ((uint64_t)1 << 53) && isum / g <= (uint64_t)INT32_MAX) mode = VM_INT32;
+    else mode = VM_F64;
+    if (threadIdx.x == 0) {
+      InstInfo r;
+      r.w_eff = W;
+      r.scale = (double)g;
+      r.end_c = -INFINITY;
+      r.end_s = -INFINITY;
+      r.mode = mode;
+      r.pad = 0;
+      info[k] = r;
+    }
+    const int64_t cap = min(W + 1, kMaxCols);
+    for (int64_t l = lo + threadIdx.x; l < hi; l += blockDim.x) {
+      const int64_t i = in.client_units[l], s = in.server_units[l];
+      const int64_t u = in.up_units[l], d = in.down_units[l];
+      StageShift sh;
+      sh.i = (int32_t)min(i, cap);
+      sh.id = (int32_t)min(i + d, cap);
+      sh.s = (int32_t)min(s, cap);
+      sh.su = (int32_t)min(s + u, cap);
+      shifts[l] = sh;
+      const double r = in.r[l];
+      if (mode == VM_INT32) {
+        rv[l] = (int64_t)((uint64_t)r / g);
+      } else {
+        rv[l] = __double_as_longlong(r);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: DP stage kernel
+//
+// One CTA owns one instance.  Rows C and S (length W_eff+1) live either in
+// SMEM (ROWS_SMEM) or in a global scratch slot, and are updated IN PLACE:
+// every stage walks the row in chunks of E*T columns from the top down.  A
+// chunk first computes all of its new cells into registers (reads only touch
+// columns <= its own, which no later chunk of this stage overwrites), then a
+// barrier, then the writes.  Each cell emits one back-pointer byte:
+//   bit0 C-stay  : j>=i    and C[k-1][j-i]   + r == C[k][j]   (planner.py:164)
+//   bit1 C-switch: j>=i+d  and S[k-1][j-i-d] + r == C[k][j]   (planner.py:166)
+//   bit2 S-stay  : j>=s    and S[k-1][j-s]       == S[k][j]   (planner.py:173)
+//   bit3 S-switch: j>=s+u  and C[k-1][j-s-u]     == S[k][j]   (planner.py:175)
+// which is exactly the predicate sequence _backtrace evaluates.
+
+struct DpArgs {
+  const int64_t* layer_off;
+  const uint8_t* sac;
+  InstInfo* info;
+  const StageShift* shifts;
+  const int64_t* rv;
+  const DpWork* work;
+  uint8_t* bp;
+  uint8_t* rows;
+  double* tab_c;  // optional full-table output (build_dp_tables), n == 1
+  double* tab_s;
+};
+
+template <int MODE, bool ROWS_SMEM, int E>
+__global__ void __launch_bounds__(kMaxThreads, 1) dp_stage_kernel(DpArgs a) {
+  using V = typename VT<MODE>::T;
+  extern __shared__ __align__(16) unsigned char smem[];
+  StageShift* st_sh = reinterpret_cast<StageShift*>(smem);
+  V* st_r = reinterpret_cast<V*>(smem + kStageTile * sizeof(StageShift));
+  const size_t stage_bytes = align_up(kStageTile * (sizeof(StageShift) + sizeof(V)), 16);
+
+  const DpWork wk = a.work[blockIdx.x];
+  const int64_t inst = wk.inst;
+  const int64_t lo = a.layer_off[inst];
+  const int L = (int)(a.layer_off[inst + 1] - lo);
+  const int ncol = (int)(a.info[inst].w_eff + 1);
+  const double g = a.info[inst].scale;
+  const bool sac = a.sac[inst] != 0;
+  const int T = blockDim.x, tid = threadIdx.x;
+  const int CH = E * T;
+
+  V* Crow;
+  if (ROWS_SMEM) Crow = reinterpret_cast<V*>(smem + stage_bytes);
+  else Crow = reinterpret_cast<V*>(a.rows + wk.row_off);
+  V* Srow = Crow + ncol;
+  const V NEG = VT<MODE>::neg();
+  const V ZERO = V(0);
+
+  for (int j = tid; j < ncol; j += T) {
+    Crow[j] = sac ? ZERO : NEG;
+    Srow[j] = sac ? NEG : ZERO;
+    if (a.tab_c) {
+      a.tab_c[j] = sac ? 0.0 : -INFINITY;
+      a.tab_s[j] = sac ? -INFINITY : 0.0;
+    }
+  }
+
+  uint8_t* bp_inst = a.bp + wk.bp_off;
+  for (int k = 0; k < L; ++k) {
+    const int kt = k % kStageTile;
+    if (kt == 0) {
+      __syncthreads();
+      const int cnt = min(kStageTile, L - k);
+      for (int t = tid; t < cnt; t += T) {
+        st_sh[t] = a.shifts[lo + k + t];
+        const int64_t bits = a.rv[lo + k + t];
+        if (MODE == VM_INT32) st_r[t] = (V)(int32_t)bits;
+        else st_r[t] = (V)__longlong_as_double(bits);
+      }
+    }
+    __syncthreads();
+    const StageShift sh = st_sh[kt];
+    const V rk = st_r[kt];
+    uint8_t* bprow = bp_inst + (int64_t)k * ncol;
+
+    for (int top = ncol; top > 0; top -= CH) {
+      const int base = top - CH;
+      V cn[E], sn[E];
+      uint32_t bits[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = base + e * T + tid;
+        cn[e] = NEG;
+        sn[e] = NEG;
+        bits[e] = 0;
+        if (j >= 0) {
+          const int ji = j - sh.i, jid = j - sh.id, js = j - sh.s, jsu = j - sh.su;
+          const V ca = ji >= 0 ? Crow[ji] : NEG;
+          const V cb = jid >= 0 ? Srow[jid] : NEG;
+          const V sa = js >= 0 ? Srow[js] : NEG;
+          const V sb = jsu >= 0 ? Crow[jsu] : NEG;
+          if (MODE == VM_INT32) {
+            // exact integer arithmetic: C-stay <=> ca >= cb, S-stay <=> sa >= sb
+            const bool c_stay = ca >= cb;
+            const bool s_stay = sa >= sb;
+            cn[e] = (c_stay ? ca : cb) + rk;
+            sn[e] = s_stay ? sa : sb;
+            bits[e] = (c_stay ? 1u : 2u) | (s_stay ? 4u : 8u);
+          } else {
+            V cm, sm;
+            if (MODE == VM_F64_NAN) {  // np.maximum propagates NaN
+              cm = (ca != ca) ? ca : ((cb != cb) ? cb : (ca >= cb ? ca : cb));
+              sm = (sa != sa) ? sa : ((sb != sb) ? sb : (sa >= sb ? sa : sb));
+            } else {
+              cm = ca >= cb ? ca : cb;
+              sm = sa >= sb ? sa : sb;
+            }
+            const V c = dadd(cm, rk);
+            cn[e] = c;
+            sn[e] = sm;
+            uint32_t b = 0;
+            if (ji >= 0 && dadd(ca, rk) == c) b |= 1u;
+            if (jid >= 0 && dadd(cb, rk) == c) b |= 2u;
+            if (js >= 0 && sa == sm) b |= 4u;
+            if (jsu >= 0 && sb == sm) b |= 8u;
+            bits[e] = b;
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = base + e * T + tid;
+        if (j >= 0) {
+          Crow[j] = cn[e];
+          Srow[j] = sn[e];
+          bprow[j] = (uint8_t)bits[e];
+          if (a.tab_c) {
+            a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn[e], g);
+            a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn[e], g);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    a.info[inst].end_c = to_f64(Crow[ncol - 1], g);
+    a.info[inst].end_s = to_f64(Srow[ncol - 1], g);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// _finish (planner.py:88-101) for a placement already written to pi
+
+__device__ void finish_policy(const sp_instances& in, int64_t inst, int64_t lo, int L,
+                              int32_t* idx, sp_policies& out, bool feasible_hint, bool hint_value) {
+  const uint8_t* pi = out.pi + lo;
+  const bool sac = in.source_at_client[inst] != 0;
+  int64_t lat = 0;
+  int prev = sac ? 1 : 0;
+  int n1 = 0;
+  for (int k = 0; k < L; ++k) {
+    const int x = pi[k];
+    if (x) {
+      lat += in.client_units[lo + k] + (prev == 0 ? in.down_units[lo + k] : 0);
+      ++n1;
+    } else {
+      lat += in.server_units[lo + k] + (prev == 1 ? in.up_units[lo + k] : 0);
+    }
+    prev = x;
+  }
+  int a = 0, b = n1;
+  for (int k = 0; k < L; ++k) {
+    if (pi[k]) idx[a++] = k;
+    else idx[b++] = k;
+  }
+  const double* r = in.r + lo;
+  const double cv = np_sum([&](int64_t m) { return r[idx[m]]; }, n1);
+  const double sl = np_sum([&](int64_t m) { return r[idx[n1 + m]]; }, L - n1);
+  out.client_value[inst] = cv;
+  out.server_load[inst] = sl;
+  out.integer_latency[inst] = lat;
+  out.feasible[inst] = feasible_hint ? (hint_value ? 1 : 0) : (lat <= in.budget[inst] ? 1 : 0);
+}
+
+
+// ---------------------------------------------------------------------------
+// _finish over caller-supplied placements
+
+__global__ void evaluate_kernel(sp_instances in, const uint8_t* pi_in, sp_policies out,
+                                int32_t* idx_scratch) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= in.n) return;
+  const int64_t lo = in.layer_off[t];
+  const int L = (int)(in.layer_off[t + 1] - lo);
+  if (out.pi != pi_in)
+    for (int k = 0; k < L; ++k) out.pi[lo + k] = pi_in[lo + k] ? 1 : 0;
+  finish_policy(in, t, lo, L, idx_scratch + lo, out, false, false);
+  out.status[t] = SP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K3: end-side argmax + back-pointer walk + finish (planner.py:146-202)
+
+__global__ void backtrack_kernel(sp_instances in, const InstInfo* info, const StageShift* shifts,
+                                 const DpWork* work, int64_t n_work, const uint8_t* bp,
+                                 int32_t* idx_scratch, sp_policies out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_work) return;
+  const DpWork wk = work[t];
+  const int64_t inst = wk.inst;
+  const int64_t lo = in.layer_off[inst];
+  const int L = (int)(in.layer_off[inst + 1] - lo);
+  const InstInfo inf = info[inst];
+  const int64_t ncol = inf.w_eff + 1;
+  double ec = inf.end_c, es = inf.end_s;
+  const int8_t must = in.must_end_at ? in.must_end_at[inst] : (int8_t)-1;
+  if (must == 1) es = -INFINITY;
+  else if (must == 0) ec = -INFINITY;
+  const double pmax = (es > ec) ? es : ec;  // Python builtin max(end_c, end_s)
+  uint8_t* pi = out.pi + lo;
+  int32_t status = SP_OK;
+  if (pmax == -INFINITY) {  // _infeasible
+    for (int k = 0; k < L; ++k) pi[k] = 0;
+    finish_policy(in, inst, lo, L, idx_scratch + lo, out, true, false);
+    out.status[inst] = SP_OK;
+    return;
+  }
+  bool client = ec >= es;
+  int64_t j = inf.w_eff;
+  const uint8_t* bpi = bp + wk.bp_off;
+  for (int k = L; k >= 1; --k) {
+    const uint8_t b = bpi[(int64_t)(k - 1) * ncol + j];
+    const StageShift sh = shifts[lo + k - 1];
+    if (client) {
+      pi[k - 1] = 1;
+      if (b & 1u) {
+        j -= sh.i;
+      } else if (b & 2u) {
+        j -= sh.id;
+        client = false;
+      } else {
+        status = SP_ERR_BACKTRACE;
+        break;
+      }
+    } else {
+      pi[k - 1] = 0;
+      if (b & 4u) {
+        j -= sh.s;
+      } else if (b & 8u) {
+        j -= sh.su;
+        client = true;
+      } else {
+        status = SP_ERR_BACKTRACE;
+        break;
+      }
+    }
+  }
+  out.status[inst] = status;
+  if (status != SP_OK) return;
+  finish_policy(in, inst, lo, L, idx_scratch + lo, out, false, false);
+}
+
+// ---------------------------------------------------------------------------
+// prefix planners: one warp per instance, warp-scan over split points m
+
+__global__ void prefix_kernel(sp_instances in, int32_t which, sp_policies out) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= in.n) return;
+  const int64_t lo = in.layer_off[w];
+  const int64_t L = in.layer_off[w + 1] - lo;
+  const bool sac = in.source_at_client[w] != 0;
+  const int64_t budget = in.budget[w];
+  const int64_t* I = in.client_units + lo;
+  const int64_t* S = in.server_units + lo;
+  const int64_t* U = in.up_units + lo;
+  const int64_t d0 = in.down_units[lo];
+
+  int64_t stot = 0, itot = 0;
+  for (int64_t k = lane; k < L; k += 32) {
+    stot += S[k];
+    itot += I[k];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    stot += __shfl_xor_sync(0xffffffffu, stot, o);
+    itot += __shfl_xor_sync(0xffffffffu, itot, o);
+  }
+  // lat(m) = sum_{k<m} i_k + sum_{k>=m} s_k + [m<L and (m>=1 or sac)] u_m + [m>=1 and !sac] d_0
+  auto lat_of = [&](int64_t m, int64_t pre_i, int64_t pre_s) {
+    int64_t v = pre_i + (stot - pre_s);
+    if (m < L && (m >= 1 || sac)) v += U[m];
+    if (m >= 1 && !sac) v += d0;
+    return v;
+  };
+  int64_t m_sel = 0;
+  bool ok_sel = false;
+  int64_t lat_sel = 0;
+  if (which == SP_ALL_SERVER) {
+    m_sel = 0;
+    lat_sel = lat_of(0, 0, 0);
+  } else if (which == SP_ALL_CLIENT) {
+    m_sel = L;
+    lat_sel = lat_of(L, itot, stot);
+  } else {
+    int64_t carry_i = 0, carry_s = 0;
+    int64_t best = -1, best_lat = 0;
+    for (int64_t base = 0; base <= L; base += 32) {
+      const int64_t m = base + lane;
+      const int64_t own_i = (m < L) ? I[m] : 0;
+      const int64_t own_s = (m < L) ? S[m] : 0;
+      int64_t inc_i = own_i, inc_s = own_s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t vi = __shfl_up_sync(0xffffffffu, inc_i, o);
+        const int64_t vs = __shfl_up_sync(0xffffffffu, inc_s, o);
+        if (lane >= o) {
+          inc_i += vi;
+          inc_s += vs;
+        }
+      }
+      const int64_t pre_i = carry_i + inc_i - own_i;  // sum_{k<m} i_k
+      const int64_t pre_s = carry_s + inc_s - own_s;
+      const int64_t lm = lat_of(m, pre_i, pre_s);
+      const bool ok = (m <= L) && lm <= budget;
+      const unsigned ball = __ballot_sync(0xffffffffu, ok);
+      if (ball) {
+        const int hl = 31 - __clz(ball);
+        best = base + hl;
+        best_lat = __shfl_sync(0xffffffffu, lm, hl);
+      }
+      carry_i += __shfl_sync(0xffffffffu, inc_i, 31);
+      carry_s += __shfl_sync(0xffffffffu, inc_s, 31);
+    }
+    if (best >= 0) {
+      m_sel = best;
+      lat_sel = best_lat;
+      ok_sel = true;
+    } else {
+      m_sel = 0;
+      lat_sel = lat_of(0, 0, 0);
+    }
+  }
+  for (int64_t k = lane; k < L; k += 32) out.pi[lo + k] = k < m_sel ? 1 : 0;
+  if (lane == 0) {
+    const double* r = in.r + lo;
+    out.client_value[w] = np_sum([&](int64_t m) { return r[m]; }, m_sel);
+    out.server_load[w] = np_sum([&](int64_t m) { return r[m_sel + m]; }, L - m_sel);
+    out.integer_latency[w] = lat_sel;
+    out.feasible[w] = (which == SP_GREEDY) ? (ok_sel ? 1 : 0) : (lat_sel <= budget ? 1 : 0);
+    out.status[w] = SP_OK;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// exhaustive planner (plan_oracle): one CTA per instance, masks strided
+
+__global__ void exhaustive_kernel(sp_instances in, sp_policies out) {
+  const int64_t inst = blockIdx.x;
+  const int64_t lo = in.layer_off[inst];
+  const int L = (int)(in.layer_off[inst + 1] - lo);
+  const bool sac = in.source_at_client[inst] != 0;
+  const int64_t budget = in.budget[inst];
+  __shared__ double s_val[32];
+  __shared__ uint32_t s_mask[32];
+  __shared__ int s_found[32];
+  double best_v = -INFINITY;
+  uint32_t best_m = 0xffffffffu;
+  int found = 0;
+  const uint32_t nmask = 1u << L;
+  for (uint32_t mask = threadIdx.x; mask < nmask; mask += blockDim.x) {
+    int64_t lat = 0;
+    double v = 0.0;
+    int prev = sac ? 1 : 0;
+    for (int k = 0; k < L; ++k) {
+      const int x = (mask >> (L - 1 - k)) & 1;  // layer 1 is the MSB
+      if (x) {
+        lat += in.client_units[lo + k] + (prev ? 0 : in.down_units[lo + k]);
+        v = dadd(v, in.r[lo + k]);
+      } else {
+        lat += in.server_units[lo + k] + (prev ? in.up_units[lo + k] : 0);
+      }
+      prev = x;
+    }
+    if (lat <= budget && (!found || v > best_v || (v == best_v && mask < best_m))) {
+      best_v = v;
+      best_m = mask;
+      found = 1;
+    }
+  }
+  // warp + block arg-reduction: larger value, then smaller mask
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best_v, o);
+    const uint32_t om = __shfl_xor_sync(0xffffffffu, best_m, o);
+    const int of = __shfl_xor_sync(0xffffffffu, found, o);
+    if (of && (!found || ov > best_v || (ov == best_v && om < best_m))) {
+      best_v = ov;
+      best_m = om;
+      found = 1;
+    }
+  }
+  if (lane == 0) {
+    s_val[wid] = best_v;
+    s_mask[wid] = best_m;
+    s_found[wid] = found;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x / 32;
+    for (int w = 1; w < nw; ++w) {
+      if (s_found[w] && (!found || s_val[w] > best_v || (s_val[w] == best_v && s_mask[w] < best_m))) {
+        best_v = s_val[w];
+        best_m = s_mask[w];
+        found = 1;
+      }
+    }
+    uint8_t* pi = out.pi + lo;
+    for (int k = 0; k < L; ++k) pi[k] = found ? (uint8_t)((best_m >> (L - 1 - k)) & 1) : 0;
+    int32_t idx[32];  // L <= 24 (planner.py:21 ORACLE_MAX_LAYERS)
+    finish_policy(in, inst, lo, L, idx, out, !found, false);
+    out.status[inst] = SP_OK;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Eq. (1) latency (evaluator.py:64-69): one thread per instance
+
+__global__ void eq1_kernel(sp_instances in, const double* cs, const double* ss, const double* up,
+                           const double* dn, const uint8_t* pi, double* lat_out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= in.n) return;
+  const int64_t lo = in.layer_off[t];
+  const int64_t L = in.layer_off[t + 1] - lo;
+  const double x0 = in.source_at_client[t] ? 1.0 : 0.0;
+  auto term = [&](int64_t k) {
+    const double x = pi[lo + k] ? 1.0 : 0.0;
+    const double xp = k == 0 ? x0 : (pi[lo + k - 1] ? 1.0 : 0.0);
+    // x * (c + (1 - xp) * d) + (1 - x) * (s + xp * u), numpy elementwise order
+    const double a = dmul(x, dadd(cs[lo + k], dmul(dadd(1.0, -xp), dn[lo + k])));
+    const double b = dmul(dadd(1.0, -x), dadd(ss[lo + k], dmul(xp, up[lo + k])));
+    return dadd(a, b);
+  };
+  lat_out[t] = np_sum(term, L);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+int validate(const sp_instances* in) {
+  if (!in) {
+    set_error(SP_ERR_INVALID, "null instance batch");
+    return SP_ERR_INVALID;
+  }
+  if (in->n < 0 || in->total_layers < 0) {
+    set_error(SP_ERR_INVALID, "negative sizes");
+    return SP_ERR_INVALID;
+  }
+  if (in->n > 0 && (!in->layer_off || !in->client_units || !in->server_units || !in->up_units ||
+                    !in->down_units || !in->r || !in->budget || !in->source_at_client)) {
+    set_error(SP_ERR_INVALID, "null array in instance batch");
+    return SP_ERR_INVALID;
+  }
+  return SP_OK;
+}
+
+int validate_out(const sp_policies* out) {
+  if (!out || !out->pi || !out->client_value || !out->server_load || !out->integer_latency ||
+      !out->feasible || !out->status) {
+    set_error(SP_ERR_INVALID, "null array in policy batch");
+    return SP_ERR_INVALID;
+  }
+  return SP_OK;
+}
+
+struct Carve {
+  uint8_t* base;
+  size_t cap, used = 0;
+  void* take(size_t bytes) {
+    used = align_up(used, 256);
+    void* p = base + used;
+    used += bytes;
+    return p;
+  }
+};
+
+int threads_for(int64_t ncol) {
+  const int64_t per = (int64_t)kCellsPerThread;
+  const int64_t nch = std::max<int64_t>(1, (ncol + per * kMaxThreads - 1) / (per * kMaxThreads));
+  int64_t t = (ncol + per * nch - 1) / (per * nch);
+  t = (t + 31) / 32 * 32;
+  return (int)std::min<int64_t>(kMaxThreads, std::max<int64_t>(64, t));
+}
+
+template <int MODE>
+size_t row_bytes(int64_t ncol) {
+  return 2 * (size_t)ncol * sizeof(typename VT<MODE>::T);
+}
+size_t row_bytes_mode(int mode, int64_t ncol) {
+  return mode == VM_INT32 ? row_bytes<VM_INT32>(ncol) : row_bytes<VM_F64>(ncol);
+}
+size_t stage_bytes_mode(int mode) {
+  const size_t v = mode == VM_INT32 ? 4 : 8;
+  return align_up(kStageTile * (sizeof(StageShift) + v), 16);
+}
+
+template <int MODE, bool SMEM>
+int launch_dp(const DpArgs& a, int64_t n_items, int threads, size_t smem, cudaStream_t st) {
+  auto kern = dp_stage_kernel<MODE, SMEM, kCellsPerThread>;
+  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kSmemCap),
+                      "cudaFuncSetAttribute(dp_stage_kernel)");
+  if (rc) return rc;
+  kern<<<(unsigned)n_items, threads, smem, st>>>(a);
+  return launch_check("dp_stage_kernel launch");
+}
+
+int launch_dp_group(int mode, bool smem_rows, const DpArgs& a, int64_t n_items, int threads,
+                    size_t smem, cudaStream_t st) {
+  if (n_items == 0) return SP_OK;
+  switch (mode * 2 + (smem_rows ? 1 : 0)) {
+    case VM_INT32 * 2 + 1: return launch_dp<VM_INT32, true>(a, n_items, threads, smem, st);
+    case VM_INT32 * 2 + 0: return launch_dp<VM_INT32, false>(a, n_items, threads, smem, st);
+    case VM_F64 * 2 + 1: return launch_dp<VM_F64, true>(a, n_items, threads, smem, st);
+    case VM_F64 * 2 + 0: return launch_dp<VM_F64, false>(a, n_items, threads, smem, st);
+    case VM_F64_NAN * 2 + 1: return launch_dp<VM_F64_NAN, true>(a, n_items, threads, smem, st);
+    default: return launch_dp<VM_F64_NAN, false>(a, n_items, threads, smem, st);
+  }
+}
+
+// Shared driver of sp_plan_dp and sp_build_dp_tables.
+int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_s, void* ws,
+           size_t ws_bytes, cudaStream_t st) {
+  const int64_t n = in->n, total = in->total_layers;
+  if (n == 0) return SP_OK;
+  Carve cv{(uint8_t*)ws, ws_bytes};
+  InstInfo* info = (InstInfo*)cv.take(sizeof(InstInfo) * n);
+  StageShift* shifts = (StageShift*)cv.take(sizeof(StageShift) * total);
+  int64_t* rv = (int64_t*)cv.take(sizeof(int64_t) * total);
+  int32_t* idx = (int32_t*)cv.take(sizeof(int32_t) * total);
+  DpWork* work = (DpWork*)cv.take(sizeof(DpWork) * n);
+  const size_t fixed = align_up(cv.used, 256);
+  if (!ws || fixed > ws_bytes) {
+    set_required_workspace(fixed + (1 << 20));
+    set_error(SP_ERR_WORKSPACE, "workspace %zu B < fixed part %zu B", ws_bytes, fixed);
+    return SP_ERR_WORKSPACE;
+  }
+  const int grid = (int)std::min<int64_t>(n, 1 << 20);
+  prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv);
+  int rc = launch_check("prep_kernel launch");
+  if (rc) return rc;
+
+  std::vector<InstInfo> hinfo(n);
+  std::vector<int64_t> hoff(n + 1);
+  rc = check_cuda(cudaMemcpyAsync(hinfo.data(), info, sizeof(InstInfo) * n, cudaMemcpyDeviceToHost, st),
+                  "copy instance info");
+  if (rc) return rc;
+  rc = check_cuda(cudaMemcpyAsync(hoff.data(), in->layer_off, sizeof(int64_t) * (n + 1),
+                                  cudaMemcpyDeviceToHost, st),
+                  "copy layer offsets");
+  if (rc) return rc;
+  rc = check_cuda(cudaStreamSynchronize(st), "sync after prep");
+  if (rc) return rc;
+
+  const size_t avail = ws_bytes - fixed;
+  uint8_t* dyn = (uint8_t*)ws + fixed;
+  struct Item {
+    int64_t inst, L, ncol;
+    int mode;
+    bool smem;
+    size_t bp, rows;
+  };
+  std::vector<Item> items;
+  items.reserve(n);
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t ncol = hinfo[k].w_eff + 1;
+    if (ncol > kMaxCols) {
+      set_error(SP_ERR_UNSUPPORTED, "instance %lld: W_eff = %lld exceeds the supported 2^31 columns",
+                (long long)k, (long long)hinfo[k].w_eff);
+      return SP_ERR_UNSUPPORTED;
+    }
+    Item it;
+    it.inst = k;
+    it.L = hoff[k + 1] - hoff[k];
+    it.ncol = ncol;
+    it.mode = hinfo[k].mode;
+    const size_t rb = row_bytes_mode(it.mode, ncol);
+    it.smem = rb + stage_bytes_mode(it.mode) <= kSmemCap;
+    it.bp = align_up((size_t)it.L * (size_t)ncol, 256);
+    it.rows = it.smem ? 0 : align_up(rb, 256);
+    items.push_back(it);
+  }
+
+  DpArgs a;
+  a.layer_off = in->layer_off;
+  a.sac = in->source_at_client;
+  a.info = info;
+  a.shifts = shifts;
+  a.rv = rv;
+  a.work = work;
+  a.bp = dyn;
+  a.rows = dyn;
+  a.tab_c = tab_c;
+  a.tab_s = tab_s;
+
+  size_t wave_bytes = 0;
+  size_t pos = 0;
+  std::vector<DpWork> hwork;
+  while (pos < items.size()) {
+    // gather one wave
+    size_t end = pos;
+    wave_bytes = 0;
+    while (end < items.size() && wave_bytes + items[end].bp + items[end].rows <= avail) {
+      wave_bytes += items[end].bp + items[end].rows;
+      ++end;
+    }
+    if (end == pos) {
+      set_required_workspace(fixed + items[pos].bp + items[pos].rows);
+      set_error(SP_ERR_WORKSPACE, "instance %lld needs %zu B of DP workspace, %zu B available",
+                (long long)items[pos].inst, items[pos].bp + items[pos].rows, avail);
+      return SP_ERR_WORKSPACE;
+    }
+    // lay out the wave: back-pointers then global rows; group work items by kernel variant
+    hwork.clear();
+    size_t off = 0;
+    std::vector<DpWork> groups[6];
+    int gthreads[6] = {0, 0, 0, 0, 0, 0};
+    size_t gsmem[6] = {0, 0, 0, 0, 0, 0};
+    double gcells[6] = {0, 0, 0, 0, 0, 0};
+    for (size_t q = pos; q < end; ++q) {
+      const Item& it = items[q];
+      DpWork w;
+      w.inst = it.inst;
+      w.bp_off = (int64_t)off;
+      off += it.bp;
+      if (!it.smem) {
+        w.row_off = (int64_t)off;
+        off += it.rows;
+      } else {
+        w.row_off = -1;
+      }
+      const int gi = it.mode * 2 + (it.smem ? 1 : 0);
+      groups[gi].push_back(w);
+      gcells[gi] += (double)it.L * (double)it.ncol;
+      gthreads[gi] = std::max(gthreads[gi], threads_for(it.ncol));
+      if (it.smem)
+        gsmem[gi] = std::max(gsmem[gi], stage_bytes_mode(it.mode) + row_bytes_mode(it.mode, it.ncol));
+      else
+        gsmem[gi] = stage_bytes_mode(it.mode);
+    }
+    for (int gi = 0; gi < 6; ++gi)
+      for (const DpWork& w : groups[gi]) hwork.push_back(w);
+    rc = check_cuda(cudaMemcpyAsync(work, hwork.data(), sizeof(DpWork) * hwork.size(),
+                                    cudaMemcpyHostToDevice, st),
+                    "upload work list");
+    if (rc) return rc;
+    int64_t first = 0;
+    for (int gi = 0; gi < 6; ++gi) {
+      const int64_t cnt = (int64_t)groups[gi].size();
+      if (!cnt) continue;
+      DpArgs ga = a;
+      ga.work = work + first;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (profiling()) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+      }
+      rc = launch_dp_group(gi / 2, gi % 2 == 1, ga, cnt, gthreads[gi], gsmem[gi], st);
+      if (rc) return rc;
+      if (profiling()) {
+        cudaEventRecord(e1, st);
+        // algorithmic HBM bytes per cell: SMEM rows -> the back-pointer byte
+        // only; global rows -> read + write of both rows + the back-pointer
+        const double vb = (gi / 2 == VM_INT32) ? 4.0 : 8.0;
+        const double per_cell = (gi % 2 == 1) ? 1.0 : 4.0 * vb + 1.0;
+        prof_record_dp(e0, e1, gcells[gi], gcells[gi] * per_cell);
+      }
+      first += cnt;
+    }
+    if (out) {
+      const int64_t nw = (int64_t)hwork.size();
+      backtrack_kernel<<<(unsigned)((nw + 127) / 128), 128, 0, st>>>(*in, info, shifts, work, nw, dyn,
+                                                                      idx, *out);
+      rc = launch_check("backtrack_kernel launch");
+      if (rc) return rc;
+    }
+    // the host work vector is reused next wave: the pageable H2D copy above is
+    // synchronous with respect to the host buffer, so reuse is safe.
+    pos = end;
+  }
+  return SP_OK;
+}
+
+}  // namespace
+}  // namespace sp
+
+using namespace sp;
+
+extern "C" {
+
+int sp_effective_budget(const sp_instances* in, int64_t* w_eff, void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  if (in->n == 0) return SP_OK;
+  if (!w_eff) {
+    set_error(SP_ERR_INVALID, "null w_eff");
+    return SP_ERR_INVALID;
+  }
+  const int grid = (int)std::min<int64_t>(in->n, 1 << 20);
+  weff_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*in, w_eff);
+  return launch_check("weff_kernel launch");
+}
+
+int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes, void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  rc = validate_out(out);
+  if (rc) return rc;
+  return run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int sp_build_dp_tables(const sp_instances* in, int64_t w_eff, double* client_table,
+                       double* server_table, void* ws, size_t ws_bytes, void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  if (in->n != 1 || !client_table || !server_table) {
+    set_error(SP_ERR_INVALID, "sp_build_dp_tables takes exactly one instance and two tables");
+    return SP_ERR_INVALID;
+  }
+  (void)w_eff;
+  return run_dp(in, nullptr, client_table, server_table, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+
+int sp_evaluate_policy(const sp_instances* in, const uint8_t* pi, sp_policies* out, void* ws,
+                       size_t ws_bytes, void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  rc = validate_out(out);
+  if (rc) return rc;
+  if (in->n == 0) return SP_OK;
+  if (!pi) {
+    set_error(SP_ERR_INVALID, "null pi");
+    return SP_ERR_INVALID;
+  }
+  const size_t need = sizeof(int32_t) * (size_t)in->total_layers;
+  if (!ws || ws_bytes < need) {
+    set_required_workspace(need);
+    set_error(SP_ERR_WORKSPACE, "sp_evaluate_policy needs %zu B of scratch", need);
+    return SP_ERR_WORKSPACE;
+  }
+  evaluate_kernel<<<(unsigned)((in->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*in, pi, *out,
+                                                                                     (int32_t*)ws);
+  return launch_check("evaluate_kernel launch");
+}
+
+int sp_plan_prefix(const sp_instances* in, int32_t which, sp_policies* out, void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  rc = validate_out(out);
+  if (rc) return rc;
+  if (which < SP_GREEDY || which > SP_ALL_CLIENT) {
+    set_error(SP_ERR_INVALID, "unknown prefix planner %d", which);
+    return SP_ERR_INVALID;
+  }
+  if (in->n == 0) return SP_OK;
+  const int64_t threads = in->n * 32;
+  prefix_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*in, which, *out);
+  return launch_check("prefix_kernel launch");
+}
+
+int sp_plan_exhaustive(const sp_instances* in, sp_policies* out, void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  rc = validate_out(out);
+  if (rc) return rc;
+  if (in->n == 0) return SP_OK;
+  exhaustive_kernel<<<(unsigned)in->n, 256, 0, (cudaStream_t)stream>>>(*in, *out);
+  return launch_check("exhaustive_kernel launch");
+}
+
+int sp_latency_eq1(const sp_instances* in, const double* client_s, const double* server_s,
+                   const double* up_s, const double* down_s, const uint8_t* pi, double* latency_s,
+                   void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  if (in->n == 0) return SP_OK;
+  if (!client_s || !server_s || !up_s || !down_s || !pi || !latency_s) {
+    set_error(SP_ERR_INVALID, "null array in sp_latency_eq1");
+    return SP_ERR_INVALID;
+  }
+  eq1_kernel<<<(unsigned)((in->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      *in, client_s, server_s, up_s, down_s, pi, latency_s);
+  return launch_check("eq1_kernel launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,181 @@
+// K4: FIFO capacity-queue replay (reference: throughput_sim.py:207-256).
+//
+// One thread replays one independent run (a (stream, capacity) pair); a
+// Monte-Carlo sweep launches tens of thousands of runs at once.  The waiting
+// queue of the reference is always the contiguous index range [head, next)
+// of arrivals, so only the in-service min-heap needs storage: a per-run
+// binary heap of (finish_ms, seq, request) in the caller's workspace, keyed
+// lexicographically on (finish, seq) exactly like the reference's heapq
+// tuples (seq is unique, so the pop order is fully determined).
+#include <algorithm>
+
+#include "sp_internal.cuh"
+
+namespace sp {
+namespace {
+
+struct HeapEntry {
+  double finish;
+  int32_t seq;
+  int32_t req;
+};
+
+__device__ __forceinline__ bool less(const HeapEntry& a, const HeapEntry& b) {
+  return a.finish < b.finish || (a.finish == b.finish && a.seq < b.seq);
+}
+
+__device__ void heap_push(HeapEntry* h, int64_t& size, HeapEntry e) {
+  int64_t c = size++;
+  while (c > 0) {
+    const int64_t p = (c - 1) >> 1;
+    const HeapEntry pe = h[p];
+    if (!less(e, pe)) break;
+    h[c] = pe;
+    c = p;
+  }
+  h[c] = e;
+}
+
+__device__ HeapEntry heap_pop(HeapEntry* h, int64_t& size) {
+  const HeapEntry top = h[0];
+  const HeapEntry last = h[--size];
+  int64_t c = 0;
+  while (true) {
+    int64_t l = 2 * c + 1;
+    if (l >= size) break;
+    HeapEntry le = h[l];
+    if (l + 1 < size) {
+      const HeapEntry re = h[l + 1];
+      if (less(re, le)) {
+        le = re;
+        ++l;
+      }
+    }
+    if (!less(le, last)) break;
+    h[c] = le;
+    c = l;
+  }
+  if (size > 0) h[c] = last;
+  return top;
+}
+
+__global__ void sim_replay_kernel(sp_sim_batch b, sp_sim_out o, HeapEntry* heap_ws) {
+  const int64_t run = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (run >= b.n_runs) return;
+  const int64_t lo = b.run_off[run];
+  const int64_t n = b.run_off[run + 1] - lo;
+  const double* arr = b.arrival_ms + lo;
+  const double* dem = b.demand + lo;
+  const double* dur = b.duration_ms + lo;
+  double* admit = o.admit_ms + lo;
+  HeapEntry* h = heap_ws + lo;  // a run never holds more than n in service
+  const double cap = b.capacity[run];
+  const double eps = dmul(1e-9, cap);
+  double free_cap = cap;
+  int64_t hsize = 0, head = 0, next = 0;
+  int32_t seq = 0;
+  int32_t status = SP_OK;
+  int64_t dead = -1;
+  for (int64_t k = 0; k < n; ++k) admit[k] = 0.0;
+  while (next < n || hsize > 0) {
+    const double t_arr = next < n ? arr[next] : INFINITY;
+    double now;
+    if (hsize > 0 && h[0].finish <= t_arr) {  // completions before equal-time arrivals
+      const HeapEntry e = heap_pop(h, hsize);
+      now = e.finish;
+      free_cap = dadd(free_cap, dem[e.req]);
+    } else {
+      now = t_arr;
+      ++next;
+    }
+    while (head < next) {
+      const double need = dem[head];
+      if (need <= dadd(free_cap, eps)) {
+        admit[head] = now;
+        free_cap = dadd(free_cap, -need);
+        HeapEntry e;
+        e.finish = dadd(now, dur[head]);
+        e.seq = seq++;
+        e.req = (int32_t)head;
+        heap_push(h, hsize, e);
+        ++head;
+      } else {
+        if (need > dadd(cap, eps)) {
+          status = SP_ERR_DEADLOCK;
+          dead = head;
+        }
+        break;
+      }
+    }
+    if (status != SP_OK) break;
+  }
+  o.status[run] = status;
+  if (o.deadlock_req) o.deadlock_req[run] = dead;
+  if (status != SP_OK) return;
+  // waits, max, numpy-order mean, sequential cumsum (throughput_sim.py:122-130, 247)
+  double mx = -INFINITY, run_sum = 0.0;
+  for (int64_t k = 0; k < n; ++k) {
+    const double w = dadd(admit[k], -arr[k]);
+    if (o.wait_ms) o.wait_ms[lo + k] = w;
+    if (o.cum_wait_ms) {
+      run_sum = (k == 0) ? w : dadd(run_sum, w);
+      o.cum_wait_ms[lo + k] = run_sum;
+    }
+    mx = (w > mx || w != w) ? w : mx;
+  }
+  if (o.max_wait_ms) o.max_wait_ms[run] = n ? mx : 0.0;
+  if (o.mean_wait_ms) {
+    const double s = np_sum([&](int64_t k) { return dadd(admit[k], -arr[k]); }, n);
+    o.mean_wait_ms[run] = n ? ddiv(s, (double)n) : 0.0;
+  }
+}
+
+__global__ void segment_sum_kernel(const double* x, const int64_t* off, int64_t n_seg, double* out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_seg) return;
+  const double* a = x + off[k];
+  out[k] = np_sum([&](int64_t i) { return a[i]; }, off[k + 1] - off[k]);
+}
+
+}  // namespace
+}  // namespace sp
+
+using namespace sp;
+
+extern "C" {
+
+int sp_segment_sum(const double* x, const int64_t* seg_off, int64_t n_seg, double* out, void* stream) {
+  if (n_seg < 0 || (n_seg > 0 && (!x || !seg_off || !out))) {
+    set_error(SP_ERR_INVALID, "sp_segment_sum: bad arguments");
+    return SP_ERR_INVALID;
+  }
+  if (n_seg == 0) return SP_OK;
+  segment_sum_kernel<<<(unsigned)((n_seg + 127) / 128), 128, 0, (cudaStream_t)stream>>>(x, seg_off, n_seg,
+                                                                                       out);
+  return launch_check("segment_sum_kernel launch");
+}
+
+size_t sp_sim_workspace_bytes(const sp_sim_batch* b) {
+  if (!b) return 0;
+  return sizeof(HeapEntry) * (size_t)std::max<int64_t>(1, b->total_requests);
+}
+
+int sp_sim_replay(const sp_sim_batch* b, sp_sim_out* o, void* ws, size_t ws_bytes, void* stream) {
+  if (!b || !o || b->n_runs < 0 || (b->n_runs > 0 && (!b->run_off || !b->capacity || !o->admit_ms ||
+                                                      !o->status))) {
+    set_error(SP_ERR_INVALID, "sp_sim_replay: bad arguments");
+    return SP_ERR_INVALID;
+  }
+  if (b->n_runs == 0) return SP_OK;
+  const size_t need = sp_sim_workspace_bytes(b);
+  if (!ws || ws_bytes < need) {
+    set_required_workspace(need);
+    set_error(SP_ERR_WORKSPACE, "sp_sim_replay needs %zu B of heap workspace", need);
+    return SP_ERR_WORKSPACE;
+  }
+  sim_replay_kernel<<<(unsigned)((b->n_runs + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      *b, *o, (HeapEntry*)ws);
+  return launch_check("sim_replay_kernel launch");
+}
+
+}  // extern "C"

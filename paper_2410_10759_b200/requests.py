@@ -1,0 +1,121 @@
+"""Request-level pipeline: (model, seq_len, devices, link, SLA) per request ->
+cost table (K1) -> optimal placement (prep + K2 + K3).
+
+This is the batched path BASELINE.json's configs exercise: every request is
+one independent SplitLLM placement problem (cost_model.profile ->
+problem.build_problem -> planner.plan_dp in the reference).  `RequestBatch`
+holds the per-request parameters in device memory; `solve()` runs the whole
+chain on one stream and leaves every result on the device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import batch as B
+from .cost_model import encode_models
+
+_REQ_FIELDS = ("model", "seq_len", "client_fps", "server_fps", "uplink_bps", "downlink_bps",
+               "propagation_s", "deadline_s", "unit_s", "flags")
+_REQ_DTYPES = dict(model=np.int32, seq_len=np.int64, flags=np.uint8)
+
+
+@dataclass
+class RequestBatch:
+    """Per-request scenario parameters (sp_requests), host or device tensors."""
+
+    model: torch.Tensor
+    seq_len: torch.Tensor
+    client_fps: torch.Tensor
+    server_fps: torch.Tensor
+    uplink_bps: torch.Tensor
+    downlink_bps: torch.Tensor
+    propagation_s: torch.Tensor
+    deadline_s: torch.Tensor
+    unit_s: torch.Tensor
+    flags: torch.Tensor
+
+    @property
+    def n(self) -> int:
+        return int(self.model.numel())
+
+    @classmethod
+    def from_numpy(cls, pin: bool = False, **arrays) -> "RequestBatch":
+        ts = {}
+        for f in _REQ_FIELDS:
+            a = np.ascontiguousarray(arrays[f], dtype=_REQ_DTYPES.get(f, np.float64))
+            t = torch.from_numpy(a)
+            ts[f] = t.pin_memory() if pin else t
+        return cls(**ts)
+
+    def to(self, device, non_blocking: bool = False) -> "RequestBatch":
+        return RequestBatch(**{f: getattr(self, f).to(device, non_blocking=non_blocking)
+                               for f in _REQ_FIELDS})
+
+    def host_bytes(self) -> int:
+        return sum(getattr(self, f).numel() * getattr(self, f).element_size() for f in _REQ_FIELDS)
+
+    def struct(self) -> N.SpRequests:
+        return N.SpRequests(self.n, *[N.ptr(getattr(self, f)).value for f in _REQ_FIELDS])
+
+
+@dataclass
+class Solved:
+    """Device results of one `solve` call."""
+
+    layer_off: torch.Tensor
+    instances: B.InstanceBatch
+    policies: B.PolicyBatch
+    status: torch.Tensor       # K1 status word per request
+    client_s: torch.Tensor
+    server_s: torch.Tensor
+    up_s: torch.Tensor
+    down_s: torch.Tensor
+
+
+class Engine:
+    """Holds the encoded model table on the device and solves request batches."""
+
+    def __init__(self, layer_lists, device=None):
+        self.device = device or N.device()
+        self.models, self._keep = encode_models(layer_lists, self.device)
+        self.n_layers = np.array([len(x) for x in layer_lists], dtype=np.int64)
+
+    def layer_offsets(self, req: RequestBatch) -> torch.Tensor:
+        off = torch.empty(req.n + 1, dtype=torch.int64, device=self.device)
+        N.check(N.library().sp_request_layer_offsets(self.models, req.struct(), N.ptr(off),
+                                                     N.stream_ptr()), "sp_request_layer_offsets")
+        return off
+
+    def cost_table(self, req: RequestBatch, total_layers: int, off: torch.Tensor | None = None):
+        dev = self.device
+        off = self.layer_offsets(req) if off is None else off
+        T = int(total_layers)
+        f = {k: torch.empty(T, dtype=torch.float64, device=dev)
+             for k in ("r", "cs", "ss", "up", "dn")}
+        i = {k: torch.empty(T, dtype=torch.int64, device=dev) for k in ("i", "s", "u", "d")}
+        budget = torch.empty(req.n, dtype=torch.int64, device=dev)
+        sac = torch.empty(req.n, dtype=torch.uint8, device=dev)
+        status = torch.empty(req.n, dtype=torch.int32, device=dev)
+        tab = N.SpCostTable(N.ptr(off).value, T, N.ptr(f["r"]).value, N.ptr(f["cs"]).value, None,
+                            None, N.ptr(f["ss"]).value, N.ptr(f["up"]).value, N.ptr(f["dn"]).value,
+                            N.ptr(i["i"]).value, N.ptr(i["s"]).value, N.ptr(i["u"]).value,
+                            N.ptr(i["d"]).value, N.ptr(budget).value, N.ptr(sac).value,
+                            N.ptr(status).value)
+        N.check(N.library().sp_build_cost_table(self.models, req.struct(), 1, tab, N.stream_ptr()),
+                "sp_build_cost_table")
+        inst = B.InstanceBatch(off, i["i"], i["s"], i["u"], i["d"], f["r"], budget, sac)
+        return inst, status, f
+
+    def solve(self, req: RequestBatch, total_layers: int | None = None,
+              off: torch.Tensor | None = None) -> Solved:
+        """K1 cost table + DP placement for every request (one stream)."""
+        if total_layers is None:
+            total_layers = int(self.n_layers[req.model.cpu().numpy()].sum())
+        inst, status, f = self.cost_table(req, total_layers, off)
+        pol = B.plan_dp(inst)
+        return Solved(inst.layer_off, inst, pol, status, f["cs"], f["ss"], f["up"], f["dn"])

@@ -1,0 +1,174 @@
+"""CUDA planners vs the reference's golden vectors and the pinned oracle.
+
+Bit-exact: placements, integer latencies and feasibility must be equal, and
+client_value / server_load equal as float64 bit patterns."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, Battery, assert_policy, load_npz
+from oracle import splitplan_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+BATTERIES = ["battery_acceptance", "battery_special", "battery_float", "battery_oracle_ties",
+             "battery_wide"]
+
+
+def _batch(bat: Battery, with_must=True):
+    from paper_2410_10759_b200 import batch as B
+    z = bat.z
+    return B.InstanceBatch.from_arrays(z["off"], z["i"], z["s"], z["u"], z["d"], z["r"],
+                                       z["budget"], z["sac"], z["must"] if with_must else None)
+
+
+def _compare(bat: Battery, planner: str, host: dict, *, backtrace_ok=False):
+    from paper_2410_10759_b200 import _native as N
+    off = bat.off
+    for k in range(bat.n):
+        exp = bat.expected(planner, k)
+        if exp is None:
+            assert host["status"][k] == N.SP_ERR_BACKTRACE, f"{bat.name}[{k}] expected assertion"
+            continue
+        assert host["status"][k] == 0, f"{bat.name}[{k}] status {host['status'][k]}"
+        got = dict(pi=host["pi"][off[k]:off[k + 1]], client_value=host["client_value"][k],
+                   server_load=host["server_load"][k], integer_latency=host["integer_latency"][k],
+                   feasible=host["feasible"][k])
+        assert_policy(got, exp, f"{bat.name}[{k}] {planner}")
+
+
+@pytest.mark.parametrize("name", BATTERIES)
+def test_dp_batch_matches_reference(gpu, name):
+    from paper_2410_10759_b200 import batch as B
+    bat = Battery(name)
+    b = _batch(bat)
+    w = B.effective_budget(b).cpu().numpy()
+    np.testing.assert_array_equal(w, bat.z["w_eff"])
+    _compare(bat, "dp", B.plan_dp(b).to_host())
+
+
+@pytest.mark.parametrize("name", BATTERIES)
+def test_prefix_planners_match_reference(gpu, name):
+    from paper_2410_10759_b200 import _native as N, batch as B
+    bat = Battery(name)
+    if not bat.has("greedy"):
+        pytest.skip("battery has no greedy outputs")
+    b = _batch(bat, with_must=False)
+    for planner, code in (("greedy", N.SP_GREEDY), ("all_server", N.SP_ALL_SERVER),
+                          ("all_client", N.SP_ALL_CLIENT)):
+        _compare(bat, planner, B.plan_prefix(b, code).to_host())
+
+
+@pytest.mark.parametrize("name", ["battery_acceptance", "battery_oracle_ties"])
+def test_exhaustive_matches_reference(gpu, name):
+    from paper_2410_10759_b200 import batch as B
+    bat = Battery(name)
+    _compare(bat, "oracle", B.plan_exhaustive(_batch(bat, with_must=False)).to_host())
+
+
+def test_dp_tables_match_reference(gpu):
+    from paper_2410_10759_b200 import planner as P
+    from paper_2410_10759_b200.problem import PlanProblem
+    z = load_npz("dp_tables")
+    off, pos = z["off"], 0
+    for k in range(len(off) - 1):
+        a, b = off[k], off[k + 1]
+        prob = PlanProblem.from_costs(z["i"][a:b], z["s"][a:b], z["u"][a:b], z["d"][a:b],
+                                      z["r"][a:b], int(z["budget"][k]),
+                                      source_at_client=bool(z["sac"][k]))
+        t = P.build_dp_tables(prob)
+        cnt = t.client.size
+        np.testing.assert_array_equal(t.client.ravel(), z["C"][pos:pos + cnt])
+        np.testing.assert_array_equal(t.server.ravel(), z["S"][pos:pos + cnt])
+        pos += cnt
+
+
+def test_dropin_fixtures(gpu):
+    """The reference's own frozen fixtures (tests/test_planner.py:26-108)."""
+    from paper_2410_10759_b200.planner import plan_dp, plan_greedy, plan_oracle, plan_trivial, run_planner
+    from paper_2410_10759_b200.problem import PlanProblem
+    a = PlanProblem.from_costs([4, 4, 4], [0, 0, 0], [1, 1, 1], [1, 1, 1], [5.0, 1.0, 5.0], 9)
+    b = PlanProblem.from_costs([4, 4, 4], [0, 0, 0], [1, 1, 1], [1, 1, 1], [1.0, 1.0, 10.0], 9)
+    p = plan_dp(a)
+    assert p.pi == (1, 1, 0) and p.server_load == 5.0 and p.client_value == 6.0
+    assert p.integer_latency == 9 and p.feasible
+    p = plan_dp(b)
+    assert p.pi == (0, 0, 1) and p.server_load == 2.0 and p.integer_latency == 6
+    g = plan_greedy(b)
+    assert g.pi == (1, 1, 0) and g.server_load == 10.0 and g.feasible
+    assert plan_trivial(a, "all_server").integer_latency == 1
+    assert plan_oracle(b).pi == (0, 0, 1)
+    assert plan_dp(b, must_end_at="server").pi[-1] == 0
+    with pytest.raises(ValueError):
+        plan_dp(b, must_end_at="edge")
+    with pytest.raises(ValueError):
+        run_planner("simulated-annealing", b)
+    assert run_planner("all-server", b).pi == (0, 0, 0)
+    nan = PlanProblem.from_costs([1, 1, 1], [1, 1, 1], [1, 1, 1], [1, 1, 1], [math.nan, 1.0, 2.0], 5)
+    with pytest.raises(AssertionError, match="no predecessor"):
+        plan_dp(nan)
+
+
+def _random_instances(seed, n, L_range, W_choices, r_kind):
+    rng = np.random.default_rng(seed)
+    out = []
+    for t in range(n):
+        L = int(rng.integers(*L_range))
+        W = int(rng.choice(W_choices))
+        hi = max(2, W // max(4, L // 3))
+        i, s = rng.integers(0, hi, L), rng.integers(0, max(2, hi // 6), L)
+        u, d = rng.integers(0, hi, L), rng.integers(0, hi, L)
+        if r_kind == "int":
+            r = rng.integers(0, 1000, L).astype(float)
+        elif r_kind == "bigint":
+            r = rng.integers(0, 2 ** 40, L).astype(float)
+        elif r_kind == "float":
+            r = rng.random(L) * 10.0 ** rng.integers(-2, 12, L)
+        else:
+            r = rng.integers(0, 10, L).astype(float)
+            r[rng.integers(0, L)] = math.inf
+        out.append(dict(i=i, s=s, u=u, d=d, r=r, budget=W, sac=bool(t % 2)))
+    return out
+
+
+@pytest.mark.parametrize("r_kind", ["int", "bigint", "float", "inf"])
+def test_dp_vs_oracle_smem_and_global_rows(gpu, r_kind):
+    """Seeded instances spanning SMEM-resident rows and global rows, in every
+    value domain (int32 exact, fp64 finite, fp64 NaN-propagating)."""
+    from paper_2410_10759_b200 import batch as B
+    seed = {"int": 1, "bigint": 2, "float": 3, "inf": 4}[r_kind]
+    insts = _random_instances(seed, 10, (3, 40), [50, 900, 9000, 20000, 40000], r_kind)
+    off = np.zeros(len(insts) + 1, np.int64)
+    np.cumsum([len(x["r"]) for x in insts], out=off[1:])
+    cat = lambda k: np.concatenate([x[k] for x in insts])
+    b = B.InstanceBatch.from_arrays(off, cat("i"), cat("s"), cat("u"), cat("d"), cat("r"),
+                                    [x["budget"] for x in insts], [x["sac"] for x in insts])
+    host = B.plan_dp(b).to_host()
+    for k, inst in enumerate(insts):
+        try:
+            exp = O.plan_dp(inst)
+        except AssertionError:
+            assert host["status"][k] != 0
+            continue
+        got = dict(pi=host["pi"][off[k]:off[k + 1]], client_value=host["client_value"][k],
+                   server_load=host["server_load"][k], integer_latency=host["integer_latency"][k],
+                   feasible=host["feasible"][k])
+        assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{r_kind}[{k}]")
+
+
+@pytest.mark.parametrize("name", ["battery_large_model", "battery_large_chain"])
+def test_full_size_batteries(gpu, name):
+    """W_eff = 1e5 model-derived instances (BASELINE cfg2 shape) and the
+    cfg5-reduced chains (L=1e5 x W=1e3, L=1e3 x W=1e5)."""
+    if not (GOLDEN / f"{name}.npz").exists():
+        pytest.skip("large battery not generated")
+    from paper_2410_10759_b200 import _native as N, batch as B
+    bat = Battery(name)
+    b = _batch(bat, with_must=False)
+    _compare(bat, "dp", B.plan_dp(b).to_host())
+    if bat.has("greedy"):
+        _compare(bat, "greedy", B.plan_prefix(b, N.SP_GREEDY).to_host())
