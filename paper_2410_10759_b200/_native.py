@@ -9,6 +9,7 @@ or a CUDA device is missing, calls raise.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -199,7 +200,8 @@ def workspace(min_bytes: int = 0) -> torch.Tensor:
             cur = None
             torch.cuda.empty_cache()
         free, _total = torch.cuda.mem_get_info(dev)
-        want = max(min_bytes, min(64 << 30, int(free * 0.45)), 64 << 20)
+        cap = int(float(os.environ.get("SPLITPLAN_WS_GB", "64")) * (1 << 30))
+        want = max(min_bytes, min(cap, int(free * 0.45)), 64 << 20)
         _ws[key] = torch.empty(want, dtype=torch.uint8, device=dev)
     return _ws[key]
 

@@ -61,30 +61,74 @@ __host__ __device__ inline double ddiv(double a, double b) {
 // (planner.py:90-91, evaluator.py:69, throughput_sim.py:122-130), so the
 // engine replays the same association order.  `get(i)` yields element i.
 
+// one leaf block (n <= 128)
 template <typename Get>
-__host__ __device__ inline double pairwise_sum(const Get& get, int64_t lo, int64_t n) {
+__host__ __device__ inline double pairwise_leaf(const Get& get, int64_t lo, int64_t n) {
   if (n < 8) {
     double res = 0.0;
     for (int64_t i = 0; i < n; ++i) res = dadd(res, get(lo + i));
     return res;
   }
-  if (n <= 128) {
-    double acc[8];
+  double acc[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = get(lo + j);
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8) {
+  for (int j = 0; j < 8; ++j) acc[j] = get(lo + j);
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = dadd(acc[j], get(lo + i + j));
-    }
-    double res = dadd(dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3])),
-                              dadd(dadd(acc[4], acc[5]), dadd(acc[6], acc[7])));
-    for (; i < n; ++i) res = dadd(res, get(lo + i));
-    return res;
+    for (int j = 0; j < 8; ++j) acc[j] = dadd(acc[j], get(lo + i + j));
   }
+  double res = dadd(dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3])),
+                    dadd(dadd(acc[4], acc[5]), dadd(acc[6], acc[7])));
+  for (; i < n; ++i) res = dadd(res, get(lo + i));
+  return res;
+}
+
+__host__ __device__ inline int64_t pairwise_split(int64_t n) {
   int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return dadd(pairwise_sum(get, lo, n2), pairwise_sum(get, lo + n2, n - n2));
+  return n2 - n2 % 8;
+}
+
+// The recursion pw(a, n) = pw(a, n2) + pw(a + n2, n - n2) for n > 128, run
+// with an explicit stack (device threads have a 1 KB default stack; depth is
+// at most 64 levels since every level halves n).
+template <typename Get>
+__host__ __device__ inline double pairwise_sum(const Get& get, int64_t lo0, int64_t n0) {
+  if (n0 <= 128) return pairwise_leaf(get, lo0, n0);
+  int64_t lo[64], nn[64];
+  double left[64];
+  uint8_t state[64];  // 1: left child pending, 2: right child pending
+  int sp = 0;
+  lo[0] = lo0;
+  nn[0] = n0;
+  state[0] = 0;
+  double ret = 0.0;
+  while (sp >= 0) {
+    if (nn[sp] > 128 && state[sp] == 0) {
+      state[sp] = 1;
+      lo[sp + 1] = lo[sp];
+      nn[sp + 1] = pairwise_split(nn[sp]);
+      state[sp + 1] = 0;
+      ++sp;
+      continue;
+    }
+    ret = pairwise_leaf(get, lo[sp], nn[sp]);
+    --sp;
+    while (sp >= 0) {  // hand the finished subtree to its parents
+      if (state[sp] == 1) {
+        left[sp] = ret;
+        state[sp] = 2;
+        const int64_t n2 = pairwise_split(nn[sp]);
+        lo[sp + 1] = lo[sp] + n2;
+        nn[sp + 1] = nn[sp] - n2;
+        state[sp + 1] = 0;
+        ++sp;
+        break;
+      }
+      ret = dadd(left[sp], ret);
+      --sp;
+    }
+  }
+  return ret;
 }
 
 template <typename Get>
