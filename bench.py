@@ -248,7 +248,7 @@ def main():
 
     # ---- device-resident timing -----------------------------------------
     lib.sp_profile_enable(1)
-    lib.sp_profile_collect(None, None, None, None, None)
+    lib.sp_profile_collect(None, None, None, None, None, None)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -259,10 +259,10 @@ def main():
         barrier()
     dev_ms = ev0.elapsed_time(ev1)
     import ctypes as C
-    dk_ms, dk_n, dk_cells, dk_bytes, all_l = (C.c_double(), C.c_int64(), C.c_double(),
-                                              C.c_double(), C.c_int64())
+    dk_ms, dk_n, dk_cells, dk_bytes, all_l, dk_var = (C.c_double(), C.c_int64(), C.c_double(),
+                                                      C.c_double(), C.c_int64(), C.c_int32())
     lib.sp_profile_collect(C.byref(dk_ms), C.byref(dk_n), C.byref(dk_cells), C.byref(dk_bytes),
-                           C.byref(all_l))
+                           C.byref(all_l), C.byref(dk_var))
     lib.sp_profile_enable(0)
 
     # ---- end-to-end timing (host buffers, copies inside) ------------------
@@ -319,7 +319,8 @@ def main():
                     "h2d_bytes_per_step": host_req.host_bytes(), "d2h_bytes_per_step": d2h},
             "gpu_launches": int(all_l.value),
             "roofline": {
-                "kernel": "dp_stage_kernel",
+                "kernel": ["dp_stage_kernel<smem rows>", "dp_cluster_kernel<DSMEM rows>",
+                           "dp_stage_kernel<global rows>"][dk_var.value],
                 "bound": "hbm",
                 "achieved": achieved,
                 "peak": peak,

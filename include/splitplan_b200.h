@@ -81,11 +81,13 @@ size_t sp_last_required_workspace(void);
  * DP-stage kernel launch is bracketed by CUDA events on its stream and every
  * kernel the library launches is counted. sp_profile_collect synchronises
  * the recorded events and returns: total DP-stage kernel ms, DP-stage
- * launches, DP cells and algorithmic DP bytes those launches processed, and
- * the count of all library kernel launches; then resets the counters. */
+ * launches, DP cells and algorithmic DP bytes those launches processed, the
+ * count of all library kernel launches, and the DP variant that took the most
+ * time (0 = rows in one CTA's SMEM, 1 = rows in cluster DSMEM, 2 = rows in
+ * global memory); then resets the counters. */
 void sp_profile_enable(int on);
 int sp_profile_collect(double* dp_kernel_ms, int64_t* dp_launches, double* dp_cells,
-                       double* dp_bytes, int64_t* all_launches);
+                       double* dp_bytes, int64_t* all_launches, int32_t* dp_variant);
 
 /* ---- planner (planner.py) ---------------------------------------------- */
 

@@ -92,7 +92,7 @@ SIGNATURES = {
     "sp_profile_enable": (None, [C.c_int]),
     "sp_profile_collect": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                      C.POINTER(C.c_double), C.POINTER(C.c_double),
-                                     C.POINTER(C.c_int64)]),
+                                     C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "sp_effective_budget": (C.c_int, [C.POINTER(SpInstances), P, P]),
     "sp_plan_dp": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_size_t, P]),
     "sp_build_dp_tables": (C.c_int, [C.POINTER(SpInstances), C.c_int64, P, P, P, C.c_size_t, P]),

@@ -14,6 +14,7 @@ thread_local size_t g_required_ws = 0;
 struct DpRec {
   cudaEvent_t a, b;
   double cells, bytes;
+  int variant;
 };
 thread_local bool g_prof = false;
 thread_local int64_t g_launches = 0;
@@ -46,8 +47,8 @@ void set_required_workspace(size_t bytes) { g_required_ws = bytes; }
 
 bool profiling() { return g_prof; }
 
-void prof_record_dp(cudaEvent_t start, cudaEvent_t stop, double cells, double bytes) {
-  g_dp.push_back(DpRec{start, stop, cells, bytes});
+void prof_record_dp(cudaEvent_t start, cudaEvent_t stop, double cells, double bytes, int variant) {
+  g_dp.push_back(DpRec{start, stop, cells, bytes, variant});
 }
 
 }  // namespace sp
@@ -57,14 +58,16 @@ extern "C" {
 void sp_profile_enable(int on) { g_prof = on != 0; }
 
 int sp_profile_collect(double* dp_kernel_ms, int64_t* dp_launches, double* dp_cells,
-                       double* dp_bytes, int64_t* all_launches) {
+                       double* dp_bytes, int64_t* all_launches, int32_t* dp_variant) {
   double ms = 0, cells = 0, bytes = 0;
+  double by_variant[3] = {0, 0, 0};
   int rc = SP_OK;
   for (DpRec& r : g_dp) {
     float t = 0.f;
     if (rc == SP_OK) rc = sp::check_cuda(cudaEventSynchronize(r.b), "profile event sync");
     if (rc == SP_OK) rc = sp::check_cuda(cudaEventElapsedTime(&t, r.a, r.b), "profile elapsed");
     ms += t;
+    if (r.variant >= 0 && r.variant < 3) by_variant[r.variant] += t;
     cells += r.cells;
     bytes += r.bytes;
     cudaEventDestroy(r.a);
@@ -75,6 +78,12 @@ int sp_profile_collect(double* dp_kernel_ms, int64_t* dp_launches, double* dp_ce
   if (dp_cells) *dp_cells = cells;
   if (dp_bytes) *dp_bytes = bytes;
   if (all_launches) *all_launches = g_launches;
+  if (dp_variant) {
+    int best = 0;
+    for (int v = 1; v < 3; ++v)
+      if (by_variant[v] > by_variant[best]) best = v;
+    *dp_variant = best;
+  }
   g_dp.clear();
   g_launches = 0;
   return rc;

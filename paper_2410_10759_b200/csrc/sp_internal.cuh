@@ -21,7 +21,7 @@ int launch_check(const char* what);  // also counts the launch when profiling
 
 // profiling (sp_abi.cu): events around DP-stage launches
 bool profiling();
-void prof_record_dp(cudaEvent_t start, cudaEvent_t stop, double cells, double bytes);
+void prof_record_dp(cudaEvent_t start, cudaEvent_t stop, double cells, double bytes, int variant);
 
 // ---------------------------------------------------------------------------
 // IEEE round-to-nearest arithmetic that the compiler may never contract into

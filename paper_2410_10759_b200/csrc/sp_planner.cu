@@ -10,6 +10,9 @@
 //   eq1_kernel        evaluator latency_of (evaluator.py:64-78)
 //
 // See DESIGN.md for the data layout and the value domains.
+#include <stdlib.h>
+#include <string.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -182,6 +185,52 @@ struct DpArgs {
   double* tab_s;
 };
 
+// One DP cell: new C/S values and the back-pointer byte from the four
+// predecessor values (NEG where the shifted index is negative).
+template <int MODE, typename V>
+__device__ __forceinline__ void cell_update(V ca, V cb, V sa, V sb, V rk, bool vi, bool vid,
+                                            bool vs, bool vsu, V& cn, V& sn, uint32_t& bits) {
+  if (MODE == VM_INT32) {
+    // exact integer arithmetic: C-stay <=> ca >= cb, S-stay <=> sa >= sb
+    const bool c_stay = ca >= cb;
+    const bool s_stay = sa >= sb;
+    cn = (c_stay ? ca : cb) + rk;
+    sn = s_stay ? sa : sb;
+    bits = (c_stay ? 1u : 2u) | (s_stay ? 4u : 8u);
+  } else {
+    V cm, sm;
+    if (MODE == VM_F64_NAN) {  // np.maximum propagates NaN
+      cm = (ca != ca) ? ca : ((cb != cb) ? cb : (ca >= cb ? ca : cb));
+      sm = (sa != sa) ? sa : ((sb != sb) ? sb : (sa >= sb ? sa : sb));
+    } else {
+      cm = ca >= cb ? ca : cb;
+      sm = sa >= sb ? sa : sb;
+    }
+    const V c = dadd(cm, rk);
+    cn = c;
+    sn = sm;
+    uint32_t b = 0;
+    if (vi && dadd(ca, rk) == c) b |= 1u;
+    if (vid && dadd(cb, rk) == c) b |= 2u;
+    if (vs && sa == sm) b |= 4u;
+    if (vsu && sb == sm) b |= 8u;
+    bits = b;
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void load_stage_tile(const DpArgs& a, int64_t lo, int k, int L,
+                                                StageShift* st_sh, typename VT<MODE>::T* st_r) {
+  using V = typename VT<MODE>::T;
+  const int cnt = min(kStageTile, L - k);
+  for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+    st_sh[t] = a.shifts[lo + k + t];
+    const int64_t bits = a.rv[lo + k + t];
+    if (MODE == VM_INT32) st_r[t] = (V)(int32_t)bits;
+    else st_r[t] = (V)__longlong_as_double(bits);
+  }
+}
+
 template <int MODE, bool ROWS_SMEM, int E>
 __global__ void __launch_bounds__(kMaxThreads, 1) dp_stage_kernel(DpArgs a) {
   using V = typename VT<MODE>::T;
@@ -221,13 +270,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_stage_kernel(DpArgs a) {
     const int kt = k % kStageTile;
     if (kt == 0) {
       __syncthreads();
-      const int cnt = min(kStageTile, L - k);
-      for (int t = tid; t < cnt; t += T) {
-        st_sh[t] = a.shifts[lo + k + t];
-        const int64_t bits = a.rv[lo + k + t];
-        if (MODE == VM_INT32) st_r[t] = (V)(int32_t)bits;
-        else st_r[t] = (V)__longlong_as_double(bits);
-      }
+      load_stage_tile<MODE>(a, lo, k, L, st_sh, st_r);
     }
     __syncthreads();
     const StageShift sh = st_sh[kt];
@@ -250,32 +293,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_stage_kernel(DpArgs a) {
           const V cb = jid >= 0 ? Srow[jid] : NEG;
           const V sa = js >= 0 ? Srow[js] : NEG;
           const V sb = jsu >= 0 ? Crow[jsu] : NEG;
-          if (MODE == VM_INT32) {
-            // exact integer arithmetic: C-stay <=> ca >= cb, S-stay <=> sa >= sb
-            const bool c_stay = ca >= cb;
-            const bool s_stay = sa >= sb;
-            cn[e] = (c_stay ? ca : cb) + rk;
-            sn[e] = s_stay ? sa : sb;
-            bits[e] = (c_stay ? 1u : 2u) | (s_stay ? 4u : 8u);
-          } else {
-            V cm, sm;
-            if (MODE == VM_F64_NAN) {  // np.maximum propagates NaN
-              cm = (ca != ca) ? ca : ((cb != cb) ? cb : (ca >= cb ? ca : cb));
-              sm = (sa != sa) ? sa : ((sb != sb) ? sb : (sa >= sb ? sa : sb));
-            } else {
-              cm = ca >= cb ? ca : cb;
-              sm = sa >= sb ? sa : sb;
-            }
-            const V c = dadd(cm, rk);
-            cn[e] = c;
-            sn[e] = sm;
-            uint32_t b = 0;
-            if (ji >= 0 && dadd(ca, rk) == c) b |= 1u;
-            if (jid >= 0 && dadd(cb, rk) == c) b |= 2u;
-            if (js >= 0 && sa == sm) b |= 4u;
-            if (jsu >= 0 && sb == sm) b |= 8u;
-            bits[e] = b;
-          }
+          cell_update<MODE, V>(ca, cb, sa, sb, rk, ji >= 0, jid >= 0, js >= 0, jsu >= 0, cn[e],
+                               sn[e], bits[e]);
         }
       }
       __syncthreads();
@@ -299,6 +318,140 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_stage_kernel(DpArgs a) {
     a.info[inst].end_c = to_f64(Crow[ncol - 1], g);
     a.info[inst].end_s = to_f64(Srow[ncol - 1], g);
   }
+}
+
+// ---------------------------------------------------------------------------
+// K2 cluster variant: rows too long for one SM live in the distributed shared
+// memory of a thread-block cluster of G CTAs (G <= 16).  CTA q owns columns
+// [q*B, (q+1)*B) of both rows, double-buffered (stage k reads buffer k&1 and
+// writes buffer (k&1)^1), so one cluster barrier per stage orders everything:
+// it releases this stage's writes and guarantees no CTA still reads the buffer
+// the next stage overwrites.  Predecessor values come from whichever CTA owns
+// the shifted column, via mapa + ld.shared::cluster (local SMEM when the owner
+// is this CTA).  Only the back-pointer bytes reach HBM.
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ int32_t ld_cluster(uint32_t addr, int32_t) {
+  int32_t v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double ld_cluster(uint32_t addr, double) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+struct ClusterGeom {
+  int G;          // CTAs per instance
+  int B;          // columns owned per CTA
+  uint32_t magic; // owner(x) = umulhi(x, magic) == x / B for x < 2^32 / B
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, ClusterGeom geo) {
+  using V = typename VT<MODE>::T;
+  extern __shared__ __align__(16) unsigned char smem[];
+  StageShift* st_sh = reinterpret_cast<StageShift*>(smem);
+  V* st_r = reinterpret_cast<V*>(smem + kStageTile * sizeof(StageShift));
+  const size_t stage_bytes = align_up(kStageTile * (sizeof(StageShift) + sizeof(V)), 16);
+  V* rows = reinterpret_cast<V*>(smem + stage_bytes);  // [buf][C|S][B]
+
+  const int G = geo.G, B = geo.B;
+  const int q = (int)cluster_rank();
+  const DpWork wk = a.work[blockIdx.x / G];
+  const int64_t inst = wk.inst;
+  const int64_t lo = a.layer_off[inst];
+  const int L = (int)(a.layer_off[inst + 1] - lo);
+  const int ncol = (int)(a.info[inst].w_eff + 1);
+  const double g = a.info[inst].scale;
+  const bool sac = a.sac[inst] != 0;
+  const int T = blockDim.x, tid = threadIdx.x;
+  const int j0 = q * B;
+  const int jn = max(0, min(ncol, j0 + B) - j0);
+  const V NEG = VT<MODE>::neg();
+  const V ZERO = V(0);
+  const uint32_t rows_sa = smem_addr(rows);
+
+  for (int t = tid; t < jn; t += T) {
+    rows[t] = sac ? ZERO : NEG;      // buf 0, C
+    rows[B + t] = sac ? NEG : ZERO;  // buf 0, S
+  }
+  // predecessor value of row `rs` (0 = C, 1 = S) in buffer `buf` at global column x
+  auto fetch = [&](int x, int buf, int rs) -> V {
+    if (x < 0) return NEG;
+    const uint32_t owner = __umulhi((uint32_t)x, geo.magic);
+    const uint32_t off = (uint32_t)x - owner * (uint32_t)B;
+    const uint32_t local = rows_sa + (uint32_t)(((buf * 2 + rs) * B + (int)off) * (int)sizeof(V));
+    return ld_cluster(cluster_addr(local, owner), V());
+  };
+
+  uint8_t* bp_inst = a.bp + wk.bp_off;
+  cluster_barrier();
+  for (int k = 0; k < L; ++k) {
+    const int kt = k % kStageTile;
+    if (kt == 0) {
+      load_stage_tile<MODE>(a, lo, k, L, st_sh, st_r);
+      __syncthreads();
+    }
+    const StageShift sh = st_sh[kt];
+    const V rk = st_r[kt];
+    const int cur = k & 1;
+    V* Cn = rows + ((cur ^ 1) * 2 + 0) * B;
+    V* Sn = rows + ((cur ^ 1) * 2 + 1) * B;
+    uint8_t* bprow = bp_inst + (int64_t)k * ncol + j0;
+    constexpr int U = 4;
+    for (int t0 = tid; t0 < jn; t0 += U * T) {
+      V ca[U], cb[U], sa[U], sb[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * T;
+        const int j = j0 + (t < jn ? t : 0);
+        ca[u] = fetch(j - sh.i, cur, 0);
+        cb[u] = fetch(j - sh.id, cur, 1);
+        sa[u] = fetch(j - sh.s, cur, 1);
+        sb[u] = fetch(j - sh.su, cur, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * T;
+        if (t < jn) {
+          const int j = j0 + t;
+          V cn, sn;
+          uint32_t bits;
+          cell_update<MODE, V>(ca[u], cb[u], sa[u], sb[u], rk, j >= sh.i, j >= sh.id, j >= sh.s,
+                               j >= sh.su, cn, sn, bits);
+          Cn[t] = cn;
+          Sn[t] = sn;
+          bprow[t] = (uint8_t)bits;
+        }
+      }
+    }
+    cluster_barrier();
+  }
+  // the CTA owning column ncol-1 publishes the end cell (buffer L & 1)
+  if (tid == 0 && ncol - 1 >= j0 && ncol - 1 < j0 + B) {
+    const int t = ncol - 1 - j0, buf = L & 1;
+    a.info[inst].end_c = to_f64(rows[(buf * 2 + 0) * B + t], g);
+    a.info[inst].end_s = to_f64(rows[(buf * 2 + 1) * B + t], g);
+  }
+  cluster_barrier();  // keep every CTA's SMEM alive until remote reads are done
 }
 
 // ---------------------------------------------------------------------------
@@ -668,9 +821,49 @@ int launch_dp(const DpArgs& a, int64_t n_items, int threads, size_t smem, cudaSt
   return launch_check("dp_stage_kernel launch");
 }
 
-int launch_dp_group(int mode, bool smem_rows, const DpArgs& a, int64_t n_items, int threads,
-                    size_t smem, cudaStream_t st) {
+template <int MODE>
+int launch_cluster(const DpArgs& a, int64_t n_items, int threads, size_t smem, ClusterGeom geo,
+                   cudaStream_t st) {
+  auto kern = dp_cluster_kernel<MODE>;
+  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kSmemCap),
+                      "cudaFuncSetAttribute(dp_cluster_kernel)");
+  if (rc) return rc;
+  if (geo.G > 8) {
+    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                    "cudaFuncSetAttribute(non-portable cluster)");
+    if (rc) return rc;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_items * geo.G), 1, 1);
+  cfg.blockDim = dim3((unsigned)threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)geo.G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, a, geo), "dp_cluster_kernel launch");
+  if (rc) return rc;
+  return launch_check("dp_cluster_kernel launch");
+}
+
+enum DpVariant { DPV_SMEM = 0, DPV_CLUSTER = 1, DPV_GLOBAL = 2 };
+
+int launch_dp_group(int mode, int variant, const DpArgs& a, int64_t n_items, int threads,
+                    size_t smem, ClusterGeom geo, cudaStream_t st) {
   if (n_items == 0) return SP_OK;
+  if (variant == DPV_CLUSTER) {
+    switch (mode) {
+      case VM_INT32: return launch_cluster<VM_INT32>(a, n_items, threads, smem, geo, st);
+      case VM_F64: return launch_cluster<VM_F64>(a, n_items, threads, smem, geo, st);
+      default: return launch_cluster<VM_F64_NAN>(a, n_items, threads, smem, geo, st);
+    }
+  }
+  const bool smem_rows = variant == DPV_SMEM;
   switch (mode * 2 + (smem_rows ? 1 : 0)) {
     case VM_INT32 * 2 + 1: return launch_dp<VM_INT32, true>(a, n_items, threads, smem, st);
     case VM_INT32 * 2 + 0: return launch_dp<VM_INT32, false>(a, n_items, threads, smem, st);
@@ -679,6 +872,39 @@ int launch_dp_group(int mode, bool smem_rows, const DpArgs& a, int64_t n_items, 
     case VM_F64_NAN * 2 + 1: return launch_dp<VM_F64_NAN, true>(a, n_items, threads, smem, st);
     default: return launch_dp<VM_F64_NAN, false>(a, n_items, threads, smem, st);
   }
+}
+
+// cluster geometry for one instance, or G == 0 if the rows do not fit on chip
+ClusterGeom cluster_geom(int mode, int64_t ncol) {
+  ClusterGeom geo{0, 0, 0};
+  const size_t vb = mode == VM_INT32 ? 4 : 8;
+  const size_t room = kSmemCap - stage_bytes_mode(mode);
+  const size_t per_col = 4 * vb;  // 2 buffers x (C, S)
+  int G = (int)((ncol * per_col + room - 1) / room);
+  G = std::max(G, 2);
+  if (G > 16) return geo;
+  const int64_t B = (ncol + G - 1) / G;
+  if ((size_t)B * per_col > room) return geo;
+  const uint64_t magic = ((uint64_t)1 << 32) / (uint64_t)B + 1;
+  // umulhi(x, magic) must equal x / B on every column index
+  for (int64_t x = 0; x < ncol; x += std::max<int64_t>(1, B / 64)) {
+    if ((int64_t)((x * magic) >> 32) != x / B) return geo;
+  }
+  for (int64_t x = std::max<int64_t>(0, ncol - 4096); x < ncol; ++x)
+    if ((int64_t)((x * magic) >> 32) != x / B) return geo;
+  geo.G = G;
+  geo.B = (int)B;
+  geo.magic = (uint32_t)magic;
+  return geo;
+}
+
+int forced_variant() {
+  const char* v = getenv("SPLITPLAN_DP_VARIANT");
+  if (!v) return -1;
+  if (!strcmp(v, "smem")) return DPV_SMEM;
+  if (!strcmp(v, "cluster")) return DPV_CLUSTER;
+  if (!strcmp(v, "global")) return DPV_GLOBAL;
+  return -1;
 }
 
 // Shared driver of sp_plan_dp and sp_build_dp_tables.
@@ -719,10 +945,11 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   uint8_t* dyn = (uint8_t*)ws + fixed;
   struct Item {
     int64_t inst, L, ncol;
-    int mode;
-    bool smem;
+    int mode, variant;
+    ClusterGeom geo;
     size_t bp, rows;
   };
+  const int force = forced_variant();
   std::vector<Item> items;
   items.reserve(n);
   for (int64_t k = 0; k < n; ++k) {
@@ -738,9 +965,16 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     it.ncol = ncol;
     it.mode = hinfo[k].mode;
     const size_t rb = row_bytes_mode(it.mode, ncol);
-    it.smem = rb + stage_bytes_mode(it.mode) <= kSmemCap;
+    const bool fits_cta = rb + stage_bytes_mode(it.mode) <= kSmemCap;
+    it.geo = cluster_geom(it.mode, ncol);
+    if (force == DPV_GLOBAL || tab_c) it.variant = DPV_GLOBAL;
+    else if (force == DPV_CLUSTER && it.geo.G) it.variant = DPV_CLUSTER;
+    else if (fits_cta && force != DPV_CLUSTER) it.variant = DPV_SMEM;
+    else if (it.geo.G) it.variant = DPV_CLUSTER;
+    else it.variant = DPV_GLOBAL;
+    if (it.variant == DPV_SMEM && !fits_cta) it.variant = DPV_GLOBAL;
     it.bp = align_up((size_t)it.L * (size_t)ncol, 256);
-    it.rows = it.smem ? 0 : align_up(rb, 256);
+    it.rows = it.variant == DPV_GLOBAL ? align_up(rb, 256) : 0;
     items.push_back(it);
   }
 
@@ -776,41 +1010,59 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     // lay out the wave: back-pointers then global rows; group work items by kernel variant
     hwork.clear();
     size_t off = 0;
-    std::vector<DpWork> groups[6];
-    int gthreads[6] = {0, 0, 0, 0, 0, 0};
-    size_t gsmem[6] = {0, 0, 0, 0, 0, 0};
-    double gcells[6] = {0, 0, 0, 0, 0, 0};
+    struct Group {
+      int mode, variant, threads = 0;
+      ClusterGeom geo{0, 0, 0};
+      size_t smem = 0;
+      double cells = 0;
+      std::vector<DpWork> items;
+    };
+    std::vector<Group> groups;
     for (size_t q = pos; q < end; ++q) {
       const Item& it = items[q];
       DpWork w;
       w.inst = it.inst;
       w.bp_off = (int64_t)off;
       off += it.bp;
-      if (!it.smem) {
+      if (it.variant == DPV_GLOBAL) {
         w.row_off = (int64_t)off;
         off += it.rows;
       } else {
         w.row_off = -1;
       }
-      const int gi = it.mode * 2 + (it.smem ? 1 : 0);
-      groups[gi].push_back(w);
-      gcells[gi] += (double)it.L * (double)it.ncol;
-      gthreads[gi] = std::max(gthreads[gi], threads_for(it.ncol));
-      if (it.smem)
-        gsmem[gi] = std::max(gsmem[gi], stage_bytes_mode(it.mode) + row_bytes_mode(it.mode, it.ncol));
-      else
-        gsmem[gi] = stage_bytes_mode(it.mode);
+      Group* g = nullptr;
+      for (Group& c : groups)
+        if (c.mode == it.mode && c.variant == it.variant &&
+            (it.variant != DPV_CLUSTER || (c.geo.G == it.geo.G && c.geo.B == it.geo.B)))
+          g = &c;
+      if (!g) {
+        groups.push_back(Group{it.mode, it.variant});
+        g = &groups.back();
+        g->geo = it.geo;
+      }
+      g->items.push_back(w);
+      g->cells += (double)it.L * (double)it.ncol;
+      const size_t vb = it.mode == VM_INT32 ? 4 : 8;
+      if (it.variant == DPV_CLUSTER) {
+        const int t = (int)std::min<int64_t>(kMaxThreads, std::max<int64_t>(64, ((it.geo.B + 3) / 4 + 31) / 32 * 32));
+        g->threads = std::max(g->threads, t);
+        g->smem = stage_bytes_mode(it.mode) + 4 * vb * (size_t)it.geo.B;
+      } else {
+        g->threads = std::max(g->threads, threads_for(it.ncol));
+        const size_t need = stage_bytes_mode(it.mode) +
+                            (it.variant == DPV_SMEM ? row_bytes_mode(it.mode, it.ncol) : 0);
+        g->smem = std::max(g->smem, need);
+      }
     }
-    for (int gi = 0; gi < 6; ++gi)
-      for (const DpWork& w : groups[gi]) hwork.push_back(w);
+    for (const Group& g : groups)
+      for (const DpWork& w : g.items) hwork.push_back(w);
     rc = check_cuda(cudaMemcpyAsync(work, hwork.data(), sizeof(DpWork) * hwork.size(),
                                     cudaMemcpyHostToDevice, st),
                     "upload work list");
     if (rc) return rc;
     int64_t first = 0;
-    for (int gi = 0; gi < 6; ++gi) {
-      const int64_t cnt = (int64_t)groups[gi].size();
-      if (!cnt) continue;
+    for (const Group& g : groups) {
+      const int64_t cnt = (int64_t)g.items.size();
       DpArgs ga = a;
       ga.work = work + first;
       cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -819,15 +1071,16 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
       }
-      rc = launch_dp_group(gi / 2, gi % 2 == 1, ga, cnt, gthreads[gi], gsmem[gi], st);
+      rc = launch_dp_group(g.mode, g.variant, ga, cnt, g.threads, g.smem, g.geo, st);
       if (rc) return rc;
       if (profiling()) {
         cudaEventRecord(e1, st);
-        // algorithmic HBM bytes per cell: SMEM rows -> the back-pointer byte
-        // only; global rows -> read + write of both rows + the back-pointer
-        const double vb = (gi / 2 == VM_INT32) ? 4.0 : 8.0;
-        const double per_cell = (gi % 2 == 1) ? 1.0 : 4.0 * vb + 1.0;
-        prof_record_dp(e0, e1, gcells[gi], gcells[gi] * per_cell);
+        // algorithmic HBM bytes per cell: rows on chip (SMEM / cluster DSMEM)
+        // -> the back-pointer byte only; global rows -> read + write of both
+        // rows + the back-pointer
+        const double vb = g.mode == VM_INT32 ? 4.0 : 8.0;
+        const double per_cell = g.variant == DPV_GLOBAL ? 4.0 * vb + 1.0 : 1.0;
+        prof_record_dp(e0, e1, g.cells, g.cells * per_cell, g.variant);
       }
       first += cnt;
     }

@@ -160,6 +160,20 @@ def test_dp_vs_oracle_smem_and_global_rows(gpu, r_kind):
         assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{r_kind}[{k}]")
 
 
+@pytest.mark.parametrize("variant", ["global", "cluster", "smem"])
+@pytest.mark.parametrize("name", ["battery_wide", "battery_float", "battery_large_model"])
+def test_dp_kernel_variants_agree(gpu, variant, name, monkeypatch):
+    """Every K2 variant (rows in one CTA's SMEM, in cluster DSMEM, in global
+    memory) is bit-exact on the same instances (the host falls back where a
+    variant cannot hold a row)."""
+    if not (GOLDEN / f"{name}.npz").exists():
+        pytest.skip("battery not generated")
+    from paper_2410_10759_b200 import batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", variant)
+    bat = Battery(name)
+    _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
+
+
 @pytest.mark.parametrize("name", ["battery_large_model", "battery_large_chain"])
 def test_full_size_batteries(gpu, name):
     """W_eff = 1e5 model-derived instances (BASELINE cfg2 shape) and the
