@@ -14,6 +14,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "sp_internal.cuh"
@@ -393,17 +394,40 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, Cl
     rows[t] = sac ? ZERO : NEG;      // buf 0, C
     rows[B + t] = sac ? NEG : ZERO;  // buf 0, S
   }
-  // predecessor value of row `rs` (0 = C, 1 = S) in buffer `buf` at global column x
-  auto fetch = [&](int x, int buf, int rs) -> V {
-    if (x < 0) return NEG;
-    const uint32_t owner = __umulhi((uint32_t)x, geo.magic);
-    const uint32_t off = (uint32_t)x - owner * (uint32_t)B;
-    const uint32_t local = rows_sa + (uint32_t)(((buf * 2 + rs) * B + (int)off) * (int)sizeof(V));
-    return ld_cluster(cluster_addr(local, owner), V());
-  };
-
+  // shared::cluster address of `rows` in every rank.  The window is linear in
+  // the rank on sm_100 (base + r * stride); verify that once and keep a table
+  // in SMEM as the fallback, so the inner loop never issues mapa (ADU pipe).
+  __shared__ uint32_t rank_base[16];
+  __shared__ int linear_ok;
+  if (tid < G) rank_base[tid] = cluster_addr(rows_sa, (uint32_t)tid);
+  __syncthreads();
+  if (tid == 0) {
+    int ok = 1;
+    const uint32_t stride = G > 1 ? rank_base[1] - rank_base[0] : 0;
+    for (int r = 0; r < G; ++r) ok &= rank_base[r] == rank_base[0] + (uint32_t)r * stride;
+    linear_ok = ok;
+  }
+  __syncthreads();
+  const bool linear = linear_ok != 0;
+  const uint32_t base0 = rank_base[0];
+  // per-rank step in the linear formula, net of the B columns a rank covers
+  const uint32_t rank_step = (G > 1 ? rank_base[1] - rank_base[0] : 0) - (uint32_t)(B * sizeof(V));
   uint8_t* bp_inst = a.bp + wk.bp_off;
   cluster_barrier();
+  // the stage loop, instantiated once per addressing scheme (uniform branch)
+  auto stages = [&](auto lin_tag) {
+    constexpr bool LIN = decltype(lin_tag)::value;
+    // predecessor value of row `rs` (0 = C, 1 = S) in buffer `buf` at global column x
+    auto fetch = [&](int x0, int buf, int rs) -> V {
+      const int x = max(x0, 0);  // branch-free: load a valid cell, select NEG below
+      const uint32_t owner = __umulhi((uint32_t)x, geo.magic);
+      const uint32_t rel = (uint32_t)(((buf * 2 + rs) * B) * (int)sizeof(V)) + (uint32_t)x * sizeof(V);
+      uint32_t addr;
+      if (LIN) addr = base0 + owner * rank_step + rel;
+      else addr = rank_base[owner] + rel - owner * (uint32_t)(B * sizeof(V));
+      const V v = ld_cluster(addr, V());
+      return x0 >= 0 ? v : NEG;
+    };
   for (int k = 0; k < L; ++k) {
     const int kt = k % kStageTile;
     if (kt == 0) {
@@ -445,6 +469,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, Cl
     }
     cluster_barrier();
   }
+  };
+  if (linear) stages(std::true_type{});
+  else stages(std::false_type{});
   // the CTA owning column ncol-1 publishes the end cell (buffer L & 1)
   if (tid == 0 && ncol - 1 >= j0 && ncol - 1 < j0 + B) {
     const int t = ncol - 1 - j0, buf = L & 1;
@@ -825,8 +852,9 @@ template <int MODE>
 int launch_cluster(const DpArgs& a, int64_t n_items, int threads, size_t smem, ClusterGeom geo,
                    cudaStream_t st) {
   auto kern = dp_cluster_kernel<MODE>;
+  // the kernel also has a little static SMEM, so ask for exactly what it uses
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)kSmemCap),
+                                           (int)smem),
                       "cudaFuncSetAttribute(dp_cluster_kernel)");
   if (rc) return rc;
   if (geo.G > 8) {
@@ -878,7 +906,7 @@ int launch_dp_group(int mode, int variant, const DpArgs& a, int64_t n_items, int
 ClusterGeom cluster_geom(int mode, int64_t ncol) {
   ClusterGeom geo{0, 0, 0};
   const size_t vb = mode == VM_INT32 ? 4 : 8;
-  const size_t room = kSmemCap - stage_bytes_mode(mode);
+  const size_t room = kSmemCap - stage_bytes_mode(mode) - 1024;  // 1 KB for static SMEM
   const size_t per_col = 4 * vb;  // 2 buffers x (C, S)
   int G = (int)((ncol * per_col + room - 1) / room);
   G = std::max(G, 2);
