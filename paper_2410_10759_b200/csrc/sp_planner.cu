@@ -23,8 +23,9 @@ namespace sp {
 namespace {
 
 constexpr int kStageTile = 128;          // stage records staged in SMEM at a time
-constexpr int kCellsPerThread = 8;       // E: columns per thread per chunk
+constexpr int kCellsPerThread = 4;       // E: columns per thread per chunk
 constexpr int kMaxThreads = 1024;
+constexpr int kStageThreads = 512;     // single-CTA DP kernels: 2 CTAs per SM
 constexpr size_t kSmemCap = 227 * 1024;  // sm_100a max dynamic SMEM per CTA
 constexpr int64_t kMaxCols = (int64_t(1) << 31) - 64;
 
@@ -159,19 +160,35 @@ __global__ void prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts,
 }
 
 // ---------------------------------------------------------------------------
-// K2: DP stage kernel
+// K2: DP stage kernels
 //
-// One CTA owns one instance.  Rows C and S (length W_eff+1) live either in
-// SMEM (ROWS_SMEM) or in a global scratch slot, and are updated IN PLACE:
-// every stage walks the row in chunks of E*T columns from the top down.  A
-// chunk first computes all of its new cells into registers (reads only touch
-// columns <= its own, which no later chunk of this stage overwrites), then a
-// barrier, then the writes.  Each cell emits one back-pointer byte:
-//   bit0 C-stay  : j>=i    and C[k-1][j-i]   + r == C[k][j]   (planner.py:164)
-//   bit1 C-switch: j>=i+d  and S[k-1][j-i-d] + r == C[k][j]   (planner.py:166)
-//   bit2 S-stay  : j>=s    and S[k-1][j-s]       == S[k][j]   (planner.py:173)
-//   bit3 S-switch: j>=s+u  and C[k-1][j-s-u]     == S[k][j]   (planner.py:175)
-// which is exactly the predicate sequence _backtrace evaluates.
+// One instance = two budget-indexed rows C and S (W_eff + 1 columns) updated
+// once per layer k (planner.py:128-143):
+//   C_k[j] = r_k + max(C_{k-1}[j - i_k], S_{k-1}[j - i_k - d_k])
+//   S_k[j] =       max(S_{k-1}[j - s_k], C_{k-1}[j - s_k - u_k])
+// Three variants hold the rows in different places:
+//   * dp_stage_kernel<ROWS_SMEM=true>   one CTA, rows in its SMEM
+//   * dp_cluster_kernel                 a thread-block cluster, rows split
+//                                       across the CTAs' distributed SMEM
+//   * dp_stage_kernel<ROWS_SMEM=false>  one CTA, rows in global memory
+// Single-CTA variants update the rows IN PLACE, walking 32-aligned chunks of
+// CH = E*T columns from the top down: a chunk computes its new cells into
+// registers (its reads only touch columns <= its own, which no later chunk of
+// this stage writes), then a barrier, then the writes.  Each row carries CH
+// cells of NEG padding in front, and each chunk clamps the stage shifts to
+// its top (shift' = min(shift, chunk_top)), so every read is a plain in-bounds
+// load: shifted indices that were negative land in the padding and read NEG.
+//
+// Back-pointers are ballot-packed per warp: for each 32-column group one
+// 32-bit word per flag -- C-stay, S-stay, and in the NaN-propagating domain
+// also C-switch and S-switch.  The flags are exactly the predicates
+// _backtrace evaluates (planner.py:159-178):
+//   C-stay  : j>=i    and C[k-1][j-i]   + r == C[k][j]
+//   C-switch: j>=i+d  and S[k-1][j-i-d] + r == C[k][j]
+//   S-stay  : j>=s    and S[k-1][j-s]       == S[k][j]
+//   S-switch: j>=s+u  and C[k-1][j-s-u]     == S[k][j]
+// Outside the NaN domain a reachable cell that does not stay always switches
+// (its value came from the other predecessor), so two words suffice.
 
 struct DpArgs {
   const int64_t* layer_off;
@@ -186,36 +203,61 @@ struct DpArgs {
   double* tab_s;
 };
 
-// One DP cell: new C/S values and the back-pointer byte from the four
-// predecessor values (NEG where the shifted index is negative).
+__host__ __device__ inline int bp_words(int mode) { return mode == VM_F64_NAN ? 4 : 2; }
+
+struct CellFlags {
+  bool c_stay, s_stay, c_sw, s_sw;
+};
+
+// One DP cell from its four predecessor values (NEG where the shifted column
+// is negative).  v* tell whether each shifted column was >= 0; only the NaN
+// domain needs them (elsewhere NEG can never reproduce a reachable value).
 template <int MODE, typename V>
-__device__ __forceinline__ void cell_update(V ca, V cb, V sa, V sb, V rk, bool vi, bool vid,
-                                            bool vs, bool vsu, V& cn, V& sn, uint32_t& bits) {
+__device__ __forceinline__ CellFlags cell_update(V ca, V cb, V sa, V sb, V rk, bool vi, bool vid,
+                                                 bool vs, bool vsu, V& cn, V& sn) {
+  CellFlags f;
   if (MODE == VM_INT32) {
     // exact integer arithmetic: C-stay <=> ca >= cb, S-stay <=> sa >= sb
-    const bool c_stay = ca >= cb;
-    const bool s_stay = sa >= sb;
-    cn = (c_stay ? ca : cb) + rk;
-    sn = s_stay ? sa : sb;
-    bits = (c_stay ? 1u : 2u) | (s_stay ? 4u : 8u);
+    f.c_stay = ca >= cb;
+    f.s_stay = sa >= sb;
+    cn = (f.c_stay ? ca : cb) + rk;
+    sn = f.s_stay ? sa : sb;
+    f.c_sw = !f.c_stay;
+    f.s_sw = !f.s_stay;
+  } else if (MODE == VM_F64) {
+    const V cm = ca >= cb ? ca : cb;
+    sn = sa >= sb ? sa : sb;
+    cn = dadd(cm, rk);
+    f.c_stay = dadd(ca, rk) == cn;  // fl(a + r) == C[k][j], not a >= b
+    f.s_stay = sa == sn;
+    f.c_sw = !f.c_stay;
+    f.s_sw = !f.s_stay;
+  } else {  // np.maximum propagates NaN
+    const V cm = (ca != ca) ? ca : ((cb != cb) ? cb : (ca >= cb ? ca : cb));
+    sn = (sa != sa) ? sa : ((sb != sb) ? sb : (sa >= sb ? sa : sb));
+    cn = dadd(cm, rk);
+    f.c_stay = vi && dadd(ca, rk) == cn;
+    f.c_sw = vid && dadd(cb, rk) == cn;
+    f.s_stay = vs && sa == sn;
+    f.s_sw = vsu && sb == sn;
+  }
+  return f;
+}
+
+// warp-collective: pack the 32 lanes' flags of one column group into words
+template <int MODE>
+__device__ __forceinline__ void emit_bp(uint32_t* row_words, int group, int ngroups, CellFlags f,
+                                        bool active) {
+  const uint32_t m0 = __ballot_sync(0xffffffffu, active && f.c_stay);
+  const uint32_t m1 = __ballot_sync(0xffffffffu, active && f.s_stay);
+  if (MODE == VM_F64_NAN) {
+    const uint32_t m2 = __ballot_sync(0xffffffffu, active && f.c_sw);
+    const uint32_t m3 = __ballot_sync(0xffffffffu, active && f.s_sw);
+    if ((threadIdx.x & 31) == 0 && group < ngroups)
+      reinterpret_cast<uint4*>(row_words)[group] = make_uint4(m0, m1, m2, m3);
   } else {
-    V cm, sm;
-    if (MODE == VM_F64_NAN) {  // np.maximum propagates NaN
-      cm = (ca != ca) ? ca : ((cb != cb) ? cb : (ca >= cb ? ca : cb));
-      sm = (sa != sa) ? sa : ((sb != sb) ? sb : (sa >= sb ? sa : sb));
-    } else {
-      cm = ca >= cb ? ca : cb;
-      sm = sa >= sb ? sa : sb;
-    }
-    const V c = dadd(cm, rk);
-    cn = c;
-    sn = sm;
-    uint32_t b = 0;
-    if (vi && dadd(ca, rk) == c) b |= 1u;
-    if (vid && dadd(cb, rk) == c) b |= 2u;
-    if (vs && sa == sm) b |= 4u;
-    if (vsu && sb == sm) b |= 8u;
-    bits = b;
+    if ((threadIdx.x & 31) == 0 && group < ngroups)
+      reinterpret_cast<uint2*>(row_words)[group] = make_uint2(m0, m1);
   }
 }
 
@@ -233,7 +275,7 @@ __device__ __forceinline__ void load_stage_tile(const DpArgs& a, int64_t lo, int
 }
 
 template <int MODE, bool ROWS_SMEM, int E>
-__global__ void __launch_bounds__(kMaxThreads, 1) dp_stage_kernel(DpArgs a) {
+__global__ void __launch_bounds__(kStageThreads, 2) dp_stage_kernel(DpArgs a) {
   using V = typename VT<MODE>::T;
   extern __shared__ __align__(16) unsigned char smem[];
   StageShift* st_sh = reinterpret_cast<StageShift*>(smem);
@@ -247,26 +289,30 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_stage_kernel(DpArgs a) {
   const int ncol = (int)(a.info[inst].w_eff + 1);
   const double g = a.info[inst].scale;
   const bool sac = a.sac[inst] != 0;
-  const int T = blockDim.x, tid = threadIdx.x;
-  const int CH = E * T;
+  const int T = blockDim.x, tid = threadIdx.x, warp = tid >> 5;
+  const int CH = E * T;  // chunk width == NEG padding in front of each row
+  const int nch = (ncol + CH - 1) / CH;
+  const int span = CH + ncol;
+  const int ngroups = (ncol + 31) >> 5;
+  const int64_t row_words = (int64_t)ngroups * bp_words(MODE);
 
-  V* Crow;
-  if (ROWS_SMEM) Crow = reinterpret_cast<V*>(smem + stage_bytes);
-  else Crow = reinterpret_cast<V*>(a.rows + wk.row_off);
-  V* Srow = Crow + ncol;
+  V* base = ROWS_SMEM ? reinterpret_cast<V*>(smem + stage_bytes)
+                      : reinterpret_cast<V*>(a.rows + wk.row_off);
+  V* Cp = base + CH;         // C row, column 0
+  V* Sp = base + span + CH;  // S row, column 0
   const V NEG = VT<MODE>::neg();
   const V ZERO = V(0);
 
-  for (int j = tid; j < ncol; j += T) {
-    Crow[j] = sac ? ZERO : NEG;
-    Srow[j] = sac ? NEG : ZERO;
-    if (a.tab_c) {
-      a.tab_c[j] = sac ? 0.0 : -INFINITY;
-      a.tab_s[j] = sac ? -INFINITY : 0.0;
+  for (int x = tid - CH; x < ncol; x += T) {
+    Cp[x] = (x >= 0 && sac) ? ZERO : NEG;
+    Sp[x] = (x >= 0 && !sac) ? ZERO : NEG;
+    if (a.tab_c && x >= 0) {
+      a.tab_c[x] = sac ? 0.0 : -INFINITY;
+      a.tab_s[x] = sac ? -INFINITY : 0.0;
     }
   }
 
-  uint8_t* bp_inst = a.bp + wk.bp_off;
+  uint32_t* bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off);
   for (int k = 0; k < L; ++k) {
     const int kt = k % kStageTile;
     if (kt == 0) {
@@ -276,36 +322,32 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_stage_kernel(DpArgs a) {
     __syncthreads();
     const StageShift sh = st_sh[kt];
     const V rk = st_r[kt];
-    uint8_t* bprow = bp_inst + (int64_t)k * ncol;
+    uint32_t* bprow = bpw + (int64_t)k * row_words;
 
-    for (int top = ncol; top > 0; top -= CH) {
-      const int base = top - CH;
+    for (int c = nch - 1; c >= 0; --c) {
+      const int c0 = c * CH, ctop = c0 + CH;
+      // chunk-uniform clamped shifts: every read stays in [-CH, ncol)
+      const V* pca = Cp - min(sh.i, ctop);
+      const V* pcb = Sp - min(sh.id, ctop);
+      const V* psa = Sp - min(sh.s, ctop);
+      const V* psb = Cp - min(sh.su, ctop);
       V cn[E], sn[E];
-      uint32_t bits[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const int j = base + e * T + tid;
-        cn[e] = NEG;
-        sn[e] = NEG;
-        bits[e] = 0;
-        if (j >= 0) {
-          const int ji = j - sh.i, jid = j - sh.id, js = j - sh.s, jsu = j - sh.su;
-          const V ca = ji >= 0 ? Crow[ji] : NEG;
-          const V cb = jid >= 0 ? Srow[jid] : NEG;
-          const V sa = js >= 0 ? Srow[js] : NEG;
-          const V sb = jsu >= 0 ? Crow[jsu] : NEG;
-          cell_update<MODE, V>(ca, cb, sa, sb, rk, ji >= 0, jid >= 0, js >= 0, jsu >= 0, cn[e],
-                               sn[e], bits[e]);
-        }
+        const int j = c0 + e * T + tid;
+        const bool active = j < ncol;
+        const int jr = active ? j : ncol - 1;
+        const CellFlags f = cell_update<MODE, V>(pca[jr], pcb[jr], psa[jr], psb[jr], rk, j >= sh.i,
+                                                 j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
+        emit_bp<MODE>(bprow, (c0 + e * T) / 32 + warp, ngroups, f, active);
       }
       __syncthreads();
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const int j = base + e * T + tid;
-        if (j >= 0) {
-          Crow[j] = cn[e];
-          Srow[j] = sn[e];
-          bprow[j] = (uint8_t)bits[e];
+        const int j = c0 + e * T + tid;
+        if (j < ncol) {
+          Cp[j] = cn[e];
+          Sp[j] = sn[e];
           if (a.tab_c) {
             a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn[e], g);
             a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn[e], g);
@@ -316,20 +358,20 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_stage_kernel(DpArgs a) {
   }
   __syncthreads();
   if (tid == 0) {
-    a.info[inst].end_c = to_f64(Crow[ncol - 1], g);
-    a.info[inst].end_s = to_f64(Srow[ncol - 1], g);
+    a.info[inst].end_c = to_f64(Cp[ncol - 1], g);
+    a.info[inst].end_s = to_f64(Sp[ncol - 1], g);
   }
 }
 
 // ---------------------------------------------------------------------------
 // K2 cluster variant: rows too long for one SM live in the distributed shared
 // memory of a thread-block cluster of G CTAs (G <= 16).  CTA q owns columns
-// [q*B, (q+1)*B) of both rows, double-buffered (stage k reads buffer k&1 and
-// writes buffer (k&1)^1), so one cluster barrier per stage orders everything:
-// it releases this stage's writes and guarantees no CTA still reads the buffer
-// the next stage overwrites.  Predecessor values come from whichever CTA owns
-// the shifted column, via mapa + ld.shared::cluster (local SMEM when the owner
-// is this CTA).  Only the back-pointer bytes reach HBM.
+// [q*B, (q+1)*B) of both rows (B a multiple of 32), double-buffered (stage k
+// reads buffer k&1 and writes buffer (k&1)^1), so one cluster barrier per
+// stage orders everything: it releases this stage's writes and guarantees no
+// CTA still reads the buffer the next stage overwrites.  Predecessor values
+// come from whichever CTA owns the shifted column via ld.shared::cluster.
+// Only the packed back-pointer words reach HBM.
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -361,8 +403,8 @@ __device__ __forceinline__ void cluster_barrier() {
 
 struct ClusterGeom {
   int G;          // CTAs per instance
-  int B;          // columns owned per CTA
-  uint32_t magic; // owner(x) = umulhi(x, magic) == x / B for x < 2^32 / B
+  int B;          // columns owned per CTA (multiple of 32)
+  uint32_t magic; // owner(x) = umulhi(x, magic) == x / B for x < G * B
 };
 
 template <int MODE>
@@ -383,9 +425,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, Cl
   const int ncol = (int)(a.info[inst].w_eff + 1);
   const double g = a.info[inst].scale;
   const bool sac = a.sac[inst] != 0;
-  const int T = blockDim.x, tid = threadIdx.x;
+  const int T = blockDim.x, tid = threadIdx.x, warp = tid >> 5;
   const int j0 = q * B;
   const int jn = max(0, min(ncol, j0 + B) - j0);
+  const int ngroups = (ncol + 31) >> 5;
+  const int64_t row_words = (int64_t)ngroups * bp_words(MODE);
   const V NEG = VT<MODE>::neg();
   const V ZERO = V(0);
   const uint32_t rows_sa = smem_addr(rows);
@@ -412,63 +456,65 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, Cl
   const uint32_t base0 = rank_base[0];
   // per-rank step in the linear formula, net of the B columns a rank covers
   const uint32_t rank_step = (G > 1 ? rank_base[1] - rank_base[0] : 0) - (uint32_t)(B * sizeof(V));
-  uint8_t* bp_inst = a.bp + wk.bp_off;
+  uint32_t* bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off);
   cluster_barrier();
   // the stage loop, instantiated once per addressing scheme (uniform branch)
   auto stages = [&](auto lin_tag) {
     constexpr bool LIN = decltype(lin_tag)::value;
     // predecessor value of row `rs` (0 = C, 1 = S) in buffer `buf` at global column x
-    auto fetch = [&](int x0, int buf, int rs) -> V {
+    auto fetch = [&](int x0, uint32_t rowoff) -> V {
       const int x = max(x0, 0);  // branch-free: load a valid cell, select NEG below
       const uint32_t owner = __umulhi((uint32_t)x, geo.magic);
-      const uint32_t rel = (uint32_t)(((buf * 2 + rs) * B) * (int)sizeof(V)) + (uint32_t)x * sizeof(V);
+      const uint32_t rel = rowoff + (uint32_t)x * sizeof(V);
       uint32_t addr;
       if (LIN) addr = base0 + owner * rank_step + rel;
       else addr = rank_base[owner] + rel - owner * (uint32_t)(B * sizeof(V));
       const V v = ld_cluster(addr, V());
       return x0 >= 0 ? v : NEG;
     };
-  for (int k = 0; k < L; ++k) {
-    const int kt = k % kStageTile;
-    if (kt == 0) {
-      load_stage_tile<MODE>(a, lo, k, L, st_sh, st_r);
-      __syncthreads();
-    }
-    const StageShift sh = st_sh[kt];
-    const V rk = st_r[kt];
-    const int cur = k & 1;
-    V* Cn = rows + ((cur ^ 1) * 2 + 0) * B;
-    V* Sn = rows + ((cur ^ 1) * 2 + 1) * B;
-    uint8_t* bprow = bp_inst + (int64_t)k * ncol + j0;
-    constexpr int U = 4;
-    for (int t0 = tid; t0 < jn; t0 += U * T) {
-      V ca[U], cb[U], sa[U], sb[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + u * T;
-        const int j = j0 + (t < jn ? t : 0);
-        ca[u] = fetch(j - sh.i, cur, 0);
-        cb[u] = fetch(j - sh.id, cur, 1);
-        sa[u] = fetch(j - sh.s, cur, 1);
-        sb[u] = fetch(j - sh.su, cur, 0);
+    for (int k = 0; k < L; ++k) {
+      const int kt = k % kStageTile;
+      if (kt == 0) {
+        load_stage_tile<MODE>(a, lo, k, L, st_sh, st_r);
+        __syncthreads();
       }
+      const StageShift sh = st_sh[kt];
+      const V rk = st_r[kt];
+      const int cur = k & 1;
+      const uint32_t offC = (uint32_t)((cur * 2 + 0) * B * (int)sizeof(V));
+      const uint32_t offS = (uint32_t)((cur * 2 + 1) * B * (int)sizeof(V));
+      V* Cn = rows + ((cur ^ 1) * 2 + 0) * B;
+      V* Sn = rows + ((cur ^ 1) * 2 + 1) * B;
+      uint32_t* bprow = bpw + (int64_t)k * row_words;
+      constexpr int U = 4;
+      for (int t0 = 0; t0 < jn; t0 += U * T) {  // warp-uniform trip count
+        V ca[U], cb[U], sa[U], sb[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + u * T;
-        if (t < jn) {
+        for (int u = 0; u < U; ++u) {
+          const int t = t0 + u * T + tid;
+          const int j = j0 + (t < jn ? t : 0);
+          ca[u] = fetch(j - sh.i, offC);
+          cb[u] = fetch(j - sh.id, offS);
+          sa[u] = fetch(j - sh.s, offS);
+          sb[u] = fetch(j - sh.su, offC);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int t = t0 + u * T + tid;
+          const bool active = t < jn;
           const int j = j0 + t;
           V cn, sn;
-          uint32_t bits;
-          cell_update<MODE, V>(ca[u], cb[u], sa[u], sb[u], rk, j >= sh.i, j >= sh.id, j >= sh.s,
-                               j >= sh.su, cn, sn, bits);
-          Cn[t] = cn;
-          Sn[t] = sn;
-          bprow[t] = (uint8_t)bits;
+          const CellFlags f = cell_update<MODE, V>(ca[u], cb[u], sa[u], sb[u], rk, j >= sh.i,
+                                                   j >= sh.id, j >= sh.s, j >= sh.su, cn, sn);
+          emit_bp<MODE>(bprow, (j0 + t0 + u * T) / 32 + warp, ngroups, f, active);
+          if (active) {
+            Cn[t] = cn;
+            Sn[t] = sn;
+          }
         }
       }
+      cluster_barrier();
     }
-    cluster_barrier();
-  }
   };
   if (linear) stages(std::true_type{});
   else stages(std::false_type{});
@@ -560,9 +606,18 @@ __global__ void backtrack_kernel(sp_instances in, const InstInfo* info, const St
   }
   bool client = ec >= es;
   int64_t j = inf.w_eff;
-  const uint8_t* bpi = bp + wk.bp_off;
+  // packed back-pointer words: per row, per 32-column group, nw words
+  // (C-stay, S-stay[, C-switch, S-switch]); see the K2 comment
+  const uint32_t* bpi = reinterpret_cast<const uint32_t*>(bp + wk.bp_off);
+  const int nw = bp_words(inf.mode);
+  const int64_t row_words = ((ncol + 31) >> 5) * nw;
   for (int k = L; k >= 1; --k) {
-    const uint8_t b = bpi[(int64_t)(k - 1) * ncol + j];
+    const uint32_t* grp = bpi + (int64_t)(k - 1) * row_words + (j >> 5) * nw;
+    const uint32_t bit = 1u << (j & 31);
+    const bool c_stay = grp[0] & bit, s_stay = grp[1] & bit;
+    const bool c_sw = nw == 4 ? (grp[2] & bit) != 0 : !c_stay;
+    const bool s_sw = nw == 4 ? (grp[3] & bit) != 0 : !s_stay;
+    const uint32_t b = (c_stay ? 1u : 0u) | (c_sw ? 2u : 0u) | (s_stay ? 4u : 0u) | (s_sw ? 8u : 0u);
     const StageShift sh = shifts[lo + k - 1];
     if (client) {
       pi[k - 1] = 1;
@@ -817,20 +872,25 @@ struct Carve {
   }
 };
 
+// threads of a single-CTA DP kernel: one chunk if the row is short, else the
+// full kStageThreads
 int threads_for(int64_t ncol) {
-  const int64_t per = (int64_t)kCellsPerThread;
-  const int64_t nch = std::max<int64_t>(1, (ncol + per * kMaxThreads - 1) / (per * kMaxThreads));
-  int64_t t = (ncol + per * nch - 1) / (per * nch);
+  int64_t t = (ncol + kCellsPerThread - 1) / kCellsPerThread;
   t = (t + 31) / 32 * 32;
-  return (int)std::min<int64_t>(kMaxThreads, std::max<int64_t>(64, t));
+  return (int)std::min<int64_t>(kStageThreads, std::max<int64_t>(32, t));
 }
 
-template <int MODE>
-size_t row_bytes(int64_t ncol) {
-  return 2 * (size_t)ncol * sizeof(typename VT<MODE>::T);
-}
+size_t value_bytes(int mode) { return mode == VM_INT32 ? 4 : 8; }
+
+// both rows of a single-CTA kernel, each with CH = E*T cells of NEG padding
 size_t row_bytes_mode(int mode, int64_t ncol) {
-  return mode == VM_INT32 ? row_bytes<VM_INT32>(ncol) : row_bytes<VM_F64>(ncol);
+  const int64_t pad = (int64_t)kCellsPerThread * threads_for(ncol);
+  return 2 * (size_t)(pad + ncol) * value_bytes(mode);
+}
+
+// packed back-pointer bytes of one instance (K2 comment)
+size_t bp_bytes(int mode, int64_t L, int64_t ncol) {
+  return (size_t)L * (size_t)((ncol + 31) / 32) * (size_t)bp_words(mode) * 4;
 }
 size_t stage_bytes_mode(int mode) {
   const size_t v = mode == VM_INT32 ? 4 : 8;
@@ -911,15 +971,13 @@ ClusterGeom cluster_geom(int mode, int64_t ncol) {
   int G = (int)((ncol * per_col + room - 1) / room);
   G = std::max(G, 2);
   if (G > 16) return geo;
-  const int64_t B = (ncol + G - 1) / G;
+  // B: a multiple of 32 so every warp's columns form one packed back-pointer group
+  const int64_t B = ((ncol + G - 1) / G + 31) / 32 * 32;
   if ((size_t)B * per_col > room) return geo;
   const uint64_t magic = ((uint64_t)1 << 32) / (uint64_t)B + 1;
-  // umulhi(x, magic) must equal x / B on every column index
-  for (int64_t x = 0; x < ncol; x += std::max<int64_t>(1, B / 64)) {
-    if ((int64_t)((x * magic) >> 32) != x / B) return geo;
-  }
-  for (int64_t x = std::max<int64_t>(0, ncol - 4096); x < ncol; ++x)
-    if ((int64_t)((x * magic) >> 32) != x / B) return geo;
+  // umulhi(x, magic) == x / B for all x < N whenever N * B < 2^32
+  // (magic * B - 2^32 <= B, so the error term x * that / 2^32 stays below 1/B)
+  if ((uint64_t)G * (uint64_t)B * (uint64_t)B >= ((uint64_t)1 << 32)) return geo;
   geo.G = G;
   geo.B = (int)B;
   geo.magic = (uint32_t)magic;
@@ -980,6 +1038,9 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   const int force = forced_variant();
   std::vector<Item> items;
   items.reserve(n);
+  ClusterGeom geo_cache{0, 0, 0};
+  int geo_mode = -1;
+  int64_t geo_ncol = -1;
   for (int64_t k = 0; k < n; ++k) {
     const int64_t ncol = hinfo[k].w_eff + 1;
     if (ncol > kMaxCols) {
@@ -994,14 +1055,19 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     it.mode = hinfo[k].mode;
     const size_t rb = row_bytes_mode(it.mode, ncol);
     const bool fits_cta = rb + stage_bytes_mode(it.mode) <= kSmemCap;
-    it.geo = cluster_geom(it.mode, ncol);
+    if (it.mode != geo_mode || ncol != geo_ncol) {
+      geo_cache = cluster_geom(it.mode, ncol);
+      geo_mode = it.mode;
+      geo_ncol = ncol;
+    }
+    it.geo = geo_cache;
     if (force == DPV_GLOBAL || tab_c) it.variant = DPV_GLOBAL;
     else if (force == DPV_CLUSTER && it.geo.G) it.variant = DPV_CLUSTER;
     else if (fits_cta && force != DPV_CLUSTER) it.variant = DPV_SMEM;
     else if (it.geo.G) it.variant = DPV_CLUSTER;
     else it.variant = DPV_GLOBAL;
     if (it.variant == DPV_SMEM && !fits_cta) it.variant = DPV_GLOBAL;
-    it.bp = align_up((size_t)it.L * (size_t)ncol, 256);
+    it.bp = align_up(bp_bytes(it.mode, it.L, ncol), 256);
     it.rows = it.variant == DPV_GLOBAL ? align_up(rb, 256) : 0;
     items.push_back(it);
   }
@@ -1059,14 +1125,19 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         w.row_off = -1;
       }
       Group* g = nullptr;
+      // single-CTA kernels size their row padding by blockDim, so a group
+      // shares one thread count; cluster groups share one geometry
+      const int want_t = it.variant == DPV_CLUSTER ? 0 : threads_for(it.ncol);
       for (Group& c : groups)
         if (c.mode == it.mode && c.variant == it.variant &&
-            (it.variant != DPV_CLUSTER || (c.geo.G == it.geo.G && c.geo.B == it.geo.B)))
+            (it.variant == DPV_CLUSTER ? (c.geo.G == it.geo.G && c.geo.B == it.geo.B)
+                                       : c.threads == want_t))
           g = &c;
       if (!g) {
         groups.push_back(Group{it.mode, it.variant});
         g = &groups.back();
         g->geo = it.geo;
+        g->threads = want_t;
       }
       g->items.push_back(w);
       g->cells += (double)it.L * (double)it.ncol;
@@ -1076,7 +1147,6 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         g->threads = std::max(g->threads, t);
         g->smem = stage_bytes_mode(it.mode) + 4 * vb * (size_t)it.geo.B;
       } else {
-        g->threads = std::max(g->threads, threads_for(it.ncol));
         const size_t need = stage_bytes_mode(it.mode) +
                             (it.variant == DPV_SMEM ? row_bytes_mode(it.mode, it.ncol) : 0);
         g->smem = std::max(g->smem, need);
@@ -1104,10 +1174,11 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       if (profiling()) {
         cudaEventRecord(e1, st);
         // algorithmic HBM bytes per cell: rows on chip (SMEM / cluster DSMEM)
-        // -> the back-pointer byte only; global rows -> read + write of both
-        // rows + the back-pointer
+        // -> the packed back-pointer bits only; global rows -> read + write of
+        // both rows plus those bits
         const double vb = g.mode == VM_INT32 ? 4.0 : 8.0;
-        const double per_cell = g.variant == DPV_GLOBAL ? 4.0 * vb + 1.0 : 1.0;
+        const double bits = bp_words(g.mode) * 4.0 / 32.0;
+        const double per_cell = g.variant == DPV_GLOBAL ? 4.0 * vb + bits : bits;
         prof_record_dp(e0, e1, g.cells, g.cells * per_cell, g.variant);
       }
       first += cnt;
