@@ -429,6 +429,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, Cl
   const int j0 = q * B;
   const int jn = max(0, min(ncol, j0 + B) - j0);
   const int ngroups = (ncol + 31) >> 5;
+  const int group_end = (j0 + jn + 31) >> 5;  // this CTA's back-pointer groups end here
   const int64_t row_words = (int64_t)ngroups * bp_words(MODE);
   const V NEG = VT<MODE>::neg();
   const V ZERO = V(0);
@@ -437,6 +438,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, Cl
   for (int t = tid; t < jn; t += T) {
     rows[t] = sac ? ZERO : NEG;      // buf 0, C
     rows[B + t] = sac ? NEG : ZERO;  // buf 0, S
+    if (a.tab_c) {
+      a.tab_c[j0 + t] = sac ? 0.0 : -INFINITY;
+      a.tab_s[j0 + t] = sac ? -INFINITY : 0.0;
+    }
   }
   // shared::cluster address of `rows` in every rank.  The window is linear in
   // the rank on sm_100 (base + r * stride); verify that once and keep a table
@@ -506,10 +511,15 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, Cl
           V cn, sn;
           const CellFlags f = cell_update<MODE, V>(ca[u], cb[u], sa[u], sb[u], rk, j >= sh.i,
                                                    j >= sh.id, j >= sh.s, j >= sh.su, cn, sn);
-          emit_bp<MODE>(bprow, (j0 + t0 + u * T) / 32 + warp, ngroups, f, active);
+          // groups past this CTA's columns belong to the next rank: never store them
+          emit_bp<MODE>(bprow, (j0 + t0 + u * T) / 32 + warp, group_end, f, active);
           if (active) {
             Cn[t] = cn;
             Sn[t] = sn;
+            if (a.tab_c) {
+              a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn, g);
+              a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn, g);
+            }
           }
         }
       }
@@ -1061,7 +1071,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       geo_ncol = ncol;
     }
     it.geo = geo_cache;
-    if (force == DPV_GLOBAL || tab_c) it.variant = DPV_GLOBAL;
+    if (force == DPV_GLOBAL || (tab_c && force < 0)) it.variant = DPV_GLOBAL;
     else if (force == DPV_CLUSTER && it.geo.G) it.variant = DPV_CLUSTER;
     else if (fits_cta && force != DPV_CLUSTER) it.variant = DPV_SMEM;
     else if (it.geo.G) it.variant = DPV_CLUSTER;

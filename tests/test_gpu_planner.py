@@ -87,6 +87,26 @@ def test_dp_tables_match_reference(gpu):
         pos += cnt
 
 
+@pytest.mark.parametrize("variant", ["global", "cluster", "smem"])
+def test_dp_tables_every_variant(gpu, variant, monkeypatch):
+    """Full tables from each K2 variant equal the reference's build_dp_tables."""
+    from paper_2410_10759_b200 import planner as P
+    from paper_2410_10759_b200.problem import PlanProblem
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", variant)
+    z = load_npz("dp_tables")
+    off, pos = z["off"], 0
+    for k in range(len(off) - 1):
+        a, b = off[k], off[k + 1]
+        prob = PlanProblem.from_costs(z["i"][a:b], z["s"][a:b], z["u"][a:b], z["d"][a:b],
+                                      z["r"][a:b], int(z["budget"][k]),
+                                      source_at_client=bool(z["sac"][k]))
+        t = P.build_dp_tables(prob)
+        cnt = t.client.size
+        np.testing.assert_array_equal(t.client.ravel(), z["C"][pos:pos + cnt], err_msg=f"C {k}")
+        np.testing.assert_array_equal(t.server.ravel(), z["S"][pos:pos + cnt], err_msg=f"S {k}")
+        pos += cnt
+
+
 def test_dropin_fixtures(gpu):
     """The reference's own frozen fixtures (tests/test_planner.py:26-108)."""
     from paper_2410_10759_b200.planner import plan_dp, plan_greedy, plan_oracle, plan_trivial, run_planner
