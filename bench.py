@@ -309,8 +309,8 @@ def main():
                 "seq_len": "U{128..2048}", "links_bps": "log-U[3e7,1e9] sym, 10 ms prop",
                 "deadline": "f x all-client time, f~U(0.05,1); unit = deadline/1e5",
                 "step": "K1 cost table + prep + K2 DP stage + K3 backtrack",
-                "l2": "inputs larger than L2: each step writes ~%.0f GB of back-pointers"
-                      % (cells / 1e9),
+                "l2": "inputs larger than L2: each step writes ~%.1f GB of packed back-pointers"
+                      % (cells / 4 / 1e9),
                 "parallelism": f"request-sharded dp{world}",
             },
             "scenarios_per_s": n * world / (step_ms / 1e3),
@@ -320,7 +320,7 @@ def main():
             "gpu_launches": int(all_l.value),
             "roofline": {
                 "kernel": ["dp_stage_kernel<smem rows>", "dp_cluster_kernel<DSMEM rows>",
-                           "dp_stage_kernel<global rows>"][dk_var.value],
+                           "dp_stage_kernel<global rows>", "dp_coop_kernel<L2 rows>"][dk_var.value],
                 "bound": "hbm",
                 "achieved": achieved,
                 "peak": peak,
@@ -346,7 +346,7 @@ def main():
 
 def cpu_baseline(req_np: dict, sample: int) -> dict:
     procs = max(1, min(os.cpu_count() or 1, 64))
-    sample = sample or max(16, 2 * procs)
+    sample = sample or max(64, 6 * procs)  # ~0.15 s of numpy per request: ~10-30 s CPU
     idx = np.arange(min(sample, len(req_np["seq_len"])))
     cells, dt = cpu_run(req_np, idx, procs)
     return {"value": cells / dt, "unit": "DP cells/s", "cores": procs, "kind": "port",

@@ -26,6 +26,7 @@ constexpr int kStageTile = 128;          // stage records staged in SMEM at a ti
 constexpr int kCellsPerThread = 4;       // E: columns per thread per chunk
 constexpr int kMaxThreads = 1024;
 constexpr int kStageThreads = 512;     // single-CTA DP kernels: 2 CTAs per SM
+constexpr int64_t kCoopMinCols = 0;      // rows longer than one SMEM go cooperative
 constexpr size_t kSmemCap = 227 * 1024;  // sm_100a max dynamic SMEM per CTA
 constexpr int64_t kMaxCols = (int64_t(1) << 31) - 64;
 
@@ -538,6 +539,118 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, Cl
 }
 
 // ---------------------------------------------------------------------------
+// K2 cooperative variant: a cluster of G CTAs shares one instance whose rows
+// live in global memory, double-buffered and sized so the rows of all
+// co-resident instances stay in L2.  CTA q computes the columns
+// [q*B, (q+1)*B) of the next buffer from any column of the current one; one
+// cluster barrier (release/acquire, which also invalidates L1) per stage.
+// Rows carry CH cells of NEG padding in front, and shifts are clamped per
+// chunk exactly as in dp_stage_kernel, so reads need no bounds checks.
+
+template <int MODE, int E>
+__global__ void __launch_bounds__(kStageThreads, 2) dp_coop_kernel(DpArgs a, ClusterGeom geo) {
+  using V = typename VT<MODE>::T;
+  extern __shared__ __align__(16) unsigned char smem[];
+  StageShift* st_sh = reinterpret_cast<StageShift*>(smem);
+  V* st_r = reinterpret_cast<V*>(smem + kStageTile * sizeof(StageShift));
+
+  const int G = geo.G, B = geo.B;
+  const int q = (int)cluster_rank();
+  const DpWork wk = a.work[blockIdx.x / G];
+  const int64_t inst = wk.inst;
+  const int64_t lo = a.layer_off[inst];
+  const int L = (int)(a.layer_off[inst + 1] - lo);
+  const int ncol = (int)(a.info[inst].w_eff + 1);
+  const double g = a.info[inst].scale;
+  const bool sac = a.sac[inst] != 0;
+  const int T = blockDim.x, tid = threadIdx.x, warp = tid >> 5;
+  const int CH = E * T;
+  const int span = CH + ncol;
+  const int j0 = q * B;
+  const int jend = min(ncol, j0 + B);
+  const int jn = max(0, jend - j0);
+  const int ngroups = (ncol + 31) >> 5;
+  const int group_end = (jend + 31) >> 5;
+  const int64_t row_words = (int64_t)ngroups * bp_words(MODE);
+  const V NEG = VT<MODE>::neg();
+  const V ZERO = V(0);
+  V* base = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][CH pad + ncol]
+  auto row = [&](int buf, int rs) { return base + (int64_t)(buf * 2 + rs) * span + CH; };
+
+  for (int buf = 0; buf < 2; ++buf) {
+    V* Cb = row(buf, 0);
+    V* Sb = row(buf, 1);
+    if (q == 0)
+      for (int x = tid - CH; x < 0; x += T) Cb[x] = Sb[x] = NEG;  // padding, never rewritten
+    if (buf == 0)
+      for (int j = j0 + tid; j < jend; j += T) {
+        Cb[j] = sac ? ZERO : NEG;
+        Sb[j] = sac ? NEG : ZERO;
+        if (a.tab_c) {
+          a.tab_c[j] = sac ? 0.0 : -INFINITY;
+          a.tab_s[j] = sac ? -INFINITY : 0.0;
+        }
+      }
+  }
+  uint32_t* bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off);
+  cluster_barrier();
+  for (int k = 0; k < L; ++k) {
+    const int kt = k % kStageTile;
+    if (kt == 0) {
+      load_stage_tile<MODE>(a, lo, k, L, st_sh, st_r);
+      __syncthreads();
+    }
+    const StageShift sh = st_sh[kt];
+    const V rk = st_r[kt];
+    const int cur = k & 1;
+    const V* Cc = row(cur, 0);
+    const V* Sc = row(cur, 1);
+    V* Cn = row(cur ^ 1, 0);
+    V* Sn = row(cur ^ 1, 1);
+    uint32_t* bprow = bpw + (int64_t)k * row_words;
+    for (int c0 = j0; c0 < jend; c0 += CH) {  // warp-uniform trip count
+      const int ctop = c0 + CH;
+      const V* pca = Cc - min(sh.i, ctop);
+      const V* pcb = Sc - min(sh.id, ctop);
+      const V* psa = Sc - min(sh.s, ctop);
+      const V* psb = Cc - min(sh.su, ctop);
+      V ca[E], cb[E], sa[E], sb[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = c0 + e * T + tid;
+        const int jr = j < jend ? j : jend - 1;
+        ca[e] = pca[jr];
+        cb[e] = pcb[jr];
+        sa[e] = psa[jr];
+        sb[e] = psb[jr];
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = c0 + e * T + tid;
+        const bool active = j < jend;
+        V cn, sn;
+        const CellFlags f = cell_update<MODE, V>(ca[e], cb[e], sa[e], sb[e], rk, j >= sh.i,
+                                                 j >= sh.id, j >= sh.s, j >= sh.su, cn, sn);
+        emit_bp<MODE>(bprow, (c0 + e * T) / 32 + warp, group_end, f, active);
+        if (active) {
+          Cn[j] = cn;
+          Sn[j] = sn;
+          if (a.tab_c) {
+            a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn, g);
+            a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn, g);
+          }
+        }
+      }
+    }
+    cluster_barrier();
+  }
+  if (tid == 0 && ncol - 1 >= j0 && ncol - 1 < jend) {
+    a.info[inst].end_c = to_f64(row(L & 1, 0)[ncol - 1], g);
+    a.info[inst].end_s = to_f64(row(L & 1, 1)[ncol - 1], g);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // _finish (planner.py:88-101) for a placement already written to pi
 
 __device__ void finish_policy(const sp_instances& in, int64_t inst, int64_t lo, int L,
@@ -949,11 +1062,75 @@ int launch_cluster(const DpArgs& a, int64_t n_items, int threads, size_t smem, C
   return launch_check("dp_cluster_kernel launch");
 }
 
-enum DpVariant { DPV_SMEM = 0, DPV_CLUSTER = 1, DPV_GLOBAL = 2 };
+enum DpVariant { DPV_SMEM = 0, DPV_CLUSTER = 1, DPV_GLOBAL = 2, DPV_COOP = 3 };
+
+template <int MODE>
+int launch_coop(const DpArgs& a, int64_t n_items, int threads, size_t smem, ClusterGeom geo,
+                cudaStream_t st) {
+  auto kern = dp_coop_kernel<MODE, kCellsPerThread>;
+  int rc = SP_OK;
+  if (geo.G > 8) {
+    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                    "cudaFuncSetAttribute(non-portable cluster)");
+    if (rc) return rc;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_items * geo.G), 1, 1);
+  cfg.blockDim = dim3((unsigned)threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)geo.G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, a, geo), "dp_coop_kernel launch");
+  if (rc) return rc;
+  return launch_check("dp_coop_kernel launch");
+}
+
+// cooperative geometry: enough CTAs per instance that the double-buffered
+// rows of every co-resident instance fit comfortably in L2
+ClusterGeom coop_geom(int mode, int64_t ncol) {
+  const size_t vb = mode == VM_INT32 ? 4 : 8;
+  const size_t l2_budget = (size_t)48 << 20;
+  const int resident_ctas = 148 * 2;
+  int G = 2;
+  for (; G < 16; G *= 2) {
+    const int64_t B = ((ncol + G - 1) / G + 31) / 32 * 32;
+    const int64_t t = std::min<int64_t>(kStageThreads, std::max<int64_t>(32, ((B + 3) / 4 + 31) / 32 * 32));
+    const size_t per_inst = 4 * (size_t)(kCellsPerThread * t + ncol) * vb;
+    if ((size_t)(resident_ctas / G) * per_inst <= l2_budget) break;
+  }
+  ClusterGeom geo;
+  geo.G = G;
+  geo.B = (int)(((ncol + G - 1) / G + 31) / 32 * 32);
+  geo.magic = 0;
+  return geo;
+}
+
+int coop_threads(const ClusterGeom& geo) {
+  return (int)std::min<int64_t>(kStageThreads,
+                                std::max<int64_t>(32, ((geo.B + 3) / 4 + 31) / 32 * 32));
+}
+
+size_t coop_row_bytes(int mode, int64_t ncol, const ClusterGeom& geo) {
+  const size_t vb = mode == VM_INT32 ? 4 : 8;
+  return 4 * (size_t)(kCellsPerThread * coop_threads(geo) + ncol) * vb;
+}
 
 int launch_dp_group(int mode, int variant, const DpArgs& a, int64_t n_items, int threads,
                     size_t smem, ClusterGeom geo, cudaStream_t st) {
   if (n_items == 0) return SP_OK;
+  if (variant == DPV_COOP) {
+    switch (mode) {
+      case VM_INT32: return launch_coop<VM_INT32>(a, n_items, threads, smem, geo, st);
+      case VM_F64: return launch_coop<VM_F64>(a, n_items, threads, smem, geo, st);
+      default: return launch_coop<VM_F64_NAN>(a, n_items, threads, smem, geo, st);
+    }
+  }
   if (variant == DPV_CLUSTER) {
     switch (mode) {
       case VM_INT32: return launch_cluster<VM_INT32>(a, n_items, threads, smem, geo, st);
@@ -1000,6 +1177,7 @@ int forced_variant() {
   if (!strcmp(v, "smem")) return DPV_SMEM;
   if (!strcmp(v, "cluster")) return DPV_CLUSTER;
   if (!strcmp(v, "global")) return DPV_GLOBAL;
+  if (!strcmp(v, "coop")) return DPV_COOP;
   return -1;
 }
 
@@ -1049,6 +1227,8 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   std::vector<Item> items;
   items.reserve(n);
   ClusterGeom geo_cache{0, 0, 0};
+  const char* pv = getenv("SPLITPLAN_DP_PREFER");
+  const bool prefer_coop = !(pv && !strcmp(pv, "cluster"));
   int geo_mode = -1;
   int64_t geo_ncol = -1;
   for (int64_t k = 0; k < n; ++k) {
@@ -1073,12 +1253,17 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     it.geo = geo_cache;
     if (force == DPV_GLOBAL || (tab_c && force < 0)) it.variant = DPV_GLOBAL;
     else if (force == DPV_CLUSTER && it.geo.G) it.variant = DPV_CLUSTER;
+    else if (force == DPV_COOP) it.variant = DPV_COOP;
     else if (fits_cta && force != DPV_CLUSTER) it.variant = DPV_SMEM;
+    else if (prefer_coop && ncol > kCoopMinCols) it.variant = DPV_COOP;
     else if (it.geo.G) it.variant = DPV_CLUSTER;
-    else it.variant = DPV_GLOBAL;
+    else it.variant = DPV_COOP;
     if (it.variant == DPV_SMEM && !fits_cta) it.variant = DPV_GLOBAL;
+    if (it.variant == DPV_COOP) it.geo = coop_geom(it.mode, ncol);
     it.bp = align_up(bp_bytes(it.mode, it.L, ncol), 256);
-    it.rows = it.variant == DPV_GLOBAL ? align_up(rb, 256) : 0;
+    it.rows = it.variant == DPV_GLOBAL  ? align_up(rb, 256)
+              : it.variant == DPV_COOP ? align_up(coop_row_bytes(it.mode, ncol, it.geo), 256)
+                                       : 0;
     items.push_back(it);
   }
 
@@ -1128,7 +1313,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       w.inst = it.inst;
       w.bp_off = (int64_t)off;
       off += it.bp;
-      if (it.variant == DPV_GLOBAL) {
+      if (it.rows) {
         w.row_off = (int64_t)off;
         off += it.rows;
       } else {
@@ -1136,12 +1321,14 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       }
       Group* g = nullptr;
       // single-CTA kernels size their row padding by blockDim, so a group
-      // shares one thread count; cluster groups share one geometry
-      const int want_t = it.variant == DPV_CLUSTER ? 0 : threads_for(it.ncol);
+      // shares one thread count; cluster / cooperative groups share a geometry
+      const bool multi = it.variant == DPV_CLUSTER || it.variant == DPV_COOP;
+      const int want_t = it.variant == DPV_CLUSTER ? 0
+                         : it.variant == DPV_COOP  ? coop_threads(it.geo)
+                                                   : threads_for(it.ncol);
       for (Group& c : groups)
         if (c.mode == it.mode && c.variant == it.variant &&
-            (it.variant == DPV_CLUSTER ? (c.geo.G == it.geo.G && c.geo.B == it.geo.B)
-                                       : c.threads == want_t))
+            (multi ? (c.geo.G == it.geo.G && c.geo.B == it.geo.B) : c.threads == want_t))
           g = &c;
       if (!g) {
         groups.push_back(Group{it.mode, it.variant});
@@ -1162,6 +1349,8 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         g->smem = std::max(g->smem, need);
       }
     }
+    // row buffers of multi-CTA / global variants must hold the group's padding
+    // (same thread count across the group, so row_bytes already agree)
     for (const Group& g : groups)
       for (const DpWork& w : g.items) hwork.push_back(w);
     rc = check_cuda(cudaMemcpyAsync(work, hwork.data(), sizeof(DpWork) * hwork.size(),
@@ -1188,7 +1377,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         // both rows plus those bits
         const double vb = g.mode == VM_INT32 ? 4.0 : 8.0;
         const double bits = bp_words(g.mode) * 4.0 / 32.0;
-        const double per_cell = g.variant == DPV_GLOBAL ? 4.0 * vb + bits : bits;
+        const double per_cell = g.variant == DPV_GLOBAL ? 4.0 * vb + bits : bits;  // coop: rows live in L2
         prof_record_dp(e0, e1, g.cells, g.cells * per_cell, g.variant);
       }
       first += cnt;

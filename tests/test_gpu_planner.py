@@ -87,7 +87,7 @@ def test_dp_tables_match_reference(gpu):
         pos += cnt
 
 
-@pytest.mark.parametrize("variant", ["global", "cluster", "smem"])
+@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop"])
 def test_dp_tables_every_variant(gpu, variant, monkeypatch):
     """Full tables from each K2 variant equal the reference's build_dp_tables."""
     from paper_2410_10759_b200 import planner as P
@@ -180,7 +180,7 @@ def test_dp_vs_oracle_smem_and_global_rows(gpu, r_kind):
         assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{r_kind}[{k}]")
 
 
-@pytest.mark.parametrize("variant", ["global", "cluster", "smem"])
+@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop"])
 @pytest.mark.parametrize("name", ["battery_wide", "battery_float", "battery_large_model"])
 def test_dp_kernel_variants_agree(gpu, variant, name, monkeypatch):
     """Every K2 variant (rows in one CTA's SMEM, in cluster DSMEM, in global
