@@ -262,6 +262,15 @@ __device__ __forceinline__ void emit_bp(uint32_t* row_words, int group, int ngro
   }
 }
 
+// Materialise a pointer in a register so the compiler cannot re-associate
+// (base + offset) + index into wide 64-bit index arithmetic per load: every
+// predecessor load then costs one IMAD.WIDE.U32 on a chunk-uniform base.
+template <typename T>
+__device__ __forceinline__ const T* opaque(const T* p) {
+  asm("" : "+l"(p));
+  return p;
+}
+
 template <int MODE>
 __device__ __forceinline__ void load_stage_tile(const DpArgs& a, int64_t lo, int k, int L,
                                                 StageShift* st_sh, typename VT<MODE>::T* st_r) {
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(kStageThreads, 2) dp_stage_kernel(DpArgs a) {
       for (int e = 0; e < E; ++e) {
         const int j = c0 + e * T + tid;
         const bool active = j < ncol;
-        const int jr = active ? j : ncol - 1;
+        const uint32_t jr = (uint32_t)(active ? j : ncol - 1);
         const CellFlags f = cell_update<MODE, V>(pca[jr], pcb[jr], psa[jr], psb[jr], rk, j >= sh.i,
                                                  j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
         emit_bp<MODE>(bprow, (c0 + e * T) / 32 + warp, ngroups, f, active);
@@ -610,15 +619,17 @@ __global__ void __launch_bounds__(kStageThreads, 2) dp_coop_kernel(DpArgs a, Clu
     uint32_t* bprow = bpw + (int64_t)k * row_words;
     for (int c0 = j0; c0 < jend; c0 += CH) {  // warp-uniform trip count
       const int ctop = c0 + CH;
-      const V* pca = Cc - min(sh.i, ctop);
-      const V* pcb = Sc - min(sh.id, ctop);
-      const V* psa = Sc - min(sh.s, ctop);
-      const V* psb = Cc - min(sh.su, ctop);
+      // chunk-uniform bases such that base + jr (jr >= c0 >= 0, unsigned) is the
+      // clamped predecessor: one IMAD.WIDE.U32 per load
+      const V* pca = opaque(Cc - min(sh.i, ctop));
+      const V* pcb = opaque(Sc - min(sh.id, ctop));
+      const V* psa = opaque(Sc - min(sh.s, ctop));
+      const V* psb = opaque(Cc - min(sh.su, ctop));
       V ca[E], cb[E], sa[E], sb[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int j = c0 + e * T + tid;
-        const int jr = j < jend ? j : jend - 1;
+        const uint32_t jr = (uint32_t)(j < jend ? j : jend - 1);
         ca[e] = pca[jr];
         cb[e] = pcb[jr];
         sa[e] = psa[jr];
@@ -633,8 +644,8 @@ __global__ void __launch_bounds__(kStageThreads, 2) dp_coop_kernel(DpArgs a, Clu
                                                  j >= sh.id, j >= sh.s, j >= sh.su, cn, sn);
         emit_bp<MODE>(bprow, (c0 + e * T) / 32 + warp, group_end, f, active);
         if (active) {
-          Cn[j] = cn;
-          Sn[j] = sn;
+          Cn[(uint32_t)j] = cn;
+          Sn[(uint32_t)j] = sn;
           if (a.tab_c) {
             a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn, g);
             a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn, g);
