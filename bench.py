@@ -166,13 +166,42 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per DP-stage launch from the committed ncu capture, if any."""
-    try:
-        doc = json.loads((ROOT / "profiles" / "dp_stage_ncu.json").read_text())
-        return doc.get("dram_bytes_per_launch")
-    except Exception:
+VARIANTS = ["dp_stage_kernel<smem rows>", "dp_cluster_kernel<DSMEM rows>",
+            "dp_stage_kernel<global rows>", "dp_coop_kernel<L2 rows>"]
+NCU_SUMMARY = {0: "dp_smem_ncu_summary.json", 3: "dp_coop_ncu_summary.json"}
+
+
+def ncu_traffic(variant: int, cells_per_launch: float):
+    """DRAM bytes per launch, scaled from the newest committed ncu capture of this
+    variant (profiles/rNN/*_ncu_summary.json holds DRAM bytes per DP cell)."""
+    name = NCU_SUMMARY.get(variant)
+    if not name:
+        return None, None
+    for d in sorted((ROOT / "profiles").glob("r*"), reverse=True):
+        f = d / name
+        if f.exists():
+            doc = json.loads(f.read_text())
+            return doc["dram_bytes_per_cell"] * cells_per_launch, str(f.relative_to(ROOT))
+    return None, None
+
+
+def onchip_roofline(variant: int, cells_per_s: float, sm_mhz: float | None) -> dict | None:
+    """The resource that actually bounds the DP stage kernel (its rows never reach HBM).
+
+    smem rows: 4 LDS + 2 STS words per cell = 24 B of SMEM traffic (4 B values);
+    peak 128 B/clk/SM x 148 SMs.  L2 rows (coop): 16 B of L2 reads + 8 B of L2
+    writes per cell; peak ~6300 B/clk chip-wide (LTS cap, B300_MICROARCH.md; not
+    yet measured on B200)."""
+    clk = (sm_mhz or 1965.0) * 1e6
+    if variant == 0:
+        per_cell, peak, res = 24.0, 128.0 * 148 * clk, "smem"
+    elif variant == 3:
+        per_cell, peak, res = 24.0, 6300.0 * clk, "l2"
+    else:
         return None
+    ach = cells_per_s * per_cell
+    return {"resource": res, "bytes_per_cell": per_cell, "achieved_GBps": ach / 1e9,
+            "peak_GBps": peak / 1e9, "frac": ach / peak}
 
 
 def main():
@@ -289,6 +318,10 @@ def main():
         avg_launch_ms = dk_ms.value / max(dk_n.value, 1)
         bytes_per_launch = dk_bytes.value / max(dk_n.value, 1)
         achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9 if avg_launch_ms > 0 else None
+        cells_per_launch = dk_cells.value / max(dk_n.value, 1)
+        kernel_rate = dk_cells.value / (dk_ms.value / 1e3) if dk_ms.value else None
+        traffic, traffic_src = ncu_traffic(dk_var.value, cells_per_launch)
+        clk = clocks.summary()
         line = {
             "metric": METRIC,
             "value": value,
@@ -319,22 +352,24 @@ def main():
                     "h2d_bytes_per_step": host_req.host_bytes(), "d2h_bytes_per_step": d2h},
             "gpu_launches": int(all_l.value),
             "roofline": {
-                "kernel": ["dp_stage_kernel<smem rows>", "dp_cluster_kernel<DSMEM rows>",
-                           "dp_stage_kernel<global rows>", "dp_coop_kernel<L2 rows>"][dk_var.value],
+                "kernel": VARIANTS[dk_var.value],
                 "bound": "hbm",
                 "achieved": achieved,
                 "peak": peak,
                 "peak_kind": peak_kind,
                 "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": ncu_traffic(),
-                "bytes_per_cell": bytes_per_launch / max(dk_cells.value / max(dk_n.value, 1), 1),
+                "traffic": traffic,
+                "traffic_source": traffic_src,
+                "bytes_per_cell": bytes_per_launch / max(cells_per_launch, 1),
                 "launches": dk_n.value,
                 "avg_launch_ms": avg_launch_ms,
                 "share_of_step": dk_ms.value / dev_ms if dev_ms else None,
-                "cells_per_s_in_kernel": dk_cells.value / (dk_ms.value / 1e3) if dk_ms.value else None,
+                "cells_per_s_in_kernel": kernel_rate,
+                "onchip": onchip_roofline(dk_var.value, kernel_rate, clk.get("sm_mhz")),
+                "row_streaming_ceiling_cells_per_s": peak * 1e9 / 33.0,
             },
-            "clocks": clocks.summary(),
+            "clocks": clk,
         }
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(req_np, args.cpu_sample)
@@ -346,7 +381,8 @@ def main():
 
 def cpu_baseline(req_np: dict, sample: int) -> dict:
     procs = max(1, min(os.cpu_count() or 1, 64))
-    sample = sample or max(64, 6 * procs)  # ~0.15 s of numpy per request: ~10-30 s CPU
+    # ~0.12 s of single-core numpy per cfg2 request: 128 per process is ~15 s wall
+    sample = sample or max(64, 128 * procs)
     idx = np.arange(min(sample, len(req_np["seq_len"])))
     cells, dt = cpu_run(req_np, idx, procs)
     return {"value": cells / dt, "unit": "DP cells/s", "cores": procs, "kind": "port",
@@ -362,7 +398,7 @@ def run_reference(args, rank: int, world: int):
     cfps, sfps = calibrated_rates()
     req_np = cfg2_requests(args.requests, args.seed * 1000, cfps, sfps)
     procs = max(1, min(os.cpu_count() or 1, 128))
-    per = args.cpu_sample or max(8, procs)
+    per = args.cpu_sample or max(8, 4 * procs)  # ~0.5 s of host work per step
     times, cells_tot = [], 0.0
     for s in range(args.warmup + args.steps):
         idx = (np.arange(per) + s * per) % args.requests
