@@ -167,8 +167,10 @@ def measured_peak_hbm():
 
 
 VARIANTS = ["dp_stage_kernel<smem rows>", "dp_cluster_kernel<DSMEM rows>",
-            "dp_stage_kernel<global rows>", "dp_coop_kernel<L2 rows>"]
-NCU_SUMMARY = {0: "dp_smem_ncu_summary.json", 3: "dp_coop_ncu_summary.json"}
+            "dp_stage_kernel<global rows>", "dp_coop_kernel<L2 rows>",
+            "dp_stream_kernel<L2 rows, bulk-copy staged windows>"]
+NCU_SUMMARY = {0: "dp_smem_ncu_summary.json", 3: "dp_coop_ncu_summary.json",
+               4: "dp_stream_ncu_summary.json"}
 
 
 def ncu_traffic(variant: int, cells_per_launch: float):
@@ -195,7 +197,7 @@ def onchip_roofline(variant: int, cells_per_s: float, sm_mhz: float | None) -> d
     clk = (sm_mhz or 1965.0) * 1e6
     if variant == 0:
         per_cell, peak, res = 24.0, 128.0 * 148 * clk, "smem"
-    elif variant == 3:
+    elif variant in (3, 4):
         per_cell, peak, res = 24.0, 6300.0 * clk, "l2"
     else:
         return None
@@ -252,17 +254,23 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    from paper_2410_10759_b200.shard import gather_policies
+
     def step_device():
-        return engine.solve(dev_req, total_layers, off)
+        s = engine.solve(dev_req, total_layers, off)
+        if world > 1:  # the job's one collective: gather every rank's result records
+            gather_policies(s.policies, s.layer_off)
+        return s
 
     def step_e2e():
         r = host_req.to(dev, non_blocking=True)
         s = engine.solve(r, total_layers, off)
-        out = (s.policies.pi.to("cpu", non_blocking=True),
-               s.policies.client_value.to("cpu", non_blocking=True),
-               s.policies.server_load.to("cpu", non_blocking=True),
-               s.policies.integer_latency.to("cpu", non_blocking=True),
-               s.policies.feasible.to("cpu", non_blocking=True))
+        pol = gather_policies(s.policies, s.layer_off)[0] if world > 1 else s.policies
+        out = (pol.pi.to("cpu", non_blocking=True),
+               pol.client_value.to("cpu", non_blocking=True),
+               pol.server_load.to("cpu", non_blocking=True),
+               pol.integer_latency.to("cpu", non_blocking=True),
+               pol.feasible.to("cpu", non_blocking=True))
         return s, out
 
     for _ in range(max(args.warmup, 0)):
@@ -345,6 +353,7 @@ def main():
                 "l2": "inputs larger than L2: each step writes ~%.1f GB of packed back-pointers"
                       % (cells / 4 / 1e9),
                 "parallelism": f"request-sharded dp{world}",
+                "collective": "none in the solve; one all_gather of result records per step when N > 1",
             },
             "scenarios_per_s": n * world / (step_ms / 1e3),
             "e2e": {"value": total_cells / (e2e_ms / args.steps / 1e3), "unit": "DP cells/s",

@@ -60,14 +60,14 @@ void sp_profile_enable(int on) { g_prof = on != 0; }
 int sp_profile_collect(double* dp_kernel_ms, int64_t* dp_launches, double* dp_cells,
                        double* dp_bytes, int64_t* all_launches, int32_t* dp_variant) {
   double ms = 0, cells = 0, bytes = 0;
-  double by_variant[4] = {0, 0, 0, 0};
+  double by_variant[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int rc = SP_OK;
   for (DpRec& r : g_dp) {
     float t = 0.f;
     if (rc == SP_OK) rc = sp::check_cuda(cudaEventSynchronize(r.b), "profile event sync");
     if (rc == SP_OK) rc = sp::check_cuda(cudaEventElapsedTime(&t, r.a, r.b), "profile elapsed");
     ms += t;
-    if (r.variant >= 0 && r.variant < 4) by_variant[r.variant] += t;
+    if (r.variant >= 0 && r.variant < 8) by_variant[r.variant] += t;
     cells += r.cells;
     bytes += r.bytes;
     cudaEventDestroy(r.a);
@@ -80,7 +80,7 @@ int sp_profile_collect(double* dp_kernel_ms, int64_t* dp_launches, double* dp_ce
   if (all_launches) *all_launches = g_launches;
   if (dp_variant) {
     int best = 0;
-    for (int v = 1; v < 4; ++v)
+    for (int v = 1; v < 8; ++v)
       if (by_variant[v] > by_variant[best]) best = v;
     *dp_variant = best;
   }

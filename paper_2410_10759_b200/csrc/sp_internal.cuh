@@ -167,8 +167,9 @@ struct StageShift {
 // work item of one DP CTA
 struct DpWork {
   int64_t inst;
-  int64_t bp_off;   // byte offset of this instance's back-pointer table
-  int64_t row_off;  // byte offset of its global rows, or -1 if rows live in SMEM
+  int64_t bp_off;        // byte offset of this instance's back-pointer table
+  int64_t row_off;       // byte offset of its global rows, or -1 if rows live in SMEM
+  int64_t bp_row_words;  // u32 words per stage row of the back-pointer table
 };
 
 }  // namespace sp

@@ -26,7 +26,6 @@ constexpr int kStageTile = 128;          // stage records staged in SMEM at a ti
 constexpr int kCellsPerThread = 4;       // E: columns per thread per chunk
 constexpr int kMaxThreads = 1024;
 constexpr int kStageThreads = 512;     // single-CTA DP kernels: 2 CTAs per SM
-constexpr int64_t kCoopMinCols = 0;      // rows longer than one SMEM go cooperative
 constexpr size_t kSmemCap = 227 * 1024;  // sm_100a max dynamic SMEM per CTA
 constexpr int64_t kMaxCols = (int64_t(1) << 31) - 64;
 
@@ -284,9 +283,17 @@ __device__ __forceinline__ void load_stage_tile(const DpArgs& a, int64_t lo, int
   }
 }
 
-template <int MODE, bool ROWS_SMEM, int E>
-__global__ void __launch_bounds__(kStageThreads, 2) dp_stage_kernel(DpArgs a) {
+// Single-CTA kernel, T threads x E columns per chunk (CH = T*E), both
+// template constants so every predecessor load is `LDS [base + imm]` on four
+// chunk-uniform bases.  Rows hold CH cells of NEG padding in front and are
+// padded at the end to whole chunks (nch*CH columns), so no load, store or
+// back-pointer word needs a bounds check: cells past W_eff compute garbage
+// that no valid cell ever reads (reads only go left), and their back-pointer
+// bits are never visited.  bp rows are nch*CH/32 groups wide.
+template <int MODE, bool ROWS_SMEM, int T, int E>
+__global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1024 / T)) dp_stage_kernel(DpArgs a) {
   using V = typename VT<MODE>::T;
+  constexpr int CH = T * E;
   extern __shared__ __align__(16) unsigned char smem[];
   StageShift* st_sh = reinterpret_cast<StageShift*>(smem);
   V* st_r = reinterpret_cast<V*>(smem + kStageTile * sizeof(StageShift));
@@ -299,12 +306,10 @@ __global__ void __launch_bounds__(kStageThreads, 2) dp_stage_kernel(DpArgs a) {
   const int ncol = (int)(a.info[inst].w_eff + 1);
   const double g = a.info[inst].scale;
   const bool sac = a.sac[inst] != 0;
-  const int T = blockDim.x, tid = threadIdx.x, warp = tid >> 5;
-  const int CH = E * T;  // chunk width == NEG padding in front of each row
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int nch = (ncol + CH - 1) / CH;
-  const int span = CH + ncol;
-  const int ngroups = (ncol + 31) >> 5;
-  const int64_t row_words = (int64_t)ngroups * bp_words(MODE);
+  const int span = CH + nch * CH;
+  const int64_t row_words = wk.bp_row_words;
 
   V* base = ROWS_SMEM ? reinterpret_cast<V*>(smem + stage_bytes)
                       : reinterpret_cast<V*>(a.rows + wk.row_off);
@@ -313,10 +318,10 @@ __global__ void __launch_bounds__(kStageThreads, 2) dp_stage_kernel(DpArgs a) {
   const V NEG = VT<MODE>::neg();
   const V ZERO = V(0);
 
-  for (int x = tid - CH; x < ncol; x += T) {
-    Cp[x] = (x >= 0 && sac) ? ZERO : NEG;
-    Sp[x] = (x >= 0 && !sac) ? ZERO : NEG;
-    if (a.tab_c && x >= 0) {
+  for (int x = tid - CH; x < nch * CH; x += T) {
+    Cp[x] = (x >= 0 && x < ncol && sac) ? ZERO : NEG;
+    Sp[x] = (x >= 0 && x < ncol && !sac) ? ZERO : NEG;
+    if (a.tab_c && x >= 0 && x < ncol) {
       a.tab_c[x] = sac ? 0.0 : -INFINITY;
       a.tab_s[x] = sac ? -INFINITY : 0.0;
     }
@@ -332,33 +337,38 @@ __global__ void __launch_bounds__(kStageThreads, 2) dp_stage_kernel(DpArgs a) {
     __syncthreads();
     const StageShift sh = st_sh[kt];
     const V rk = st_r[kt];
-    uint32_t* bprow = bpw + (int64_t)k * row_words;
+    uint32_t* bprow = bpw + (int64_t)k * row_words + warp * bp_words(MODE);
 
     for (int c = nch - 1; c >= 0; --c) {
       const int c0 = c * CH, ctop = c0 + CH;
-      // chunk-uniform clamped shifts: every read stays in [-CH, ncol)
-      const V* pca = Cp - min(sh.i, ctop);
-      const V* pcb = Sp - min(sh.id, ctop);
-      const V* psa = Sp - min(sh.s, ctop);
-      const V* psb = Cp - min(sh.su, ctop);
+      // chunk-uniform clamped shifts: every read stays in [-CH, nch*CH)
+      const V* pca = Cp - min(sh.i, ctop) + c0 + tid;
+      const V* pcb = Sp - min(sh.id, ctop) + c0 + tid;
+      const V* psa = Sp - min(sh.s, ctop) + c0 + tid;
+      const V* psb = Cp - min(sh.su, ctop) + c0 + tid;
+      uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
       V cn[E], sn[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int j = c0 + e * T + tid;
-        const bool active = j < ncol;
-        const uint32_t jr = (uint32_t)(active ? j : ncol - 1);
-        const CellFlags f = cell_update<MODE, V>(pca[jr], pcb[jr], psa[jr], psb[jr], rk, j >= sh.i,
-                                                 j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
-        emit_bp<MODE>(bprow, (c0 + e * T) / 32 + warp, ngroups, f, active);
+        const CellFlags f = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk,
+                                                 j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su,
+                                                 cn[e], sn[e]);
+        emit_bp<MODE>(bpc + e * (T / 32) * bp_words(MODE), 0, 1, f, true);
       }
       __syncthreads();
+      V* qc = Cp + c0 + tid;
+      V* qs = Sp + c0 + tid;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const int j = c0 + e * T + tid;
-        if (j < ncol) {
-          Cp[j] = cn[e];
-          Sp[j] = sn[e];
-          if (a.tab_c) {
+        qc[e * T] = cn[e];
+        qs[e * T] = sn[e];
+      }
+      if (a.tab_c) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = c0 + e * T + tid;
+          if (j < ncol) {
             a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn[e], g);
             a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn[e], g);
           }
@@ -438,9 +448,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, Cl
   const int T = blockDim.x, tid = threadIdx.x, warp = tid >> 5;
   const int j0 = q * B;
   const int jn = max(0, min(ncol, j0 + B) - j0);
-  const int ngroups = (ncol + 31) >> 5;
   const int group_end = (j0 + jn + 31) >> 5;  // this CTA's back-pointer groups end here
-  const int64_t row_words = (int64_t)ngroups * bp_words(MODE);
+  const int64_t row_words = wk.bp_row_words;
   const V NEG = VT<MODE>::neg();
   const V ZERO = V(0);
   const uint32_t rows_sa = smem_addr(rows);
@@ -578,9 +587,8 @@ __global__ void __launch_bounds__(kStageThreads, 2) dp_coop_kernel(DpArgs a, Clu
   const int j0 = q * B;
   const int jend = min(ncol, j0 + B);
   const int jn = max(0, jend - j0);
-  const int ngroups = (ncol + 31) >> 5;
   const int group_end = (jend + 31) >> 5;
-  const int64_t row_words = (int64_t)ngroups * bp_words(MODE);
+  const int64_t row_words = wk.bp_row_words;
   const V NEG = VT<MODE>::neg();
   const V ZERO = V(0);
   V* base = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][CH pad + ncol]
@@ -662,6 +670,201 @@ __global__ void __launch_bounds__(kStageThreads, 2) dp_coop_kernel(DpArgs a, Clu
 }
 
 // ---------------------------------------------------------------------------
+// K2 streaming variant (rows longer than one SM's shared memory): a cluster
+// of G CTAs shares one instance, CTA q owning NC chunks of CH = T*E columns.
+// The rows live in global memory, double-buffered, sized so that the rows of
+// every co-resident instance stay in L2.  For each chunk the four predecessor
+// windows (C at i, S at i+d, S at s, C at s+u; CH + 16 B each, 16-B aligned)
+// are fetched by the bulk-copy engine (cp.async.bulk, completion on an
+// mbarrier) into an NSLOT-deep ring of shared-memory slots, issued NSLOT
+// chunks ahead by one thread; the compute then reads them with conflict-free
+// LDS exactly like the single-CTA kernel and stores the new cells straight to
+// the next row buffer (coalesced 128-B warp stores).  One cluster barrier
+// (release/acquire) per stage publishes the row; a proxy fence orders the
+// generic stores before the next stage's async-proxy reads.
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+struct StreamGeom {
+  int G;   // CTAs per instance (cluster size)
+  int NC;  // chunks per CTA
+};
+
+// values of NEG padding in front of a streamed row (>= CH + one 16-B group,
+// a whole number of 16-B groups) and the full row span
+template <typename V, int CH>
+__host__ __device__ constexpr int stream_pad() { return CH + 16 / (int)sizeof(V); }
+
+template <int MODE, int T, int E, int NSLOT>
+__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 512 / T)) dp_stream_kernel(DpArgs a, StreamGeom geo) {
+  using V = typename VT<MODE>::T;
+  constexpr int CH = T * E;
+  constexpr int AL = 16 / (int)sizeof(V);  // values per 16 B
+  constexpr int WIN = CH + AL;              // values per staged window
+  constexpr int PAD = stream_pad<V, CH>();
+  extern __shared__ __align__(16) unsigned char smem[];
+  StageShift* st_sh = reinterpret_cast<StageShift*>(smem);
+  V* st_r = reinterpret_cast<V*>(smem + kStageTile * sizeof(StageShift));
+  const size_t stage_bytes = align_up(kStageTile * (sizeof(StageShift) + sizeof(V)), 128);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stage_bytes);
+  V* slots = reinterpret_cast<V*>(smem + stage_bytes + 128);  // [NSLOT][4][WIN]
+
+  const int G = geo.G, NC = geo.NC;
+  const int q = (int)cluster_rank();
+  const DpWork wk = a.work[blockIdx.x / G];
+  const int64_t inst = wk.inst;
+  const int64_t lo = a.layer_off[inst];
+  const int L = (int)(a.layer_off[inst + 1] - lo);
+  const int ncol = (int)(a.info[inst].w_eff + 1);
+  const double g = a.info[inst].scale;
+  const bool sac = a.sac[inst] != 0;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int B = NC * CH;
+  const int j0 = q * B;
+  const int64_t span = (int64_t)PAD + (int64_t)G * B + AL;
+  const int64_t row_words = wk.bp_row_words;
+  const V NEG = VT<MODE>::neg();
+  const V ZERO = V(0);
+  V* base = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][PAD + G*B + AL]
+  auto row = [&](int buf, int rs) { return base + (int64_t)(buf * 2 + rs) * span + PAD; };
+
+  for (int buf = 0; buf < 2; ++buf) {
+    V* Cb = row(buf, 0);
+    V* Sb = row(buf, 1);
+    if (q == 0)
+      for (int x = tid - PAD; x < 0; x += T) Cb[x] = Sb[x] = NEG;  // padding, never rewritten
+    if (q == G - 1)
+      for (int x = G * B + tid; x < G * B + AL; x += T) Cb[x] = Sb[x] = NEG;
+    if (buf == 0)
+      for (int j = j0 + tid; j < j0 + B; j += T) {
+        const bool valid = j < ncol;
+        Cb[j] = (valid && sac) ? ZERO : NEG;
+        Sb[j] = (valid && !sac) ? ZERO : NEG;
+        if (a.tab_c && valid) {
+          a.tab_c[j] = sac ? 0.0 : -INFINITY;
+          a.tab_s[j] = sac ? -INFINITY : 0.0;
+        }
+      }
+  }
+  if (tid == 0) {
+    for (int b = 0; b < NSLOT; ++b) mbar_init(&bars[b], 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async_global();
+  uint32_t* bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off);
+  cluster_barrier();
+
+  uint32_t use = 0;  // slot uses so far (uniform across the CTA)
+  for (int k = 0; k < L; ++k) {
+    const int kt = k % kStageTile;
+    if (kt == 0) {
+      __syncthreads();
+      load_stage_tile<MODE>(a, lo, k, L, st_sh, st_r);
+      __syncthreads();
+    }
+    const StageShift sh = st_sh[kt];
+    const V rk = st_r[kt];
+    const int cur = k & 1;
+    const V* Cc = row(cur, 0);
+    const V* Sc = row(cur, 1);
+    V* Cn = row(cur ^ 1, 0);
+    V* Sn = row(cur ^ 1, 1);
+    uint32_t* bprow = bpw + (int64_t)k * row_words + warp * bp_words(MODE);
+
+    // window w of chunk c: first (16-B aligned) value and the in-window offset
+    auto issue = [&](int c, int slot) {
+      const int c0 = j0 + c * CH, ctop = c0 + CH;
+      const V* src[4] = {Cc, Sc, Sc, Cc};
+      const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
+      mbar_expect_tx(&bars[slot], 4u * WIN * sizeof(V));
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const int start = c0 - min(shf[w], ctop);
+        const int al = start & ~(AL - 1);
+        bulk_g2s(slots + (slot * 4 + w) * WIN, src[w] + al, WIN * sizeof(V), &bars[slot]);
+      }
+    };
+    if (tid == 0) {
+      fence_proxy_async_global();
+      for (int c = 0; c < min(NSLOT, NC); ++c) issue(c, (int)((use + c) % NSLOT));
+    }
+    for (int c = 0; c < NC; ++c) {
+      const uint32_t u = use + c;
+      const int slot = (int)(u % NSLOT);
+      const int c0 = j0 + c * CH, ctop = c0 + CH;
+      const V* ws = slots + slot * 4 * WIN + tid;
+      const V* pca = ws + 0 * WIN + ((c0 - min(sh.i, ctop)) & (AL - 1));
+      const V* pcb = ws + 1 * WIN + ((c0 - min(sh.id, ctop)) & (AL - 1));
+      const V* psa = ws + 2 * WIN + ((c0 - min(sh.s, ctop)) & (AL - 1));
+      const V* psb = ws + 3 * WIN + ((c0 - min(sh.su, ctop)) & (AL - 1));
+      uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
+      mbar_wait(&bars[slot], (u / NSLOT) & 1);
+      V* qc = Cn + c0 + tid;
+      V* qs = Sn + c0 + tid;
+      V cn[E], sn[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = c0 + e * T + tid;
+        const CellFlags f = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk,
+                                                 j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su,
+                                                 cn[e], sn[e]);
+        emit_bp<MODE>(bpc + e * (T / 32) * bp_words(MODE), 0, 1, f, true);
+        qc[e * T] = cn[e];
+        qs[e * T] = sn[e];
+      }
+      if (a.tab_c) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = c0 + e * T + tid;
+          if (j < ncol) {
+            a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn[e], g);
+            a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn[e], g);
+          }
+        }
+      }
+      __syncthreads();  // every thread is done reading this slot
+      if (tid == 0 && c + NSLOT < NC) issue(c + NSLOT, slot);
+    }
+    use += NC;
+    fence_proxy_async_global();  // this stage's generic stores before the next stage's bulk reads
+    cluster_barrier();
+  }
+  if (tid == 0 && ncol - 1 >= j0 && ncol - 1 < j0 + B) {
+    a.info[inst].end_c = to_f64(row(L & 1, 0)[ncol - 1], g);
+    a.info[inst].end_s = to_f64(row(L & 1, 1)[ncol - 1], g);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // _finish (planner.py:88-101) for a placement already written to pi
 
 __device__ void finish_policy(const sp_instances& in, int64_t inst, int64_t lo, int L,
@@ -724,7 +927,6 @@ __global__ void backtrack_kernel(sp_instances in, const InstInfo* info, const St
   const int64_t lo = in.layer_off[inst];
   const int L = (int)(in.layer_off[inst + 1] - lo);
   const InstInfo inf = info[inst];
-  const int64_t ncol = inf.w_eff + 1;
   double ec = inf.end_c, es = inf.end_s;
   const int8_t must = in.must_end_at ? in.must_end_at[inst] : (int8_t)-1;
   if (must == 1) es = -INFINITY;
@@ -744,7 +946,7 @@ __global__ void backtrack_kernel(sp_instances in, const InstInfo* info, const St
   // (C-stay, S-stay[, C-switch, S-switch]); see the K2 comment
   const uint32_t* bpi = reinterpret_cast<const uint32_t*>(bp + wk.bp_off);
   const int nw = bp_words(inf.mode);
-  const int64_t row_words = ((ncol + 31) >> 5) * nw;
+  const int64_t row_words = wk.bp_row_words;
   for (int k = L; k >= 1; --k) {
     const uint32_t* grp = bpi + (int64_t)(k - 1) * row_words + (j >> 5) * nw;
     const uint32_t bit = 1u << (j & 31);
@@ -1006,41 +1208,167 @@ struct Carve {
   }
 };
 
-// threads of a single-CTA DP kernel: one chunk if the row is short, else the
-// full kStageThreads
-int threads_for(int64_t ncol) {
-  int64_t t = (ncol + kCellsPerThread - 1) / kCellsPerThread;
-  t = (t + 31) / 32 * 32;
-  return (int)std::min<int64_t>(kStageThreads, std::max<int64_t>(32, t));
-}
-
 size_t value_bytes(int mode) { return mode == VM_INT32 ? 4 : 8; }
 
-// both rows of a single-CTA kernel, each with CH = E*T cells of NEG padding
-size_t row_bytes_mode(int mode, int64_t ncol) {
-  const int64_t pad = (int64_t)kCellsPerThread * threads_for(ncol);
-  return 2 * (size_t)(pad + ncol) * value_bytes(mode);
-}
+// packed back-pointer words per stage row for rows of `cols` columns
+int64_t bp_row_words_for(int mode, int64_t cols) { return ((cols + 31) / 32) * bp_words(mode); }
 
-// packed back-pointer bytes of one instance (K2 comment)
-size_t bp_bytes(int mode, int64_t L, int64_t ncol) {
-  return (size_t)L * (size_t)((ncol + 31) / 32) * (size_t)bp_words(mode) * 4;
-}
 size_t stage_bytes_mode(int mode) {
-  const size_t v = mode == VM_INT32 ? 4 : 8;
-  return align_up(kStageTile * (sizeof(StageShift) + v), 16);
+  return align_up(kStageTile * (sizeof(StageShift) + value_bytes(mode)), 16);
 }
 
-template <int MODE, bool SMEM>
-int launch_dp(const DpArgs& a, int64_t n_items, int threads, size_t smem, cudaStream_t st) {
-  auto kern = dp_stage_kernel<MODE, SMEM, kCellsPerThread>;
+enum DpVariant { DPV_SMEM = 0, DPV_CLUSTER = 1, DPV_GLOBAL = 2, DPV_COOP = 3, DPV_STREAM = 4 };
+
+// ---- single-CTA kernels: T x E configurations ------------------------------
+
+constexpr int kSingleT[] = {64, 128, 256, 512};
+constexpr int kSingleE = 4;
+constexpr int kNumSingle = 4;
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+// about four chunks per stage, at most 512 threads
+int single_cfg_for(int64_t ncol) {
+  const int force = env_int("SPLITPLAN_DP_THREADS", 0);
+  for (int c = 0; c < kNumSingle; ++c)
+    if (force == kSingleT[c]) return c;
+  for (int c = 0; c < kNumSingle; ++c)
+    if ((int64_t)kSingleT[c] * kSingleE * 4 >= ncol) return c;
+  return kNumSingle - 1;
+}
+int64_t single_ch(int cfg) { return (int64_t)kSingleT[cfg] * kSingleE; }
+int64_t single_cols(int cfg, int64_t ncol) {
+  const int64_t ch = single_ch(cfg);
+  return (ncol + ch - 1) / ch * ch;
+}
+// both rows: CH cells of NEG padding + whole chunks
+size_t single_row_bytes(int mode, int64_t ncol, int cfg) {
+  return 2 * (size_t)(single_ch(cfg) + single_cols(cfg, ncol)) * value_bytes(mode);
+}
+
+template <int MODE, bool SMEM, int T>
+int launch_single_t(const DpArgs& a, int64_t n_items, size_t smem, cudaStream_t st) {
+  auto kern = dp_stage_kernel<MODE, SMEM, T, kSingleE>;
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)kSmemCap),
                       "cudaFuncSetAttribute(dp_stage_kernel)");
   if (rc) return rc;
-  kern<<<(unsigned)n_items, threads, smem, st>>>(a);
+  kern<<<(unsigned)n_items, T, smem, st>>>(a);
   return launch_check("dp_stage_kernel launch");
 }
+
+template <int MODE, bool SMEM>
+int launch_single(const DpArgs& a, int64_t n_items, int cfg, size_t smem, cudaStream_t st) {
+  switch (cfg) {
+    case 0: return launch_single_t<MODE, SMEM, 64>(a, n_items, smem, st);
+    case 1: return launch_single_t<MODE, SMEM, 128>(a, n_items, smem, st);
+    case 2: return launch_single_t<MODE, SMEM, 256>(a, n_items, smem, st);
+    default: return launch_single_t<MODE, SMEM, 512>(a, n_items, smem, st);
+  }
+}
+
+// ---- streaming (L2-resident rows, bulk-copy staged windows) ----------------
+
+constexpr int kStreamT = 256, kStreamE = 4, kStreamSlots = 4;
+constexpr int kStreamCH = kStreamT * kStreamE;
+constexpr size_t kL2RowBudget = (size_t)56 << 20;  // live rows of co-resident instances
+
+size_t stream_smem(int mode) {
+  const size_t vb = value_bytes(mode);
+  const size_t stage = align_up(kStageTile * (sizeof(StageShift) + vb), 128);
+  return stage + 128 + (size_t)kStreamSlots * 4 * (kStreamCH + 16 / vb) * vb;
+}
+int64_t stream_span(int mode, const StreamGeom& g) {
+  const int64_t al = 16 / (int64_t)value_bytes(mode);
+  return (kStreamCH + al) + (int64_t)g.G * g.NC * kStreamCH + al;
+}
+size_t stream_row_bytes(int mode, const StreamGeom& g) {
+  return 4 * (size_t)stream_span(mode, g) * value_bytes(mode);
+}
+
+template <int MODE>
+int stream_occupancy() {
+  auto kern = dp_stream_kernel<MODE, kStreamT, kStreamE, kStreamSlots>;
+  int n = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(MODE)) !=
+          cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kStreamT, stream_smem(MODE)) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  return n > 0 ? n : 2;
+}
+
+// co-resident streaming CTAs on this device (cached per value domain)
+int stream_resident_ctas(int mode) {
+  static int cache[3] = {0, 0, 0};
+  if (!cache[mode]) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      sms = 148;
+    }
+    const int per_sm = mode == VM_INT32 ? stream_occupancy<VM_INT32>()
+                       : mode == VM_F64 ? stream_occupancy<VM_F64>()
+                                        : stream_occupancy<VM_F64_NAN>();
+    cache[mode] = sms * per_sm;
+  }
+  return cache[mode];
+}
+
+// Smallest cluster whose co-resident instances keep their rows within the L2
+// budget; the chunks are then spread evenly over it.
+StreamGeom stream_geom(int mode, int64_t ncol) {
+  const int64_t nchunks = (ncol + kStreamCH - 1) / kStreamCH;
+  const int resident = stream_resident_ctas(mode);
+  const int force = env_int("SPLITPLAN_DP_CLUSTER", 0);
+  StreamGeom g{16, 1};
+  for (int G = 1; G <= 16; ++G) {
+    StreamGeom t{G, (int)((nchunks + G - 1) / G)};
+    if (force ? G == force : (size_t)(resident / G) * stream_row_bytes(mode, t) <= kL2RowBudget) {
+      g = t;
+      break;
+    }
+  }
+  g.NC = (int)((nchunks + g.G - 1) / g.G);
+  g.G = (int)((nchunks + g.NC - 1) / g.NC);
+  return g;
+}
+
+template <int MODE>
+int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
+  auto kern = dp_stream_kernel<MODE, kStreamT, kStreamE, kStreamSlots>;
+  const size_t smem = stream_smem(MODE);
+  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                      "cudaFuncSetAttribute(dp_stream_kernel)");
+  if (rc) return rc;
+  if (geo.G > 8) {
+    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                    "cudaFuncSetAttribute(non-portable cluster)");
+    if (rc) return rc;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_items * geo.G), 1, 1);
+  cfg.blockDim = dim3((unsigned)kStreamT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)geo.G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, a, geo), "dp_stream_kernel launch");
+  if (rc) return rc;
+  return launch_check("dp_stream_kernel launch");
+}
+
+// ---- cluster (DSMEM rows) and cooperative (L2 rows, LDG) kernels ------------
 
 template <int MODE>
 int launch_cluster(const DpArgs& a, int64_t n_items, int threads, size_t smem, ClusterGeom geo,
@@ -1073,8 +1401,6 @@ int launch_cluster(const DpArgs& a, int64_t n_items, int threads, size_t smem, C
   return launch_check("dp_cluster_kernel launch");
 }
 
-enum DpVariant { DPV_SMEM = 0, DPV_CLUSTER = 1, DPV_GLOBAL = 2, DPV_COOP = 3 };
-
 template <int MODE>
 int launch_coop(const DpArgs& a, int64_t n_items, int threads, size_t smem, ClusterGeom geo,
                 cudaStream_t st) {
@@ -1105,7 +1431,7 @@ int launch_coop(const DpArgs& a, int64_t n_items, int threads, size_t smem, Clus
 // cooperative geometry: enough CTAs per instance that the double-buffered
 // rows of every co-resident instance fit comfortably in L2
 ClusterGeom coop_geom(int mode, int64_t ncol) {
-  const size_t vb = mode == VM_INT32 ? 4 : 8;
+  const size_t vb = value_bytes(mode);
   const size_t l2_budget = (size_t)48 << 20;
   const int resident_ctas = 148 * 2;
   int G = 2;
@@ -1128,42 +1454,13 @@ int coop_threads(const ClusterGeom& geo) {
 }
 
 size_t coop_row_bytes(int mode, int64_t ncol, const ClusterGeom& geo) {
-  const size_t vb = mode == VM_INT32 ? 4 : 8;
-  return 4 * (size_t)(kCellsPerThread * coop_threads(geo) + ncol) * vb;
-}
-
-int launch_dp_group(int mode, int variant, const DpArgs& a, int64_t n_items, int threads,
-                    size_t smem, ClusterGeom geo, cudaStream_t st) {
-  if (n_items == 0) return SP_OK;
-  if (variant == DPV_COOP) {
-    switch (mode) {
-      case VM_INT32: return launch_coop<VM_INT32>(a, n_items, threads, smem, geo, st);
-      case VM_F64: return launch_coop<VM_F64>(a, n_items, threads, smem, geo, st);
-      default: return launch_coop<VM_F64_NAN>(a, n_items, threads, smem, geo, st);
-    }
-  }
-  if (variant == DPV_CLUSTER) {
-    switch (mode) {
-      case VM_INT32: return launch_cluster<VM_INT32>(a, n_items, threads, smem, geo, st);
-      case VM_F64: return launch_cluster<VM_F64>(a, n_items, threads, smem, geo, st);
-      default: return launch_cluster<VM_F64_NAN>(a, n_items, threads, smem, geo, st);
-    }
-  }
-  const bool smem_rows = variant == DPV_SMEM;
-  switch (mode * 2 + (smem_rows ? 1 : 0)) {
-    case VM_INT32 * 2 + 1: return launch_dp<VM_INT32, true>(a, n_items, threads, smem, st);
-    case VM_INT32 * 2 + 0: return launch_dp<VM_INT32, false>(a, n_items, threads, smem, st);
-    case VM_F64 * 2 + 1: return launch_dp<VM_F64, true>(a, n_items, threads, smem, st);
-    case VM_F64 * 2 + 0: return launch_dp<VM_F64, false>(a, n_items, threads, smem, st);
-    case VM_F64_NAN * 2 + 1: return launch_dp<VM_F64_NAN, true>(a, n_items, threads, smem, st);
-    default: return launch_dp<VM_F64_NAN, false>(a, n_items, threads, smem, st);
-  }
+  return 4 * (size_t)(kCellsPerThread * coop_threads(geo) + ncol) * value_bytes(mode);
 }
 
 // cluster geometry for one instance, or G == 0 if the rows do not fit on chip
 ClusterGeom cluster_geom(int mode, int64_t ncol) {
   ClusterGeom geo{0, 0, 0};
-  const size_t vb = mode == VM_INT32 ? 4 : 8;
+  const size_t vb = value_bytes(mode);
   const size_t room = kSmemCap - stage_bytes_mode(mode) - 1024;  // 1 KB for static SMEM
   const size_t per_col = 4 * vb;  // 2 buffers x (C, S)
   int G = (int)((ncol * per_col + room - 1) / room);
@@ -1189,7 +1486,116 @@ int forced_variant() {
   if (!strcmp(v, "cluster")) return DPV_CLUSTER;
   if (!strcmp(v, "global")) return DPV_GLOBAL;
   if (!strcmp(v, "coop")) return DPV_COOP;
+  if (!strcmp(v, "stream")) return DPV_STREAM;
   return -1;
+}
+
+// Launch plan of one instance: kernel variant, its configuration, and the
+// workspace / shared memory it needs.
+struct DpPlan {
+  int variant = DPV_SMEM;
+  int cfg = 0;                  // single-CTA T x E configuration
+  int threads = 0;
+  ClusterGeom cgeo{0, 0, 0};    // cluster / coop
+  StreamGeom sgeo{0, 0};        // stream
+  size_t bp = 0, rows = 0, smem = 0;
+  int64_t bp_row_words = 0;
+  // launches sharing a key go out together
+  bool same_launch(const DpPlan& o) const {
+    return variant == o.variant && cfg == o.cfg && threads == o.threads && cgeo.G == o.cgeo.G &&
+           cgeo.B == o.cgeo.B && sgeo.G == o.sgeo.G && sgeo.NC == o.sgeo.NC;
+  }
+};
+
+DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) {
+  DpPlan p;
+  const size_t vb = value_bytes(mode);
+  p.cfg = single_cfg_for(ncol);
+  const size_t single_rows = single_row_bytes(mode, ncol, p.cfg);
+  const bool fits_cta = single_rows + stage_bytes_mode(mode) <= kSmemCap;
+  if (force == DPV_GLOBAL || (tables && force < 0)) p.variant = DPV_GLOBAL;
+  else if (force == DPV_SMEM && fits_cta) p.variant = DPV_SMEM;
+  else if (force == DPV_CLUSTER && cluster_geom(mode, ncol).G) p.variant = DPV_CLUSTER;
+  else if (force == DPV_COOP) p.variant = DPV_COOP;
+  else if (force == DPV_STREAM) p.variant = DPV_STREAM;
+  else if (fits_cta && force != DPV_CLUSTER) p.variant = DPV_SMEM;
+  else p.variant = DPV_STREAM;
+
+  switch (p.variant) {
+    case DPV_SMEM:
+    case DPV_GLOBAL:
+      p.threads = kSingleT[p.cfg];
+      p.bp_row_words = bp_row_words_for(mode, single_cols(p.cfg, ncol));
+      p.rows = p.variant == DPV_GLOBAL ? align_up(single_rows, 256) : 0;
+      p.smem = stage_bytes_mode(mode) + (p.variant == DPV_SMEM ? single_rows : 0);
+      break;
+    case DPV_STREAM:
+      p.sgeo = stream_geom(mode, ncol);
+      p.threads = kStreamT;
+      p.bp_row_words = bp_row_words_for(mode, (int64_t)p.sgeo.G * p.sgeo.NC * kStreamCH);
+      p.rows = align_up(stream_row_bytes(mode, p.sgeo), 256);
+      p.smem = stream_smem(mode);
+      break;
+    case DPV_COOP:
+      p.cgeo = coop_geom(mode, ncol);
+      p.threads = coop_threads(p.cgeo);
+      p.bp_row_words = bp_row_words_for(mode, ncol);
+      p.rows = align_up(coop_row_bytes(mode, ncol, p.cgeo), 256);
+      p.smem = stage_bytes_mode(mode);
+      break;
+    case DPV_CLUSTER:
+      p.cgeo = cluster_geom(mode, ncol);
+      p.threads = (int)std::min<int64_t>(kMaxThreads,
+                                         std::max<int64_t>(64, ((p.cgeo.B + 3) / 4 + 31) / 32 * 32));
+      p.bp_row_words = bp_row_words_for(mode, ncol);
+      p.smem = stage_bytes_mode(mode) + 4 * vb * (size_t)p.cgeo.B;
+      break;
+  }
+  p.bp = align_up((size_t)L * (size_t)p.bp_row_words * 4, 256);
+  return p;
+}
+
+int launch_plan(int mode, const DpPlan& p, const DpArgs& a, int64_t n_items, cudaStream_t st) {
+  if (n_items == 0) return SP_OK;
+  switch (p.variant) {
+    case DPV_STREAM:
+      switch (mode) {
+        case VM_INT32: return launch_stream<VM_INT32>(a, n_items, p.sgeo, st);
+        case VM_F64: return launch_stream<VM_F64>(a, n_items, p.sgeo, st);
+        default: return launch_stream<VM_F64_NAN>(a, n_items, p.sgeo, st);
+      }
+    case DPV_COOP:
+      switch (mode) {
+        case VM_INT32: return launch_coop<VM_INT32>(a, n_items, p.threads, p.smem, p.cgeo, st);
+        case VM_F64: return launch_coop<VM_F64>(a, n_items, p.threads, p.smem, p.cgeo, st);
+        default: return launch_coop<VM_F64_NAN>(a, n_items, p.threads, p.smem, p.cgeo, st);
+      }
+    case DPV_CLUSTER:
+      switch (mode) {
+        case VM_INT32: return launch_cluster<VM_INT32>(a, n_items, p.threads, p.smem, p.cgeo, st);
+        case VM_F64: return launch_cluster<VM_F64>(a, n_items, p.threads, p.smem, p.cgeo, st);
+        default: return launch_cluster<VM_F64_NAN>(a, n_items, p.threads, p.smem, p.cgeo, st);
+      }
+    default: {
+      const bool sm = p.variant == DPV_SMEM;
+      switch (mode * 2 + (sm ? 1 : 0)) {
+        case VM_INT32 * 2 + 1: return launch_single<VM_INT32, true>(a, n_items, p.cfg, p.smem, st);
+        case VM_INT32 * 2 + 0: return launch_single<VM_INT32, false>(a, n_items, p.cfg, p.smem, st);
+        case VM_F64 * 2 + 1: return launch_single<VM_F64, true>(a, n_items, p.cfg, p.smem, st);
+        case VM_F64 * 2 + 0: return launch_single<VM_F64, false>(a, n_items, p.cfg, p.smem, st);
+        case VM_F64_NAN * 2 + 1: return launch_single<VM_F64_NAN, true>(a, n_items, p.cfg, p.smem, st);
+        default: return launch_single<VM_F64_NAN, false>(a, n_items, p.cfg, p.smem, st);
+      }
+    }
+  }
+}
+
+// algorithmic HBM bytes per DP cell of a variant: rows on chip or in L2 ->
+// the packed back-pointer bits only; global rows of the single-CTA kernel ->
+// read + write of both rows plus those bits
+double hbm_bytes_per_cell(int mode, int variant) {
+  const double bits = bp_words(mode) * 4.0 / 32.0;
+  return variant == DPV_GLOBAL ? 4.0 * (double)value_bytes(mode) + bits : bits;
 }
 
 // Shared driver of sp_plan_dp and sp_build_dp_tables.
@@ -1228,20 +1634,17 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
 
   const size_t avail = ws_bytes - fixed;
   uint8_t* dyn = (uint8_t*)ws + fixed;
+  const int force = forced_variant();
   struct Item {
     int64_t inst, L, ncol;
-    int mode, variant;
-    ClusterGeom geo;
-    size_t bp, rows;
+    int mode;
+    DpPlan plan;
   };
-  const int force = forced_variant();
   std::vector<Item> items;
   items.reserve(n);
-  ClusterGeom geo_cache{0, 0, 0};
-  const char* pv = getenv("SPLITPLAN_DP_PREFER");
-  const bool prefer_coop = !(pv && !strcmp(pv, "cluster"));
-  int geo_mode = -1;
-  int64_t geo_ncol = -1;
+  DpPlan cached;
+  int cached_mode = -1;
+  int64_t cached_ncol = -1, cached_L = -1;
   for (int64_t k = 0; k < n; ++k) {
     const int64_t ncol = hinfo[k].w_eff + 1;
     if (ncol > kMaxCols) {
@@ -1254,27 +1657,13 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     it.L = hoff[k + 1] - hoff[k];
     it.ncol = ncol;
     it.mode = hinfo[k].mode;
-    const size_t rb = row_bytes_mode(it.mode, ncol);
-    const bool fits_cta = rb + stage_bytes_mode(it.mode) <= kSmemCap;
-    if (it.mode != geo_mode || ncol != geo_ncol) {
-      geo_cache = cluster_geom(it.mode, ncol);
-      geo_mode = it.mode;
-      geo_ncol = ncol;
+    if (it.mode != cached_mode || ncol != cached_ncol || it.L != cached_L) {
+      cached = plan_instance(it.mode, it.L, ncol, force, tab_c != nullptr);
+      cached_mode = it.mode;
+      cached_ncol = ncol;
+      cached_L = it.L;
     }
-    it.geo = geo_cache;
-    if (force == DPV_GLOBAL || (tab_c && force < 0)) it.variant = DPV_GLOBAL;
-    else if (force == DPV_CLUSTER && it.geo.G) it.variant = DPV_CLUSTER;
-    else if (force == DPV_COOP) it.variant = DPV_COOP;
-    else if (fits_cta && force != DPV_CLUSTER) it.variant = DPV_SMEM;
-    else if (prefer_coop && ncol > kCoopMinCols) it.variant = DPV_COOP;
-    else if (it.geo.G) it.variant = DPV_CLUSTER;
-    else it.variant = DPV_COOP;
-    if (it.variant == DPV_SMEM && !fits_cta) it.variant = DPV_GLOBAL;
-    if (it.variant == DPV_COOP) it.geo = coop_geom(it.mode, ncol);
-    it.bp = align_up(bp_bytes(it.mode, it.L, ncol), 256);
-    it.rows = it.variant == DPV_GLOBAL  ? align_up(rb, 256)
-              : it.variant == DPV_COOP ? align_up(coop_row_bytes(it.mode, ncol, it.geo), 256)
-                                       : 0;
+    it.plan = cached;
     items.push_back(it);
   }
 
@@ -1290,78 +1679,56 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   a.tab_c = tab_c;
   a.tab_s = tab_s;
 
-  size_t wave_bytes = 0;
   size_t pos = 0;
   std::vector<DpWork> hwork;
+  struct Group {
+    int mode;
+    DpPlan plan;
+    double cells = 0;
+    std::vector<DpWork> items;
+  };
+  std::vector<Group> groups;
   while (pos < items.size()) {
-    // gather one wave
-    size_t end = pos;
-    wave_bytes = 0;
-    while (end < items.size() && wave_bytes + items[end].bp + items[end].rows <= avail) {
-      wave_bytes += items[end].bp + items[end].rows;
+    // gather one wave that fits the workspace
+    size_t end = pos, wave_bytes = 0;
+    while (end < items.size() && wave_bytes + items[end].plan.bp + items[end].plan.rows <= avail) {
+      wave_bytes += items[end].plan.bp + items[end].plan.rows;
       ++end;
     }
     if (end == pos) {
-      set_required_workspace(fixed + items[pos].bp + items[pos].rows);
+      set_required_workspace(fixed + items[pos].plan.bp + items[pos].plan.rows);
       set_error(SP_ERR_WORKSPACE, "instance %lld needs %zu B of DP workspace, %zu B available",
-                (long long)items[pos].inst, items[pos].bp + items[pos].rows, avail);
+                (long long)items[pos].inst, items[pos].plan.bp + items[pos].plan.rows, avail);
       return SP_ERR_WORKSPACE;
     }
-    // lay out the wave: back-pointers then global rows; group work items by kernel variant
+    // lay out the wave (back-pointers, then global rows) grouped by launch
     hwork.clear();
+    groups.clear();
     size_t off = 0;
-    struct Group {
-      int mode, variant, threads = 0;
-      ClusterGeom geo{0, 0, 0};
-      size_t smem = 0;
-      double cells = 0;
-      std::vector<DpWork> items;
-    };
-    std::vector<Group> groups;
     for (size_t q = pos; q < end; ++q) {
       const Item& it = items[q];
       DpWork w;
       w.inst = it.inst;
       w.bp_off = (int64_t)off;
-      off += it.bp;
-      if (it.rows) {
+      w.bp_row_words = it.plan.bp_row_words;
+      off += it.plan.bp;
+      if (it.plan.rows) {
         w.row_off = (int64_t)off;
-        off += it.rows;
+        off += it.plan.rows;
       } else {
         w.row_off = -1;
       }
       Group* g = nullptr;
-      // single-CTA kernels size their row padding by blockDim, so a group
-      // shares one thread count; cluster / cooperative groups share a geometry
-      const bool multi = it.variant == DPV_CLUSTER || it.variant == DPV_COOP;
-      const int want_t = it.variant == DPV_CLUSTER ? 0
-                         : it.variant == DPV_COOP  ? coop_threads(it.geo)
-                                                   : threads_for(it.ncol);
       for (Group& c : groups)
-        if (c.mode == it.mode && c.variant == it.variant &&
-            (multi ? (c.geo.G == it.geo.G && c.geo.B == it.geo.B) : c.threads == want_t))
-          g = &c;
+        if (c.mode == it.mode && c.plan.same_launch(it.plan)) g = &c;
       if (!g) {
-        groups.push_back(Group{it.mode, it.variant});
+        groups.push_back(Group{it.mode, it.plan});
         g = &groups.back();
-        g->geo = it.geo;
-        g->threads = want_t;
       }
+      g->plan.smem = std::max(g->plan.smem, it.plan.smem);
       g->items.push_back(w);
       g->cells += (double)it.L * (double)it.ncol;
-      const size_t vb = it.mode == VM_INT32 ? 4 : 8;
-      if (it.variant == DPV_CLUSTER) {
-        const int t = (int)std::min<int64_t>(kMaxThreads, std::max<int64_t>(64, ((it.geo.B + 3) / 4 + 31) / 32 * 32));
-        g->threads = std::max(g->threads, t);
-        g->smem = stage_bytes_mode(it.mode) + 4 * vb * (size_t)it.geo.B;
-      } else {
-        const size_t need = stage_bytes_mode(it.mode) +
-                            (it.variant == DPV_SMEM ? row_bytes_mode(it.mode, it.ncol) : 0);
-        g->smem = std::max(g->smem, need);
-      }
     }
-    // row buffers of multi-CTA / global variants must hold the group's padding
-    // (same thread count across the group, so row_bytes already agree)
     for (const Group& g : groups)
       for (const DpWork& w : g.items) hwork.push_back(w);
     rc = check_cuda(cudaMemcpyAsync(work, hwork.data(), sizeof(DpWork) * hwork.size(),
@@ -1379,17 +1746,12 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
       }
-      rc = launch_dp_group(g.mode, g.variant, ga, cnt, g.threads, g.smem, g.geo, st);
+      rc = launch_plan(g.mode, g.plan, ga, cnt, st);
       if (rc) return rc;
       if (profiling()) {
         cudaEventRecord(e1, st);
-        // algorithmic HBM bytes per cell: rows on chip (SMEM / cluster DSMEM)
-        // -> the packed back-pointer bits only; global rows -> read + write of
-        // both rows plus those bits
-        const double vb = g.mode == VM_INT32 ? 4.0 : 8.0;
-        const double bits = bp_words(g.mode) * 4.0 / 32.0;
-        const double per_cell = g.variant == DPV_GLOBAL ? 4.0 * vb + bits : bits;  // coop: rows live in L2
-        prof_record_dp(e0, e1, g.cells, g.cells * per_cell, g.variant);
+        prof_record_dp(e0, e1, g.cells, g.cells * hbm_bytes_per_cell(g.mode, g.plan.variant),
+                       g.plan.variant);
       }
       first += cnt;
     }

@@ -87,7 +87,7 @@ def test_dp_tables_match_reference(gpu):
         pos += cnt
 
 
-@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop"])
+@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop", "stream"])
 def test_dp_tables_every_variant(gpu, variant, monkeypatch):
     """Full tables from each K2 variant equal the reference's build_dp_tables."""
     from paper_2410_10759_b200 import planner as P
@@ -180,7 +180,7 @@ def test_dp_vs_oracle_smem_and_global_rows(gpu, r_kind):
         assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{r_kind}[{k}]")
 
 
-@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop"])
+@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop", "stream"])
 @pytest.mark.parametrize("name", ["battery_wide", "battery_float", "battery_large_model"])
 def test_dp_kernel_variants_agree(gpu, variant, name, monkeypatch):
     """Every K2 variant (rows in one CTA's SMEM, in cluster DSMEM, in global
@@ -192,6 +192,28 @@ def test_dp_kernel_variants_agree(gpu, variant, name, monkeypatch):
     monkeypatch.setenv("SPLITPLAN_DP_VARIANT", variant)
     bat = Battery(name)
     _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
+
+
+@pytest.mark.parametrize("threads", ["64", "128", "256", "512"])
+def test_single_cta_thread_configs(gpu, threads, monkeypatch):
+    """Every T x E instantiation of the single-CTA kernel (SMEM and global rows)."""
+    from paper_2410_10759_b200 import batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_THREADS", threads)
+    for variant in ("smem", "global"):
+        monkeypatch.setenv("SPLITPLAN_DP_VARIANT", variant)
+        bat = Battery("battery_float")
+        _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
+
+
+@pytest.mark.parametrize("cluster", ["1", "3", "16"])
+def test_stream_cluster_sizes(gpu, cluster, monkeypatch):
+    """The streaming kernel at forced cluster sizes (1 CTA, odd, the non-portable 16)."""
+    from paper_2410_10759_b200 import batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "stream")
+    monkeypatch.setenv("SPLITPLAN_DP_CLUSTER", cluster)
+    for name in ("battery_wide", "battery_large_model"):
+        bat = Battery(name)
+        _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
 
 
 @pytest.mark.parametrize("name", ["battery_large_model", "battery_large_chain"])
