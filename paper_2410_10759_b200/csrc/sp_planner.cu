@@ -672,16 +672,24 @@ __global__ void __launch_bounds__(kStageThreads, 2) dp_coop_kernel(DpArgs a, Clu
 // ---------------------------------------------------------------------------
 // K2 streaming variant (rows longer than one SM's shared memory): a cluster
 // of G CTAs shares one instance, CTA q owning NC chunks of CH = T*E columns.
-// The rows live in global memory, double-buffered, sized so that the rows of
-// every co-resident instance stay in L2.  For each chunk the four predecessor
-// windows (C at i, S at i+d, S at s, C at s+u; CH + 16 B each, 16-B aligned)
-// are fetched by the bulk-copy engine (cp.async.bulk, completion on an
-// mbarrier) into an NSLOT-deep ring of shared-memory slots, issued NSLOT
-// chunks ahead by one thread; the compute then reads them with conflict-free
-// LDS exactly like the single-CTA kernel and stores the new cells straight to
-// the next row buffer (coalesced 128-B warp stores).  One cluster barrier
-// (release/acquire) per stage publishes the row; a proxy fence orders the
-// generic stores before the next stage's async-proxy reads.
+// The rows live in global memory, TRIPLE-buffered, sized so the rows of every
+// co-resident instance stay in L2.  Each CTA is warp-specialised:
+//   * one producer warp fetches, for every chunk, the four predecessor windows
+//     (C at i, S at i+d, S at s, C at s+u; CH values + 128 B, 128-B aligned)
+//     with the bulk-copy engine (cp.async.bulk, completion on a `full`
+//     mbarrier) into an NSLOT-deep ring of shared-memory slots;
+//   * T compute threads read them with conflict-free LDS like the single-CTA
+//     kernel, store the new cells straight to the next row buffer (coalesced
+//     warp stores) and the back-pointer words with an L2 evict-first policy,
+//     and release the slot on its `empty` mbarrier.
+// Stages are ordered by per-CTA progress counters in shared memory, read by
+// the other CTAs of the cluster through DSMEM, instead of a cluster-wide
+// barrier: stage s reads row s-1 from buffer (s-1)%3 and writes row s to
+// buffer s%3, so the producer of CTA q may start stage s once every CTA at or
+// left of q finished stage s-1 (all reads go left: shifts are >= 0) and every
+// CTA finished stage s-2 (the last reader of the buffer stage s overwrites).
+// CTAs therefore run up to one stage apart and the bulk copies of the next
+// stage overlap the tail of the current one.
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
@@ -689,6 +697,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -713,30 +724,80 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ void named_barrier(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_cluster_relaxed(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.relaxed.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cluster_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cluster.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_cluster() {
+  asm volatile("fence.acq_rel.cluster;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_bp_words(uint32_t* p, uint32_t a, uint32_t b, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_bp_words(uint32_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a), "r"(b),
+               "r"(c), "r"(d), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+// warp-collective back-pointer emission with an L2 evict-first store
+template <int MODE>
+__device__ __forceinline__ void emit_bp_stream(uint32_t* words, CellFlags f, uint64_t pol) {
+  const uint32_t m0 = __ballot_sync(0xffffffffu, f.c_stay);
+  const uint32_t m1 = __ballot_sync(0xffffffffu, f.s_stay);
+  if (MODE == VM_F64_NAN) {
+    const uint32_t m2 = __ballot_sync(0xffffffffu, f.c_sw);
+    const uint32_t m3 = __ballot_sync(0xffffffffu, f.s_sw);
+    if ((threadIdx.x & 31) == 0) st_bp_words(words, m0, m1, m2, m3, pol);
+  } else {
+    if ((threadIdx.x & 31) == 0) st_bp_words(words, m0, m1, pol);
+  }
+}
 
 struct StreamGeom {
   int G;   // CTAs per instance (cluster size)
   int NC;  // chunks per CTA
 };
 
-// values of NEG padding in front of a streamed row (>= CH + one 16-B group,
-// a whole number of 16-B groups) and the full row span
+constexpr int kRowBufs = 3;
+
+// values of NEG padding in front of a streamed row: one chunk plus one 128-B
+// line, so every window start (>= -CH) rounded down to 16 B stays in the row
+// and every CTA block starts on a 128-B line
 template <typename V, int CH>
-__host__ __device__ constexpr int stream_pad() { return CH + 16 / (int)sizeof(V); }
+__host__ __device__ constexpr int stream_pad() { return CH + 128 / (int)sizeof(V); }
 
 template <int MODE, int T, int E, int NSLOT>
-__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 512 / T)) dp_stream_kernel(DpArgs a, StreamGeom geo) {
+__global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(DpArgs a, StreamGeom geo) {
   using V = typename VT<MODE>::T;
   constexpr int CH = T * E;
-  constexpr int AL = 16 / (int)sizeof(V);  // values per 16 B
-  constexpr int WIN = CH + AL;              // values per staged window
+  constexpr int AL = 16 / (int)sizeof(V);        // values per 16 B
+  constexpr int WIN = CH + AL;                    // values per staged window
   constexpr int PAD = stream_pad<V, CH>();
+  constexpr int LINE = 128 / (int)sizeof(V);      // values per 128-B line
+  constexpr int NWARP = T / 32;                   // compute warps
   extern __shared__ __align__(16) unsigned char smem[];
-  StageShift* st_sh = reinterpret_cast<StageShift*>(smem);
-  V* st_r = reinterpret_cast<V*>(smem + kStageTile * sizeof(StageShift));
-  const size_t stage_bytes = align_up(kStageTile * (sizeof(StageShift) + sizeof(V)), 128);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stage_bytes);
-  V* slots = reinterpret_cast<V*>(smem + stage_bytes + 128);  // [NSLOT][4][WIN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + NSLOT;
+  uint32_t* prog = reinterpret_cast<uint32_t*>(empty + NSLOT);  // stages this CTA completed
+  V* slots = reinterpret_cast<V*>(smem + 256);                    // [NSLOT][4][WIN]
 
   const int G = geo.G, NC = geo.NC;
   const int q = (int)cluster_rank();
@@ -747,25 +808,25 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : 512 / T)) dp_stream_kernel(
   const int ncol = (int)(a.info[inst].w_eff + 1);
   const double g = a.info[inst].scale;
   const bool sac = a.sac[inst] != 0;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int B = NC * CH;
   const int j0 = q * B;
-  const int64_t span = (int64_t)PAD + (int64_t)G * B + AL;
+  const int64_t span = (int64_t)PAD + (int64_t)G * B + LINE;
   const int64_t row_words = wk.bp_row_words;
   const V NEG = VT<MODE>::neg();
   const V ZERO = V(0);
-  V* base = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][PAD + G*B + AL]
+  V* base = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][PAD + G*B + LINE]
   auto row = [&](int buf, int rs) { return base + (int64_t)(buf * 2 + rs) * span + PAD; };
 
-  for (int buf = 0; buf < 2; ++buf) {
+  for (int buf = 0; buf < kRowBufs; ++buf) {
     V* Cb = row(buf, 0);
     V* Sb = row(buf, 1);
     if (q == 0)
-      for (int x = tid - PAD; x < 0; x += T) Cb[x] = Sb[x] = NEG;  // padding, never rewritten
+      for (int x = tid - PAD; x < 0; x += blockDim.x) Cb[x] = Sb[x] = NEG;  // never rewritten
     if (q == G - 1)
-      for (int x = G * B + tid; x < G * B + AL; x += T) Cb[x] = Sb[x] = NEG;
+      for (int x = G * B + tid; x < G * B + LINE; x += blockDim.x) Cb[x] = Sb[x] = NEG;
     if (buf == 0)
-      for (int j = j0 + tid; j < j0 + B; j += T) {
+      for (int j = j0 + tid; j < j0 + B; j += blockDim.x) {
         const bool valid = j < ncol;
         Cb[j] = (valid && sac) ? ZERO : NEG;
         Sb[j] = (valid && !sac) ? ZERO : NEG;
@@ -776,92 +837,123 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : 512 / T)) dp_stream_kernel(
       }
   }
   if (tid == 0) {
-    for (int b = 0; b < NSLOT; ++b) mbar_init(&bars[b], 1);
+    for (int b = 0; b < NSLOT; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], NWARP);
+    }
+    *prog = 0;
     fence_mbar_init();
   }
   fence_proxy_async_global();
-  uint32_t* bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off);
-  cluster_barrier();
+  __threadfence();
+  cluster_barrier();  // rows initialised, barriers and counters live in every CTA
 
-  uint32_t use = 0;  // slot uses so far (uniform across the CTA)
-  for (int k = 0; k < L; ++k) {
-    const int kt = k % kStageTile;
-    if (kt == 0) {
-      __syncthreads();
-      load_stage_tile<MODE>(a, lo, k, L, st_sh, st_r);
-      __syncthreads();
-    }
-    const StageShift sh = st_sh[kt];
-    const V rk = st_r[kt];
-    const int cur = k & 1;
-    const V* Cc = row(cur, 0);
-    const V* Sc = row(cur, 1);
-    V* Cn = row(cur ^ 1, 0);
-    V* Sn = row(cur ^ 1, 1);
-    uint32_t* bprow = bpw + (int64_t)k * row_words + warp * bp_words(MODE);
-
-    // window w of chunk c: first (16-B aligned) value and the in-window offset
-    auto issue = [&](int c, int slot) {
-      const int c0 = j0 + c * CH, ctop = c0 + CH;
-      const V* src[4] = {Cc, Sc, Sc, Cc};
-      const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
-      mbar_expect_tx(&bars[slot], 4u * WIN * sizeof(V));
+  if (warp == NWARP) {
+    // ---------------- producer warp ----------------
+    // lane o watches CTA o's progress counter (G <= 16 <= 32 lanes)
+    const uint32_t my_prog = lane < G ? cluster_addr(smem_addr(prog), (uint32_t)lane) : 0u;
+    {
+      uint32_t u = 0;
+      for (int k = 0; k < L; ++k) {  // stage s = k + 1
+        // every CTA <= q finished stage k (row k ready), every CTA finished k-1
+        const uint32_t need = lane < G ? (uint32_t)(lane <= q ? k : max(k - 1, 0)) : 0u;
+        while (!__all_sync(0xffffffffu, lane >= G || ld_cluster_relaxed(my_prog) >= need)) {
+        }
+        if (lane == 0) {
+          fence_acq_rel_cluster();
+          fence_proxy_async_global();
+          const StageShift sh = a.shifts[lo + k];
+          const V* Cc = row(k % kRowBufs, 0);
+          const V* Sc = row(k % kRowBufs, 1);
+          const V* src[4] = {Cc, Sc, Sc, Cc};
+          const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
+          for (int c = 0; c < NC; ++c, ++u) {
+            const int slot = (int)(u % NSLOT);
+            mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
+            const int c0 = j0 + c * CH, ctop = c0 + CH;
+            mbar_expect_tx(&full[slot], 4u * WIN * sizeof(V));
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const int start = c0 - min(shf[w], ctop);
-        const int al = start & ~(AL - 1);
-        bulk_g2s(slots + (slot * 4 + w) * WIN, src[w] + al, WIN * sizeof(V), &bars[slot]);
+            for (int w = 0; w < 4; ++w) {
+              const int start = c0 - min(shf[w], ctop);
+              bulk_g2s(slots + (slot * 4 + w) * WIN, src[w] + (start & ~(AL - 1)), WIN * sizeof(V),
+                       &full[slot]);
+            }
+          }
+        }
+        __syncwarp();
       }
-    };
-    if (tid == 0) {
-      fence_proxy_async_global();
-      for (int c = 0; c < min(NSLOT, NC); ++c) issue(c, (int)((use + c) % NSLOT));
     }
-    for (int c = 0; c < NC; ++c) {
-      const uint32_t u = use + c;
-      const int slot = (int)(u % NSLOT);
-      const int c0 = j0 + c * CH, ctop = c0 + CH;
-      const V* ws = slots + slot * 4 * WIN + tid;
-      const V* pca = ws + 0 * WIN + ((c0 - min(sh.i, ctop)) & (AL - 1));
-      const V* pcb = ws + 1 * WIN + ((c0 - min(sh.id, ctop)) & (AL - 1));
-      const V* psa = ws + 2 * WIN + ((c0 - min(sh.s, ctop)) & (AL - 1));
-      const V* psb = ws + 3 * WIN + ((c0 - min(sh.su, ctop)) & (AL - 1));
-      uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
-      mbar_wait(&bars[slot], (u / NSLOT) & 1);
-      V* qc = Cn + c0 + tid;
-      V* qs = Sn + c0 + tid;
-      V cn[E], sn[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int j = c0 + e * T + tid;
-        const CellFlags f = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk,
-                                                 j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su,
-                                                 cn[e], sn[e]);
-        emit_bp<MODE>(bpc + e * (T / 32) * bp_words(MODE), 0, 1, f, true);
-        qc[e * T] = cn[e];
-        qs[e * T] = sn[e];
-      }
-      if (a.tab_c) {
+  } else {
+    // ---------------- compute warps ----------------
+    const uint64_t pol = evict_first_policy();
+    uint32_t* bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off);
+    uint32_t u = 0;
+    for (int k = 0; k < L; ++k) {
+      const StageShift sh = a.shifts[lo + k];
+      const int64_t rbits = a.rv[lo + k];
+      const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
+      V* Cn = row((k + 1) % kRowBufs, 0);
+      V* Sn = row((k + 1) % kRowBufs, 1);
+      uint32_t* bprow = bpw + (int64_t)k * row_words + warp * bp_words(MODE);
+      for (int c = 0; c < NC; ++c, ++u) {
+        const int slot = (int)(u % NSLOT);
+        const int c0 = j0 + c * CH, ctop = c0 + CH;
+        const V* ws = slots + slot * 4 * WIN + tid;
+        const V* pca = ws + 0 * WIN + ((c0 - min(sh.i, ctop)) & (AL - 1));
+        const V* pcb = ws + 1 * WIN + ((c0 - min(sh.id, ctop)) & (AL - 1));
+        const V* psa = ws + 2 * WIN + ((c0 - min(sh.s, ctop)) & (AL - 1));
+        const V* psb = ws + 3 * WIN + ((c0 - min(sh.su, ctop)) & (AL - 1));
+        uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
+        mbar_wait(&full[slot], (u / NSLOT) & 1);
+        V cn[E], sn[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const int j = c0 + e * T + tid;
-          if (j < ncol) {
-            a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn[e], g);
-            a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn[e], g);
+          const CellFlags f = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk,
+                                                   j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su,
+                                                   cn[e], sn[e]);
+          emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f, pol);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done reading the slot
+        V* qc = Cn + c0 + tid;
+        V* qs = Sn + c0 + tid;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          qc[e * T] = cn[e];
+          qs[e * T] = sn[e];
+        }
+        if (a.tab_c) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int j = c0 + e * T + tid;
+            if (j < ncol) {
+              a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn[e], g);
+              a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn[e], g);
+            }
           }
         }
       }
-      __syncthreads();  // every thread is done reading this slot
-      if (tid == 0 && c + NSLOT < NC) issue(c + NSLOT, slot);
+      // publish row k+1 of this CTA's block
+      named_barrier(1, T);
+      if (tid == 0) {
+        fence_acq_rel_cluster();
+        fence_proxy_async_global();
+        st_cluster_release(prog, (uint32_t)(k + 1));
+      }
     }
-    use += NC;
-    fence_proxy_async_global();  // this stage's generic stores before the next stage's bulk reads
-    cluster_barrier();
   }
+  __syncthreads();
+  cluster_barrier();  // no CTA leaves while others may still read its counter
   if (tid == 0 && ncol - 1 >= j0 && ncol - 1 < j0 + B) {
-    a.info[inst].end_c = to_f64(row(L & 1, 0)[ncol - 1], g);
-    a.info[inst].end_s = to_f64(row(L & 1, 1)[ncol - 1], g);
+    a.info[inst].end_c = to_f64(row(L % kRowBufs, 0)[ncol - 1], g);
+    a.info[inst].end_s = to_f64(row(L % kRowBufs, 1)[ncol - 1], g);
   }
+  __syncthreads();
+  // the rows are dead: drop their L2 lines instead of writing them back
+  for (int buf = 0; buf < kRowBufs; ++buf)
+    for (int rs = 0; rs < 2; ++rs)
+      for (int x = tid * LINE; x < B; x += blockDim.x * LINE) discard_l2(row(buf, rs) + j0 + x);
 }
 
 // ---------------------------------------------------------------------------
@@ -1272,34 +1364,49 @@ int launch_single(const DpArgs& a, int64_t n_items, int cfg, size_t smem, cudaSt
 
 // ---- streaming (L2-resident rows, bulk-copy staged windows) ----------------
 
-constexpr int kStreamT = 256, kStreamE = 4, kStreamSlots = 4;
-constexpr int kStreamCH = kStreamT * kStreamE;
-constexpr size_t kL2RowBudget = (size_t)56 << 20;  // live rows of co-resident instances
+constexpr int kStreamE = 4, kStreamSlots = 4;
+
+// compute threads of the streaming kernel (128 or 256; SPLITPLAN_STREAM_T)
+int stream_threads() {
+  static int t = 0;
+  if (!t) t = env_int("SPLITPLAN_STREAM_T", 256) == 128 ? 128 : 256;
+  return t;
+}
+int64_t stream_ch() { return (int64_t)stream_threads() * kStreamE; }
+// live rows of co-resident instances kept in L2 (SPLITPLAN_L2_BUDGET_MB)
+size_t l2_row_budget() {
+  static size_t b = 0;
+  if (!b) b = (size_t)env_int("SPLITPLAN_L2_BUDGET_MB", 96) << 20;
+  return b;
+}
 
 size_t stream_smem(int mode) {
   const size_t vb = value_bytes(mode);
-  const size_t stage = align_up(kStageTile * (sizeof(StageShift) + vb), 128);
-  return stage + 128 + (size_t)kStreamSlots * 4 * (kStreamCH + 16 / vb) * vb;
+  return 256 + (size_t)kStreamSlots * 4 * (stream_ch() + 16 / vb) * vb;
 }
 int64_t stream_span(int mode, const StreamGeom& g) {
-  const int64_t al = 16 / (int64_t)value_bytes(mode);
-  return (kStreamCH + al) + (int64_t)g.G * g.NC * kStreamCH + al;
+  const int64_t line = 128 / (int64_t)value_bytes(mode);
+  return (stream_ch() + line) + (int64_t)g.G * g.NC * stream_ch() + line;
 }
 size_t stream_row_bytes(int mode, const StreamGeom& g) {
-  return 4 * (size_t)stream_span(mode, g) * value_bytes(mode);
+  return 2 * kRowBufs * (size_t)stream_span(mode, g) * value_bytes(mode);
 }
 
-template <int MODE>
-int stream_occupancy() {
-  auto kern = dp_stream_kernel<MODE, kStreamT, kStreamE, kStreamSlots>;
+template <int MODE, int T>
+int stream_occupancy_t() {
+  auto kern = dp_stream_kernel<MODE, T, kStreamE, kStreamSlots>;
   int n = 0;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(MODE)) !=
           cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kStreamT, stream_smem(MODE)) != cudaSuccess) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, T + 32, stream_smem(MODE)) != cudaSuccess) {
     cudaGetLastError();
     n = 0;
   }
   return n > 0 ? n : 2;
+}
+template <int MODE>
+int stream_occupancy() {
+  return stream_threads() == 128 ? stream_occupancy_t<MODE, 128>() : stream_occupancy_t<MODE, 256>();
 }
 
 // co-resident streaming CTAs on this device (cached per value domain)
@@ -1323,13 +1430,13 @@ int stream_resident_ctas(int mode) {
 // Smallest cluster whose co-resident instances keep their rows within the L2
 // budget; the chunks are then spread evenly over it.
 StreamGeom stream_geom(int mode, int64_t ncol) {
-  const int64_t nchunks = (ncol + kStreamCH - 1) / kStreamCH;
+  const int64_t nchunks = (ncol + stream_ch() - 1) / stream_ch();
   const int resident = stream_resident_ctas(mode);
   const int force = env_int("SPLITPLAN_DP_CLUSTER", 0);
   StreamGeom g{16, 1};
   for (int G = 1; G <= 16; ++G) {
     StreamGeom t{G, (int)((nchunks + G - 1) / G)};
-    if (force ? G == force : (size_t)(resident / G) * stream_row_bytes(mode, t) <= kL2RowBudget) {
+    if (force ? G == force : (size_t)(resident / G) * stream_row_bytes(mode, t) <= l2_row_budget()) {
       g = t;
       break;
     }
@@ -1339,9 +1446,9 @@ StreamGeom stream_geom(int mode, int64_t ncol) {
   return g;
 }
 
-template <int MODE>
-int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
-  auto kern = dp_stream_kernel<MODE, kStreamT, kStreamE, kStreamSlots>;
+template <int MODE, int T>
+int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
+  auto kern = dp_stream_kernel<MODE, T, kStreamE, kStreamSlots>;
   const size_t smem = stream_smem(MODE);
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "cudaFuncSetAttribute(dp_stream_kernel)");
@@ -1353,7 +1460,7 @@ int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(n_items * geo.G), 1, 1);
-  cfg.blockDim = dim3((unsigned)kStreamT, 1, 1);
+  cfg.blockDim = dim3((unsigned)(T + 32), 1, 1);  // + the producer warp
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1366,6 +1473,11 @@ int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t
   rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, a, geo), "dp_stream_kernel launch");
   if (rc) return rc;
   return launch_check("dp_stream_kernel launch");
+}
+template <int MODE>
+int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
+  return stream_threads() == 128 ? launch_stream_t<MODE, 128>(a, n_items, geo, st)
+                                 : launch_stream_t<MODE, 256>(a, n_items, geo, st);
 }
 
 // ---- cluster (DSMEM rows) and cooperative (L2 rows, LDG) kernels ------------
@@ -1531,8 +1643,8 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) 
       break;
     case DPV_STREAM:
       p.sgeo = stream_geom(mode, ncol);
-      p.threads = kStreamT;
-      p.bp_row_words = bp_row_words_for(mode, (int64_t)p.sgeo.G * p.sgeo.NC * kStreamCH);
+      p.threads = stream_threads();
+      p.bp_row_words = bp_row_words_for(mode, (int64_t)p.sgeo.G * p.sgeo.NC * stream_ch());
       p.rows = align_up(stream_row_bytes(mode, p.sgeo), 256);
       p.smem = stream_smem(mode);
       break;
