@@ -36,34 +36,16 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "DP cells/sec and solved scenarios/sec at 1/2/4/8 B200; % HBM roofline"
 L2_BYTES = 126 * 2 ** 20
-CLIENT_S, SERVER_S = 7.727, 0.0979
 
 
 # ---------------------------------------------------------------------------
 # workload
 
 
-def calibrated_rates():
-    from paper_2410_10759_b200 import cost_model as cm
-    ref = cm.build_preset("bert-12", 4096)
-    return (cm.calibrate(ref, 4096, CLIENT_S).flops_per_s,
-            cm.calibrate(ref, 4096, SERVER_S).flops_per_s)
-
-
-def cfg2_requests(n: int, seed: int, cfps: float, sfps: float) -> dict:
-    """Seeded cfg2 request parameters (host numpy arrays)."""
-    from paper_2410_10759_b200 import cost_model as cm
-    rng = np.random.default_rng(seed)
-    seq = rng.integers(128, 2049, n)
-    bw = np.exp(rng.uniform(math.log(3e7), math.log(1e9), n))
-    f = rng.uniform(0.05, 1.0, n)
-    spec = cm.build_preset("gpt2-24", 128)
-    flops = np.array([cm.model_flops(spec, int(s)) for s in seq], dtype=float)
-    deadline = f * flops / cfps
-    return dict(model=np.zeros(n, np.int32), seq_len=seq.astype(np.int64),
-                client_fps=np.full(n, cfps), server_fps=np.full(n, sfps), uplink_bps=bw,
-                downlink_bps=bw.copy(), propagation_s=np.full(n, 0.01), deadline_s=deadline,
-                unit_s=deadline / 1e5, flags=np.full(n, 2, np.uint8))  # source at client
+def cfg2_requests(n: int, seed: int) -> dict:
+    """Seeded cfg2 request parameters (host numpy arrays), workloads.cfg2."""
+    from paper_2410_10759_b200 import workloads as W
+    return W.cfg2(n, seed)[0]
 
 
 # ---------------------------------------------------------------------------
@@ -236,8 +218,7 @@ def main():
     from paper_2410_10759_b200 import cost_model as cm
     from paper_2410_10759_b200.requests import Engine, RequestBatch
 
-    cfps, sfps = calibrated_rates()
-    req_np = cfg2_requests(args.requests, args.seed * 1000 + rank, cfps, sfps)
+    req_np = cfg2_requests(args.requests, args.seed * 1000 + rank)
     n = args.requests
     L = len(cm.build_preset("gpt2-24", 128).layers)
     total_layers = n * L
@@ -404,8 +385,7 @@ def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
     from paper_2410_10759_b200 import cost_model as cm  # noqa: F401  (host-only import)
-    cfps, sfps = calibrated_rates()
-    req_np = cfg2_requests(args.requests, args.seed * 1000, cfps, sfps)
+    req_np = cfg2_requests(args.requests, args.seed * 1000)
     procs = max(1, min(os.cpu_count() or 1, 128))
     per = args.cpu_sample or max(8, 4 * procs)  # ~0.5 s of host work per step
     times, cells_tot = [], 0.0

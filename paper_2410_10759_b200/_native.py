@@ -179,6 +179,8 @@ def ptr(t) -> P:
 
 def to_dev(a, dtype, dev=None) -> torch.Tensor:
     dev = dev or device()
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype).contiguous()
     arr = np.ascontiguousarray(a)
     t = torch.from_numpy(arr)
     if t.dtype != dtype:

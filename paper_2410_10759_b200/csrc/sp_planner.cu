@@ -1376,7 +1376,7 @@ int64_t stream_ch() { return (int64_t)stream_threads() * kStreamE; }
 // live rows of co-resident instances kept in L2 (SPLITPLAN_L2_BUDGET_MB)
 size_t l2_row_budget() {
   static size_t b = 0;
-  if (!b) b = (size_t)env_int("SPLITPLAN_L2_BUDGET_MB", 96) << 20;
+  if (!b) b = (size_t)env_int("SPLITPLAN_L2_BUDGET_MB", 110) << 20;
   return b;
 }
 
@@ -1427,23 +1427,33 @@ int stream_resident_ctas(int mode) {
   return cache[mode];
 }
 
-// Smallest cluster whose co-resident instances keep their rows within the L2
-// budget; the chunks are then spread evenly over it.
+// Cluster size: at least large enough that the rows of every co-resident
+// instance fit the L2 budget; among those, the G minimising G * (NC + 2) --
+// the CTA-time of one stage in chunk units, padding waste included, plus
+// about two chunks of stage-synchronisation latency per CTA (measured on
+// B200: at W = 1e5, G = 7 x 14 chunks beats 8 x 13 and 14 x 7).
 StreamGeom stream_geom(int mode, int64_t ncol) {
   const int64_t nchunks = (ncol + stream_ch() - 1) / stream_ch();
   const int resident = stream_resident_ctas(mode);
   const int force = env_int("SPLITPLAN_DP_CLUSTER", 0);
-  StreamGeom g{16, 1};
-  for (int G = 1; G <= 16; ++G) {
+  auto geom = [&](int G) {
     StreamGeom t{G, (int)((nchunks + G - 1) / G)};
-    if (force ? G == force : (size_t)(resident / G) * stream_row_bytes(mode, t) <= l2_row_budget()) {
-      g = t;
+    t.G = (int)((nchunks + t.NC - 1) / t.NC);
+    return t;
+  };
+  if (force >= 1 && force <= 16) return geom(force);
+  int gmin = 16;
+  for (int G = 1; G <= 16; ++G)
+    if ((size_t)(resident / G) * stream_row_bytes(mode, geom(G)) <= l2_row_budget()) {
+      gmin = G;
       break;
     }
+  StreamGeom best = geom(gmin);
+  for (int G = gmin + 1; G <= 16; ++G) {
+    const StreamGeom t = geom(G);
+    if ((int64_t)t.G * (t.NC + 2) < (int64_t)best.G * (best.NC + 2)) best = t;
   }
-  g.NC = (int)((nchunks + g.G - 1) / g.G);
-  g.G = (int)((nchunks + g.NC - 1) / g.NC);
-  return g;
+  return best;
 }
 
 template <int MODE, int T>

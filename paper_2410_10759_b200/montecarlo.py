@@ -1,0 +1,188 @@
+"""Monte-Carlo scenario sweeps (BASELINE.json configs[3]).
+
+A scenario is a workload mix of independent requests under one SLA scale
+and one link bandwidth.  For every scenario the reference's own pipeline
+would run, per request, `build_problem` + `run_planner` for dp / greedy /
+all_server (`evaluator.py:172-208`), turn the results into a scenario table
+(`throughput_sim.scenarios_from_cells`, `throughput_sim.py:133-163`), size
+the server (`capacity_for_requests`, `:172-176`) and replay the three
+demand variants over one seeded arrival skeleton (`compare_variants`,
+`:264-272`).  Here the whole grid runs as three batched device passes:
+
+    K1 cost table + prep + K2 + K3   every request of every scenario (dp)
+    prefix kernel                    greedy and all_server on the same instances
+    K4 replay                        3 runs per scenario in one launch
+
+with the table bookkeeping (filter, coordinate sort, normalisation) and the
+numpy PCG64 skeletons on the host, exactly as the reference computes them.
+Scenarios are independent, so `run(..., group=...)` shards them over ranks
+and gathers the per-scenario records once at the end.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import batch as B
+from . import workloads as W
+from .requests import Engine, RequestBatch
+from .throughput_sim import VARIANTS, replay_arrays
+
+BETA_PER_MS = 0.057
+HORIZON = 2000
+OMEGA_REQUESTS = 500
+EXEC_MAX = 10
+
+
+@dataclass
+class MonteCarloResult:
+    scenario_ids: np.ndarray   # [S]
+    table_size: np.ndarray     # [S] scenario-table rows after the feasibility filter
+    capacity: np.ndarray       # [S]
+    max_wait_ms: np.ndarray    # [S, 3] dp, greedy, nosplit
+    mean_wait_ms: np.ndarray   # [S, 3]
+    status: np.ndarray         # [S, 3] SP_OK, SP_ERR_DEADLOCK, or -1 (empty table: not simulated)
+    requests: int              # requests planned
+    dp_cells: float            # DP cells solved
+
+
+def solve_requests(req: dict, layer_lists) -> dict:
+    """dp / greedy / all_server server loads and feasibility for every request."""
+    eng = Engine(layer_lists)
+    sol = eng.solve(RequestBatch.from_numpy(**req).to(N.device()))
+    out = {"dp": sol.policies}
+    out["greedy"] = B.plan_prefix(sol.instances, N.SP_GREEDY)
+    out["all_server"] = B.plan_prefix(sol.instances, N.SP_ALL_SERVER)
+    w_eff = B.effective_budget(sol.instances)
+    lens = (sol.layer_off[1:] - sol.layer_off[:-1]).to(torch.float64)
+    cells = float((lens * (w_eff + 1).to(torch.float64)).sum().item())
+    host = {k: dict(load=v.server_load.cpu().numpy(), ok=v.feasible.cpu().numpy().astype(bool))
+            for k, v in out.items()}
+    host["cells"] = cells
+    return host
+
+
+def scenario_tables(req: dict, off: np.ndarray, model_names, solved: dict):
+    """Per scenario, the reference's scenario table: coordinates whose dp,
+    greedy and all_server rows are feasible, sorted by (model, seq_len,
+    deadline, up, down), one row per coordinate, demands normalised by the
+    mean nosplit load (throughput_sim.py:133-163).
+
+    Returns CSR offsets over rows, the per-row demands [rows, 3] and deadlines."""
+    names = np.asarray(model_names, dtype=object)[req["model"]]
+    name_rank = np.unique(names, return_inverse=True)[1]
+    S = len(off) - 1
+    scen = np.repeat(np.arange(S), np.diff(off))
+    keep = solved["dp"]["ok"] & solved["greedy"]["ok"] & solved["all_server"]["ok"]
+    order = np.lexsort((req["downlink_bps"], req["uplink_bps"], req["deadline_s"], req["seq_len"],
+                        name_rank, scen))
+    order = order[keep[order]]
+    # identical coordinates collapse to one row (a dict keyed by coordinate)
+    key = np.stack([scen[order], name_rank[order], req["seq_len"][order]]).T
+    fkey = np.stack([req["deadline_s"][order], req["uplink_bps"][order],
+                     req["downlink_bps"][order]]).T
+    dup = np.zeros(order.size, dtype=bool)
+    if order.size > 1:
+        dup[1:] = np.all(key[1:] == key[:-1], axis=1) & np.all(fkey[1:] == fkey[:-1], axis=1)
+    order = order[~dup]
+    rows_scen = scen[order]
+    row_off = np.zeros(S + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows_scen, minlength=S), out=row_off[1:])
+    loads = np.stack([solved["dp"]["load"][order], solved["greedy"]["load"][order],
+                      solved["all_server"]["load"][order]], axis=1)
+    demand = np.empty_like(loads)
+    for s in range(S):
+        a, b = row_off[s], row_off[s + 1]
+        if a == b:
+            continue
+        norm = np.mean(loads[a:b, 2])  # throughput_sim.py:156, numpy order
+        demand[a:b] = loads[a:b] / norm
+    return row_off, demand, req["deadline_s"][order]
+
+
+def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORIZON,
+        omega_requests: float = OMEGA_REQUESTS, group=None) -> MonteCarloResult:
+    """The cfg4 sweep over `scenario_ids` (default: all 65,536), sharded over
+    the ranks of `group` when torch.distributed is initialised."""
+    import torch.distributed as dist
+    sids = np.arange(16 * 16 * W.CFG4_MIXES) if scenario_ids is None else np.asarray(scenario_ids)
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    if world > 1:
+        from .shard import shard_bounds
+        rank = dist.get_rank(group)
+        b = shard_bounds(len(sids), world)
+        local = run(sids[b[rank]:b[rank + 1]], beta_per_ms, horizon, omega_requests, group=None) \
+            if b[rank + 1] > b[rank] else None
+        return _gather(local, sids, b, group)
+
+    req, layer_lists, off = W.cfg4(sids)
+    solved = solve_requests(req, layer_lists)
+    row_off, demand, deadline_s = scenario_tables(req, off, W.CFG4_MODELS, solved)
+    S = len(sids)
+    sizes = np.diff(row_off)
+    capacity = np.zeros(S)
+    # skeletons (numpy PCG64, throughput_sim.py:179-186) and the three projected streams
+    arr_all, dem_all, dur_all, caps, run_len = [], [], [], [], []
+    for s in range(S):
+        a, b = row_off[s], row_off[s + 1]
+        if a == b:
+            continue
+        capacity[s] = float(omega_requests) * np.mean(demand[a:b, 2])  # :172-176
+        g = np.random.default_rng(int(sids[s]))
+        arrivals = np.cumsum(g.exponential(scale=1.0 / beta_per_ms, size=horizon))
+        idx = g.integers(0, b - a, size=horizon)
+        execs = g.integers(1, EXEC_MAX + 1, size=horizon)
+        dur = (deadline_s[a:b] * 1000.0)[idx] * execs
+        for v in range(3):
+            arr_all.append(arrivals)
+            dem_all.append(demand[a:b, v][idx])
+            dur_all.append(dur)
+            caps.append(capacity[s])
+            run_len.append(horizon)
+    max_w = np.zeros((S, 3))
+    mean_w = np.zeros((S, 3))
+    status = np.full((S, 3), -1, dtype=np.int32)
+    if run_len:
+        roff = np.zeros(len(run_len) + 1, dtype=np.int64)
+        np.cumsum(run_len, out=roff[1:])
+        o = replay_arrays(roff, np.concatenate(arr_all), np.concatenate(dem_all),
+                          np.concatenate(dur_all), np.asarray(caps))
+        sim = np.flatnonzero(sizes > 0)
+        nr = len(run_len)
+        max_w[sim] = o["mx"][:nr].cpu().numpy().reshape(-1, 3)
+        mean_w[sim] = o["mean"][:nr].cpu().numpy().reshape(-1, 3)
+        status[sim] = o["st"][:nr].cpu().numpy().reshape(-1, 3)
+    return MonteCarloResult(sids, sizes, capacity, max_w, mean_w, status, int(off[-1]),
+                            solved["cells"])
+
+
+def _gather(local, sids, bounds, group) -> MonteCarloResult:
+    """One all_gather of the fixed-size per-scenario records (scenario order)."""
+    import torch.distributed as dist
+    from .shard import _all_gather_padded
+    dev = N.device() if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    n_local = 0 if local is None else len(local.scenario_ids)
+    rec = torch.zeros((n_local, 12), dtype=torch.float64)
+    stats = torch.zeros(2, dtype=torch.float64)
+    if local is not None:
+        rec[:, 0] = torch.from_numpy(local.table_size.astype(np.float64))
+        rec[:, 1] = torch.from_numpy(local.capacity)
+        rec[:, 2:5] = torch.from_numpy(local.max_wait_ms)
+        rec[:, 5:8] = torch.from_numpy(local.mean_wait_ms)
+        rec[:, 8:11] = torch.from_numpy(local.status.astype(np.float64))
+        stats[0], stats[1] = local.requests, local.dp_cells
+    rows = [int(bounds[r + 1] - bounds[r]) for r in range(len(bounds) - 1)]
+    parts = _all_gather_padded(rec.to(dev), rows, group)
+    dist.all_reduce(stats_d := stats.to(dev), group=group)
+    allrec = torch.cat(parts).cpu().numpy()
+    st = stats_d.cpu().numpy()
+    return MonteCarloResult(np.asarray(sids), allrec[:, 0].astype(np.int64), allrec[:, 1],
+                            allrec[:, 2:5], allrec[:, 5:8], allrec[:, 8:11].astype(np.int32),
+                            int(st[0]), float(st[1]))
+
+
+__all__ = ["MonteCarloResult", "run", "solve_requests", "scenario_tables", "VARIANTS"]

@@ -186,29 +186,24 @@ def generate_stream(config: SimConfig) -> Stream:
 # replay on the GPU
 
 
-def replay_many(streams: Sequence[Stream], capacities: Sequence[float],
-                raise_on_deadlock: bool = True) -> list[SimResult | CapacityDeadlockError]:
-    """Replay independent (stream, capacity) runs in one K4 launch."""
+def replay_arrays(run_off, arrival_ms, demand, duration_ms, capacity) -> dict:
+    """K4 over independent runs given as CSR arrays (host numpy or device
+    tensors): run k replays requests [run_off[k], run_off[k+1]) against
+    capacity[k].  Returns the device outputs: admit / wait / cumulative wait
+    per request, max / mean wait, status and the deadlocked request per run."""
     dev = N.device()
-    lens = np.array([len(s.arrival_ms) for s in streams], dtype=np.int64)
-    off = np.zeros(len(streams) + 1, dtype=np.int64)
-    np.cumsum(lens, out=off[1:])
-    total = int(off[-1])
-    cat = lambda f: (np.concatenate([np.asarray(f(s), dtype=np.float64) for s in streams])
-                     if total else np.zeros(0))
-    t = dict(off=N.to_dev(off, torch.int64, dev), arr=N.to_dev(cat(lambda s: s.arrival_ms),
-                                                                 torch.float64, dev),
-             dem=N.to_dev(cat(lambda s: s.demand), torch.float64, dev),
-             dur=N.to_dev(cat(lambda s: s.duration_ms), torch.float64, dev),
-             cap=N.to_dev(np.asarray(capacities, dtype=np.float64), torch.float64, dev))
-    nr = len(streams)
+    t = dict(off=N.to_dev(run_off, torch.int64, dev), arr=N.to_dev(arrival_ms, torch.float64, dev),
+             dem=N.to_dev(demand, torch.float64, dev), dur=N.to_dev(duration_ms, torch.float64, dev),
+             cap=N.to_dev(capacity, torch.float64, dev))
+    nr = t["off"].numel() - 1
+    total = t["arr"].numel()
     o = dict(admit=torch.empty(max(total, 1), dtype=torch.float64, device=dev),
              wait=torch.empty(max(total, 1), dtype=torch.float64, device=dev),
              cum=torch.empty(max(total, 1), dtype=torch.float64, device=dev),
-             mx=torch.empty(nr, dtype=torch.float64, device=dev),
-             mean=torch.empty(nr, dtype=torch.float64, device=dev),
-             st=torch.zeros(nr, dtype=torch.int32, device=dev),
-             dead=torch.empty(nr, dtype=torch.int64, device=dev))
+             mx=torch.empty(max(nr, 1), dtype=torch.float64, device=dev),
+             mean=torch.empty(max(nr, 1), dtype=torch.float64, device=dev),
+             st=torch.zeros(max(nr, 1), dtype=torch.int32, device=dev),
+             dead=torch.empty(max(nr, 1), dtype=torch.int64, device=dev))
     b = N.SpSimBatch(nr, total, *[N.ptr(t[k]).value for k in ("off", "arr", "dem", "dur", "cap")])
     so = N.SpSimOut(*[N.ptr(o[k]).value for k in ("admit", "wait", "cum", "mx", "mean", "st",
                                                    "dead")])
@@ -216,6 +211,20 @@ def replay_many(streams: Sequence[Stream], capacities: Sequence[float],
     need = int(lib.sp_sim_workspace_bytes(b))
     ws = N.workspace(need)
     N.check(lib.sp_sim_replay(b, so, N.ptr(ws), ws.numel(), N.stream_ptr()), "sp_sim_replay")
+    return o
+
+
+def replay_many(streams: Sequence[Stream], capacities: Sequence[float],
+                raise_on_deadlock: bool = True) -> list[SimResult | CapacityDeadlockError]:
+    """Replay independent (stream, capacity) runs in one K4 launch."""
+    lens = np.array([len(s.arrival_ms) for s in streams], dtype=np.int64)
+    off = np.zeros(len(streams) + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    total = int(off[-1])
+    cat = lambda f: (np.concatenate([np.asarray(f(s), dtype=np.float64) for s in streams])
+                     if total else np.zeros(0))
+    o = replay_arrays(off, cat(lambda s: s.arrival_ms), cat(lambda s: s.demand),
+                      cat(lambda s: s.duration_ms), np.asarray(capacities, dtype=np.float64))
     h = {k: v.cpu().numpy() for k, v in o.items()}
     out = []
     for r, s in enumerate(streams):

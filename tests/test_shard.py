@@ -99,3 +99,43 @@ def test_shard_by_cost_balances_cells():
         assert per.max() - per.min() <= 2 * cost.max()
     assert list(shard_by_cost([], 4)) == [0, 0, 0, 0, 0]
     assert list(shard_by_cost([0, 0, 0], 2)) in ([0, 1, 3], [0, 2, 3], [0, 3, 3], [0, 0, 3])
+
+
+def _mc_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2410_10759_b200.montecarlo import MonteCarloResult, _gather
+        sids = np.arange(10)
+        b = shard_bounds(len(sids), world)
+
+        def fake(lo, hi):
+            n = hi - lo
+            s = np.arange(lo, hi, dtype=np.float64)
+            return MonteCarloResult(sids[lo:hi], np.arange(lo, hi), s * 2.0,
+                                    np.stack([s, s + 1, s + 2], 1), np.stack([s / 3, s / 5, s / 7], 1),
+                                    np.zeros((n, 3), np.int32), 64 * n, 1e6 * n)
+        got = _gather(fake(b[rank], b[rank + 1]), sids, b, None)
+        exp = fake(0, 10)
+        ok = (np.array_equal(got.table_size, exp.table_size) and np.array_equal(got.capacity, exp.capacity)
+              and np.array_equal(got.max_wait_ms, exp.max_wait_ms)
+              and np.array_equal(got.mean_wait_ms, exp.mean_wait_ms)
+              and got.requests == exp.requests and got.dp_cells == exp.dp_cells)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_montecarlo_gather_gloo_world2():
+    """Per-scenario records of a sharded Monte-Carlo sweep reassemble in scenario order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert results == {0: True, 1: True}
