@@ -957,6 +957,293 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
 }
 
 // ---------------------------------------------------------------------------
+// K2 grid variant: ONE very large instance (L = 1e5 stages x
+// W = 1e7 columns) spread over every co-resident CTA of the GPU (cooperative
+// launch).  Same producer-warp / bulk-copy / mbarrier-ring structure as the
+// streaming kernel, but the per-CTA progress counters live in global memory
+// and each producer waits only on the CTAs that own its windows: the owners
+// of columns [j0 - max_shift - 16 B, j0 + B) for the rows it reads (RAW) and
+// the CTAs that read its block two stages earlier (WAR on the triple-
+// buffered rows).  With small per-stage shifts that is just the two
+// neighbours, so the GPU runs as a wavefront with no grid-wide barrier.
+// A launch advances a range of stages [k_begin, k_begin + k_count) from an
+// initial row (the origin row or a checkpoint) and can write the final row
+// (a checkpoint) and the range's back-pointers; the host chains launches
+// into checkpoint / recompute passes when the full back-pointer table does
+// not fit in memory.
+
+struct GridArgs {
+  const StageShift* shifts;  // stage records of the instance (index = stage)
+  const int64_t* rv;         // stage values in the value domain
+  int k_begin, k_count;      // stage range of this launch
+  int ncol;                  // W_eff + 1
+  int G, NC;                 // CTAs, chunks per CTA
+  int sac;
+  const void* init_c;        // row k_begin, ncol values each, or null: origin row
+  const void* init_s;
+  void* out_c;               // row k_begin + k_count, or null
+  void* out_s;
+  uint8_t* rows;             // [3][C|S][PAD + G*B + LINE]
+  uint32_t* bp;              // back-pointers of the range's stages, or null
+  int64_t bp_row_words;
+  uint32_t* prog;            // [G] stages completed in this launch (zeroed)
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int max_shift(const StageShift& sh) {
+  return max(max(sh.i, sh.id), max(sh.s, sh.su));
+}
+
+template <int MODE, int T, int E, int NSLOT>
+__global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
+  using V = typename VT<MODE>::T;
+  constexpr int CH = T * E;
+  constexpr int AL = 16 / (int)sizeof(V);
+  constexpr int WIN = CH + AL;
+  constexpr int PAD = stream_pad<V, CH>();
+  constexpr int LINE = 128 / (int)sizeof(V);
+  constexpr int NWARP = T / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + NSLOT;
+  V* slots = reinterpret_cast<V*>(smem + 256);
+
+  const int G = a.G, NC = a.NC;
+  const int q = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int B = NC * CH;
+  const int j0 = q * B;
+  const int ncol = a.ncol;
+  const int64_t span = (int64_t)PAD + (int64_t)G * B + LINE;
+  const V NEG = VT<MODE>::neg();
+  const V ZERO = V(0);
+  V* base = reinterpret_cast<V*>(a.rows);
+  auto row = [&](int buf, int rs) { return base + (int64_t)(buf * 2 + rs) * span + PAD; };
+  auto owner = [&](int x) { return min(G - 1, max(0, x) / B); };
+
+  for (int buf = 0; buf < kRowBufs; ++buf) {
+    V* Cb = row(buf, 0);
+    V* Sb = row(buf, 1);
+    if (q == 0)
+      for (int x = tid - PAD; x < 0; x += blockDim.x) Cb[x] = Sb[x] = NEG;
+    if (q == G - 1)
+      for (int x = G * B + tid; x < G * B + LINE; x += blockDim.x) Cb[x] = Sb[x] = NEG;
+    if (buf == 0) {
+      const V* ic = reinterpret_cast<const V*>(a.init_c);
+      const V* is = reinterpret_cast<const V*>(a.init_s);
+      for (int j = j0 + tid; j < j0 + B; j += blockDim.x) {
+        const bool valid = j < ncol;
+        if (ic) {
+          Cb[j] = valid ? ic[j] : NEG;
+          Sb[j] = valid ? is[j] : NEG;
+        } else {
+          Cb[j] = (valid && a.sac) ? ZERO : NEG;
+          Sb[j] = (valid && !a.sac) ? ZERO : NEG;
+        }
+      }
+    }
+  }
+  if (tid == 0) {
+    for (int b = 0; b < NSLOT; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], NWARP);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    fence_proxy_async_global();
+    st_release_gpu(&a.prog[q], 1u);  // rows initialised (counter = completed stages + 1)
+  }
+
+  if (warp == NWARP) {
+    // ---------------- producer warp ----------------
+    uint32_t u = 0;
+    for (int t = 0; t < a.k_count; ++t) {
+      const int k = a.k_begin + t;
+      const StageShift sh = a.shifts[k];
+      // RAW: owners of the windows read this stage (row t complete => counter >= t + 1)
+      const int lo_o = owner(j0 - max_shift(sh) - AL);
+      // WAR: CTAs that read this block's target buffer two stages ago
+      int hi_o = q;
+      if (t >= 2) hi_o = owner(j0 + B - 1 + max_shift(a.shifts[k - 2]) + CH + AL);
+      for (int o0 = lo_o; o0 <= hi_o; o0 += 32) {
+        const int o = o0 + lane;
+        const uint32_t need = o <= q ? (uint32_t)(t + 1) : (uint32_t)max(t - 1, 0) + 1u;
+        while (!__all_sync(0xffffffffu, o > hi_o || ld_acquire_gpu(&a.prog[o]) >= need)) {
+        }
+      }
+      if (lane == 0) {
+        fence_proxy_async_global();
+        const V* Cc = row(t % kRowBufs, 0);
+        const V* Sc = row(t % kRowBufs, 1);
+        const V* src[4] = {Cc, Sc, Sc, Cc};
+        const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
+        for (int c = 0; c < NC; ++c, ++u) {
+          const int slot = (int)(u % NSLOT);
+          mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
+          const int c0 = j0 + c * CH, ctop = c0 + CH;
+          mbar_expect_tx(&full[slot], 4u * WIN * sizeof(V));
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int start = c0 - min(shf[w], ctop);
+            bulk_g2s(slots + (slot * 4 + w) * WIN, src[w] + (start & ~(AL - 1)), WIN * sizeof(V),
+                     &full[slot]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- compute warps ----------------
+    const uint64_t pol = evict_first_policy();
+    uint32_t u = 0;
+    for (int t = 0; t < a.k_count; ++t) {
+      const int k = a.k_begin + t;
+      const StageShift sh = a.shifts[k];
+      const int64_t rbits = a.rv[k];
+      const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
+      V* Cn = row((t + 1) % kRowBufs, 0);
+      V* Sn = row((t + 1) % kRowBufs, 1);
+      uint32_t* bprow = a.bp ? a.bp + (int64_t)t * a.bp_row_words + warp * bp_words(MODE) : nullptr;
+      for (int c = 0; c < NC; ++c, ++u) {
+        const int slot = (int)(u % NSLOT);
+        const int c0 = j0 + c * CH, ctop = c0 + CH;
+        const V* ws = slots + slot * 4 * WIN + tid;
+        const V* pca = ws + 0 * WIN + ((c0 - min(sh.i, ctop)) & (AL - 1));
+        const V* pcb = ws + 1 * WIN + ((c0 - min(sh.id, ctop)) & (AL - 1));
+        const V* psa = ws + 2 * WIN + ((c0 - min(sh.s, ctop)) & (AL - 1));
+        const V* psb = ws + 3 * WIN + ((c0 - min(sh.su, ctop)) & (AL - 1));
+        mbar_wait(&full[slot], (u / NSLOT) & 1);
+        V cn[E], sn[E];
+        CellFlags f[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = c0 + e * T + tid;
+          f[e] = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk, j >= sh.i,
+                                      j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (bprow) {
+          uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
+#pragma unroll
+          for (int e = 0; e < E; ++e) emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f[e], pol);
+        }
+        V* qc = Cn + c0 + tid;
+        V* qs = Sn + c0 + tid;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          qc[e * T] = cn[e];
+          qs[e * T] = sn[e];
+        }
+      }
+      named_barrier(1, T);
+      if (tid == 0) {
+        __threadfence();
+        fence_proxy_async_global();
+        st_release_gpu(&a.prog[q], (uint32_t)(t + 2));
+      }
+    }
+    // the range's final row (this CTA's own block: its own writes)
+    if (a.out_c) {
+      named_barrier(1, T);
+      V* oc = reinterpret_cast<V*>(a.out_c);
+      V* os = reinterpret_cast<V*>(a.out_s);
+      const V* Cf = row(a.k_count % kRowBufs, 0);
+      const V* Sf = row(a.k_count % kRowBufs, 1);
+      for (int j = j0 + tid; j < min(j0 + B, ncol); j += T) {
+        oc[j] = Cf[j];
+        os[j] = Sf[j];
+      }
+    }
+  }
+}
+
+// End of the forward pass of a grid-solved instance: the end side from the
+// final row's last cell (planner.py:190-200), or the infeasible policy.
+// state = {j, client side, infeasible}.
+__global__ void grid_end_kernel(sp_instances in, InstInfo* info, int64_t inst, const void* last_c,
+                                const void* last_s, int64_t* state) {
+  const InstInfo inf = info[inst];
+  const int64_t jl = inf.w_eff;
+  double ec, es;
+  if (inf.mode == VM_INT32) {
+    ec = to_f64(reinterpret_cast<const int32_t*>(last_c)[jl], inf.scale);
+    es = to_f64(reinterpret_cast<const int32_t*>(last_s)[jl], inf.scale);
+  } else {
+    ec = reinterpret_cast<const double*>(last_c)[jl];
+    es = reinterpret_cast<const double*>(last_s)[jl];
+  }
+  info[inst].end_c = ec;
+  info[inst].end_s = es;
+  const int8_t must = in.must_end_at ? in.must_end_at[inst] : (int8_t)-1;
+  if (must == 1) es = -INFINITY;
+  else if (must == 0) ec = -INFINITY;
+  const double pmax = (es > ec) ? es : ec;
+  state[0] = jl;
+  state[1] = ec >= es ? 1 : 0;
+  state[2] = pmax == -INFINITY ? 1 : 0;
+}
+
+// Walk one segment of back-pointers (stages k_begin + k_count - 1 .. k_begin)
+// from state {j, side}, writing pi; the same decisions as backtrack_kernel.
+__global__ void grid_backtrack_kernel(sp_instances in, int64_t inst, const StageShift* shifts,
+                                      const uint32_t* bp, int64_t row_words, int mode, int k_begin,
+                                      int k_count, int64_t* state, sp_policies out) {
+  const int64_t lo = in.layer_off[inst];
+  int64_t j = state[0];
+  bool client = state[1] != 0;
+  const int nw = bp_words(mode);
+  uint8_t* pi = out.pi + lo;
+  for (int t = k_count - 1; t >= 0; --t) {
+    const int k = k_begin + t;
+    const uint32_t* grp = bp + (int64_t)t * row_words + (j >> 5) * nw;
+    const uint32_t bit = 1u << (j & 31);
+    const bool c_stay = grp[0] & bit, s_stay = grp[1] & bit;
+    const bool c_sw = nw == 4 ? (grp[2] & bit) != 0 : !c_stay;
+    const bool s_sw = nw == 4 ? (grp[3] & bit) != 0 : !s_stay;
+    const StageShift sh = shifts[lo + k];
+    if (client) {
+      pi[k] = 1;
+      if (c_stay) {
+        j -= sh.i;
+      } else if (c_sw) {
+        j -= sh.id;
+        client = false;
+      } else {
+        out.status[inst] = SP_ERR_BACKTRACE;
+        state[2] = 2;
+        return;
+      }
+    } else {
+      pi[k] = 0;
+      if (s_stay) {
+        j -= sh.s;
+      } else if (s_sw) {
+        j -= sh.su;
+        client = true;
+      } else {
+        out.status[inst] = SP_ERR_BACKTRACE;
+        state[2] = 2;
+        return;
+      }
+    }
+  }
+  state[0] = j;
+  state[1] = client ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
 // _finish (planner.py:88-101) for a placement already written to pi
 
 __device__ void finish_policy(const sp_instances& in, int64_t inst, int64_t lo, int L,
@@ -990,6 +1277,18 @@ __device__ void finish_policy(const sp_instances& in, int64_t inst, int64_t lo, 
   out.feasible[inst] = feasible_hint ? (hint_value ? 1 : 0) : (lat <= in.budget[inst] ? 1 : 0);
 }
 
+
+// _finish of one grid-solved instance; state[2]: 0 ok, 1 infeasible, 2 backtrace error
+__global__ void grid_finish_kernel(sp_instances in, int64_t inst, const int64_t* state,
+                                   int32_t* idx_scratch, sp_policies out) {
+  const int64_t lo = in.layer_off[inst];
+  const int L = (int)(in.layer_off[inst + 1] - lo);
+  if (state[2] == 2) return;  // status already set
+  if (state[2] == 1)
+    for (int k = 0; k < L; ++k) out.pi[lo + k] = 0;
+  finish_policy(in, inst, lo, L, idx_scratch + lo, out, state[2] == 1, false);
+  out.status[inst] = SP_OK;
+}
 
 // ---------------------------------------------------------------------------
 // _finish over caller-supplied placements
@@ -1609,6 +1908,7 @@ int forced_variant() {
   if (!strcmp(v, "global")) return DPV_GLOBAL;
   if (!strcmp(v, "coop")) return DPV_COOP;
   if (!strcmp(v, "stream")) return DPV_STREAM;
+  if (!strcmp(v, "grid")) return 5;  // DPV_GRID
   return -1;
 }
 
@@ -1720,6 +2020,203 @@ double hbm_bytes_per_cell(int mode, int variant) {
   return variant == DPV_GLOBAL ? 4.0 * (double)value_bytes(mode) + bits : bits;
 }
 
+// ---- grid path: one huge instance over the whole GPU --------------------------
+
+constexpr int kGridT = 256, kGridE = 4, kGridSlots = 4;
+constexpr int kGridCH = kGridT * kGridE;
+constexpr int64_t kGridMinCols = (int64_t)1 << 22;
+enum { DPV_GRID = 5 };
+
+size_t grid_smem(int mode) {
+  const size_t vb = value_bytes(mode);
+  return 256 + (size_t)kGridSlots * 4 * (kGridCH + 16 / vb) * vb;
+}
+
+template <int MODE>
+int grid_resident() {
+  auto kern = dp_grid_kernel<MODE, kGridT, kGridE, kGridSlots>;
+  int n = 0, dev = 0, sms = 148;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grid_smem(MODE)) !=
+          cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kGridT + 32, grid_smem(MODE)) != cudaSuccess ||
+      cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n * sms;
+}
+
+template <int MODE>
+int launch_grid_t(const GridArgs& g, cudaStream_t st) {
+  auto kern = dp_grid_kernel<MODE, kGridT, kGridE, kGridSlots>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)g.G, 1, 1);
+  cfg.blockDim = dim3((unsigned)(kGridT + 32), 1, 1);
+  cfg.dynamicSmemBytes = grid_smem(MODE);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the waits are safe
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, g), "dp_grid_kernel launch");
+  if (rc) return rc;
+  return launch_check("dp_grid_kernel launch");
+}
+
+int launch_grid(int mode, const GridArgs& g, cudaStream_t st) {
+  switch (mode) {
+    case VM_INT32: return launch_grid_t<VM_INT32>(g, st);
+    case VM_F64: return launch_grid_t<VM_F64>(g, st);
+    default: return launch_grid_t<VM_F64_NAN>(g, st);
+  }
+}
+
+// Solve one instance over the whole GPU.  With the full back-pointer table in
+// memory: one forward launch and one backtrack.  Otherwise checkpoint /
+// recompute: a forward pass that keeps a row every K stages, then, segment by
+// segment from the end, a recompute of the segment's back-pointers from its
+// checkpoint and a backtrack through it (2x the DP work, sqrt(L) memory).
+int run_grid_instance(const sp_instances* in, sp_policies* out, InstInfo* info, const StageShift* shifts,
+                      const int64_t* rv, int32_t* idx, int64_t inst, int64_t lo, int L, int64_t ncol,
+                      int mode, uint8_t* dyn, size_t avail, cudaStream_t st) {
+  const size_t vb = value_bytes(mode);
+  const int resident = mode == VM_INT32 ? grid_resident<VM_INT32>()
+                       : mode == VM_F64 ? grid_resident<VM_F64>()
+                                        : grid_resident<VM_F64_NAN>();
+  if (resident <= 0) return check_cuda(cudaErrorInvalidConfiguration, "dp_grid_kernel occupancy");
+  const int64_t nchunks = (ncol + kGridCH - 1) / kGridCH;
+  int G = (int)std::min<int64_t>(resident, nchunks);
+  const int NC = (int)((nchunks + G - 1) / G);
+  G = (int)((nchunks + NC - 1) / NC);
+  const int64_t B = (int64_t)NC * kGridCH;
+  const int64_t line = 128 / (int64_t)vb;
+  const int64_t span = (kGridCH + line) + G * B + line;
+  const int64_t row_words = bp_row_words_for(mode, G * B);
+  const size_t rows_bytes = align_up(2 * kRowBufs * (size_t)span * vb, 256);
+  const size_t ckpt_bytes = align_up(2 * (size_t)ncol * vb, 256);
+  const size_t bp_stage = (size_t)row_words * 4;
+  const size_t fixed = align_up((size_t)G * 4, 256) + 256 + rows_bytes;
+  // segment length: everything at once if it fits, else ~sqrt(L * ckpt / bp) stages
+  int K = L;
+  auto need = [&](int k) {
+    const size_t nseg = (size_t)((L + k - 1) / k);
+    return fixed + (k == L ? 2 : nseg + 1) * ckpt_bytes + align_up((size_t)k * bp_stage, 256);
+  };
+  const int force_k = env_int("SPLITPLAN_GRID_SEGMENT", 0);
+  if (force_k > 0) K = std::min(force_k, L);
+  if (need(K) > avail) {
+    K = (int)std::max<double>(1.0, std::sqrt((double)L * (double)ckpt_bytes / (double)bp_stage));
+    K = std::min(K, L);
+    while (K > 1 && need(K) > avail && need(K / 2) < need(K)) K /= 2;
+  }
+  if (need(K) > avail) {
+    set_required_workspace(need(K) + (avail > 0 ? 0 : 0) + (64 << 20));
+    set_error(SP_ERR_WORKSPACE, "instance %lld (%d x %lld) needs %zu B of DP workspace, %zu B available",
+              (long long)inst, L, (long long)ncol, need(K), avail);
+    return SP_ERR_WORKSPACE;
+  }
+  Carve cv{dyn, avail};
+  uint32_t* prog = (uint32_t*)cv.take((size_t)G * 4);
+  int64_t* state = (int64_t*)cv.take(4 * sizeof(int64_t));
+  uint8_t* rows = (uint8_t*)cv.take(rows_bytes);
+  const int nseg = (L + K - 1) / K;
+  const int nckpt = K == L ? 2 : nseg + 1;
+  std::vector<uint8_t*> ckpt(nckpt);
+  for (int c = 0; c < nckpt; ++c) ckpt[c] = (uint8_t*)cv.take(ckpt_bytes);
+  uint32_t* bp = (uint32_t*)cv.take((size_t)K * bp_stage);
+
+  GridArgs g;
+  g.shifts = shifts + lo;
+  g.rv = rv + lo;
+  g.ncol = (int)ncol;
+  g.G = G;
+  g.NC = NC;
+  g.sac = 0;
+  g.rows = rows;
+  g.bp_row_words = row_words;
+  g.prog = prog;
+  {
+    uint8_t sac = 0;
+    int rc = check_cuda(cudaMemcpyAsync(&sac, in->source_at_client + inst, 1, cudaMemcpyDeviceToHost, st),
+                        "copy source_at_client");
+    if (rc) return rc;
+    rc = check_cuda(cudaStreamSynchronize(st), "sync");
+    if (rc) return rc;
+    g.sac = sac ? 1 : 0;
+  }
+  auto launch = [&](int k0, int cnt, const uint8_t* init, uint8_t* outrow, uint32_t* bpp) -> int {
+    g.k_begin = k0;
+    g.k_count = cnt;
+    g.init_c = init;
+    g.init_s = init ? init + ncol * vb : nullptr;
+    g.out_c = outrow;
+    g.out_s = outrow ? outrow + ncol * vb : nullptr;
+    g.bp = bpp;
+    int rc = check_cuda(cudaMemsetAsync(prog, 0, (size_t)G * 4, st), "zero progress counters");
+    if (rc) return rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (profiling()) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, st);
+    }
+    rc = launch_grid(mode, g, st);
+    if (rc) return rc;
+    if (profiling()) {
+      cudaEventRecord(e1, st);
+      const double cells = (double)cnt * (double)ncol;
+      prof_record_dp(e0, e1, cells, cells * (bpp ? hbm_bytes_per_cell(mode, DPV_SMEM) : 0.0), DPV_GRID);
+    }
+    return SP_OK;
+  };
+  int rc;
+  if (K == L) {
+    rc = launch(0, L, nullptr, ckpt[1], bp);
+    if (rc) return rc;
+  } else {
+    for (int sg = 0; sg < nseg; ++sg) {
+      const int k0 = sg * K;
+      rc = launch(k0, std::min(K, L - k0), sg ? ckpt[sg] : nullptr, ckpt[sg + 1], nullptr);
+      if (rc) return rc;
+    }
+  }
+  uint8_t* last = ckpt[K == L ? 1 : nseg];
+  grid_end_kernel<<<1, 1, 0, st>>>(*in, info, inst, last, last + ncol * vb, state);
+  rc = launch_check("grid_end_kernel launch");
+  if (rc) return rc;
+  int64_t hstate[3];
+  rc = check_cuda(cudaMemcpyAsync(hstate, state, sizeof(hstate), cudaMemcpyDeviceToHost, st), "copy end state");
+  if (rc) return rc;
+  rc = check_cuda(cudaStreamSynchronize(st), "sync end state");
+  if (rc) return rc;
+  if (out && hstate[2] == 0) {
+    if (K == L) {
+      grid_backtrack_kernel<<<1, 1, 0, st>>>(*in, inst, shifts, bp, row_words, mode, 0, L, state, *out);
+      rc = launch_check("grid_backtrack_kernel launch");
+      if (rc) return rc;
+    } else {
+      for (int sg = nseg - 1; sg >= 0; --sg) {
+        const int k0 = sg * K, cnt = std::min(K, L - k0);
+        rc = launch(k0, cnt, sg ? ckpt[sg] : nullptr, nullptr, bp);
+        if (rc) return rc;
+        grid_backtrack_kernel<<<1, 1, 0, st>>>(*in, inst, shifts, bp, row_words, mode, k0, cnt, state,
+                                                *out);
+        rc = launch_check("grid_backtrack_kernel launch");
+        if (rc) return rc;
+      }
+    }
+  }
+  if (out) {
+    grid_finish_kernel<<<1, 1, 0, st>>>(*in, inst, state, idx, *out);
+    rc = launch_check("grid_finish_kernel launch");
+    if (rc) return rc;
+  }
+  // the caller's next use of the workspace is stream-ordered after these
+  return SP_OK;
+}
+
 // Shared driver of sp_plan_dp and sp_build_dp_tables.
 int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_s, void* ws,
            size_t ws_bytes, cudaStream_t st) {
@@ -1787,6 +2284,25 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     }
     it.plan = cached;
     items.push_back(it);
+  }
+
+  // instances too large for a wave (or wider than 4M columns) run alone over
+  // the whole GPU (grid path, checkpointing if needed)
+  {
+    std::vector<Item> rest;
+    rest.reserve(items.size());
+    for (const Item& it : items) {
+      const bool grid = tab_c == nullptr &&
+                        (force == DPV_GRID || it.ncol >= kGridMinCols || it.plan.bp + it.plan.rows > avail);
+      if (!grid) {
+        rest.push_back(it);
+        continue;
+      }
+      rc = run_grid_instance(in, out, info, shifts, rv, idx, it.inst, hoff[it.inst], (int)it.L, it.ncol,
+                             it.mode, dyn, avail, st);
+      if (rc) return rc;
+    }
+    items.swap(rest);
   }
 
   DpArgs a;

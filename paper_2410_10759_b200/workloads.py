@@ -10,6 +10,7 @@ tests, and `bench.py`.  Nothing here touches the GPU.
     cfg3  Llama-2-7B-like (L = 130), long sequences, W = 1e4          (configs[2])
     cfg4  Monte-Carlo scenario grid: 16 SLA scales x 16 bandwidths x
           256 workload-mix seeds, 64 requests each                     (configs[3])
+    cfg5  one chain of L = 1e5 stages x W = 1e7 budget columns        (configs[4])
 
 Device calibration follows the reference acceptance suite: client 7.727 s and
 server 0.0979 s for bert-12 at 4096 tokens (`test_acceptance.py:23-52`).
@@ -154,3 +155,15 @@ def cfg4(scenarios=None) -> tuple[dict, list, np.ndarray]:
     off = np.arange(len(sids) + 1, dtype=np.int64) * CFG4_REQUESTS
     bw = np.array(bw)
     return _requests(model, seq, cfps, sfps, bw, bw.copy(), np.array(dl), 1e-3), layer_lists, off
+
+
+def cfg5(L: int = 100_000, W: int = 10_000_000, seed: int = 5) -> dict:
+    """configs[4]: one huge chain via PlanProblem.from_costs (problem.py:179-185):
+    i, s, u, d ~ U{0..200}, r ~ U{0..100} (integral floats), source at the
+    client, budget W.  The worst path exceeds W, so W_eff = W.  Returns the
+    CSR instance arrays of `batch.InstanceBatch.from_arrays`."""
+    rng = np.random.default_rng(seed)
+    i, s, u, d = (rng.integers(0, 201, L) for _ in range(4))
+    r = rng.integers(0, 101, L).astype(np.float64)
+    return dict(layer_off=np.array([0, L], dtype=np.int64), i=i, s=s, u=u, d=d, r=r,
+                budget=np.array([W], dtype=np.int64), sac=np.array([1], dtype=np.uint8))

@@ -138,3 +138,31 @@ def test_cfg3_full_batch_properties(gpu):
     assert bool((dp.client_value[gf] >= gr.client_value[gf]).all())
     # feasible <=> latency within the original budget
     assert torch.equal(dp.feasible.bool(), dp.integer_latency <= sol.instances.budget)
+
+
+def test_cfg5_huge_instance_full_size(gpu):
+    """configs[4]: ONE chain of 1e5 stages x 1e7 columns (1e12 DP cells) solved
+    over the whole GPU with checkpoint / recompute (its 250 GB back-pointer
+    table does not fit in HBM).  Bit-exact parity runs at reduced scale
+    (battery_large_chain, test_grid_checkpoint_recompute); here the full-size
+    placement must be self-consistent and dominate the trivial placements."""
+    import torch
+    from paper_2410_10759_b200 import _native as N
+    from paper_2410_10759_b200 import batch as B
+    from paper_2410_10759_b200 import workloads as W
+    x = W.cfg5()
+    b = B.InstanceBatch.from_arrays(x["layer_off"], x["i"], x["s"], x["u"], x["d"], x["r"],
+                                    x["budget"], x["sac"])
+    assert int(B.effective_budget(b).item()) == 10_000_000
+    dp = B.plan_dp(b)
+    ev = B.PolicyBatch.empty(1, b.total_layers)
+    N.check(N.with_workspace(lambda ws, nb: N.library().sp_evaluate_policy(
+        b.struct(), N.ptr(dp.pi), ev.struct(), ws, nb, N.stream_ptr())), "sp_evaluate_policy")
+    torch.cuda.synchronize()
+    assert int(dp.status.item()) == 0 and bool(dp.feasible.item())
+    assert int(ev.integer_latency.item()) == int(dp.integer_latency.item()) <= 10_000_000
+    assert ev.client_value.item() == dp.client_value.item()
+    for which in (N.SP_GREEDY, N.SP_ALL_SERVER):
+        p = B.plan_prefix(b, which)
+        if bool(p.feasible.item()):
+            assert dp.client_value.item() >= p.client_value.item()

@@ -180,7 +180,7 @@ def test_dp_vs_oracle_smem_and_global_rows(gpu, r_kind):
         assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{r_kind}[{k}]")
 
 
-@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop", "stream"])
+@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop", "stream", "grid"])
 @pytest.mark.parametrize("name", ["battery_wide", "battery_float", "battery_large_model"])
 def test_dp_kernel_variants_agree(gpu, variant, name, monkeypatch):
     """Every K2 variant (rows in one CTA's SMEM, in cluster DSMEM, in global
@@ -214,6 +214,36 @@ def test_stream_cluster_sizes(gpu, cluster, monkeypatch):
     for name in ("battery_wide", "battery_large_model"):
         bat = Battery(name)
         _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
+
+
+@pytest.mark.parametrize("segment", ["0", "7", "1"])
+def test_grid_checkpoint_recompute(gpu, segment, monkeypatch):
+    """The whole-GPU path for one huge instance, with the back-pointers kept
+    whole (segment 0) or recomputed from checkpoint rows every 7 / 1 stages."""
+    from paper_2410_10759_b200 import batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "grid")
+    monkeypatch.setenv("SPLITPLAN_GRID_SEGMENT", segment)
+    for name in ("battery_wide", "battery_special"):
+        bat = Battery(name)
+        _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
+    for r_kind in ("int", "float", "inf"):
+        insts = _random_instances(7, 6, (3, 30), [900, 20000], r_kind)
+        off = np.zeros(len(insts) + 1, np.int64)
+        np.cumsum([len(x["r"]) for x in insts], out=off[1:])
+        cat = lambda k: np.concatenate([x[k] for x in insts])
+        b = B.InstanceBatch.from_arrays(off, cat("i"), cat("s"), cat("u"), cat("d"), cat("r"),
+                                        [x["budget"] for x in insts], [x["sac"] for x in insts])
+        host = B.plan_dp(b).to_host()
+        for k, inst in enumerate(insts):
+            try:
+                exp = O.plan_dp(inst)
+            except AssertionError:
+                assert host["status"][k] != 0
+                continue
+            got = dict(pi=host["pi"][off[k]:off[k + 1]], client_value=host["client_value"][k],
+                       server_load=host["server_load"][k], integer_latency=host["integer_latency"][k],
+                       feasible=host["feasible"][k])
+            assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"grid {r_kind}[{k}]")
 
 
 @pytest.mark.parametrize("name", ["battery_large_model", "battery_large_chain"])
