@@ -150,7 +150,8 @@ def measured_peak_hbm():
 
 VARIANTS = ["dp_stage_kernel<smem rows>", "dp_cluster_kernel<DSMEM rows>",
             "dp_stage_kernel<global rows>", "dp_coop_kernel<L2 rows>",
-            "dp_stream_kernel<L2 rows, bulk-copy staged windows>"]
+            "dp_stream_kernel<L2 rows, bulk-copy staged windows>",
+            "dp_grid_kernel<one instance over the GPU>"]
 NCU_SUMMARY = {0: "dp_smem_ncu_summary.json", 3: "dp_coop_ncu_summary.json",
                4: "dp_stream_ncu_summary.json"}
 
@@ -179,7 +180,7 @@ def onchip_roofline(variant: int, cells_per_s: float, sm_mhz: float | None) -> d
     clk = (sm_mhz or 1965.0) * 1e6
     if variant == 0:
         per_cell, peak, res = 24.0, 128.0 * 148 * clk, "smem"
-    elif variant in (3, 4):
+    elif variant in (3, 4, 5):
         per_cell, peak, res = 24.0, 6300.0 * clk, "l2"
     else:
         return None
