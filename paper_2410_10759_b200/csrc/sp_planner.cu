@@ -980,21 +980,36 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
 // into checkpoint / recompute passes when the full back-pointer table does
 // not fit in memory.
 
+constexpr int kMaxParts = 8;
+
+// One huge instance over the whole GPU (or, partitioned, over several GPUs).
+// The capacity axis can be split into `nparts` partitions of Gp CTAs each
+// (one per device in a multi-GPU run): partition p owns global columns
+// [p*Wp, (p+1)*Wp), Wp = Gp*B, keeps its own triple-buffered rows, and
+// mirrors the left neighbour's last `halo` columns of every row in front of
+// its column 0 -- the halo, written by the neighbour's CTAs with plain
+// (peer) stores as they produce those columns.  Dependencies are computed
+// in the global CTA index space, so the protocol is the same whether the
+// partitions are launched together (one device, emulating several) or one
+// per device.
 struct GridArgs {
   const StageShift* shifts;  // stage records of the instance (index = stage)
   const int64_t* rv;         // stage values in the value domain
   int k_begin, k_count;      // stage range of this launch
   int ncol;                  // W_eff + 1
-  int G, NC;                 // CTAs, chunks per CTA
+  int G, NC;                 // CTAs per partition, chunks per CTA
   int sac;
   const void* init_c;        // row k_begin, ncol values each, or null: origin row
   const void* init_s;
   void* out_c;               // row k_begin + k_count, or null
   void* out_s;
-  uint8_t* rows;             // [3][C|S][PAD + G*B + LINE]
   uint32_t* bp;              // back-pointers of the range's stages, or null
   int64_t bp_row_words;
-  uint32_t* prog;            // [G] stages completed in this launch (zeroed)
+  uint32_t* prog;            // [nparts * G] stages completed + 1 (zeroed)
+  int nparts;                // partitions of the capacity axis
+  int part_base;             // first partition of this launch (grid = launched parts x G)
+  int halo;                  // mirrored left-neighbour columns (multiple of 128 B)
+  uint8_t* rows[kMaxParts];  // per partition: [3][C|S][NEG pad | halo | Wp | line]
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
@@ -1016,7 +1031,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
   constexpr int CH = T * E;
   constexpr int AL = 16 / (int)sizeof(V);
   constexpr int WIN = CH + AL;
-  constexpr int PAD = stream_pad<V, CH>();
+  constexpr int PAD = stream_pad<V, CH>();  // NEG area in front of the halo
   constexpr int LINE = 128 / (int)sizeof(V);
   constexpr int NWARP = T / 32;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1025,39 +1040,61 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
   V* slots = reinterpret_cast<V*>(smem + 256);
 
   const int G = a.G, NC = a.NC;
-  const int q = blockIdx.x;
+  const int part = a.part_base + (int)blockIdx.x / G;
+  const int q = (int)blockIdx.x % G;
+  const int GT = a.nparts * G;  // CTAs over the whole capacity axis
+  const int gq = part * G + q;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int B = NC * CH;
-  const int j0 = q * B;
+  const int Wp = G * B;
+  const int p0 = part * Wp;      // global column of this partition's local column 0
+  const int j0 = q * B;          // local
+  const int j0g = p0 + j0;       // global
   const int ncol = a.ncol;
-  const int64_t span = (int64_t)PAD + (int64_t)G * B + LINE;
+  const int H = a.halo;
+  const int64_t span = (int64_t)PAD + H + Wp + LINE;
   const V NEG = VT<MODE>::neg();
   const V ZERO = V(0);
-  V* base = reinterpret_cast<V*>(a.rows);
-  auto row = [&](int buf, int rs) { return base + (int64_t)(buf * 2 + rs) * span + PAD; };
-  auto owner = [&](int x) { return min(G - 1, max(0, x) / B); };
+  auto row_of = [&](int p, int buf, int rs) {
+    return reinterpret_cast<V*>(a.rows[p]) + (int64_t)(buf * 2 + rs) * span + PAD + H;
+  };
+  auto row = [&](int buf, int rs) { return row_of(part, buf, rs); };
+  auto owner = [&](int x) { return min(GT - 1, max(0, x) / B); };  // global CTA of global column x
+  const V* ic = reinterpret_cast<const V*>(a.init_c);
+  const V* is = reinterpret_cast<const V*>(a.init_s);
+  auto init_at = [&](int x, V& c, V& sv) {  // row k_begin at global column x
+    const bool valid = x >= 0 && x < ncol;
+    if (ic) {
+      c = valid ? ic[x] : NEG;
+      sv = valid ? is[x] : NEG;
+    } else {
+      c = (valid && a.sac) ? ZERO : NEG;
+      sv = (valid && !a.sac) ? ZERO : NEG;
+    }
+  };
 
   for (int buf = 0; buf < kRowBufs; ++buf) {
     V* Cb = row(buf, 0);
     V* Sb = row(buf, 1);
-    if (q == 0)
-      for (int x = tid - PAD; x < 0; x += blockDim.x) Cb[x] = Sb[x] = NEG;
-    if (q == G - 1)
-      for (int x = G * B + tid; x < G * B + LINE; x += blockDim.x) Cb[x] = Sb[x] = NEG;
-    if (buf == 0) {
-      const V* ic = reinterpret_cast<const V*>(a.init_c);
-      const V* is = reinterpret_cast<const V*>(a.init_s);
-      for (int j = j0 + tid; j < j0 + B; j += blockDim.x) {
-        const bool valid = j < ncol;
-        if (ic) {
-          Cb[j] = valid ? ic[j] : NEG;
-          Sb[j] = valid ? is[j] : NEG;
-        } else {
-          Cb[j] = (valid && a.sac) ? ZERO : NEG;
-          Sb[j] = (valid && !a.sac) ? ZERO : NEG;
+    if (q == 0) {
+      for (int x = tid - PAD - H; x < -H; x += blockDim.x) Cb[x] = Sb[x] = NEG;  // NEG area
+      // halo of buffer 0: row k_begin of the neighbour's last columns (all NEG
+      // in partition 0).  Buffers 1 and 2 belong to the neighbour's CTAs, which
+      // write them before any read (RAW) -- never touch them here.
+      if (buf == 0)
+        for (int x = tid - H; x < 0; x += blockDim.x) {
+          V c = NEG, sv = NEG;
+          if (part > 0) init_at(p0 + x, c, sv);
+          Cb[x] = c;
+          Sb[x] = sv;
         }
-      }
+      else if (part == 0)
+        for (int x = tid - H; x < 0; x += blockDim.x) Cb[x] = Sb[x] = NEG;
     }
+    if (q == G - 1)
+      for (int x = Wp + tid; x < Wp + LINE; x += blockDim.x) Cb[x] = Sb[x] = NEG;
+    if (buf == 0)
+      for (int j = j0 + tid; j < j0 + B; j += blockDim.x) init_at(p0 + j, Cb[j], Sb[j]);
   }
   if (tid == 0) {
     for (int b = 0; b < NSLOT; ++b) {
@@ -1070,7 +1107,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
   if (tid == 0) {
     __threadfence();
     fence_proxy_async_global();
-    st_release_gpu(&a.prog[q], 1u);  // rows initialised (counter = completed stages + 1)
+    st_release_gpu(&a.prog[gq], 1u);  // rows initialised (counter = completed stages + 1)
   }
 
   if (warp == NWARP) {
@@ -1080,13 +1117,14 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
       const int k = a.k_begin + t;
       const StageShift sh = a.shifts[k];
       // RAW: owners of the windows read this stage (row t complete => counter >= t + 1)
-      const int lo_o = owner(j0 - max_shift(sh) - AL);
-      // WAR: CTAs that read this block's target buffer two stages ago
-      int hi_o = q;
-      if (t >= 2) hi_o = owner(j0 + B - 1 + max_shift(a.shifts[k - 2]) + CH + AL);
+      const int lo_o = owner(j0g - max_shift(sh) - AL);
+      // WAR: CTAs that read this block's target buffers (own rows and the
+      // right neighbour's halo copy) two stages ago
+      int hi_o = gq;
+      if (t >= 2) hi_o = owner(j0g + B - 1 + max_shift(a.shifts[k - 2]) + CH + AL);
       for (int o0 = lo_o; o0 <= hi_o; o0 += 32) {
         const int o = o0 + lane;
-        const uint32_t need = o <= q ? (uint32_t)(t + 1) : (uint32_t)max(t - 1, 0) + 1u;
+        const uint32_t need = o <= gq ? (uint32_t)(t + 1) : (uint32_t)max(t - 1, 0) + 1u;
         while (!__all_sync(0xffffffffu, o > hi_o || ld_acquire_gpu(&a.prog[o]) >= need)) {
         }
       }
@@ -1099,13 +1137,17 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
         for (int c = 0; c < NC; ++c, ++u) {
           const int slot = (int)(u % NSLOT);
           mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
-          const int c0 = j0 + c * CH, ctop = c0 + CH;
+          const int c0g = j0g + c * CH, ctop = c0g + CH;
           mbar_expect_tx(&full[slot], 4u * WIN * sizeof(V));
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
-            const int start = c0 - min(shf[w], ctop);
-            bulk_g2s(slots + (slot * 4 + w) * WIN, src[w] + (start & ~(AL - 1)), WIN * sizeof(V),
-                     &full[slot]);
+            const int start = c0g - min(shf[w], ctop);
+            // Partition 0 keeps NEG in front of column 0 (halo + NEG area), so
+            // partially negative windows read it in place.  In later
+            // partitions start < 0 only when the shift was clamped (every cell
+            // of the window unreachable): read the NEG area.
+            const int local = (start < 0 && part > 0) ? -H - PAD : (start & ~(AL - 1)) - p0;
+            bulk_g2s(slots + (slot * 4 + w) * WIN, src[w] + local, WIN * sizeof(V), &full[slot]);
           }
         }
       }
@@ -1117,6 +1159,8 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
     uint32_t u = 0;
     StageShift sh_next = a.shifts[a.k_begin];
     int64_t rbits_next = a.rv[a.k_begin];
+    // global columns mirrored into the right neighbour's halo
+    const int halo_lo = part + 1 < a.nparts ? p0 + Wp - H : INT_MAX;
     for (int t = 0; t < a.k_count; ++t) {
       const StageShift sh = sh_next;
       const int64_t rbits = rbits_next;
@@ -1130,25 +1174,26 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
       uint32_t* bprow = a.bp ? a.bp + (int64_t)t * a.bp_row_words + warp * bp_words(MODE) : nullptr;
       for (int c = 0; c < NC; ++c, ++u) {
         const int slot = (int)(u % NSLOT);
-        const int c0 = j0 + c * CH, ctop = c0 + CH;
+        const int c0 = j0 + c * CH;       // local
+        const int c0g = p0 + c0, ctop = c0g + CH;
         const V* ws = slots + slot * 4 * WIN + tid;
-        const V* pca = ws + 0 * WIN + ((c0 - min(sh.i, ctop)) & (AL - 1));
-        const V* pcb = ws + 1 * WIN + ((c0 - min(sh.id, ctop)) & (AL - 1));
-        const V* psa = ws + 2 * WIN + ((c0 - min(sh.s, ctop)) & (AL - 1));
-        const V* psb = ws + 3 * WIN + ((c0 - min(sh.su, ctop)) & (AL - 1));
+        const V* pca = ws + 0 * WIN + ((c0g - min(sh.i, ctop)) & (AL - 1));
+        const V* pcb = ws + 1 * WIN + ((c0g - min(sh.id, ctop)) & (AL - 1));
+        const V* psa = ws + 2 * WIN + ((c0g - min(sh.s, ctop)) & (AL - 1));
+        const V* psb = ws + 3 * WIN + ((c0g - min(sh.su, ctop)) & (AL - 1));
         mbar_wait(&full[slot], (u / NSLOT) & 1);
         V cn[E], sn[E];
         CellFlags f[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          const int j = c0 + e * T + tid;
+          const int j = c0g + e * T + tid;
           f[e] = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk, j >= sh.i,
                                       j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
         if (bprow) {
-          uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
+          uint32_t* bpc = bprow + (c0g >> 5) * bp_words(MODE);
 #pragma unroll
           for (int e = 0; e < E; ++e) emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f[e], pol);
         }
@@ -1159,12 +1204,24 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
           qc[e * T] = cn[e];
           qs[e * T] = sn[e];
         }
+        if (ctop > halo_lo) {  // the right neighbour mirrors these columns
+          V* hc = row_of(part + 1, (t + 1) % kRowBufs, 0) - (p0 + Wp);
+          V* hs = row_of(part + 1, (t + 1) % kRowBufs, 1) - (p0 + Wp);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int j = c0g + e * T + tid;
+            if (j >= halo_lo) {
+              hc[j] = cn[e];
+              hs[j] = sn[e];
+            }
+          }
+        }
       }
       named_barrier(1, T);
       if (tid == 0) {
         __threadfence();
         fence_proxy_async_global();
-        st_release_gpu(&a.prog[q], (uint32_t)(t + 2));
+        st_release_gpu(&a.prog[gq], (uint32_t)(t + 2));
       }
     }
     // the range's final row (this CTA's own block: its own writes)
@@ -1174,9 +1231,9 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
       V* os = reinterpret_cast<V*>(a.out_s);
       const V* Cf = row(a.k_count % kRowBufs, 0);
       const V* Sf = row(a.k_count % kRowBufs, 1);
-      for (int j = j0 + tid; j < min(j0 + B, ncol); j += T) {
-        oc[j] = Cf[j];
-        os[j] = Sf[j];
+      for (int j = j0 + tid; j < j0 + B && p0 + j < ncol; j += T) {
+        oc[p0 + j] = Cf[j];
+        os[p0 + j] = Sf[j];
       }
     }
   }
@@ -1676,7 +1733,10 @@ int launch_single(const DpArgs& a, int64_t n_items, int cfg, size_t smem, cudaSt
 
 // ---- streaming (L2-resident rows, bulk-copy staged windows) ----------------
 
-constexpr int kStreamE = 4, kStreamSlots = 4;
+constexpr int kStreamE = 4;
+// bulk-copy ring depth: ~100 KB of slots per CTA (2 CTAs per SM)
+template <int MODE> constexpr int ring_slots() { return MODE == VM_INT32 ? 6 : 3; }
+inline int ring_slots_rt(int mode) { return mode == VM_INT32 ? 6 : 3; }
 
 // compute threads of the streaming kernel (128 or 256; SPLITPLAN_STREAM_T)
 int stream_threads() {
@@ -1694,7 +1754,7 @@ size_t l2_row_budget() {
 
 size_t stream_smem(int mode) {
   const size_t vb = value_bytes(mode);
-  return 256 + (size_t)kStreamSlots * 4 * (stream_ch() + 16 / vb) * vb;
+  return 256 + (size_t)ring_slots_rt(mode) * 4 * (stream_ch() + 16 / vb) * vb;
 }
 int64_t stream_span(int mode, const StreamGeom& g) {
   const int64_t line = 128 / (int64_t)value_bytes(mode);
@@ -1706,7 +1766,7 @@ size_t stream_row_bytes(int mode, const StreamGeom& g) {
 
 template <int MODE, int T>
 int stream_occupancy_t() {
-  auto kern = dp_stream_kernel<MODE, T, kStreamE, kStreamSlots>;
+  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>()>;
   int n = 0;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(MODE)) !=
           cudaSuccess ||
@@ -1770,7 +1830,7 @@ StreamGeom stream_geom(int mode, int64_t ncol) {
 
 template <int MODE, int T>
 int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
-  auto kern = dp_stream_kernel<MODE, T, kStreamE, kStreamSlots>;
+  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>()>;
   const size_t smem = stream_smem(MODE);
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "cudaFuncSetAttribute(dp_stream_kernel)");
@@ -2035,19 +2095,19 @@ double hbm_bytes_per_cell(int mode, int variant) {
 
 // ---- grid path: one huge instance over the whole GPU --------------------------
 
-constexpr int kGridT = 256, kGridE = 4, kGridSlots = 4;
+constexpr int kGridT = 256, kGridE = 4;
 constexpr int kGridCH = kGridT * kGridE;
 constexpr int64_t kGridMinCols = (int64_t)1 << 22;
 enum { DPV_GRID = 5 };
 
 size_t grid_smem(int mode) {
   const size_t vb = value_bytes(mode);
-  return 256 + (size_t)kGridSlots * 4 * (kGridCH + 16 / vb) * vb;
+  return 256 + (size_t)ring_slots_rt(mode) * 4 * (kGridCH + 16 / vb) * vb;
 }
 
 template <int MODE>
 int grid_resident() {
-  auto kern = dp_grid_kernel<MODE, kGridT, kGridE, kGridSlots>;
+  auto kern = dp_grid_kernel<MODE, kGridT, kGridE, ring_slots<MODE>()>;
   int n = 0, dev = 0, sms = 148;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grid_smem(MODE)) !=
           cudaSuccess ||
@@ -2062,9 +2122,9 @@ int grid_resident() {
 
 template <int MODE>
 int launch_grid_t(const GridArgs& g, cudaStream_t st) {
-  auto kern = dp_grid_kernel<MODE, kGridT, kGridE, kGridSlots>;
+  auto kern = dp_grid_kernel<MODE, kGridT, kGridE, ring_slots<MODE>()>;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)g.G, 1, 1);
+  cfg.gridDim = dim3((unsigned)(g.G * (g.nparts - g.part_base)), 1, 1);  // every partition of this launch
   cfg.blockDim = dim3((unsigned)(kGridT + 32), 1, 1);
   cfg.dynamicSmemBytes = grid_smem(MODE);
   cfg.stream = st;
@@ -2091,26 +2151,60 @@ int launch_grid(int mode, const GridArgs& g, cudaStream_t st) {
 // recompute: a forward pass that keeps a row every K stages, then, segment by
 // segment from the end, a recompute of the segment's back-pointers from its
 // checkpoint and a backtrack through it (2x the DP work, sqrt(L) memory).
+int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* info,
+                            const StageShift* shifts, const int64_t* rv, int32_t* idx, int64_t inst,
+                            int64_t lo, int L, int64_t ncol, int mode, uint8_t* dyn, size_t avail,
+                            cudaStream_t st, int force_parts);
+
 int run_grid_instance(const sp_instances* in, sp_policies* out, InstInfo* info, const StageShift* shifts,
                       const int64_t* rv, int32_t* idx, int64_t inst, int64_t lo, int L, int64_t ncol,
                       int mode, uint8_t* dyn, size_t avail, cudaStream_t st) {
+  return run_grid_instance_parts(in, out, info, shifts, rv, idx, inst, lo, L, ncol, mode, dyn, avail, st, 0);
+}
+
+int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* info,
+                            const StageShift* shifts, const int64_t* rv, int32_t* idx, int64_t inst,
+                            int64_t lo, int L, int64_t ncol, int mode, uint8_t* dyn, size_t avail,
+                            cudaStream_t st, int force_parts) {
   const size_t vb = value_bytes(mode);
   const int resident = mode == VM_INT32 ? grid_resident<VM_INT32>()
                        : mode == VM_F64 ? grid_resident<VM_F64>()
                                         : grid_resident<VM_F64_NAN>();
   if (resident <= 0) return check_cuda(cudaErrorInvalidConfiguration, "dp_grid_kernel occupancy");
   const int64_t nchunks = (ncol + kGridCH - 1) / kGridCH;
-  int G = (int)std::min<int64_t>(resident, nchunks);
-  const int NC = (int)((nchunks + G - 1) / G);
-  G = (int)((nchunks + NC - 1) / NC);
+  // partitions of the capacity axis (one per device in a multi-GPU run;
+  // SPLITPLAN_GRID_PARTS > 1 emulates them on this device)
+  int nparts = force_parts ? force_parts : std::max(1, std::min(kMaxParts, env_int("SPLITPLAN_GRID_PARTS", 1)));
+  nparts = (int)std::min<int64_t>(nparts, nchunks);
+  int G = (int)std::min<int64_t>(resident / nparts, (nchunks + nparts - 1) / nparts);
+  G = std::max(G, 1);
+  const int NC = (int)((nchunks + (int64_t)G * nparts - 1) / ((int64_t)G * nparts));
+  G = (int)((nchunks + (int64_t)NC * nparts - 1) / ((int64_t)NC * nparts));
   const int64_t B = (int64_t)NC * kGridCH;
   const int64_t line = 128 / (int64_t)vb;
-  const int64_t span = (kGridCH + line) + G * B + line;
-  const int64_t row_words = bp_row_words_for(mode, G * B);
+  // halo: the widest read-back of any stage plus alignment slack, whole lines
+  int64_t halo = 0;
+  if (nparts > 1) {
+    std::vector<StageShift> hs(L);
+    int rc0 = check_cuda(cudaMemcpyAsync(hs.data(), shifts + lo, sizeof(StageShift) * L,
+                                         cudaMemcpyDeviceToHost, st), "copy stage shifts");
+    if (rc0) return rc0;
+    rc0 = check_cuda(cudaStreamSynchronize(st), "sync");
+    if (rc0) return rc0;
+    int ms = 0;
+    for (const StageShift& x : hs) ms = std::max(ms, std::max(std::max(x.i, x.id), std::max(x.s, x.su)));
+    halo = ((int64_t)ms + 2 * line + line - 1) / line * line;
+    if (halo > (int64_t)G * B) {  // the read-back spans a whole partition: no point splitting
+      return run_grid_instance_parts(in, out, info, shifts, rv, idx, inst, lo, L, ncol, mode, dyn, avail,
+                                     st, 1);
+    }
+  }
+  const int64_t span = (kGridCH + line) + halo + G * B + line;
+  const int64_t row_words = bp_row_words_for(mode, (int64_t)nparts * G * B);
   const size_t rows_bytes = align_up(2 * kRowBufs * (size_t)span * vb, 256);
   const size_t ckpt_bytes = align_up(2 * (size_t)ncol * vb, 256);
   const size_t bp_stage = (size_t)row_words * 4;
-  const size_t fixed = align_up((size_t)G * 4, 256) + 256 + rows_bytes;
+  const size_t fixed = align_up((size_t)G * nparts * 4, 256) + 256 + nparts * rows_bytes;
   // segment length: everything at once if it fits, else ~sqrt(L * ckpt / bp) stages
   int K = L;
   auto need = [&](int k) {
@@ -2131,23 +2225,27 @@ int run_grid_instance(const sp_instances* in, sp_policies* out, InstInfo* info, 
     return SP_ERR_WORKSPACE;
   }
   Carve cv{dyn, avail};
-  uint32_t* prog = (uint32_t*)cv.take((size_t)G * 4);
+  uint32_t* prog = (uint32_t*)cv.take((size_t)G * nparts * 4);
   int64_t* state = (int64_t*)cv.take(4 * sizeof(int64_t));
-  uint8_t* rows = (uint8_t*)cv.take(rows_bytes);
+  uint8_t* rows[kMaxParts] = {};
+  for (int p = 0; p < nparts; ++p) rows[p] = (uint8_t*)cv.take(rows_bytes);
   const int nseg = (L + K - 1) / K;
   const int nckpt = K == L ? 2 : nseg + 1;
   std::vector<uint8_t*> ckpt(nckpt);
   for (int c = 0; c < nckpt; ++c) ckpt[c] = (uint8_t*)cv.take(ckpt_bytes);
   uint32_t* bp = (uint32_t*)cv.take((size_t)K * bp_stage);
 
-  GridArgs g;
+  GridArgs g = {};
   g.shifts = shifts + lo;
   g.rv = rv + lo;
   g.ncol = (int)ncol;
   g.G = G;
   g.NC = NC;
   g.sac = 0;
-  g.rows = rows;
+  for (int p = 0; p < nparts; ++p) g.rows[p] = rows[p];
+  g.nparts = nparts;
+  g.part_base = 0;
+  g.halo = (int)halo;
   g.bp_row_words = row_words;
   g.prog = prog;
   {
@@ -2167,7 +2265,7 @@ int run_grid_instance(const sp_instances* in, sp_policies* out, InstInfo* info, 
     g.out_c = outrow;
     g.out_s = outrow ? outrow + ncol * vb : nullptr;
     g.bp = bpp;
-    int rc = check_cuda(cudaMemsetAsync(prog, 0, (size_t)G * 4, st), "zero progress counters");
+    int rc = check_cuda(cudaMemsetAsync(prog, 0, (size_t)G * nparts * 4, st), "zero progress counters");
     if (rc) return rc;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (profiling()) {

@@ -246,6 +246,20 @@ def test_grid_checkpoint_recompute(gpu, segment, monkeypatch):
             assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"grid {r_kind}[{k}]")
 
 
+@pytest.mark.parametrize("parts,segment", [("2", "0"), ("3", "13"), ("8", "0")])
+def test_grid_capacity_partitions(gpu, parts, segment, monkeypatch):
+    """The capacity axis split into partitions (one per device in a multi-GPU
+    run, emulated here on one GPU) with the left neighbour's columns mirrored
+    in a halo: bit-exact against the live reference's cfg5-reduced chains."""
+    from paper_2410_10759_b200 import batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "grid")
+    monkeypatch.setenv("SPLITPLAN_GRID_PARTS", parts)
+    monkeypatch.setenv("SPLITPLAN_GRID_SEGMENT", segment)
+    for name, must in (("battery_large_chain", False), ("battery_wide", True)):
+        bat = Battery(name)
+        _compare(bat, "dp", B.plan_dp(_batch(bat, with_must=must)).to_host())
+
+
 @pytest.mark.parametrize("name", ["battery_large_model", "battery_large_chain"])
 def test_full_size_batteries(gpu, name):
     """W_eff = 1e5 model-derived instances (BASELINE cfg2 shape) and the
