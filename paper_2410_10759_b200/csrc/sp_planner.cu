@@ -772,8 +772,9 @@ __device__ __forceinline__ void emit_bp_stream(uint32_t* words, CellFlags f, uin
 }
 
 struct StreamGeom {
-  int G;   // CTAs per instance (cluster size)
-  int NC;  // chunks per CTA
+  int G;        // CTAs per instance (cluster size)
+  int NC;       // chunks per CTA
+  int n_items;  // instances of the launch (set at launch)
 };
 
 constexpr int kRowBufs = 3;
@@ -784,7 +785,11 @@ constexpr int kRowBufs = 3;
 template <typename V, int CH>
 __host__ __device__ constexpr int stream_pad() { return CH + 128 / (int)sizeof(V); }
 
-template <int MODE, int T, int E, int NSLOT>
+// NI instances share one cluster and alternate stage by stage (A0 B0 A1 B1
+// ...): while the producer waits for the other CTAs to finish instance A's
+// stage k, the compute warps work through instance B's stage k, so the
+// stage synchronisation latency overlaps useful work.
+template <int MODE, int T, int E, int NSLOT, int NI>
 __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(DpArgs a, StreamGeom geo) {
   using V = typename VT<MODE>::T;
   constexpr int CH = T * E;
@@ -796,52 +801,63 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + NSLOT;
-  uint32_t* prog = reinterpret_cast<uint32_t*>(empty + NSLOT);  // stages this CTA completed
+  uint32_t* prog = reinterpret_cast<uint32_t*>(empty + NSLOT);  // [NI] stages completed
   V* slots = reinterpret_cast<V*>(smem + 256);                    // [NSLOT][4][WIN]
 
   const int G = geo.G, NC = geo.NC;
   const int q = (int)cluster_rank();
-  const DpWork wk = a.work[blockIdx.x / G];
-  const int64_t inst = wk.inst;
-  const int64_t lo = a.layer_off[inst];
-  const int L = (int)(a.layer_off[inst + 1] - lo);
-  const int ncol = (int)(a.info[inst].w_eff + 1);
-  const double g = a.info[inst].scale;
-  const bool sac = a.sac[inst] != 0;
+  const int first = (int)(blockIdx.x / G) * NI;
+  const int ni = min(NI, geo.n_items - first);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int B = NC * CH;
   const int j0 = q * B;
   const int64_t span = (int64_t)PAD + (int64_t)G * B + LINE;
-  const int64_t row_words = wk.bp_row_words;
   const V NEG = VT<MODE>::neg();
   const V ZERO = V(0);
-  V* base = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][PAD + G*B + LINE]
-  auto row = [&](int buf, int rs) { return base + (int64_t)(buf * 2 + rs) * span + PAD; };
+  int64_t inst[NI], lo[NI], row_words[NI];
+  int L[NI], ncol[NI];
+  V* base[NI];
+  int maxL = 0;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const DpWork wk = a.work[first + min(i, ni - 1)];
+    inst[i] = wk.inst;
+    lo[i] = a.layer_off[wk.inst];
+    L[i] = i < ni ? (int)(a.layer_off[wk.inst + 1] - lo[i]) : 0;
+    ncol[i] = (int)(a.info[wk.inst].w_eff + 1);
+    base[i] = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][PAD + G*B + LINE]
+    row_words[i] = wk.bp_row_words;
+    maxL = max(maxL, L[i]);
+  }
+  auto row = [&](int i, int buf, int rs) { return base[i] + (int64_t)(buf * 2 + rs) * span + PAD; };
 
-  for (int buf = 0; buf < kRowBufs; ++buf) {
-    V* Cb = row(buf, 0);
-    V* Sb = row(buf, 1);
-    if (q == 0)
-      for (int x = tid - PAD; x < 0; x += blockDim.x) Cb[x] = Sb[x] = NEG;  // never rewritten
-    if (q == G - 1)
-      for (int x = G * B + tid; x < G * B + LINE; x += blockDim.x) Cb[x] = Sb[x] = NEG;
-    if (buf == 0)
-      for (int j = j0 + tid; j < j0 + B; j += blockDim.x) {
-        const bool valid = j < ncol;
-        Cb[j] = (valid && sac) ? ZERO : NEG;
-        Sb[j] = (valid && !sac) ? ZERO : NEG;
-        if (a.tab_c && valid) {
-          a.tab_c[j] = sac ? 0.0 : -INFINITY;
-          a.tab_s[j] = sac ? -INFINITY : 0.0;
+  for (int i = 0; i < ni; ++i) {
+    const bool sac = a.sac[inst[i]] != 0;
+    for (int buf = 0; buf < kRowBufs; ++buf) {
+      V* Cb = row(i, buf, 0);
+      V* Sb = row(i, buf, 1);
+      if (q == 0)
+        for (int x = tid - PAD; x < 0; x += blockDim.x) Cb[x] = Sb[x] = NEG;  // never rewritten
+      if (q == G - 1)
+        for (int x = G * B + tid; x < G * B + LINE; x += blockDim.x) Cb[x] = Sb[x] = NEG;
+      if (buf == 0)
+        for (int j = j0 + tid; j < j0 + B; j += blockDim.x) {
+          const bool valid = j < ncol[i];
+          Cb[j] = (valid && sac) ? ZERO : NEG;
+          Sb[j] = (valid && !sac) ? ZERO : NEG;
+          if (a.tab_c && valid) {
+            a.tab_c[j] = sac ? 0.0 : -INFINITY;
+            a.tab_s[j] = sac ? -INFINITY : 0.0;
+          }
         }
-      }
+    }
   }
   if (tid == 0) {
     for (int b = 0; b < NSLOT; ++b) {
       mbar_init(&full[b], 1);
       mbar_init(&empty[b], NWARP);
     }
-    *prog = 0;
+    for (int i = 0; i < NI; ++i) prog[i] = 0;
     fence_mbar_init();
   }
   fence_proxy_async_global();
@@ -850,21 +866,22 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
 
   if (warp == NWARP) {
     // ---------------- producer warp ----------------
-    // lane o watches CTA o's progress counter (G <= 16 <= 32 lanes)
+    // lane o watches CTA o's progress counters (G <= 16 <= 32 lanes)
     const uint32_t my_prog = lane < G ? cluster_addr(smem_addr(prog), (uint32_t)lane) : 0u;
-    {
-      uint32_t u = 0;
-      for (int k = 0; k < L; ++k) {  // stage s = k + 1
-        const StageShift sh = a.shifts[lo + k];  // issued before the wait: latency overlaps it
+    uint32_t u = 0;
+    for (int k = 0; k < maxL; ++k) {  // stage k of each instance in turn
+      for (int i = 0; i < ni; ++i) {
+        if (k >= L[i]) continue;
+        const StageShift sh = a.shifts[lo[i] + k];  // issued before the wait: latency overlaps it
         // every CTA <= q finished stage k (row k ready), every CTA finished k-1
         const uint32_t need = lane < G ? (uint32_t)(lane <= q ? k : max(k - 1, 0)) : 0u;
-        while (!__all_sync(0xffffffffu, lane >= G || ld_cluster_relaxed(my_prog) >= need)) {
+        while (!__all_sync(0xffffffffu, lane >= G || ld_cluster_relaxed(my_prog + 4u * i) >= need)) {
         }
         if (lane == 0) {
           fence_acq_rel_cluster();
           fence_proxy_async_global();
-          const V* Cc = row(k % kRowBufs, 0);
-          const V* Sc = row(k % kRowBufs, 1);
+          const V* Cc = row(i, k % kRowBufs, 0);
+          const V* Sc = row(i, k % kRowBufs, 1);
           const V* src[4] = {Cc, Sc, Sc, Cc};
           const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
           for (int c = 0; c < NC; ++c, ++u) {
@@ -886,82 +903,85 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
   } else {
     // ---------------- compute warps ----------------
     const uint64_t pol = evict_first_policy();
-    uint32_t* bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off);
     uint32_t u = 0;
-    // stage records are software-pipelined one stage ahead so their global
-    // load latency never sits at a stage boundary
-    StageShift sh_next = a.shifts[lo];
-    int64_t rbits_next = a.rv[lo];
-    for (int k = 0; k < L; ++k) {
-      const StageShift sh = sh_next;
-      const int64_t rbits = rbits_next;
-      if (k + 1 < L) {
-        sh_next = a.shifts[lo + k + 1];
-        rbits_next = a.rv[lo + k + 1];
-      }
-      const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
-      V* Cn = row((k + 1) % kRowBufs, 0);
-      V* Sn = row((k + 1) % kRowBufs, 1);
-      uint32_t* bprow = bpw + (int64_t)k * row_words + warp * bp_words(MODE);
-      for (int c = 0; c < NC; ++c, ++u) {
-        const int slot = (int)(u % NSLOT);
-        const int c0 = j0 + c * CH, ctop = c0 + CH;
-        const V* ws = slots + slot * 4 * WIN + tid;
-        const V* pca = ws + 0 * WIN + ((c0 - min(sh.i, ctop)) & (AL - 1));
-        const V* pcb = ws + 1 * WIN + ((c0 - min(sh.id, ctop)) & (AL - 1));
-        const V* psa = ws + 2 * WIN + ((c0 - min(sh.s, ctop)) & (AL - 1));
-        const V* psb = ws + 3 * WIN + ((c0 - min(sh.su, ctop)) & (AL - 1));
-        uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
-        mbar_wait(&full[slot], (u / NSLOT) & 1);
-        V cn[E], sn[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int j = c0 + e * T + tid;
-          const CellFlags f = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk,
-                                                   j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su,
-                                                   cn[e], sn[e]);
-          emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f, pol);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done reading the slot
-        V* qc = Cn + c0 + tid;
-        V* qs = Sn + c0 + tid;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          qc[e * T] = cn[e];
-          qs[e * T] = sn[e];
-        }
-        if (a.tab_c) {
+    for (int k = 0; k < maxL; ++k) {
+      for (int i = 0; i < ni; ++i) {
+        if (k >= L[i]) continue;
+        const StageShift sh = a.shifts[lo[i] + k];
+        const int64_t rbits = a.rv[lo[i] + k];
+        const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
+        V* Cn = row(i, (k + 1) % kRowBufs, 0);
+        V* Sn = row(i, (k + 1) % kRowBufs, 1);
+        const DpWork wk = a.work[first + i];
+        uint32_t* bprow = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off) + (int64_t)k * row_words[i] +
+                          warp * bp_words(MODE);
+        for (int c = 0; c < NC; ++c, ++u) {
+          const int slot = (int)(u % NSLOT);
+          const int c0 = j0 + c * CH, ctop = c0 + CH;
+          const V* ws = slots + slot * 4 * WIN + tid;
+          const V* pca = ws + 0 * WIN + ((c0 - min(sh.i, ctop)) & (AL - 1));
+          const V* pcb = ws + 1 * WIN + ((c0 - min(sh.id, ctop)) & (AL - 1));
+          const V* psa = ws + 2 * WIN + ((c0 - min(sh.s, ctop)) & (AL - 1));
+          const V* psb = ws + 3 * WIN + ((c0 - min(sh.su, ctop)) & (AL - 1));
+          uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
+          mbar_wait(&full[slot], (u / NSLOT) & 1);
+          V cn[E], sn[E];
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int j = c0 + e * T + tid;
-            if (j < ncol) {
-              a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn[e], g);
-              a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn[e], g);
+            const CellFlags f = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk,
+                                                     j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su,
+                                                     cn[e], sn[e]);
+            emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f, pol);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done reading the slot
+          V* qc = Cn + c0 + tid;
+          V* qs = Sn + c0 + tid;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            qc[e * T] = cn[e];
+            qs[e * T] = sn[e];
+          }
+          if (a.tab_c) {
+            const int nc = ncol[i];
+            const double g = a.info[inst[i]].scale;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const int j = c0 + e * T + tid;
+              if (j < nc) {
+                a.tab_c[(int64_t)(k + 1) * nc + j] = to_f64(cn[e], g);
+                a.tab_s[(int64_t)(k + 1) * nc + j] = to_f64(sn[e], g);
+              }
             }
           }
         }
-      }
-      // publish row k+1 of this CTA's block
-      named_barrier(1, T);
-      if (tid == 0) {
-        fence_acq_rel_cluster();
-        fence_proxy_async_global();
-        st_cluster_release(prog, (uint32_t)(k + 1));
+        // publish row k+1 of this CTA's block of instance i
+        named_barrier(1, T);
+        if (tid == 0) {
+          fence_acq_rel_cluster();
+          fence_proxy_async_global();
+          st_cluster_release(prog + i, (uint32_t)(k + 1));
+        }
       }
     }
   }
   __syncthreads();
-  cluster_barrier();  // no CTA leaves while others may still read its counter
-  if (tid == 0 && ncol - 1 >= j0 && ncol - 1 < j0 + B) {
-    a.info[inst].end_c = to_f64(row(L % kRowBufs, 0)[ncol - 1], g);
-    a.info[inst].end_s = to_f64(row(L % kRowBufs, 1)[ncol - 1], g);
+  cluster_barrier();  // no CTA leaves while others may still read its counters
+  for (int i = 0; i < ni; ++i) {
+    const int nc = ncol[i];
+    if (tid == 0 && nc - 1 >= j0 && nc - 1 < j0 + B) {
+      const double g = a.info[inst[i]].scale;
+      a.info[inst[i]].end_c = to_f64(row(i, L[i] % kRowBufs, 0)[nc - 1], g);
+      a.info[inst[i]].end_s = to_f64(row(i, L[i] % kRowBufs, 1)[nc - 1], g);
+    }
   }
   __syncthreads();
   // the rows are dead: drop their L2 lines instead of writing them back
-  for (int buf = 0; buf < kRowBufs; ++buf)
-    for (int rs = 0; rs < 2; ++rs)
-      for (int x = tid * LINE; x < B; x += blockDim.x * LINE) discard_l2(row(buf, rs) + j0 + x);
+  for (int i = 0; i < ni; ++i)
+    for (int buf = 0; buf < kRowBufs; ++buf)
+      for (int rs = 0; rs < 2; ++rs)
+        for (int x = tid * LINE; x < B; x += blockDim.x * LINE) discard_l2(row(i, buf, rs) + j0 + x);
 }
 
 // ---------------------------------------------------------------------------
@@ -1764,9 +1784,18 @@ size_t stream_row_bytes(int mode, const StreamGeom& g) {
   return 2 * kRowBufs * (size_t)stream_span(mode, g) * value_bytes(mode);
 }
 
+// instances per cluster of the streaming kernel (1 or 2; SPLITPLAN_STREAM_PAIR).
+// Pairs were measured slower on B200 (3.4-4.1e11 vs 4.4e11 cells/s at W = 1e5:
+// the doubled L2 footprint costs more than the hidden stage latency saves).
+int stream_pair() {
+  static int p = 0;
+  if (!p) p = env_int("SPLITPLAN_STREAM_PAIR", 1) == 2 ? 2 : 1;
+  return p;
+}
+
 template <int MODE, int T>
 int stream_occupancy_t() {
-  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>()>;
+  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>(), 2>;
   int n = 0;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(MODE)) !=
           cudaSuccess ||
@@ -1800,37 +1829,41 @@ int stream_resident_ctas(int mode) {
 }
 
 // Cluster size: at least large enough that the rows of every co-resident
-// instance fit the L2 budget; among those, the G minimising G * (NC + 2) --
-// the CTA-time of one stage in chunk units, padding waste included, plus
-// about two chunks of stage-synchronisation latency per CTA (measured on
-// B200: at W = 1e5, G = 7 x 14 chunks beats 8 x 13 and 14 x 7).
+// instance (stream_pair() per cluster) fit the L2 budget; among those, the G
+// minimising G * (NC + sync) -- the CTA-time of one stage in chunk units,
+// padding waste included, plus the stage-synchronisation latency per CTA
+// (about two chunks for single instances, measured on B200: at W = 1e5,
+// G = 7 x 14 chunks beats 8 x 13 and 14 x 7; paired instances hide most of
+// it behind the partner's stage).
 StreamGeom stream_geom(int mode, int64_t ncol) {
   const int64_t nchunks = (ncol + stream_ch() - 1) / stream_ch();
   const int resident = stream_resident_ctas(mode);
   const int force = env_int("SPLITPLAN_DP_CLUSTER", 0);
   auto geom = [&](int G) {
-    StreamGeom t{G, (int)((nchunks + G - 1) / G)};
+    StreamGeom t{G, (int)((nchunks + G - 1) / G), 0};
     t.G = (int)((nchunks + t.NC - 1) / t.NC);
     return t;
   };
   if (force >= 1 && force <= 16) return geom(force);
+  const int pair = stream_pair();
+  const int sync = pair == 2 ? 0 : 2;
   int gmin = 16;
   for (int G = 1; G <= 16; ++G)
-    if ((size_t)(resident / G) * stream_row_bytes(mode, geom(G)) <= l2_row_budget()) {
+    if ((size_t)(resident / G) * pair * stream_row_bytes(mode, geom(G)) <= l2_row_budget()) {
       gmin = G;
       break;
     }
   StreamGeom best = geom(gmin);
   for (int G = gmin + 1; G <= 16; ++G) {
     const StreamGeom t = geom(G);
-    if ((int64_t)t.G * (t.NC + 2) < (int64_t)best.G * (best.NC + 2)) best = t;
+    if ((int64_t)t.G * (t.NC + sync) < (int64_t)best.G * (best.NC + sync)) best = t;
   }
   return best;
 }
 
-template <int MODE, int T>
+template <int MODE, int T, int NI>
 int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
-  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>()>;
+  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>(), NI>;
   const size_t smem = stream_smem(MODE);
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "cudaFuncSetAttribute(dp_stream_kernel)");
@@ -1840,8 +1873,9 @@ int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream
                     "cudaFuncSetAttribute(non-portable cluster)");
     if (rc) return rc;
   }
+  geo.n_items = (int)n_items;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(n_items * geo.G), 1, 1);
+  cfg.gridDim = dim3((unsigned)((n_items + NI - 1) / NI * geo.G), 1, 1);
   cfg.blockDim = dim3((unsigned)(T + 32), 1, 1);  // + the producer warp
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -1858,8 +1892,11 @@ int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream
 }
 template <int MODE>
 int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
-  return stream_threads() == 128 ? launch_stream_t<MODE, 128>(a, n_items, geo, st)
-                                 : launch_stream_t<MODE, 256>(a, n_items, geo, st);
+  if (stream_pair() == 2)
+    return stream_threads() == 128 ? launch_stream_t<MODE, 128, 2>(a, n_items, geo, st)
+                                   : launch_stream_t<MODE, 256, 2>(a, n_items, geo, st);
+  return stream_threads() == 128 ? launch_stream_t<MODE, 128, 1>(a, n_items, geo, st)
+                                 : launch_stream_t<MODE, 256, 1>(a, n_items, geo, st);
 }
 
 // ---- cluster (DSMEM rows) and cooperative (L2 rows, LDG) kernels ------------
