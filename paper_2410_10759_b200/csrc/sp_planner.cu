@@ -789,7 +789,7 @@ __host__ __device__ constexpr int stream_pad() { return CH + 128 / (int)sizeof(V
 // ...): while the producer waits for the other CTAs to finish instance A's
 // stage k, the compute warps work through instance B's stage k, so the
 // stage synchronisation latency overlaps useful work.
-template <int MODE, int T, int E, int NSLOT, int NI>
+template <int MODE, int T, int E, int NSLOT, int NI, int NBUF>
 __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(DpArgs a, StreamGeom geo) {
   using V = typename VT<MODE>::T;
   constexpr int CH = T * E;
@@ -833,7 +833,7 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
 
   for (int i = 0; i < ni; ++i) {
     const bool sac = a.sac[inst[i]] != 0;
-    for (int buf = 0; buf < kRowBufs; ++buf) {
+    for (int buf = 0; buf < NBUF; ++buf) {
       V* Cb = row(i, buf, 0);
       V* Sb = row(i, buf, 1);
       if (q == 0)
@@ -873,15 +873,17 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
       for (int i = 0; i < ni; ++i) {
         if (k >= L[i]) continue;
         const StageShift sh = a.shifts[lo[i] + k];  // issued before the wait: latency overlaps it
-        // every CTA <= q finished stage k (row k ready), every CTA finished k-1
-        const uint32_t need = lane < G ? (uint32_t)(lane <= q ? k : max(k - 1, 0)) : 0u;
+        // every CTA <= q finished stage k (row k ready); WAR on the buffer this
+        // stage overwrites: with 3 buffers every CTA finished k-1, with 2 every CTA k
+        const uint32_t need =
+            lane < G ? (uint32_t)(lane <= q || NBUF == 2 ? k : max(k - 1, 0)) : 0u;
         while (!__all_sync(0xffffffffu, lane >= G || ld_cluster_relaxed(my_prog + 4u * i) >= need)) {
         }
         if (lane == 0) {
           fence_acq_rel_cluster();
           fence_proxy_async_global();
-          const V* Cc = row(i, k % kRowBufs, 0);
-          const V* Sc = row(i, k % kRowBufs, 1);
+          const V* Cc = row(i, k % NBUF, 0);
+          const V* Sc = row(i, k % NBUF, 1);
           const V* src[4] = {Cc, Sc, Sc, Cc};
           const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
           for (int c = 0; c < NC; ++c, ++u) {
@@ -910,8 +912,8 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
         const StageShift sh = a.shifts[lo[i] + k];
         const int64_t rbits = a.rv[lo[i] + k];
         const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
-        V* Cn = row(i, (k + 1) % kRowBufs, 0);
-        V* Sn = row(i, (k + 1) % kRowBufs, 1);
+        V* Cn = row(i, (k + 1) % NBUF, 0);
+        V* Sn = row(i, (k + 1) % NBUF, 1);
         const DpWork wk = a.work[first + i];
         uint32_t* bprow = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off) + (int64_t)k * row_words[i] +
                           warp * bp_words(MODE);
@@ -972,14 +974,14 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
     const int nc = ncol[i];
     if (tid == 0 && nc - 1 >= j0 && nc - 1 < j0 + B) {
       const double g = a.info[inst[i]].scale;
-      a.info[inst[i]].end_c = to_f64(row(i, L[i] % kRowBufs, 0)[nc - 1], g);
-      a.info[inst[i]].end_s = to_f64(row(i, L[i] % kRowBufs, 1)[nc - 1], g);
+      a.info[inst[i]].end_c = to_f64(row(i, L[i] % NBUF, 0)[nc - 1], g);
+      a.info[inst[i]].end_s = to_f64(row(i, L[i] % NBUF, 1)[nc - 1], g);
     }
   }
   __syncthreads();
   // the rows are dead: drop their L2 lines instead of writing them back
   for (int i = 0; i < ni; ++i)
-    for (int buf = 0; buf < kRowBufs; ++buf)
+    for (int buf = 0; buf < NBUF; ++buf)
       for (int rs = 0; rs < 2; ++rs)
         for (int x = tid * LINE; x < B; x += blockDim.x * LINE) discard_l2(row(i, buf, rs) + j0 + x);
 }
@@ -1758,12 +1760,8 @@ constexpr int kStreamE = 4;
 template <int MODE> constexpr int ring_slots() { return MODE == VM_INT32 ? 6 : 3; }
 inline int ring_slots_rt(int mode) { return mode == VM_INT32 ? 6 : 3; }
 
-// compute threads of the streaming kernel (128 or 256; SPLITPLAN_STREAM_T)
-int stream_threads() {
-  static int t = 0;
-  if (!t) t = env_int("SPLITPLAN_STREAM_T", 256) == 128 ? 128 : 256;
-  return t;
-}
+// compute threads of the streaming kernel (256: 128 was measured slower)
+int stream_threads() { return 256; }
 int64_t stream_ch() { return (int64_t)stream_threads() * kStreamE; }
 // live rows of co-resident instances kept in L2 (SPLITPLAN_L2_BUDGET_MB)
 size_t l2_row_budget() {
@@ -1780,8 +1778,15 @@ int64_t stream_span(int mode, const StreamGeom& g) {
   const int64_t line = 128 / (int64_t)value_bytes(mode);
   return (stream_ch() + line) + (int64_t)g.G * g.NC * stream_ch() + line;
 }
+// row buffers of the streaming kernel: 3 (one stage of slack between CTAs)
+// or 2 (full-barrier semantics, 2/3 of the L2 footprint); SPLITPLAN_STREAM_BUFS
+int stream_bufs() {
+  static int b = 0;
+  if (!b) b = env_int("SPLITPLAN_STREAM_BUFS", 3) == 2 ? 2 : 3;
+  return b;
+}
 size_t stream_row_bytes(int mode, const StreamGeom& g) {
-  return 2 * kRowBufs * (size_t)stream_span(mode, g) * value_bytes(mode);
+  return 2 * (size_t)stream_bufs() * (size_t)stream_span(mode, g) * value_bytes(mode);
 }
 
 // instances per cluster of the streaming kernel (1 or 2; SPLITPLAN_STREAM_PAIR).
@@ -1795,7 +1800,7 @@ int stream_pair() {
 
 template <int MODE, int T>
 int stream_occupancy_t() {
-  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>(), 2>;
+  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>(), 2, 3>;
   int n = 0;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(MODE)) !=
           cudaSuccess ||
@@ -1807,7 +1812,7 @@ int stream_occupancy_t() {
 }
 template <int MODE>
 int stream_occupancy() {
-  return stream_threads() == 128 ? stream_occupancy_t<MODE, 128>() : stream_occupancy_t<MODE, 256>();
+  return stream_occupancy_t<MODE, 256>();
 }
 
 // co-resident streaming CTAs on this device (cached per value domain)
@@ -1861,9 +1866,9 @@ StreamGeom stream_geom(int mode, int64_t ncol) {
   return best;
 }
 
-template <int MODE, int T, int NI>
+template <int MODE, int T, int NI, int NBUF>
 int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
-  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>(), NI>;
+  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>(), NI, NBUF>;
   const size_t smem = stream_smem(MODE);
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "cudaFuncSetAttribute(dp_stream_kernel)");
@@ -1892,11 +1897,13 @@ int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream
 }
 template <int MODE>
 int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
-  if (stream_pair() == 2)
-    return stream_threads() == 128 ? launch_stream_t<MODE, 128, 2>(a, n_items, geo, st)
-                                   : launch_stream_t<MODE, 256, 2>(a, n_items, geo, st);
-  return stream_threads() == 128 ? launch_stream_t<MODE, 128, 1>(a, n_items, geo, st)
-                                 : launch_stream_t<MODE, 256, 1>(a, n_items, geo, st);
+  const int sel = (stream_pair() == 2 ? 1 : 0) + (stream_bufs() == 2 ? 2 : 0);
+  switch (sel) {
+    case 0: return launch_stream_t<MODE, 256, 1, 3>(a, n_items, geo, st);
+    case 1: return launch_stream_t<MODE, 256, 2, 3>(a, n_items, geo, st);
+    case 2: return launch_stream_t<MODE, 256, 1, 2>(a, n_items, geo, st);
+    default: return launch_stream_t<MODE, 256, 2, 2>(a, n_items, geo, st);
+  }
 }
 
 // ---- cluster (DSMEM rows) and cooperative (L2 rows, LDG) kernels ------------
