@@ -738,6 +738,22 @@ __device__ __forceinline__ void st_cluster_release(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ void fence_acq_rel_cluster() {
   asm volatile("fence.acq_rel.cluster;" ::: "memory");
 }
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t evict_normal_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_hint(int32_t* p, int32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -772,9 +788,10 @@ __device__ __forceinline__ void emit_bp_stream(uint32_t* words, CellFlags f, uin
 }
 
 struct StreamGeom {
-  int G;        // CTAs per instance (cluster size)
-  int NC;       // chunks per CTA
-  int n_items;  // instances of the launch (set at launch)
+  int G;         // CTAs per instance (cluster size)
+  int NC;        // chunks per CTA
+  int n_items;   // instances of the launch (set at launch)
+  int row_hint;  // L2 policy of the row stores (set at launch)
 };
 
 constexpr int kRowBufs = 3;
@@ -905,6 +922,9 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
   } else {
     // ---------------- compute warps ----------------
     const uint64_t pol = evict_first_policy();
+    // the rows are re-read next stage: keep them in L2 ahead of the streamed
+    // back-pointers (geo.row_hint 0: normal, 1: evict_last)
+    const uint64_t rpol = geo.row_hint ? evict_last_policy() : evict_normal_policy();
     uint32_t u = 0;
     for (int k = 0; k < maxL; ++k) {
       for (int i = 0; i < ni; ++i) {
@@ -942,8 +962,8 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
           V* qs = Sn + c0 + tid;
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            qc[e * T] = cn[e];
-            qs[e * T] = sn[e];
+            st_hint(qc + e * T, cn[e], rpol);
+            st_hint(qs + e * T, sn[e], rpol);
           }
           if (a.tab_c) {
             const int nc = ncol[i];
@@ -1778,11 +1798,12 @@ int64_t stream_span(int mode, const StreamGeom& g) {
   const int64_t line = 128 / (int64_t)value_bytes(mode);
   return (stream_ch() + line) + (int64_t)g.G * g.NC * stream_ch() + line;
 }
-// row buffers of the streaming kernel: 3 (one stage of slack between CTAs)
-// or 2 (full-barrier semantics, 2/3 of the L2 footprint); SPLITPLAN_STREAM_BUFS
+// row buffers of the streaming kernel: 2 (full-barrier semantics, default:
+// 2/3 of the L2 footprint lets G shrink to 5 at W = 1e5, measured 4.5e11 vs
+// 4.4e11 cells/s with 3) or 3 (one stage of slack); SPLITPLAN_STREAM_BUFS
 int stream_bufs() {
   static int b = 0;
-  if (!b) b = env_int("SPLITPLAN_STREAM_BUFS", 3) == 2 ? 2 : 3;
+  if (!b) b = env_int("SPLITPLAN_STREAM_BUFS", 2) == 3 ? 3 : 2;
   return b;
 }
 size_t stream_row_bytes(int mode, const StreamGeom& g) {
@@ -1845,7 +1866,7 @@ StreamGeom stream_geom(int mode, int64_t ncol) {
   const int resident = stream_resident_ctas(mode);
   const int force = env_int("SPLITPLAN_DP_CLUSTER", 0);
   auto geom = [&](int G) {
-    StreamGeom t{G, (int)((nchunks + G - 1) / G), 0};
+    StreamGeom t{G, (int)((nchunks + G - 1) / G), 0, 0};
     t.G = (int)((nchunks + t.NC - 1) / t.NC);
     return t;
   };
@@ -1879,6 +1900,7 @@ int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream
     if (rc) return rc;
   }
   geo.n_items = (int)n_items;
+  geo.row_hint = env_int("SPLITPLAN_ROW_EVICT_LAST", 0) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((n_items + NI - 1) / NI * geo.G), 1, 1);
   cfg.blockDim = dim3((unsigned)(T + 32), 1, 1);  // + the producer warp
@@ -2036,7 +2058,7 @@ struct DpPlan {
   int cfg = 0;                  // single-CTA T x E configuration
   int threads = 0;
   ClusterGeom cgeo{0, 0, 0};    // cluster / coop
-  StreamGeom sgeo{0, 0};        // stream
+  StreamGeom sgeo{0, 0, 0, 0};  // stream
   size_t bp = 0, rows = 0, smem = 0;
   int64_t bp_row_words = 0;
   // launches sharing a key go out together

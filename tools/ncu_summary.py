@@ -29,11 +29,14 @@ KEYS = {
     "warp_inst": "smsp__inst_executed.sum",
     "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
     "sm_clock_hz": "sm__cycles_elapsed.avg.per_second",
+    "lts_sectors_per_s": "lts__t_sectors.sum.per_second",
+    "lts_sectors_pct": "lts__t_sectors.avg.pct_of_peak_sustained_elapsed",
+    "smem_wavefront_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
     "grid": "launch__grid_size",
     "block": "launch__block_size",
     "cluster": "launch__cluster_dim_x",
 }
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1e-3, "us": 1e-6,
+SCALE = {"sector/ns": 1e9, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1e-3, "us": 1e-6,
          "ns": 1e-9, "s": 1, "Ghz": 1e9, "Mhz": 1e6, "hz": 1}
 
 
@@ -69,6 +72,9 @@ def main():
         "warp_inst_per_cell": out.get("warp_inst", 0) / cells,
         "cells_per_s_under_ncu": cells / secs,
     })
+    if out.get("lts_sectors_per_s") and out.get("lts_sectors_pct"):
+        # the L2 (LTS) sector-throughput peak this capture implies
+        out["l2_peak_Bps_implied"] = out["lts_sectors_per_s"] * 32 / (out["lts_sectors_pct"] / 100)
     print(json.dumps(out, indent=1))
 
 
