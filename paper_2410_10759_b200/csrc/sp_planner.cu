@@ -743,11 +743,6 @@ __device__ __forceinline__ uint64_t evict_last_policy() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-__device__ __forceinline__ uint64_t evict_normal_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
 __device__ __forceinline__ void st_hint(int32_t* p, int32_t v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
 }
@@ -792,6 +787,8 @@ struct StreamGeom {
   int NC;        // chunks per CTA
   int n_items;   // instances of the launch (set at launch)
   int row_hint;  // L2 policy of the row stores (set at launch)
+  int diag;      // diagnostics only (SPLITPLAN_STREAM_DIAG; results are wrong when set):
+                 // bit 0 skips the stage waits, bit 1 skips the window copies
 };
 
 constexpr int kRowBufs = 3;
@@ -807,7 +804,7 @@ __host__ __device__ constexpr int stream_pad() { return CH + 128 / (int)sizeof(V
 // stage k, the compute warps work through instance B's stage k, so the
 // stage synchronisation latency overlaps useful work.
 template <int MODE, int T, int E, int NSLOT, int NI, int NBUF>
-__global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(DpArgs a, StreamGeom geo) {
+__global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGeom geo) {
   using V = typename VT<MODE>::T;
   constexpr int CH = T * E;
   constexpr int AL = 16 / (int)sizeof(V);        // values per 16 B
@@ -894,7 +891,8 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
         // stage overwrites: with 3 buffers every CTA finished k-1, with 2 every CTA k
         const uint32_t need =
             lane < G ? (uint32_t)(lane <= q || NBUF == 2 ? k : max(k - 1, 0)) : 0u;
-        while (!__all_sync(0xffffffffu, lane >= G || ld_cluster_relaxed(my_prog + 4u * i) >= need)) {
+        while (!(geo.diag & 1) &&
+               !__all_sync(0xffffffffu, lane >= G || ld_cluster_relaxed(my_prog + 4u * i) >= need)) {
         }
         if (lane == 0) {
           fence_acq_rel_cluster();
@@ -907,6 +905,10 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
             const int slot = (int)(u % NSLOT);
             mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
             const int c0 = j0 + c * CH, ctop = c0 + CH;
+            if (geo.diag & 2) {
+              mbar_arrive(&full[slot]);
+              continue;
+            }
             mbar_expect_tx(&full[slot], 4u * WIN * sizeof(V));
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
@@ -924,7 +926,7 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
     const uint64_t pol = evict_first_policy();
     // the rows are re-read next stage: keep them in L2 ahead of the streamed
     // back-pointers (geo.row_hint 0: normal, 1: evict_last)
-    const uint64_t rpol = geo.row_hint ? evict_last_policy() : evict_normal_policy();
+    const uint64_t rpol = evict_last_policy();
     uint32_t u = 0;
     for (int k = 0; k < maxL; ++k) {
       for (int i = 0; i < ni; ++i) {
@@ -960,10 +962,18 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
           if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done reading the slot
           V* qc = Cn + c0 + tid;
           V* qs = Sn + c0 + tid;
+          if (geo.row_hint) {
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            st_hint(qc + e * T, cn[e], rpol);
-            st_hint(qs + e * T, sn[e], rpol);
+            for (int e = 0; e < E; ++e) {
+              st_hint(qc + e * T, cn[e], rpol);
+              st_hint(qs + e * T, sn[e], rpol);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              qc[e * T] = cn[e];
+              qs[e * T] = sn[e];
+            }
           }
           if (a.tab_c) {
             const int nc = ncol[i];
@@ -1004,6 +1014,316 @@ __global__ void __launch_bounds__(T + 32, (T <= 128 ? 4 : 2)) dp_stream_kernel(D
     for (int buf = 0; buf < NBUF; ++buf)
       for (int rs = 0; rs < 2; ++rs)
         for (int x = tid * LINE; x < B; x += blockDim.x * LINE) discard_l2(row(i, buf, rs) + j0 + x);
+}
+
+// ---------------------------------------------------------------------------
+// K2 own-block variant (int32 domain; EXPERIMENTAL, forced only with
+// SPLITPLAN_DP_VARIANT=own): a cluster of G CTAs per instance, CTA q owning
+// columns [q*B, (q+1)*B) of both rows in its own shared memory, updated in
+// place top-down like the single-CTA kernel.  Only what other CTAs need goes
+// through L2:
+//  * a predecessor window (C or S row shifted by i, i+d, s or s+u) that lies
+//    entirely in the own block is read straight from shared memory; windows
+//    reaching left of the block are bulk-copied from the previous row's global
+//    copy into per-window ring slots (full/empty mbarriers), and a window
+//    straddling the block edge gets its own part patched into the slot;
+//  * column p of the new row is stored to the global copy only if a CTA to
+//    the right reads it next stage: p >= (q+1)*B - max(next stage's shifts).
+// At cfg2 widths that removes ~3/4 of the window reads and ~1/3 of the row
+// writes of the streaming kernel.  Ordering: the producer waits, per window,
+// until the CTAs owning its remote columns published the previous row (RAW),
+// and before the compute warps overwrite a global row buffer it checks that
+// every CTA to the right has finished the stage that read it (WAR, NBUF
+// buffers); a publisher warp releases the CTA's progress at cluster scope off
+// the compute critical path, so stages pipeline as a wavefront.
+// Measured on B200 (profiles/r01/own_experiment): 2.3e11 cells/s at cfg2
+// against 4.7e11 for the streaming kernel, and 4.6e11 vs 1.0e12 for the
+// single-CTA kernel at W = 1e4: the L2 traffic it saves is not what bounds
+// the streaming kernel (removing every window copy there gains only 35 %),
+// while its per-chunk bookkeeping doubles the instructions per cell and one
+// CTA per SM halves the warps that hide the per-chunk barrier.  Kept with
+// parity tests as a recorded experiment, not selected automatically.
+struct OwnGeom {
+  int G;        // CTAs per instance (cluster size)
+  int NC;       // chunks per CTA
+  int n_items;  // instances of the launch
+  int pad;
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+
+// kind of a predecessor window [start, start + CH) for CTA q owning columns from j0:
+// 0 = own (shared memory; for q == 0 also the NEG pad below column 0),
+// 1 = remote (slot), 2 = straddles the block edge (remote part from the slot)
+template <int CH>
+__device__ __forceinline__ int own_win_kind(int q, int j0, int start) {
+  if (q == 0 || start >= j0) return 0;
+  return start + CH <= j0 ? 1 : 2;
+}
+
+template <int MODE, int T, int E, int NSW, int NBUF>
+__global__ void __launch_bounds__(T + 64, (T <= 256 ? 2 : 1)) dp_own_kernel(DpArgs a, OwnGeom geo) {
+  using V = typename VT<MODE>::T;
+  constexpr int CH = T * E;
+  constexpr int AL = 16 / (int)sizeof(V);
+  constexpr int WIN = CH + AL;
+  constexpr int PAD = stream_pad<V, CH>();
+  constexpr int LINE = 128 / (int)sizeof(V);
+  constexpr int NWARP = T / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [NSW]
+  uint64_t* empty = full + NSW;                         // [NSW]
+  uint32_t* prog = reinterpret_cast<uint32_t*>(empty + NSW);  // stages published
+  uint32_t* war = prog + 1;                                   // stages cleared for global stores
+  uint32_t* done = prog + 2;                                  // stages finished by the compute warps
+
+  const int G = geo.G, NC = geo.NC;
+  const int B = NC * CH;
+  const int q = (int)cluster_rank();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const DpWork wk = a.work[blockIdx.x / G];
+  const int64_t inst = wk.inst;
+  const int64_t lo = a.layer_off[inst];
+  const int L = (int)(a.layer_off[inst + 1] - lo);
+  const int ncol = (int)(a.info[inst].w_eff + 1);
+  const bool sac = a.sac[inst] != 0;
+  const int j0 = q * B;
+  const int64_t span = (int64_t)PAD + (int64_t)G * B + LINE;
+  V* const gbase = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][PAD + G*B + LINE]
+  auto grow = [&](int buf, int rs) { return gbase + (int64_t)(buf * 2 + rs) * span + PAD; };
+  V* const ownC = reinterpret_cast<V*>(smem + 256) + CH;  // [CH pad | B own columns]
+  V* const ownS = ownC + B + CH;
+  V* const slots = ownS + B;  // [NSW][WIN]
+  const V NEG = VT<MODE>::neg();
+  const V ZERO = V(0);
+
+  // row 0: own block in shared memory and in global buffer 0; NEG pads
+  for (int x = tid - CH; x < B; x += blockDim.x) {
+    const int j = j0 + x;
+    const bool valid = x >= 0 && j < ncol;
+    const V c = (valid && sac) ? ZERO : NEG, s = (valid && !sac) ? ZERO : NEG;
+    ownC[x] = c;
+    ownS[x] = s;
+    if (x >= 0) {
+      grow(0, 0)[j] = c;
+      grow(0, 1)[j] = s;
+    }
+  }
+  for (int buf = 0; buf < NBUF; ++buf) {
+    if (q == 0)
+      for (int x = tid - PAD; x < 0; x += blockDim.x) grow(buf, 0)[x] = grow(buf, 1)[x] = NEG;
+    if (q == G - 1)
+      for (int x = G * B + tid; x < G * B + LINE; x += blockDim.x) grow(buf, 0)[x] = grow(buf, 1)[x] = NEG;
+  }
+  if (tid == 0) {
+    for (int b = 0; b < NSW; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], NWARP);
+    }
+    *prog = 0;
+    *war = 0;
+    *done = 0;
+    fence_mbar_init();
+  }
+  fence_proxy_async_global();
+  __threadfence();
+  cluster_barrier();
+
+  if (warp == NWARP) {
+    // ---------------- producer warp: remote windows + WAR clearance ----------------
+    const uint32_t peer = lane < G ? cluster_addr(smem_addr(prog), (uint32_t)lane) : 0u;
+    uint32_t u = 0;
+    StageShift sh = a.shifts[lo];
+    for (int k = 0; k < L; ++k) {
+      const StageShift shn = a.shifts[lo + min(k + 1, L - 1)];  // prefetch
+      // WAR: the compute warps' stage-k stores go to buffer (k+1) % NBUF, last
+      // read (stage k+1-NBUF) by the CTAs to the right
+      const int war_need = k + 2 - NBUF;
+      if (war_need > 0) {
+        while (!__all_sync(0xffffffffu, lane <= q || lane >= G || ld_cluster_relaxed(peer) >= (uint32_t)war_need)) {
+        }
+        if (lane == 0) fence_acq_rel_cluster();
+      }
+      if (lane == 0) st_release_cta(war, (uint32_t)(k + 1));
+      uint32_t ready = 0;  // lanes (CTAs) known to have published row k
+      const V* Cr = grow(k % NBUF, 0);
+      const V* Sr = grow(k % NBUF, 1);
+      const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
+      for (int c = NC - 1; c >= 0; --c) {
+        const int c0 = j0 + c * CH, ctop = c0 + CH;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int start = c0 - min(shf[w], ctop);
+          if (own_win_kind<CH>(q, j0, start) == 0) continue;
+          // RAW: owners of the remote columns [max(start, 0), min(start + CH, j0))
+          const int hi_col = min(start + CH, j0) - 1;
+          const int olo = max(start, 0) / B;
+          const int ohi = hi_col >= 0 ? hi_col / B : -1;
+          const uint32_t want = (ohi >= olo) ? ((0xffffffffu >> (31 - ohi)) & (0xffffffffu << olo)) : 0u;
+          if ((ready & want) != want) {
+            do {
+              ready = __ballot_sync(0xffffffffu, lane < G && ld_cluster_relaxed(peer) >= (uint32_t)k);
+            } while ((ready & want) != want);
+            if (lane == 0) {
+              fence_acq_rel_cluster();
+              fence_proxy_async_global();
+            }
+          }
+          if (lane == 0) {
+            // the window's columns left of the block (all of it unless it
+            // straddles the edge; the compute warps fill in the own part)
+            const int sa = start & ~(AL - 1);
+            const uint32_t bytes = (uint32_t)(min(WIN, j0 - sa) * (int)sizeof(V));
+            const int slot = (int)(u % NSW);
+            mbar_wait(&empty[slot], ((u / NSW) & 1) ^ 1);
+            mbar_expect_tx(&full[slot], bytes);
+            const V* src = (w == 0 || w == 3) ? Cr : Sr;
+            bulk_g2s(slots + slot * WIN, src + sa, bytes, &full[slot]);
+          }
+          ++u;
+          __syncwarp();
+        }
+      }
+      sh = shn;
+    }
+  } else if (warp == NWARP + 1) {
+    // ---------------- publisher warp ----------------
+    // publishes the latest stage the compute warps finished (their stores are
+    // ordered before `done` by their stage-end barrier); the compute warps never
+    // wait for it, and a slow release simply covers several stages at once
+    if (lane == 0) {
+      uint32_t pub = 0;
+      while (pub < (uint32_t)L) {
+        const uint32_t d = ld_acquire_cta(done);
+        if (d == pub) {
+          __nanosleep(64);
+          continue;
+        }
+        fence_acq_rel_cluster();
+        st_cluster_release(prog, d);
+        pub = d;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- compute warps ----------------
+    // Every predecessor read is an index into the shared array `sv` (so it is
+    // an LDS): own rows at ownC / ownS, ring slots at slots.
+    V* const sv = reinterpret_cast<V*>(smem);
+    const int iC = (int)(ownC - sv), iS = (int)(ownS - sv), iSl = (int)(slots - sv);
+    const uint64_t pol = evict_first_policy();
+    uint32_t* const bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off) + warp * bp_words(MODE);
+    const int64_t row_words = wk.bp_row_words;
+    uint32_t u = 0;
+    StageShift sh = a.shifts[lo];
+    StageShift shn = a.shifts[lo + min(1, L - 1)];
+    int64_t rbits = a.rv[lo];
+    for (int k = 0; k < L; ++k) {
+      const StageShift shn2 = a.shifts[lo + min(k + 2, L - 1)];  // prefetch
+      const int64_t rbn = a.rv[lo + min(k + 1, L - 1)];
+      const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
+      // global copy: only the columns a CTA to the right reads next stage
+      int thrC = INT_MAX, thrS = INT_MAX;
+      if (k + 1 < L && q + 1 < G) {
+        thrC = j0 + B - max(shn.i, shn.su);
+        thrS = j0 + B - max(shn.id, shn.s);
+      }
+      const int thr = min(thrC, thrS);
+      V* const gC = grow((k + 1) % NBUF, 0);
+      V* const gS = grow((k + 1) % NBUF, 1);
+      uint32_t* const bprow = bpw + (int64_t)k * row_words;
+      const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
+      const int rowi[4] = {iC - j0, iS - j0, iS - j0, iC - j0};  // own index of column p: rowi + p
+      bool war_ok = false;
+      for (int c = NC - 1; c >= 0; --c) {
+        const int c0 = j0 + c * CH, ctop = c0 + CH;
+        int base[4];
+        uint32_t used = 0, strad = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int start = c0 - min(shf[w], ctop);
+          base[w] = rowi[w] + start + tid;  // own-row index of this thread's first predecessor
+          if (q > 0 && start < j0) {        // remote columns: this window has a ring slot
+            const int slot = (int)(u % NSW);
+            mbar_wait(&full[slot], (u / NSW) & 1);
+            ++u;
+            const int sa = start & ~(AL - 1);
+            const int sb = iSl + slot * WIN - sa;  // slot index of column p: sb + p
+            base[w] = sb + start + tid;
+            used |= 1u << w;
+            if (start + CH > j0) {  // straddles the block edge: copy the own part in
+              strad = 1;
+              const int ob = rowi[w];
+              for (int p = j0 + tid; p < start + CH; p += T) sv[sb + p] = sv[ob + p];
+            }
+          }
+        }
+        if (strad) named_barrier(1, T);  // patched slots visible to every compute warp
+        V cn[E], sn[E];
+        uint32_t* const bpc = bprow + (c0 >> 5) * bp_words(MODE);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = c0 + e * T + tid;
+          const CellFlags f = cell_update<MODE, V>(sv[base[0] + e * T], sv[base[1] + e * T],
+                                                   sv[base[2] + e * T], sv[base[3] + e * T], rk,
+                                                   j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
+          emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f, pol);
+        }
+        // release this chunk's ring slots (the same slot sequence as above)
+        __syncwarp();
+        if (lane == 0) {
+          uint32_t v = u;
+#pragma unroll
+          for (int w = 3; w >= 0; --w)
+            if (used & (1u << w)) mbar_arrive(&empty[(int)(--v % NSW)]);
+        }
+        named_barrier(1, T);  // every read of this chunk's predecessors is done: update in place
+        const int oi = iC + (c0 - j0) + tid, os = iS + (c0 - j0) + tid;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          sv[oi + e * T] = cn[e];
+          sv[os + e * T] = sn[e];
+        }
+        if (ctop > thr) {
+          if (!war_ok) {
+            while (ld_acquire_cta(war) < (uint32_t)(k + 1)) {
+            }
+            war_ok = true;
+          }
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int j = c0 + e * T + tid;
+            if (j >= thrC) gC[j] = cn[e];
+            if (j >= thrS) gS[j] = sn[e];
+          }
+        }
+      }
+      fence_proxy_async_global();  // the global row copy is read next by bulk copies
+      named_barrier(1, T);         // stage done: own rows complete, global stores ordered
+      if (tid == 0) st_release_cta(done, (uint32_t)(k + 1));
+      sh = shn;
+      shn = shn2;
+      rbits = rbn;
+    }
+  }
+  __syncthreads();
+  cluster_barrier();  // no CTA leaves while others may still poll its counters
+  if (tid == 0 && ncol - 1 >= j0 && ncol - 1 < j0 + B) {
+    const double g = a.info[inst].scale;
+    a.info[inst].end_c = to_f64(ownC[ncol - 1 - j0], g);
+    a.info[inst].end_s = to_f64(ownS[ncol - 1 - j0], g);
+  }
+  // the global rows are dead: drop their L2 lines instead of writing them back
+  for (int buf = 0; buf < NBUF; ++buf)
+    for (int rs = 0; rs < 2; ++rs)
+      for (int x = tid * LINE; x < B; x += blockDim.x * LINE) discard_l2(grow(buf, rs) + j0 + x);
 }
 
 // ---------------------------------------------------------------------------
@@ -1720,7 +2040,7 @@ size_t stage_bytes_mode(int mode) {
   return align_up(kStageTile * (sizeof(StageShift) + value_bytes(mode)), 16);
 }
 
-enum DpVariant { DPV_SMEM = 0, DPV_CLUSTER = 1, DPV_GLOBAL = 2, DPV_COOP = 3, DPV_STREAM = 4 };
+enum DpVariant { DPV_SMEM = 0, DPV_CLUSTER = 1, DPV_GLOBAL = 2, DPV_COOP = 3, DPV_STREAM = 4, DPV_OWN = 6 };
 
 // ---- single-CTA kernels: T x E configurations ------------------------------
 
@@ -1775,14 +2095,27 @@ int launch_single(const DpArgs& a, int64_t n_items, int cfg, size_t smem, cudaSt
 
 // ---- streaming (L2-resident rows, bulk-copy staged windows) ----------------
 
-constexpr int kStreamE = 4;
-// bulk-copy ring depth: ~100 KB of slots per CTA (2 CTAs per SM)
+// Streaming-kernel configurations (compute threads T, columns per thread per
+// chunk E, bulk-copy ring depth NSLOT), ~100 KB of ring per CTA so two CTAs
+// share an SM.  The int32 domain can take 8 columns per thread (half the
+// per-chunk address / barrier overhead per cell); the fp64 domains keep 4.
+struct StreamCfg {
+  int T, E, NSLOT;
+};
+constexpr StreamCfg kStreamCfgs[] = {{256, 4, 6}, {256, 8, 3}, {128, 8, 6}, {256, 4, 3}};
+constexpr int kStreamCfgF64 = 3;
+// bulk-copy ring depth of the grid kernel (T = 256, E = 4)
 template <int MODE> constexpr int ring_slots() { return MODE == VM_INT32 ? 6 : 3; }
 inline int ring_slots_rt(int mode) { return mode == VM_INT32 ? 6 : 3; }
+int stream_cfg_index(int mode) {
+  if (mode != VM_INT32) return kStreamCfgF64;
+  const int c = env_int("SPLITPLAN_STREAM_CFG", 1);  // 256 x 8 (measured 4.67e11 vs 4.54e11 cells/s at cfg2)
+  return c < 0 || c > 2 ? 1 : c;
+}
+StreamCfg stream_cfg(int mode) { return kStreamCfgs[stream_cfg_index(mode)]; }
 
-// compute threads of the streaming kernel (256: 128 was measured slower)
-int stream_threads() { return 256; }
-int64_t stream_ch() { return (int64_t)stream_threads() * kStreamE; }
+int stream_threads(int mode) { return stream_cfg(mode).T; }
+int64_t stream_ch(int mode) { return (int64_t)stream_cfg(mode).T * stream_cfg(mode).E; }
 // live rows of co-resident instances kept in L2 (SPLITPLAN_L2_BUDGET_MB)
 size_t l2_row_budget() {
   static size_t b = 0;
@@ -1792,11 +2125,11 @@ size_t l2_row_budget() {
 
 size_t stream_smem(int mode) {
   const size_t vb = value_bytes(mode);
-  return 256 + (size_t)ring_slots_rt(mode) * 4 * (stream_ch() + 16 / vb) * vb;
+  return 256 + (size_t)stream_cfg(mode).NSLOT * 4 * (stream_ch(mode) + 16 / vb) * vb;
 }
 int64_t stream_span(int mode, const StreamGeom& g) {
   const int64_t line = 128 / (int64_t)value_bytes(mode);
-  return (stream_ch() + line) + (int64_t)g.G * g.NC * stream_ch() + line;
+  return (stream_ch(mode) + line) + (int64_t)g.G * g.NC * stream_ch(mode) + line;
 }
 // row buffers of the streaming kernel: 2 (full-barrier semantics, default:
 // 2/3 of the L2 footprint lets G shrink to 5 at W = 1e5, measured 4.5e11 vs
@@ -1819,9 +2152,9 @@ int stream_pair() {
   return p;
 }
 
-template <int MODE, int T>
+template <int MODE, int T, int E, int NSLOT>
 int stream_occupancy_t() {
-  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>(), 2, 3>;
+  auto kern = dp_stream_kernel<MODE, T, E, NSLOT, 1, 2>;
   int n = 0;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(MODE)) !=
           cudaSuccess ||
@@ -1833,7 +2166,12 @@ int stream_occupancy_t() {
 }
 template <int MODE>
 int stream_occupancy() {
-  return stream_occupancy_t<MODE, 256>();
+  if (MODE != VM_INT32) return stream_occupancy_t<MODE, 256, 4, 3>();
+  switch (stream_cfg_index(MODE)) {
+    case 1: return stream_occupancy_t<MODE, 256, 8, 3>();
+    case 2: return stream_occupancy_t<MODE, 128, 8, 6>();
+    default: return stream_occupancy_t<MODE, 256, 4, 6>();
+  }
 }
 
 // co-resident streaming CTAs on this device (cached per value domain)
@@ -1862,7 +2200,7 @@ int stream_resident_ctas(int mode) {
 // G = 7 x 14 chunks beats 8 x 13 and 14 x 7; paired instances hide most of
 // it behind the partner's stage).
 StreamGeom stream_geom(int mode, int64_t ncol) {
-  const int64_t nchunks = (ncol + stream_ch() - 1) / stream_ch();
+  const int64_t nchunks = (ncol + stream_ch(mode) - 1) / stream_ch(mode);
   const int resident = stream_resident_ctas(mode);
   const int force = env_int("SPLITPLAN_DP_CLUSTER", 0);
   auto geom = [&](int G) {
@@ -1887,9 +2225,9 @@ StreamGeom stream_geom(int mode, int64_t ncol) {
   return best;
 }
 
-template <int MODE, int T, int NI, int NBUF>
+template <int MODE, int T, int E, int NSLOT, int NI, int NBUF>
 int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
-  auto kern = dp_stream_kernel<MODE, T, kStreamE, ring_slots<MODE>(), NI, NBUF>;
+  auto kern = dp_stream_kernel<MODE, T, E, NSLOT, NI, NBUF>;
   const size_t smem = stream_smem(MODE);
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "cudaFuncSetAttribute(dp_stream_kernel)");
@@ -1901,6 +2239,7 @@ int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream
   }
   geo.n_items = (int)n_items;
   geo.row_hint = env_int("SPLITPLAN_ROW_EVICT_LAST", 0) ? 1 : 0;
+  geo.diag = env_int("SPLITPLAN_STREAM_DIAG", 0);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((n_items + NI - 1) / NI * geo.G), 1, 1);
   cfg.blockDim = dim3((unsigned)(T + 32), 1, 1);  // + the producer warp
@@ -1919,12 +2258,109 @@ int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream
 }
 template <int MODE>
 int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
+  if (MODE == VM_INT32 && stream_cfg_index(MODE) == 1)
+    return launch_stream_t<MODE, 256, 8, 3, 1, 2>(a, n_items, geo, st);
+  if (MODE == VM_INT32 && stream_cfg_index(MODE) == 2)
+    return launch_stream_t<MODE, 128, 8, 6, 1, 2>(a, n_items, geo, st);
+  constexpr int NS = MODE == VM_INT32 ? 6 : 3;
   const int sel = (stream_pair() == 2 ? 1 : 0) + (stream_bufs() == 2 ? 2 : 0);
   switch (sel) {
-    case 0: return launch_stream_t<MODE, 256, 1, 3>(a, n_items, geo, st);
-    case 1: return launch_stream_t<MODE, 256, 2, 3>(a, n_items, geo, st);
-    case 2: return launch_stream_t<MODE, 256, 1, 2>(a, n_items, geo, st);
-    default: return launch_stream_t<MODE, 256, 2, 2>(a, n_items, geo, st);
+    case 0: return launch_stream_t<MODE, 256, 4, NS, 1, 3>(a, n_items, geo, st);
+    case 1: return launch_stream_t<MODE, 256, 4, NS, 2, 3>(a, n_items, geo, st);
+    case 2: return launch_stream_t<MODE, 256, 4, NS, 1, 2>(a, n_items, geo, st);
+    default: return launch_stream_t<MODE, 256, 4, NS, 2, 2>(a, n_items, geo, st);
+  }
+}
+
+// ---- own-block kernel (int32 rows in the cluster's shared memory) ----------
+
+struct OwnCfg {
+  int T, E, NSW;
+};
+constexpr OwnCfg kOwnCfgs[] = {{512, 4, 8}, {256, 8, 8}, {256, 4, 8}};
+int own_cfg_index() {
+  const int c = env_int("SPLITPLAN_OWN_CFG", 0);
+  return c < 0 || c > 2 ? 0 : c;
+}
+// CTAs per SM the own-block geometry is sized for (SPLITPLAN_OWN_OCC 1 or 2)
+size_t own_smem_budget() {
+  return env_int("SPLITPLAN_OWN_OCC", 1) == 2 ? (size_t)113 * 1024 : kSmemCap;
+}
+// global row buffers (3: one stage of slack for the wavefront; SPLITPLAN_OWN_BUFS 2..4)
+int own_bufs() { return std::min(4, std::max(2, env_int("SPLITPLAN_OWN_BUFS", 3))); }
+int64_t own_ch() { return (int64_t)kOwnCfgs[own_cfg_index()].T * kOwnCfgs[own_cfg_index()].E; }
+size_t own_smem(int mode, int NC) {
+  const size_t vb = value_bytes(mode);
+  const int64_t ch = own_ch();
+  return 256 + (size_t)(2 * (ch + NC * ch) + kOwnCfgs[own_cfg_index()].NSW * (ch + 16 / (int64_t)vb)) * vb;
+}
+// cluster geometry: the fewest CTAs whose blocks fit shared memory (G = 0: not possible)
+StreamGeom own_geom(int mode, int64_t ncol) {
+  StreamGeom g{0, 0, 0, 0, 0};
+  if (mode != VM_INT32) return g;
+  const int64_t nchunks = (ncol + own_ch() - 1) / own_ch();
+  int ncmax = 0;
+  while (own_smem(mode, ncmax + 1) <= own_smem_budget()) ++ncmax;
+  if (ncmax < 1) return g;
+  int G = (int)((nchunks + ncmax - 1) / ncmax);
+  const int force = env_int("SPLITPLAN_DP_CLUSTER", 0);
+  if (force >= 1 && force <= 16) G = std::max(G, force);
+  if (G > 16) return g;
+  const int NC = (int)((nchunks + G - 1) / G);
+  g.G = (int)((nchunks + NC - 1) / NC);
+  g.NC = NC;
+  return g;
+}
+int64_t own_span(int mode, const StreamGeom& g) {
+  const int64_t line = 128 / (int64_t)value_bytes(mode);
+  return (own_ch() + line) + (int64_t)g.G * g.NC * own_ch() + line;
+}
+size_t own_row_bytes(int mode, const StreamGeom& g) {
+  return 2 * (size_t)own_bufs() * (size_t)own_span(mode, g) * value_bytes(mode);
+}
+
+template <int MODE, int T, int E, int NSW, int NBUF>
+int launch_own_t(const DpArgs& a, int64_t n_items, StreamGeom sg, size_t smem, cudaStream_t st) {
+  auto kern = dp_own_kernel<MODE, T, E, NSW, NBUF>;
+  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                      "cudaFuncSetAttribute(dp_own_kernel)");
+  if (rc) return rc;
+  if (sg.G > 8) {
+    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                    "cudaFuncSetAttribute(non-portable cluster)");
+    if (rc) return rc;
+  }
+  OwnGeom geo{sg.G, sg.NC, (int)n_items, 0};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_items * sg.G), 1, 1);
+  cfg.blockDim = dim3((unsigned)(T + 64), 1, 1);  // + producer and publisher warps
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)sg.G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, a, geo), "dp_own_kernel launch");
+  if (rc) return rc;
+  return launch_check("dp_own_kernel launch");
+}
+int launch_own(int mode, const DpArgs& a, int64_t n_items, StreamGeom sg, size_t smem, cudaStream_t st) {
+  if (mode != VM_INT32) return check_cuda(cudaErrorInvalidValue, "dp_own_kernel: int32 domain only");
+  const int sel = own_cfg_index() * 3 + (own_bufs() - 2);
+  switch (sel) {
+    case 6: return launch_own_t<VM_INT32, 256, 4, 8, 2>(a, n_items, sg, smem, st);
+    case 7: return launch_own_t<VM_INT32, 256, 4, 8, 3>(a, n_items, sg, smem, st);
+    case 8: return launch_own_t<VM_INT32, 256, 4, 8, 4>(a, n_items, sg, smem, st);
+    case 0: return launch_own_t<VM_INT32, 512, 4, 8, 2>(a, n_items, sg, smem, st);
+    case 1: return launch_own_t<VM_INT32, 512, 4, 8, 3>(a, n_items, sg, smem, st);
+    case 2: return launch_own_t<VM_INT32, 512, 4, 8, 4>(a, n_items, sg, smem, st);
+    case 3: return launch_own_t<VM_INT32, 256, 8, 8, 2>(a, n_items, sg, smem, st);
+    case 4: return launch_own_t<VM_INT32, 256, 8, 8, 3>(a, n_items, sg, smem, st);
+    case 5: return launch_own_t<VM_INT32, 256, 8, 8, 4>(a, n_items, sg, smem, st);
+    default: return launch_own_t<VM_INT32, 512, 4, 8, 3>(a, n_items, sg, smem, st);
   }
 }
 
@@ -2048,6 +2484,7 @@ int forced_variant() {
   if (!strcmp(v, "coop")) return DPV_COOP;
   if (!strcmp(v, "stream")) return DPV_STREAM;
   if (!strcmp(v, "grid")) return 5;  // DPV_GRID
+  if (!strcmp(v, "own")) return DPV_OWN;
   return -1;
 }
 
@@ -2079,6 +2516,7 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) 
   else if (force == DPV_CLUSTER && cluster_geom(mode, ncol).G) p.variant = DPV_CLUSTER;
   else if (force == DPV_COOP) p.variant = DPV_COOP;
   else if (force == DPV_STREAM) p.variant = DPV_STREAM;
+  else if (force == DPV_OWN && own_geom(mode, ncol).G) p.variant = DPV_OWN;
   else if (fits_cta && force != DPV_CLUSTER) p.variant = DPV_SMEM;
   else p.variant = DPV_STREAM;
 
@@ -2092,10 +2530,17 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) 
       break;
     case DPV_STREAM:
       p.sgeo = stream_geom(mode, ncol);
-      p.threads = stream_threads();
-      p.bp_row_words = bp_row_words_for(mode, (int64_t)p.sgeo.G * p.sgeo.NC * stream_ch());
+      p.threads = stream_threads(mode);
+      p.bp_row_words = bp_row_words_for(mode, (int64_t)p.sgeo.G * p.sgeo.NC * stream_ch(mode));
       p.rows = align_up(stream_row_bytes(mode, p.sgeo), 256);
       p.smem = stream_smem(mode);
+      break;
+    case DPV_OWN:
+      p.sgeo = own_geom(mode, ncol);
+      p.threads = kOwnCfgs[own_cfg_index()].T;
+      p.bp_row_words = bp_row_words_for(mode, (int64_t)p.sgeo.G * p.sgeo.NC * own_ch());
+      p.rows = align_up(own_row_bytes(mode, p.sgeo), 256);
+      p.smem = own_smem(mode, p.sgeo.NC);
       break;
     case DPV_COOP:
       p.cgeo = coop_geom(mode, ncol);
@@ -2119,6 +2564,8 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) 
 int launch_plan(int mode, const DpPlan& p, const DpArgs& a, int64_t n_items, cudaStream_t st) {
   if (n_items == 0) return SP_OK;
   switch (p.variant) {
+    case DPV_OWN:
+      return launch_own(mode, a, n_items, p.sgeo, p.smem, st);
     case DPV_STREAM:
       switch (mode) {
         case VM_INT32: return launch_stream<VM_INT32>(a, n_items, p.sgeo, st);

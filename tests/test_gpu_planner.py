@@ -180,7 +180,7 @@ def test_dp_vs_oracle_smem_and_global_rows(gpu, r_kind):
         assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{r_kind}[{k}]")
 
 
-@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop", "stream", "grid"])
+@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop", "stream", "grid", "own"])
 @pytest.mark.parametrize("name", ["battery_wide", "battery_float", "battery_large_model"])
 def test_dp_kernel_variants_agree(gpu, variant, name, monkeypatch):
     """Every K2 variant (rows in one CTA's SMEM, in cluster DSMEM, in global
@@ -212,6 +212,24 @@ def test_stream_cluster_sizes(gpu, cluster, monkeypatch):
     monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "stream")
     monkeypatch.setenv("SPLITPLAN_DP_CLUSTER", cluster)
     for name in ("battery_wide", "battery_large_model"):
+        bat = Battery(name)
+        _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
+
+
+@pytest.mark.parametrize("cluster,cfg,bufs,occ", [("1", "0", "3", "1"), ("2", "0", "2", "1"), ("5", "0", "3", "1"),
+                                                  ("7", "1", "3", "1"), ("8", "0", "4", "1"), ("3", "1", "2", "1"),
+                                                  ("4", "2", "3", "2"), ("13", "2", "2", "2")])
+def test_own_kernel_geometries(gpu, cluster, cfg, bufs, occ, monkeypatch):
+    """The own-block kernel (rows in the cluster CTAs' shared memory, remote
+    windows over L2) at forced cluster sizes, both thread configurations and
+    2-4 global row buffers: many windows are remote or straddle a block edge."""
+    from paper_2410_10759_b200 import batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "own")
+    monkeypatch.setenv("SPLITPLAN_DP_CLUSTER", cluster)
+    monkeypatch.setenv("SPLITPLAN_OWN_CFG", cfg)
+    monkeypatch.setenv("SPLITPLAN_OWN_BUFS", bufs)
+    monkeypatch.setenv("SPLITPLAN_OWN_OCC", occ)
+    for name in ("battery_wide", "battery_large_model", "battery_acceptance"):
         bat = Battery(name)
         _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
 

@@ -51,7 +51,7 @@ def main():
     from paper_2410_10759_b200 import _native as N
     from paper_2410_10759_b200 import batch as B
     lib = N.library()
-    names = ["smem", "cluster", "global", "coop", "stream", "grid"]
+    names = ["smem", "cluster", "global", "coop", "stream", "grid", "own"]
     for W in [int(w) for w in args.W.split(",")]:
         n = args.n or max(148, int(1.2e10 / (args.L * (W + 1))))
         b = B.InstanceBatch.from_arrays(*make(n, args.L, W, 1, args.r))
