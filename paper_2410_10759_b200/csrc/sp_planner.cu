@@ -2116,10 +2116,13 @@ StreamCfg stream_cfg(int mode) { return kStreamCfgs[stream_cfg_index(mode)]; }
 
 int stream_threads(int mode) { return stream_cfg(mode).T; }
 int64_t stream_ch(int mode) { return (int64_t)stream_cfg(mode).T * stream_cfg(mode).E; }
-// live rows of co-resident instances kept in L2 (SPLITPLAN_L2_BUDGET_MB)
+// live rows of co-resident instances kept in L2 (SPLITPLAN_L2_BUDGET_MB).
+// Measured at cfg2 (profiles/r01/stream_cfg_diag/ncu_dram_G*.csv): ~69 MB of
+// rows stay resident (0.05 B/cell of DRAM reads), ~94 MB already spill
+// (2.3 B/cell of DRAM reads, 6.6 B/cell of write-backs).
 size_t l2_row_budget() {
   static size_t b = 0;
-  if (!b) b = (size_t)env_int("SPLITPLAN_L2_BUDGET_MB", 110) << 20;
+  if (!b) b = (size_t)env_int("SPLITPLAN_L2_BUDGET_MB", 80) << 20;
   return b;
 }
 

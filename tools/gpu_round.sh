@@ -1,14 +1,13 @@
 #!/bin/bash
-# One GPU-box pass: parity suite, smoke, DP micro-bench per variant, bench line.
-# usage: bash tools/gpu_round.sh [tag]   (outputs under gpurun_out/<tag>/)
+# One GPU-box pass: parity suite, smoke, bench line, launch list and one full
+# ncu capture of the bench's DP kernel.   usage: bash tools/gpu_round.sh [tag]
 tag=${1:-run}
 out=gpurun_out/$tag
 mkdir -p $out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $out/smi.csv 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > $out/pytest_gpu.log 2>&1; echo "pytest_rc=$?" >> $out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1
-timeout 600 python tools/dpbench.py > $out/dpbench_auto.log 2>&1
-for v in smem stream coop; do
-  timeout 300 python tools/dpbench.py --variant $v --W 10000,28000,100000 > $out/dpbench_$v.log 2>&1
-done
-timeout 900 python bench.py --no-cpu-baseline > $out/bench.json 2> $out/bench.err
+timeout 900 python bench.py > $out/bench.json 2> $out/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $out/bench_ref.json 2> $out/bench_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $out/bench_under_ncu.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:dp_stream -c 1 -o $out/dp_stream_full python tools/k2bench.py --requests 1000 --reps 1 > $out/ncu_full.log 2>&1
