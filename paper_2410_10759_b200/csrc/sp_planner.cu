@@ -1367,9 +1367,11 @@ struct GridArgs {
   void* out_s;
   uint32_t* bp;              // back-pointers of the range's stages, or null
   int64_t bp_row_words;
-  uint32_t* prog;            // [nparts * G] stages completed + 1 (zeroed)
+  uint32_t* progs[kMaxParts];  // per partition: [G] stages completed + 1 (zeroed)
   int nparts;                // partitions of the capacity axis
-  int part_base;             // first partition of this launch (grid = launched parts x G)
+  int part_base;             // first partition of this launch
+  int launch_parts;          // partitions of this launch (grid = launch_parts x G)
+  int sys;                   // partitions on different devices: system-scope ordering
   int halo;                  // mirrored left-neighbour columns (multiple of 128 B)
   uint8_t* rows[kMaxParts];  // per partition: [3][C|S][NEG pad | halo | Wp | line]
 };
@@ -1381,6 +1383,15 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ int max_shift(const StageShift& sh) {
@@ -1422,6 +1433,19 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
   };
   auto row = [&](int buf, int rs) { return row_of(part, buf, rs); };
   auto owner = [&](int x) { return min(GT - 1, max(0, x) / B); };  // global CTA of global column x
+  // progress counter of global CTA o (in its partition's -- possibly a peer device's -- memory)
+  auto prog_of = [&](int o) { return a.progs[o / G] + (o % G); };
+  auto publish = [&](uint32_t v) {
+    if (a.sys) {
+      __threadfence_system();
+      fence_proxy_async_global();
+      st_release_sys(prog_of(gq), v);
+    } else {
+      __threadfence();
+      fence_proxy_async_global();
+      st_release_gpu(prog_of(gq), v);
+    }
+  };
   const V* ic = reinterpret_cast<const V*>(a.init_c);
   const V* is = reinterpret_cast<const V*>(a.init_s);
   auto init_at = [&](int x, V& c, V& sv) {  // row k_begin at global column x
@@ -1466,11 +1490,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    fence_proxy_async_global();
-    st_release_gpu(&a.prog[gq], 1u);  // rows initialised (counter = completed stages + 1)
-  }
+  if (tid == 0) publish(1u);  // rows initialised (counter = completed stages + 1)
 
   if (warp == NWARP) {
     // ---------------- producer warp ----------------
@@ -1487,7 +1507,13 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
       for (int o0 = lo_o; o0 <= hi_o; o0 += 32) {
         const int o = o0 + lane;
         const uint32_t need = o <= gq ? (uint32_t)(t + 1) : (uint32_t)max(t - 1, 0) + 1u;
-        while (!__all_sync(0xffffffffu, o > hi_o || ld_acquire_gpu(&a.prog[o]) >= need)) {
+        // (a watchdog turns a lost partition -- e.g. launches that were not
+        // co-scheduled -- into a launch failure instead of a hang)
+        const long long t0 = clock64();
+        for (uint32_t it = 1;; ++it) {
+          const bool ok = o > hi_o || (a.sys ? ld_acquire_sys(prog_of(o)) : ld_acquire_gpu(prog_of(o))) >= need;
+          if (__all_sync(0xffffffffu, ok)) break;
+          if ((it & 1023u) == 0 && clock64() - t0 > (30ll << 30)) __trap();
         }
       }
       if (lane == 0) {
@@ -1580,11 +1606,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
         }
       }
       named_barrier(1, T);
-      if (tid == 0) {
-        __threadfence();
-        fence_proxy_async_global();
-        st_release_gpu(&a.prog[gq], (uint32_t)(t + 2));
-      }
+      if (tid == 0) publish((uint32_t)(t + 2));
     }
     // the range's final row (this CTA's own block: its own writes)
     if (a.out_c) {
@@ -2639,8 +2661,12 @@ int grid_resident() {
 template <int MODE>
 int launch_grid_t(const GridArgs& g, cudaStream_t st) {
   auto kern = dp_grid_kernel<MODE, kGridT, kGridE, ring_slots<MODE>()>;
+  // per device: a partition may be launched on a peer device
+  int rc0 = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grid_smem(MODE)),
+                       "cudaFuncSetAttribute(dp_grid_kernel)");
+  if (rc0) return rc0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(g.G * (g.nparts - g.part_base)), 1, 1);  // every partition of this launch
+  cfg.gridDim = dim3((unsigned)(g.G * g.launch_parts), 1, 1);  // every partition of this launch
   cfg.blockDim = dim3((unsigned)(kGridT + 32), 1, 1);
   cfg.dynamicSmemBytes = grid_smem(MODE);
   cfg.stream = st;
@@ -2661,6 +2687,47 @@ int launch_grid(int mode, const GridArgs& g, cudaStream_t st) {
     default: return launch_grid_t<VM_F64_NAN>(g, st);
   }
 }
+
+__global__ void zero_progs_kernel(GridArgs g) {
+  for (int p = 0; p < g.nparts; ++p)
+    for (int x = threadIdx.x; x < g.G; x += blockDim.x) g.progs[p][x] = 0u;
+}
+
+// Partitions on other devices (SPLITPLAN_GRID_DEVICES > 1): their row buffers,
+// progress counters and stage-record copies live in that device's memory;
+// every device reaches the others' (and the caller's workspace) through peer
+// access.  Released when the solve returns.
+struct PeerParts {
+  int cur = 0;
+  int dev[kMaxParts] = {};
+  cudaStream_t stream[kMaxParts] = {};
+  cudaEvent_t done[kMaxParts] = {};
+  std::vector<std::pair<int, void*>> allocs;
+  cudaEvent_t start = nullptr;
+  ~PeerParts() {
+    for (int p = 0; p < kMaxParts; ++p) {
+      if (!stream[p]) continue;
+      cudaSetDevice(dev[p]);
+      cudaStreamSynchronize(stream[p]);
+      cudaStreamDestroy(stream[p]);
+      if (done[p]) cudaEventDestroy(done[p]);
+    }
+    for (auto& a : allocs) {
+      cudaSetDevice(a.first);
+      cudaFree(a.second);
+    }
+    cudaSetDevice(cur);
+    if (start) cudaEventDestroy(start);
+  }
+  void* alloc(int d, size_t bytes) {
+    void* ptr = nullptr;
+    cudaSetDevice(d);
+    if (cudaMalloc(&ptr, bytes) != cudaSuccess) ptr = nullptr;
+    else allocs.push_back({d, ptr});
+    cudaSetDevice(cur);
+    return ptr;
+  }
+};
 
 // Solve one instance over the whole GPU.  With the full back-pointer table in
 // memory: one forward launch and one backtrack.  Otherwise checkpoint /
@@ -2690,9 +2757,23 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
   const int64_t nchunks = (ncol + kGridCH - 1) / kGridCH;
   // partitions of the capacity axis (one per device in a multi-GPU run;
   // SPLITPLAN_GRID_PARTS > 1 emulates them on this device)
-  int nparts = force_parts ? force_parts : std::max(1, std::min(kMaxParts, env_int("SPLITPLAN_GRID_PARTS", 1)));
+  // SPLITPLAN_GRID_DEVICES > 1 places partition p on device (current + p),
+  // one launch per device; SPLITPLAN_GRID_SEPARATE=1 runs emulated partitions
+  // as separate concurrent launches on this device (the multi-device protocol
+  // with every partition here).
+  int ndev_avail = 1;
+  if (cudaGetDeviceCount(&ndev_avail) != cudaSuccess) {
+    cudaGetLastError();
+    ndev_avail = 1;
+  }
+  const int ndev = force_parts ? 1 : std::max(1, std::min(std::min(kMaxParts, ndev_avail),
+                                                          env_int("SPLITPLAN_GRID_DEVICES", 1)));
+  int nparts = force_parts ? force_parts
+                           : (ndev > 1 ? ndev : std::max(1, std::min(kMaxParts, env_int("SPLITPLAN_GRID_PARTS", 1))));
   nparts = (int)std::min<int64_t>(nparts, nchunks);
-  int G = (int)std::min<int64_t>(resident / nparts, (nchunks + nparts - 1) / nparts);
+  const bool multi = ndev > 1 && nparts > 1;
+  const bool separate = multi || (nparts > 1 && env_int("SPLITPLAN_GRID_SEPARATE", 0) != 0);
+  int G = (int)std::min<int64_t>(multi ? resident : resident / nparts, (nchunks + nparts - 1) / nparts);
   G = std::max(G, 1);
   const int NC = (int)((nchunks + (int64_t)G * nparts - 1) / ((int64_t)G * nparts));
   G = (int)((nchunks + (int64_t)NC * nparts - 1) / ((int64_t)NC * nparts));
@@ -2744,7 +2825,62 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
   uint32_t* prog = (uint32_t*)cv.take((size_t)G * nparts * 4);
   int64_t* state = (int64_t*)cv.take(4 * sizeof(int64_t));
   uint8_t* rows[kMaxParts] = {};
-  for (int p = 0; p < nparts; ++p) rows[p] = (uint8_t*)cv.take(rows_bytes);
+  uint32_t* progs[kMaxParts] = {};
+  const StageShift* pshifts[kMaxParts] = {};
+  const int64_t* prv[kMaxParts] = {};
+  PeerParts peers;
+  cudaGetDevice(&peers.cur);
+  for (int p = 0; p < nparts; ++p) {
+    peers.dev[p] = multi ? (peers.cur + p) % ndev_avail : peers.cur;
+    pshifts[p] = shifts + lo;
+    prv[p] = rv + lo;
+    if (peers.dev[p] == peers.cur) {
+      rows[p] = (uint8_t*)cv.take(rows_bytes);
+      progs[p] = prog + (size_t)p * G;
+      continue;
+    }
+    rows[p] = (uint8_t*)peers.alloc(peers.dev[p], rows_bytes);
+    progs[p] = (uint32_t*)peers.alloc(peers.dev[p], (size_t)G * 4);
+    StageShift* sh_copy = (StageShift*)peers.alloc(peers.dev[p], sizeof(StageShift) * L);
+    int64_t* rv_copy = (int64_t*)peers.alloc(peers.dev[p], sizeof(int64_t) * L);
+    if (!rows[p] || !progs[p] || !sh_copy || !rv_copy) {
+      set_error(SP_ERR_CUDA, "partition %d: device %d allocation failed", p, peers.dev[p]);
+      return SP_ERR_CUDA;
+    }
+    int rc0 = check_cuda(cudaMemcpyPeerAsync(sh_copy, peers.dev[p], shifts + lo, peers.cur,
+                                             sizeof(StageShift) * L, st), "copy stage records to peer");
+    if (rc0) return rc0;
+    rc0 = check_cuda(cudaMemcpyPeerAsync(rv_copy, peers.dev[p], rv + lo, peers.cur, sizeof(int64_t) * L, st),
+                     "copy stage values to peer");
+    if (rc0) return rc0;
+    pshifts[p] = sh_copy;
+    prv[p] = rv_copy;
+  }
+  if (multi) {  // every used device reaches every other one
+    for (int p = 0; p < nparts; ++p)
+      for (int r = 0; r < nparts; ++r) {
+        if (peers.dev[p] == peers.dev[r]) continue;
+        cudaSetDevice(peers.dev[p]);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(peers.dev[r], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          cudaSetDevice(peers.cur);
+          return check_cuda(e, "cudaDeviceEnablePeerAccess");
+        }
+        cudaGetLastError();
+      }
+    cudaSetDevice(peers.cur);
+  }
+  if (separate) {
+    int rc0 = check_cuda(cudaEventCreateWithFlags(&peers.start, cudaEventDisableTiming), "event");
+    if (rc0) return rc0;
+    for (int p = 0; p < nparts; ++p) {
+      cudaSetDevice(peers.dev[p]);
+      rc0 = check_cuda(cudaStreamCreateWithFlags(&peers.stream[p], cudaStreamNonBlocking), "partition stream");
+      if (!rc0) rc0 = check_cuda(cudaEventCreateWithFlags(&peers.done[p], cudaEventDisableTiming), "event");
+      cudaSetDevice(peers.cur);
+      if (rc0) return rc0;
+    }
+  }
   const int nseg = (L + K - 1) / K;
   const int nckpt = K == L ? 2 : nseg + 1;
   std::vector<uint8_t*> ckpt(nckpt);
@@ -2761,9 +2897,11 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
   for (int p = 0; p < nparts; ++p) g.rows[p] = rows[p];
   g.nparts = nparts;
   g.part_base = 0;
+  g.launch_parts = nparts;
+  g.sys = (multi || env_int("SPLITPLAN_GRID_SYS", 0)) ? 1 : 0;
   g.halo = (int)halo;
   g.bp_row_words = row_words;
-  g.prog = prog;
+  for (int p = 0; p < nparts; ++p) g.progs[p] = progs[p];
   {
     uint8_t sac = 0;
     int rc = check_cuda(cudaMemcpyAsync(&sac, in->source_at_client + inst, 1, cudaMemcpyDeviceToHost, st),
@@ -2781,7 +2919,9 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
     g.out_c = outrow;
     g.out_s = outrow ? outrow + ncol * vb : nullptr;
     g.bp = bpp;
-    int rc = check_cuda(cudaMemsetAsync(prog, 0, (size_t)G * nparts * 4, st), "zero progress counters");
+    // every partition's counters are zero before any partition starts
+    zero_progs_kernel<<<1, 256, 0, st>>>(g);
+    int rc = launch_check("zero_progs_kernel launch");
     if (rc) return rc;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (profiling()) {
@@ -2789,8 +2929,30 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
       cudaEventCreate(&e1);
       cudaEventRecord(e0, st);
     }
-    rc = launch_grid(mode, g, st);
-    if (rc) return rc;
+    if (!separate) {
+      rc = launch_grid(mode, g, st);
+      if (rc) return rc;
+    } else {  // one launch per partition, all in flight together
+      rc = check_cuda(cudaEventRecord(peers.start, st), "record partition start");
+      if (rc) return rc;
+      for (int p = 0; p < nparts && !rc; ++p) {
+        GridArgs gp = g;
+        gp.part_base = p;
+        gp.launch_parts = 1;
+        gp.shifts = pshifts[p];
+        gp.rv = prv[p];
+        cudaSetDevice(peers.dev[p]);
+        rc = check_cuda(cudaStreamWaitEvent(peers.stream[p], peers.start, 0), "partition wait");
+        if (!rc) rc = launch_grid(mode, gp, peers.stream[p]);
+        if (!rc) rc = check_cuda(cudaEventRecord(peers.done[p], peers.stream[p]), "record partition end");
+      }
+      cudaSetDevice(peers.cur);
+      if (rc) return rc;
+      for (int p = 0; p < nparts; ++p) {
+        rc = check_cuda(cudaStreamWaitEvent(st, peers.done[p], 0), "join partitions");
+        if (rc) return rc;
+      }
+    }
     if (profiling()) {
       cudaEventRecord(e1, st);
       const double cells = (double)cnt * (double)ncol;

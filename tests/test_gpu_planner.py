@@ -264,8 +264,10 @@ def test_grid_checkpoint_recompute(gpu, segment, monkeypatch):
             assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"grid {r_kind}[{k}]")
 
 
-@pytest.mark.parametrize("parts,segment", [("2", "0"), ("3", "13"), ("8", "0")])
-def test_grid_capacity_partitions(gpu, parts, segment, monkeypatch):
+@pytest.mark.parametrize("parts,segment,mode", [("2", "0", ""), ("3", "13", ""), ("8", "0", ""),
+                                                ("2", "0", "separate"), ("4", "13", "separate"),
+                                                ("3", "0", "separate+sys")])
+def test_grid_capacity_partitions(gpu, parts, segment, mode, monkeypatch):
     """The capacity axis split into partitions (one per device in a multi-GPU
     run, emulated here on one GPU) with the left neighbour's columns mirrored
     in a halo: bit-exact against the live reference's cfg5-reduced chains."""
@@ -273,6 +275,11 @@ def test_grid_capacity_partitions(gpu, parts, segment, monkeypatch):
     monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "grid")
     monkeypatch.setenv("SPLITPLAN_GRID_PARTS", parts)
     monkeypatch.setenv("SPLITPLAN_GRID_SEGMENT", segment)
+    # "separate": one launch per partition, all in flight together (the
+    # multi-device protocol with every partition on this GPU); "+sys":
+    # system-scope progress counters as across devices
+    monkeypatch.setenv("SPLITPLAN_GRID_SEPARATE", "1" if "separate" in mode else "0")
+    monkeypatch.setenv("SPLITPLAN_GRID_SYS", "1" if "sys" in mode else "0")
     for name, must in (("battery_large_chain", False), ("battery_wide", True)):
         bat = Battery(name)
         _compare(bat, "dp", B.plan_dp(_batch(bat, with_must=must)).to_host())
