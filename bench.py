@@ -375,6 +375,12 @@ def main():
                 "cells_per_s_in_kernel": kernel_rate,
                 "onchip": onchip_roofline(dk_var.value, kernel_rate, clk.get("sm_mhz")),
                 "row_streaming_ceiling_cells_per_s": peak * 1e9 / 33.0,
+                # the survey's row-streaming design moves 33 B per cell through
+                # HBM: the HBM bandwidth it would need for this kernel's rate
+                "row_streaming_equivalent": ({
+                    "bytes_per_cell": 33.0,
+                    "GBps": kernel_rate * 33.0 / 1e9,
+                    "frac_of_hbm_peak": kernel_rate * 33.0 / (peak * 1e9)} if kernel_rate else None),
             },
             "clocks": clk,
         }
