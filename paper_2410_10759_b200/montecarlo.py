@@ -74,8 +74,11 @@ def scenario_tables(req: dict, off: np.ndarray, model_names, solved: dict):
     mean nosplit load (throughput_sim.py:133-163).
 
     Returns CSR offsets over rows, the per-row demands [rows, 3] and deadlines."""
-    names = np.asarray(model_names, dtype=object)[req["model"]]
-    name_rank = np.unique(names, return_inverse=True)[1]
+    # rank of each request's model name in sorted name order (the reference
+    # sorts coordinates by name): a per-model lookup, not a sort of strings
+    uniq = sorted(set(model_names))
+    rank_of = np.array([uniq.index(x) for x in model_names], dtype=np.int64)
+    name_rank = rank_of[np.asarray(req["model"])]
     S = len(off) - 1
     scen = np.repeat(np.arange(S), np.diff(off))
     keep = solved["dp"]["ok"] & solved["greedy"]["ok"] & solved["all_server"]["ok"]
@@ -105,6 +108,65 @@ def scenario_tables(req: dict, off: np.ndarray, model_names, solved: dict):
     return row_off, demand, req["deadline_s"][order]
 
 
+def _skeleton_rows(sids, a, b, beta_per_ms, horizon, arr, gidx, execs, lo, hi):
+    """Seeded skeletons of rows [lo, hi) (numpy PCG64, throughput_sim.py:179-186)."""
+    for r in range(lo, hi):
+        g = np.random.default_rng(int(sids[r]))
+        arr[r] = np.cumsum(g.exponential(scale=1.0 / beta_per_ms, size=horizon))
+        gidx[r] = g.integers(0, b[r] - a[r], size=horizon) + a[r]
+        execs[r] = g.integers(1, EXEC_MAX + 1, size=horizon)
+
+
+def _skeleton_job(job):
+    from multiprocessing import shared_memory
+    names, n, horizon, sids, a, b, beta_per_ms, lo, hi = job
+    shms = [shared_memory.SharedMemory(name=x) for x in names]
+    try:
+        arr = np.ndarray((n, horizon), np.float64, buffer=shms[0].buf)
+        gidx = np.ndarray((n, horizon), np.int64, buffer=shms[1].buf)
+        execs = np.ndarray((n, horizon), np.int64, buffer=shms[2].buf)
+        _skeleton_rows(sids, a, b, beta_per_ms, horizon, arr, gidx, execs, lo, hi)
+        del arr, gidx, execs
+    finally:
+        for x in shms:
+            x.close()
+
+
+def skeletons(sids, a, b, beta_per_ms, horizon, procs=None):
+    """Arrival skeletons of scenarios `sids` (tables rows [a, b)): arrivals,
+    global table-row indices and execution counts, [n, horizon] each.
+
+    Bit-identical to the reference's per-scenario `default_rng(seed)` draws.
+    numpy's generator holds the GIL for part of every call, so large grids are
+    generated by forked worker processes writing into shared memory."""
+    import os
+    n = len(sids)
+    procs = procs or int(os.environ.get("SPLITPLAN_SKELETON_PROCS", "0")) or min(32, os.cpu_count() or 1)
+    if n < 1024 or procs <= 1:
+        arr = np.empty((n, horizon))
+        gidx = np.empty((n, horizon), np.int64)
+        execs = np.empty((n, horizon), np.int64)
+        _skeleton_rows(sids, a, b, beta_per_ms, horizon, arr, gidx, execs, 0, n)
+        return arr, gidx, execs
+    from multiprocessing import get_context, shared_memory
+    shms = [shared_memory.SharedMemory(create=True, size=max(1, n * horizon * 8)) for _ in range(3)]
+    try:
+        names = [x.name for x in shms]
+        step = (n + procs - 1) // procs
+        jobs = [(names, n, horizon, sids, a, b, beta_per_ms, lo, min(n, lo + step))
+                for lo in range(0, n, step)]
+        with get_context("fork").Pool(len(jobs)) as pool:
+            pool.map(_skeleton_job, jobs, chunksize=1)
+        arr = np.ndarray((n, horizon), np.float64, buffer=shms[0].buf).copy()
+        gidx = np.ndarray((n, horizon), np.int64, buffer=shms[1].buf).copy()
+        execs = np.ndarray((n, horizon), np.int64, buffer=shms[2].buf).copy()
+        return arr, gidx, execs
+    finally:
+        for x in shms:
+            x.close()
+            x.unlink()
+
+
 def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORIZON,
         omega_requests: float = OMEGA_REQUESTS, group=None) -> MonteCarloResult:
     """The cfg4 sweep over `scenario_ids` (default: all 65,536), sharded over
@@ -130,41 +192,31 @@ def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORI
     for s in sim:  # throughput_sim.py:172-176 (numpy-order mean)
         capacity[s] = float(omega_requests) * np.mean(demand[row_off[s]:row_off[s + 1], 2])
 
-    # seeded skeletons (numpy PCG64, throughput_sim.py:179-186); numpy's
-    # Generator releases the GIL while it fills arrays, so threads overlap
-    def skeleton(s):
-        a, b = row_off[s], row_off[s + 1]
-        g = np.random.default_rng(int(sids[s]))
-        arrivals = np.cumsum(g.exponential(scale=1.0 / beta_per_ms, size=horizon))
-        idx = g.integers(0, b - a, size=horizon)
-        execs = g.integers(1, EXEC_MAX + 1, size=horizon)
-        return arrivals, idx + a, execs
-
-    from concurrent.futures import ThreadPoolExecutor
-    import os
     max_w = np.zeros((S, 3))
     mean_w = np.zeros((S, 3))
     status = np.full((S, 3), -1, dtype=np.int32)
-    dl_ms = deadline_s * 1000.0
-    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as pool:
-        for blk in range(0, len(sim), SIM_BLOCK):
-            ids = sim[blk:blk + SIM_BLOCK]
-            n = len(ids)
-            sk = list(pool.map(skeleton, ids, chunksize=64))
-            arr = np.empty((n, 3, horizon))
-            dem = np.empty((n, 3, horizon))
-            dur = np.empty((n, 3, horizon))
-            for r, (arrv, gi, ex) in enumerate(sk):
-                arr[r] = arrv
-                d = dl_ms[gi] * ex  # :189-198, deadline times execution count
-                dur[r] = d
-                for v in range(3):
-                    dem[r, v] = demand[gi, v]
-            roff = np.arange(3 * n + 1, dtype=np.int64) * horizon
-            o = replay_arrays(roff, arr.ravel(), dem.ravel(), dur.ravel(), np.repeat(capacity[ids], 3))
-            max_w[ids] = o["mx"][:3 * n].cpu().numpy().reshape(-1, 3)
-            mean_w[ids] = o["mean"][:3 * n].cpu().numpy().reshape(-1, 3)
-            status[ids] = o["st"][:3 * n].cpu().numpy().reshape(-1, 3)
+    dev = N.device()
+    # the scenario tables live on the device; each run's demand / duration
+    # columns are gathered there from the skeleton's table-row indices
+    # (throughput_sim.py:189-198: duration = deadline x execution count)
+    demand_d = torch.from_numpy(np.ascontiguousarray(demand)).to(dev)
+    dl_ms_d = torch.from_numpy(deadline_s * 1000.0).to(dev)
+    for blk in range(0, len(sim), SIM_BLOCK):
+        ids = sim[blk:blk + SIM_BLOCK]
+        n = len(ids)
+        arrivals, gidx, execs = skeletons(sids[ids], row_off[ids], row_off[ids + 1], beta_per_ms, horizon)
+        arr_d = torch.from_numpy(arrivals).pin_memory().to(dev, non_blocking=True)
+        gidx_d = torch.from_numpy(gidx.astype(np.int32)).pin_memory().to(dev, non_blocking=True).long()
+        ex_d = torch.from_numpy(execs.astype(np.int8)).pin_memory().to(dev, non_blocking=True)
+        arr3 = arr_d[:, None, :].expand(n, 3, horizon).reshape(-1)
+        dur3 = (dl_ms_d[gidx_d] * ex_d.to(torch.float64))[:, None, :].expand(n, 3, horizon).reshape(-1)
+        dem3 = demand_d[gidx_d].permute(0, 2, 1).reshape(-1)
+        roff = np.arange(3 * n + 1, dtype=np.int64) * horizon
+        o = replay_arrays(roff, arr3, dem3, dur3, np.repeat(capacity[ids], 3))
+        max_w[ids] = o["mx"][:3 * n].cpu().numpy().reshape(-1, 3)
+        mean_w[ids] = o["mean"][:3 * n].cpu().numpy().reshape(-1, 3)
+        status[ids] = o["st"][:3 * n].cpu().numpy().reshape(-1, 3)
+        del o, arr3, dur3, dem3, arr_d, gidx_d, ex_d
     return MonteCarloResult(sids, sizes, capacity, max_w, mean_w, status, int(off[-1]),
                             solved["cells"])
 
@@ -194,4 +246,4 @@ def _gather(local, sids, bounds, group) -> MonteCarloResult:
                             int(st[0]), float(st[1]))
 
 
-__all__ = ["MonteCarloResult", "run", "solve_requests", "scenario_tables", "VARIANTS"]
+__all__ = ["MonteCarloResult", "run", "skeletons", "solve_requests", "scenario_tables", "VARIANTS"]
