@@ -105,6 +105,21 @@ int sp_effective_budget(const sp_instances* in, int64_t* w_eff, void* stream);
 int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes,
                void* stream);
 
+/* sp_plan_dp with the capacity axis of huge instances split over devices.
+ * Instances that take the whole-GPU path (>= 4M budget columns, or whose
+ * back-pointers exceed the workspace) are partitioned
+ * along the budget axis: partition p runs on devices[p] (its row buffers,
+ * progress counters and stage records in that device's memory, peer access
+ * enabled between the listed devices), each partition mirrors its left
+ * neighbour's last columns (the halo) by NVLink peer stores from inside the
+ * DP kernel, and partitions order their stages through system-scope
+ * progress counters.  devices[0] must be the current device, which owns
+ * `in`, `out`, `ws` and `stream`; a device may be listed more than once.
+ * Other instances are planned on the current device as by sp_plan_dp.
+ * Replaces the same reference functions as sp_plan_dp (planner.py:182-202). */
+int sp_plan_dp_devices(const sp_instances* in, sp_policies* out, const int32_t* devices,
+                       int32_t n_devices, void* ws, size_t ws_bytes, void* stream);
+
 /* Full DP tables of ONE instance (in->n == 1) as float64, row-major
  * [(L+1) x (w_eff+1)], unreachable cells = -inf.  Replaces planner.py:128-143
  * `build_dp_tables`.  w_eff must equal sp_effective_budget()'s value. */

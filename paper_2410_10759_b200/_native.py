@@ -95,6 +95,8 @@ SIGNATURES = {
                                      C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "sp_effective_budget": (C.c_int, [C.POINTER(SpInstances), P, P]),
     "sp_plan_dp": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_size_t, P]),
+    "sp_plan_dp_devices": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_int32, P,
+                                     C.c_size_t, P]),
     "sp_build_dp_tables": (C.c_int, [C.POINTER(SpInstances), C.c_int64, P, P, P, C.c_size_t, P]),
     "sp_plan_prefix": (C.c_int, [C.POINTER(SpInstances), C.c_int32, C.POINTER(SpPolicies), P]),
     "sp_plan_exhaustive": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P]),

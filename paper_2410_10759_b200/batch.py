@@ -119,10 +119,21 @@ def effective_budget(batch: InstanceBatch) -> torch.Tensor:
     return out
 
 
-def plan_dp(batch: InstanceBatch, out: PolicyBatch | None = None) -> PolicyBatch:
-    """K1-prep + K2 DP stage + K3 backtrack over the whole batch (sp_plan_dp)."""
+def plan_dp(batch: InstanceBatch, out: PolicyBatch | None = None, devices=None) -> PolicyBatch:
+    """K1-prep + K2 DP stage + K3 backtrack over the whole batch (sp_plan_dp).
+
+    `devices` (a list of CUDA device indices, the current one first) splits
+    the capacity axis of huge instances over those devices
+    (sp_plan_dp_devices)."""
     out = out or PolicyBatch.empty(batch.n, batch.total_layers, batch.r.device)
     s, o = batch.struct(), out.struct()
+    if devices:
+        import ctypes as C
+        arr = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+        rc = N.with_workspace(lambda ws, nb: N.library().sp_plan_dp_devices(
+            s, o, C.cast(arr, C.c_void_p), len(devices), ws, nb, N.stream_ptr()))
+        N.check(rc, "sp_plan_dp_devices")
+        return out
     rc = N.with_workspace(lambda ws, nb: N.library().sp_plan_dp(s, o, ws, nb, N.stream_ptr()))
     N.check(rc, "sp_plan_dp")
     return out

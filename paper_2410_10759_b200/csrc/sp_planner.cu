@@ -2693,6 +2693,9 @@ __global__ void zero_progs_kernel(GridArgs g) {
     for (int x = threadIdx.x; x < g.G; x += blockDim.x) g.progs[p][x] = 0u;
 }
 
+// Devices of the calling thread's sp_plan_dp_devices call (empty otherwise).
+thread_local std::vector<int> tl_grid_devices;
+
 // Partitions on other devices (SPLITPLAN_GRID_DEVICES > 1): their row buffers,
 // progress counters and stage-record copies live in that device's memory;
 // every device reaches the others' (and the caller's workspace) through peer
@@ -2766,14 +2769,33 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
     cudaGetLastError();
     ndev_avail = 1;
   }
-  const int ndev = force_parts ? 1 : std::max(1, std::min(std::min(kMaxParts, ndev_avail),
-                                                          env_int("SPLITPLAN_GRID_DEVICES", 1)));
+  // partition -> device: sp_plan_dp_devices' list, else SPLITPLAN_GRID_DEVICES
+  // consecutive devices from the current one
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  std::vector<int> devlist = tl_grid_devices;
+  if (devlist.empty()) {
+    const int n = std::max(1, std::min(std::min(kMaxParts, ndev_avail), env_int("SPLITPLAN_GRID_DEVICES", 1)));
+    for (int p = 0; p < n; ++p) devlist.push_back((cur_dev + p) % ndev_avail);
+  }
+  if ((int)devlist.size() > kMaxParts) devlist.resize(kMaxParts);
+  const int ndev = force_parts ? 1 : (int)devlist.size();
   int nparts = force_parts ? force_parts
                            : (ndev > 1 ? ndev : std::max(1, std::min(kMaxParts, env_int("SPLITPLAN_GRID_PARTS", 1))));
   nparts = (int)std::min<int64_t>(nparts, nchunks);
   const bool multi = ndev > 1 && nparts > 1;
   const bool separate = multi || (nparts > 1 && env_int("SPLITPLAN_GRID_SEPARATE", 0) != 0);
-  int G = (int)std::min<int64_t>(multi ? resident : resident / nparts, (nchunks + nparts - 1) / nparts);
+  // CTAs per partition: every partition placed on one device must be co-resident there
+  int per_dev = nparts;
+  if (multi) {
+    per_dev = 1;
+    for (int p = 0; p < nparts; ++p) {
+      int c = 0;
+      for (int r = 0; r < nparts; ++r) c += devlist[r] == devlist[p];
+      per_dev = std::max(per_dev, c);
+    }
+  }
+  int G = (int)std::min<int64_t>(resident / per_dev, (nchunks + nparts - 1) / nparts);
   G = std::max(G, 1);
   const int NC = (int)((nchunks + (int64_t)G * nparts - 1) / ((int64_t)G * nparts));
   G = (int)((nchunks + (int64_t)NC * nparts - 1) / ((int64_t)NC * nparts));
@@ -2829,9 +2851,9 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
   const StageShift* pshifts[kMaxParts] = {};
   const int64_t* prv[kMaxParts] = {};
   PeerParts peers;
-  cudaGetDevice(&peers.cur);
+  peers.cur = cur_dev;
   for (int p = 0; p < nparts; ++p) {
-    peers.dev[p] = multi ? (peers.cur + p) % ndev_avail : peers.cur;
+    peers.dev[p] = multi ? devlist[p] : peers.cur;
     pshifts[p] = shifts + lo;
     prv[p] = rv + lo;
     if (peers.dev[p] == peers.cur) {
@@ -3222,6 +3244,33 @@ int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_byt
   rc = validate_out(out);
   if (rc) return rc;
   return run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int sp_plan_dp_devices(const sp_instances* in, sp_policies* out, const int32_t* devices,
+                       int32_t n_devices, void* ws, size_t ws_bytes, void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  rc = validate_out(out);
+  if (rc) return rc;
+  int cur = 0, count = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess || cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    set_error(SP_ERR_CUDA, "no CUDA device");
+    return SP_ERR_CUDA;
+  }
+  if (!devices || n_devices < 1 || n_devices > kMaxParts || devices[0] != cur) {
+    set_error(SP_ERR_INVALID, "devices: 1..%d entries, the first the current device (%d)", kMaxParts, cur);
+    return SP_ERR_INVALID;
+  }
+  for (int p = 0; p < n_devices; ++p)
+    if (devices[p] < 0 || devices[p] >= count) {
+      set_error(SP_ERR_INVALID, "devices[%d] = %d: no such device", p, devices[p]);
+      return SP_ERR_INVALID;
+    }
+  tl_grid_devices.assign(devices, devices + n_devices);
+  rc = run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+  tl_grid_devices.clear();
+  return rc;
 }
 
 int sp_build_dp_tables(const sp_instances* in, int64_t w_eff, double* client_table,

@@ -297,3 +297,25 @@ def test_full_size_batteries(gpu, name):
     _compare(bat, "dp", B.plan_dp(b).to_host())
     if bat.has("greedy"):
         _compare(bat, "greedy", B.plan_prefix(b, N.SP_GREEDY).to_host())
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0, 0]])
+def test_plan_dp_devices_partitions(gpu, devices, monkeypatch):
+    """sp_plan_dp_devices: the capacity axis of whole-GPU instances split over
+    a device list (here the one GPU listed several times: one launch per
+    partition, system-scope counters, the multi-device code path)."""
+    from paper_2410_10759_b200 import batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "grid")
+    for name, must in (("battery_large_chain", False), ("battery_wide", True)):
+        bat = Battery(name)
+        _compare(bat, "dp", B.plan_dp(_batch(bat, with_must=must), devices=devices).to_host())
+
+
+def test_plan_dp_devices_rejects_bad_lists(gpu):
+    from paper_2410_10759_b200 import _native as N, batch as B
+    import torch
+    bat = Battery("battery_wide")
+    b = _batch(bat)
+    for bad in ([1 + torch.cuda.device_count()], [torch.cuda.device_count() + 3, 0]):
+        with pytest.raises(Exception):
+            B.plan_dp(b, devices=bad)
