@@ -384,7 +384,7 @@ def main():
             },
             "clocks": clk,
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
             line["cpu_baseline"] = cpu_baseline(req_np, args.cpu_sample)
         print(json.dumps(line), flush=True)
     if world > 1:
