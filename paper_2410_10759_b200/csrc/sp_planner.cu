@@ -2066,8 +2066,8 @@ enum DpVariant { DPV_SMEM = 0, DPV_CLUSTER = 1, DPV_GLOBAL = 2, DPV_COOP = 3, DP
 
 // ---- single-CTA kernels: T x E configurations ------------------------------
 
-constexpr int kSingleT[] = {64, 128, 256, 512};
-constexpr int kSingleE = 4;
+constexpr int kSingleT[] = {64, 128, 256, 512, 128, 256};
+constexpr int kSingleEs[] = {4, 4, 4, 4, 8, 8};  // configs 4, 5: int32 domain only
 constexpr int kNumSingle = 4;
 
 int env_int(const char* name, int dflt) {
@@ -2075,16 +2075,25 @@ int env_int(const char* name, int dflt) {
   return v && *v ? atoi(v) : dflt;
 }
 
-// about four chunks per stage, at most 512 threads
-int single_cfg_for(int64_t ncol) {
+// about four chunks per stage, at most 512 threads (E = 4); int32 rows up
+// to 12k columns take 8 columns per thread, at most 256 threads (measured
+// +3-9 % at W = 1e3-1e4, -4 % from 18k: profiles/r01/single_e8)
+// (SPLITPLAN_DP_SINGLE_E = 4 or 8 forces one)
+int single_cfg_for(int64_t ncol, int mode = VM_F64) {
   const int force = env_int("SPLITPLAN_DP_THREADS", 0);
+  const int e = env_int("SPLITPLAN_DP_SINGLE_E", 0);
+  if (mode == VM_INT32 && (e == 8 || (e == 0 && ncol <= 12288))) {
+    if (force == 128) return 4;
+    if (force == 256) return 5;
+    return (int64_t)kSingleT[4] * 8 * 4 >= ncol ? 4 : 5;
+  }
   for (int c = 0; c < kNumSingle; ++c)
     if (force == kSingleT[c]) return c;
   for (int c = 0; c < kNumSingle; ++c)
-    if ((int64_t)kSingleT[c] * kSingleE * 4 >= ncol) return c;
+    if ((int64_t)kSingleT[c] * kSingleEs[c] * 4 >= ncol) return c;
   return kNumSingle - 1;
 }
-int64_t single_ch(int cfg) { return (int64_t)kSingleT[cfg] * kSingleE; }
+int64_t single_ch(int cfg) { return (int64_t)kSingleT[cfg] * kSingleEs[cfg]; }
 int64_t single_cols(int cfg, int64_t ncol) {
   const int64_t ch = single_ch(cfg);
   return (ncol + ch - 1) / ch * ch;
@@ -2094,9 +2103,9 @@ size_t single_row_bytes(int mode, int64_t ncol, int cfg) {
   return 2 * (size_t)(single_ch(cfg) + single_cols(cfg, ncol)) * value_bytes(mode);
 }
 
-template <int MODE, bool SMEM, int T>
+template <int MODE, bool SMEM, int T, int E = 4>
 int launch_single_t(const DpArgs& a, int64_t n_items, size_t smem, cudaStream_t st) {
-  auto kern = dp_stage_kernel<MODE, SMEM, T, kSingleE>;
+  auto kern = dp_stage_kernel<MODE, SMEM, T, E>;
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)kSmemCap),
                       "cudaFuncSetAttribute(dp_stage_kernel)");
@@ -2107,6 +2116,8 @@ int launch_single_t(const DpArgs& a, int64_t n_items, size_t smem, cudaStream_t 
 
 template <int MODE, bool SMEM>
 int launch_single(const DpArgs& a, int64_t n_items, int cfg, size_t smem, cudaStream_t st) {
+  if (MODE == VM_INT32 && SMEM && cfg == 4) return launch_single_t<MODE, SMEM, 128, 8>(a, n_items, smem, st);
+  if (MODE == VM_INT32 && SMEM && cfg == 5) return launch_single_t<MODE, SMEM, 256, 8>(a, n_items, smem, st);
   switch (cfg) {
     case 0: return launch_single_t<MODE, SMEM, 64>(a, n_items, smem, st);
     case 1: return launch_single_t<MODE, SMEM, 128>(a, n_items, smem, st);
@@ -2533,7 +2544,7 @@ struct DpPlan {
 DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) {
   DpPlan p;
   const size_t vb = value_bytes(mode);
-  p.cfg = single_cfg_for(ncol);
+  p.cfg = single_cfg_for(ncol, (force == DPV_GLOBAL || tables) ? VM_F64 : mode);
   const size_t single_rows = single_row_bytes(mode, ncol, p.cfg);
   const bool fits_cta = single_rows + stage_bytes_mode(mode) <= kSmemCap;
   if (force == DPV_GLOBAL || (tables && force < 0)) p.variant = DPV_GLOBAL;

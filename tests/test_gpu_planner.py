@@ -199,9 +199,22 @@ def test_single_cta_thread_configs(gpu, threads, monkeypatch):
     """Every T x E instantiation of the single-CTA kernel (SMEM and global rows)."""
     from paper_2410_10759_b200 import batch as B
     monkeypatch.setenv("SPLITPLAN_DP_THREADS", threads)
+    monkeypatch.setenv("SPLITPLAN_DP_SINGLE_E", "4")
     for variant in ("smem", "global"):
         monkeypatch.setenv("SPLITPLAN_DP_VARIANT", variant)
         bat = Battery("battery_float")
+        _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
+
+
+@pytest.mark.parametrize("threads", ["128", "256", ""])
+def test_single_cta_eight_columns_per_thread(gpu, threads, monkeypatch):
+    """The int32 single-CTA kernel with 8 columns per thread per chunk."""
+    from paper_2410_10759_b200 import batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_SINGLE_E", "8")
+    monkeypatch.setenv("SPLITPLAN_DP_THREADS", threads)
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "smem")
+    for name in ("battery_acceptance", "battery_wide", "battery_special"):
+        bat = Battery(name)
         _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
 
 
