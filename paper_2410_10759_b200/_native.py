@@ -205,7 +205,8 @@ def workspace(min_bytes: int = 0) -> torch.Tensor:
             torch.cuda.empty_cache()
         free, _total = torch.cuda.mem_get_info(dev)
         cap = int(float(os.environ.get("SPLITPLAN_WS_GB", "64")) * (1 << 30))
-        want = max(min_bytes, min(cap, int(free * 0.45)), 64 << 20)
+        # default cap 64 GB (SPLITPLAN_WS_GB); never more than 85 % of what is free
+        want = max(min_bytes, min(cap, int(free * 0.85)), 64 << 20)
         _ws[key] = torch.empty(want, dtype=torch.uint8, device=dev)
     return _ws[key]
 

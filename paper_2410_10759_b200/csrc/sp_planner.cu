@@ -2835,7 +2835,10 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
   const size_t ckpt_bytes = align_up(2 * (size_t)ncol * vb, 256);
   const size_t bp_stage = (size_t)row_words * 4;
   const size_t fixed = align_up((size_t)G * nparts * 4, 256) + 256 + nparts * rows_bytes;
-  // segment length: everything at once if it fits, else ~sqrt(L * ckpt / bp) stages
+  // segment length K: everything at once if it fits; else the longest
+  // segments the workspace holds.  Segments are aligned to the END of the
+  // chain and the last one keeps its back-pointers from the forward pass, so
+  // the recompute costs L - K stages (2L - K in total), not L.
   int K = L;
   auto need = [&](int k) {
     const size_t nseg = (size_t)((L + k - 1) / k);
@@ -2844,9 +2847,15 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
   const int force_k = env_int("SPLITPLAN_GRID_SEGMENT", 0);
   if (force_k > 0) K = std::min(force_k, L);
   if (need(K) > avail) {
-    K = (int)std::max<double>(1.0, std::sqrt((double)L * (double)ckpt_bytes / (double)bp_stage));
-    K = std::min(K, L);
-    while (K > 1 && need(K) > avail && need(K / 2) < need(K)) K /= 2;
+    const size_t base = fixed + 2 * ckpt_bytes;
+    K = avail > base ? (int)std::min<size_t>((size_t)L, (avail - base) / bp_stage) : 1;
+    K = std::max(K, 1);
+    while (K > 1 && need(K) > avail) K -= std::max(1, K / 64);
+    if (need(K) > avail) {  // fall back to the smallest footprint, ~sqrt(L * ckpt / bp) stages
+      K = (int)std::max<double>(1.0, std::sqrt((double)L * (double)ckpt_bytes / (double)bp_stage));
+      K = std::min(K, L);
+      while (K > 1 && need(K) > avail && need(K / 2) < need(K)) K /= 2;
+    }
   }
   if (need(K) > avail) {
     set_required_workspace(need(K) + (avail > 0 ? 0 : 0) + (64 << 20));
@@ -2994,13 +3003,15 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
     return SP_OK;
   };
   int rc;
+  // segment boundaries, aligned to the end: segment sg is [seg_begin(sg), seg_begin(sg + 1))
+  auto seg_begin = [&](int sg) { return sg == 0 ? 0 : L - (nseg - sg) * K; };  // seg_begin(nseg) == L
   if (K == L) {
     rc = launch(0, L, nullptr, ckpt[1], bp);
     if (rc) return rc;
   } else {
     for (int sg = 0; sg < nseg; ++sg) {
-      const int k0 = sg * K;
-      rc = launch(k0, std::min(K, L - k0), sg ? ckpt[sg] : nullptr, ckpt[sg + 1], nullptr);
+      const int k0 = seg_begin(sg), cnt = seg_begin(sg + 1) - k0;
+      rc = launch(k0, cnt, sg ? ckpt[sg] : nullptr, ckpt[sg + 1], sg + 1 == nseg ? bp : nullptr);
       if (rc) return rc;
     }
   }
@@ -3020,9 +3031,11 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
       if (rc) return rc;
     } else {
       for (int sg = nseg - 1; sg >= 0; --sg) {
-        const int k0 = sg * K, cnt = std::min(K, L - k0);
-        rc = launch(k0, cnt, sg ? ckpt[sg] : nullptr, nullptr, bp);
-        if (rc) return rc;
+        const int k0 = seg_begin(sg), cnt = seg_begin(sg + 1) - k0;
+        if (sg + 1 < nseg) {  // the last segment's back-pointers are still there
+          rc = launch(k0, cnt, sg ? ckpt[sg] : nullptr, nullptr, bp);
+          if (rc) return rc;
+        }
         grid_backtrack_kernel<<<1, 1, 0, st>>>(*in, inst, shifts, bp, row_words, mode, k0, cnt, state,
                                                 *out);
         rc = launch_check("grid_backtrack_kernel launch");

@@ -23,6 +23,10 @@ def main():
     ap.add_argument("--L", type=int, default=100_000)
     ap.add_argument("--W", type=int, default=10_000_000)
     args = ap.parse_args()
+    import os
+    # the whole-GPU path keeps as many back-pointer stages as the workspace
+    # holds (the rest is recomputed from checkpoints): give it most of HBM
+    os.environ.setdefault("SPLITPLAN_WS_GB", "150")
     import torch
     from paper_2410_10759_b200 import _native as N
     from paper_2410_10759_b200 import batch as B

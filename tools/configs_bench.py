@@ -95,11 +95,13 @@ def bench_cfg5():
     cells = 1e5 * (1e7 + 1)
     return {"config": "cfg5", "L": 100000, "W": 10000000, "problem_cells": cells, "solve_s": sec,
             "problem_cells_per_s": cells / sec, "feasible": bool(p.feasible.item()),
-            "method": "grid wave kernel, checkpoint/recompute (2x DP work)", "timing": "CUDA events"}
+            "method": "grid wave kernel, checkpoint/recompute (the last segment keeps its back-pointers: 2L - K stages of DP work)", "timing": "CUDA events"}
 
 
 def main():
     ap = argparse.ArgumentParser()
+    import os
+    os.environ.setdefault("SPLITPLAN_WS_GB", "150")  # cfg5 keeps more back-pointer stages (less recompute)
     ap.add_argument("--configs", default="cfg1,cfg3,cfg4,cfg5")
     ap.add_argument("--cfg3-n", type=int, default=100_000)
     ap.add_argument("--cfg4-scenarios", type=int, default=4096)
