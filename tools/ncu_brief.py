@@ -8,7 +8,8 @@ import json
 import subprocess
 import sys
 
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1,
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
+         "s": 1,
          "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9}
 
 

@@ -36,7 +36,7 @@ KEYS = {
     "block": "launch__block_size",
     "cluster": "launch__cluster_dim_x",
 }
-SCALE = {"sector/ns": 1e9, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1e-3, "us": 1e-6,
+SCALE = {"sector/ns": 1e9, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ms": 1e-3, "us": 1e-6,
          "ns": 1e-9, "s": 1, "Ghz": 1e9, "Mhz": 1e6, "hz": 1}
 
 
