@@ -1626,6 +1626,241 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
 // End of the forward pass of a grid-solved instance: the end side from the
 // final row's last cell (planner.py:190-200), or the infeasible policy.
 // state = {j, client side, infeasible}.
+// ---------------------------------------------------------------------------
+// K2 grid variant with ONE row buffer (single partition, every stage's
+// shifts <= the halo width): the rows of a 1e7-column instance are 80 MB
+// instead of 240 MB with three buffers, so they stay in L2 instead of
+// streaming through HBM (profiles/r01/dp_grid_ncu_summary.json: 15.5 B/cell
+// of DRAM traffic with three buffers).  Each CTA updates its block IN PLACE,
+// chunks top-down: every predecessor window of chunk c lies below the top of
+// chunk c (reads go left), so the chunks above c that already hold the new
+// row are never read again this stage, and window copies already sit in
+// shared-memory slots before chunk c stores over them.  Nobody else reads the
+// main buffer: the right neighbour takes this block's last `hw` columns from
+// a small per-CTA halo buffer (3 stage slots) written alongside the row.
+// Producer waits per stage: own and left neighbour finished the previous
+// stage (RAW), right neighbour finished the stage two back (WAR on the halo
+// slot this stage overwrites).
+struct GridInplaceArgs {
+  const StageShift* shifts;
+  const int64_t* rv;
+  int k_begin, k_count;
+  int ncol, G, NC, sac, hw;  // hw: halo columns (multiple of 128 B, <= B)
+  const void* init_c;
+  const void* init_s;
+  void* out_c;
+  void* out_s;
+  uint32_t* bp;
+  int64_t bp_row_words;
+  uint32_t* prog;  // [G] completed stages + 1 (zeroed)
+  uint8_t* rows;   // [C|S][PAD | G*B | line]
+  uint8_t* halo;   // [G][3][C|S][hw]
+  int row_hint;    // 1: row stores with an L2 evict_last policy (SPLITPLAN_ROW_EVICT_LAST)
+};
+
+template <int MODE, int T, int E, int NSLOT>
+__global__ void __launch_bounds__(T + 32, 2) dp_grid_inplace_kernel(GridInplaceArgs a) {
+  using V = typename VT<MODE>::T;
+  constexpr int CH = T * E;
+  constexpr int AL = 16 / (int)sizeof(V);
+  constexpr int WIN = CH + AL;
+  constexpr int PAD = stream_pad<V, CH>();
+  constexpr int LINE = 128 / (int)sizeof(V);
+  constexpr int NWARP = T / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + NSLOT;
+  V* slots = reinterpret_cast<V*>(smem + 256);
+
+  const int G = a.G, NC = a.NC;
+  const int q = (int)blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int B = NC * CH;
+  const int Wt = G * B;
+  const int j0 = q * B;
+  const int ncol = a.ncol, hw = a.hw;
+  const int64_t span = (int64_t)PAD + Wt + LINE;
+  const V NEG = VT<MODE>::neg();
+  const V ZERO = V(0);
+  V* const Cm = reinterpret_cast<V*>(a.rows) + PAD;          // C row, column 0
+  V* const Sm = reinterpret_cast<V*>(a.rows) + span + PAD;   // S row, column 0
+  // halo of CTA o, stage slot t % 3: columns [o*B + B - hw, o*B + B) of row t
+  auto halo = [&](int o, int slot, int rs) {
+    return reinterpret_cast<V*>(a.halo) + ((int64_t)(o * 3 + slot) * 2 + rs) * hw;
+  };
+  const V* ic = reinterpret_cast<const V*>(a.init_c);
+  const V* is = reinterpret_cast<const V*>(a.init_s);
+
+  // row k_begin in the main buffer, its top hw columns in halo slot 0, NEG pads
+  for (int x = j0 + tid; x < j0 + B; x += blockDim.x) {
+    const bool valid = x < ncol;
+    V c, s;
+    if (ic) {
+      c = valid ? ic[x] : NEG;
+      s = valid ? is[x] : NEG;
+    } else {
+      c = (valid && a.sac) ? ZERO : NEG;
+      s = (valid && !a.sac) ? ZERO : NEG;
+    }
+    Cm[x] = c;
+    Sm[x] = s;
+    if (x >= j0 + B - hw) {
+      halo(q, 0, 0)[x - (j0 + B - hw)] = c;
+      halo(q, 0, 1)[x - (j0 + B - hw)] = s;
+    }
+  }
+  if (q == 0)
+    for (int x = tid - PAD; x < 0; x += blockDim.x) Cm[x] = Sm[x] = NEG;
+  if (q == G - 1)
+    for (int x = Wt + tid; x < Wt + LINE; x += blockDim.x) Cm[x] = Sm[x] = NEG;
+  if (tid == 0) {
+    for (int b = 0; b < NSLOT; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], NWARP);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    fence_proxy_async_global();
+    st_release_gpu(&a.prog[q], 1u);
+  }
+
+  if (warp == NWARP) {
+    // ---------------- producer warp ----------------
+    uint32_t u = 0;
+    for (int t = 0; t < a.k_count; ++t) {
+      const StageShift sh = a.shifts[a.k_begin + t];
+      // lane 0: own block (row t complete), lane 1: left neighbour (its halo
+      // of row t), lane 2: right neighbour (finished stage t - 2: halo slot reuse)
+      const int o = lane == 0 ? q : (lane == 1 ? q - 1 : q + 1);
+      const bool watch = lane < 3 && o >= 0 && o < G;
+      const uint32_t need = lane < 2 ? (uint32_t)(t + 1) : (uint32_t)max(t - 1, 0) + 1u;
+      const long long t0 = clock64();
+      for (uint32_t it = 1;; ++it) {
+        if (__all_sync(0xffffffffu, !watch || ld_acquire_gpu(&a.prog[o]) >= need)) break;
+        if ((it & 1023u) == 0 && clock64() - t0 > (30ll << 30)) __trap();
+      }
+      if (lane == 0) {
+        fence_proxy_async_global();
+        const V* hc = q > 0 ? halo(q - 1, t % 3, 0) - (j0 - hw) : nullptr;  // index by global column
+        const V* hs = q > 0 ? halo(q - 1, t % 3, 1) - (j0 - hw) : nullptr;
+        const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
+        for (int c = NC - 1; c >= 0; --c, ++u) {
+          const int slot = (int)(u % NSLOT);
+          mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
+          const int c0 = j0 + c * CH, ctop = c0 + CH;
+          mbar_expect_tx(&full[slot], 4u * WIN * sizeof(V));
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const bool cw = w == 0 || w == 3;
+            const int start = c0 - min(shf[w], ctop);
+            V* dst = slots + (slot * 4 + w) * WIN;
+            if (q == 0 || start < 0) {  // partition start: NEG pad in front of column 0
+              const int sa = start < 0 && q > 0 ? -PAD : (start & ~(AL - 1));
+              bulk_g2s(dst, (cw ? Cm : Sm) + sa, WIN * sizeof(V), &full[slot]);
+              continue;
+            }
+            const int sa = start & ~(AL - 1);
+            const int split = min(max(j0 - sa, 0), WIN);  // values from the left halo
+            if (split > 0)
+              bulk_g2s(dst, (cw ? hc : hs) + sa, split * sizeof(V), &full[slot]);
+            if (split < WIN)
+              bulk_g2s(dst + split, (cw ? Cm : Sm) + sa + split, (WIN - split) * sizeof(V), &full[slot]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- compute warps ----------------
+    const uint64_t pol = evict_first_policy();
+    const uint64_t rpol = evict_last_policy();
+    uint32_t u = 0;
+    StageShift sh_next = a.shifts[a.k_begin];
+    int64_t rbits_next = a.rv[a.k_begin];
+    const int hlo = j0 + B - hw;  // first column mirrored into this CTA's halo
+    for (int t = 0; t < a.k_count; ++t) {
+      const StageShift sh = sh_next;
+      const int64_t rbits = rbits_next;
+      if (t + 1 < a.k_count) {
+        sh_next = a.shifts[a.k_begin + t + 1];
+        rbits_next = a.rv[a.k_begin + t + 1];
+      }
+      const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
+      V* const hc = halo(q, (t + 1) % 3, 0) - hlo;
+      V* const hs = halo(q, (t + 1) % 3, 1) - hlo;
+      uint32_t* bprow = a.bp ? a.bp + (int64_t)t * a.bp_row_words + warp * bp_words(MODE) : nullptr;
+      for (int c = NC - 1; c >= 0; --c, ++u) {
+        const int slot = (int)(u % NSLOT);
+        const int c0 = j0 + c * CH, ctop = c0 + CH;
+        const V* ws = slots + slot * 4 * WIN + tid;
+        const V* pca = ws + 0 * WIN + ((c0 - min(sh.i, ctop)) & (AL - 1));
+        const V* pcb = ws + 1 * WIN + ((c0 - min(sh.id, ctop)) & (AL - 1));
+        const V* psa = ws + 2 * WIN + ((c0 - min(sh.s, ctop)) & (AL - 1));
+        const V* psb = ws + 3 * WIN + ((c0 - min(sh.su, ctop)) & (AL - 1));
+        mbar_wait(&full[slot], (u / NSLOT) & 1);
+        V cn[E], sn[E];
+        CellFlags f[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = c0 + e * T + tid;
+          f[e] = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk, j >= sh.i,
+                                      j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (bprow) {
+          uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
+#pragma unroll
+          for (int e = 0; e < E; ++e) emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f[e], pol);
+        }
+        V* qc = Cm + c0 + tid;
+        V* qs = Sm + c0 + tid;
+        if (a.row_hint) {  // keep the rows ahead of the streamed back-pointers in L2
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            st_hint(qc + e * T, cn[e], rpol);
+            st_hint(qs + e * T, sn[e], rpol);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            qc[e * T] = cn[e];
+            qs[e * T] = sn[e];
+          }
+        }
+        if (ctop > hlo) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int j = c0 + e * T + tid;
+            if (j >= hlo) {
+              hc[j] = cn[e];
+              hs[j] = sn[e];
+            }
+          }
+        }
+      }
+      named_barrier(1, T);
+      if (tid == 0) {
+        __threadfence();
+        fence_proxy_async_global();
+        st_release_gpu(&a.prog[q], (uint32_t)(t + 2));
+      }
+    }
+    if (a.out_c) {
+      named_barrier(1, T);
+      V* oc = reinterpret_cast<V*>(a.out_c);
+      V* os = reinterpret_cast<V*>(a.out_s);
+      for (int j = j0 + tid; j < j0 + B && j < ncol; j += T) {
+        oc[j] = Cm[j];
+        os[j] = Sm[j];
+      }
+    }
+  }
+}
+
 __global__ void grid_end_kernel(sp_instances in, InstInfo* info, int64_t inst, const void* last_c,
                                 const void* last_s, int64_t* state) {
   const InstInfo inf = info[inst];
@@ -2691,6 +2926,34 @@ int launch_grid_t(const GridArgs& g, cudaStream_t st) {
   return launch_check("dp_grid_kernel launch");
 }
 
+template <int MODE>
+int launch_grid_inplace_t(const GridInplaceArgs& g, cudaStream_t st) {
+  auto kern = dp_grid_inplace_kernel<MODE, kGridT, kGridE, ring_slots<MODE>()>;
+  int rc0 = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grid_smem(MODE)),
+                       "cudaFuncSetAttribute(dp_grid_inplace_kernel)");
+  if (rc0) return rc0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)g.G, 1, 1);
+  cfg.blockDim = dim3((unsigned)(kGridT + 32), 1, 1);
+  cfg.dynamicSmemBytes = grid_smem(MODE);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the waits are safe
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, g), "dp_grid_inplace_kernel launch");
+  if (rc) return rc;
+  return launch_check("dp_grid_inplace_kernel launch");
+}
+int launch_grid_inplace(int mode, const GridInplaceArgs& g, cudaStream_t st) {
+  switch (mode) {
+    case VM_INT32: return launch_grid_inplace_t<VM_INT32>(g, st);
+    case VM_F64: return launch_grid_inplace_t<VM_F64>(g, st);
+    default: return launch_grid_inplace_t<VM_F64_NAN>(g, st);
+  }
+}
+
 int launch_grid(int mode, const GridArgs& g, cudaStream_t st) {
   switch (mode) {
     case VM_INT32: return launch_grid_t<VM_INT32>(g, st);
@@ -2829,9 +3092,27 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
                                      st, 1);
     }
   }
+  // one row buffer updated in place (a single launch whose stage shifts all
+  // fit a one-neighbour halo): 1/3 of the row memory, L2-resident at cfg5
+  int64_t inplace_hw = 0;
+  if (nparts == 1 && !separate && env_int("SPLITPLAN_GRID_INPLACE", 1) != 0) {
+    std::vector<StageShift> hs(L);
+    int rc0 = check_cuda(cudaMemcpyAsync(hs.data(), shifts + lo, sizeof(StageShift) * L,
+                                         cudaMemcpyDeviceToHost, st), "copy stage shifts");
+    if (rc0) return rc0;
+    rc0 = check_cuda(cudaStreamSynchronize(st), "sync");
+    if (rc0) return rc0;
+    int ms = 0;
+    for (const StageShift& x : hs) ms = std::max(ms, std::max(std::max(x.i, x.id), std::max(x.s, x.su)));
+    const int64_t hw = ((int64_t)ms + 16 / (int64_t)vb + line - 1) / line * line;
+    if (hw <= B) inplace_hw = hw;
+  }
+  const bool inplace = inplace_hw > 0;
   const int64_t span = (kGridCH + line) + halo + G * B + line;
   const int64_t row_words = bp_row_words_for(mode, (int64_t)nparts * G * B);
-  const size_t rows_bytes = align_up(2 * kRowBufs * (size_t)span * vb, 256);
+  const size_t rows_bytes = inplace ? align_up(2 * (size_t)span * vb, 256) +
+                                          align_up((size_t)G * 3 * 2 * (size_t)inplace_hw * vb, 256)
+                                    : align_up(2 * kRowBufs * (size_t)span * vb, 256);
   const size_t ckpt_bytes = align_up(2 * (size_t)ncol * vb, 256);
   const size_t bp_stage = (size_t)row_words * 4;
   const size_t fixed = align_up((size_t)G * nparts * 4, 256) + 256 + nparts * rows_bytes;
@@ -2971,7 +3252,30 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
       cudaEventCreate(&e1);
       cudaEventRecord(e0, st);
     }
-    if (!separate) {
+    if (inplace) {
+      GridInplaceArgs gi = {};
+      gi.shifts = g.shifts;
+      gi.rv = g.rv;
+      gi.k_begin = g.k_begin;
+      gi.k_count = g.k_count;
+      gi.ncol = g.ncol;
+      gi.G = G;
+      gi.NC = NC;
+      gi.sac = g.sac;
+      gi.hw = (int)inplace_hw;
+      gi.init_c = g.init_c;
+      gi.init_s = g.init_s;
+      gi.out_c = g.out_c;
+      gi.out_s = g.out_s;
+      gi.bp = g.bp;
+      gi.bp_row_words = g.bp_row_words;
+      gi.prog = progs[0];
+      gi.rows = rows[0];
+      gi.halo = rows[0] + align_up(2 * (size_t)span * vb, 256);
+      gi.row_hint = env_int("SPLITPLAN_ROW_EVICT_LAST", 0) ? 1 : 0;
+      rc = launch_grid_inplace(mode, gi, st);
+      if (rc) return rc;
+    } else if (!separate) {
       rc = launch_grid(mode, g, st);
       if (rc) return rc;
     } else {  // one launch per partition, all in flight together

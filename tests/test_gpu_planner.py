@@ -247,13 +247,17 @@ def test_own_kernel_geometries(gpu, cluster, cfg, bufs, occ, monkeypatch):
         _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
 
 
+@pytest.mark.parametrize("inplace", ["1", "0"])
 @pytest.mark.parametrize("segment", ["0", "7", "1"])
-def test_grid_checkpoint_recompute(gpu, segment, monkeypatch):
+def test_grid_checkpoint_recompute(gpu, segment, inplace, monkeypatch):
     """The whole-GPU path for one huge instance, with the back-pointers kept
-    whole (segment 0) or recomputed from checkpoint rows every 7 / 1 stages."""
+    whole (segment 0) or recomputed from checkpoint rows every 7 / 1 stages;
+    one row buffer updated in place (where the shifts fit a one-neighbour
+    halo) or three buffers."""
     from paper_2410_10759_b200 import batch as B
     monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "grid")
     monkeypatch.setenv("SPLITPLAN_GRID_SEGMENT", segment)
+    monkeypatch.setenv("SPLITPLAN_GRID_INPLACE", inplace)
     for name in ("battery_wide", "battery_special"):
         bat = Battery(name)
         _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
