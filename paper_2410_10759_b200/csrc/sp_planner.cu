@@ -789,6 +789,7 @@ struct StreamGeom {
   int row_hint;  // L2 policy of the row stores (set at launch)
   int diag;      // diagnostics only (SPLITPLAN_STREAM_DIAG; results are wrong when set):
                  // bit 0 skips the stage waits, bit 1 skips the window copies
+  int cfg;       // kStreamCfgs index (host side)
 };
 
 constexpr int kRowBufs = 3;
@@ -2370,37 +2371,40 @@ int launch_single(const DpArgs& a, int64_t n_items, int cfg, size_t smem, cudaSt
 struct StreamCfg {
   int T, E, NSLOT;
 };
-constexpr StreamCfg kStreamCfgs[] = {{256, 4, 6}, {256, 8, 3}, {128, 8, 6}, {256, 4, 3}};
+constexpr StreamCfg kStreamCfgs[] = {{256, 4, 6}, {256, 8, 3}, {128, 8, 6}, {256, 4, 3}, {256, 6, 4}};
 constexpr int kStreamCfgF64 = 3;
 // bulk-copy ring depth of the grid kernel (T = 256, E = 4)
 template <int MODE> constexpr int ring_slots() { return MODE == VM_INT32 ? 6 : 3; }
 inline int ring_slots_rt(int mode) { return mode == VM_INT32 ? 6 : 3; }
-int stream_cfg_index(int mode) {
+// SPLITPLAN_STREAM_CFG forces one configuration; otherwise the int32 domain
+// picks between 256 x 8 and 256 x 6 per width (stream_geom), the fp64
+// domains use 256 x 4.
+int stream_forced_cfg(int mode) {
   if (mode != VM_INT32) return kStreamCfgF64;
-  const int c = env_int("SPLITPLAN_STREAM_CFG", 1);  // 256 x 8 (measured 4.67e11 vs 4.54e11 cells/s at cfg2)
-  return c < 0 || c > 2 ? 1 : c;
+  const int c = env_int("SPLITPLAN_STREAM_CFG", -1);
+  return c < 0 || c > 4 || c == kStreamCfgF64 ? -1 : c;
 }
-StreamCfg stream_cfg(int mode) { return kStreamCfgs[stream_cfg_index(mode)]; }
 
-int stream_threads(int mode) { return stream_cfg(mode).T; }
-int64_t stream_ch(int mode) { return (int64_t)stream_cfg(mode).T * stream_cfg(mode).E; }
+int stream_threads(int cfg) { return kStreamCfgs[cfg].T; }
+int64_t stream_ch(int cfg) { return (int64_t)kStreamCfgs[cfg].T * kStreamCfgs[cfg].E; }
 // live rows of co-resident instances kept in L2 (SPLITPLAN_L2_BUDGET_MB).
 // Measured at cfg2 (profiles/r01/stream_cfg_diag/ncu_dram_G*.csv): ~69 MB of
 // rows stay resident (0.05 B/cell of DRAM reads), ~94 MB already spill
-// (2.3 B/cell of DRAM reads, 6.6 B/cell of write-backs).
+// (2.3 B/cell of DRAM reads, 6.6 B/cell of write-backs); 256 x 6 at G = 6
+// (81 MB) runs fastest (profiles/r01/stream_cfg_diag/e6_k2.jsonl).
 size_t l2_row_budget() {
   static size_t b = 0;
-  if (!b) b = (size_t)env_int("SPLITPLAN_L2_BUDGET_MB", 80) << 20;
+  if (!b) b = (size_t)env_int("SPLITPLAN_L2_BUDGET_MB", 90) << 20;
   return b;
 }
 
-size_t stream_smem(int mode) {
+size_t stream_smem(int mode, int cfg) {
   const size_t vb = value_bytes(mode);
-  return 256 + (size_t)stream_cfg(mode).NSLOT * 4 * (stream_ch(mode) + 16 / vb) * vb;
+  return 256 + (size_t)kStreamCfgs[cfg].NSLOT * 4 * (stream_ch(cfg) + 16 / vb) * vb;
 }
 int64_t stream_span(int mode, const StreamGeom& g) {
   const int64_t line = 128 / (int64_t)value_bytes(mode);
-  return (stream_ch(mode) + line) + (int64_t)g.G * g.NC * stream_ch(mode) + line;
+  return (stream_ch(g.cfg) + line) + (int64_t)g.G * g.NC * stream_ch(g.cfg) + line;
 }
 // row buffers of the streaming kernel: 2 (full-barrier semantics, default:
 // 2/3 of the L2 footprint lets G shrink to 5 at W = 1e5, measured 4.5e11 vs
@@ -2414,9 +2418,10 @@ size_t stream_row_bytes(int mode, const StreamGeom& g) {
   return 2 * (size_t)stream_bufs() * (size_t)stream_span(mode, g) * value_bytes(mode);
 }
 
-// instances per cluster of the streaming kernel (1 or 2; SPLITPLAN_STREAM_PAIR).
-// Pairs were measured slower on B200 (3.4-4.1e11 vs 4.4e11 cells/s at W = 1e5:
-// the doubled L2 footprint costs more than the hidden stage latency saves).
+// instances per cluster of the streaming kernel (1 or 2; SPLITPLAN_STREAM_PAIR,
+// 256 x 4 only).  Pairs were measured slower on B200 (3.4-4.1e11 vs 4.4e11
+// cells/s at W = 1e5: the doubled L2 footprint costs more than the hidden
+// stage latency saves).
 int stream_pair() {
   static int p = 0;
   if (!p) p = env_int("SPLITPLAN_STREAM_PAIR", 1) == 2 ? 2 : 1;
@@ -2424,64 +2429,71 @@ int stream_pair() {
 }
 
 template <int MODE, int T, int E, int NSLOT>
-int stream_occupancy_t() {
+int stream_occupancy_t(int cfg) {
   auto kern = dp_stream_kernel<MODE, T, E, NSLOT, 1, 2>;
   int n = 0;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(MODE)) !=
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stream_smem(MODE, cfg)) !=
           cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, T + 32, stream_smem(MODE)) != cudaSuccess) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, T + 32, stream_smem(MODE, cfg)) != cudaSuccess) {
     cudaGetLastError();
     n = 0;
   }
   return n > 0 ? n : 2;
 }
 template <int MODE>
-int stream_occupancy() {
-  if (MODE != VM_INT32) return stream_occupancy_t<MODE, 256, 4, 3>();
-  switch (stream_cfg_index(MODE)) {
-    case 1: return stream_occupancy_t<MODE, 256, 8, 3>();
-    case 2: return stream_occupancy_t<MODE, 128, 8, 6>();
-    default: return stream_occupancy_t<MODE, 256, 4, 6>();
+int stream_occupancy(int cfg) {
+  if (MODE != VM_INT32) return stream_occupancy_t<MODE, 256, 4, 3>(cfg);
+  switch (cfg) {
+    case 1: return stream_occupancy_t<MODE, 256, 8, 3>(cfg);
+    case 2: return stream_occupancy_t<MODE, 128, 8, 6>(cfg);
+    case 4: return stream_occupancy_t<MODE, 256, 6, 4>(cfg);
+    default: return stream_occupancy_t<MODE, 256, 4, 6>(cfg);
   }
 }
 
-// co-resident streaming CTAs on this device (cached per value domain)
-int stream_resident_ctas(int mode) {
-  static int cache[3] = {0, 0, 0};
-  if (!cache[mode]) {
+// co-resident streaming CTAs on this device (cached per value domain and configuration)
+int stream_resident_ctas(int mode, int cfg) {
+  static int cache[3][5] = {};
+  if (!cache[mode][cfg]) {
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
       cudaGetLastError();
       sms = 148;
     }
-    const int per_sm = mode == VM_INT32 ? stream_occupancy<VM_INT32>()
-                       : mode == VM_F64 ? stream_occupancy<VM_F64>()
-                                        : stream_occupancy<VM_F64_NAN>();
-    cache[mode] = sms * per_sm;
+    const int per_sm = mode == VM_INT32 ? stream_occupancy<VM_INT32>(cfg)
+                       : mode == VM_F64 ? stream_occupancy<VM_F64>(cfg)
+                                        : stream_occupancy<VM_F64_NAN>(cfg);
+    cache[mode][cfg] = sms * per_sm;
   }
-  return cache[mode];
+  return cache[mode][cfg];
 }
 
-// Cluster size: at least large enough that the rows of every co-resident
-// instance (stream_pair() per cluster) fit the L2 budget; among those, the G
-// minimising G * (NC + sync) -- the CTA-time of one stage in chunk units,
-// padding waste included, plus the stage-synchronisation latency per CTA
-// (about two chunks for single instances, measured on B200: at W = 1e5,
-// G = 7 x 14 chunks beats 8 x 13 and 14 x 7; paired instances hide most of
-// it behind the partner's stage).
-StreamGeom stream_geom(int mode, int64_t ncol) {
-  const int64_t nchunks = (ncol + stream_ch(mode) - 1) / stream_ch(mode);
-  const int resident = stream_resident_ctas(mode);
+// Cluster size for one configuration: at least large enough that the rows of
+// every co-resident instance (stream_pair() per cluster) fit the L2 budget;
+// among those, the G minimising G * (NC * CH + sync) -- the CTA-time of one
+// stage in columns, padding waste included, plus the stage-synchronisation
+// latency per CTA (about 4096 columns for single instances, measured on
+// B200; paired instances hide most of it behind the partner's stage).
+// Returns the geometry and its cost.
+StreamGeom stream_geom_cfg(int mode, int64_t ncol, int cfg, int64_t* cost) {
+  const int64_t ch = stream_ch(cfg);
+  const int64_t nchunks = (ncol + ch - 1) / ch;
+  const int resident = stream_resident_ctas(mode, cfg);
   const int force = env_int("SPLITPLAN_DP_CLUSTER", 0);
   auto geom = [&](int G) {
-    StreamGeom t{G, (int)((nchunks + G - 1) / G), 0, 0};
+    StreamGeom t{G, (int)((nchunks + G - 1) / G), 0, 0, 0, cfg};
     t.G = (int)((nchunks + t.NC - 1) / t.NC);
     return t;
   };
-  if (force >= 1 && force <= 16) return geom(force);
-  const int pair = stream_pair();
-  const int sync = pair == 2 ? 0 : 2;
+  const int pair = cfg == 0 ? stream_pair() : 1;
+  const int64_t sync = pair == 2 ? 0 : 4096;
+  auto cost_of = [&](const StreamGeom& t) { return (int64_t)t.G * ((int64_t)t.NC * ch + sync); };
+  if (force >= 1 && force <= 16) {
+    const StreamGeom t = geom(force);
+    *cost = cost_of(t);
+    return t;
+  }
   int gmin = 16;
   for (int G = 1; G <= 16; ++G)
     if ((size_t)(resident / G) * pair * stream_row_bytes(mode, geom(G)) <= l2_row_budget()) {
@@ -2491,15 +2503,24 @@ StreamGeom stream_geom(int mode, int64_t ncol) {
   StreamGeom best = geom(gmin);
   for (int G = gmin + 1; G <= 16; ++G) {
     const StreamGeom t = geom(G);
-    if ((int64_t)t.G * (t.NC + sync) < (int64_t)best.G * (best.NC + sync)) best = t;
+    if (cost_of(t) < cost_of(best)) best = t;
   }
+  *cost = cost_of(best);
   return best;
+}
+StreamGeom stream_geom(int mode, int64_t ncol) {
+  const int forced = stream_forced_cfg(mode);
+  int64_t c1 = 0, c2 = 0;
+  if (forced >= 0) return stream_geom_cfg(mode, ncol, forced, &c1);
+  const StreamGeom e8 = stream_geom_cfg(mode, ncol, 1, &c1);
+  const StreamGeom e6 = stream_geom_cfg(mode, ncol, 4, &c2);
+  return c2 < c1 ? e6 : e8;
 }
 
 template <int MODE, int T, int E, int NSLOT, int NI, int NBUF>
 int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
   auto kern = dp_stream_kernel<MODE, T, E, NSLOT, NI, NBUF>;
-  const size_t smem = stream_smem(MODE);
+  const size_t smem = stream_smem(MODE, geo.cfg);
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "cudaFuncSetAttribute(dp_stream_kernel)");
   if (rc) return rc;
@@ -2529,10 +2550,9 @@ int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream
 }
 template <int MODE>
 int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t st) {
-  if (MODE == VM_INT32 && stream_cfg_index(MODE) == 1)
-    return launch_stream_t<MODE, 256, 8, 3, 1, 2>(a, n_items, geo, st);
-  if (MODE == VM_INT32 && stream_cfg_index(MODE) == 2)
-    return launch_stream_t<MODE, 128, 8, 6, 1, 2>(a, n_items, geo, st);
+  if (MODE == VM_INT32 && geo.cfg == 1) return launch_stream_t<MODE, 256, 8, 3, 1, 2>(a, n_items, geo, st);
+  if (MODE == VM_INT32 && geo.cfg == 4) return launch_stream_t<MODE, 256, 6, 4, 1, 2>(a, n_items, geo, st);
+  if (MODE == VM_INT32 && geo.cfg == 2) return launch_stream_t<MODE, 128, 8, 6, 1, 2>(a, n_items, geo, st);
   constexpr int NS = MODE == VM_INT32 ? 6 : 3;
   const int sel = (stream_pair() == 2 ? 1 : 0) + (stream_bufs() == 2 ? 2 : 0);
   switch (sel) {
@@ -2772,7 +2792,7 @@ struct DpPlan {
   // launches sharing a key go out together
   bool same_launch(const DpPlan& o) const {
     return variant == o.variant && cfg == o.cfg && threads == o.threads && cgeo.G == o.cgeo.G &&
-           cgeo.B == o.cgeo.B && sgeo.G == o.sgeo.G && sgeo.NC == o.sgeo.NC;
+           cgeo.B == o.cgeo.B && sgeo.G == o.sgeo.G && sgeo.NC == o.sgeo.NC && sgeo.cfg == o.sgeo.cfg;
   }
 };
 
@@ -2801,10 +2821,10 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) 
       break;
     case DPV_STREAM:
       p.sgeo = stream_geom(mode, ncol);
-      p.threads = stream_threads(mode);
-      p.bp_row_words = bp_row_words_for(mode, (int64_t)p.sgeo.G * p.sgeo.NC * stream_ch(mode));
+      p.threads = stream_threads(p.sgeo.cfg);
+      p.bp_row_words = bp_row_words_for(mode, (int64_t)p.sgeo.G * p.sgeo.NC * stream_ch(p.sgeo.cfg));
       p.rows = align_up(stream_row_bytes(mode, p.sgeo), 256);
-      p.smem = stream_smem(mode);
+      p.smem = stream_smem(mode, p.sgeo.cfg);
       break;
     case DPV_OWN:
       p.sgeo = own_geom(mode, ncol);
