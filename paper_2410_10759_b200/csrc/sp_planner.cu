@@ -96,7 +96,7 @@ __global__ void weff_kernel(sp_instances in, int64_t* w_eff) {
 // ---------------------------------------------------------------------------
 // prep: W_eff, value domain, clamped shifts, scaled values
 
-__global__ void prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts, int64_t* rv) {
+__global__ void prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts, int64_t* rv, int2* reach) {
   __shared__ int64_t sh64[32];
   __shared__ uint64_t shu[32];
   __shared__ int shi[32];
@@ -156,6 +156,23 @@ __global__ void prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts,
         rv[l] = __double_as_longlong(r);
       }
     }
+    // reachable frontier: the first column of row k of C and of S that holds a
+    // reachable value (rows are monotone in j; every column below it is
+    // unreachable, NEG-like).  reach[lo + k] describes the row stage k reads.
+    // Not in the NaN domain, where "unreachable" cells may hold NaN.
+    __syncthreads();  // the block's clamped shifts are in global memory
+    if (threadIdx.x == 0 && reach) {
+      const bool sac = in.source_at_client[k] != 0;
+      int64_t mc = sac ? 0 : cap, ms = sac ? cap : 0;
+      for (int64_t l = lo; l < hi; ++l) {
+        reach[l] = mode == VM_F64_NAN ? make_int2(0, 0) : make_int2((int)min(mc, cap), (int)min(ms, cap));
+        const StageShift sh = shifts[l];
+        const int64_t nc = min(mc + sh.i, ms + sh.id), ns = min(ms + sh.s, mc + sh.su);
+        mc = min(nc, cap);
+        ms = min(ns, cap);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -196,6 +213,7 @@ struct DpArgs {
   InstInfo* info;
   const StageShift* shifts;
   const int64_t* rv;
+  const int2* reach;  // per stage: first reachable column of the C / S row it reads
   const DpWork* work;
   uint8_t* bp;
   uint8_t* rows;
@@ -818,6 +836,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGe
   uint64_t* empty = full + NSLOT;
   uint32_t* prog = reinterpret_cast<uint32_t*>(empty + NSLOT);  // [NI] stages completed
   V* slots = reinterpret_cast<V*>(smem + 256);                    // [NSLOT][4][WIN]
+  V* negwin = slots + NSLOT * 4 * WIN;                             // [WIN] of NEG: windows below the frontier
 
   const int G = geo.G, NC = geo.NC;
   const int q = (int)cluster_rank();
@@ -867,6 +886,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGe
         }
     }
   }
+  for (int x = tid; x < WIN; x += blockDim.x) negwin[x] = NEG;
   if (tid == 0) {
     for (int b = 0; b < NSLOT; ++b) {
       mbar_init(&full[b], 1);
@@ -888,6 +908,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGe
       for (int i = 0; i < ni; ++i) {
         if (k >= L[i]) continue;
         const StageShift sh = a.shifts[lo[i] + k];  // issued before the wait: latency overlaps it
+        const int2 rch = a.reach ? a.reach[lo[i] + k] : make_int2(0, 0);  // first reachable columns of C_k, S_k
         // every CTA <= q finished stage k (row k ready); WAR on the buffer this
         // stage overwrites: with 3 buffers every CTA finished k-1, with 2 every CTA k
         const uint32_t need =
@@ -910,13 +931,21 @@ __global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGe
               mbar_arrive(&full[slot]);
               continue;
             }
-            mbar_expect_tx(&full[slot], 4u * WIN * sizeof(V));
+            // a window entirely below its row's reachable frontier is all NEG:
+            // no copy, the compute warps read the NEG window instead
+            int start[4];
+            uint32_t ncopy = 0;
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
-              const int start = c0 - min(shf[w], ctop);
-              bulk_g2s(slots + (slot * 4 + w) * WIN, src[w] + (start & ~(AL - 1)), WIN * sizeof(V),
-                       &full[slot]);
+              start[w] = c0 - min(shf[w], ctop);
+              ncopy += start[w] + CH > ((w == 0 || w == 3) ? rch.x : rch.y) ? 1u : 0u;
             }
+            mbar_expect_tx(&full[slot], ncopy * WIN * sizeof(V));
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+              if (start[w] + CH > ((w == 0 || w == 3) ? rch.x : rch.y))
+                bulk_g2s(slots + (slot * 4 + w) * WIN, src[w] + (start[w] & ~(AL - 1)), WIN * sizeof(V),
+                         &full[slot]);
           }
         }
         __syncwarp();
@@ -933,6 +962,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGe
       for (int i = 0; i < ni; ++i) {
         if (k >= L[i]) continue;
         const StageShift sh = a.shifts[lo[i] + k];
+        const int2 rch = a.reach ? a.reach[lo[i] + k] : make_int2(0, 0);
         const int64_t rbits = a.rv[lo[i] + k];
         const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
         V* Cn = row(i, (k + 1) % NBUF, 0);
@@ -944,10 +974,13 @@ __global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGe
           const int slot = (int)(u % NSLOT);
           const int c0 = j0 + c * CH, ctop = c0 + CH;
           const V* ws = slots + slot * 4 * WIN + tid;
-          const V* pca = ws + 0 * WIN + ((c0 - min(sh.i, ctop)) & (AL - 1));
-          const V* pcb = ws + 1 * WIN + ((c0 - min(sh.id, ctop)) & (AL - 1));
-          const V* psa = ws + 2 * WIN + ((c0 - min(sh.s, ctop)) & (AL - 1));
-          const V* psb = ws + 3 * WIN + ((c0 - min(sh.su, ctop)) & (AL - 1));
+          const int sa = c0 - min(sh.i, ctop), sb = c0 - min(sh.id, ctop);
+          const int sc = c0 - min(sh.s, ctop), sd = c0 - min(sh.su, ctop);
+          // windows below the reachable frontier were not copied: read NEG
+          const V* pca = (sa + CH > rch.x ? ws + 0 * WIN : negwin + tid) + (sa & (AL - 1));
+          const V* pcb = (sb + CH > rch.y ? ws + 1 * WIN : negwin + tid) + (sb & (AL - 1));
+          const V* psa = (sc + CH > rch.y ? ws + 2 * WIN : negwin + tid) + (sc & (AL - 1));
+          const V* psb = (sd + CH > rch.x ? ws + 3 * WIN : negwin + tid) + (sd & (AL - 1));
           uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
           mbar_wait(&full[slot], (u / NSLOT) & 1);
           V cn[E], sn[E];
@@ -2399,8 +2432,8 @@ size_t l2_row_budget() {
 }
 
 size_t stream_smem(int mode, int cfg) {
-  const size_t vb = value_bytes(mode);
-  return 256 + (size_t)kStreamCfgs[cfg].NSLOT * 4 * (stream_ch(cfg) + 16 / vb) * vb;
+  const size_t vb = value_bytes(mode);  // ring slots + one NEG window
+  return 256 + (size_t)(kStreamCfgs[cfg].NSLOT * 4 + 1) * (stream_ch(cfg) + 16 / vb) * vb;
 }
 int64_t stream_span(int mode, const StreamGeom& g) {
   const int64_t line = 128 / (int64_t)value_bytes(mode);
@@ -3387,6 +3420,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   int64_t* rv = (int64_t*)cv.take(sizeof(int64_t) * total);
   int32_t* idx = (int32_t*)cv.take(sizeof(int32_t) * total);
   DpWork* work = (DpWork*)cv.take(sizeof(DpWork) * n);
+  int2* reach = (int2*)cv.take(sizeof(int2) * total);
   const size_t fixed = align_up(cv.used, 256);
   if (!ws || fixed > ws_bytes) {
     set_required_workspace(fixed + (1 << 20));
@@ -3394,7 +3428,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     return SP_ERR_WORKSPACE;
   }
   const int grid = (int)std::min<int64_t>(n, 1 << 20);
-  prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv);
+  prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv, reach);
   int rc = launch_check("prep_kernel launch");
   if (rc) return rc;
 
@@ -3469,6 +3503,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   a.sac = in->source_at_client;
   a.info = info;
   a.shifts = shifts;
+  a.reach = env_int("SPLITPLAN_NO_REACH", 0) ? nullptr : reach;
   a.rv = rv;
   a.work = work;
   a.bp = dyn;
