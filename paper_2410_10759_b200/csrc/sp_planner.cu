@@ -963,6 +963,10 @@ __global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGe
         if (k >= L[i]) continue;
         const StageShift sh = a.shifts[lo[i] + k];
         const int2 rch = a.reach ? a.reach[lo[i] + k] : make_int2(0, 0);
+        // every cell of row k+1 below both frontiers is unreachable
+        const int64_t next_front = a.reach ? min(min((int64_t)rch.x + sh.i, (int64_t)rch.y + sh.id),
+                                                 min((int64_t)rch.y + sh.s, (int64_t)rch.x + sh.su))
+                                           : 0;
         const int64_t rbits = a.rv[lo[i] + k];
         const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
         V* Cn = row(i, (k + 1) % NBUF, 0);
@@ -984,13 +988,18 @@ __global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGe
           uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
           mbar_wait(&full[slot], (u / NSLOT) & 1);
           V cn[E], sn[E];
+          if ((int64_t)ctop <= next_front && !a.tab_c) {  // whole chunk unreachable: NEG, no back-pointers
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int j = c0 + e * T + tid;
-            const CellFlags f = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk,
-                                                     j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su,
-                                                     cn[e], sn[e]);
-            emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f, pol);
+            for (int e = 0; e < E; ++e) cn[e] = sn[e] = NEG;
+          } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const int j = c0 + e * T + tid;
+              const CellFlags f = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk,
+                                                       j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su,
+                                                       cn[e], sn[e]);
+              emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f, pol);
+            }
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done reading the slot
@@ -1391,6 +1400,7 @@ constexpr int kMaxParts = 8;
 struct GridArgs {
   const StageShift* shifts;  // stage records of the instance (index = stage)
   const int64_t* rv;         // stage values in the value domain
+  const int2* reach;         // per stage: first reachable global column of the C / S row it reads
   int k_begin, k_count;      // stage range of this launch
   int ncol;                  // W_eff + 1
   int G, NC;                 // CTAs per partition, chunks per CTA
@@ -1445,6 +1455,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + NSLOT;
   V* slots = reinterpret_cast<V*>(smem + 256);
+  V* negwin = slots + NSLOT * 4 * WIN;  // [WIN] of NEG: windows below the reachable frontier
 
   const int G = a.G, NC = a.NC;
   const int part = a.part_base + (int)blockIdx.x / G;
@@ -1516,6 +1527,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
     if (buf == 0)
       for (int j = j0 + tid; j < j0 + B; j += blockDim.x) init_at(p0 + j, Cb[j], Sb[j]);
   }
+  for (int x = tid; x < WIN; x += blockDim.x) negwin[x] = NEG;
   if (tid == 0) {
     for (int b = 0; b < NSLOT; ++b) {
       mbar_init(&full[b], 1);
@@ -1556,14 +1568,20 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
         const V* Sc = row(t % kRowBufs, 1);
         const V* src[4] = {Cc, Sc, Sc, Cc};
         const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
+        const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
+        const int mrow[4] = {rch.x, rch.y, rch.y, rch.x};
         for (int c = 0; c < NC; ++c, ++u) {
           const int slot = (int)(u % NSLOT);
           mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
           const int c0g = j0g + c * CH, ctop = c0g + CH;
-          mbar_expect_tx(&full[slot], 4u * WIN * sizeof(V));
+          uint32_t ncopy = 0;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) ncopy += c0g - min(shf[w], ctop) + CH > mrow[w] ? 1u : 0u;
+          mbar_expect_tx(&full[slot], ncopy * WIN * sizeof(V));
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
             const int start = c0g - min(shf[w], ctop);
+            if (start + CH <= mrow[w]) continue;  // below the reachable frontier: all NEG, no copy
             // Partition 0 keeps NEG in front of column 0 (halo + NEG area), so
             // partially negative windows read it in place.  In later
             // partitions start < 0 only when the shift was clamped (every cell
@@ -1594,27 +1612,40 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
       V* Cn = row((t + 1) % kRowBufs, 0);
       V* Sn = row((t + 1) % kRowBufs, 1);
       uint32_t* bprow = a.bp ? a.bp + (int64_t)t * a.bp_row_words + warp * bp_words(MODE) : nullptr;
+      const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
+      // every cell of row t+1 below both frontiers is unreachable
+      const int64_t next_front = a.reach ? min(min((int64_t)rch.x + sh.i, (int64_t)rch.y + sh.id),
+                                               min((int64_t)rch.y + sh.s, (int64_t)rch.x + sh.su))
+                                         : 0;
       for (int c = 0; c < NC; ++c, ++u) {
         const int slot = (int)(u % NSLOT);
         const int c0 = j0 + c * CH;       // local
         const int c0g = p0 + c0, ctop = c0g + CH;
+        const int sa = c0g - min(sh.i, ctop), sb = c0g - min(sh.id, ctop);
+        const int sc = c0g - min(sh.s, ctop), sd = c0g - min(sh.su, ctop);
         const V* ws = slots + slot * 4 * WIN + tid;
-        const V* pca = ws + 0 * WIN + ((c0g - min(sh.i, ctop)) & (AL - 1));
-        const V* pcb = ws + 1 * WIN + ((c0g - min(sh.id, ctop)) & (AL - 1));
-        const V* psa = ws + 2 * WIN + ((c0g - min(sh.s, ctop)) & (AL - 1));
-        const V* psb = ws + 3 * WIN + ((c0g - min(sh.su, ctop)) & (AL - 1));
+        const V* pca = (sa + CH > rch.x ? ws + 0 * WIN : negwin + tid) + (sa & (AL - 1));
+        const V* pcb = (sb + CH > rch.y ? ws + 1 * WIN : negwin + tid) + (sb & (AL - 1));
+        const V* psa = (sc + CH > rch.y ? ws + 2 * WIN : negwin + tid) + (sc & (AL - 1));
+        const V* psb = (sd + CH > rch.x ? ws + 3 * WIN : negwin + tid) + (sd & (AL - 1));
         mbar_wait(&full[slot], (u / NSLOT) & 1);
         V cn[E], sn[E];
         CellFlags f[E];
+        const bool dead = (int64_t)ctop <= next_front;  // whole chunk unreachable: NEG, no back-pointers
+        if (dead) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int j = c0g + e * T + tid;
-          f[e] = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk, j >= sh.i,
-                                      j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
+          for (int e = 0; e < E; ++e) cn[e] = sn[e] = NEG;
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int j = c0g + e * T + tid;
+            f[e] = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk, j >= sh.i,
+                                        j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
-        if (bprow) {
+        if (bprow && !dead) {
           uint32_t* bpc = bprow + (c0g >> 5) * bp_words(MODE);
 #pragma unroll
           for (int e = 0; e < E; ++e) emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f[e], pol);
@@ -1678,6 +1709,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
 struct GridInplaceArgs {
   const StageShift* shifts;
   const int64_t* rv;
+  const int2* reach;
   int k_begin, k_count;
   int ncol, G, NC, sac, hw;  // hw: halo columns (multiple of 128 B, <= B)
   const void* init_c;
@@ -1705,6 +1737,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_inplace_kernel(GridInplaceA
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + NSLOT;
   V* slots = reinterpret_cast<V*>(smem + 256);
+  V* negwin = slots + NSLOT * 4 * WIN;  // [WIN] of NEG: windows below the reachable frontier
 
   const int G = a.G, NC = a.NC;
   const int q = (int)blockIdx.x;
@@ -1747,6 +1780,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_inplace_kernel(GridInplaceA
     for (int x = tid - PAD; x < 0; x += blockDim.x) Cm[x] = Sm[x] = NEG;
   if (q == G - 1)
     for (int x = Wt + tid; x < Wt + LINE; x += blockDim.x) Cm[x] = Sm[x] = NEG;
+  for (int x = tid; x < WIN; x += blockDim.x) negwin[x] = NEG;
   if (tid == 0) {
     for (int b = 0; b < NSLOT; ++b) {
       mbar_init(&full[b], 1);
@@ -1781,15 +1815,21 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_inplace_kernel(GridInplaceA
         const V* hc = q > 0 ? halo(q - 1, t % 3, 0) - (j0 - hw) : nullptr;  // index by global column
         const V* hs = q > 0 ? halo(q - 1, t % 3, 1) - (j0 - hw) : nullptr;
         const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
+        const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
+        const int mrow[4] = {rch.x, rch.y, rch.y, rch.x};
         for (int c = NC - 1; c >= 0; --c, ++u) {
           const int slot = (int)(u % NSLOT);
           mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
           const int c0 = j0 + c * CH, ctop = c0 + CH;
-          mbar_expect_tx(&full[slot], 4u * WIN * sizeof(V));
+          uint32_t ncopy = 0;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) ncopy += c0 - min(shf[w], ctop) + CH > mrow[w] ? 1u : 0u;
+          mbar_expect_tx(&full[slot], ncopy * WIN * sizeof(V));
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
             const bool cw = w == 0 || w == 3;
             const int start = c0 - min(shf[w], ctop);
+            if (start + CH <= mrow[w]) continue;  // below the reachable frontier: all NEG, no copy
             V* dst = slots + (slot * 4 + w) * WIN;
             if (q == 0 || start < 0) {  // partition start: NEG pad in front of column 0
               const int sa = start < 0 && q > 0 ? -PAD : (start & ~(AL - 1));
@@ -1826,26 +1866,38 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_inplace_kernel(GridInplaceA
       V* const hc = halo(q, (t + 1) % 3, 0) - hlo;
       V* const hs = halo(q, (t + 1) % 3, 1) - hlo;
       uint32_t* bprow = a.bp ? a.bp + (int64_t)t * a.bp_row_words + warp * bp_words(MODE) : nullptr;
+      const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
+      const int64_t next_front = a.reach ? min(min((int64_t)rch.x + sh.i, (int64_t)rch.y + sh.id),
+                                               min((int64_t)rch.y + sh.s, (int64_t)rch.x + sh.su))
+                                         : 0;
       for (int c = NC - 1; c >= 0; --c, ++u) {
         const int slot = (int)(u % NSLOT);
         const int c0 = j0 + c * CH, ctop = c0 + CH;
+        const int sa = c0 - min(sh.i, ctop), sb = c0 - min(sh.id, ctop);
+        const int sc = c0 - min(sh.s, ctop), sd = c0 - min(sh.su, ctop);
         const V* ws = slots + slot * 4 * WIN + tid;
-        const V* pca = ws + 0 * WIN + ((c0 - min(sh.i, ctop)) & (AL - 1));
-        const V* pcb = ws + 1 * WIN + ((c0 - min(sh.id, ctop)) & (AL - 1));
-        const V* psa = ws + 2 * WIN + ((c0 - min(sh.s, ctop)) & (AL - 1));
-        const V* psb = ws + 3 * WIN + ((c0 - min(sh.su, ctop)) & (AL - 1));
+        const V* pca = (sa + CH > rch.x ? ws + 0 * WIN : negwin + tid) + (sa & (AL - 1));
+        const V* pcb = (sb + CH > rch.y ? ws + 1 * WIN : negwin + tid) + (sb & (AL - 1));
+        const V* psa = (sc + CH > rch.y ? ws + 2 * WIN : negwin + tid) + (sc & (AL - 1));
+        const V* psb = (sd + CH > rch.x ? ws + 3 * WIN : negwin + tid) + (sd & (AL - 1));
         mbar_wait(&full[slot], (u / NSLOT) & 1);
         V cn[E], sn[E];
         CellFlags f[E];
+        const bool dead = (int64_t)ctop <= next_front;  // whole chunk unreachable: NEG, no back-pointers
+        if (dead) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int j = c0 + e * T + tid;
-          f[e] = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk, j >= sh.i,
-                                      j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
+          for (int e = 0; e < E; ++e) cn[e] = sn[e] = NEG;
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int j = c0 + e * T + tid;
+            f[e] = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk, j >= sh.i,
+                                        j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
-        if (bprow) {
+        if (bprow && !dead) {
           uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
 #pragma unroll
           for (int e = 0; e < E; ++e) emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f[e], pol);
@@ -2938,8 +2990,8 @@ constexpr int64_t kGridMinCols = (int64_t)1 << 22;
 enum { DPV_GRID = 5 };
 
 size_t grid_smem(int mode) {
-  const size_t vb = value_bytes(mode);
-  return 256 + (size_t)ring_slots_rt(mode) * 4 * (kGridCH + 16 / vb) * vb;
+  const size_t vb = value_bytes(mode);  // ring slots + one NEG window
+  return 256 + (size_t)(ring_slots_rt(mode) * 4 + 1) * (kGridCH + 16 / vb) * vb;
 }
 
 template <int MODE>
@@ -3065,19 +3117,20 @@ struct PeerParts {
 // segment from the end, a recompute of the segment's back-pointers from its
 // checkpoint and a backtrack through it (2x the DP work, sqrt(L) memory).
 int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* info,
-                            const StageShift* shifts, const int64_t* rv, int32_t* idx, int64_t inst,
-                            int64_t lo, int L, int64_t ncol, int mode, uint8_t* dyn, size_t avail,
+                            const StageShift* shifts, const int64_t* rv, const int2* reach, int32_t* idx,
+                            int64_t inst, int64_t lo, int L, int64_t ncol, int mode, uint8_t* dyn, size_t avail,
                             cudaStream_t st, int force_parts);
 
 int run_grid_instance(const sp_instances* in, sp_policies* out, InstInfo* info, const StageShift* shifts,
-                      const int64_t* rv, int32_t* idx, int64_t inst, int64_t lo, int L, int64_t ncol,
-                      int mode, uint8_t* dyn, size_t avail, cudaStream_t st) {
-  return run_grid_instance_parts(in, out, info, shifts, rv, idx, inst, lo, L, ncol, mode, dyn, avail, st, 0);
+                      const int64_t* rv, const int2* reach, int32_t* idx, int64_t inst, int64_t lo, int L,
+                      int64_t ncol, int mode, uint8_t* dyn, size_t avail, cudaStream_t st) {
+  return run_grid_instance_parts(in, out, info, shifts, rv, reach, idx, inst, lo, L, ncol, mode, dyn, avail, st,
+                                 0);
 }
 
 int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* info,
-                            const StageShift* shifts, const int64_t* rv, int32_t* idx, int64_t inst,
-                            int64_t lo, int L, int64_t ncol, int mode, uint8_t* dyn, size_t avail,
+                            const StageShift* shifts, const int64_t* rv, const int2* reach, int32_t* idx,
+                            int64_t inst, int64_t lo, int L, int64_t ncol, int mode, uint8_t* dyn, size_t avail,
                             cudaStream_t st, int force_parts) {
   const size_t vb = value_bytes(mode);
   const int resident = mode == VM_INT32 ? grid_resident<VM_INT32>()
@@ -3141,14 +3194,17 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
     for (const StageShift& x : hs) ms = std::max(ms, std::max(std::max(x.i, x.id), std::max(x.s, x.su)));
     halo = ((int64_t)ms + 2 * line + line - 1) / line * line;
     if (halo > (int64_t)G * B) {  // the read-back spans a whole partition: no point splitting
-      return run_grid_instance_parts(in, out, info, shifts, rv, idx, inst, lo, L, ncol, mode, dyn, avail,
-                                     st, 1);
+      return run_grid_instance_parts(in, out, info, shifts, rv, reach, idx, inst, lo, L, ncol, mode, dyn,
+                                     avail, st, 1);
     }
   }
   // one row buffer updated in place (a single launch whose stage shifts all
-  // fit a one-neighbour halo): 1/3 of the row memory, L2-resident at cfg5
+  // fit a one-neighbour halo): 1/3 of the row memory, L2-resident at cfg5.
+  // Off by default (SPLITPLAN_GRID_INPLACE=1): with the reachable-frontier
+  // skips the three-buffer kernel is faster at cfg5 (3.34 s vs 3.87 s,
+  // profiles/r01/reach/cfg5_inplace_vs_3buf_reach.jsonl)
   int64_t inplace_hw = 0;
-  if (nparts == 1 && !separate && env_int("SPLITPLAN_GRID_INPLACE", 1) != 0) {
+  if (nparts == 1 && !separate && env_int("SPLITPLAN_GRID_INPLACE", 0) != 0) {
     std::vector<StageShift> hs(L);
     int rc0 = check_cuda(cudaMemcpyAsync(hs.data(), shifts + lo, sizeof(StageShift) * L,
                                          cudaMemcpyDeviceToHost, st), "copy stage shifts");
@@ -3204,12 +3260,14 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
   uint32_t* progs[kMaxParts] = {};
   const StageShift* pshifts[kMaxParts] = {};
   const int64_t* prv[kMaxParts] = {};
+  const int2* preach[kMaxParts] = {};
   PeerParts peers;
   peers.cur = cur_dev;
   for (int p = 0; p < nparts; ++p) {
     peers.dev[p] = multi ? devlist[p] : peers.cur;
     pshifts[p] = shifts + lo;
     prv[p] = rv + lo;
+    preach[p] = reach ? reach + lo : nullptr;
     if (peers.dev[p] == peers.cur) {
       rows[p] = (uint8_t*)cv.take(rows_bytes);
       progs[p] = prog + (size_t)p * G;
@@ -3231,6 +3289,17 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
     if (rc0) return rc0;
     pshifts[p] = sh_copy;
     prv[p] = rv_copy;
+    if (reach) {
+      int2* reach_copy = (int2*)peers.alloc(peers.dev[p], sizeof(int2) * L);
+      if (!reach_copy) {
+        set_error(SP_ERR_CUDA, "partition %d: device %d allocation failed", p, peers.dev[p]);
+        return SP_ERR_CUDA;
+      }
+      rc0 = check_cuda(cudaMemcpyPeerAsync(reach_copy, peers.dev[p], reach + lo, peers.cur, sizeof(int2) * L, st),
+                       "copy reachable frontiers to peer");
+      if (rc0) return rc0;
+      preach[p] = reach_copy;
+    }
   }
   if (multi) {  // every used device reaches every other one
     for (int p = 0; p < nparts; ++p)
@@ -3265,6 +3334,7 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
 
   GridArgs g = {};
   g.shifts = shifts + lo;
+  g.reach = reach ? reach + lo : nullptr;
   g.rv = rv + lo;
   g.ncol = (int)ncol;
   g.G = G;
@@ -3308,6 +3378,7 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
     if (inplace) {
       GridInplaceArgs gi = {};
       gi.shifts = g.shifts;
+      gi.reach = g.reach;
       gi.rv = g.rv;
       gi.k_begin = g.k_begin;
       gi.k_count = g.k_count;
@@ -3339,6 +3410,7 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
         gp.part_base = p;
         gp.launch_parts = 1;
         gp.shifts = pshifts[p];
+        gp.reach = preach[p];
         gp.rv = prv[p];
         cudaSetDevice(peers.dev[p]);
         rc = check_cuda(cudaStreamWaitEvent(peers.stream[p], peers.start, 0), "partition wait");
@@ -3479,6 +3551,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     items.push_back(it);
   }
 
+  const int2* a_reach = env_int("SPLITPLAN_NO_REACH", 0) ? nullptr : reach;
   // instances too large for a wave (or wider than 4M columns) run alone over
   // the whole GPU (grid path, checkpointing if needed)
   {
@@ -3491,7 +3564,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         rest.push_back(it);
         continue;
       }
-      rc = run_grid_instance(in, out, info, shifts, rv, idx, it.inst, hoff[it.inst], (int)it.L, it.ncol,
+      rc = run_grid_instance(in, out, info, shifts, rv, a_reach, idx, it.inst, hoff[it.inst], (int)it.L, it.ncol,
                              it.mode, dyn, avail, st);
       if (rc) return rc;
     }
@@ -3503,7 +3576,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   a.sac = in->source_at_client;
   a.info = info;
   a.shifts = shifts;
-  a.reach = env_int("SPLITPLAN_NO_REACH", 0) ? nullptr : reach;
+  a.reach = a_reach;
   a.rv = rv;
   a.work = work;
   a.bp = dyn;
