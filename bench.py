@@ -208,8 +208,8 @@ def onchip_roofline(variant: int, cells_per_s: float, sm_mhz: float | None) -> d
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--requests", type=int, default=10_000)
     ap.add_argument("--cpu-sample", type=int, default=0, help="requests timed on the CPU")
