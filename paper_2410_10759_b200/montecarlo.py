@@ -36,7 +36,7 @@ BETA_PER_MS = 0.057
 HORIZON = 2000
 OMEGA_REQUESTS = 500
 EXEC_MAX = 10
-SIM_BLOCK = 8192  # scenarios per replay launch (bounds host and device memory)
+SIM_BLOCK = 16384  # scenarios per replay launch (bounds host and device memory)
 
 
 @dataclass
@@ -82,8 +82,8 @@ def scenario_tables(req: dict, off: np.ndarray, model_names, solved: dict):
     S = len(off) - 1
     scen = np.repeat(np.arange(S), np.diff(off))
     keep = solved["dp"]["ok"] & solved["greedy"]["ok"] & solved["all_server"]["ok"]
-    order = np.lexsort((req["downlink_bps"], req["uplink_bps"], req["deadline_s"], req["seq_len"],
-                        name_rank, scen))
+    order = lexsort_device((req["downlink_bps"], req["uplink_bps"], req["deadline_s"], req["seq_len"],
+                            name_rank, scen))
     order = order[keep[order]]
     # identical coordinates collapse to one row (a dict keyed by coordinate)
     key = np.stack([scen[order], name_rank[order], req["seq_len"][order]]).T
@@ -98,14 +98,33 @@ def scenario_tables(req: dict, off: np.ndarray, model_names, solved: dict):
     np.cumsum(np.bincount(rows_scen, minlength=S), out=row_off[1:])
     loads = np.stack([solved["dp"]["load"][order], solved["greedy"]["load"][order],
                       solved["all_server"]["load"][order]], axis=1)
-    demand = np.empty_like(loads)
-    for s in range(S):
-        a, b = row_off[s], row_off[s + 1]
-        if a == b:
-            continue
-        norm = np.mean(loads[a:b, 2])  # throughput_sim.py:156, numpy order
-        demand[a:b] = loads[a:b] / norm
+    norm = segment_means(loads[:, 2], row_off)  # throughput_sim.py:156, numpy-order np.mean
+    demand = loads / norm[rows_scen][:, None]
     return row_off, demand, req["deadline_s"][order]
+
+
+def lexsort_device(keys, device=None) -> np.ndarray:
+    """np.lexsort(keys) (last key primary) as successive stable sorts on the
+    device, least significant key first -- the same permutation."""
+    dev = device or N.device()
+    n = len(keys[0])
+    idx = torch.arange(n, device=dev)
+    for k in keys:
+        kt = torch.from_numpy(np.ascontiguousarray(k)).to(dev)
+        idx = idx[torch.sort(kt[idx], stable=True).indices]
+    return idx.cpu().numpy()
+
+
+def segment_means(values: np.ndarray, row_off: np.ndarray) -> np.ndarray:
+    """np.mean of every CSR segment in numpy's summation order (sp_segment_sum
+    on the device, then / n); NaN for empty segments."""
+    from .evaluator import segment_sums
+    dev = N.device()
+    x = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(dev)
+    off = torch.from_numpy(np.ascontiguousarray(row_off, dtype=np.int64)).to(dev)
+    sums = segment_sums(x, off).cpu().numpy()
+    with np.errstate(invalid="ignore", divide="ignore"):
+        return sums / np.diff(row_off).astype(np.float64)
 
 
 def _skeleton_rows(sids, a, b, beta_per_ms, horizon, arr, gidx, execs, lo, hi):
@@ -132,6 +151,23 @@ def _skeleton_job(job):
             x.close()
 
 
+_POOL = None
+
+
+def _pool(procs: int):
+    """Forked worker processes for the skeletons, kept for the process's
+    lifetime (numpy only: the workers never touch CUDA)."""
+    global _POOL
+    if _POOL is None or _POOL[1] != procs:
+        import atexit
+        from multiprocessing import get_context
+        if _POOL is not None:
+            _POOL[0].terminate()
+        _POOL = (get_context("fork").Pool(procs), procs)
+        atexit.register(_POOL[0].terminate)
+    return _POOL[0]
+
+
 def skeletons(sids, a, b, beta_per_ms, horizon, procs=None):
     """Arrival skeletons of scenarios `sids` (tables rows [a, b)): arrivals,
     global table-row indices and execution counts, [n, horizon] each.
@@ -148,15 +184,14 @@ def skeletons(sids, a, b, beta_per_ms, horizon, procs=None):
         execs = np.empty((n, horizon), np.int64)
         _skeleton_rows(sids, a, b, beta_per_ms, horizon, arr, gidx, execs, 0, n)
         return arr, gidx, execs
-    from multiprocessing import get_context, shared_memory
+    from multiprocessing import shared_memory
     shms = [shared_memory.SharedMemory(create=True, size=max(1, n * horizon * 8)) for _ in range(3)]
     try:
         names = [x.name for x in shms]
         step = (n + procs - 1) // procs
         jobs = [(names, n, horizon, sids, a, b, beta_per_ms, lo, min(n, lo + step))
                 for lo in range(0, n, step)]
-        with get_context("fork").Pool(len(jobs)) as pool:
-            pool.map(_skeleton_job, jobs, chunksize=1)
+        _pool(procs).map(_skeleton_job, jobs, chunksize=1)
         arr = np.ndarray((n, horizon), np.float64, buffer=shms[0].buf).copy()
         gidx = np.ndarray((n, horizon), np.int64, buffer=shms[1].buf).copy()
         execs = np.ndarray((n, horizon), np.int64, buffer=shms[2].buf).copy()
@@ -189,8 +224,8 @@ def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORI
     sizes = np.diff(row_off)
     capacity = np.zeros(S)
     sim = np.flatnonzero(sizes > 0)
-    for s in sim:  # throughput_sim.py:172-176 (numpy-order mean)
-        capacity[s] = float(omega_requests) * np.mean(demand[row_off[s]:row_off[s + 1], 2])
+    # throughput_sim.py:172-176: omega x numpy-order mean of the nosplit demands
+    capacity[sim] = float(omega_requests) * segment_means(demand[:, 2], row_off)[sim]
 
     max_w = np.zeros((S, 3))
     mean_w = np.zeros((S, 3))

@@ -77,3 +77,15 @@ def test_cfg4_skeletons_match_reference_draws():
         assert np.array_equal(inline[0][r], arr)
         assert np.array_equal(inline[1][r], idx + a[r])
         assert np.array_equal(inline[2][r], ex)
+
+
+def test_lexsort_device_equals_numpy():
+    """The Monte-Carlo table sort (successive stable sorts, here on the CPU
+    device) is np.lexsort's permutation, ties and float keys included."""
+    import torch
+    from paper_2410_10759_b200 import montecarlo as MC
+    rng = np.random.default_rng(5)
+    n = 50_000
+    keys = (rng.choice([3e7, 1e8, 1e9], n), rng.choice([3e7, 2e8], n), rng.random(n).round(2),
+            rng.integers(128, 4096, n), rng.integers(0, 3, n), np.repeat(np.arange(n // 64 + 1), 64)[:n])
+    assert np.array_equal(np.lexsort(keys), MC.lexsort_device(keys, device=torch.device("cpu")))
