@@ -336,3 +336,17 @@ def test_plan_dp_devices_rejects_bad_lists(gpu):
     for bad in ([1 + torch.cuda.device_count()], [torch.cuda.device_count() + 3, 0]):
         with pytest.raises(Exception):
             B.plan_dp(b, devices=bad)
+
+
+@pytest.mark.parametrize("variant", ["stream", "grid"])
+@pytest.mark.parametrize("no_reach", ["0", "1"])
+def test_reachable_frontier_skips(gpu, variant, no_reach, monkeypatch):
+    """Window copies below the reachable frontier skipped and dead chunks left
+    uncomputed (default) or everything computed (SPLITPLAN_NO_REACH=1): the
+    same placements either way."""
+    from paper_2410_10759_b200 import batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", variant)
+    monkeypatch.setenv("SPLITPLAN_NO_REACH", no_reach)
+    for name, must in (("battery_large_chain", False), ("battery_wide", True), ("battery_large_model", True)):
+        bat = Battery(name)
+        _compare(bat, "dp", B.plan_dp(_batch(bat, with_must=must)).to_host())
