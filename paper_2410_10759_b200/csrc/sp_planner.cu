@@ -1,13 +1,20 @@
 // Planner kernels of the B200 placement engine (reference: planner.py).
 //
-//   prep_kernel       per-instance W_eff, value domain, clamped stage shifts
-//   dp_stage_kernel   K2: the two-state DP over the integer budget axis
-//                     (planner.py:128-143) with a uint8 back-pointer per cell
-//   backtrack_kernel  K3: end-side choice + pointer walk + _finish
-//                     (planner.py:88-107, 146-202)
-//   prefix_kernel     greedy / all-server / all-client (planner.py:205-225)
-//   exhaustive_kernel plan_oracle (planner.py:228-268)
-//   eq1_kernel        evaluator latency_of (evaluator.py:64-78)
+//   dp_core.cuh        prep_kernel (W_eff, value domain, clamped stage shifts,
+//                      reachable frontiers), the per-cell update, and
+//                      dp_stage_kernel: K2 with rows in one CTA's SMEM
+//                      (planner.py:128-143), 2-bit packed back-pointers
+//   dp_stream.cuh      K2 for wide rows: dp_stream_kernel (L2 rows, bulk-copy
+//                      windows), dp_own_kernel (experiment)
+//   dp_grid.cuh        K2 for one huge instance (cfg5): dp_grid_kernel,
+//                      dp_grid_inplace_kernel, checkpoint/backtrack kernels
+//   dp_cluster_coop.cuh  forced-only K2 variants (parity coverage)
+//   this file          backtrack_kernel (K3: end-side choice + pointer walk +
+//                      _finish, planner.py:88-107, 146-202), prefix_kernel
+//                      (greedy / all-server / all-client, planner.py:205-225),
+//                      exhaustive_kernel (plan_oracle, planner.py:228-268),
+//                      eq1_kernel (latency_of, evaluator.py:64-78), the host
+//                      planning of waves / variants / geometry, and the C ABI.
 //
 // See DESIGN.md for the data layout and the value domains.
 #include <stdlib.h>
@@ -31,2039 +38,10 @@ constexpr int64_t kMaxCols = (int64_t(1) << 31) - 64;
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// ---------------------------------------------------------------------------
-// value domains
-
-template <int MODE> struct VT;
-template <> struct VT<VM_INT32> {
-  using T = int32_t;
-  static __device__ __forceinline__ T neg() { return INT32_MIN; }
-};
-template <> struct VT<VM_F64> {
-  using T = double;
-  static __device__ __forceinline__ T neg() { return -INFINITY; }
-};
-template <> struct VT<VM_F64_NAN> {
-  using T = double;
-  static __device__ __forceinline__ T neg() { return -INFINITY; }
-};
-
-__device__ __forceinline__ double to_f64(int32_t v, double g) {
-  return v >= 0 ? dmul((double)v, g) : -INFINITY;
-}
-__device__ __forceinline__ double to_f64(double v, double) { return v; }
-
-__device__ __forceinline__ uint64_t gcd_u64(uint64_t a, uint64_t b) {
-  while (b) {
-    uint64_t t = a % b;
-    a = b;
-    b = t;
-  }
-  return a;
-}
-
-// ---------------------------------------------------------------------------
-// block reductions (128-thread prep blocks)
-
-template <typename T, typename Op>
-__device__ T block_reduce(T v, Op op, T* sh) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if (lane == 0) sh[wid] = v;
-  __syncthreads();
-  T r = sh[0];
-  for (int w = 1; w < nw; ++w) r = op(r, sh[w]);
-  __syncthreads();
-  return r;
-}
-
-// ---------------------------------------------------------------------------
-// W_eff only (planner.py:120-125)
-
-__global__ void weff_kernel(sp_instances in, int64_t* w_eff) {
-  __shared__ int64_t sh64[32];
-  for (int64_t k = blockIdx.x; k < in.n; k += gridDim.x) {
-    const int64_t lo = in.layer_off[k], hi = in.layer_off[k + 1];
-    int64_t worst = 0;
-    for (int64_t l = lo + threadIdx.x; l < hi; l += blockDim.x)
-      worst += max(in.client_units[l] + in.down_units[l], in.server_units[l] + in.up_units[l]);
-    worst = block_reduce(worst, [](int64_t a, int64_t b) { return a + b; }, sh64);
-    if (threadIdx.x == 0) w_eff[k] = min(in.budget[k], worst);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// prep: W_eff, value domain, clamped shifts, scaled values
-
-__global__ void prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts, int64_t* rv, int2* reach) {
-  __shared__ int64_t sh64[32];
-  __shared__ uint64_t shu[32];
-  __shared__ int shi[32];
-  for (int64_t k = blockIdx.x; k < in.n; k += gridDim.x) {
-    const int64_t lo = in.layer_off[k], hi = in.layer_off[k + 1];
-    int64_t worst = 0;
-    int finite = 1, integral = 1;
-    uint64_t isum = 0, g = 0;
-    for (int64_t l = lo + threadIdx.x; l < hi; l += blockDim.x) {
-      worst += max(in.client_units[l] + in.down_units[l], in.server_units[l] + in.up_units[l]);
-      const double r = in.r[l];
-      if (!isfinite(r)) {
-        finite = 0;
-      } else if (r != floor(r) || r >= 9007199254740992.0) {
-        integral = 0;
-      } else {
-        const uint64_t v = (uint64_t)r;  // r >= 0 (problem.py:151-153)
-        isum = min(isum + v, (uint64_t)1 << 62);
-        g = gcd_u64(g, v);
-      }
-    }
-    worst = block_reduce(worst, [](int64_t a, int64_t b) { return a + b; }, sh64);
-    finite = block_reduce(finite, [](int a, int b) { return a & b; }, shi);
-    integral = block_reduce(integral, [](int a, int b) { return a & b; }, shi);
-    isum = block_reduce(isum, [](uint64_t a, uint64_t b) { return min(a + b, (uint64_t)1 << 62); }, shu);
-    g = block_reduce(g, [](uint64_t a, uint64_t b) { return gcd_u64(a, b); }, shu);
-    if (g == 0) g = 1;
-    const int64_t W = min(in.budget[k], worst);
-    int32_t mode;
-    if (!finite) mode = VM_F64_NAN;
-    else if (integral && isum < ((uint64_t)1 << 53) && isum / g <= (uint64_t)INT32_MAX) mode = VM_INT32;
-    else mode = VM_F64;
-    if (threadIdx.x == 0) {
-      InstInfo r;
-      r.w_eff = W;
-      r.scale = (double)g;
-      r.end_c = -INFINITY;
-      r.end_s = -INFINITY;
-      r.mode = mode;
-      r.pad = 0;
-      info[k] = r;
-    }
-    const int64_t cap = min(W + 1, kMaxCols);
-    for (int64_t l = lo + threadIdx.x; l < hi; l += blockDim.x) {
-      const int64_t i = in.client_units[l], s = in.server_units[l];
-      const int64_t u = in.up_units[l], d = in.down_units[l];
-      StageShift sh;
-      sh.i = (int32_t)min(i, cap);
-      sh.id = (int32_t)min(i + d, cap);
-      sh.s = (int32_t)min(s, cap);
-      sh.su = (int32_t)min(s + u, cap);
-      shifts[l] = sh;
-      const double r = in.r[l];
-      if (mode == VM_INT32) {
-        rv[l] = (int64_t)((uint64_t)r / g);
-      } else {
-        rv[l] = __double_as_longlong(r);
-      }
-    }
-    // reachable frontier: the first column of row k of C and of S that holds a
-    // reachable value (rows are monotone in j; every column below it is
-    // unreachable, NEG-like).  reach[lo + k] describes the row stage k reads.
-    // Not in the NaN domain, where "unreachable" cells may hold NaN.
-    __syncthreads();  // the block's clamped shifts are in global memory
-    if (threadIdx.x == 0 && reach) {
-      const bool sac = in.source_at_client[k] != 0;
-      int64_t mc = sac ? 0 : cap, ms = sac ? cap : 0;
-      for (int64_t l = lo; l < hi; ++l) {
-        reach[l] = mode == VM_F64_NAN ? make_int2(0, 0) : make_int2((int)min(mc, cap), (int)min(ms, cap));
-        const StageShift sh = shifts[l];
-        const int64_t nc = min(mc + sh.i, ms + sh.id), ns = min(ms + sh.s, mc + sh.su);
-        mc = min(nc, cap);
-        ms = min(ns, cap);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K2: DP stage kernels
-//
-// One instance = two budget-indexed rows C and S (W_eff + 1 columns) updated
-// once per layer k (planner.py:128-143):
-//   C_k[j] = r_k + max(C_{k-1}[j - i_k], S_{k-1}[j - i_k - d_k])
-//   S_k[j] =       max(S_{k-1}[j - s_k], C_{k-1}[j - s_k - u_k])
-// Three variants hold the rows in different places:
-//   * dp_stage_kernel<ROWS_SMEM=true>   one CTA, rows in its SMEM
-//   * dp_cluster_kernel                 a thread-block cluster, rows split
-//                                       across the CTAs' distributed SMEM
-//   * dp_stage_kernel<ROWS_SMEM=false>  one CTA, rows in global memory
-// Single-CTA variants update the rows IN PLACE, walking 32-aligned chunks of
-// CH = E*T columns from the top down: a chunk computes its new cells into
-// registers (its reads only touch columns <= its own, which no later chunk of
-// this stage writes), then a barrier, then the writes.  Each row carries CH
-// cells of NEG padding in front, and each chunk clamps the stage shifts to
-// its top (shift' = min(shift, chunk_top)), so every read is a plain in-bounds
-// load: shifted indices that were negative land in the padding and read NEG.
-//
-// Back-pointers are ballot-packed per warp: for each 32-column group one
-// 32-bit word per flag -- C-stay, S-stay, and in the NaN-propagating domain
-// also C-switch and S-switch.  The flags are exactly the predicates
-// _backtrace evaluates (planner.py:159-178):
-//   C-stay  : j>=i    and C[k-1][j-i]   + r == C[k][j]
-//   C-switch: j>=i+d  and S[k-1][j-i-d] + r == C[k][j]
-//   S-stay  : j>=s    and S[k-1][j-s]       == S[k][j]
-//   S-switch: j>=s+u  and C[k-1][j-s-u]     == S[k][j]
-// Outside the NaN domain a reachable cell that does not stay always switches
-// (its value came from the other predecessor), so two words suffice.
-
-struct DpArgs {
-  const int64_t* layer_off;
-  const uint8_t* sac;
-  InstInfo* info;
-  const StageShift* shifts;
-  const int64_t* rv;
-  const int2* reach;  // per stage: first reachable column of the C / S row it reads
-  const DpWork* work;
-  uint8_t* bp;
-  uint8_t* rows;
-  double* tab_c;  // optional full-table output (build_dp_tables), n == 1
-  double* tab_s;
-};
-
-__host__ __device__ inline int bp_words(int mode) { return mode == VM_F64_NAN ? 4 : 2; }
-
-struct CellFlags {
-  bool c_stay, s_stay, c_sw, s_sw;
-};
-
-// One DP cell from its four predecessor values (NEG where the shifted column
-// is negative).  v* tell whether each shifted column was >= 0; only the NaN
-// domain needs them (elsewhere NEG can never reproduce a reachable value).
-template <int MODE, typename V>
-__device__ __forceinline__ CellFlags cell_update(V ca, V cb, V sa, V sb, V rk, bool vi, bool vid,
-                                                 bool vs, bool vsu, V& cn, V& sn) {
-  CellFlags f;
-  if (MODE == VM_INT32) {
-    // exact integer arithmetic: C-stay <=> ca >= cb, S-stay <=> sa >= sb
-    f.c_stay = ca >= cb;
-    f.s_stay = sa >= sb;
-    cn = (f.c_stay ? ca : cb) + rk;
-    sn = f.s_stay ? sa : sb;
-    f.c_sw = !f.c_stay;
-    f.s_sw = !f.s_stay;
-  } else if (MODE == VM_F64) {
-    const V cm = ca >= cb ? ca : cb;
-    sn = sa >= sb ? sa : sb;
-    cn = dadd(cm, rk);
-    f.c_stay = dadd(ca, rk) == cn;  // fl(a + r) == C[k][j], not a >= b
-    f.s_stay = sa == sn;
-    f.c_sw = !f.c_stay;
-    f.s_sw = !f.s_stay;
-  } else {  // np.maximum propagates NaN
-    const V cm = (ca != ca) ? ca : ((cb != cb) ? cb : (ca >= cb ? ca : cb));
-    sn = (sa != sa) ? sa : ((sb != sb) ? sb : (sa >= sb ? sa : sb));
-    cn = dadd(cm, rk);
-    f.c_stay = vi && dadd(ca, rk) == cn;
-    f.c_sw = vid && dadd(cb, rk) == cn;
-    f.s_stay = vs && sa == sn;
-    f.s_sw = vsu && sb == sn;
-  }
-  return f;
-}
-
-// warp-collective: pack the 32 lanes' flags of one column group into words
-template <int MODE>
-__device__ __forceinline__ void emit_bp(uint32_t* row_words, int group, int ngroups, CellFlags f,
-                                        bool active) {
-  const uint32_t m0 = __ballot_sync(0xffffffffu, active && f.c_stay);
-  const uint32_t m1 = __ballot_sync(0xffffffffu, active && f.s_stay);
-  if (MODE == VM_F64_NAN) {
-    const uint32_t m2 = __ballot_sync(0xffffffffu, active && f.c_sw);
-    const uint32_t m3 = __ballot_sync(0xffffffffu, active && f.s_sw);
-    if ((threadIdx.x & 31) == 0 && group < ngroups)
-      reinterpret_cast<uint4*>(row_words)[group] = make_uint4(m0, m1, m2, m3);
-  } else {
-    if ((threadIdx.x & 31) == 0 && group < ngroups)
-      reinterpret_cast<uint2*>(row_words)[group] = make_uint2(m0, m1);
-  }
-}
-
-// Materialise a pointer in a register so the compiler cannot re-associate
-// (base + offset) + index into wide 64-bit index arithmetic per load: every
-// predecessor load then costs one IMAD.WIDE.U32 on a chunk-uniform base.
-template <typename T>
-__device__ __forceinline__ const T* opaque(const T* p) {
-  asm("" : "+l"(p));
-  return p;
-}
-
-template <int MODE>
-__device__ __forceinline__ void load_stage_tile(const DpArgs& a, int64_t lo, int k, int L,
-                                                StageShift* st_sh, typename VT<MODE>::T* st_r) {
-  using V = typename VT<MODE>::T;
-  const int cnt = min(kStageTile, L - k);
-  for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
-    st_sh[t] = a.shifts[lo + k + t];
-    const int64_t bits = a.rv[lo + k + t];
-    if (MODE == VM_INT32) st_r[t] = (V)(int32_t)bits;
-    else st_r[t] = (V)__longlong_as_double(bits);
-  }
-}
-
-// Single-CTA kernel, T threads x E columns per chunk (CH = T*E), both
-// template constants so every predecessor load is `LDS [base + imm]` on four
-// chunk-uniform bases.  Rows hold CH cells of NEG padding in front and are
-// padded at the end to whole chunks (nch*CH columns), so no load, store or
-// back-pointer word needs a bounds check: cells past W_eff compute garbage
-// that no valid cell ever reads (reads only go left), and their back-pointer
-// bits are never visited.  bp rows are nch*CH/32 groups wide.
-template <int MODE, bool ROWS_SMEM, int T, int E>
-__global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1024 / T)) dp_stage_kernel(DpArgs a) {
-  using V = typename VT<MODE>::T;
-  constexpr int CH = T * E;
-  extern __shared__ __align__(16) unsigned char smem[];
-  StageShift* st_sh = reinterpret_cast<StageShift*>(smem);
-  V* st_r = reinterpret_cast<V*>(smem + kStageTile * sizeof(StageShift));
-  const size_t stage_bytes = align_up(kStageTile * (sizeof(StageShift) + sizeof(V)), 16);
-
-  const DpWork wk = a.work[blockIdx.x];
-  const int64_t inst = wk.inst;
-  const int64_t lo = a.layer_off[inst];
-  const int L = (int)(a.layer_off[inst + 1] - lo);
-  const int ncol = (int)(a.info[inst].w_eff + 1);
-  const double g = a.info[inst].scale;
-  const bool sac = a.sac[inst] != 0;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int nch = (ncol + CH - 1) / CH;
-  const int span = CH + nch * CH;
-  const int64_t row_words = wk.bp_row_words;
-
-  V* base = ROWS_SMEM ? reinterpret_cast<V*>(smem + stage_bytes)
-                      : reinterpret_cast<V*>(a.rows + wk.row_off);
-  V* Cp = base + CH;         // C row, column 0
-  V* Sp = base + span + CH;  // S row, column 0
-  const V NEG = VT<MODE>::neg();
-  const V ZERO = V(0);
-
-  for (int x = tid - CH; x < nch * CH; x += T) {
-    Cp[x] = (x >= 0 && x < ncol && sac) ? ZERO : NEG;
-    Sp[x] = (x >= 0 && x < ncol && !sac) ? ZERO : NEG;
-    if (a.tab_c && x >= 0 && x < ncol) {
-      a.tab_c[x] = sac ? 0.0 : -INFINITY;
-      a.tab_s[x] = sac ? -INFINITY : 0.0;
-    }
-  }
-
-  uint32_t* bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off);
-  for (int k = 0; k < L; ++k) {
-    const int kt = k % kStageTile;
-    if (kt == 0) {
-      __syncthreads();
-      load_stage_tile<MODE>(a, lo, k, L, st_sh, st_r);
-    }
-    __syncthreads();
-    const StageShift sh = st_sh[kt];
-    const V rk = st_r[kt];
-    uint32_t* bprow = bpw + (int64_t)k * row_words + warp * bp_words(MODE);
-
-    for (int c = nch - 1; c >= 0; --c) {
-      const int c0 = c * CH, ctop = c0 + CH;
-      // chunk-uniform clamped shifts: every read stays in [-CH, nch*CH)
-      const V* pca = Cp - min(sh.i, ctop) + c0 + tid;
-      const V* pcb = Sp - min(sh.id, ctop) + c0 + tid;
-      const V* psa = Sp - min(sh.s, ctop) + c0 + tid;
-      const V* psb = Cp - min(sh.su, ctop) + c0 + tid;
-      uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
-      V cn[E], sn[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int j = c0 + e * T + tid;
-        const CellFlags f = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk,
-                                                 j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su,
-                                                 cn[e], sn[e]);
-        emit_bp<MODE>(bpc + e * (T / 32) * bp_words(MODE), 0, 1, f, true);
-      }
-      __syncthreads();
-      V* qc = Cp + c0 + tid;
-      V* qs = Sp + c0 + tid;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        qc[e * T] = cn[e];
-        qs[e * T] = sn[e];
-      }
-      if (a.tab_c) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int j = c0 + e * T + tid;
-          if (j < ncol) {
-            a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn[e], g);
-            a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn[e], g);
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    a.info[inst].end_c = to_f64(Cp[ncol - 1], g);
-    a.info[inst].end_s = to_f64(Sp[ncol - 1], g);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K2 cluster variant: rows too long for one SM live in the distributed shared
-// memory of a thread-block cluster of G CTAs (G <= 16).  CTA q owns columns
-// [q*B, (q+1)*B) of both rows (B a multiple of 32), double-buffered (stage k
-// reads buffer k&1 and writes buffer (k&1)^1), so one cluster barrier per
-// stage orders everything: it releases this stage's writes and guarantees no
-// CTA still reads the buffer the next stage overwrites.  Predecessor values
-// come from whichever CTA owns the shifted column via ld.shared::cluster.
-// Only the packed back-pointer words reach HBM.
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ uint32_t cluster_addr(uint32_t local, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ int32_t ld_cluster(uint32_t addr, int32_t) {
-  int32_t v;
-  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ double ld_cluster(uint32_t addr, double) {
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_barrier() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-
-struct ClusterGeom {
-  int G;          // CTAs per instance
-  int B;          // columns owned per CTA (multiple of 32)
-  uint32_t magic; // owner(x) = umulhi(x, magic) == x / B for x < G * B
-};
-
-template <int MODE>
-__global__ void __launch_bounds__(kMaxThreads, 1) dp_cluster_kernel(DpArgs a, ClusterGeom geo) {
-  using V = typename VT<MODE>::T;
-  extern __shared__ __align__(16) unsigned char smem[];
-  StageShift* st_sh = reinterpret_cast<StageShift*>(smem);
-  V* st_r = reinterpret_cast<V*>(smem + kStageTile * sizeof(StageShift));
-  const size_t stage_bytes = align_up(kStageTile * (sizeof(StageShift) + sizeof(V)), 16);
-  V* rows = reinterpret_cast<V*>(smem + stage_bytes);  // [buf][C|S][B]
-
-  const int G = geo.G, B = geo.B;
-  const int q = (int)cluster_rank();
-  const DpWork wk = a.work[blockIdx.x / G];
-  const int64_t inst = wk.inst;
-  const int64_t lo = a.layer_off[inst];
-  const int L = (int)(a.layer_off[inst + 1] - lo);
-  const int ncol = (int)(a.info[inst].w_eff + 1);
-  const double g = a.info[inst].scale;
-  const bool sac = a.sac[inst] != 0;
-  const int T = blockDim.x, tid = threadIdx.x, warp = tid >> 5;
-  const int j0 = q * B;
-  const int jn = max(0, min(ncol, j0 + B) - j0);
-  const int group_end = (j0 + jn + 31) >> 5;  // this CTA's back-pointer groups end here
-  const int64_t row_words = wk.bp_row_words;
-  const V NEG = VT<MODE>::neg();
-  const V ZERO = V(0);
-  const uint32_t rows_sa = smem_addr(rows);
-
-  for (int t = tid; t < jn; t += T) {
-    rows[t] = sac ? ZERO : NEG;      // buf 0, C
-    rows[B + t] = sac ? NEG : ZERO;  // buf 0, S
-    if (a.tab_c) {
-      a.tab_c[j0 + t] = sac ? 0.0 : -INFINITY;
-      a.tab_s[j0 + t] = sac ? -INFINITY : 0.0;
-    }
-  }
-  // shared::cluster address of `rows` in every rank.  The window is linear in
-  // the rank on sm_100 (base + r * stride); verify that once and keep a table
-  // in SMEM as the fallback, so the inner loop never issues mapa (ADU pipe).
-  __shared__ uint32_t rank_base[16];
-  __shared__ int linear_ok;
-  if (tid < G) rank_base[tid] = cluster_addr(rows_sa, (uint32_t)tid);
-  __syncthreads();
-  if (tid == 0) {
-    int ok = 1;
-    const uint32_t stride = G > 1 ? rank_base[1] - rank_base[0] : 0;
-    for (int r = 0; r < G; ++r) ok &= rank_base[r] == rank_base[0] + (uint32_t)r * stride;
-    linear_ok = ok;
-  }
-  __syncthreads();
-  const bool linear = linear_ok != 0;
-  const uint32_t base0 = rank_base[0];
-  // per-rank step in the linear formula, net of the B columns a rank covers
-  const uint32_t rank_step = (G > 1 ? rank_base[1] - rank_base[0] : 0) - (uint32_t)(B * sizeof(V));
-  uint32_t* bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off);
-  cluster_barrier();
-  // the stage loop, instantiated once per addressing scheme (uniform branch)
-  auto stages = [&](auto lin_tag) {
-    constexpr bool LIN = decltype(lin_tag)::value;
-    // predecessor value of row `rs` (0 = C, 1 = S) in buffer `buf` at global column x
-    auto fetch = [&](int x0, uint32_t rowoff) -> V {
-      const int x = max(x0, 0);  // branch-free: load a valid cell, select NEG below
-      const uint32_t owner = __umulhi((uint32_t)x, geo.magic);
-      const uint32_t rel = rowoff + (uint32_t)x * sizeof(V);
-      uint32_t addr;
-      if (LIN) addr = base0 + owner * rank_step + rel;
-      else addr = rank_base[owner] + rel - owner * (uint32_t)(B * sizeof(V));
-      const V v = ld_cluster(addr, V());
-      return x0 >= 0 ? v : NEG;
-    };
-    for (int k = 0; k < L; ++k) {
-      const int kt = k % kStageTile;
-      if (kt == 0) {
-        load_stage_tile<MODE>(a, lo, k, L, st_sh, st_r);
-        __syncthreads();
-      }
-      const StageShift sh = st_sh[kt];
-      const V rk = st_r[kt];
-      const int cur = k & 1;
-      const uint32_t offC = (uint32_t)((cur * 2 + 0) * B * (int)sizeof(V));
-      const uint32_t offS = (uint32_t)((cur * 2 + 1) * B * (int)sizeof(V));
-      V* Cn = rows + ((cur ^ 1) * 2 + 0) * B;
-      V* Sn = rows + ((cur ^ 1) * 2 + 1) * B;
-      uint32_t* bprow = bpw + (int64_t)k * row_words;
-      constexpr int U = 4;
-      for (int t0 = 0; t0 < jn; t0 += U * T) {  // warp-uniform trip count
-        V ca[U], cb[U], sa[U], sb[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int t = t0 + u * T + tid;
-          const int j = j0 + (t < jn ? t : 0);
-          ca[u] = fetch(j - sh.i, offC);
-          cb[u] = fetch(j - sh.id, offS);
-          sa[u] = fetch(j - sh.s, offS);
-          sb[u] = fetch(j - sh.su, offC);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int t = t0 + u * T + tid;
-          const bool active = t < jn;
-          const int j = j0 + t;
-          V cn, sn;
-          const CellFlags f = cell_update<MODE, V>(ca[u], cb[u], sa[u], sb[u], rk, j >= sh.i,
-                                                   j >= sh.id, j >= sh.s, j >= sh.su, cn, sn);
-          // groups past this CTA's columns belong to the next rank: never store them
-          emit_bp<MODE>(bprow, (j0 + t0 + u * T) / 32 + warp, group_end, f, active);
-          if (active) {
-            Cn[t] = cn;
-            Sn[t] = sn;
-            if (a.tab_c) {
-              a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn, g);
-              a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn, g);
-            }
-          }
-        }
-      }
-      cluster_barrier();
-    }
-  };
-  if (linear) stages(std::true_type{});
-  else stages(std::false_type{});
-  // the CTA owning column ncol-1 publishes the end cell (buffer L & 1)
-  if (tid == 0 && ncol - 1 >= j0 && ncol - 1 < j0 + B) {
-    const int t = ncol - 1 - j0, buf = L & 1;
-    a.info[inst].end_c = to_f64(rows[(buf * 2 + 0) * B + t], g);
-    a.info[inst].end_s = to_f64(rows[(buf * 2 + 1) * B + t], g);
-  }
-  cluster_barrier();  // keep every CTA's SMEM alive until remote reads are done
-}
-
-// ---------------------------------------------------------------------------
-// K2 cooperative variant: a cluster of G CTAs shares one instance whose rows
-// live in global memory, double-buffered and sized so the rows of all
-// co-resident instances stay in L2.  CTA q computes the columns
-// [q*B, (q+1)*B) of the next buffer from any column of the current one; one
-// cluster barrier (release/acquire, which also invalidates L1) per stage.
-// Rows carry CH cells of NEG padding in front, and shifts are clamped per
-// chunk exactly as in dp_stage_kernel, so reads need no bounds checks.
-
-template <int MODE, int E>
-__global__ void __launch_bounds__(kStageThreads, 2) dp_coop_kernel(DpArgs a, ClusterGeom geo) {
-  using V = typename VT<MODE>::T;
-  extern __shared__ __align__(16) unsigned char smem[];
-  StageShift* st_sh = reinterpret_cast<StageShift*>(smem);
-  V* st_r = reinterpret_cast<V*>(smem + kStageTile * sizeof(StageShift));
-
-  const int G = geo.G, B = geo.B;
-  const int q = (int)cluster_rank();
-  const DpWork wk = a.work[blockIdx.x / G];
-  const int64_t inst = wk.inst;
-  const int64_t lo = a.layer_off[inst];
-  const int L = (int)(a.layer_off[inst + 1] - lo);
-  const int ncol = (int)(a.info[inst].w_eff + 1);
-  const double g = a.info[inst].scale;
-  const bool sac = a.sac[inst] != 0;
-  const int T = blockDim.x, tid = threadIdx.x, warp = tid >> 5;
-  const int CH = E * T;
-  const int span = CH + ncol;
-  const int j0 = q * B;
-  const int jend = min(ncol, j0 + B);
-  const int jn = max(0, jend - j0);
-  const int group_end = (jend + 31) >> 5;
-  const int64_t row_words = wk.bp_row_words;
-  const V NEG = VT<MODE>::neg();
-  const V ZERO = V(0);
-  V* base = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][CH pad + ncol]
-  auto row = [&](int buf, int rs) { return base + (int64_t)(buf * 2 + rs) * span + CH; };
-
-  for (int buf = 0; buf < 2; ++buf) {
-    V* Cb = row(buf, 0);
-    V* Sb = row(buf, 1);
-    if (q == 0)
-      for (int x = tid - CH; x < 0; x += T) Cb[x] = Sb[x] = NEG;  // padding, never rewritten
-    if (buf == 0)
-      for (int j = j0 + tid; j < jend; j += T) {
-        Cb[j] = sac ? ZERO : NEG;
-        Sb[j] = sac ? NEG : ZERO;
-        if (a.tab_c) {
-          a.tab_c[j] = sac ? 0.0 : -INFINITY;
-          a.tab_s[j] = sac ? -INFINITY : 0.0;
-        }
-      }
-  }
-  uint32_t* bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off);
-  cluster_barrier();
-  for (int k = 0; k < L; ++k) {
-    const int kt = k % kStageTile;
-    if (kt == 0) {
-      load_stage_tile<MODE>(a, lo, k, L, st_sh, st_r);
-      __syncthreads();
-    }
-    const StageShift sh = st_sh[kt];
-    const V rk = st_r[kt];
-    const int cur = k & 1;
-    const V* Cc = row(cur, 0);
-    const V* Sc = row(cur, 1);
-    V* Cn = row(cur ^ 1, 0);
-    V* Sn = row(cur ^ 1, 1);
-    uint32_t* bprow = bpw + (int64_t)k * row_words;
-    for (int c0 = j0; c0 < jend; c0 += CH) {  // warp-uniform trip count
-      const int ctop = c0 + CH;
-      // chunk-uniform bases such that base + jr (jr >= c0 >= 0, unsigned) is the
-      // clamped predecessor: one IMAD.WIDE.U32 per load
-      const V* pca = opaque(Cc - min(sh.i, ctop));
-      const V* pcb = opaque(Sc - min(sh.id, ctop));
-      const V* psa = opaque(Sc - min(sh.s, ctop));
-      const V* psb = opaque(Cc - min(sh.su, ctop));
-      V ca[E], cb[E], sa[E], sb[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int j = c0 + e * T + tid;
-        const uint32_t jr = (uint32_t)(j < jend ? j : jend - 1);
-        ca[e] = pca[jr];
-        cb[e] = pcb[jr];
-        sa[e] = psa[jr];
-        sb[e] = psb[jr];
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int j = c0 + e * T + tid;
-        const bool active = j < jend;
-        V cn, sn;
-        const CellFlags f = cell_update<MODE, V>(ca[e], cb[e], sa[e], sb[e], rk, j >= sh.i,
-                                                 j >= sh.id, j >= sh.s, j >= sh.su, cn, sn);
-        emit_bp<MODE>(bprow, (c0 + e * T) / 32 + warp, group_end, f, active);
-        if (active) {
-          Cn[(uint32_t)j] = cn;
-          Sn[(uint32_t)j] = sn;
-          if (a.tab_c) {
-            a.tab_c[(int64_t)(k + 1) * ncol + j] = to_f64(cn, g);
-            a.tab_s[(int64_t)(k + 1) * ncol + j] = to_f64(sn, g);
-          }
-        }
-      }
-    }
-    cluster_barrier();
-  }
-  if (tid == 0 && ncol - 1 >= j0 && ncol - 1 < jend) {
-    a.info[inst].end_c = to_f64(row(L & 1, 0)[ncol - 1], g);
-    a.info[inst].end_s = to_f64(row(L & 1, 1)[ncol - 1], g);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K2 streaming variant (rows longer than one SM's shared memory): a cluster
-// of G CTAs shares one instance, CTA q owning NC chunks of CH = T*E columns.
-// The rows live in global memory, TRIPLE-buffered, sized so the rows of every
-// co-resident instance stay in L2.  Each CTA is warp-specialised:
-//   * one producer warp fetches, for every chunk, the four predecessor windows
-//     (C at i, S at i+d, S at s, C at s+u; CH values + 128 B, 128-B aligned)
-//     with the bulk-copy engine (cp.async.bulk, completion on a `full`
-//     mbarrier) into an NSLOT-deep ring of shared-memory slots;
-//   * T compute threads read them with conflict-free LDS like the single-CTA
-//     kernel, store the new cells straight to the next row buffer (coalesced
-//     warp stores) and the back-pointer words with an L2 evict-first policy,
-//     and release the slot on its `empty` mbarrier.
-// Stages are ordered by per-CTA progress counters in shared memory, read by
-// the other CTAs of the cluster through DSMEM, instead of a cluster-wide
-// barrier: stage s reads row s-1 from buffer (s-1)%3 and writes row s to
-// buffer s%3, so the producer of CTA q may start stage s once every CTA at or
-// left of q finished stage s-1 (all reads go left: shifts are >= 0) and every
-// CTA finished stage s-2 (the last reader of the buffer stage s overwrites).
-// CTAs therefore run up to one stage apart and the bulk copies of the next
-// stage overlap the tail of the current one.
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void named_barrier(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_cluster_relaxed(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.relaxed.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_cluster_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.cluster.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ void fence_acq_rel_cluster() {
-  asm volatile("fence.acq_rel.cluster;" ::: "memory");
-}
-__device__ __forceinline__ uint64_t evict_last_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void st_hint(int32_t* p, int32_t v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ uint64_t evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void st_bp_words(uint32_t* p, uint32_t a, uint32_t b, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void st_bp_words(uint32_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
-                                            uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a), "r"(b),
-               "r"(c), "r"(d), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void discard_l2(const void* p) {
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
-}
-
-// warp-collective back-pointer emission with an L2 evict-first store
-template <int MODE>
-__device__ __forceinline__ void emit_bp_stream(uint32_t* words, CellFlags f, uint64_t pol) {
-  const uint32_t m0 = __ballot_sync(0xffffffffu, f.c_stay);
-  const uint32_t m1 = __ballot_sync(0xffffffffu, f.s_stay);
-  if (MODE == VM_F64_NAN) {
-    const uint32_t m2 = __ballot_sync(0xffffffffu, f.c_sw);
-    const uint32_t m3 = __ballot_sync(0xffffffffu, f.s_sw);
-    if ((threadIdx.x & 31) == 0) st_bp_words(words, m0, m1, m2, m3, pol);
-  } else {
-    if ((threadIdx.x & 31) == 0) st_bp_words(words, m0, m1, pol);
-  }
-}
-
-struct StreamGeom {
-  int G;         // CTAs per instance (cluster size)
-  int NC;        // chunks per CTA
-  int n_items;   // instances of the launch (set at launch)
-  int row_hint;  // L2 policy of the row stores (set at launch)
-  int diag;      // diagnostics only (SPLITPLAN_STREAM_DIAG; results are wrong when set):
-                 // bit 0 skips the stage waits, bit 1 skips the window copies
-  int cfg;       // kStreamCfgs index (host side)
-};
-
-constexpr int kRowBufs = 3;
-
-// values of NEG padding in front of a streamed row: one chunk plus one 128-B
-// line, so every window start (>= -CH) rounded down to 16 B stays in the row
-// and every CTA block starts on a 128-B line
-template <typename V, int CH>
-__host__ __device__ constexpr int stream_pad() { return CH + 128 / (int)sizeof(V); }
-
-// NI instances share one cluster and alternate stage by stage (A0 B0 A1 B1
-// ...): while the producer waits for the other CTAs to finish instance A's
-// stage k, the compute warps work through instance B's stage k, so the
-// stage synchronisation latency overlaps useful work.
-template <int MODE, int T, int E, int NSLOT, int NI, int NBUF>
-__global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGeom geo) {
-  using V = typename VT<MODE>::T;
-  constexpr int CH = T * E;
-  constexpr int AL = 16 / (int)sizeof(V);        // values per 16 B
-  constexpr int WIN = CH + AL;                    // values per staged window
-  constexpr int PAD = stream_pad<V, CH>();
-  constexpr int LINE = 128 / (int)sizeof(V);      // values per 128-B line
-  constexpr int NWARP = T / 32;                   // compute warps
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + NSLOT;
-  uint32_t* prog = reinterpret_cast<uint32_t*>(empty + NSLOT);  // [NI] stages completed
-  V* slots = reinterpret_cast<V*>(smem + 256);                    // [NSLOT][4][WIN]
-  V* negwin = slots + NSLOT * 4 * WIN;                             // [WIN] of NEG: windows below the frontier
-
-  const int G = geo.G, NC = geo.NC;
-  const int q = (int)cluster_rank();
-  const int first = (int)(blockIdx.x / G) * NI;
-  const int ni = min(NI, geo.n_items - first);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int B = NC * CH;
-  const int j0 = q * B;
-  const int64_t span = (int64_t)PAD + (int64_t)G * B + LINE;
-  const V NEG = VT<MODE>::neg();
-  const V ZERO = V(0);
-  int64_t inst[NI], lo[NI], row_words[NI];
-  int L[NI], ncol[NI];
-  V* base[NI];
-  int maxL = 0;
-#pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const DpWork wk = a.work[first + min(i, ni - 1)];
-    inst[i] = wk.inst;
-    lo[i] = a.layer_off[wk.inst];
-    L[i] = i < ni ? (int)(a.layer_off[wk.inst + 1] - lo[i]) : 0;
-    ncol[i] = (int)(a.info[wk.inst].w_eff + 1);
-    base[i] = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][PAD + G*B + LINE]
-    row_words[i] = wk.bp_row_words;
-    maxL = max(maxL, L[i]);
-  }
-  auto row = [&](int i, int buf, int rs) { return base[i] + (int64_t)(buf * 2 + rs) * span + PAD; };
-
-  for (int i = 0; i < ni; ++i) {
-    const bool sac = a.sac[inst[i]] != 0;
-    for (int buf = 0; buf < NBUF; ++buf) {
-      V* Cb = row(i, buf, 0);
-      V* Sb = row(i, buf, 1);
-      if (q == 0)
-        for (int x = tid - PAD; x < 0; x += blockDim.x) Cb[x] = Sb[x] = NEG;  // never rewritten
-      if (q == G - 1)
-        for (int x = G * B + tid; x < G * B + LINE; x += blockDim.x) Cb[x] = Sb[x] = NEG;
-      if (buf == 0)
-        for (int j = j0 + tid; j < j0 + B; j += blockDim.x) {
-          const bool valid = j < ncol[i];
-          Cb[j] = (valid && sac) ? ZERO : NEG;
-          Sb[j] = (valid && !sac) ? ZERO : NEG;
-          if (a.tab_c && valid) {
-            a.tab_c[j] = sac ? 0.0 : -INFINITY;
-            a.tab_s[j] = sac ? -INFINITY : 0.0;
-          }
-        }
-    }
-  }
-  for (int x = tid; x < WIN; x += blockDim.x) negwin[x] = NEG;
-  if (tid == 0) {
-    for (int b = 0; b < NSLOT; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], NWARP);
-    }
-    for (int i = 0; i < NI; ++i) prog[i] = 0;
-    fence_mbar_init();
-  }
-  fence_proxy_async_global();
-  __threadfence();
-  cluster_barrier();  // rows initialised, barriers and counters live in every CTA
-
-  if (warp == NWARP) {
-    // ---------------- producer warp ----------------
-    // lane o watches CTA o's progress counters (G <= 16 <= 32 lanes)
-    const uint32_t my_prog = lane < G ? cluster_addr(smem_addr(prog), (uint32_t)lane) : 0u;
-    uint32_t u = 0;
-    for (int k = 0; k < maxL; ++k) {  // stage k of each instance in turn
-      for (int i = 0; i < ni; ++i) {
-        if (k >= L[i]) continue;
-        const StageShift sh = a.shifts[lo[i] + k];  // issued before the wait: latency overlaps it
-        const int2 rch = a.reach ? a.reach[lo[i] + k] : make_int2(0, 0);  // first reachable columns of C_k, S_k
-        // every CTA <= q finished stage k (row k ready); WAR on the buffer this
-        // stage overwrites: with 3 buffers every CTA finished k-1, with 2 every CTA k
-        const uint32_t need =
-            lane < G ? (uint32_t)(lane <= q || NBUF == 2 ? k : max(k - 1, 0)) : 0u;
-        while (!(geo.diag & 1) &&
-               !__all_sync(0xffffffffu, lane >= G || ld_cluster_relaxed(my_prog + 4u * i) >= need)) {
-        }
-        if (lane == 0) {
-          fence_acq_rel_cluster();
-          fence_proxy_async_global();
-          const V* Cc = row(i, k % NBUF, 0);
-          const V* Sc = row(i, k % NBUF, 1);
-          const V* src[4] = {Cc, Sc, Sc, Cc};
-          const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
-          for (int c = 0; c < NC; ++c, ++u) {
-            const int slot = (int)(u % NSLOT);
-            mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
-            const int c0 = j0 + c * CH, ctop = c0 + CH;
-            if (geo.diag & 2) {
-              mbar_arrive(&full[slot]);
-              continue;
-            }
-            // a window entirely below its row's reachable frontier is all NEG:
-            // no copy, the compute warps read the NEG window instead
-            int start[4];
-            uint32_t ncopy = 0;
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              start[w] = c0 - min(shf[w], ctop);
-              ncopy += start[w] + CH > ((w == 0 || w == 3) ? rch.x : rch.y) ? 1u : 0u;
-            }
-            mbar_expect_tx(&full[slot], ncopy * WIN * sizeof(V));
-#pragma unroll
-            for (int w = 0; w < 4; ++w)
-              if (start[w] + CH > ((w == 0 || w == 3) ? rch.x : rch.y))
-                bulk_g2s(slots + (slot * 4 + w) * WIN, src[w] + (start[w] & ~(AL - 1)), WIN * sizeof(V),
-                         &full[slot]);
-          }
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    // ---------------- compute warps ----------------
-    const uint64_t pol = evict_first_policy();
-    // the rows are re-read next stage: keep them in L2 ahead of the streamed
-    // back-pointers (geo.row_hint 0: normal, 1: evict_last)
-    const uint64_t rpol = evict_last_policy();
-    uint32_t u = 0;
-    for (int k = 0; k < maxL; ++k) {
-      for (int i = 0; i < ni; ++i) {
-        if (k >= L[i]) continue;
-        const StageShift sh = a.shifts[lo[i] + k];
-        const int2 rch = a.reach ? a.reach[lo[i] + k] : make_int2(0, 0);
-        // every cell of row k+1 below both frontiers is unreachable
-        const int64_t next_front = a.reach ? min(min((int64_t)rch.x + sh.i, (int64_t)rch.y + sh.id),
-                                                 min((int64_t)rch.y + sh.s, (int64_t)rch.x + sh.su))
-                                           : 0;
-        const int64_t rbits = a.rv[lo[i] + k];
-        const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
-        V* Cn = row(i, (k + 1) % NBUF, 0);
-        V* Sn = row(i, (k + 1) % NBUF, 1);
-        const DpWork wk = a.work[first + i];
-        uint32_t* bprow = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off) + (int64_t)k * row_words[i] +
-                          warp * bp_words(MODE);
-        for (int c = 0; c < NC; ++c, ++u) {
-          const int slot = (int)(u % NSLOT);
-          const int c0 = j0 + c * CH, ctop = c0 + CH;
-          const V* ws = slots + slot * 4 * WIN + tid;
-          const int sa = c0 - min(sh.i, ctop), sb = c0 - min(sh.id, ctop);
-          const int sc = c0 - min(sh.s, ctop), sd = c0 - min(sh.su, ctop);
-          // windows below the reachable frontier were not copied: read NEG
-          const V* pca = (sa + CH > rch.x ? ws + 0 * WIN : negwin + tid) + (sa & (AL - 1));
-          const V* pcb = (sb + CH > rch.y ? ws + 1 * WIN : negwin + tid) + (sb & (AL - 1));
-          const V* psa = (sc + CH > rch.y ? ws + 2 * WIN : negwin + tid) + (sc & (AL - 1));
-          const V* psb = (sd + CH > rch.x ? ws + 3 * WIN : negwin + tid) + (sd & (AL - 1));
-          uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
-          mbar_wait(&full[slot], (u / NSLOT) & 1);
-          V cn[E], sn[E];
-          if ((int64_t)ctop <= next_front && !a.tab_c) {  // whole chunk unreachable: NEG, no back-pointers
-#pragma unroll
-            for (int e = 0; e < E; ++e) cn[e] = sn[e] = NEG;
-          } else {
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              const int j = c0 + e * T + tid;
-              const CellFlags f = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk,
-                                                       j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su,
-                                                       cn[e], sn[e]);
-              emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f, pol);
-            }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done reading the slot
-          V* qc = Cn + c0 + tid;
-          V* qs = Sn + c0 + tid;
-          if (geo.row_hint) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              st_hint(qc + e * T, cn[e], rpol);
-              st_hint(qs + e * T, sn[e], rpol);
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              qc[e * T] = cn[e];
-              qs[e * T] = sn[e];
-            }
-          }
-          if (a.tab_c) {
-            const int nc = ncol[i];
-            const double g = a.info[inst[i]].scale;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              const int j = c0 + e * T + tid;
-              if (j < nc) {
-                a.tab_c[(int64_t)(k + 1) * nc + j] = to_f64(cn[e], g);
-                a.tab_s[(int64_t)(k + 1) * nc + j] = to_f64(sn[e], g);
-              }
-            }
-          }
-        }
-        // publish row k+1 of this CTA's block of instance i
-        named_barrier(1, T);
-        if (tid == 0) {
-          fence_acq_rel_cluster();
-          fence_proxy_async_global();
-          st_cluster_release(prog + i, (uint32_t)(k + 1));
-        }
-      }
-    }
-  }
-  __syncthreads();
-  cluster_barrier();  // no CTA leaves while others may still read its counters
-  for (int i = 0; i < ni; ++i) {
-    const int nc = ncol[i];
-    if (tid == 0 && nc - 1 >= j0 && nc - 1 < j0 + B) {
-      const double g = a.info[inst[i]].scale;
-      a.info[inst[i]].end_c = to_f64(row(i, L[i] % NBUF, 0)[nc - 1], g);
-      a.info[inst[i]].end_s = to_f64(row(i, L[i] % NBUF, 1)[nc - 1], g);
-    }
-  }
-  __syncthreads();
-  // the rows are dead: drop their L2 lines instead of writing them back
-  for (int i = 0; i < ni; ++i)
-    for (int buf = 0; buf < NBUF; ++buf)
-      for (int rs = 0; rs < 2; ++rs)
-        for (int x = tid * LINE; x < B; x += blockDim.x * LINE) discard_l2(row(i, buf, rs) + j0 + x);
-}
-
-// ---------------------------------------------------------------------------
-// K2 own-block variant (int32 domain; EXPERIMENTAL, forced only with
-// SPLITPLAN_DP_VARIANT=own): a cluster of G CTAs per instance, CTA q owning
-// columns [q*B, (q+1)*B) of both rows in its own shared memory, updated in
-// place top-down like the single-CTA kernel.  Only what other CTAs need goes
-// through L2:
-//  * a predecessor window (C or S row shifted by i, i+d, s or s+u) that lies
-//    entirely in the own block is read straight from shared memory; windows
-//    reaching left of the block are bulk-copied from the previous row's global
-//    copy into per-window ring slots (full/empty mbarriers), and a window
-//    straddling the block edge gets its own part patched into the slot;
-//  * column p of the new row is stored to the global copy only if a CTA to
-//    the right reads it next stage: p >= (q+1)*B - max(next stage's shifts).
-// At cfg2 widths that removes ~3/4 of the window reads and ~1/3 of the row
-// writes of the streaming kernel.  Ordering: the producer waits, per window,
-// until the CTAs owning its remote columns published the previous row (RAW),
-// and before the compute warps overwrite a global row buffer it checks that
-// every CTA to the right has finished the stage that read it (WAR, NBUF
-// buffers); a publisher warp releases the CTA's progress at cluster scope off
-// the compute critical path, so stages pipeline as a wavefront.
-// Measured on B200 (profiles/r01/own_experiment): 2.3e11 cells/s at cfg2
-// against 4.7e11 for the streaming kernel, and 4.6e11 vs 1.0e12 for the
-// single-CTA kernel at W = 1e4: the L2 traffic it saves is not what bounds
-// the streaming kernel (removing every window copy there gains only 35 %),
-// while its per-chunk bookkeeping doubles the instructions per cell and one
-// CTA per SM halves the warps that hide the per-chunk barrier.  Kept with
-// parity tests as a recorded experiment, not selected automatically.
-struct OwnGeom {
-  int G;        // CTAs per instance (cluster size)
-  int NC;       // chunks per CTA
-  int n_items;  // instances of the launch
-  int pad;
-};
-
-__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
-}
-
-// kind of a predecessor window [start, start + CH) for CTA q owning columns from j0:
-// 0 = own (shared memory; for q == 0 also the NEG pad below column 0),
-// 1 = remote (slot), 2 = straddles the block edge (remote part from the slot)
-template <int CH>
-__device__ __forceinline__ int own_win_kind(int q, int j0, int start) {
-  if (q == 0 || start >= j0) return 0;
-  return start + CH <= j0 ? 1 : 2;
-}
-
-template <int MODE, int T, int E, int NSW, int NBUF>
-__global__ void __launch_bounds__(T + 64, (T <= 256 ? 2 : 1)) dp_own_kernel(DpArgs a, OwnGeom geo) {
-  using V = typename VT<MODE>::T;
-  constexpr int CH = T * E;
-  constexpr int AL = 16 / (int)sizeof(V);
-  constexpr int WIN = CH + AL;
-  constexpr int PAD = stream_pad<V, CH>();
-  constexpr int LINE = 128 / (int)sizeof(V);
-  constexpr int NWARP = T / 32;
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [NSW]
-  uint64_t* empty = full + NSW;                         // [NSW]
-  uint32_t* prog = reinterpret_cast<uint32_t*>(empty + NSW);  // stages published
-  uint32_t* war = prog + 1;                                   // stages cleared for global stores
-  uint32_t* done = prog + 2;                                  // stages finished by the compute warps
-
-  const int G = geo.G, NC = geo.NC;
-  const int B = NC * CH;
-  const int q = (int)cluster_rank();
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const DpWork wk = a.work[blockIdx.x / G];
-  const int64_t inst = wk.inst;
-  const int64_t lo = a.layer_off[inst];
-  const int L = (int)(a.layer_off[inst + 1] - lo);
-  const int ncol = (int)(a.info[inst].w_eff + 1);
-  const bool sac = a.sac[inst] != 0;
-  const int j0 = q * B;
-  const int64_t span = (int64_t)PAD + (int64_t)G * B + LINE;
-  V* const gbase = reinterpret_cast<V*>(a.rows + wk.row_off);  // [buf][C|S][PAD + G*B + LINE]
-  auto grow = [&](int buf, int rs) { return gbase + (int64_t)(buf * 2 + rs) * span + PAD; };
-  V* const ownC = reinterpret_cast<V*>(smem + 256) + CH;  // [CH pad | B own columns]
-  V* const ownS = ownC + B + CH;
-  V* const slots = ownS + B;  // [NSW][WIN]
-  const V NEG = VT<MODE>::neg();
-  const V ZERO = V(0);
-
-  // row 0: own block in shared memory and in global buffer 0; NEG pads
-  for (int x = tid - CH; x < B; x += blockDim.x) {
-    const int j = j0 + x;
-    const bool valid = x >= 0 && j < ncol;
-    const V c = (valid && sac) ? ZERO : NEG, s = (valid && !sac) ? ZERO : NEG;
-    ownC[x] = c;
-    ownS[x] = s;
-    if (x >= 0) {
-      grow(0, 0)[j] = c;
-      grow(0, 1)[j] = s;
-    }
-  }
-  for (int buf = 0; buf < NBUF; ++buf) {
-    if (q == 0)
-      for (int x = tid - PAD; x < 0; x += blockDim.x) grow(buf, 0)[x] = grow(buf, 1)[x] = NEG;
-    if (q == G - 1)
-      for (int x = G * B + tid; x < G * B + LINE; x += blockDim.x) grow(buf, 0)[x] = grow(buf, 1)[x] = NEG;
-  }
-  if (tid == 0) {
-    for (int b = 0; b < NSW; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], NWARP);
-    }
-    *prog = 0;
-    *war = 0;
-    *done = 0;
-    fence_mbar_init();
-  }
-  fence_proxy_async_global();
-  __threadfence();
-  cluster_barrier();
-
-  if (warp == NWARP) {
-    // ---------------- producer warp: remote windows + WAR clearance ----------------
-    const uint32_t peer = lane < G ? cluster_addr(smem_addr(prog), (uint32_t)lane) : 0u;
-    uint32_t u = 0;
-    StageShift sh = a.shifts[lo];
-    for (int k = 0; k < L; ++k) {
-      const StageShift shn = a.shifts[lo + min(k + 1, L - 1)];  // prefetch
-      // WAR: the compute warps' stage-k stores go to buffer (k+1) % NBUF, last
-      // read (stage k+1-NBUF) by the CTAs to the right
-      const int war_need = k + 2 - NBUF;
-      if (war_need > 0) {
-        while (!__all_sync(0xffffffffu, lane <= q || lane >= G || ld_cluster_relaxed(peer) >= (uint32_t)war_need)) {
-        }
-        if (lane == 0) fence_acq_rel_cluster();
-      }
-      if (lane == 0) st_release_cta(war, (uint32_t)(k + 1));
-      uint32_t ready = 0;  // lanes (CTAs) known to have published row k
-      const V* Cr = grow(k % NBUF, 0);
-      const V* Sr = grow(k % NBUF, 1);
-      const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
-      for (int c = NC - 1; c >= 0; --c) {
-        const int c0 = j0 + c * CH, ctop = c0 + CH;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int start = c0 - min(shf[w], ctop);
-          if (own_win_kind<CH>(q, j0, start) == 0) continue;
-          // RAW: owners of the remote columns [max(start, 0), min(start + CH, j0))
-          const int hi_col = min(start + CH, j0) - 1;
-          const int olo = max(start, 0) / B;
-          const int ohi = hi_col >= 0 ? hi_col / B : -1;
-          const uint32_t want = (ohi >= olo) ? ((0xffffffffu >> (31 - ohi)) & (0xffffffffu << olo)) : 0u;
-          if ((ready & want) != want) {
-            do {
-              ready = __ballot_sync(0xffffffffu, lane < G && ld_cluster_relaxed(peer) >= (uint32_t)k);
-            } while ((ready & want) != want);
-            if (lane == 0) {
-              fence_acq_rel_cluster();
-              fence_proxy_async_global();
-            }
-          }
-          if (lane == 0) {
-            // the window's columns left of the block (all of it unless it
-            // straddles the edge; the compute warps fill in the own part)
-            const int sa = start & ~(AL - 1);
-            const uint32_t bytes = (uint32_t)(min(WIN, j0 - sa) * (int)sizeof(V));
-            const int slot = (int)(u % NSW);
-            mbar_wait(&empty[slot], ((u / NSW) & 1) ^ 1);
-            mbar_expect_tx(&full[slot], bytes);
-            const V* src = (w == 0 || w == 3) ? Cr : Sr;
-            bulk_g2s(slots + slot * WIN, src + sa, bytes, &full[slot]);
-          }
-          ++u;
-          __syncwarp();
-        }
-      }
-      sh = shn;
-    }
-  } else if (warp == NWARP + 1) {
-    // ---------------- publisher warp ----------------
-    // publishes the latest stage the compute warps finished (their stores are
-    // ordered before `done` by their stage-end barrier); the compute warps never
-    // wait for it, and a slow release simply covers several stages at once
-    if (lane == 0) {
-      uint32_t pub = 0;
-      while (pub < (uint32_t)L) {
-        const uint32_t d = ld_acquire_cta(done);
-        if (d == pub) {
-          __nanosleep(64);
-          continue;
-        }
-        fence_acq_rel_cluster();
-        st_cluster_release(prog, d);
-        pub = d;
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---------------- compute warps ----------------
-    // Every predecessor read is an index into the shared array `sv` (so it is
-    // an LDS): own rows at ownC / ownS, ring slots at slots.
-    V* const sv = reinterpret_cast<V*>(smem);
-    const int iC = (int)(ownC - sv), iS = (int)(ownS - sv), iSl = (int)(slots - sv);
-    const uint64_t pol = evict_first_policy();
-    uint32_t* const bpw = reinterpret_cast<uint32_t*>(a.bp + wk.bp_off) + warp * bp_words(MODE);
-    const int64_t row_words = wk.bp_row_words;
-    uint32_t u = 0;
-    StageShift sh = a.shifts[lo];
-    StageShift shn = a.shifts[lo + min(1, L - 1)];
-    int64_t rbits = a.rv[lo];
-    for (int k = 0; k < L; ++k) {
-      const StageShift shn2 = a.shifts[lo + min(k + 2, L - 1)];  // prefetch
-      const int64_t rbn = a.rv[lo + min(k + 1, L - 1)];
-      const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
-      // global copy: only the columns a CTA to the right reads next stage
-      int thrC = INT_MAX, thrS = INT_MAX;
-      if (k + 1 < L && q + 1 < G) {
-        thrC = j0 + B - max(shn.i, shn.su);
-        thrS = j0 + B - max(shn.id, shn.s);
-      }
-      const int thr = min(thrC, thrS);
-      V* const gC = grow((k + 1) % NBUF, 0);
-      V* const gS = grow((k + 1) % NBUF, 1);
-      uint32_t* const bprow = bpw + (int64_t)k * row_words;
-      const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
-      const int rowi[4] = {iC - j0, iS - j0, iS - j0, iC - j0};  // own index of column p: rowi + p
-      bool war_ok = false;
-      for (int c = NC - 1; c >= 0; --c) {
-        const int c0 = j0 + c * CH, ctop = c0 + CH;
-        int base[4];
-        uint32_t used = 0, strad = 0;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int start = c0 - min(shf[w], ctop);
-          base[w] = rowi[w] + start + tid;  // own-row index of this thread's first predecessor
-          if (q > 0 && start < j0) {        // remote columns: this window has a ring slot
-            const int slot = (int)(u % NSW);
-            mbar_wait(&full[slot], (u / NSW) & 1);
-            ++u;
-            const int sa = start & ~(AL - 1);
-            const int sb = iSl + slot * WIN - sa;  // slot index of column p: sb + p
-            base[w] = sb + start + tid;
-            used |= 1u << w;
-            if (start + CH > j0) {  // straddles the block edge: copy the own part in
-              strad = 1;
-              const int ob = rowi[w];
-              for (int p = j0 + tid; p < start + CH; p += T) sv[sb + p] = sv[ob + p];
-            }
-          }
-        }
-        if (strad) named_barrier(1, T);  // patched slots visible to every compute warp
-        V cn[E], sn[E];
-        uint32_t* const bpc = bprow + (c0 >> 5) * bp_words(MODE);
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int j = c0 + e * T + tid;
-          const CellFlags f = cell_update<MODE, V>(sv[base[0] + e * T], sv[base[1] + e * T],
-                                                   sv[base[2] + e * T], sv[base[3] + e * T], rk,
-                                                   j >= sh.i, j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
-          emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f, pol);
-        }
-        // release this chunk's ring slots (the same slot sequence as above)
-        __syncwarp();
-        if (lane == 0) {
-          uint32_t v = u;
-#pragma unroll
-          for (int w = 3; w >= 0; --w)
-            if (used & (1u << w)) mbar_arrive(&empty[(int)(--v % NSW)]);
-        }
-        named_barrier(1, T);  // every read of this chunk's predecessors is done: update in place
-        const int oi = iC + (c0 - j0) + tid, os = iS + (c0 - j0) + tid;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          sv[oi + e * T] = cn[e];
-          sv[os + e * T] = sn[e];
-        }
-        if (ctop > thr) {
-          if (!war_ok) {
-            while (ld_acquire_cta(war) < (uint32_t)(k + 1)) {
-            }
-            war_ok = true;
-          }
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int j = c0 + e * T + tid;
-            if (j >= thrC) gC[j] = cn[e];
-            if (j >= thrS) gS[j] = sn[e];
-          }
-        }
-      }
-      fence_proxy_async_global();  // the global row copy is read next by bulk copies
-      named_barrier(1, T);         // stage done: own rows complete, global stores ordered
-      if (tid == 0) st_release_cta(done, (uint32_t)(k + 1));
-      sh = shn;
-      shn = shn2;
-      rbits = rbn;
-    }
-  }
-  __syncthreads();
-  cluster_barrier();  // no CTA leaves while others may still poll its counters
-  if (tid == 0 && ncol - 1 >= j0 && ncol - 1 < j0 + B) {
-    const double g = a.info[inst].scale;
-    a.info[inst].end_c = to_f64(ownC[ncol - 1 - j0], g);
-    a.info[inst].end_s = to_f64(ownS[ncol - 1 - j0], g);
-  }
-  // the global rows are dead: drop their L2 lines instead of writing them back
-  for (int buf = 0; buf < NBUF; ++buf)
-    for (int rs = 0; rs < 2; ++rs)
-      for (int x = tid * LINE; x < B; x += blockDim.x * LINE) discard_l2(grow(buf, rs) + j0 + x);
-}
-
-// ---------------------------------------------------------------------------
-// K2 grid variant: ONE very large instance (L = 1e5 stages x
-// W = 1e7 columns) spread over every co-resident CTA of the GPU (cooperative
-// launch).  Same producer-warp / bulk-copy / mbarrier-ring structure as the
-// streaming kernel, but the per-CTA progress counters live in global memory
-// and each producer waits only on the CTAs that own its windows: the owners
-// of columns [j0 - max_shift - 16 B, j0 + B) for the rows it reads (RAW) and
-// the CTAs that read its block two stages earlier (WAR on the triple-
-// buffered rows).  With small per-stage shifts that is just the two
-// neighbours, so the GPU runs as a wavefront with no grid-wide barrier.
-// A launch advances a range of stages [k_begin, k_begin + k_count) from an
-// initial row (the origin row or a checkpoint) and can write the final row
-// (a checkpoint) and the range's back-pointers; the host chains launches
-// into checkpoint / recompute passes when the full back-pointer table does
-// not fit in memory.
-
-constexpr int kMaxParts = 8;
-
-// One huge instance over the whole GPU (or, partitioned, over several GPUs).
-// The capacity axis can be split into `nparts` partitions of Gp CTAs each
-// (one per device in a multi-GPU run): partition p owns global columns
-// [p*Wp, (p+1)*Wp), Wp = Gp*B, keeps its own triple-buffered rows, and
-// mirrors the left neighbour's last `halo` columns of every row in front of
-// its column 0 -- the halo, written by the neighbour's CTAs with plain
-// (peer) stores as they produce those columns.  Dependencies are computed
-// in the global CTA index space, so the protocol is the same whether the
-// partitions are launched together (one device, emulating several) or one
-// per device.
-struct GridArgs {
-  const StageShift* shifts;  // stage records of the instance (index = stage)
-  const int64_t* rv;         // stage values in the value domain
-  const int2* reach;         // per stage: first reachable global column of the C / S row it reads
-  int k_begin, k_count;      // stage range of this launch
-  int ncol;                  // W_eff + 1
-  int G, NC;                 // CTAs per partition, chunks per CTA
-  int sac;
-  const void* init_c;        // row k_begin, ncol values each, or null: origin row
-  const void* init_s;
-  void* out_c;               // row k_begin + k_count, or null
-  void* out_s;
-  uint32_t* bp;              // back-pointers of the range's stages, or null
-  int64_t bp_row_words;
-  uint32_t* progs[kMaxParts];  // per partition: [G] stages completed + 1 (zeroed)
-  int nparts;                // partitions of the capacity axis
-  int part_base;             // first partition of this launch
-  int launch_parts;          // partitions of this launch (grid = launch_parts x G)
-  int sys;                   // partitions on different devices: system-scope ordering
-  int halo;                  // mirrored left-neighbour columns (multiple of 128 B)
-  uint8_t* rows[kMaxParts];  // per partition: [3][C|S][NEG pad | halo | Wp | line]
-};
-
-__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ int max_shift(const StageShift& sh) {
-  return max(max(sh.i, sh.id), max(sh.s, sh.su));
-}
-
-template <int MODE, int T, int E, int NSLOT>
-__global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
-  using V = typename VT<MODE>::T;
-  constexpr int CH = T * E;
-  constexpr int AL = 16 / (int)sizeof(V);
-  constexpr int WIN = CH + AL;
-  constexpr int PAD = stream_pad<V, CH>();  // NEG area in front of the halo
-  constexpr int LINE = 128 / (int)sizeof(V);
-  constexpr int NWARP = T / 32;
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + NSLOT;
-  V* slots = reinterpret_cast<V*>(smem + 256);
-  V* negwin = slots + NSLOT * 4 * WIN;  // [WIN] of NEG: windows below the reachable frontier
-
-  const int G = a.G, NC = a.NC;
-  const int part = a.part_base + (int)blockIdx.x / G;
-  const int q = (int)blockIdx.x % G;
-  const int GT = a.nparts * G;  // CTAs over the whole capacity axis
-  const int gq = part * G + q;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int B = NC * CH;
-  const int Wp = G * B;
-  const int p0 = part * Wp;      // global column of this partition's local column 0
-  const int j0 = q * B;          // local
-  const int j0g = p0 + j0;       // global
-  const int ncol = a.ncol;
-  const int H = a.halo;
-  const int64_t span = (int64_t)PAD + H + Wp + LINE;
-  const V NEG = VT<MODE>::neg();
-  const V ZERO = V(0);
-  auto row_of = [&](int p, int buf, int rs) {
-    return reinterpret_cast<V*>(a.rows[p]) + (int64_t)(buf * 2 + rs) * span + PAD + H;
-  };
-  auto row = [&](int buf, int rs) { return row_of(part, buf, rs); };
-  auto owner = [&](int x) { return min(GT - 1, max(0, x) / B); };  // global CTA of global column x
-  // progress counter of global CTA o (in its partition's -- possibly a peer device's -- memory)
-  auto prog_of = [&](int o) { return a.progs[o / G] + (o % G); };
-  auto publish = [&](uint32_t v) {
-    if (a.sys) {
-      __threadfence_system();
-      fence_proxy_async_global();
-      st_release_sys(prog_of(gq), v);
-    } else {
-      __threadfence();
-      fence_proxy_async_global();
-      st_release_gpu(prog_of(gq), v);
-    }
-  };
-  const V* ic = reinterpret_cast<const V*>(a.init_c);
-  const V* is = reinterpret_cast<const V*>(a.init_s);
-  auto init_at = [&](int x, V& c, V& sv) {  // row k_begin at global column x
-    const bool valid = x >= 0 && x < ncol;
-    if (ic) {
-      c = valid ? ic[x] : NEG;
-      sv = valid ? is[x] : NEG;
-    } else {
-      c = (valid && a.sac) ? ZERO : NEG;
-      sv = (valid && !a.sac) ? ZERO : NEG;
-    }
-  };
-
-  for (int buf = 0; buf < kRowBufs; ++buf) {
-    V* Cb = row(buf, 0);
-    V* Sb = row(buf, 1);
-    if (q == 0) {
-      for (int x = tid - PAD - H; x < -H; x += blockDim.x) Cb[x] = Sb[x] = NEG;  // NEG area
-      // halo of buffer 0: row k_begin of the neighbour's last columns (all NEG
-      // in partition 0).  Buffers 1 and 2 belong to the neighbour's CTAs, which
-      // write them before any read (RAW) -- never touch them here.
-      if (buf == 0)
-        for (int x = tid - H; x < 0; x += blockDim.x) {
-          V c = NEG, sv = NEG;
-          if (part > 0) init_at(p0 + x, c, sv);
-          Cb[x] = c;
-          Sb[x] = sv;
-        }
-      else if (part == 0)
-        for (int x = tid - H; x < 0; x += blockDim.x) Cb[x] = Sb[x] = NEG;
-    }
-    if (q == G - 1)
-      for (int x = Wp + tid; x < Wp + LINE; x += blockDim.x) Cb[x] = Sb[x] = NEG;
-    if (buf == 0)
-      for (int j = j0 + tid; j < j0 + B; j += blockDim.x) init_at(p0 + j, Cb[j], Sb[j]);
-  }
-  for (int x = tid; x < WIN; x += blockDim.x) negwin[x] = NEG;
-  if (tid == 0) {
-    for (int b = 0; b < NSLOT; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], NWARP);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) publish(1u);  // rows initialised (counter = completed stages + 1)
-
-  if (warp == NWARP) {
-    // ---------------- producer warp ----------------
-    uint32_t u = 0;
-    for (int t = 0; t < a.k_count; ++t) {
-      const int k = a.k_begin + t;
-      const StageShift sh = a.shifts[k];
-      // RAW: owners of the windows read this stage (row t complete => counter >= t + 1)
-      const int lo_o = owner(j0g - max_shift(sh) - AL);
-      // WAR: CTAs that read this block's target buffers (own rows and the
-      // right neighbour's halo copy) two stages ago
-      int hi_o = gq;
-      if (t >= 2) hi_o = owner(j0g + B - 1 + max_shift(a.shifts[k - 2]) + CH + AL);
-      for (int o0 = lo_o; o0 <= hi_o; o0 += 32) {
-        const int o = o0 + lane;
-        const uint32_t need = o <= gq ? (uint32_t)(t + 1) : (uint32_t)max(t - 1, 0) + 1u;
-        // (a watchdog turns a lost partition -- e.g. launches that were not
-        // co-scheduled -- into a launch failure instead of a hang)
-        const long long t0 = clock64();
-        for (uint32_t it = 1;; ++it) {
-          const bool ok = o > hi_o || (a.sys ? ld_acquire_sys(prog_of(o)) : ld_acquire_gpu(prog_of(o))) >= need;
-          if (__all_sync(0xffffffffu, ok)) break;
-          if ((it & 1023u) == 0 && clock64() - t0 > (30ll << 30)) __trap();
-        }
-      }
-      if (lane == 0) {
-        fence_proxy_async_global();
-        const V* Cc = row(t % kRowBufs, 0);
-        const V* Sc = row(t % kRowBufs, 1);
-        const V* src[4] = {Cc, Sc, Sc, Cc};
-        const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
-        const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
-        const int mrow[4] = {rch.x, rch.y, rch.y, rch.x};
-        for (int c = 0; c < NC; ++c, ++u) {
-          const int slot = (int)(u % NSLOT);
-          mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
-          const int c0g = j0g + c * CH, ctop = c0g + CH;
-          uint32_t ncopy = 0;
-#pragma unroll
-          for (int w = 0; w < 4; ++w) ncopy += c0g - min(shf[w], ctop) + CH > mrow[w] ? 1u : 0u;
-          mbar_expect_tx(&full[slot], ncopy * WIN * sizeof(V));
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const int start = c0g - min(shf[w], ctop);
-            if (start + CH <= mrow[w]) continue;  // below the reachable frontier: all NEG, no copy
-            // Partition 0 keeps NEG in front of column 0 (halo + NEG area), so
-            // partially negative windows read it in place.  In later
-            // partitions start < 0 only when the shift was clamped (every cell
-            // of the window unreachable): read the NEG area.
-            const int local = (start < 0 && part > 0) ? -H - PAD : (start & ~(AL - 1)) - p0;
-            bulk_g2s(slots + (slot * 4 + w) * WIN, src[w] + local, WIN * sizeof(V), &full[slot]);
-          }
-        }
-      }
-      __syncwarp();
-    }
-  } else {
-    // ---------------- compute warps ----------------
-    const uint64_t pol = evict_first_policy();
-    uint32_t u = 0;
-    StageShift sh_next = a.shifts[a.k_begin];
-    int64_t rbits_next = a.rv[a.k_begin];
-    // global columns mirrored into the right neighbour's halo
-    const int halo_lo = part + 1 < a.nparts ? p0 + Wp - H : INT_MAX;
-    for (int t = 0; t < a.k_count; ++t) {
-      const StageShift sh = sh_next;
-      const int64_t rbits = rbits_next;
-      if (t + 1 < a.k_count) {
-        sh_next = a.shifts[a.k_begin + t + 1];
-        rbits_next = a.rv[a.k_begin + t + 1];
-      }
-      const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
-      V* Cn = row((t + 1) % kRowBufs, 0);
-      V* Sn = row((t + 1) % kRowBufs, 1);
-      uint32_t* bprow = a.bp ? a.bp + (int64_t)t * a.bp_row_words + warp * bp_words(MODE) : nullptr;
-      const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
-      // every cell of row t+1 below both frontiers is unreachable
-      const int64_t next_front = a.reach ? min(min((int64_t)rch.x + sh.i, (int64_t)rch.y + sh.id),
-                                               min((int64_t)rch.y + sh.s, (int64_t)rch.x + sh.su))
-                                         : 0;
-      for (int c = 0; c < NC; ++c, ++u) {
-        const int slot = (int)(u % NSLOT);
-        const int c0 = j0 + c * CH;       // local
-        const int c0g = p0 + c0, ctop = c0g + CH;
-        const int sa = c0g - min(sh.i, ctop), sb = c0g - min(sh.id, ctop);
-        const int sc = c0g - min(sh.s, ctop), sd = c0g - min(sh.su, ctop);
-        const V* ws = slots + slot * 4 * WIN + tid;
-        const V* pca = (sa + CH > rch.x ? ws + 0 * WIN : negwin + tid) + (sa & (AL - 1));
-        const V* pcb = (sb + CH > rch.y ? ws + 1 * WIN : negwin + tid) + (sb & (AL - 1));
-        const V* psa = (sc + CH > rch.y ? ws + 2 * WIN : negwin + tid) + (sc & (AL - 1));
-        const V* psb = (sd + CH > rch.x ? ws + 3 * WIN : negwin + tid) + (sd & (AL - 1));
-        mbar_wait(&full[slot], (u / NSLOT) & 1);
-        V cn[E], sn[E];
-        CellFlags f[E];
-        const bool dead = (int64_t)ctop <= next_front;  // whole chunk unreachable: NEG, no back-pointers
-        if (dead) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) cn[e] = sn[e] = NEG;
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int j = c0g + e * T + tid;
-            f[e] = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk, j >= sh.i,
-                                        j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        if (bprow && !dead) {
-          uint32_t* bpc = bprow + (c0g >> 5) * bp_words(MODE);
-#pragma unroll
-          for (int e = 0; e < E; ++e) emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f[e], pol);
-        }
-        V* qc = Cn + c0 + tid;
-        V* qs = Sn + c0 + tid;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          qc[e * T] = cn[e];
-          qs[e * T] = sn[e];
-        }
-        if (ctop > halo_lo) {  // the right neighbour mirrors these columns
-          V* hc = row_of(part + 1, (t + 1) % kRowBufs, 0) - (p0 + Wp);
-          V* hs = row_of(part + 1, (t + 1) % kRowBufs, 1) - (p0 + Wp);
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int j = c0g + e * T + tid;
-            if (j >= halo_lo) {
-              hc[j] = cn[e];
-              hs[j] = sn[e];
-            }
-          }
-        }
-      }
-      named_barrier(1, T);
-      if (tid == 0) publish((uint32_t)(t + 2));
-    }
-    // the range's final row (this CTA's own block: its own writes)
-    if (a.out_c) {
-      named_barrier(1, T);
-      V* oc = reinterpret_cast<V*>(a.out_c);
-      V* os = reinterpret_cast<V*>(a.out_s);
-      const V* Cf = row(a.k_count % kRowBufs, 0);
-      const V* Sf = row(a.k_count % kRowBufs, 1);
-      for (int j = j0 + tid; j < j0 + B && p0 + j < ncol; j += T) {
-        oc[p0 + j] = Cf[j];
-        os[p0 + j] = Sf[j];
-      }
-    }
-  }
-}
-
-// End of the forward pass of a grid-solved instance: the end side from the
-// final row's last cell (planner.py:190-200), or the infeasible policy.
-// state = {j, client side, infeasible}.
-// ---------------------------------------------------------------------------
-// K2 grid variant with ONE row buffer (single partition, every stage's
-// shifts <= the halo width): the rows of a 1e7-column instance are 80 MB
-// instead of 240 MB with three buffers, so they stay in L2 instead of
-// streaming through HBM (profiles/r01/dp_grid_ncu_summary.json: 15.5 B/cell
-// of DRAM traffic with three buffers).  Each CTA updates its block IN PLACE,
-// chunks top-down: every predecessor window of chunk c lies below the top of
-// chunk c (reads go left), so the chunks above c that already hold the new
-// row are never read again this stage, and window copies already sit in
-// shared-memory slots before chunk c stores over them.  Nobody else reads the
-// main buffer: the right neighbour takes this block's last `hw` columns from
-// a small per-CTA halo buffer (3 stage slots) written alongside the row.
-// Producer waits per stage: own and left neighbour finished the previous
-// stage (RAW), right neighbour finished the stage two back (WAR on the halo
-// slot this stage overwrites).
-struct GridInplaceArgs {
-  const StageShift* shifts;
-  const int64_t* rv;
-  const int2* reach;
-  int k_begin, k_count;
-  int ncol, G, NC, sac, hw;  // hw: halo columns (multiple of 128 B, <= B)
-  const void* init_c;
-  const void* init_s;
-  void* out_c;
-  void* out_s;
-  uint32_t* bp;
-  int64_t bp_row_words;
-  uint32_t* prog;  // [G] completed stages + 1 (zeroed)
-  uint8_t* rows;   // [C|S][PAD | G*B | line]
-  uint8_t* halo;   // [G][3][C|S][hw]
-  int row_hint;    // 1: row stores with an L2 evict_last policy (SPLITPLAN_ROW_EVICT_LAST)
-};
-
-template <int MODE, int T, int E, int NSLOT>
-__global__ void __launch_bounds__(T + 32, 2) dp_grid_inplace_kernel(GridInplaceArgs a) {
-  using V = typename VT<MODE>::T;
-  constexpr int CH = T * E;
-  constexpr int AL = 16 / (int)sizeof(V);
-  constexpr int WIN = CH + AL;
-  constexpr int PAD = stream_pad<V, CH>();
-  constexpr int LINE = 128 / (int)sizeof(V);
-  constexpr int NWARP = T / 32;
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + NSLOT;
-  V* slots = reinterpret_cast<V*>(smem + 256);
-  V* negwin = slots + NSLOT * 4 * WIN;  // [WIN] of NEG: windows below the reachable frontier
-
-  const int G = a.G, NC = a.NC;
-  const int q = (int)blockIdx.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int B = NC * CH;
-  const int Wt = G * B;
-  const int j0 = q * B;
-  const int ncol = a.ncol, hw = a.hw;
-  const int64_t span = (int64_t)PAD + Wt + LINE;
-  const V NEG = VT<MODE>::neg();
-  const V ZERO = V(0);
-  V* const Cm = reinterpret_cast<V*>(a.rows) + PAD;          // C row, column 0
-  V* const Sm = reinterpret_cast<V*>(a.rows) + span + PAD;   // S row, column 0
-  // halo of CTA o, stage slot t % 3: columns [o*B + B - hw, o*B + B) of row t
-  auto halo = [&](int o, int slot, int rs) {
-    return reinterpret_cast<V*>(a.halo) + ((int64_t)(o * 3 + slot) * 2 + rs) * hw;
-  };
-  const V* ic = reinterpret_cast<const V*>(a.init_c);
-  const V* is = reinterpret_cast<const V*>(a.init_s);
-
-  // row k_begin in the main buffer, its top hw columns in halo slot 0, NEG pads
-  for (int x = j0 + tid; x < j0 + B; x += blockDim.x) {
-    const bool valid = x < ncol;
-    V c, s;
-    if (ic) {
-      c = valid ? ic[x] : NEG;
-      s = valid ? is[x] : NEG;
-    } else {
-      c = (valid && a.sac) ? ZERO : NEG;
-      s = (valid && !a.sac) ? ZERO : NEG;
-    }
-    Cm[x] = c;
-    Sm[x] = s;
-    if (x >= j0 + B - hw) {
-      halo(q, 0, 0)[x - (j0 + B - hw)] = c;
-      halo(q, 0, 1)[x - (j0 + B - hw)] = s;
-    }
-  }
-  if (q == 0)
-    for (int x = tid - PAD; x < 0; x += blockDim.x) Cm[x] = Sm[x] = NEG;
-  if (q == G - 1)
-    for (int x = Wt + tid; x < Wt + LINE; x += blockDim.x) Cm[x] = Sm[x] = NEG;
-  for (int x = tid; x < WIN; x += blockDim.x) negwin[x] = NEG;
-  if (tid == 0) {
-    for (int b = 0; b < NSLOT; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], NWARP);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    fence_proxy_async_global();
-    st_release_gpu(&a.prog[q], 1u);
-  }
-
-  if (warp == NWARP) {
-    // ---------------- producer warp ----------------
-    uint32_t u = 0;
-    for (int t = 0; t < a.k_count; ++t) {
-      const StageShift sh = a.shifts[a.k_begin + t];
-      // lane 0: own block (row t complete), lane 1: left neighbour (its halo
-      // of row t), lane 2: right neighbour (finished stage t - 2: halo slot reuse)
-      const int o = lane == 0 ? q : (lane == 1 ? q - 1 : q + 1);
-      const bool watch = lane < 3 && o >= 0 && o < G;
-      const uint32_t need = lane < 2 ? (uint32_t)(t + 1) : (uint32_t)max(t - 1, 0) + 1u;
-      const long long t0 = clock64();
-      for (uint32_t it = 1;; ++it) {
-        if (__all_sync(0xffffffffu, !watch || ld_acquire_gpu(&a.prog[o]) >= need)) break;
-        if ((it & 1023u) == 0 && clock64() - t0 > (30ll << 30)) __trap();
-      }
-      if (lane == 0) {
-        fence_proxy_async_global();
-        const V* hc = q > 0 ? halo(q - 1, t % 3, 0) - (j0 - hw) : nullptr;  // index by global column
-        const V* hs = q > 0 ? halo(q - 1, t % 3, 1) - (j0 - hw) : nullptr;
-        const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
-        const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
-        const int mrow[4] = {rch.x, rch.y, rch.y, rch.x};
-        for (int c = NC - 1; c >= 0; --c, ++u) {
-          const int slot = (int)(u % NSLOT);
-          mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
-          const int c0 = j0 + c * CH, ctop = c0 + CH;
-          uint32_t ncopy = 0;
-#pragma unroll
-          for (int w = 0; w < 4; ++w) ncopy += c0 - min(shf[w], ctop) + CH > mrow[w] ? 1u : 0u;
-          mbar_expect_tx(&full[slot], ncopy * WIN * sizeof(V));
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const bool cw = w == 0 || w == 3;
-            const int start = c0 - min(shf[w], ctop);
-            if (start + CH <= mrow[w]) continue;  // below the reachable frontier: all NEG, no copy
-            V* dst = slots + (slot * 4 + w) * WIN;
-            if (q == 0 || start < 0) {  // partition start: NEG pad in front of column 0
-              const int sa = start < 0 && q > 0 ? -PAD : (start & ~(AL - 1));
-              bulk_g2s(dst, (cw ? Cm : Sm) + sa, WIN * sizeof(V), &full[slot]);
-              continue;
-            }
-            const int sa = start & ~(AL - 1);
-            const int split = min(max(j0 - sa, 0), WIN);  // values from the left halo
-            if (split > 0)
-              bulk_g2s(dst, (cw ? hc : hs) + sa, split * sizeof(V), &full[slot]);
-            if (split < WIN)
-              bulk_g2s(dst + split, (cw ? Cm : Sm) + sa + split, (WIN - split) * sizeof(V), &full[slot]);
-          }
-        }
-      }
-      __syncwarp();
-    }
-  } else {
-    // ---------------- compute warps ----------------
-    const uint64_t pol = evict_first_policy();
-    const uint64_t rpol = evict_last_policy();
-    uint32_t u = 0;
-    StageShift sh_next = a.shifts[a.k_begin];
-    int64_t rbits_next = a.rv[a.k_begin];
-    const int hlo = j0 + B - hw;  // first column mirrored into this CTA's halo
-    for (int t = 0; t < a.k_count; ++t) {
-      const StageShift sh = sh_next;
-      const int64_t rbits = rbits_next;
-      if (t + 1 < a.k_count) {
-        sh_next = a.shifts[a.k_begin + t + 1];
-        rbits_next = a.rv[a.k_begin + t + 1];
-      }
-      const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
-      V* const hc = halo(q, (t + 1) % 3, 0) - hlo;
-      V* const hs = halo(q, (t + 1) % 3, 1) - hlo;
-      uint32_t* bprow = a.bp ? a.bp + (int64_t)t * a.bp_row_words + warp * bp_words(MODE) : nullptr;
-      const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
-      const int64_t next_front = a.reach ? min(min((int64_t)rch.x + sh.i, (int64_t)rch.y + sh.id),
-                                               min((int64_t)rch.y + sh.s, (int64_t)rch.x + sh.su))
-                                         : 0;
-      for (int c = NC - 1; c >= 0; --c, ++u) {
-        const int slot = (int)(u % NSLOT);
-        const int c0 = j0 + c * CH, ctop = c0 + CH;
-        const int sa = c0 - min(sh.i, ctop), sb = c0 - min(sh.id, ctop);
-        const int sc = c0 - min(sh.s, ctop), sd = c0 - min(sh.su, ctop);
-        const V* ws = slots + slot * 4 * WIN + tid;
-        const V* pca = (sa + CH > rch.x ? ws + 0 * WIN : negwin + tid) + (sa & (AL - 1));
-        const V* pcb = (sb + CH > rch.y ? ws + 1 * WIN : negwin + tid) + (sb & (AL - 1));
-        const V* psa = (sc + CH > rch.y ? ws + 2 * WIN : negwin + tid) + (sc & (AL - 1));
-        const V* psb = (sd + CH > rch.x ? ws + 3 * WIN : negwin + tid) + (sd & (AL - 1));
-        mbar_wait(&full[slot], (u / NSLOT) & 1);
-        V cn[E], sn[E];
-        CellFlags f[E];
-        const bool dead = (int64_t)ctop <= next_front;  // whole chunk unreachable: NEG, no back-pointers
-        if (dead) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) cn[e] = sn[e] = NEG;
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int j = c0 + e * T + tid;
-            f[e] = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk, j >= sh.i,
-                                        j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        if (bprow && !dead) {
-          uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
-#pragma unroll
-          for (int e = 0; e < E; ++e) emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f[e], pol);
-        }
-        V* qc = Cm + c0 + tid;
-        V* qs = Sm + c0 + tid;
-        if (a.row_hint) {  // keep the rows ahead of the streamed back-pointers in L2
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            st_hint(qc + e * T, cn[e], rpol);
-            st_hint(qs + e * T, sn[e], rpol);
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            qc[e * T] = cn[e];
-            qs[e * T] = sn[e];
-          }
-        }
-        if (ctop > hlo) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int j = c0 + e * T + tid;
-            if (j >= hlo) {
-              hc[j] = cn[e];
-              hs[j] = sn[e];
-            }
-          }
-        }
-      }
-      named_barrier(1, T);
-      if (tid == 0) {
-        __threadfence();
-        fence_proxy_async_global();
-        st_release_gpu(&a.prog[q], (uint32_t)(t + 2));
-      }
-    }
-    if (a.out_c) {
-      named_barrier(1, T);
-      V* oc = reinterpret_cast<V*>(a.out_c);
-      V* os = reinterpret_cast<V*>(a.out_s);
-      for (int j = j0 + tid; j < j0 + B && j < ncol; j += T) {
-        oc[j] = Cm[j];
-        os[j] = Sm[j];
-      }
-    }
-  }
-}
-
-__global__ void grid_end_kernel(sp_instances in, InstInfo* info, int64_t inst, const void* last_c,
-                                const void* last_s, int64_t* state) {
-  const InstInfo inf = info[inst];
-  const int64_t jl = inf.w_eff;
-  double ec, es;
-  if (inf.mode == VM_INT32) {
-    ec = to_f64(reinterpret_cast<const int32_t*>(last_c)[jl], inf.scale);
-    es = to_f64(reinterpret_cast<const int32_t*>(last_s)[jl], inf.scale);
-  } else {
-    ec = reinterpret_cast<const double*>(last_c)[jl];
-    es = reinterpret_cast<const double*>(last_s)[jl];
-  }
-  info[inst].end_c = ec;
-  info[inst].end_s = es;
-  const int8_t must = in.must_end_at ? in.must_end_at[inst] : (int8_t)-1;
-  if (must == 1) es = -INFINITY;
-  else if (must == 0) ec = -INFINITY;
-  const double pmax = (es > ec) ? es : ec;
-  state[0] = jl;
-  state[1] = ec >= es ? 1 : 0;
-  state[2] = pmax == -INFINITY ? 1 : 0;
-}
-
-// Walk one segment of back-pointers (stages k_begin + k_count - 1 .. k_begin)
-// from state {j, side}, writing pi; the same decisions as backtrack_kernel.
-__global__ void grid_backtrack_kernel(sp_instances in, int64_t inst, const StageShift* shifts,
-                                      const uint32_t* bp, int64_t row_words, int mode, int k_begin,
-                                      int k_count, int64_t* state, sp_policies out) {
-  const int64_t lo = in.layer_off[inst];
-  int64_t j = state[0];
-  bool client = state[1] != 0;
-  const int nw = bp_words(mode);
-  uint8_t* pi = out.pi + lo;
-  for (int t = k_count - 1; t >= 0; --t) {
-    const int k = k_begin + t;
-    const uint32_t* grp = bp + (int64_t)t * row_words + (j >> 5) * nw;
-    const uint32_t bit = 1u << (j & 31);
-    const bool c_stay = grp[0] & bit, s_stay = grp[1] & bit;
-    const bool c_sw = nw == 4 ? (grp[2] & bit) != 0 : !c_stay;
-    const bool s_sw = nw == 4 ? (grp[3] & bit) != 0 : !s_stay;
-    const StageShift sh = shifts[lo + k];
-    if (client) {
-      pi[k] = 1;
-      if (c_stay) {
-        j -= sh.i;
-      } else if (c_sw) {
-        j -= sh.id;
-        client = false;
-      } else {
-        out.status[inst] = SP_ERR_BACKTRACE;
-        state[2] = 2;
-        return;
-      }
-    } else {
-      pi[k] = 0;
-      if (s_stay) {
-        j -= sh.s;
-      } else if (s_sw) {
-        j -= sh.su;
-        client = true;
-      } else {
-        out.status[inst] = SP_ERR_BACKTRACE;
-        state[2] = 2;
-        return;
-      }
-    }
-  }
-  state[0] = j;
-  state[1] = client ? 1 : 0;
-}
-
-// ---------------------------------------------------------------------------
-// _finish (planner.py:88-101) for a placement already written to pi
-
-__device__ void finish_policy(const sp_instances& in, int64_t inst, int64_t lo, int L,
-                              int32_t* idx, sp_policies& out, bool feasible_hint, bool hint_value) {
-  const uint8_t* pi = out.pi + lo;
-  const bool sac = in.source_at_client[inst] != 0;
-  int64_t lat = 0;
-  int prev = sac ? 1 : 0;
-  int n1 = 0;
-  for (int k = 0; k < L; ++k) {
-    const int x = pi[k];
-    if (x) {
-      lat += in.client_units[lo + k] + (prev == 0 ? in.down_units[lo + k] : 0);
-      ++n1;
-    } else {
-      lat += in.server_units[lo + k] + (prev == 1 ? in.up_units[lo + k] : 0);
-    }
-    prev = x;
-  }
-  int a = 0, b = n1;
-  for (int k = 0; k < L; ++k) {
-    if (pi[k]) idx[a++] = k;
-    else idx[b++] = k;
-  }
-  const double* r = in.r + lo;
-  const double cv = np_sum([&](int64_t m) { return r[idx[m]]; }, n1);
-  const double sl = np_sum([&](int64_t m) { return r[idx[n1 + m]]; }, L - n1);
-  out.client_value[inst] = cv;
-  out.server_load[inst] = sl;
-  out.integer_latency[inst] = lat;
-  out.feasible[inst] = feasible_hint ? (hint_value ? 1 : 0) : (lat <= in.budget[inst] ? 1 : 0);
-}
-
-
-// _finish of one grid-solved instance; state[2]: 0 ok, 1 infeasible, 2 backtrace error
-__global__ void grid_finish_kernel(sp_instances in, int64_t inst, const int64_t* state,
-                                   int32_t* idx_scratch, sp_policies out) {
-  const int64_t lo = in.layer_off[inst];
-  const int L = (int)(in.layer_off[inst + 1] - lo);
-  if (state[2] == 2) return;  // status already set
-  if (state[2] == 1)
-    for (int k = 0; k < L; ++k) out.pi[lo + k] = 0;
-  finish_policy(in, inst, lo, L, idx_scratch + lo, out, state[2] == 1, false);
-  out.status[inst] = SP_OK;
-}
+#include "dp_core.cuh"
+#include "dp_cluster_coop.cuh"
+#include "dp_stream.cuh"
+#include "dp_grid.cuh"
 
 // ---------------------------------------------------------------------------
 // _finish over caller-supplied placements
