@@ -105,6 +105,16 @@ int sp_effective_budget(const sp_instances* in, int64_t* w_eff, void* stream);
 int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes,
                void* stream);
 
+/* Workspace sizes for sp_plan_dp on these instances (the `*_workspace_bytes`
+ * query of SURVEY.md 8b): min_bytes runs every instance (in waves; whole-GPU
+ * instances with checkpoint / recompute), full_bytes plans every wave-path
+ * instance in one wave and keeps every back-pointer stage of whole-GPU ones.
+ * Runs the prep kernel, so it needs the fixed part of the workspace
+ * (n x 48 + total_layers x 40 bytes); SP_ERR_WORKSPACE otherwise, with
+ * sp_last_required_workspace().  Synchronises `stream`; launches no DP. */
+int sp_plan_dp_workspace_bytes(const sp_instances* in, size_t* min_bytes, size_t* full_bytes, void* ws,
+                               size_t ws_bytes, void* stream);
+
 /* sp_plan_dp with the capacity axis of huge instances split over devices.
  * Instances that take the whole-GPU path (>= 4M budget columns, or whose
  * back-pointers exceed the workspace) are partitioned

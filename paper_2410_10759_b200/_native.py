@@ -97,6 +97,8 @@ SIGNATURES = {
     "sp_plan_dp": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_size_t, P]),
     "sp_plan_dp_devices": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_int32, P,
                                      C.c_size_t, P]),
+    "sp_plan_dp_workspace_bytes": (C.c_int, [C.POINTER(SpInstances), C.POINTER(C.c_size_t),
+                                             C.POINTER(C.c_size_t), P, C.c_size_t, P]),
     "sp_build_dp_tables": (C.c_int, [C.POINTER(SpInstances), C.c_int64, P, P, P, C.c_size_t, P]),
     "sp_plan_prefix": (C.c_int, [C.POINTER(SpInstances), C.c_int32, C.POINTER(SpPolicies), P]),
     "sp_plan_exhaustive": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P]),

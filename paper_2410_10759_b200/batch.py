@@ -139,6 +139,17 @@ def plan_dp(batch: InstanceBatch, out: PolicyBatch | None = None, devices=None) 
     return out
 
 
+def dp_workspace_bytes(batch: InstanceBatch) -> tuple[int, int]:
+    """(min, full) workspace bytes of plan_dp on this batch (sp_plan_dp_workspace_bytes)."""
+    import ctypes as C
+    s = batch.struct()
+    mn, full = C.c_size_t(0), C.c_size_t(0)
+    rc = N.with_workspace(lambda ws, nb: N.library().sp_plan_dp_workspace_bytes(
+        s, C.byref(mn), C.byref(full), ws, nb, N.stream_ptr()))
+    N.check(rc, "sp_plan_dp_workspace_bytes")
+    return int(mn.value), int(full.value)
+
+
 def plan_prefix(batch: InstanceBatch, which: int, out: PolicyBatch | None = None) -> PolicyBatch:
     out = out or PolicyBatch.empty(batch.n, batch.total_layers, batch.r.device)
     s, o = batch.struct(), out.struct()

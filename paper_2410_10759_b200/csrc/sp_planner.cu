@@ -1089,6 +1089,33 @@ struct PeerParts {
   }
 };
 
+// Workspace of the whole-GPU path for one instance on one device (single
+// partition): the smallest that runs it (checkpoint / recompute with
+// ~sqrt(L) segments) and the one that keeps every back-pointer stage.
+void grid_workspace_bytes(int mode, int64_t L, int64_t ncol, size_t* min_bytes, size_t* full_bytes) {
+  const size_t vb = value_bytes(mode);
+  const int resident = mode == VM_INT32 ? grid_resident<VM_INT32>()
+                       : mode == VM_F64 ? grid_resident<VM_F64>()
+                                        : grid_resident<VM_F64_NAN>();
+  const int64_t nchunks = (ncol + kGridCH - 1) / kGridCH;
+  int G = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(resident, 1), nchunks));
+  const int NC = (int)((nchunks + G - 1) / G);
+  G = (int)((nchunks + NC - 1) / NC);
+  const int64_t B = (int64_t)NC * kGridCH, line = 128 / (int64_t)vb;
+  const int64_t span = (kGridCH + line) + G * B + line;
+  const size_t bp_stage = (size_t)bp_row_words_for(mode, G * B) * 4;
+  const size_t ckpt = align_up(2 * (size_t)ncol * vb, 256);
+  const size_t fixed = align_up((size_t)G * 4, 256) + 256 + align_up(2 * kRowBufs * (size_t)span * vb, 256);
+  auto need = [&](int64_t k) {
+    const size_t nseg = (size_t)((L + k - 1) / k);
+    return fixed + (k == L ? 2 : nseg + 1) * ckpt + align_up((size_t)k * bp_stage, 256);
+  };
+  int64_t K = std::max<int64_t>(1, (int64_t)std::sqrt((double)L * (double)ckpt / (double)bp_stage));
+  K = std::min(K, L);
+  *min_bytes = need(K);
+  *full_bytes = need(L);
+}
+
 // Solve one instance over the whole GPU.  With the full back-pointer table in
 // memory: one forward launch and one backtrack.  Otherwise checkpoint /
 // recompute: a forward pass that keeps a row every K stages, then, segment by
@@ -1461,7 +1488,7 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
 
 // Shared driver of sp_plan_dp and sp_build_dp_tables.
 int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_s, void* ws,
-           size_t ws_bytes, cudaStream_t st) {
+           size_t ws_bytes, cudaStream_t st, size_t* q_min = nullptr, size_t* q_full = nullptr) {
   const int64_t n = in->n, total = in->total_layers;
   if (n == 0) return SP_OK;
   Carve cv{(uint8_t*)ws, ws_bytes};
@@ -1529,6 +1556,19 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     items.push_back(it);
   }
 
+  if (q_min) {  // workspace query (sp_plan_dp_workspace_bytes): no DP launched
+    size_t mn = 0, full = 0;
+    for (const Item& it : items) {
+      const bool grid = tab_c == nullptr && (force == DPV_GRID || it.ncol >= kGridMinCols);
+      size_t imin = it.plan.bp + it.plan.rows, ifull = imin;
+      if (grid) grid_workspace_bytes(it.mode, it.L, it.ncol, &imin, &ifull);
+      mn = std::max(mn, imin);
+      full = grid ? std::max(full, ifull) : full + ifull;
+    }
+    *q_min = fixed + mn;
+    *q_full = fixed + std::max(full, mn);
+    return SP_OK;
+  }
   const int2* a_reach = env_int("SPLITPLAN_NO_REACH", 0) ? nullptr : reach;
   // instances too large for a wave (or wider than 4M columns) run alone over
   // the whole GPU (grid path, checkpointing if needed)
@@ -1678,6 +1718,19 @@ int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_byt
   rc = validate_out(out);
   if (rc) return rc;
   return run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int sp_plan_dp_workspace_bytes(const sp_instances* in, size_t* min_bytes, size_t* full_bytes, void* ws,
+                               size_t ws_bytes, void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  if (!min_bytes || !full_bytes) {
+    set_error(SP_ERR_INVALID, "null output");
+    return SP_ERR_INVALID;
+  }
+  *min_bytes = *full_bytes = 0;
+  if (in->n == 0) return SP_OK;
+  return run_dp(in, nullptr, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, min_bytes, full_bytes);
 }
 
 int sp_plan_dp_devices(const sp_instances* in, sp_policies* out, const int32_t* devices,

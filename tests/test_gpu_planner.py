@@ -350,3 +350,25 @@ def test_reachable_frontier_skips(gpu, variant, no_reach, monkeypatch):
     for name, must in (("battery_large_chain", False), ("battery_wide", True), ("battery_large_model", True)):
         bat = Battery(name)
         _compare(bat, "dp", B.plan_dp(_batch(bat, with_must=must)).to_host())
+
+
+def test_dp_workspace_query(gpu):
+    """sp_plan_dp_workspace_bytes: plan_dp runs in exactly the reported minimum
+    workspace (bit-exact), and fails cleanly below it."""
+    import torch
+    from paper_2410_10759_b200 import _native as N, batch as B
+    bat = Battery("battery_large_model")
+    b = _batch(bat)
+    mn, full = B.dp_workspace_bytes(b)
+    assert 0 < mn <= full
+    lib = N.library()
+    for size, ok in ((mn, True), (full, True), (mn - 4096, False)):
+        ws = torch.empty(size, dtype=torch.uint8, device=N.device())
+        out = B.PolicyBatch.empty(b.n, b.total_layers, b.r.device)
+        rc = lib.sp_plan_dp(b.struct(), out.struct(), N.ptr(ws), size, N.stream_ptr())
+        torch.cuda.synchronize()
+        if ok:
+            assert rc == 0, N.library().sp_last_error()
+            _compare(bat, "dp", out.to_host())
+        else:
+            assert rc == N.SP_ERR_WORKSPACE
