@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 1
+#define SP_ABI_VERSION 2  /* 2: + sp_plan_dp_devices, sp_plan_dp_workspace_bytes */
 
 enum sp_status {
   SP_OK = 0,
