@@ -436,9 +436,6 @@ struct StreamCfg {
 };
 constexpr StreamCfg kStreamCfgs[] = {{256, 4, 6}, {256, 8, 3}, {128, 8, 6}, {256, 4, 3}, {256, 6, 4}};
 constexpr int kStreamCfgF64 = 3;
-// bulk-copy ring depth of the grid kernel (T = 256, E = 4)
-template <int MODE> constexpr int ring_slots() { return MODE == VM_INT32 ? 6 : 3; }
-inline int ring_slots_rt(int mode) { return mode == VM_INT32 ? 6 : 3; }
 // SPLITPLAN_STREAM_CFG forces one configuration; otherwise the int32 domain
 // picks between 256 x 8 and 256 x 6 per width (stream_geom), the fp64
 // domains use 256 x 4.
@@ -962,19 +959,25 @@ double hbm_bytes_per_cell(int mode, int variant) {
 
 // ---- grid path: one huge instance over the whole GPU --------------------------
 
-constexpr int kGridT = 256, kGridE = 4;
-constexpr int kGridCH = kGridT * kGridE;
+// grid kernel configuration: 256 threads; int32 rows 6 columns per thread and
+// a 4-slot ring (the streaming kernel's cfg2 geometry), fp64 4 and 3 slots
+constexpr int kGridT = 256;
+template <int MODE> constexpr int grid_e() { return MODE == VM_INT32 ? 6 : 4; }
+template <int MODE> constexpr int grid_slots() { return MODE == VM_INT32 ? 4 : 3; }
+inline int grid_e_rt(int mode) { return mode == VM_INT32 ? 6 : 4; }
+inline int grid_slots_rt(int mode) { return mode == VM_INT32 ? 4 : 3; }
+inline int64_t grid_ch(int mode) { return (int64_t)kGridT * grid_e_rt(mode); }
 constexpr int64_t kGridMinCols = (int64_t)1 << 22;
 enum { DPV_GRID = 5 };
 
 size_t grid_smem(int mode) {
   const size_t vb = value_bytes(mode);  // ring slots + one NEG window
-  return 256 + (size_t)(ring_slots_rt(mode) * 4 + 1) * (kGridCH + 16 / vb) * vb;
+  return 256 + (size_t)(grid_slots_rt(mode) * 4 + 1) * (grid_ch(mode) + 16 / vb) * vb;
 }
 
 template <int MODE>
 int grid_resident() {
-  auto kern = dp_grid_kernel<MODE, kGridT, kGridE, ring_slots<MODE>()>;
+  auto kern = dp_grid_kernel<MODE, kGridT, grid_e<MODE>(), grid_slots<MODE>()>;
   int n = 0, dev = 0, sms = 148;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grid_smem(MODE)) !=
           cudaSuccess ||
@@ -989,7 +992,7 @@ int grid_resident() {
 
 template <int MODE>
 int launch_grid_t(const GridArgs& g, cudaStream_t st) {
-  auto kern = dp_grid_kernel<MODE, kGridT, kGridE, ring_slots<MODE>()>;
+  auto kern = dp_grid_kernel<MODE, kGridT, grid_e<MODE>(), grid_slots<MODE>()>;
   // per device: a partition may be launched on a peer device
   int rc0 = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grid_smem(MODE)),
                        "cudaFuncSetAttribute(dp_grid_kernel)");
@@ -1011,7 +1014,7 @@ int launch_grid_t(const GridArgs& g, cudaStream_t st) {
 
 template <int MODE>
 int launch_grid_inplace_t(const GridInplaceArgs& g, cudaStream_t st) {
-  auto kern = dp_grid_inplace_kernel<MODE, kGridT, kGridE, ring_slots<MODE>()>;
+  auto kern = dp_grid_inplace_kernel<MODE, kGridT, grid_e<MODE>(), grid_slots<MODE>()>;
   int rc0 = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grid_smem(MODE)),
                        "cudaFuncSetAttribute(dp_grid_inplace_kernel)");
   if (rc0) return rc0;
@@ -1097,12 +1100,12 @@ void grid_workspace_bytes(int mode, int64_t L, int64_t ncol, size_t* min_bytes, 
   const int resident = mode == VM_INT32 ? grid_resident<VM_INT32>()
                        : mode == VM_F64 ? grid_resident<VM_F64>()
                                         : grid_resident<VM_F64_NAN>();
-  const int64_t nchunks = (ncol + kGridCH - 1) / kGridCH;
+  const int64_t nchunks = (ncol + grid_ch(mode) - 1) / grid_ch(mode);
   int G = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(resident, 1), nchunks));
   const int NC = (int)((nchunks + G - 1) / G);
   G = (int)((nchunks + NC - 1) / NC);
-  const int64_t B = (int64_t)NC * kGridCH, line = 128 / (int64_t)vb;
-  const int64_t span = (kGridCH + line) + G * B + line;
+  const int64_t B = (int64_t)NC * grid_ch(mode), line = 128 / (int64_t)vb;
+  const int64_t span = (grid_ch(mode) + line) + G * B + line;
   const size_t bp_stage = (size_t)bp_row_words_for(mode, G * B) * 4;
   const size_t ckpt = align_up(2 * (size_t)ncol * vb, 256);
   const size_t fixed = align_up((size_t)G * 4, 256) + 256 + align_up(2 * kRowBufs * (size_t)span * vb, 256);
@@ -1142,7 +1145,7 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
                        : mode == VM_F64 ? grid_resident<VM_F64>()
                                         : grid_resident<VM_F64_NAN>();
   if (resident <= 0) return check_cuda(cudaErrorInvalidConfiguration, "dp_grid_kernel occupancy");
-  const int64_t nchunks = (ncol + kGridCH - 1) / kGridCH;
+  const int64_t nchunks = (ncol + grid_ch(mode) - 1) / grid_ch(mode);
   // partitions of the capacity axis (one per device in a multi-GPU run;
   // SPLITPLAN_GRID_PARTS > 1 emulates them on this device)
   // SPLITPLAN_GRID_DEVICES > 1 places partition p on device (current + p),
@@ -1184,7 +1187,7 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
   G = std::max(G, 1);
   const int NC = (int)((nchunks + (int64_t)G * nparts - 1) / ((int64_t)G * nparts));
   G = (int)((nchunks + (int64_t)NC * nparts - 1) / ((int64_t)NC * nparts));
-  const int64_t B = (int64_t)NC * kGridCH;
+  const int64_t B = (int64_t)NC * grid_ch(mode);
   const int64_t line = 128 / (int64_t)vb;
   // halo: the widest read-back of any stage plus alignment slack, whole lines
   int64_t halo = 0;
@@ -1222,7 +1225,7 @@ int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* 
     if (hw <= B) inplace_hw = hw;
   }
   const bool inplace = inplace_hw > 0;
-  const int64_t span = (kGridCH + line) + halo + G * B + line;
+  const int64_t span = (grid_ch(mode) + line) + halo + G * B + line;
   const int64_t row_words = bp_row_words_for(mode, (int64_t)nparts * G * B);
   const size_t rows_bytes = inplace ? align_up(2 * (size_t)span * vb, 256) +
                                           align_up((size_t)G * 3 * 2 * (size_t)inplace_hw * vb, 256)
