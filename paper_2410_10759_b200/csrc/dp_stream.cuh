@@ -125,7 +125,6 @@ struct StreamGeom {
   int row_hint;  // L2 policy of the row stores (set at launch)
   int diag;      // diagnostics only (SPLITPLAN_STREAM_DIAG; results are wrong when set):
                  // bit 0 skips the stage waits, bit 1 skips the window copies
-  int discard;   // drop dead row lines from L2 each stage (SPLITPLAN_ROW_DISCARD)
   int cfg;       // kStreamCfgs index (host side)
 };
 
@@ -234,19 +233,6 @@ __global__ void __launch_bounds__(T + 32, 2) dp_stream_kernel(DpArgs a, StreamGe
             lane < G ? (uint32_t)(lane <= q || NBUF == 2 ? k : max(k - 1, 0)) : 0u;
         while (!(geo.diag & 1) &&
                !__all_sync(0xffffffffu, lane >= G || ld_cluster_relaxed(my_prog + 4u * i) >= need)) {
-        }
-        if (geo.discard) {
-          // the buffer this stage overwrites holds a row every CTA has finished
-          // reading: drop this block's lines from L2 instead of letting them be
-          // written back when evicted (the compute warps store over them after
-          // this stage's first slot, ordered by its mbarrier)
-          V* dc = row(i, (k + 1) % NBUF, 0) + j0;
-          V* ds = row(i, (k + 1) % NBUF, 1) + j0;
-          for (int x = lane * LINE; x < B; x += 32 * LINE) {
-            discard_l2(dc + x);
-            discard_l2(ds + x);
-          }
-          __syncwarp();
         }
         if (lane == 0) {
           fence_acq_rel_cluster();

@@ -542,7 +542,7 @@ StreamGeom stream_geom_cfg(int mode, int64_t ncol, int cfg, int64_t* cost) {
   const int resident = stream_resident_ctas(mode, cfg);
   const int force = env_int("SPLITPLAN_DP_CLUSTER", 0);
   auto geom = [&](int G) {
-    StreamGeom t{G, (int)((nchunks + G - 1) / G), 0, 0, 0, 0, cfg};
+    StreamGeom t{G, (int)((nchunks + G - 1) / G), 0, 0, 0, cfg};
     t.G = (int)((nchunks + t.NC - 1) / t.NC);
     return t;
   };
@@ -592,7 +592,6 @@ int launch_stream_t(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream
   geo.n_items = (int)n_items;
   geo.row_hint = env_int("SPLITPLAN_ROW_EVICT_LAST", 0) ? 1 : 0;
   geo.diag = env_int("SPLITPLAN_STREAM_DIAG", 0);
-  geo.discard = env_int("SPLITPLAN_ROW_DISCARD", 0);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((n_items + NI - 1) / NI * geo.G), 1, 1);
   cfg.blockDim = dim3((unsigned)(T + 32), 1, 1);  // + the producer warp
@@ -648,7 +647,7 @@ size_t own_smem(int mode, int NC) {
 }
 // cluster geometry: the fewest CTAs whose blocks fit shared memory (G = 0: not possible)
 StreamGeom own_geom(int mode, int64_t ncol) {
-  StreamGeom g{0, 0, 0, 0, 0, 0, 0};
+  StreamGeom g{0, 0, 0, 0, 0};
   if (mode != VM_INT32) return g;
   const int64_t nchunks = (ncol + own_ch() - 1) / own_ch();
   int ncmax = 0;
