@@ -30,7 +30,9 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 2  /* 2: + sp_plan_dp_devices, sp_plan_dp_workspace_bytes */
+#define SP_ABI_VERSION 3  /* 2: + sp_plan_dp_devices, sp_plan_dp_workspace_bytes;
+                             3: per-partition workspaces, sp_grid_* (one process per
+                                device), sp_ipc_*, sp_last_full_workspace */
 
 enum sp_status {
   SP_OK = 0,
@@ -76,6 +78,10 @@ int sp_abi_version(void);
 const char* sp_last_error(void);
 /* bytes the last SP_ERR_WORKSPACE call needed */
 size_t sp_last_required_workspace(void);
+/* after a successful sp_plan_dp: the workspace that would have planned every
+ * wave-path instance in ONE wave and kept every back-pointer stage of the
+ * whole-GPU ones (no recompute); a caller growing its workspace uses it */
+size_t sp_last_full_workspace(void);
 
 /* Instrumentation (thread-local, off by default).  While enabled, every
  * DP-stage kernel launch is bracketed by CUDA events on its stream and every
@@ -115,24 +121,92 @@ int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_byt
 int sp_plan_dp_workspace_bytes(const sp_instances* in, size_t* min_bytes, size_t* full_bytes, void* ws,
                                size_t ws_bytes, void* stream);
 
-/* sp_plan_dp with the capacity axis of huge instances split over devices.
- * Instances that take the whole-GPU path (>= 4M budget columns, or whose
- * back-pointers exceed the workspace) are partitioned
- * along the budget axis: partition p runs on devices[p] (its row buffers,
- * progress counters and stage records in that device's memory, peer access
- * enabled between the listed devices), each partition mirrors its left
- * neighbour's last columns (the halo) by NVLink peer stores from inside the
- * DP kernel, and partitions order their stages through system-scope
- * progress counters.  devices[0] must be the current device, which owns
- * `in`, `out`, `ws` and `stream`; a device may be listed more than once.
- * Other instances are planned on the current device as by sp_plan_dp.
+/* sp_plan_dp with the capacity axis of huge instances split over devices
+ * (SURVEY.md 8(e), cfg5).  Instances that take the whole-GPU path (>= 4M
+ * budget columns, or whose back-pointers exceed the workspace) are split
+ * along the budget axis into one partition per listed device: partition p
+ * runs on devices[p] and keeps EVERYTHING of its columns -- row buffers,
+ * progress counters, stage records, checkpoint rows and back-pointers -- in
+ * part_ws[p] (device memory of devices[p], part_ws_bytes[p] bytes, owned by
+ * the caller).  Each partition mirrors its left neighbour's last columns (the
+ * halo) by NVLink peer stores from inside the DP kernel, partitions order
+ * their stages through system-scope progress counters, and the backtrack
+ * walks the partitions from the right, each reading its own back-pointers
+ * and handing (stage, column, side) to its left neighbour when the column
+ * leaves its range (planner.py:146-179).  devices[0] must be the current
+ * device, which owns `in`, `out`, `ws` and `stream`; a device may be listed
+ * more than once.  Other instances are planned in `ws` as by sp_plan_dp.
  * Replaces the same reference functions as sp_plan_dp (planner.py:182-202). */
-int sp_plan_dp_devices(const sp_instances* in, sp_policies* out, const int32_t* devices,
-                       int32_t n_devices, void* ws, size_t ws_bytes, void* stream);
+int sp_plan_dp_devices(const sp_instances* in, sp_policies* out, const int32_t* devices, int32_t n_devices,
+                       void* ws, size_t ws_bytes, void* const* part_ws, const size_t* part_ws_bytes,
+                       void* stream);
+
+/* Workspace sizes for sp_plan_dp_devices: ws_min for `ws`, and per
+ * partition workspace the smallest that runs (checkpoint / recompute) and the
+ * one keeping every back-pointer stage.  Runs the prep kernel in `ws` (it
+ * needs the fixed part; SP_ERR_WORKSPACE otherwise). */
+int sp_plan_dp_devices_workspace_bytes(const sp_instances* in, const int32_t* devices, int32_t n_devices,
+                                       size_t* ws_min, size_t* part_min, size_t* part_full, void* ws,
+                                       size_t ws_bytes, void* stream);
+
+/* ---- capacity partitions, one process per device ------------------------
+ * The same partitioned solve driven by one process per partition (torchrun,
+ * one rank per GPU): every rank plans identically, allocates one partition
+ * workspace of plan.part_bytes, maps every other rank's workspace into its
+ * address space (sp_ipc_export / sp_ipc_import over the process group), and
+ * runs the phases in lockstep:
+ *   forward:   for seg in 0..nseg-1: reset; barrier; forward(seg, write_ckpt=1,
+ *              keep_bp = seg == nseg-1); barrier
+ *   end:       the owner partition runs sp_grid_part_end; broadcast state
+ *   backtrack: for seg = nseg-1..0: (recompute seg with keep_bp=1 unless it
+ *              is the last), then partitions nparts-1..0 in turn run
+ *              sp_grid_part_backtrack on the handed-over state
+ *   finish:    combine pi (each stage written by exactly one partition) and
+ *              evaluate it (sp_evaluate_policy).                              */
+typedef struct sp_grid_plan {
+  int32_t mode, n_layers, ctas, chunks_per_cta, nparts, seg_stages, nseg, nckpt, sac, owner_part;
+  int64_t ncol, part_cols, halo, span, row_words;
+  uint64_t rec_off, prog_off, state_off, rows_off, ckpt_off, bp_off, ckpt_bytes, bp_stage, part_bytes;
+} sp_grid_plan;
+
+/* Geometry for ONE instance (in->n == 1, layer_off[0] == 0) over `nparts`
+ * partitions of at most `ctas_per_part` CTAs (0: all co-resident CTAs of the
+ * device) in partition workspaces of `part_ws_bytes`; force_segment > 0 fixes
+ * the checkpoint segment length.  ws: scratch for the prep kernel.
+ * Synchronises `stream`. */
+int sp_grid_plan_make(const sp_instances* in, int32_t nparts, int32_t ctas_per_part, size_t part_ws_bytes,
+                      int32_t force_segment, sp_grid_plan* plan, void* ws, size_t ws_bytes, void* stream);
+/* stage records and state of a partition workspace (prep kernel into it) */
+int sp_grid_part_prepare(const sp_grid_plan* plan, const sp_instances* in, void* part_ws, void* stream);
+/* zero the partition's progress counters (before every forward launch, on
+ * every partition, before any partition launches) */
+int sp_grid_part_reset(const sp_grid_plan* plan, void* part_ws, void* stream);
+/* DP stages of segment `seg` on partition `part` (a cooperative launch that
+ * spins on its neighbours' counters: every partition of the phase must be
+ * launched).  part_ws[nparts]: every partition workspace as mapped here. */
+int sp_grid_part_forward(const sp_grid_plan* plan, int32_t part, void* const* part_ws, int32_t seg,
+                         int32_t write_ckpt, int32_t keep_bp, void* stream);
+/* end side from the final row (owner partition plan->owner_part):
+ * state[4] (device) = {column, client side, flag 0 ok / 1 infeasible /
+ * 2 backtrace error, next stage} (planner.py:190-200) */
+int sp_grid_part_end(const sp_grid_plan* plan, void* owner_ws, int8_t must_end_at, int64_t* state,
+                     void* stream);
+/* walk segment `seg` through this partition's back-pointers while the column
+ * stays in its range; writes pi[stage] (device u8[L]) and advances state */
+int sp_grid_part_backtrack(const sp_grid_plan* plan, int32_t part, void* part_ws, int32_t seg, int64_t* state,
+                           uint8_t* pi, void* stream);
+
+/* CUDA IPC of a device buffer: a 64-byte handle of its allocation plus the
+ * buffer's offset in it; import maps it (returns the buffer and the mapping
+ * base to close). */
+int sp_ipc_export(const void* dptr, void* handle64, size_t* offset);
+int sp_ipc_import(const void* handle64, size_t offset, void** dptr, void** base);
+int sp_ipc_close(void* base);
 
 /* Full DP tables of ONE instance (in->n == 1) as float64, row-major
  * [(L+1) x (w_eff+1)], unreachable cells = -inf.  Replaces planner.py:128-143
- * `build_dp_tables`.  w_eff must equal sp_effective_budget()'s value. */
+ * `build_dp_tables`.  w_eff must equal sp_effective_budget()'s value
+ * (SP_ERR_INVALID otherwise, before anything is written). */
 int sp_build_dp_tables(const sp_instances* in, int64_t w_eff, double* client_table,
                        double* server_table, void* ws, size_t ws_bytes, void* stream);
 
@@ -141,7 +215,8 @@ int sp_build_dp_tables(const sp_instances* in, int64_t w_eff, double* client_tab
  * `plan_trivial`.  `which` is an sp_prefix_planner. */
 int sp_plan_prefix(const sp_instances* in, int32_t which, sp_policies* out, void* stream);
 
-/* Exhaustive planner over all 2^L placements (L <= 24).  Replaces
+/* Exhaustive planner over all 2^L placements (L <= 24; SP_ERR_UNSUPPORTED
+ * for longer instances).  Replaces
  * planner.py:228-268 `plan_oracle`: maximum client value among feasible
  * masks, ties to the smallest mask with layer 1 as the MSB. */
 int sp_plan_exhaustive(const sp_instances* in, sp_policies* out, void* stream);

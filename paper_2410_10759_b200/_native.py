@@ -79,6 +79,14 @@ class SpSimBatch(C.Structure):
                 ("arrival_ms", P), ("demand", P), ("duration_ms", P), ("capacity", P)]
 
 
+class SpGridPlan(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("mode", "n_layers", "ctas", "chunks_per_cta", "nparts", "seg_stages",
+                                         "nseg", "nckpt", "sac", "owner_part")] + \
+               [(n, C.c_int64) for n in ("ncol", "part_cols", "halo", "span", "row_words")] + \
+               [(n, C.c_uint64) for n in ("rec_off", "prog_off", "state_off", "rows_off", "ckpt_off", "bp_off",
+                                          "ckpt_bytes", "bp_stage", "part_bytes")]
+
+
 class SpSimOut(C.Structure):
     _fields_ = [("admit_ms", P), ("wait_ms", P), ("cum_wait_ms", P), ("max_wait_ms", P),
                 ("mean_wait_ms", P), ("status", P), ("deadlock_req", P)]
@@ -89,6 +97,7 @@ SIGNATURES = {
     "sp_abi_version": (C.c_int, []),
     "sp_last_error": (C.c_char_p, []),
     "sp_last_required_workspace": (C.c_size_t, []),
+    "sp_last_full_workspace": (C.c_size_t, []),
     "sp_profile_enable": (None, [C.c_int]),
     "sp_profile_collect": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                      C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -96,7 +105,21 @@ SIGNATURES = {
     "sp_effective_budget": (C.c_int, [C.POINTER(SpInstances), P, P]),
     "sp_plan_dp": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_size_t, P]),
     "sp_plan_dp_devices": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_int32, P,
-                                     C.c_size_t, P]),
+                                     C.c_size_t, P, P, P]),
+    "sp_plan_dp_devices_workspace_bytes": (C.c_int, [C.POINTER(SpInstances), P, C.c_int32,
+                                                     C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                                     C.POINTER(C.c_size_t), P, C.c_size_t, P]),
+    "sp_grid_plan_make": (C.c_int, [C.POINTER(SpInstances), C.c_int32, C.c_int32, C.c_size_t, C.c_int32,
+                                    C.POINTER(SpGridPlan), P, C.c_size_t, P]),
+    "sp_grid_part_prepare": (C.c_int, [C.POINTER(SpGridPlan), C.POINTER(SpInstances), P, P]),
+    "sp_grid_part_reset": (C.c_int, [C.POINTER(SpGridPlan), P, P]),
+    "sp_grid_part_forward": (C.c_int, [C.POINTER(SpGridPlan), C.c_int32, P, C.c_int32, C.c_int32, C.c_int32,
+                                       P]),
+    "sp_grid_part_end": (C.c_int, [C.POINTER(SpGridPlan), P, C.c_int8, P, P]),
+    "sp_grid_part_backtrack": (C.c_int, [C.POINTER(SpGridPlan), C.c_int32, P, C.c_int32, P, P, P]),
+    "sp_ipc_export": (C.c_int, [P, P, C.POINTER(C.c_size_t)]),
+    "sp_ipc_import": (C.c_int, [P, C.c_size_t, C.POINTER(P), C.POINTER(P)]),
+    "sp_ipc_close": (C.c_int, [P]),
     "sp_plan_dp_workspace_bytes": (C.c_int, [C.POINTER(SpInstances), C.POINTER(C.c_size_t),
                                              C.POINTER(C.c_size_t), P, C.c_size_t, P]),
     "sp_build_dp_tables": (C.c_int, [C.POINTER(SpInstances), C.c_int64, P, P, P, C.c_size_t, P]),
@@ -193,32 +216,77 @@ def to_dev(a, dtype, dev=None) -> torch.Tensor:
 
 
 _ws: dict[int, torch.Tensor] = {}
+_WS_MIN = 64 << 20
+_WS_ROUND = 64 << 20
+
+
+def _round_ws(n: int) -> int:
+    return max(_WS_MIN, (int(n) + _WS_ROUND - 1) // _WS_ROUND * _WS_ROUND)
+
+
+def workspace_cap(dev=None) -> int:
+    """Largest scratch buffer grown opportunistically: SPLITPLAN_WS_GB, else
+    75 % of the device's memory.  Growth beyond what a call requires happens
+    only when the call reports it would use the room (sp_last_full_workspace:
+    one wave instead of several, fewer checkpoint segments)."""
+    env = os.environ.get("SPLITPLAN_WS_GB")
+    if env:
+        return int(float(env) * (1 << 30))
+    _free, total = torch.cuda.mem_get_info(dev or device())
+    return int(total * 0.75)
+
+
+def free_bytes(dev) -> int:
+    """Free device memory including what PyTorch's caching allocator holds unused."""
+    free, _total = torch.cuda.mem_get_info(dev)
+    return int(free) + int(torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev))
 
 
 def workspace(min_bytes: int = 0) -> torch.Tensor:
-    """Per-device cached scratch buffer, grown on demand."""
+    """Per-device cached scratch buffer: 64 MB at first, then grown to what a
+    call reports it needs (at least doubling); never grabbed speculatively."""
     dev = device()
-    key = dev.index
-    cur = _ws.get(key)
+    cur = _ws.get(dev.index)
     if cur is None or cur.numel() < min_bytes:
+        want = _round_ws(max(min_bytes, 2 * cur.numel() if cur is not None else 0))
+        if cur is not None and want > max(workspace_cap(), min_bytes):
+            want = _round_ws(min_bytes)
         if cur is not None:
-            del _ws[key]
+            del _ws[dev.index]
             cur = None
             torch.cuda.empty_cache()
-        free, _total = torch.cuda.mem_get_info(dev)
-        cap = int(float(os.environ.get("SPLITPLAN_WS_GB", "64")) * (1 << 30))
-        # default cap 64 GB (SPLITPLAN_WS_GB); never more than 85 % of what is free
-        want = max(min_bytes, min(cap, int(free * 0.85)), 64 << 20)
-        _ws[key] = torch.empty(want, dtype=torch.uint8, device=dev)
-    return _ws[key]
+        _ws[dev.index] = torch.empty(want, dtype=torch.uint8, device=dev)
+    return _ws[dev.index]
+
+
+def grow_workspace_hint(full_bytes: int) -> None:
+    """After a call that ran in waves: grow the cached workspace to what one
+    wave needs (sp_last_full_workspace), within the cap and free memory."""
+    dev = device()
+    cur = _ws.get(dev.index)
+    have = cur.numel() if cur is not None else 0
+    target = min(int(full_bytes), workspace_cap(dev), have + int(free_bytes(dev) * 0.9))
+    if target <= have + (have >> 2):  # not worth a reallocation
+        return
+    workspace(target)
+
+
+def release_workspace() -> None:
+    """Drop the cached scratch buffer of the current device."""
+    _ws.pop(device().index, None)
+    torch.cuda.empty_cache()
 
 
 def with_workspace(fn, *args):
     """Call fn(*args, ws_ptr, ws_bytes), growing the workspace on SP_ERR_WORKSPACE."""
     ws = workspace()
     rc = fn(*args, ptr(ws), C.c_size_t(ws.numel()))
-    if rc == SP_ERR_WORKSPACE:
+    for _ in range(8):  # each retry covers the largest instance seen failing so far
+        if rc != SP_ERR_WORKSPACE:
+            break
         need = int(library().sp_last_required_workspace())
+        if need <= ws.numel():
+            break
         ws = workspace(need + (1 << 20))
         rc = fn(*args, ptr(ws), C.c_size_t(ws.numel()))
     return rc

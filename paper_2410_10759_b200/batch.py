@@ -11,6 +11,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import ctypes as C
+
 import numpy as np
 import torch
 
@@ -124,24 +126,54 @@ def plan_dp(batch: InstanceBatch, out: PolicyBatch | None = None, devices=None) 
 
     `devices` (a list of CUDA device indices, the current one first) splits
     the capacity axis of huge instances over those devices
-    (sp_plan_dp_devices)."""
+    (sp_plan_dp_devices), one partition workspace per listed device."""
     out = out or PolicyBatch.empty(batch.n, batch.total_layers, batch.r.device)
     s, o = batch.struct(), out.struct()
+    lib = N.library()
     if devices:
-        import ctypes as C
+        parts = partition_workspaces(batch, devices)
         arr = (C.c_int32 * len(devices))(*[int(d) for d in devices])
-        rc = N.with_workspace(lambda ws, nb: N.library().sp_plan_dp_devices(
-            s, o, C.cast(arr, C.c_void_p), len(devices), ws, nb, N.stream_ptr()))
+        wptr = (C.c_void_p * len(devices))(*[t.data_ptr() for t in parts])
+        wlen = (C.c_size_t * len(devices))(*[t.numel() for t in parts])
+        rc = N.with_workspace(lambda ws, nb: lib.sp_plan_dp_devices(
+            s, o, C.cast(arr, C.c_void_p), len(devices), ws, nb, C.cast(wptr, C.c_void_p),
+            C.cast(wlen, C.c_void_p), N.stream_ptr()))
         N.check(rc, "sp_plan_dp_devices")
         return out
-    rc = N.with_workspace(lambda ws, nb: N.library().sp_plan_dp(s, o, ws, nb, N.stream_ptr()))
+    rc = N.with_workspace(lambda ws, nb: lib.sp_plan_dp(s, o, ws, nb, N.stream_ptr()))
     N.check(rc, "sp_plan_dp")
+    N.grow_workspace_hint(int(lib.sp_last_full_workspace()))
+    return out
+
+
+def partition_workspaces(batch: InstanceBatch, devices) -> list[torch.Tensor]:
+    """One workspace per capacity partition, each on its device: the size that
+    keeps every back-pointer stage if it fits the device, else the minimum
+    (checkpoint / recompute) -- sp_plan_dp_devices_workspace_bytes."""
+    s = batch.struct()
+    arr = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+    ws_min, pmin, pfull = C.c_size_t(0), C.c_size_t(0), C.c_size_t(0)
+    rc = N.with_workspace(lambda ws, nb: N.library().sp_plan_dp_devices_workspace_bytes(
+        s, C.cast(arr, C.c_void_p), len(devices), C.byref(ws_min), C.byref(pmin), C.byref(pfull), ws, nb,
+        N.stream_ptr()))
+    N.check(rc, "sp_plan_dp_devices_workspace_bytes")
+    N.workspace(int(ws_min.value))
+    # the partitions of one device share 80 % of its free memory; each takes
+    # what keeps every back-pointer stage if that fits its share, else its
+    # share (the library checkpoints within it), never below the minimum
+    share = {}
+    for d in set(int(x) for x in devices):
+        dev = torch.device("cuda", d)
+        share[d] = min(int(N.free_bytes(dev) * 0.8), N.workspace_cap(dev)) // sum(int(x) == d for x in devices)
+    out = []
+    for d in devices:
+        want = max(int(pmin.value), min(int(pfull.value), share[int(d)]))
+        out.append(torch.empty(max(want, 256), dtype=torch.uint8, device=torch.device("cuda", int(d))))
     return out
 
 
 def dp_workspace_bytes(batch: InstanceBatch) -> tuple[int, int]:
     """(min, full) workspace bytes of plan_dp on this batch (sp_plan_dp_workspace_bytes)."""
-    import ctypes as C
     s = batch.struct()
     mn, full = C.c_size_t(0), C.c_size_t(0)
     rc = N.with_workspace(lambda ws, nb: N.library().sp_plan_dp_workspace_bytes(

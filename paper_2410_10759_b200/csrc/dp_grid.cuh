@@ -34,6 +34,21 @@ constexpr int kMaxParts = 8;
 // in the global CTA index space, so the protocol is the same whether the
 // partitions are launched together (one device, emulating several) or one
 // per device.
+//
+// Every buffer of a partition lives in that partition's own workspace (on its
+// device): rows, progress counters, checkpoint rows and back-pointers of its
+// columns.  Only the halo stores (into the right neighbour's rows), the
+// counter polls and the halo part of a checkpoint restart (from the left
+// neighbour's checkpoint) touch a neighbour's memory.
+struct GridPart {
+  uint8_t* rows;          // [3][C|S][NEG pad | halo | Wp | line]
+  uint32_t* prog;         // [G] stages completed + 1 (zeroed before a launch)
+  uint32_t* bp;           // back-pointers of this launch's stages, local columns, or null
+  const void* init;       // row k_begin, local columns [0, Wp): C then S, or null (origin row)
+  const void* init_left;  // the left neighbour's row k_begin (same layout), or null
+  void* out;              // row k_begin + k_count, local columns: C then S, or null
+};
+
 struct GridArgs {
   const StageShift* shifts;  // stage records of the instance (index = stage)
   const int64_t* rv;         // stage values in the value domain
@@ -42,19 +57,13 @@ struct GridArgs {
   int ncol;                  // W_eff + 1
   int G, NC;                 // CTAs per partition, chunks per CTA
   int sac;
-  const void* init_c;        // row k_begin, ncol values each, or null: origin row
-  const void* init_s;
-  void* out_c;               // row k_begin + k_count, or null
-  void* out_s;
-  uint32_t* bp;              // back-pointers of the range's stages, or null
-  int64_t bp_row_words;
-  uint32_t* progs[kMaxParts];  // per partition: [G] stages completed + 1 (zeroed)
+  int64_t bp_row_words;      // u32 words per stage row of one partition's back-pointers
   int nparts;                // partitions of the capacity axis
   int part_base;             // first partition of this launch
   int launch_parts;          // partitions of this launch (grid = launch_parts x G)
-  int sys;                   // partitions on different devices: system-scope ordering
+  int sys;                   // partitions on different devices / processes: system-scope ordering
   int halo;                  // mirrored left-neighbour columns (multiple of 128 B)
-  uint8_t* rows[kMaxParts];  // per partition: [3][C|S][NEG pad | halo | Wp | line]
+  GridPart parts[kMaxParts];
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
@@ -75,7 +84,7 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ int max_shift(const StageShift& sh) {
+__host__ __device__ __forceinline__ int max_shift(const StageShift& sh) {
   return max(max(sh.i, sh.id), max(sh.s, sh.su));
 }
 
@@ -111,12 +120,12 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
   const V NEG = VT<MODE>::neg();
   const V ZERO = V(0);
   auto row_of = [&](int p, int buf, int rs) {
-    return reinterpret_cast<V*>(a.rows[p]) + (int64_t)(buf * 2 + rs) * span + PAD + H;
+    return reinterpret_cast<V*>(a.parts[p].rows) + (int64_t)(buf * 2 + rs) * span + PAD + H;
   };
   auto row = [&](int buf, int rs) { return row_of(part, buf, rs); };
   auto owner = [&](int x) { return min(GT - 1, max(0, x) / B); };  // global CTA of global column x
   // progress counter of global CTA o (in its partition's -- possibly a peer device's -- memory)
-  auto prog_of = [&](int o) { return a.progs[o / G] + (o % G); };
+  auto prog_of = [&](int o) { return a.parts[o / G].prog + (o % G); };
   auto publish = [&](uint32_t v) {
     if (a.sys) {
       __threadfence_system();
@@ -128,13 +137,16 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
       st_release_gpu(prog_of(gq), v);
     }
   };
-  const V* ic = reinterpret_cast<const V*>(a.init_c);
-  const V* is = reinterpret_cast<const V*>(a.init_s);
-  auto init_at = [&](int x, V& c, V& sv) {  // row k_begin at global column x
+  const V* ic = reinterpret_cast<const V*>(a.parts[part].init);
+  const V* il = reinterpret_cast<const V*>(a.parts[part].init_left);
+  auto init_at = [&](int x, V& c, V& sv) {  // row k_begin at global column x (>= p0 - H)
     const bool valid = x >= 0 && x < ncol;
     if (ic) {
-      c = valid ? ic[x] : NEG;
-      sv = valid ? is[x] : NEG;
+      // own columns from this partition's checkpoint, halo columns (x < p0)
+      // from the left neighbour's
+      const V* src = x >= p0 ? ic + (x - p0) : il + (Wp + x - p0);
+      c = valid ? src[0] : NEG;
+      sv = valid ? src[Wp] : NEG;
     } else {
       c = (valid && a.sac) ? ZERO : NEG;
       sv = (valid && !a.sac) ? ZERO : NEG;
@@ -248,7 +260,8 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
       const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
       V* Cn = row((t + 1) % kRowBufs, 0);
       V* Sn = row((t + 1) % kRowBufs, 1);
-      uint32_t* bprow = a.bp ? a.bp + (int64_t)t * a.bp_row_words + warp * bp_words(MODE) : nullptr;
+      uint32_t* bpp = a.parts[part].bp;
+      uint32_t* bprow = bpp ? bpp + (int64_t)t * a.bp_row_words + warp * bp_words(MODE) : nullptr;
       const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
       // every cell of row t+1 below both frontiers is unreachable
       const int64_t next_front = a.reach ? min(min((int64_t)rch.x + sh.i, (int64_t)rch.y + sh.id),
@@ -283,7 +296,7 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
         if (bprow && !dead) {
-          uint32_t* bpc = bprow + (c0g >> 5) * bp_words(MODE);
+          uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);  // local column groups
 #pragma unroll
           for (int e = 0; e < E; ++e) emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f[e], pol);
         }
@@ -311,320 +324,74 @@ __global__ void __launch_bounds__(T + 32, 2) dp_grid_kernel(GridArgs a) {
       if (tid == 0) publish((uint32_t)(t + 2));
     }
     // the range's final row (this CTA's own block: its own writes)
-    if (a.out_c) {
+    if (a.parts[part].out) {
       named_barrier(1, T);
-      V* oc = reinterpret_cast<V*>(a.out_c);
-      V* os = reinterpret_cast<V*>(a.out_s);
+      V* oc = reinterpret_cast<V*>(a.parts[part].out);
       const V* Cf = row(a.k_count % kRowBufs, 0);
       const V* Sf = row(a.k_count % kRowBufs, 1);
-      for (int j = j0 + tid; j < j0 + B && p0 + j < ncol; j += T) {
-        oc[p0 + j] = Cf[j];
-        os[p0 + j] = Sf[j];
+      for (int j = j0 + tid; j < j0 + B; j += T) {
+        oc[j] = Cf[j];
+        oc[Wp + j] = Sf[j];
       }
     }
   }
 }
 
 // End of the forward pass of a grid-solved instance: the end side from the
-// final row's last cell (planner.py:190-200), or the infeasible policy.
-// state = {j, client side, infeasible}.
-// ---------------------------------------------------------------------------
-// K2 grid variant with ONE row buffer (single partition, every stage's
-// shifts <= the halo width): the rows of a 1e7-column instance are 80 MB
-// instead of 240 MB with three buffers, so they stay in L2 instead of
-// streaming through HBM (profiles/r01/dp_grid_ncu_summary.json: 15.5 B/cell
-// of DRAM traffic with three buffers).  Each CTA updates its block IN PLACE,
-// chunks top-down: every predecessor window of chunk c lies below the top of
-// chunk c (reads go left), so the chunks above c that already hold the new
-// row are never read again this stage, and window copies already sit in
-// shared-memory slots before chunk c stores over them.  Nobody else reads the
-// main buffer: the right neighbour takes this block's last `hw` columns from
-// a small per-CTA halo buffer (3 stage slots) written alongside the row.
-// Producer waits per stage: own and left neighbour finished the previous
-// stage (RAW), right neighbour finished the stage two back (WAR on the halo
-// slot this stage overwrites).
-struct GridInplaceArgs {
-  const StageShift* shifts;
-  const int64_t* rv;
-  const int2* reach;
-  int k_begin, k_count;
-  int ncol, G, NC, sac, hw;  // hw: halo columns (multiple of 128 B, <= B)
-  const void* init_c;
-  const void* init_s;
-  void* out_c;
-  void* out_s;
-  uint32_t* bp;
-  int64_t bp_row_words;
-  uint32_t* prog;  // [G] completed stages + 1 (zeroed)
-  uint8_t* rows;   // [C|S][PAD | G*B | line]
-  uint8_t* halo;   // [G][3][C|S][hw]
-  int row_hint;    // 1: row stores with an L2 evict_last policy (SPLITPLAN_ROW_EVICT_LAST)
-};
-
-template <int MODE, int T, int E, int NSLOT>
-__global__ void __launch_bounds__(T + 32, 2) dp_grid_inplace_kernel(GridInplaceArgs a) {
-  using V = typename VT<MODE>::T;
-  constexpr int CH = T * E;
-  constexpr int AL = 16 / (int)sizeof(V);
-  constexpr int WIN = CH + AL;
-  constexpr int PAD = stream_pad<V, CH>();
-  constexpr int LINE = 128 / (int)sizeof(V);
-  constexpr int NWARP = T / 32;
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + NSLOT;
-  V* slots = reinterpret_cast<V*>(smem + 256);
-  V* negwin = slots + NSLOT * 4 * WIN;  // [WIN] of NEG: windows below the reachable frontier
-
-  const int G = a.G, NC = a.NC;
-  const int q = (int)blockIdx.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int B = NC * CH;
-  const int Wt = G * B;
-  const int j0 = q * B;
-  const int ncol = a.ncol, hw = a.hw;
-  const int64_t span = (int64_t)PAD + Wt + LINE;
-  const V NEG = VT<MODE>::neg();
-  const V ZERO = V(0);
-  V* const Cm = reinterpret_cast<V*>(a.rows) + PAD;          // C row, column 0
-  V* const Sm = reinterpret_cast<V*>(a.rows) + span + PAD;   // S row, column 0
-  // halo of CTA o, stage slot t % 3: columns [o*B + B - hw, o*B + B) of row t
-  auto halo = [&](int o, int slot, int rs) {
-    return reinterpret_cast<V*>(a.halo) + ((int64_t)(o * 3 + slot) * 2 + rs) * hw;
-  };
-  const V* ic = reinterpret_cast<const V*>(a.init_c);
-  const V* is = reinterpret_cast<const V*>(a.init_s);
-
-  // row k_begin in the main buffer, its top hw columns in halo slot 0, NEG pads
-  for (int x = j0 + tid; x < j0 + B; x += blockDim.x) {
-    const bool valid = x < ncol;
-    V c, s;
-    if (ic) {
-      c = valid ? ic[x] : NEG;
-      s = valid ? is[x] : NEG;
-    } else {
-      c = (valid && a.sac) ? ZERO : NEG;
-      s = (valid && !a.sac) ? ZERO : NEG;
-    }
-    Cm[x] = c;
-    Sm[x] = s;
-    if (x >= j0 + B - hw) {
-      halo(q, 0, 0)[x - (j0 + B - hw)] = c;
-      halo(q, 0, 1)[x - (j0 + B - hw)] = s;
-    }
-  }
-  if (q == 0)
-    for (int x = tid - PAD; x < 0; x += blockDim.x) Cm[x] = Sm[x] = NEG;
-  if (q == G - 1)
-    for (int x = Wt + tid; x < Wt + LINE; x += blockDim.x) Cm[x] = Sm[x] = NEG;
-  for (int x = tid; x < WIN; x += blockDim.x) negwin[x] = NEG;
-  if (tid == 0) {
-    for (int b = 0; b < NSLOT; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], NWARP);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    fence_proxy_async_global();
-    st_release_gpu(&a.prog[q], 1u);
-  }
-
-  if (warp == NWARP) {
-    // ---------------- producer warp ----------------
-    uint32_t u = 0;
-    for (int t = 0; t < a.k_count; ++t) {
-      const StageShift sh = a.shifts[a.k_begin + t];
-      // lane 0: own block (row t complete), lane 1: left neighbour (its halo
-      // of row t), lane 2: right neighbour (finished stage t - 2: halo slot reuse)
-      const int o = lane == 0 ? q : (lane == 1 ? q - 1 : q + 1);
-      const bool watch = lane < 3 && o >= 0 && o < G;
-      const uint32_t need = lane < 2 ? (uint32_t)(t + 1) : (uint32_t)max(t - 1, 0) + 1u;
-      const long long t0 = clock64();
-      for (uint32_t it = 1;; ++it) {
-        if (__all_sync(0xffffffffu, !watch || ld_acquire_gpu(&a.prog[o]) >= need)) break;
-        if ((it & 1023u) == 0 && clock64() - t0 > (30ll << 30)) __trap();
-      }
-      if (lane == 0) {
-        fence_proxy_async_global();
-        const V* hc = q > 0 ? halo(q - 1, t % 3, 0) - (j0 - hw) : nullptr;  // index by global column
-        const V* hs = q > 0 ? halo(q - 1, t % 3, 1) - (j0 - hw) : nullptr;
-        const int shf[4] = {sh.i, sh.id, sh.s, sh.su};
-        const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
-        const int mrow[4] = {rch.x, rch.y, rch.y, rch.x};
-        for (int c = NC - 1; c >= 0; --c, ++u) {
-          const int slot = (int)(u % NSLOT);
-          mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
-          const int c0 = j0 + c * CH, ctop = c0 + CH;
-          uint32_t ncopy = 0;
-#pragma unroll
-          for (int w = 0; w < 4; ++w) ncopy += c0 - min(shf[w], ctop) + CH > mrow[w] ? 1u : 0u;
-          mbar_expect_tx(&full[slot], ncopy * WIN * sizeof(V));
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const bool cw = w == 0 || w == 3;
-            const int start = c0 - min(shf[w], ctop);
-            if (start + CH <= mrow[w]) continue;  // below the reachable frontier: all NEG, no copy
-            V* dst = slots + (slot * 4 + w) * WIN;
-            if (q == 0 || start < 0) {  // partition start: NEG pad in front of column 0
-              const int sa = start < 0 && q > 0 ? -PAD : (start & ~(AL - 1));
-              bulk_g2s(dst, (cw ? Cm : Sm) + sa, WIN * sizeof(V), &full[slot]);
-              continue;
-            }
-            const int sa = start & ~(AL - 1);
-            const int split = min(max(j0 - sa, 0), WIN);  // values from the left halo
-            if (split > 0)
-              bulk_g2s(dst, (cw ? hc : hs) + sa, split * sizeof(V), &full[slot]);
-            if (split < WIN)
-              bulk_g2s(dst + split, (cw ? Cm : Sm) + sa + split, (WIN - split) * sizeof(V), &full[slot]);
-          }
-        }
-      }
-      __syncwarp();
-    }
-  } else {
-    // ---------------- compute warps ----------------
-    const uint64_t pol = evict_first_policy();
-    const uint64_t rpol = evict_last_policy();
-    uint32_t u = 0;
-    StageShift sh_next = a.shifts[a.k_begin];
-    int64_t rbits_next = a.rv[a.k_begin];
-    const int hlo = j0 + B - hw;  // first column mirrored into this CTA's halo
-    for (int t = 0; t < a.k_count; ++t) {
-      const StageShift sh = sh_next;
-      const int64_t rbits = rbits_next;
-      if (t + 1 < a.k_count) {
-        sh_next = a.shifts[a.k_begin + t + 1];
-        rbits_next = a.rv[a.k_begin + t + 1];
-      }
-      const V rk = MODE == VM_INT32 ? (V)(int32_t)rbits : (V)__longlong_as_double(rbits);
-      V* const hc = halo(q, (t + 1) % 3, 0) - hlo;
-      V* const hs = halo(q, (t + 1) % 3, 1) - hlo;
-      uint32_t* bprow = a.bp ? a.bp + (int64_t)t * a.bp_row_words + warp * bp_words(MODE) : nullptr;
-      const int2 rch = a.reach ? a.reach[a.k_begin + t] : make_int2(0, 0);
-      const int64_t next_front = a.reach ? min(min((int64_t)rch.x + sh.i, (int64_t)rch.y + sh.id),
-                                               min((int64_t)rch.y + sh.s, (int64_t)rch.x + sh.su))
-                                         : 0;
-      for (int c = NC - 1; c >= 0; --c, ++u) {
-        const int slot = (int)(u % NSLOT);
-        const int c0 = j0 + c * CH, ctop = c0 + CH;
-        const int sa = c0 - min(sh.i, ctop), sb = c0 - min(sh.id, ctop);
-        const int sc = c0 - min(sh.s, ctop), sd = c0 - min(sh.su, ctop);
-        const V* ws = slots + slot * 4 * WIN + tid;
-        const V* pca = (sa + CH > rch.x ? ws + 0 * WIN : negwin + tid) + (sa & (AL - 1));
-        const V* pcb = (sb + CH > rch.y ? ws + 1 * WIN : negwin + tid) + (sb & (AL - 1));
-        const V* psa = (sc + CH > rch.y ? ws + 2 * WIN : negwin + tid) + (sc & (AL - 1));
-        const V* psb = (sd + CH > rch.x ? ws + 3 * WIN : negwin + tid) + (sd & (AL - 1));
-        mbar_wait(&full[slot], (u / NSLOT) & 1);
-        V cn[E], sn[E];
-        CellFlags f[E];
-        const bool dead = (int64_t)ctop <= next_front;  // whole chunk unreachable: NEG, no back-pointers
-        if (dead) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) cn[e] = sn[e] = NEG;
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int j = c0 + e * T + tid;
-            f[e] = cell_update<MODE, V>(pca[e * T], pcb[e * T], psa[e * T], psb[e * T], rk, j >= sh.i,
-                                        j >= sh.id, j >= sh.s, j >= sh.su, cn[e], sn[e]);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        if (bprow && !dead) {
-          uint32_t* bpc = bprow + (c0 >> 5) * bp_words(MODE);
-#pragma unroll
-          for (int e = 0; e < E; ++e) emit_bp_stream<MODE>(bpc + e * (T / 32) * bp_words(MODE), f[e], pol);
-        }
-        V* qc = Cm + c0 + tid;
-        V* qs = Sm + c0 + tid;
-        if (a.row_hint) {  // keep the rows ahead of the streamed back-pointers in L2
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            st_hint(qc + e * T, cn[e], rpol);
-            st_hint(qs + e * T, sn[e], rpol);
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            qc[e * T] = cn[e];
-            qs[e * T] = sn[e];
-          }
-        }
-        if (ctop > hlo) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int j = c0 + e * T + tid;
-            if (j >= hlo) {
-              hc[j] = cn[e];
-              hs[j] = sn[e];
-            }
-          }
-        }
-      }
-      named_barrier(1, T);
-      if (tid == 0) {
-        __threadfence();
-        fence_proxy_async_global();
-        st_release_gpu(&a.prog[q], (uint32_t)(t + 2));
-      }
-    }
-    if (a.out_c) {
-      named_barrier(1, T);
-      V* oc = reinterpret_cast<V*>(a.out_c);
-      V* os = reinterpret_cast<V*>(a.out_s);
-      for (int j = j0 + tid; j < j0 + B && j < ncol; j += T) {
-        oc[j] = Cm[j];
-        os[j] = Sm[j];
-      }
-    }
-  }
-}
-
-__global__ void grid_end_kernel(sp_instances in, InstInfo* info, int64_t inst, const void* last_c,
-                                const void* last_s, int64_t* state) {
-  const InstInfo inf = info[inst];
-  const int64_t jl = inf.w_eff;
+// final row's last cell (planner.py:190-200), read from the checkpoint of
+// the partition owning column W_eff (`last`: its C row then S row, Wp values
+// each), or the infeasible policy.  state = {j, client side, flag (0 ok,
+// 1 infeasible, 2 backtrace error), next stage to decide}.
+__global__ void grid_end_kernel(InstInfo* info, int64_t p0, int64_t Wp, int L, int must_val,
+                                const int8_t* must_ptr, const void* last, int64_t* state) {
+  const InstInfo inf = *info;
+  const int64_t jl = inf.w_eff - p0;  // local column in the owning partition
   double ec, es;
   if (inf.mode == VM_INT32) {
-    ec = to_f64(reinterpret_cast<const int32_t*>(last_c)[jl], inf.scale);
-    es = to_f64(reinterpret_cast<const int32_t*>(last_s)[jl], inf.scale);
+    ec = to_f64(reinterpret_cast<const int32_t*>(last)[jl], inf.scale);
+    es = to_f64(reinterpret_cast<const int32_t*>(last)[Wp + jl], inf.scale);
   } else {
-    ec = reinterpret_cast<const double*>(last_c)[jl];
-    es = reinterpret_cast<const double*>(last_s)[jl];
+    ec = reinterpret_cast<const double*>(last)[jl];
+    es = reinterpret_cast<const double*>(last)[Wp + jl];
   }
-  info[inst].end_c = ec;
-  info[inst].end_s = es;
-  const int8_t must = in.must_end_at ? in.must_end_at[inst] : (int8_t)-1;
+  info->end_c = ec;
+  info->end_s = es;
+  const int must = must_ptr ? (int)*must_ptr : must_val;
   if (must == 1) es = -INFINITY;
   else if (must == 0) ec = -INFINITY;
   const double pmax = (es > ec) ? es : ec;
-  state[0] = jl;
+  state[0] = inf.w_eff;
   state[1] = ec >= es ? 1 : 0;
   state[2] = pmax == -INFINITY ? 1 : 0;
+  state[3] = L - 1;
 }
 
-// Walk one segment of back-pointers (stages k_begin + k_count - 1 .. k_begin)
-// from state {j, side}, writing pi; the same decisions as backtrack_kernel.
-__global__ void grid_backtrack_kernel(sp_instances in, int64_t inst, const StageShift* shifts,
-                                      const uint32_t* bp, int64_t row_words, int mode, int k_begin,
-                                      int k_count, int64_t* state, sp_policies out) {
-  const int64_t lo = in.layer_off[inst];
+// Walk the back-pointers of ONE capacity partition (global columns
+// [p0, p0 + Wp)) through one segment of stages [k_begin, k_begin + k_count),
+// from state {j, side, flag, next stage k}, writing pi[k] (stage-indexed).
+// The walk stops when j leaves the partition to the left -- the state is
+// then handed to the left neighbour, which continues from stage k -- or at
+// the segment's first stage.  j never grows, so one pass over the partitions
+// from right to left finishes a segment.  Same decisions as backtrack_kernel
+// (planner.py:146-179).  bp: this partition's back-pointers of the segment,
+// stage rows of row_words u32 over local columns.
+__global__ void grid_backtrack_part_kernel(const StageShift* shifts, const uint32_t* bp, int64_t row_words,
+                                           int mode, int k_begin, int k_count, int64_t p0, int64_t* state,
+                                           uint8_t* pi) {
+  if (state[2] != 0) return;  // infeasible or failed: nothing to walk
   int64_t j = state[0];
   bool client = state[1] != 0;
+  int k = (int)state[3];
   const int nw = bp_words(mode);
-  uint8_t* pi = out.pi + lo;
-  for (int t = k_count - 1; t >= 0; --t) {
-    const int k = k_begin + t;
-    const uint32_t* grp = bp + (int64_t)t * row_words + (j >> 5) * nw;
-    const uint32_t bit = 1u << (j & 31);
+  for (; k >= k_begin && j >= p0; --k) {
+    const int t = k - k_begin;
+    const int64_t jl = j - p0;
+    const uint32_t* grp = bp + (int64_t)t * row_words + (jl >> 5) * nw;
+    const uint32_t bit = 1u << (jl & 31);
     const bool c_stay = grp[0] & bit, s_stay = grp[1] & bit;
     const bool c_sw = nw == 4 ? (grp[2] & bit) != 0 : !c_stay;
     const bool s_sw = nw == 4 ? (grp[3] & bit) != 0 : !s_stay;
-    const StageShift sh = shifts[lo + k];
+    const StageShift sh = shifts[k];
     if (client) {
       pi[k] = 1;
       if (c_stay) {
@@ -633,7 +400,6 @@ __global__ void grid_backtrack_kernel(sp_instances in, int64_t inst, const Stage
         j -= sh.id;
         client = false;
       } else {
-        out.status[inst] = SP_ERR_BACKTRACE;
         state[2] = 2;
         return;
       }
@@ -645,7 +411,6 @@ __global__ void grid_backtrack_kernel(sp_instances in, int64_t inst, const Stage
         j -= sh.su;
         client = true;
       } else {
-        out.status[inst] = SP_ERR_BACKTRACE;
         state[2] = 2;
         return;
       }
@@ -653,6 +418,7 @@ __global__ void grid_backtrack_kernel(sp_instances in, int64_t inst, const Stage
   }
   state[0] = j;
   state[1] = client ? 1 : 0;
+  state[3] = k;
 }
 
 // ---------------------------------------------------------------------------
@@ -695,7 +461,10 @@ __global__ void grid_finish_kernel(sp_instances in, int64_t inst, const int64_t*
                                    int32_t* idx_scratch, sp_policies out) {
   const int64_t lo = in.layer_off[inst];
   const int L = (int)(in.layer_off[inst + 1] - lo);
-  if (state[2] == 2) return;  // status already set
+  if (state[2] == 2) {  // planner.py:168-169 / 177-178 AssertionError
+    out.status[inst] = SP_ERR_BACKTRACE;
+    return;
+  }
   if (state[2] == 1)
     for (int k = 0; k < L; ++k) out.pi[lo + k] = 0;
   finish_policy(in, inst, lo, L, idx_scratch + lo, out, state[2] == 1, false);

@@ -10,6 +10,7 @@
 namespace {
 thread_local char g_err[1024] = "";
 thread_local size_t g_required_ws = 0;
+thread_local size_t g_full_ws = 0;
 
 struct DpRec {
   cudaEvent_t a, b;
@@ -44,6 +45,7 @@ int launch_check(const char* what) {
 }
 
 void set_required_workspace(size_t bytes) { g_required_ws = bytes; }
+void set_full_workspace(size_t bytes) { g_full_ws = bytes; }
 
 bool profiling() { return g_prof; }
 
@@ -94,5 +96,7 @@ int sp_abi_version(void) { return SP_ABI_VERSION; }
 const char* sp_last_error(void) { return g_err; }
 
 size_t sp_last_required_workspace(void) { return g_required_ws; }
+
+size_t sp_last_full_workspace(void) { return g_full_ws; }
 
 }  // extern "C"

@@ -5,10 +5,9 @@
 //                      dp_stage_kernel: K2 with rows in one CTA's SMEM
 //                      (planner.py:128-143), 2-bit packed back-pointers
 //   dp_stream.cuh      K2 for wide rows: dp_stream_kernel (L2 rows, bulk-copy
-//                      windows), dp_own_kernel (experiment)
-//   dp_grid.cuh        K2 for one huge instance (cfg5): dp_grid_kernel,
-//                      dp_grid_inplace_kernel, checkpoint/backtrack kernels
-//   dp_cluster_coop.cuh  forced-only K2 variants (parity coverage)
+//                      windows)
+//   dp_grid.cuh        K2 for one huge instance (cfg5): dp_grid_kernel over
+//                      capacity partitions, checkpoint/backtrack kernels
 //   this file          backtrack_kernel (K3: end-side choice + pointer walk +
 //                      _finish, planner.py:88-107, 146-202), prefix_kernel
 //                      (greedy / all-server / all-client, planner.py:205-225),
@@ -30,16 +29,12 @@ namespace sp {
 namespace {
 
 constexpr int kStageTile = 128;          // stage records staged in SMEM at a time
-constexpr int kCellsPerThread = 4;       // E: columns per thread per chunk
-constexpr int kMaxThreads = 1024;
-constexpr int kStageThreads = 512;     // single-CTA DP kernels: 2 CTAs per SM
 constexpr size_t kSmemCap = 227 * 1024;  // sm_100a max dynamic SMEM per CTA
 constexpr int64_t kMaxCols = (int64_t(1) << 31) - 64;
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 #include "dp_core.cuh"
-#include "dp_cluster_coop.cuh"
 #include "dp_stream.cuh"
 #include "dp_grid.cuh"
 
@@ -361,7 +356,7 @@ size_t stage_bytes_mode(int mode) {
   return align_up(kStageTile * (sizeof(StageShift) + value_bytes(mode)), 16);
 }
 
-enum DpVariant { DPV_SMEM = 0, DPV_CLUSTER = 1, DPV_GLOBAL = 2, DPV_COOP = 3, DPV_STREAM = 4, DPV_OWN = 6 };
+enum DpVariant { DPV_SMEM = 0, DPV_GLOBAL = 2, DPV_STREAM = 4 };
 
 // ---- single-CTA kernels: T x E configurations ------------------------------
 
@@ -466,26 +461,11 @@ int64_t stream_span(int mode, const StreamGeom& g) {
   const int64_t line = 128 / (int64_t)value_bytes(mode);
   return (stream_ch(g.cfg) + line) + (int64_t)g.G * g.NC * stream_ch(g.cfg) + line;
 }
-// row buffers of the streaming kernel: 2 (full-barrier semantics, default:
-// 2/3 of the L2 footprint lets G shrink to 5 at W = 1e5, measured 4.5e11 vs
-// 4.4e11 cells/s with 3) or 3 (one stage of slack); SPLITPLAN_STREAM_BUFS
-int stream_bufs() {
-  static int b = 0;
-  if (!b) b = env_int("SPLITPLAN_STREAM_BUFS", 2) == 3 ? 3 : 2;
-  return b;
-}
+// row buffers of the streaming kernel (profiles/r01/bufs_experiment: three
+// buffers, one stage of slack, measured no faster: the L2 footprint grows by half)
+constexpr int kStreamBufs = 2;
 size_t stream_row_bytes(int mode, const StreamGeom& g) {
-  return 2 * (size_t)stream_bufs() * (size_t)stream_span(mode, g) * value_bytes(mode);
-}
-
-// instances per cluster of the streaming kernel (1 or 2; SPLITPLAN_STREAM_PAIR,
-// 256 x 4 only).  Pairs were measured slower on B200 (3.4-4.1e11 vs 4.4e11
-// cells/s at W = 1e5: the doubled L2 footprint costs more than the hidden
-// stage latency saves).
-int stream_pair() {
-  static int p = 0;
-  if (!p) p = env_int("SPLITPLAN_STREAM_PAIR", 1) == 2 ? 2 : 1;
-  return p;
+  return 2 * (size_t)kStreamBufs * (size_t)stream_span(mode, g) * value_bytes(mode);
 }
 
 template <int MODE, int T, int E, int NSLOT>
@@ -530,11 +510,10 @@ int stream_resident_ctas(int mode, int cfg) {
 }
 
 // Cluster size for one configuration: at least large enough that the rows of
-// every co-resident instance (stream_pair() per cluster) fit the L2 budget;
-// among those, the G minimising G * (NC * CH + sync) -- the CTA-time of one
-// stage in columns, padding waste included, plus the stage-synchronisation
-// latency per CTA (about 4096 columns for single instances, measured on
-// B200; paired instances hide most of it behind the partner's stage).
+// every co-resident instance fit the L2 budget; among those, the G
+// minimising G * (NC * CH + sync) -- the CTA-time of one stage in columns,
+// padding waste included, plus the stage-synchronisation latency per CTA
+// (about 4096 columns, measured on B200).
 // Returns the geometry and its cost.
 StreamGeom stream_geom_cfg(int mode, int64_t ncol, int cfg, int64_t* cost) {
   const int64_t ch = stream_ch(cfg);
@@ -546,8 +525,7 @@ StreamGeom stream_geom_cfg(int mode, int64_t ncol, int cfg, int64_t* cost) {
     t.G = (int)((nchunks + t.NC - 1) / t.NC);
     return t;
   };
-  const int pair = cfg == 0 ? stream_pair() : 1;
-  const int64_t sync = pair == 2 ? 0 : 4096;
+  const int64_t sync = 4096;
   auto cost_of = [&](const StreamGeom& t) { return (int64_t)t.G * ((int64_t)t.NC * ch + sync); };
   if (force >= 1 && force <= 16) {
     const StreamGeom t = geom(force);
@@ -556,7 +534,7 @@ StreamGeom stream_geom_cfg(int mode, int64_t ncol, int cfg, int64_t* cost) {
   }
   int gmin = 16;
   for (int G = 1; G <= 16; ++G)
-    if ((size_t)(resident / G) * pair * stream_row_bytes(mode, geom(G)) <= l2_row_budget()) {
+    if ((size_t)(resident / G) * stream_row_bytes(mode, geom(G)) <= l2_row_budget()) {
       gmin = G;
       break;
     }
@@ -614,228 +592,16 @@ int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t
   if (MODE == VM_INT32 && geo.cfg == 4) return launch_stream_t<MODE, 256, 6, 4, 1, 2>(a, n_items, geo, st);
   if (MODE == VM_INT32 && geo.cfg == 2) return launch_stream_t<MODE, 128, 8, 6, 1, 2>(a, n_items, geo, st);
   constexpr int NS = MODE == VM_INT32 ? 6 : 3;
-  const int sel = (stream_pair() == 2 ? 1 : 0) + (stream_bufs() == 2 ? 2 : 0);
-  switch (sel) {
-    case 0: return launch_stream_t<MODE, 256, 4, NS, 1, 3>(a, n_items, geo, st);
-    case 1: return launch_stream_t<MODE, 256, 4, NS, 2, 3>(a, n_items, geo, st);
-    case 2: return launch_stream_t<MODE, 256, 4, NS, 1, 2>(a, n_items, geo, st);
-    default: return launch_stream_t<MODE, 256, 4, NS, 2, 2>(a, n_items, geo, st);
-  }
-}
-
-// ---- own-block kernel (int32 rows in the cluster's shared memory) ----------
-
-struct OwnCfg {
-  int T, E, NSW;
-};
-constexpr OwnCfg kOwnCfgs[] = {{512, 4, 8}, {256, 8, 8}, {256, 4, 8}};
-int own_cfg_index() {
-  const int c = env_int("SPLITPLAN_OWN_CFG", 0);
-  return c < 0 || c > 2 ? 0 : c;
-}
-// CTAs per SM the own-block geometry is sized for (SPLITPLAN_OWN_OCC 1 or 2)
-size_t own_smem_budget() {
-  return env_int("SPLITPLAN_OWN_OCC", 1) == 2 ? (size_t)113 * 1024 : kSmemCap;
-}
-// global row buffers (3: one stage of slack for the wavefront; SPLITPLAN_OWN_BUFS 2..4)
-int own_bufs() { return std::min(4, std::max(2, env_int("SPLITPLAN_OWN_BUFS", 3))); }
-int64_t own_ch() { return (int64_t)kOwnCfgs[own_cfg_index()].T * kOwnCfgs[own_cfg_index()].E; }
-size_t own_smem(int mode, int NC) {
-  const size_t vb = value_bytes(mode);
-  const int64_t ch = own_ch();
-  return 256 + (size_t)(2 * (ch + NC * ch) + kOwnCfgs[own_cfg_index()].NSW * (ch + 16 / (int64_t)vb)) * vb;
-}
-// cluster geometry: the fewest CTAs whose blocks fit shared memory (G = 0: not possible)
-StreamGeom own_geom(int mode, int64_t ncol) {
-  StreamGeom g{0, 0, 0, 0, 0};
-  if (mode != VM_INT32) return g;
-  const int64_t nchunks = (ncol + own_ch() - 1) / own_ch();
-  int ncmax = 0;
-  while (own_smem(mode, ncmax + 1) <= own_smem_budget()) ++ncmax;
-  if (ncmax < 1) return g;
-  int G = (int)((nchunks + ncmax - 1) / ncmax);
-  const int force = env_int("SPLITPLAN_DP_CLUSTER", 0);
-  if (force >= 1 && force <= 16) G = std::max(G, force);
-  if (G > 16) return g;
-  const int NC = (int)((nchunks + G - 1) / G);
-  g.G = (int)((nchunks + NC - 1) / NC);
-  g.NC = NC;
-  return g;
-}
-int64_t own_span(int mode, const StreamGeom& g) {
-  const int64_t line = 128 / (int64_t)value_bytes(mode);
-  return (own_ch() + line) + (int64_t)g.G * g.NC * own_ch() + line;
-}
-size_t own_row_bytes(int mode, const StreamGeom& g) {
-  return 2 * (size_t)own_bufs() * (size_t)own_span(mode, g) * value_bytes(mode);
-}
-
-template <int MODE, int T, int E, int NSW, int NBUF>
-int launch_own_t(const DpArgs& a, int64_t n_items, StreamGeom sg, size_t smem, cudaStream_t st) {
-  auto kern = dp_own_kernel<MODE, T, E, NSW, NBUF>;
-  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                      "cudaFuncSetAttribute(dp_own_kernel)");
-  if (rc) return rc;
-  if (sg.G > 8) {
-    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                    "cudaFuncSetAttribute(non-portable cluster)");
-    if (rc) return rc;
-  }
-  OwnGeom geo{sg.G, sg.NC, (int)n_items, 0};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(n_items * sg.G), 1, 1);
-  cfg.blockDim = dim3((unsigned)(T + 64), 1, 1);  // + producer and publisher warps
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)sg.G;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, a, geo), "dp_own_kernel launch");
-  if (rc) return rc;
-  return launch_check("dp_own_kernel launch");
-}
-int launch_own(int mode, const DpArgs& a, int64_t n_items, StreamGeom sg, size_t smem, cudaStream_t st) {
-  if (mode != VM_INT32) return check_cuda(cudaErrorInvalidValue, "dp_own_kernel: int32 domain only");
-  const int sel = own_cfg_index() * 3 + (own_bufs() - 2);
-  switch (sel) {
-    case 6: return launch_own_t<VM_INT32, 256, 4, 8, 2>(a, n_items, sg, smem, st);
-    case 7: return launch_own_t<VM_INT32, 256, 4, 8, 3>(a, n_items, sg, smem, st);
-    case 8: return launch_own_t<VM_INT32, 256, 4, 8, 4>(a, n_items, sg, smem, st);
-    case 0: return launch_own_t<VM_INT32, 512, 4, 8, 2>(a, n_items, sg, smem, st);
-    case 1: return launch_own_t<VM_INT32, 512, 4, 8, 3>(a, n_items, sg, smem, st);
-    case 2: return launch_own_t<VM_INT32, 512, 4, 8, 4>(a, n_items, sg, smem, st);
-    case 3: return launch_own_t<VM_INT32, 256, 8, 8, 2>(a, n_items, sg, smem, st);
-    case 4: return launch_own_t<VM_INT32, 256, 8, 8, 3>(a, n_items, sg, smem, st);
-    case 5: return launch_own_t<VM_INT32, 256, 8, 8, 4>(a, n_items, sg, smem, st);
-    default: return launch_own_t<VM_INT32, 512, 4, 8, 3>(a, n_items, sg, smem, st);
-  }
-}
-
-// ---- cluster (DSMEM rows) and cooperative (L2 rows, LDG) kernels ------------
-
-template <int MODE>
-int launch_cluster(const DpArgs& a, int64_t n_items, int threads, size_t smem, ClusterGeom geo,
-                   cudaStream_t st) {
-  auto kern = dp_cluster_kernel<MODE>;
-  // the kernel also has a little static SMEM, so ask for exactly what it uses
-  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem),
-                      "cudaFuncSetAttribute(dp_cluster_kernel)");
-  if (rc) return rc;
-  if (geo.G > 8) {
-    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                    "cudaFuncSetAttribute(non-portable cluster)");
-    if (rc) return rc;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(n_items * geo.G), 1, 1);
-  cfg.blockDim = dim3((unsigned)threads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)geo.G;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, a, geo), "dp_cluster_kernel launch");
-  if (rc) return rc;
-  return launch_check("dp_cluster_kernel launch");
-}
-
-template <int MODE>
-int launch_coop(const DpArgs& a, int64_t n_items, int threads, size_t smem, ClusterGeom geo,
-                cudaStream_t st) {
-  auto kern = dp_coop_kernel<MODE, kCellsPerThread>;
-  int rc = SP_OK;
-  if (geo.G > 8) {
-    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                    "cudaFuncSetAttribute(non-portable cluster)");
-    if (rc) return rc;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(n_items * geo.G), 1, 1);
-  cfg.blockDim = dim3((unsigned)threads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)geo.G;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, a, geo), "dp_coop_kernel launch");
-  if (rc) return rc;
-  return launch_check("dp_coop_kernel launch");
-}
-
-// cooperative geometry: enough CTAs per instance that the double-buffered
-// rows of every co-resident instance fit comfortably in L2
-ClusterGeom coop_geom(int mode, int64_t ncol) {
-  const size_t vb = value_bytes(mode);
-  const size_t l2_budget = (size_t)48 << 20;
-  const int resident_ctas = 148 * 2;
-  int G = 2;
-  for (; G < 16; G *= 2) {
-    const int64_t B = ((ncol + G - 1) / G + 31) / 32 * 32;
-    const int64_t t = std::min<int64_t>(kStageThreads, std::max<int64_t>(32, ((B + 3) / 4 + 31) / 32 * 32));
-    const size_t per_inst = 4 * (size_t)(kCellsPerThread * t + ncol) * vb;
-    if ((size_t)(resident_ctas / G) * per_inst <= l2_budget) break;
-  }
-  ClusterGeom geo;
-  geo.G = G;
-  geo.B = (int)(((ncol + G - 1) / G + 31) / 32 * 32);
-  geo.magic = 0;
-  return geo;
-}
-
-int coop_threads(const ClusterGeom& geo) {
-  return (int)std::min<int64_t>(kStageThreads,
-                                std::max<int64_t>(32, ((geo.B + 3) / 4 + 31) / 32 * 32));
-}
-
-size_t coop_row_bytes(int mode, int64_t ncol, const ClusterGeom& geo) {
-  return 4 * (size_t)(kCellsPerThread * coop_threads(geo) + ncol) * value_bytes(mode);
-}
-
-// cluster geometry for one instance, or G == 0 if the rows do not fit on chip
-ClusterGeom cluster_geom(int mode, int64_t ncol) {
-  ClusterGeom geo{0, 0, 0};
-  const size_t vb = value_bytes(mode);
-  const size_t room = kSmemCap - stage_bytes_mode(mode) - 1024;  // 1 KB for static SMEM
-  const size_t per_col = 4 * vb;  // 2 buffers x (C, S)
-  int G = (int)((ncol * per_col + room - 1) / room);
-  G = std::max(G, 2);
-  if (G > 16) return geo;
-  // B: a multiple of 32 so every warp's columns form one packed back-pointer group
-  const int64_t B = ((ncol + G - 1) / G + 31) / 32 * 32;
-  if ((size_t)B * per_col > room) return geo;
-  const uint64_t magic = ((uint64_t)1 << 32) / (uint64_t)B + 1;
-  // umulhi(x, magic) == x / B for all x < N whenever N * B < 2^32
-  // (magic * B - 2^32 <= B, so the error term x * that / 2^32 stays below 1/B)
-  if ((uint64_t)G * (uint64_t)B * (uint64_t)B >= ((uint64_t)1 << 32)) return geo;
-  geo.G = G;
-  geo.B = (int)B;
-  geo.magic = (uint32_t)magic;
-  return geo;
+  return launch_stream_t<MODE, 256, 4, NS, 1, kStreamBufs>(a, n_items, geo, st);
 }
 
 int forced_variant() {
   const char* v = getenv("SPLITPLAN_DP_VARIANT");
   if (!v) return -1;
   if (!strcmp(v, "smem")) return DPV_SMEM;
-  if (!strcmp(v, "cluster")) return DPV_CLUSTER;
   if (!strcmp(v, "global")) return DPV_GLOBAL;
-  if (!strcmp(v, "coop")) return DPV_COOP;
   if (!strcmp(v, "stream")) return DPV_STREAM;
   if (!strcmp(v, "grid")) return 5;  // DPV_GRID
-  if (!strcmp(v, "own")) return DPV_OWN;
   return -1;
 }
 
@@ -845,14 +611,13 @@ struct DpPlan {
   int variant = DPV_SMEM;
   int cfg = 0;                  // single-CTA T x E configuration
   int threads = 0;
-  ClusterGeom cgeo{0, 0, 0};    // cluster / coop
   StreamGeom sgeo{0, 0, 0, 0};  // stream
   size_t bp = 0, rows = 0, smem = 0;
   int64_t bp_row_words = 0;
   // launches sharing a key go out together
   bool same_launch(const DpPlan& o) const {
-    return variant == o.variant && cfg == o.cfg && threads == o.threads && cgeo.G == o.cgeo.G &&
-           cgeo.B == o.cgeo.B && sgeo.G == o.sgeo.G && sgeo.NC == o.sgeo.NC && sgeo.cfg == o.sgeo.cfg;
+    return variant == o.variant && cfg == o.cfg && threads == o.threads && sgeo.G == o.sgeo.G &&
+           sgeo.NC == o.sgeo.NC && sgeo.cfg == o.sgeo.cfg;
   }
 };
 
@@ -864,11 +629,8 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) 
   const bool fits_cta = single_rows + stage_bytes_mode(mode) <= kSmemCap;
   if (force == DPV_GLOBAL || (tables && force < 0)) p.variant = DPV_GLOBAL;
   else if (force == DPV_SMEM && fits_cta) p.variant = DPV_SMEM;
-  else if (force == DPV_CLUSTER && cluster_geom(mode, ncol).G) p.variant = DPV_CLUSTER;
-  else if (force == DPV_COOP) p.variant = DPV_COOP;
   else if (force == DPV_STREAM) p.variant = DPV_STREAM;
-  else if (force == DPV_OWN && own_geom(mode, ncol).G) p.variant = DPV_OWN;
-  else if (fits_cta && force != DPV_CLUSTER) p.variant = DPV_SMEM;
+  else if (fits_cta) p.variant = DPV_SMEM;
   else p.variant = DPV_STREAM;
 
   switch (p.variant) {
@@ -886,27 +648,6 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) 
       p.rows = align_up(stream_row_bytes(mode, p.sgeo), 256);
       p.smem = stream_smem(mode, p.sgeo.cfg);
       break;
-    case DPV_OWN:
-      p.sgeo = own_geom(mode, ncol);
-      p.threads = kOwnCfgs[own_cfg_index()].T;
-      p.bp_row_words = bp_row_words_for(mode, (int64_t)p.sgeo.G * p.sgeo.NC * own_ch());
-      p.rows = align_up(own_row_bytes(mode, p.sgeo), 256);
-      p.smem = own_smem(mode, p.sgeo.NC);
-      break;
-    case DPV_COOP:
-      p.cgeo = coop_geom(mode, ncol);
-      p.threads = coop_threads(p.cgeo);
-      p.bp_row_words = bp_row_words_for(mode, ncol);
-      p.rows = align_up(coop_row_bytes(mode, ncol, p.cgeo), 256);
-      p.smem = stage_bytes_mode(mode);
-      break;
-    case DPV_CLUSTER:
-      p.cgeo = cluster_geom(mode, ncol);
-      p.threads = (int)std::min<int64_t>(kMaxThreads,
-                                         std::max<int64_t>(64, ((p.cgeo.B + 3) / 4 + 31) / 32 * 32));
-      p.bp_row_words = bp_row_words_for(mode, ncol);
-      p.smem = stage_bytes_mode(mode) + 4 * vb * (size_t)p.cgeo.B;
-      break;
   }
   p.bp = align_up((size_t)L * (size_t)p.bp_row_words * 4, 256);
   return p;
@@ -915,25 +656,11 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) 
 int launch_plan(int mode, const DpPlan& p, const DpArgs& a, int64_t n_items, cudaStream_t st) {
   if (n_items == 0) return SP_OK;
   switch (p.variant) {
-    case DPV_OWN:
-      return launch_own(mode, a, n_items, p.sgeo, p.smem, st);
     case DPV_STREAM:
       switch (mode) {
         case VM_INT32: return launch_stream<VM_INT32>(a, n_items, p.sgeo, st);
         case VM_F64: return launch_stream<VM_F64>(a, n_items, p.sgeo, st);
         default: return launch_stream<VM_F64_NAN>(a, n_items, p.sgeo, st);
-      }
-    case DPV_COOP:
-      switch (mode) {
-        case VM_INT32: return launch_coop<VM_INT32>(a, n_items, p.threads, p.smem, p.cgeo, st);
-        case VM_F64: return launch_coop<VM_F64>(a, n_items, p.threads, p.smem, p.cgeo, st);
-        default: return launch_coop<VM_F64_NAN>(a, n_items, p.threads, p.smem, p.cgeo, st);
-      }
-    case DPV_CLUSTER:
-      switch (mode) {
-        case VM_INT32: return launch_cluster<VM_INT32>(a, n_items, p.threads, p.smem, p.cgeo, st);
-        case VM_F64: return launch_cluster<VM_F64>(a, n_items, p.threads, p.smem, p.cgeo, st);
-        default: return launch_cluster<VM_F64_NAN>(a, n_items, p.threads, p.smem, p.cgeo, st);
       }
     default: {
       const bool sm = p.variant == DPV_SMEM;
@@ -1012,34 +739,6 @@ int launch_grid_t(const GridArgs& g, cudaStream_t st) {
   return launch_check("dp_grid_kernel launch");
 }
 
-template <int MODE>
-int launch_grid_inplace_t(const GridInplaceArgs& g, cudaStream_t st) {
-  auto kern = dp_grid_inplace_kernel<MODE, kGridT, grid_e<MODE>(), grid_slots<MODE>()>;
-  int rc0 = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grid_smem(MODE)),
-                       "cudaFuncSetAttribute(dp_grid_inplace_kernel)");
-  if (rc0) return rc0;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)g.G, 1, 1);
-  cfg.blockDim = dim3((unsigned)(kGridT + 32), 1, 1);
-  cfg.dynamicSmemBytes = grid_smem(MODE);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the waits are safe
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, g), "dp_grid_inplace_kernel launch");
-  if (rc) return rc;
-  return launch_check("dp_grid_inplace_kernel launch");
-}
-int launch_grid_inplace(int mode, const GridInplaceArgs& g, cudaStream_t st) {
-  switch (mode) {
-    case VM_INT32: return launch_grid_inplace_t<VM_INT32>(g, st);
-    case VM_F64: return launch_grid_inplace_t<VM_F64>(g, st);
-    default: return launch_grid_inplace_t<VM_F64_NAN>(g, st);
-  }
-}
-
 int launch_grid(int mode, const GridArgs& g, cudaStream_t st) {
   switch (mode) {
     case VM_INT32: return launch_grid_t<VM_INT32>(g, st);
@@ -1048,450 +747,477 @@ int launch_grid(int mode, const GridArgs& g, cudaStream_t st) {
   }
 }
 
-__global__ void zero_progs_kernel(GridArgs g) {
-  for (int p = 0; p < g.nparts; ++p)
-    for (int x = threadIdx.x; x < g.G; x += blockDim.x) g.progs[p][x] = 0u;
+// ---- capacity partitions: geometry, partition workspaces, phases -----------
+
+// Geometry of one huge instance split into `nparts` capacity partitions of G
+// CTAs each, and the layout of ONE partition's workspace (the same for every
+// partition; each partition's lives on that partition's device):
+//   [stage records: shifts L x 16 B | values L x 8 B | frontiers L x 8 B]
+//   [progress counters G x 4 B][state 128 B][rows 3 x (C, S) x span]
+//   [checkpoint rows nckpt x (C, S) x Wp][back-pointers K stages x row_words]
+// Checkpoint c holds row seg_begin(c) of the partition's own columns
+// (c = 1..nseg; nseg = 1 keeps only the final row).
+struct GridGeom {
+  int mode = 0, L = 0, G = 1, NC = 1, nparts = 1, K = 1, nseg = 1, nckpt = 2, sac = 0;
+  int64_t ncol = 0, B = 0, Wp = 0, halo = 0, span = 0, row_words = 0;
+  size_t rec_off = 0, prog_off = 0, state_off = 0, rows_off = 0, ckpt_off = 0, bp_off = 0;
+  size_t ckpt_bytes = 0, bp_stage = 0, part_bytes = 0;
+  int seg_begin(int sg) const { return sg == 0 ? 0 : L - (nseg - sg) * K; }  // seg_begin(nseg) == L
+  int owner_part() const { return (int)((ncol - 1) / Wp); }                 // partition of column W_eff
+  // pointers into one partition workspace
+  StageShift* shifts(uint8_t* pw) const { return (StageShift*)(pw + rec_off); }
+  int64_t* rv(uint8_t* pw) const { return (int64_t*)(pw + rec_off + (size_t)L * sizeof(StageShift)); }
+  int2* reach(uint8_t* pw) const {
+    return (int2*)(pw + rec_off + (size_t)L * (sizeof(StageShift) + sizeof(int64_t)));
+  }
+  uint32_t* prog(uint8_t* pw) const { return (uint32_t*)(pw + prog_off); }
+  int64_t* state(uint8_t* pw) const { return (int64_t*)(pw + state_off); }
+  InstInfo* info(uint8_t* pw) const { return (InstInfo*)(pw + state_off + 64); }
+  uint8_t* ckpt(uint8_t* pw, int c) const { return pw + ckpt_off + (size_t)c * ckpt_bytes; }
+  uint32_t* bp(uint8_t* pw) const { return (uint32_t*)(pw + bp_off); }
+};
+
+void grid_layout(GridGeom& g, int K) {
+  const size_t vb = value_bytes(g.mode);
+  g.K = K;
+  g.nseg = (g.L + K - 1) / K;
+  g.nckpt = g.nseg + 1;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  g.rec_off = take((size_t)g.L * (sizeof(StageShift) + sizeof(int64_t) + sizeof(int2)));
+  g.prog_off = take((size_t)g.G * 4);
+  g.state_off = take(128);
+  g.rows_off = take(2 * (size_t)kRowBufs * (size_t)g.span * vb);
+  g.ckpt_bytes = align_up(2 * (size_t)g.Wp * vb, 256);
+  g.ckpt_off = take((size_t)g.nckpt * g.ckpt_bytes);
+  g.bp_stage = (size_t)g.row_words * 4;
+  g.bp_off = take((size_t)K * g.bp_stage);
+  g.part_bytes = o;
 }
 
-// Devices of the calling thread's sp_plan_dp_devices call (empty otherwise).
-thread_local std::vector<int> tl_grid_devices;
+int grid_resident_rt(int mode) {
+  return mode == VM_INT32 ? grid_resident<VM_INT32>()
+         : mode == VM_F64 ? grid_resident<VM_F64>()
+                          : grid_resident<VM_F64_NAN>();
+}
 
-// Partitions on other devices (SPLITPLAN_GRID_DEVICES > 1): their row buffers,
-// progress counters and stage-record copies live in that device's memory;
-// every device reaches the others' (and the caller's workspace) through peer
-// access.  Released when the solve returns.
-struct PeerParts {
+// Capacity partitions and segment length for one instance: `ctas` CTAs per
+// partition at most (what stays co-resident on its device), every partition
+// workspace at most `avail` bytes.  Sets *too_wide when a stage's read-back
+// spans a whole partition (the halo would be the partition): use one.
+// SP_ERR_WORKSPACE (with the required bytes) when even checkpointing at the
+// smallest footprint does not fit.
+int grid_geometry(int mode, int L, int64_t ncol, int nparts, int ctas, int max_shift, size_t avail,
+                  int force_k, GridGeom* out, bool* too_wide) {
+  GridGeom g;
+  g.mode = mode;
+  g.L = L;
+  g.ncol = ncol;
+  *too_wide = false;
+  const int64_t ch = grid_ch(mode), line = 128 / (int64_t)value_bytes(mode);
+  const int64_t nchunks = (ncol + ch - 1) / ch;
+  nparts = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(nparts, kMaxParts), nchunks));
+  int G = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(ctas, 1), (nchunks + nparts - 1) / nparts));
+  const int NC = (int)((nchunks + (int64_t)G * nparts - 1) / ((int64_t)G * nparts));
+  G = (int)((nchunks + (int64_t)NC * nparts - 1) / ((int64_t)NC * nparts));
+  nparts = (int)((nchunks + (int64_t)NC * G - 1) / ((int64_t)NC * G));  // no partition left empty
+  g.G = G;
+  g.NC = NC;
+  g.nparts = nparts;
+  g.B = (int64_t)NC * ch;
+  g.Wp = (int64_t)G * g.B;
+  if (nparts > 1) {  // the widest read-back of any stage plus alignment slack, whole lines
+    g.halo = ((int64_t)max_shift + 2 * line + line - 1) / line * line;
+    if (g.halo > g.Wp) {
+      *too_wide = true;
+      return SP_OK;
+    }
+  }
+  g.span = (ch + line) + g.halo + g.Wp + line;
+  g.row_words = bp_row_words_for(mode, g.Wp);
+  auto need = [&](int k) {
+    GridGeom t = g;
+    grid_layout(t, k);
+    return t.part_bytes;
+  };
+  int K = force_k > 0 ? std::min(force_k, L) : L;
+  if (force_k <= 0 && need(K) > avail) {
+    // footprint ~ nseg checkpoints + K back-pointer stages: smallest near
+    // K = sqrt(L * ckpt / bp); above that it grows with K.  Take the longest
+    // segments that fit.
+    GridGeom t = g;
+    grid_layout(t, 1);
+    int kopt = (int)std::max(1.0, std::sqrt((double)L * (double)t.ckpt_bytes / (double)t.bp_stage));
+    kopt = std::min(kopt, L);
+    K = kopt;
+    if (need(kopt) <= avail) {
+      int lo = kopt, hi = L;  // need(lo) fits, need(hi) does not
+      while (hi - lo > 1) {
+        const int mid = lo + (hi - lo) / 2;
+        if (need(mid) <= avail) lo = mid;
+        else hi = mid;
+      }
+      K = lo;
+    }
+  }
+  grid_layout(g, K);
+  *out = g;
+  if (g.part_bytes > avail) {
+    set_required_workspace(g.part_bytes);
+    set_error(SP_ERR_WORKSPACE, "capacity partition (%d stages x %lld columns) needs %zu B of workspace, %zu B available",
+              L, (long long)g.Wp, g.part_bytes, avail);
+    return SP_ERR_WORKSPACE;
+  }
+  return SP_OK;
+}
+
+// Launch arguments of one phase: stages [k0, k0 + cnt) from checkpoint
+// `init_ckpt` (0: the origin row), writing checkpoint `out_ckpt` (0: none),
+// keeping the back-pointers when `keep_bp`.  pw[p]: partition p's workspace
+// as seen from the launching device (peers through peer access / IPC).
+GridArgs grid_args(const GridGeom& g, uint8_t* const* pw, int k0, int cnt, int init_ckpt, int out_ckpt,
+                   bool keep_bp, int sys) {
+  GridArgs a = {};
+  a.k_begin = k0;
+  a.k_count = cnt;
+  a.ncol = (int)g.ncol;
+  a.G = g.G;
+  a.NC = g.NC;
+  a.sac = g.sac;
+  a.bp_row_words = g.row_words;
+  a.nparts = g.nparts;
+  a.part_base = 0;
+  a.launch_parts = g.nparts;
+  a.sys = sys;
+  a.halo = (int)g.halo;
+  for (int p = 0; p < g.nparts; ++p) {
+    GridPart& q = a.parts[p];
+    if (!pw[p]) continue;  // not mapped in this process: never touched by this launch
+    q.rows = pw[p] + g.rows_off;
+    q.prog = g.prog(pw[p]);
+    q.bp = keep_bp ? g.bp(pw[p]) : nullptr;
+    q.init = init_ckpt > 0 ? g.ckpt(pw[p], init_ckpt) : nullptr;
+    q.init_left = (init_ckpt > 0 && p > 0 && pw[p - 1]) ? g.ckpt(pw[p - 1], init_ckpt) : nullptr;
+    q.out = out_ckpt > 0 ? g.ckpt(pw[p], out_ckpt) : nullptr;
+  }
+  return a;
+}
+
+// the stage records a launch on partition p's device reads (its own copy)
+void grid_set_records(GridArgs& a, const GridGeom& g, uint8_t* pw, bool use_reach) {
+  a.shifts = g.shifts(pw);
+  a.rv = g.rv(pw);
+  a.reach = use_reach ? g.reach(pw) : nullptr;
+}
+
+// One instance solved over capacity partitions inside this process (one
+// device, or one device per partition).  Owns the per-partition streams and
+// events; every partition workspace is the caller's.
+struct GridRun {
+  GridGeom g;
   int cur = 0;
   int dev[kMaxParts] = {};
-  cudaStream_t stream[kMaxParts] = {};
-  cudaEvent_t done[kMaxParts] = {};
-  std::vector<std::pair<int, void*>> allocs;
+  uint8_t* pw[kMaxParts] = {};
+  bool separate = false, multi = false, use_reach = true;
+  int sys = 0;
+  cudaStream_t pst[kMaxParts] = {};
+  cudaEvent_t ev[kMaxParts] = {};
+  cudaEvent_t zev[kMaxParts] = {};
   cudaEvent_t start = nullptr;
-  ~PeerParts() {
+  ~GridRun() {
     for (int p = 0; p < kMaxParts; ++p) {
-      if (!stream[p]) continue;
+      if (!pst[p]) continue;
       cudaSetDevice(dev[p]);
-      cudaStreamSynchronize(stream[p]);
-      cudaStreamDestroy(stream[p]);
-      if (done[p]) cudaEventDestroy(done[p]);
-    }
-    for (auto& a : allocs) {
-      cudaSetDevice(a.first);
-      cudaFree(a.second);
+      cudaStreamSynchronize(pst[p]);
+      cudaStreamDestroy(pst[p]);
+      if (ev[p]) cudaEventDestroy(ev[p]);
+      if (zev[p]) cudaEventDestroy(zev[p]);
     }
     cudaSetDevice(cur);
     if (start) cudaEventDestroy(start);
   }
-  void* alloc(int d, size_t bytes) {
-    void* ptr = nullptr;
-    cudaSetDevice(d);
-    if (cudaMalloc(&ptr, bytes) != cudaSuccess) ptr = nullptr;
-    else allocs.push_back({d, ptr});
+  int init_streams() {
+    int rc = check_cuda(cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event");
+    for (int p = 0; p < g.nparts && !rc; ++p) {
+      cudaSetDevice(dev[p]);
+      rc = check_cuda(cudaStreamCreateWithFlags(&pst[p], cudaStreamNonBlocking), "partition stream");
+      if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&ev[p], cudaEventDisableTiming), "event");
+      if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&zev[p], cudaEventDisableTiming), "event");
+    }
     cudaSetDevice(cur);
-    return ptr;
+    return rc;
+  }
+  // forward / recompute phase over every partition, stream-ordered after st
+  int phase(int k0, int cnt, int init_ckpt, int out_ckpt, bool keep_bp, cudaStream_t st) {
+    GridArgs a = grid_args(g, pw, k0, cnt, init_ckpt, out_ckpt, keep_bp, sys);
+    int rc;
+    if (!separate) {  // one launch covers every partition (all on this device)
+      for (int p = 0; p < g.nparts; ++p) {
+        rc = check_cuda(cudaMemsetAsync(g.prog(pw[p]), 0, (size_t)g.G * 4, st), "zero progress counters");
+        if (rc) return rc;
+      }
+      grid_set_records(a, g, pw[0], use_reach);
+      return launch_grid(g.mode, a, st);
+    }
+    // one launch per partition, all in flight together; every partition's
+    // counters are zero before any partition starts
+    rc = check_cuda(cudaEventRecord(start, st), "record phase start");
+    for (int p = 0; p < g.nparts && !rc; ++p) {
+      cudaSetDevice(dev[p]);
+      rc = check_cuda(cudaStreamWaitEvent(pst[p], start, 0), "partition wait");
+      if (!rc) rc = check_cuda(cudaMemsetAsync(g.prog(pw[p]), 0, (size_t)g.G * 4, pst[p]), "zero counters");
+      if (!rc) rc = check_cuda(cudaEventRecord(zev[p], pst[p]), "record counters zeroed");
+    }
+    for (int p = 0; p < g.nparts && !rc; ++p) {
+      cudaSetDevice(dev[p]);
+      for (int q = 0; q < g.nparts && !rc; ++q) rc = check_cuda(cudaStreamWaitEvent(pst[p], zev[q], 0), "wait");
+      GridArgs ap = a;
+      ap.part_base = p;
+      ap.launch_parts = 1;
+      grid_set_records(ap, g, pw[p], use_reach);
+      if (!rc) rc = launch_grid(g.mode, ap, pst[p]);
+      if (!rc) rc = check_cuda(cudaEventRecord(ev[p], pst[p]), "record partition end");
+    }
+    cudaSetDevice(cur);
+    for (int p = 0; p < g.nparts && !rc; ++p) rc = check_cuda(cudaStreamWaitEvent(st, ev[p], 0), "join partitions");
+    return rc;
+  }
+  // backtrack through segment sg, partitions right to left, each on its own
+  // device reading its own back-pointers; (j, side, next stage) handed over
+  // in `state`
+  int backtrack(int sg, int64_t* state, uint8_t* pi, cudaStream_t st) {
+    const int k0 = g.seg_begin(sg), cnt = g.seg_begin(sg + 1) - k0;
+    int rc = SP_OK;
+    if (!separate) {
+      for (int p = g.nparts - 1; p >= 0 && !rc; --p) {
+        grid_backtrack_part_kernel<<<1, 1, 0, st>>>(g.shifts(pw[p]), g.bp(pw[p]), g.row_words, g.mode, k0, cnt,
+                                                    (int64_t)p * g.Wp, state, pi);
+        rc = launch_check("grid_backtrack_part_kernel launch");
+      }
+      return rc;
+    }
+    rc = check_cuda(cudaEventRecord(start, st), "record backtrack start");
+    cudaEvent_t prev = start;
+    for (int p = g.nparts - 1; p >= 0 && !rc; --p) {
+      cudaSetDevice(dev[p]);
+      rc = check_cuda(cudaStreamWaitEvent(pst[p], prev, 0), "backtrack handoff wait");
+      if (rc) break;
+      grid_backtrack_part_kernel<<<1, 1, 0, pst[p]>>>(g.shifts(pw[p]), g.bp(pw[p]), g.row_words, g.mode, k0, cnt,
+                                                      (int64_t)p * g.Wp, state, pi);
+      rc = launch_check("grid_backtrack_part_kernel launch");
+      if (!rc) rc = check_cuda(cudaEventRecord(ev[p], pst[p]), "record handoff");
+      prev = ev[p];
+    }
+    cudaSetDevice(cur);
+    if (!rc) rc = check_cuda(cudaStreamWaitEvent(st, prev, 0), "join backtrack");
+    return rc;
   }
 };
 
-// Workspace of the whole-GPU path for one instance on one device (single
-// partition): the smallest that runs it (checkpoint / recompute with
-// ~sqrt(L) segments) and the one that keeps every back-pointer stage.
-void grid_workspace_bytes(int mode, int64_t L, int64_t ncol, size_t* min_bytes, size_t* full_bytes) {
-  const size_t vb = value_bytes(mode);
-  const int resident = mode == VM_INT32 ? grid_resident<VM_INT32>()
-                       : mode == VM_F64 ? grid_resident<VM_F64>()
-                                        : grid_resident<VM_F64_NAN>();
-  const int64_t nchunks = (ncol + grid_ch(mode) - 1) / grid_ch(mode);
-  int G = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(resident, 1), nchunks));
-  const int NC = (int)((nchunks + G - 1) / G);
-  G = (int)((nchunks + NC - 1) / NC);
-  const int64_t B = (int64_t)NC * grid_ch(mode), line = 128 / (int64_t)vb;
-  const int64_t span = (grid_ch(mode) + line) + G * B + line;
-  const size_t bp_stage = (size_t)bp_row_words_for(mode, G * B) * 4;
-  const size_t ckpt = align_up(2 * (size_t)ncol * vb, 256);
-  const size_t fixed = align_up((size_t)G * 4, 256) + 256 + align_up(2 * kRowBufs * (size_t)span * vb, 256);
-  auto need = [&](int64_t k) {
-    const size_t nseg = (size_t)((L + k - 1) / k);
-    return fixed + (k == L ? 2 : nseg + 1) * ckpt + align_up((size_t)k * bp_stage, 256);
-  };
-  int64_t K = std::max<int64_t>(1, (int64_t)std::sqrt((double)L * (double)ckpt / (double)bp_stage));
-  K = std::min(K, L);
-  *min_bytes = need(K);
-  *full_bytes = need(L);
+// Devices and partition workspaces of an sp_plan_dp_devices call.
+struct DevPlan {
+  int n = 0;
+  int dev[kMaxParts] = {};
+  uint8_t* ws[kMaxParts] = {};
+  size_t bytes[kMaxParts] = {};
+};
+
+int read_max_shift(const StageShift* shifts, int L, cudaStream_t st, int* ms) {
+  std::vector<StageShift> hs(L);
+  int rc = check_cuda(cudaMemcpyAsync(hs.data(), shifts, sizeof(StageShift) * L, cudaMemcpyDeviceToHost, st),
+                      "copy stage shifts");
+  if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync");
+  int m = 0;
+  for (const StageShift& x : hs) m = std::max(m, max_shift(x));
+  *ms = m;
+  return rc;
 }
 
-// Solve one instance over the whole GPU.  With the full back-pointer table in
-// memory: one forward launch and one backtrack.  Otherwise checkpoint /
-// recompute: a forward pass that keeps a row every K stages, then, segment by
+// Solve one instance over capacity partitions.  With
+// every back-pointer stage in memory: one forward launch and one backtrack.
+// Otherwise checkpoint / recompute: a forward pass keeping a checkpoint row
+// at every segment boundary (segments aligned to the END of the chain, the
+// last keeping its back-pointers from the forward pass), then, segment by
 // segment from the end, a recompute of the segment's back-pointers from its
-// checkpoint and a backtrack through it (2x the DP work, sqrt(L) memory).
-int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* info,
-                            const StageShift* shifts, const int64_t* rv, const int2* reach, int32_t* idx,
-                            int64_t inst, int64_t lo, int L, int64_t ncol, int mode, uint8_t* dyn, size_t avail,
-                            cudaStream_t st, int force_parts);
-
+// checkpoint and a backtrack through it: 2L - K stages of DP work.  Every
+// partition keeps its rows, checkpoints and back-pointers in its own
+// workspace; the backtrack walks partition by partition from the right,
+// handing (stage, column, side) leftwards.
+// `dp` (sp_plan_dp_devices): one partition per listed device, each in the
+// caller's workspace for it; otherwise SPLITPLAN_GRID_PARTS partitions (1 by
+// default) carved from `dyn` on this device.
 int run_grid_instance(const sp_instances* in, sp_policies* out, InstInfo* info, const StageShift* shifts,
-                      const int64_t* rv, const int2* reach, int32_t* idx, int64_t inst, int64_t lo, int L,
-                      int64_t ncol, int mode, uint8_t* dyn, size_t avail, cudaStream_t st) {
-  return run_grid_instance_parts(in, out, info, shifts, rv, reach, idx, inst, lo, L, ncol, mode, dyn, avail, st,
-                                 0);
-}
-
-int run_grid_instance_parts(const sp_instances* in, sp_policies* out, InstInfo* info,
-                            const StageShift* shifts, const int64_t* rv, const int2* reach, int32_t* idx,
-                            int64_t inst, int64_t lo, int L, int64_t ncol, int mode, uint8_t* dyn, size_t avail,
-                            cudaStream_t st, int force_parts) {
-  const size_t vb = value_bytes(mode);
-  const int resident = mode == VM_INT32 ? grid_resident<VM_INT32>()
-                       : mode == VM_F64 ? grid_resident<VM_F64>()
-                                        : grid_resident<VM_F64_NAN>();
-  if (resident <= 0) return check_cuda(cudaErrorInvalidConfiguration, "dp_grid_kernel occupancy");
-  const int64_t nchunks = (ncol + grid_ch(mode) - 1) / grid_ch(mode);
-  // partitions of the capacity axis (one per device in a multi-GPU run;
-  // SPLITPLAN_GRID_PARTS > 1 emulates them on this device)
-  // SPLITPLAN_GRID_DEVICES > 1 places partition p on device (current + p),
-  // one launch per device; SPLITPLAN_GRID_SEPARATE=1 runs emulated partitions
-  // as separate concurrent launches on this device (the multi-device protocol
-  // with every partition here).
-  int ndev_avail = 1;
-  if (cudaGetDeviceCount(&ndev_avail) != cudaSuccess) {
-    cudaGetLastError();
-    ndev_avail = 1;
-  }
-  // partition -> device: sp_plan_dp_devices' list, else SPLITPLAN_GRID_DEVICES
-  // consecutive devices from the current one
-  int cur_dev = 0;
-  cudaGetDevice(&cur_dev);
-  std::vector<int> devlist = tl_grid_devices;
-  if (devlist.empty()) {
-    const int n = std::max(1, std::min(std::min(kMaxParts, ndev_avail), env_int("SPLITPLAN_GRID_DEVICES", 1)));
-    for (int p = 0; p < n; ++p) devlist.push_back((cur_dev + p) % ndev_avail);
-  }
-  if ((int)devlist.size() > kMaxParts) devlist.resize(kMaxParts);
-  const int ndev = force_parts ? 1 : (int)devlist.size();
-  int nparts = force_parts ? force_parts
-                           : (ndev > 1 ? ndev : std::max(1, std::min(kMaxParts, env_int("SPLITPLAN_GRID_PARTS", 1))));
-  nparts = (int)std::min<int64_t>(nparts, nchunks);
-  const bool multi = ndev > 1 && nparts > 1;
-  const bool separate = multi || (nparts > 1 && env_int("SPLITPLAN_GRID_SEPARATE", 0) != 0);
-  // CTAs per partition: every partition placed on one device must be co-resident there
-  int per_dev = nparts;
-  if (multi) {
-    per_dev = 1;
-    for (int p = 0; p < nparts; ++p) {
-      int c = 0;
-      for (int r = 0; r < nparts; ++r) c += devlist[r] == devlist[p];
-      per_dev = std::max(per_dev, c);
-    }
-  }
-  int G = (int)std::min<int64_t>(resident / per_dev, (nchunks + nparts - 1) / nparts);
-  G = std::max(G, 1);
-  const int NC = (int)((nchunks + (int64_t)G * nparts - 1) / ((int64_t)G * nparts));
-  G = (int)((nchunks + (int64_t)NC * nparts - 1) / ((int64_t)NC * nparts));
-  const int64_t B = (int64_t)NC * grid_ch(mode);
-  const int64_t line = 128 / (int64_t)vb;
-  // halo: the widest read-back of any stage plus alignment slack, whole lines
-  int64_t halo = 0;
+                      const int64_t* rv, const int2* reach, int32_t* idx, int64_t* gstate, int64_t inst, int64_t lo,
+                      int L, int64_t ncol, int mode, uint8_t* dyn, size_t avail, cudaStream_t st,
+                      const DevPlan* dp) {
+  GridRun R;
+  cudaGetDevice(&R.cur);
+  int nparts = dp ? dp->n : std::max(1, std::min(kMaxParts, env_int("SPLITPLAN_GRID_PARTS", 1)));
+  int ms = 0;
+  int rc = SP_OK;
   if (nparts > 1) {
-    std::vector<StageShift> hs(L);
-    int rc0 = check_cuda(cudaMemcpyAsync(hs.data(), shifts + lo, sizeof(StageShift) * L,
-                                         cudaMemcpyDeviceToHost, st), "copy stage shifts");
-    if (rc0) return rc0;
-    rc0 = check_cuda(cudaStreamSynchronize(st), "sync");
-    if (rc0) return rc0;
-    int ms = 0;
-    for (const StageShift& x : hs) ms = std::max(ms, std::max(std::max(x.i, x.id), std::max(x.s, x.su)));
-    halo = ((int64_t)ms + 2 * line + line - 1) / line * line;
-    if (halo > (int64_t)G * B) {  // the read-back spans a whole partition: no point splitting
-      return run_grid_instance_parts(in, out, info, shifts, rv, reach, idx, inst, lo, L, ncol, mode, dyn,
-                                     avail, st, 1);
-    }
+    rc = read_max_shift(shifts + lo, L, st, &ms);
+    if (rc) return rc;
   }
-  // one row buffer updated in place (a single launch whose stage shifts all
-  // fit a one-neighbour halo): 1/3 of the row memory, L2-resident at cfg5.
-  // Off by default (SPLITPLAN_GRID_INPLACE=1): with the reachable-frontier
-  // skips the three-buffer kernel is faster at cfg5 (3.34 s vs 3.87 s,
-  // profiles/r01/reach/cfg5_inplace_vs_3buf_reach.jsonl)
-  int64_t inplace_hw = 0;
-  if (nparts == 1 && !separate && env_int("SPLITPLAN_GRID_INPLACE", 0) != 0) {
-    std::vector<StageShift> hs(L);
-    int rc0 = check_cuda(cudaMemcpyAsync(hs.data(), shifts + lo, sizeof(StageShift) * L,
-                                         cudaMemcpyDeviceToHost, st), "copy stage shifts");
-    if (rc0) return rc0;
-    rc0 = check_cuda(cudaStreamSynchronize(st), "sync");
-    if (rc0) return rc0;
-    int ms = 0;
-    for (const StageShift& x : hs) ms = std::max(ms, std::max(std::max(x.i, x.id), std::max(x.s, x.su)));
-    const int64_t hw = ((int64_t)ms + 16 / (int64_t)vb + line - 1) / line * line;
-    if (hw <= B) inplace_hw = hw;
-  }
-  const bool inplace = inplace_hw > 0;
-  const int64_t span = (grid_ch(mode) + line) + halo + G * B + line;
-  const int64_t row_words = bp_row_words_for(mode, (int64_t)nparts * G * B);
-  const size_t rows_bytes = inplace ? align_up(2 * (size_t)span * vb, 256) +
-                                          align_up((size_t)G * 3 * 2 * (size_t)inplace_hw * vb, 256)
-                                    : align_up(2 * kRowBufs * (size_t)span * vb, 256);
-  const size_t ckpt_bytes = align_up(2 * (size_t)ncol * vb, 256);
-  const size_t bp_stage = (size_t)row_words * 4;
-  const size_t fixed = align_up((size_t)G * nparts * 4, 256) + 256 + nparts * rows_bytes;
-  // segment length K: everything at once if it fits; else the longest
-  // segments the workspace holds.  Segments are aligned to the END of the
-  // chain and the last one keeps its back-pointers from the forward pass, so
-  // the recompute costs L - K stages (2L - K in total), not L.
-  int K = L;
-  auto need = [&](int k) {
-    const size_t nseg = (size_t)((L + k - 1) / k);
-    return fixed + (k == L ? 2 : nseg + 1) * ckpt_bytes + align_up((size_t)k * bp_stage, 256);
-  };
+  const int resident = grid_resident_rt(mode);
+  if (resident <= 0) return check_cuda(cudaErrorInvalidConfiguration, "dp_grid_kernel occupancy");
   const int force_k = env_int("SPLITPLAN_GRID_SEGMENT", 0);
-  if (force_k > 0) K = std::min(force_k, L);
-  if (need(K) > avail) {
-    const size_t base = fixed + 2 * ckpt_bytes;
-    K = avail > base ? (int)std::min<size_t>((size_t)L, (avail - base) / bp_stage) : 1;
-    K = std::max(K, 1);
-    while (K > 1 && need(K) > avail) K -= std::max(1, K / 64);
-    if (need(K) > avail) {  // fall back to the smallest footprint, ~sqrt(L * ckpt / bp) stages
-      K = (int)std::max<double>(1.0, std::sqrt((double)L * (double)ckpt_bytes / (double)bp_stage));
-      K = std::min(K, L);
-      while (K > 1 && need(K) > avail && need(K / 2) < need(K)) K /= 2;
+  GridGeom g;
+  for (;;) {
+    // CTAs per partition: every partition placed on one device must be co-resident there
+    int per_dev = dp ? 1 : nparts;
+    size_t part_avail = dp ? dp->bytes[0] : avail / (size_t)nparts;
+    if (dp) {
+      for (int p = 0; p < nparts; ++p) {
+        int c = 0;
+        for (int r = 0; r < nparts; ++r) c += dp->dev[r] == dp->dev[p];
+        per_dev = std::max(per_dev, c);
+        part_avail = std::min(part_avail, dp->bytes[p]);
+      }
     }
-  }
-  if (need(K) > avail) {
-    set_required_workspace(need(K) + (avail > 0 ? 0 : 0) + (64 << 20));
-    set_error(SP_ERR_WORKSPACE, "instance %lld (%d x %lld) needs %zu B of DP workspace, %zu B available",
-              (long long)inst, L, (long long)ncol, need(K), avail);
-    return SP_ERR_WORKSPACE;
-  }
-  Carve cv{dyn, avail};
-  uint32_t* prog = (uint32_t*)cv.take((size_t)G * nparts * 4);
-  int64_t* state = (int64_t*)cv.take(4 * sizeof(int64_t));
-  uint8_t* rows[kMaxParts] = {};
-  uint32_t* progs[kMaxParts] = {};
-  const StageShift* pshifts[kMaxParts] = {};
-  const int64_t* prv[kMaxParts] = {};
-  const int2* preach[kMaxParts] = {};
-  PeerParts peers;
-  peers.cur = cur_dev;
-  for (int p = 0; p < nparts; ++p) {
-    peers.dev[p] = multi ? devlist[p] : peers.cur;
-    pshifts[p] = shifts + lo;
-    prv[p] = rv + lo;
-    preach[p] = reach ? reach + lo : nullptr;
-    if (peers.dev[p] == peers.cur) {
-      rows[p] = (uint8_t*)cv.take(rows_bytes);
-      progs[p] = prog + (size_t)p * G;
+    part_avail = part_avail / 256 * 256;
+    bool too_wide = false;
+    rc = grid_geometry(mode, L, ncol, nparts, resident / per_dev, ms, part_avail, force_k, &g, &too_wide);
+    if (!dp && !too_wide && g.nparts < nparts) {  // fewer chunks than partitions: re-split dyn
+      nparts = g.nparts;
       continue;
     }
-    rows[p] = (uint8_t*)peers.alloc(peers.dev[p], rows_bytes);
-    progs[p] = (uint32_t*)peers.alloc(peers.dev[p], (size_t)G * 4);
-    StageShift* sh_copy = (StageShift*)peers.alloc(peers.dev[p], sizeof(StageShift) * L);
-    int64_t* rv_copy = (int64_t*)peers.alloc(peers.dev[p], sizeof(int64_t) * L);
-    if (!rows[p] || !progs[p] || !sh_copy || !rv_copy) {
-      set_error(SP_ERR_CUDA, "partition %d: device %d allocation failed", p, peers.dev[p]);
-      return SP_ERR_CUDA;
-    }
-    int rc0 = check_cuda(cudaMemcpyPeerAsync(sh_copy, peers.dev[p], shifts + lo, peers.cur,
-                                             sizeof(StageShift) * L, st), "copy stage records to peer");
-    if (rc0) return rc0;
-    rc0 = check_cuda(cudaMemcpyPeerAsync(rv_copy, peers.dev[p], rv + lo, peers.cur, sizeof(int64_t) * L, st),
-                     "copy stage values to peer");
-    if (rc0) return rc0;
-    pshifts[p] = sh_copy;
-    prv[p] = rv_copy;
-    if (reach) {
-      int2* reach_copy = (int2*)peers.alloc(peers.dev[p], sizeof(int2) * L);
-      if (!reach_copy) {
-        set_error(SP_ERR_CUDA, "partition %d: device %d allocation failed", p, peers.dev[p]);
-        return SP_ERR_CUDA;
-      }
-      rc0 = check_cuda(cudaMemcpyPeerAsync(reach_copy, peers.dev[p], reach + lo, peers.cur, sizeof(int2) * L, st),
-                       "copy reachable frontiers to peer");
-      if (rc0) return rc0;
-      preach[p] = reach_copy;
-    }
+    if (rc == SP_ERR_WORKSPACE && !dp)  // every partition is carved from dyn
+      set_required_workspace((size_t)g.nparts * g.part_bytes);
+    if (rc) return rc;
+    if (!too_wide) break;
+    nparts = 1;  // the read-back spans a whole partition: no point splitting
   }
-  if (multi) {  // every used device reaches every other one
-    for (int p = 0; p < nparts; ++p)
-      for (int r = 0; r < nparts; ++r) {
-        if (peers.dev[p] == peers.dev[r]) continue;
-        cudaSetDevice(peers.dev[p]);
-        const cudaError_t e = cudaDeviceEnablePeerAccess(peers.dev[r], 0);
+  R.g = g;
+  const bool dev_list = dp != nullptr;
+  for (int p = 0; p < g.nparts; ++p) {
+    R.dev[p] = dev_list ? dp->dev[p] : R.cur;
+    R.pw[p] = dev_list ? dp->ws[p] : dyn + (size_t)p * g.part_bytes;
+    if (R.dev[p] != R.cur) R.multi = true;
+  }
+  R.separate = g.nparts > 1 && (dev_list || env_int("SPLITPLAN_GRID_SEPARATE", 0) != 0);
+  R.sys = (dev_list || env_int("SPLITPLAN_GRID_SYS", 0)) ? 1 : 0;
+  R.use_reach = reach != nullptr;
+  if (R.multi) {  // every used device reaches every other one
+    for (int p = 0; p < g.nparts; ++p)
+      for (int r = 0; r < g.nparts; ++r) {
+        if (R.dev[p] == R.dev[r]) continue;
+        cudaSetDevice(R.dev[p]);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(R.dev[r], 0);
         if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
-          cudaSetDevice(peers.cur);
+          cudaSetDevice(R.cur);
           return check_cuda(e, "cudaDeviceEnablePeerAccess");
         }
         cudaGetLastError();
       }
-    cudaSetDevice(peers.cur);
+    cudaSetDevice(R.cur);
   }
-  if (separate) {
-    int rc0 = check_cuda(cudaEventCreateWithFlags(&peers.start, cudaEventDisableTiming), "event");
-    if (rc0) return rc0;
-    for (int p = 0; p < nparts; ++p) {
-      cudaSetDevice(peers.dev[p]);
-      rc0 = check_cuda(cudaStreamCreateWithFlags(&peers.stream[p], cudaStreamNonBlocking), "partition stream");
-      if (!rc0) rc0 = check_cuda(cudaEventCreateWithFlags(&peers.done[p], cudaEventDisableTiming), "event");
-      cudaSetDevice(peers.cur);
-      if (rc0) return rc0;
-    }
+  if (R.separate) {
+    rc = R.init_streams();
+    if (rc) return rc;
   }
-  const int nseg = (L + K - 1) / K;
-  const int nckpt = K == L ? 2 : nseg + 1;
-  std::vector<uint8_t*> ckpt(nckpt);
-  for (int c = 0; c < nckpt; ++c) ckpt[c] = (uint8_t*)cv.take(ckpt_bytes);
-  uint32_t* bp = (uint32_t*)cv.take((size_t)K * bp_stage);
-
-  GridArgs g = {};
-  g.shifts = shifts + lo;
-  g.reach = reach ? reach + lo : nullptr;
-  g.rv = rv + lo;
-  g.ncol = (int)ncol;
-  g.G = G;
-  g.NC = NC;
-  g.sac = 0;
-  for (int p = 0; p < nparts; ++p) g.rows[p] = rows[p];
-  g.nparts = nparts;
-  g.part_base = 0;
-  g.launch_parts = nparts;
-  g.sys = (multi || env_int("SPLITPLAN_GRID_SYS", 0)) ? 1 : 0;
-  g.halo = (int)halo;
-  g.bp_row_words = row_words;
-  for (int p = 0; p < nparts; ++p) g.progs[p] = progs[p];
+  // every partition gets its own copy of the stage records
+  for (int p = 0; p < g.nparts && !rc; ++p) {
+    rc = check_cuda(cudaMemcpyAsync(g.shifts(R.pw[p]), shifts + lo, sizeof(StageShift) * L, cudaMemcpyDefault, st),
+                    "copy stage shifts to partition");
+    if (!rc)
+      rc = check_cuda(cudaMemcpyAsync(g.rv(R.pw[p]), rv + lo, sizeof(int64_t) * L, cudaMemcpyDefault, st),
+                      "copy stage values to partition");
+    if (!rc && reach)
+      rc = check_cuda(cudaMemcpyAsync(g.reach(R.pw[p]), reach + lo, sizeof(int2) * L, cudaMemcpyDefault, st),
+                      "copy frontiers to partition");
+  }
+  if (rc) return rc;
   {
     uint8_t sac = 0;
-    int rc = check_cuda(cudaMemcpyAsync(&sac, in->source_at_client + inst, 1, cudaMemcpyDeviceToHost, st),
-                        "copy source_at_client");
+    rc = check_cuda(cudaMemcpyAsync(&sac, in->source_at_client + inst, 1, cudaMemcpyDeviceToHost, st),
+                    "copy source_at_client");
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync");
     if (rc) return rc;
-    rc = check_cuda(cudaStreamSynchronize(st), "sync");
-    if (rc) return rc;
-    g.sac = sac ? 1 : 0;
+    R.g.sac = sac ? 1 : 0;
   }
-  auto launch = [&](int k0, int cnt, const uint8_t* init, uint8_t* outrow, uint32_t* bpp) -> int {
-    g.k_begin = k0;
-    g.k_count = cnt;
-    g.init_c = init;
-    g.init_s = init ? init + ncol * vb : nullptr;
-    g.out_c = outrow;
-    g.out_s = outrow ? outrow + ncol * vb : nullptr;
-    g.bp = bpp;
-    // every partition's counters are zero before any partition starts
-    zero_progs_kernel<<<1, 256, 0, st>>>(g);
-    int rc = launch_check("zero_progs_kernel launch");
-    if (rc) return rc;
+  const GridGeom& G = R.g;
+  auto timed_phase = [&](int k0, int cnt, int init_ckpt, int out_ckpt, bool keep_bp) -> int {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (profiling()) {
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0, st);
     }
-    if (inplace) {
-      GridInplaceArgs gi = {};
-      gi.shifts = g.shifts;
-      gi.reach = g.reach;
-      gi.rv = g.rv;
-      gi.k_begin = g.k_begin;
-      gi.k_count = g.k_count;
-      gi.ncol = g.ncol;
-      gi.G = G;
-      gi.NC = NC;
-      gi.sac = g.sac;
-      gi.hw = (int)inplace_hw;
-      gi.init_c = g.init_c;
-      gi.init_s = g.init_s;
-      gi.out_c = g.out_c;
-      gi.out_s = g.out_s;
-      gi.bp = g.bp;
-      gi.bp_row_words = g.bp_row_words;
-      gi.prog = progs[0];
-      gi.rows = rows[0];
-      gi.halo = rows[0] + align_up(2 * (size_t)span * vb, 256);
-      gi.row_hint = env_int("SPLITPLAN_ROW_EVICT_LAST", 0) ? 1 : 0;
-      rc = launch_grid_inplace(mode, gi, st);
-      if (rc) return rc;
-    } else if (!separate) {
-      rc = launch_grid(mode, g, st);
-      if (rc) return rc;
-    } else {  // one launch per partition, all in flight together
-      rc = check_cuda(cudaEventRecord(peers.start, st), "record partition start");
-      if (rc) return rc;
-      for (int p = 0; p < nparts && !rc; ++p) {
-        GridArgs gp = g;
-        gp.part_base = p;
-        gp.launch_parts = 1;
-        gp.shifts = pshifts[p];
-        gp.reach = preach[p];
-        gp.rv = prv[p];
-        cudaSetDevice(peers.dev[p]);
-        rc = check_cuda(cudaStreamWaitEvent(peers.stream[p], peers.start, 0), "partition wait");
-        if (!rc) rc = launch_grid(mode, gp, peers.stream[p]);
-        if (!rc) rc = check_cuda(cudaEventRecord(peers.done[p], peers.stream[p]), "record partition end");
-      }
-      cudaSetDevice(peers.cur);
-      if (rc) return rc;
-      for (int p = 0; p < nparts; ++p) {
-        rc = check_cuda(cudaStreamWaitEvent(st, peers.done[p], 0), "join partitions");
-        if (rc) return rc;
-      }
-    }
+    int r = R.phase(k0, cnt, init_ckpt, out_ckpt, keep_bp, st);
+    if (r) return r;
     if (profiling()) {
       cudaEventRecord(e1, st);
       const double cells = (double)cnt * (double)ncol;
-      prof_record_dp(e0, e1, cells, cells * (bpp ? hbm_bytes_per_cell(mode, DPV_SMEM) : 0.0), DPV_GRID);
+      prof_record_dp(e0, e1, cells, cells * (keep_bp ? hbm_bytes_per_cell(mode, DPV_SMEM) : 0.0), DPV_GRID);
     }
     return SP_OK;
   };
-  int rc;
-  // segment boundaries, aligned to the end: segment sg is [seg_begin(sg), seg_begin(sg + 1))
-  auto seg_begin = [&](int sg) { return sg == 0 ? 0 : L - (nseg - sg) * K; };  // seg_begin(nseg) == L
-  if (K == L) {
-    rc = launch(0, L, nullptr, ckpt[1], bp);
-    if (rc) return rc;
-  } else {
-    for (int sg = 0; sg < nseg; ++sg) {
-      const int k0 = seg_begin(sg), cnt = seg_begin(sg + 1) - k0;
-      rc = launch(k0, cnt, sg ? ckpt[sg] : nullptr, ckpt[sg + 1], sg + 1 == nseg ? bp : nullptr);
-      if (rc) return rc;
-    }
+  // forward pass
+  for (int sg = 0; sg < G.nseg && !rc; ++sg) {
+    const int k0 = G.seg_begin(sg), cnt = G.seg_begin(sg + 1) - k0;
+    rc = timed_phase(k0, cnt, sg, sg + 1, sg + 1 == G.nseg);
   }
-  uint8_t* last = ckpt[K == L ? 1 : nseg];
-  grid_end_kernel<<<1, 1, 0, st>>>(*in, info, inst, last, last + ncol * vb, state);
+  if (rc) return rc;
+  const int own = G.owner_part();
+  grid_end_kernel<<<1, 1, 0, st>>>(info + inst, (int64_t)own * G.Wp, G.Wp, L, -1,
+                                   in->must_end_at ? in->must_end_at + inst : nullptr, G.ckpt(R.pw[own], G.nseg),
+                                   gstate);
   rc = launch_check("grid_end_kernel launch");
-  if (rc) return rc;
-  int64_t hstate[3];
-  rc = check_cuda(cudaMemcpyAsync(hstate, state, sizeof(hstate), cudaMemcpyDeviceToHost, st), "copy end state");
-  if (rc) return rc;
-  rc = check_cuda(cudaStreamSynchronize(st), "sync end state");
-  if (rc) return rc;
-  if (out && hstate[2] == 0) {
-    if (K == L) {
-      grid_backtrack_kernel<<<1, 1, 0, st>>>(*in, inst, shifts, bp, row_words, mode, 0, L, state, *out);
-      rc = launch_check("grid_backtrack_kernel launch");
-      if (rc) return rc;
-    } else {
-      for (int sg = nseg - 1; sg >= 0; --sg) {
-        const int k0 = seg_begin(sg), cnt = seg_begin(sg + 1) - k0;
-        if (sg + 1 < nseg) {  // the last segment's back-pointers are still there
-          rc = launch(k0, cnt, sg ? ckpt[sg] : nullptr, nullptr, bp);
-          if (rc) return rc;
-        }
-        grid_backtrack_kernel<<<1, 1, 0, st>>>(*in, inst, shifts, bp, row_words, mode, k0, cnt, state,
-                                                *out);
-        rc = launch_check("grid_backtrack_kernel launch");
-        if (rc) return rc;
-      }
+  if (rc || !out) return rc;
+  for (int sg = G.nseg - 1; sg >= 0 && !rc; --sg) {
+    if (sg + 1 < G.nseg) {  // the last segment's back-pointers are still there
+      const int k0 = G.seg_begin(sg), cnt = G.seg_begin(sg + 1) - k0;
+      rc = timed_phase(k0, cnt, sg, 0, true);
     }
+    if (!rc) rc = R.backtrack(sg, gstate, out->pi + lo, st);
   }
-  if (out) {
-    grid_finish_kernel<<<1, 1, 0, st>>>(*in, inst, state, idx, *out);
-    rc = launch_check("grid_finish_kernel launch");
-    if (rc) return rc;
-  }
+  if (rc) return rc;
+  grid_finish_kernel<<<1, 1, 0, st>>>(*in, inst, gstate, idx, *out);
+  return launch_check("grid_finish_kernel launch");
   // the caller's next use of the workspace is stream-ordered after these
-  return SP_OK;
+}
+
+// Workspace of the whole-GPU path for one instance in one partition on this
+// device: the smallest that runs it (checkpoint / recompute) and the one that
+// keeps every back-pointer stage.
+void grid_workspace_bytes(int mode, int64_t L, int64_t ncol, int nparts, int per_dev, int max_shift,
+                          size_t* min_bytes, size_t* full_bytes) {
+  GridGeom g;
+  bool too_wide = false;
+  const int resident = std::max(1, grid_resident_rt(mode));
+  const size_t huge = ~(size_t)0 >> 2;
+  grid_geometry(mode, (int)L, ncol, nparts, resident / std::max(per_dev, 1), max_shift, huge, 0, &g, &too_wide);
+  if (too_wide) grid_geometry(mode, (int)L, ncol, 1, resident, max_shift, huge, 0, &g, &too_wide);
+  *full_bytes = g.part_bytes;
+  GridGeom t = g;
+  grid_layout(t, 1);
+  int kopt = (int)std::max(1.0, std::sqrt((double)L * (double)t.ckpt_bytes / (double)t.bp_stage));
+  kopt = (int)std::min<int64_t>(kopt, L);
+  grid_layout(t, kopt);
+  *min_bytes = std::min(t.part_bytes, g.part_bytes);
+  const int force_k = env_int("SPLITPLAN_GRID_SEGMENT", 0);
+  if (force_k > 0) {  // a forced segment length needs exactly its layout
+    grid_layout(t, (int)std::min<int64_t>(force_k, L));
+    *min_bytes = *full_bytes = t.part_bytes;
+  }
 }
 
 // Shared driver of sp_plan_dp and sp_build_dp_tables.
+// `dp`: sp_plan_dp_devices' devices and partition workspaces (null: one
+// device, partitions in `ws`).  Workspace query (q_min != null): nothing is
+// planned; q_min / q_full receive the bytes of `ws` (and q_part_min /
+// q_part_full those of each partition workspace when `dp` is set).
+// `w_eff_check` >= 0: build_dp_tables' caller-sized tables, checked against
+// the instance's W_eff before anything is written.
 int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_s, void* ws,
-           size_t ws_bytes, cudaStream_t st, size_t* q_min = nullptr, size_t* q_full = nullptr) {
+           size_t ws_bytes, cudaStream_t st, size_t* q_min = nullptr, size_t* q_full = nullptr,
+           const DevPlan* dp = nullptr, size_t* q_part_min = nullptr, size_t* q_part_full = nullptr,
+           int64_t w_eff_check = -1) {
   const int64_t n = in->n, total = in->total_layers;
   if (n == 0) return SP_OK;
   Carve cv{(uint8_t*)ws, ws_bytes};
@@ -1501,6 +1227,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   int32_t* idx = (int32_t*)cv.take(sizeof(int32_t) * total);
   DpWork* work = (DpWork*)cv.take(sizeof(DpWork) * n);
   int2* reach = (int2*)cv.take(sizeof(int2) * total);
+  int64_t* gstate = (int64_t*)cv.take(64);
   const size_t fixed = align_up(cv.used, 256);
   if (!ws || fixed > ws_bytes) {
     set_required_workspace(fixed + (1 << 20));
@@ -1524,6 +1251,11 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   rc = check_cuda(cudaStreamSynchronize(st), "sync after prep");
   if (rc) return rc;
 
+  if (w_eff_check >= 0 && hinfo[0].w_eff != w_eff_check) {
+    set_error(SP_ERR_INVALID, "w_eff = %lld does not match the instance's effective budget %lld",
+              (long long)w_eff_check, (long long)hinfo[0].w_eff);
+    return SP_ERR_INVALID;
+  }
   const size_t avail = ws_bytes - fixed;
   uint8_t* dyn = (uint8_t*)ws + fixed;
   const int force = forced_variant();
@@ -1559,22 +1291,47 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     items.push_back(it);
   }
 
-  if (q_min) {  // workspace query (sp_plan_dp_workspace_bytes): no DP launched
-    size_t mn = 0, full = 0;
+  if (q_min) {  // workspace query: no DP launched
+    size_t mn = 0, full = 0, pmn = 0, pfull = 0;
+    const int nparts = dp ? dp->n : std::max(1, std::min(kMaxParts, env_int("SPLITPLAN_GRID_PARTS", 1)));
+    int per_dev = dp ? 1 : nparts;
+    if (dp)
+      for (int p = 0; p < dp->n; ++p) {
+        int c = 0;
+        for (int r = 0; r < dp->n; ++r) c += dp->dev[r] == dp->dev[p];
+        per_dev = std::max(per_dev, c);
+      }
     for (const Item& it : items) {
       const bool grid = tab_c == nullptr && (force == DPV_GRID || it.ncol >= kGridMinCols);
       size_t imin = it.plan.bp + it.plan.rows, ifull = imin;
-      if (grid) grid_workspace_bytes(it.mode, it.L, it.ncol, &imin, &ifull);
+      if (grid) {
+        int ms = 0;
+        if (nparts > 1) {
+          rc = read_max_shift(shifts + hoff[it.inst], (int)it.L, st, &ms);
+          if (rc) return rc;
+        }
+        grid_workspace_bytes(it.mode, it.L, it.ncol, nparts, per_dev, ms, &imin, &ifull);
+        if (dp) {  // partitions live in their own workspaces
+          pmn = std::max(pmn, imin);
+          pfull = std::max(pfull, ifull);
+          continue;
+        }
+        imin *= (size_t)nparts;
+        ifull *= (size_t)nparts;
+      }
       mn = std::max(mn, imin);
       full = grid ? std::max(full, ifull) : full + ifull;
     }
     *q_min = fixed + mn;
     *q_full = fixed + std::max(full, mn);
+    if (q_part_min) *q_part_min = pmn;
+    if (q_part_full) *q_part_full = pfull;
     return SP_OK;
   }
   const int2* a_reach = env_int("SPLITPLAN_NO_REACH", 0) ? nullptr : reach;
   // instances too large for a wave (or wider than 4M columns) run alone over
   // the whole GPU (grid path, checkpointing if needed)
+  size_t grid_full = 0;
   {
     std::vector<Item> rest;
     rest.reserve(items.size());
@@ -1585,11 +1342,28 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         rest.push_back(it);
         continue;
       }
-      rc = run_grid_instance(in, out, info, shifts, rv, a_reach, idx, it.inst, hoff[it.inst], (int)it.L, it.ncol,
-                             it.mode, dyn, avail, st);
+      if (!dp) {  // the workspace that keeps every back-pointer stage (no recompute)
+        const int np = std::max(1, std::min(kMaxParts, env_int("SPLITPLAN_GRID_PARTS", 1)));
+        int ms = 0;
+        if (np > 1) {
+          rc = read_max_shift(shifts + hoff[it.inst], (int)it.L, st, &ms);
+          if (rc) return rc;
+        }
+        size_t gmin = 0, gfull = 0;
+        grid_workspace_bytes(it.mode, it.L, it.ncol, np, np, ms, &gmin, &gfull);
+        grid_full = std::max(grid_full, fixed + (size_t)np * gfull);
+      }
+      rc = run_grid_instance(in, out, info, shifts, rv, a_reach, idx, gstate, it.inst, hoff[it.inst], (int)it.L,
+                             it.ncol, it.mode, dyn, avail, st, dp);
+      if (rc == SP_ERR_WORKSPACE && !dp) set_required_workspace(fixed + sp_last_required_workspace());
       if (rc) return rc;
     }
     items.swap(rest);
+  }
+  {  // what one wave of every remaining instance would need (sp_last_full_workspace)
+    size_t one = fixed;
+    for (const Item& it : items) one += it.plan.bp + it.plan.rows;
+    set_full_workspace(std::max(one, grid_full));
   }
 
   DpArgs a;
@@ -1736,12 +1510,9 @@ int sp_plan_dp_workspace_bytes(const sp_instances* in, size_t* min_bytes, size_t
   return run_dp(in, nullptr, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, min_bytes, full_bytes);
 }
 
-int sp_plan_dp_devices(const sp_instances* in, sp_policies* out, const int32_t* devices,
-                       int32_t n_devices, void* ws, size_t ws_bytes, void* stream) {
-  int rc = validate(in);
-  if (rc) return rc;
-  rc = validate_out(out);
-  if (rc) return rc;
+// validate a device list and its partition workspaces into a DevPlan
+static int dev_plan(const int32_t* devices, int32_t n_devices, void* const* part_ws, const size_t* part_ws_bytes,
+                    bool need_ws, DevPlan* dp) {
   int cur = 0, count = 0;
   if (cudaGetDevice(&cur) != cudaSuccess || cudaGetDeviceCount(&count) != cudaSuccess) {
     cudaGetLastError();
@@ -1752,16 +1523,305 @@ int sp_plan_dp_devices(const sp_instances* in, sp_policies* out, const int32_t* 
     set_error(SP_ERR_INVALID, "devices: 1..%d entries, the first the current device (%d)", kMaxParts, cur);
     return SP_ERR_INVALID;
   }
-  for (int p = 0; p < n_devices; ++p)
+  dp->n = n_devices;
+  for (int p = 0; p < n_devices; ++p) {
     if (devices[p] < 0 || devices[p] >= count) {
       set_error(SP_ERR_INVALID, "devices[%d] = %d: no such device", p, devices[p]);
       return SP_ERR_INVALID;
     }
-  tl_grid_devices.assign(devices, devices + n_devices);
-  rc = run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
-  tl_grid_devices.clear();
-  return rc;
+    dp->dev[p] = devices[p];
+    if (!need_ws) continue;
+    if (!part_ws || !part_ws_bytes || !part_ws[p]) {
+      set_error(SP_ERR_INVALID, "partition %d: null workspace", p);
+      return SP_ERR_INVALID;
+    }
+    dp->ws[p] = (uint8_t*)part_ws[p];
+    dp->bytes[p] = part_ws_bytes[p];
+  }
+  return SP_OK;
 }
+
+int sp_plan_dp_devices(const sp_instances* in, sp_policies* out, const int32_t* devices, int32_t n_devices,
+                       void* ws, size_t ws_bytes, void* const* part_ws, const size_t* part_ws_bytes,
+                       void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  rc = validate_out(out);
+  if (rc) return rc;
+  DevPlan dp;
+  rc = dev_plan(devices, n_devices, part_ws, part_ws_bytes, true, &dp);
+  if (rc) return rc;
+  return run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr, &dp);
+}
+
+int sp_plan_dp_devices_workspace_bytes(const sp_instances* in, const int32_t* devices, int32_t n_devices,
+                                       size_t* ws_min, size_t* part_min, size_t* part_full, void* ws,
+                                       size_t ws_bytes, void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  if (!ws_min || !part_min || !part_full) {
+    set_error(SP_ERR_INVALID, "null output");
+    return SP_ERR_INVALID;
+  }
+  *ws_min = *part_min = *part_full = 0;
+  if (in->n == 0) return SP_OK;
+  DevPlan dp;
+  rc = dev_plan(devices, n_devices, nullptr, nullptr, false, &dp);
+  if (rc) return rc;
+  size_t full = 0;
+  return run_dp(in, nullptr, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, ws_min, &full, &dp, part_min,
+                part_full);
+}
+
+// ---- capacity partitions, one process per device ---------------------------
+
+static GridGeom geom_of(const sp_grid_plan* p) {
+  GridGeom g;
+  g.mode = p->mode;
+  g.L = p->n_layers;
+  g.G = p->ctas;
+  g.NC = p->chunks_per_cta;
+  g.nparts = p->nparts;
+  g.K = p->seg_stages;
+  g.nseg = p->nseg;
+  g.nckpt = p->nckpt;
+  g.sac = p->sac;
+  g.ncol = p->ncol;
+  g.B = p->part_cols / std::max(p->ctas, 1);
+  g.Wp = p->part_cols;
+  g.halo = p->halo;
+  g.span = p->span;
+  g.row_words = p->row_words;
+  g.rec_off = p->rec_off;
+  g.prog_off = p->prog_off;
+  g.state_off = p->state_off;
+  g.rows_off = p->rows_off;
+  g.ckpt_off = p->ckpt_off;
+  g.bp_off = p->bp_off;
+  g.ckpt_bytes = p->ckpt_bytes;
+  g.bp_stage = p->bp_stage;
+  g.part_bytes = p->part_bytes;
+  return g;
+}
+
+static int check_plan(const sp_grid_plan* p, int part) {
+  if (!p || p->nparts < 1 || p->nparts > kMaxParts || part < 0 || part >= p->nparts || p->part_bytes == 0) {
+    set_error(SP_ERR_INVALID, "bad grid plan or partition index %d", part);
+    return SP_ERR_INVALID;
+  }
+  return SP_OK;
+}
+
+int sp_grid_plan_make(const sp_instances* in, int32_t nparts, int32_t ctas_per_part, size_t part_ws_bytes,
+                      int32_t force_segment, sp_grid_plan* plan, void* ws, size_t ws_bytes, void* stream) {
+  int rc = validate(in);
+  if (rc) return rc;
+  if (in->n != 1 || !plan || nparts < 1 || nparts > kMaxParts) {
+    set_error(SP_ERR_INVALID, "sp_grid_plan_make takes exactly one instance and 1..%d partitions", kMaxParts);
+    return SP_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t L = in->total_layers;
+  Carve cv{(uint8_t*)ws, ws_bytes};
+  InstInfo* info = (InstInfo*)cv.take(sizeof(InstInfo));
+  StageShift* shifts = (StageShift*)cv.take(sizeof(StageShift) * L);
+  int64_t* rv = (int64_t*)cv.take(sizeof(int64_t) * L);
+  int2* reach = (int2*)cv.take(sizeof(int2) * L);
+  if (!ws || align_up(cv.used, 256) > ws_bytes) {
+    set_required_workspace(align_up(cv.used, 256));
+    set_error(SP_ERR_WORKSPACE, "sp_grid_plan_make needs %zu B of scratch", align_up(cv.used, 256));
+    return SP_ERR_WORKSPACE;
+  }
+  prep_kernel<<<1, 128, 0, st>>>(*in, info, shifts, rv, reach);
+  rc = launch_check("prep_kernel launch");
+  InstInfo hinfo;
+  uint8_t sac = 0;
+  int64_t off0 = 0;
+  if (!rc) rc = check_cuda(cudaMemcpyAsync(&hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st), "copy info");
+  if (!rc) rc = check_cuda(cudaMemcpyAsync(&sac, in->source_at_client, 1, cudaMemcpyDeviceToHost, st), "copy sac");
+  if (!rc) rc = check_cuda(cudaMemcpyAsync(&off0, in->layer_off, 8, cudaMemcpyDeviceToHost, st), "copy offset");
+  int ms = 0;
+  if (!rc) rc = read_max_shift(shifts, (int)L, st, &ms);
+  if (rc) return rc;
+  if (off0 != 0) {
+    set_error(SP_ERR_INVALID, "layer_off[0] must be 0");
+    return SP_ERR_INVALID;
+  }
+  const int64_t ncol = hinfo.w_eff + 1;
+  if (ncol > kMaxCols) {
+    set_error(SP_ERR_UNSUPPORTED, "W_eff = %lld exceeds the supported 2^31 columns", (long long)hinfo.w_eff);
+    return SP_ERR_UNSUPPORTED;
+  }
+  const int resident = grid_resident_rt(hinfo.mode);
+  if (resident <= 0) return check_cuda(cudaErrorInvalidConfiguration, "dp_grid_kernel occupancy");
+  const int ctas = ctas_per_part > 0 ? std::min(ctas_per_part, resident) : resident;
+  GridGeom g;
+  bool too_wide = false;
+  rc = grid_geometry(hinfo.mode, (int)L, ncol, nparts, ctas, ms, part_ws_bytes / 256 * 256, force_segment, &g,
+                     &too_wide);
+  if (!rc && too_wide)  // the read-back spans a whole partition: one partition
+    rc = grid_geometry(hinfo.mode, (int)L, ncol, 1, ctas, ms, part_ws_bytes / 256 * 256, force_segment, &g,
+                       &too_wide);
+  if (rc) return rc;
+  g.sac = sac ? 1 : 0;
+  sp_grid_plan p = {};
+  p.mode = g.mode;
+  p.n_layers = g.L;
+  p.ctas = g.G;
+  p.chunks_per_cta = g.NC;
+  p.nparts = g.nparts;
+  p.seg_stages = g.K;
+  p.nseg = g.nseg;
+  p.nckpt = g.nckpt;
+  p.sac = g.sac;
+  p.owner_part = g.owner_part();
+  p.ncol = g.ncol;
+  p.part_cols = g.Wp;
+  p.halo = g.halo;
+  p.span = g.span;
+  p.row_words = g.row_words;
+  p.rec_off = g.rec_off;
+  p.prog_off = g.prog_off;
+  p.state_off = g.state_off;
+  p.rows_off = g.rows_off;
+  p.ckpt_off = g.ckpt_off;
+  p.bp_off = g.bp_off;
+  p.ckpt_bytes = g.ckpt_bytes;
+  p.bp_stage = g.bp_stage;
+  p.part_bytes = g.part_bytes;
+  *plan = p;
+  return SP_OK;
+}
+
+int sp_grid_part_prepare(const sp_grid_plan* plan, const sp_instances* in, void* part_ws, void* stream) {
+  int rc = check_plan(plan, 0);
+  if (!rc) rc = validate(in);
+  if (rc) return rc;
+  if (in->n != 1 || in->total_layers != plan->n_layers || !part_ws) {
+    set_error(SP_ERR_INVALID, "sp_grid_part_prepare: the plan's single instance and a workspace");
+    return SP_ERR_INVALID;
+  }
+  const GridGeom g = geom_of(plan);
+  uint8_t* pw = (uint8_t*)part_ws;
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = check_cuda(cudaMemsetAsync(g.state(pw), 0, 128, st), "zero partition state");
+  if (rc) return rc;
+  prep_kernel<<<1, 128, 0, st>>>(*in, g.info(pw), g.shifts(pw), g.rv(pw), g.reach(pw));
+  return launch_check("prep_kernel launch");
+}
+
+int sp_grid_part_reset(const sp_grid_plan* plan, void* part_ws, void* stream) {
+  int rc = check_plan(plan, 0);
+  if (rc) return rc;
+  const GridGeom g = geom_of(plan);
+  return check_cuda(cudaMemsetAsync(g.prog((uint8_t*)part_ws), 0, (size_t)g.G * 4, (cudaStream_t)stream),
+                    "zero progress counters");
+}
+
+int sp_grid_part_forward(const sp_grid_plan* plan, int32_t part, void* const* part_ws, int32_t seg,
+                         int32_t write_ckpt, int32_t keep_bp, void* stream) {
+  int rc = check_plan(plan, part);
+  if (rc) return rc;
+  if (!part_ws || seg < 0 || seg >= plan->nseg) {
+    set_error(SP_ERR_INVALID, "sp_grid_part_forward: segment %d of %d", seg, plan->nseg);
+    return SP_ERR_INVALID;
+  }
+  for (int p = 0; p < plan->nparts; ++p)
+    if (!part_ws[p]) {
+      set_error(SP_ERR_INVALID, "partition %d workspace not mapped", p);
+      return SP_ERR_INVALID;
+    }
+  const GridGeom g = geom_of(plan);
+  uint8_t* pw[kMaxParts] = {};
+  for (int p = 0; p < g.nparts; ++p) pw[p] = (uint8_t*)part_ws[p];
+  const int k0 = g.seg_begin(seg), cnt = g.seg_begin(seg + 1) - k0;
+  GridArgs a = grid_args(g, pw, k0, cnt, seg, write_ckpt ? seg + 1 : 0, keep_bp != 0, 1);
+  a.part_base = part;
+  a.launch_parts = 1;
+  grid_set_records(a, g, pw[part], true);
+  return launch_grid(g.mode, a, (cudaStream_t)stream);
+}
+
+int sp_grid_part_end(const sp_grid_plan* plan, void* owner_ws, int8_t must_end_at, int64_t* state, void* stream) {
+  int rc = check_plan(plan, plan ? plan->owner_part : 0);
+  if (rc) return rc;
+  if (!owner_ws || !state) {
+    set_error(SP_ERR_INVALID, "sp_grid_part_end: null workspace or state");
+    return SP_ERR_INVALID;
+  }
+  const GridGeom g = geom_of(plan);
+  uint8_t* pw = (uint8_t*)owner_ws;
+  grid_end_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(g.info(pw), (int64_t)plan->owner_part * g.Wp, g.Wp, g.L,
+                                                      must_end_at, nullptr, g.ckpt(pw, g.nseg), state);
+  return launch_check("grid_end_kernel launch");
+}
+
+int sp_grid_part_backtrack(const sp_grid_plan* plan, int32_t part, void* part_ws, int32_t seg, int64_t* state,
+                           uint8_t* pi, void* stream) {
+  int rc = check_plan(plan, part);
+  if (rc) return rc;
+  if (!part_ws || !state || !pi || seg < 0 || seg >= plan->nseg) {
+    set_error(SP_ERR_INVALID, "sp_grid_part_backtrack: bad arguments");
+    return SP_ERR_INVALID;
+  }
+  const GridGeom g = geom_of(plan);
+  uint8_t* pw = (uint8_t*)part_ws;
+  const int k0 = g.seg_begin(seg), cnt = g.seg_begin(seg + 1) - k0;
+  grid_backtrack_part_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(g.shifts(pw), g.bp(pw), g.row_words, g.mode, k0,
+                                                                 cnt, (int64_t)part * g.Wp, state, pi);
+  return launch_check("grid_backtrack_part_kernel launch");
+}
+
+// ---- CUDA IPC of partition workspaces (one process per device) --------------
+
+typedef int (*AddrRangeFn)(unsigned long long*, size_t*, unsigned long long);
+
+int sp_ipc_export(const void* dptr, void* handle, size_t* offset) {
+  if (!dptr || !handle || !offset) {
+    set_error(SP_ERR_INVALID, "sp_ipc_export: null argument");
+    return SP_ERR_INVALID;
+  }
+  // the handle names the whole allocation: find its base through the driver
+  // entry point (no libcuda link dependency)
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  int rc = check_cuda(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q),
+                      "cudaGetDriverEntryPoint(cuMemGetAddressRange)");
+  if (rc) return rc;
+  if (!fn || q != cudaDriverEntryPointSuccess) {
+    set_error(SP_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    return SP_ERR_CUDA;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (((AddrRangeFn)fn)(&base, &size, (unsigned long long)(uintptr_t)dptr) != 0) {
+    set_error(SP_ERR_CUDA, "cuMemGetAddressRange failed");
+    return SP_ERR_CUDA;
+  }
+  cudaIpcMemHandle_t h;
+  rc = check_cuda(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base), "cudaIpcGetMemHandle");
+  if (rc) return rc;
+  memcpy(handle, &h, sizeof(h));
+  *offset = (size_t)((uintptr_t)dptr - (uintptr_t)base);
+  return SP_OK;
+}
+
+int sp_ipc_import(const void* handle, size_t offset, void** dptr, void** base) {
+  if (!handle || !dptr || !base) {
+    set_error(SP_ERR_INVALID, "sp_ipc_import: null argument");
+    return SP_ERR_INVALID;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  int rc = check_cuda(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  if (rc) return rc;
+  *base = p;
+  *dptr = (uint8_t*)p + offset;
+  return SP_OK;
+}
+
+int sp_ipc_close(void* base) { return check_cuda(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle"); }
 
 int sp_build_dp_tables(const sp_instances* in, int64_t w_eff, double* client_table,
                        double* server_table, void* ws, size_t ws_bytes, void* stream) {
@@ -1771,8 +1831,12 @@ int sp_build_dp_tables(const sp_instances* in, int64_t w_eff, double* client_tab
     set_error(SP_ERR_INVALID, "sp_build_dp_tables takes exactly one instance and two tables");
     return SP_ERR_INVALID;
   }
-  (void)w_eff;
-  return run_dp(in, nullptr, client_table, server_table, ws, ws_bytes, (cudaStream_t)stream);
+  if (w_eff < 0) {
+    set_error(SP_ERR_INVALID, "negative w_eff");
+    return SP_ERR_INVALID;
+  }
+  return run_dp(in, nullptr, client_table, server_table, ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr,
+                nullptr, nullptr, nullptr, w_eff);
 }
 
 
@@ -1819,6 +1883,22 @@ int sp_plan_exhaustive(const sp_instances* in, sp_policies* out, void* stream) {
   rc = validate_out(out);
   if (rc) return rc;
   if (in->n == 0) return SP_OK;
+  // L <= 24 (planner.py:21 ORACLE_MAX_LAYERS): the kernel enumerates 2^L masks
+  // in 32-bit words and keeps a 32-entry index list
+  std::vector<int64_t> hoff(in->n + 1);
+  rc = check_cuda(cudaMemcpyAsync(hoff.data(), in->layer_off, sizeof(int64_t) * (in->n + 1),
+                                  cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+                  "copy layer offsets");
+  if (!rc) rc = check_cuda(cudaStreamSynchronize((cudaStream_t)stream), "sync");
+  if (rc) return rc;
+  for (int64_t k = 0; k < in->n; ++k) {
+    const int64_t L = hoff[k + 1] - hoff[k];
+    if (L < 0 || L > 24) {
+      set_error(SP_ERR_UNSUPPORTED, "oracle limited to 24 layers, got %lld (instance %lld)", (long long)L,
+                (long long)k);
+      return SP_ERR_UNSUPPORTED;
+    }
+  }
   exhaustive_kernel<<<(unsigned)in->n, 256, 0, (cudaStream_t)stream>>>(*in, *out);
   return launch_check("exhaustive_kernel launch");
 }

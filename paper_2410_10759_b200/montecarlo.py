@@ -61,7 +61,8 @@ def solve_requests(req: dict, layer_lists) -> dict:
     w_eff = B.effective_budget(sol.instances)
     lens = (sol.layer_off[1:] - sol.layer_off[:-1]).to(torch.float64)
     cells = float((lens * (w_eff + 1).to(torch.float64)).sum().item())
-    host = {k: dict(load=v.server_load.cpu().numpy(), ok=v.feasible.cpu().numpy().astype(bool))
+    valid = (sol.status == 0).cpu().numpy()  # cost-table errors are error cells, never kept
+    host = {k: dict(load=v.server_load.cpu().numpy(), ok=v.feasible.cpu().numpy().astype(bool) & valid)
             for k, v in out.items()}
     host["cells"] = cells
     return host

@@ -87,10 +87,11 @@ def plan_batch(name: str, batch: B.InstanceBatch) -> B.PolicyBatch:
     if key == "all_client":
         return B.plan_prefix(batch, N.SP_ALL_CLIENT)
     if key == "oracle":
-        if batch.n_layers_host is not None and batch.n_layers_host.size and \
-                int(batch.n_layers_host.max()) > ORACLE_MAX_LAYERS:
-            raise ValueError(f"oracle limited to {ORACLE_MAX_LAYERS} layers, "
-                             f"got {int(batch.n_layers_host.max())}")
+        lens = batch.n_layers_host
+        if lens is None:  # e.g. a cost-table batch: lengths from the device offsets
+            lens = np.diff(batch.layer_off.cpu().numpy())
+        if lens.size and int(lens.max()) > ORACLE_MAX_LAYERS:
+            raise ValueError(f"oracle limited to {ORACLE_MAX_LAYERS} layers, got {int(lens.max())}")
         return B.plan_exhaustive(batch)
     raise ValueError(f"unknown planner {name!r}")
 

@@ -70,7 +70,7 @@ class Solved:
     layer_off: torch.Tensor
     instances: B.InstanceBatch
     policies: B.PolicyBatch
-    status: torch.Tensor       # K1 status word per request
+    status: torch.Tensor       # K1 status word per request (0 ok; else the placement is not valid)
     client_s: torch.Tensor
     server_s: torch.Tensor
     up_s: torch.Tensor
@@ -118,4 +118,8 @@ class Engine:
             total_layers = int(self.n_layers[req.model.cpu().numpy()].sum())
         inst, status, f = self.cost_table(req, total_layers, off)
         pol = B.plan_dp(inst)
+        # a request whose cost table failed (NaN / inf / negative / overflowing
+        # times: the reference raises and records an error cell) is never a
+        # feasible placement; its status word says why
+        pol.feasible.mul_((status == 0).to(torch.uint8))
         return Solved(inst.layer_off, inst, pol, status, f["cs"], f["ss"], f["up"], f["dn"])

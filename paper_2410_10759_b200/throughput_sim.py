@@ -13,7 +13,7 @@ from __future__ import annotations
 import csv
 import io
 import json
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from pathlib import Path
 from typing import Sequence
 
@@ -84,7 +84,11 @@ class Stream:
 
 @dataclass(frozen=True)
 class SimResult:
-    """Per-request records plus the kernel-computed aggregates."""
+    """Per-request records plus queueing aggregates (throughput_sim.py:109-130).
+
+    Replays (`replay_many`) attach the kernel-computed aggregates for the
+    exact arrays they returned; a result built any other way (or copied with
+    `dataclasses.replace`) computes them from `wait_ms` like the reference."""
 
     arrival_ms: np.ndarray
     admit_ms: np.ndarray
@@ -92,21 +96,36 @@ class SimResult:
     demand: np.ndarray
     duration_ms: np.ndarray
     served_count: int
-    _max: float = field(default=0.0, repr=False, compare=False)
-    _mean: float = field(default=0.0, repr=False, compare=False)
-    _cum: np.ndarray | None = field(default=None, repr=False, compare=False)
+
+    def _cached(self):
+        c = self.__dict__.get("_agg")
+        return c[1] if c is not None and c[0] is self.wait_ms else None
 
     @property
     def max_wait_ms(self) -> float:
-        return float(self._max) if len(self.wait_ms) else 0.0
+        if not len(self.wait_ms):
+            return 0.0
+        c = self._cached()
+        return float(c[0]) if c is not None else float(np.max(self.wait_ms))
 
     @property
     def mean_wait_ms(self) -> float:
-        return float(self._mean) if len(self.wait_ms) else 0.0
+        if not len(self.wait_ms):
+            return 0.0
+        c = self._cached()
+        return float(c[1]) if c is not None else float(np.mean(self.wait_ms))
 
     @property
     def cumulative_wait_ms(self) -> np.ndarray:
-        return self._cum if self._cum is not None else np.zeros(0)
+        c = self._cached()
+        return c[2] if c is not None else np.cumsum(self.wait_ms)
+
+
+def _attach(res: SimResult, max_w: float, mean_w: float, cum: np.ndarray) -> SimResult:
+    """Attach the kernel's aggregates (not a dataclass field: copies recompute
+    them), tied to the wait array they describe."""
+    object.__setattr__(res, "_agg", (res.wait_ms, (max_w, mean_w, cum)))
+    return res
 
 
 # ---------------------------------------------------------------------------
@@ -238,11 +257,10 @@ def replay_many(streams: Sequence[Stream], capacities: Sequence[float],
                 raise err
             out.append(err)
             continue
-        out.append(SimResult(arrival_ms=s.arrival_ms, admit_ms=h["admit"][a:z].copy(),
-                             wait_ms=h["wait"][a:z].copy(), demand=s.demand,
-                             duration_ms=s.duration_ms, served_count=int(z - a),
-                             _max=float(h["mx"][r]), _mean=float(h["mean"][r]),
-                             _cum=h["cum"][a:z].copy()))
+        res = SimResult(arrival_ms=s.arrival_ms, admit_ms=h["admit"][a:z].copy(),
+                        wait_ms=h["wait"][a:z].copy(), demand=s.demand,
+                        duration_ms=s.duration_ms, served_count=int(z - a))
+        out.append(_attach(res, float(h["mx"][r]), float(h["mean"][r]), h["cum"][a:z].copy()))
     return out
 
 

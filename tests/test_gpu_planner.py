@@ -87,7 +87,7 @@ def test_dp_tables_match_reference(gpu):
         pos += cnt
 
 
-@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop", "stream"])
+@pytest.mark.parametrize("variant", ["global", "smem", "stream"])
 def test_dp_tables_every_variant(gpu, variant, monkeypatch):
     """Full tables from each K2 variant equal the reference's build_dp_tables."""
     from paper_2410_10759_b200 import planner as P
@@ -180,12 +180,12 @@ def test_dp_vs_oracle_smem_and_global_rows(gpu, r_kind):
         assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{r_kind}[{k}]")
 
 
-@pytest.mark.parametrize("variant", ["global", "cluster", "smem", "coop", "stream", "grid", "own"])
+@pytest.mark.parametrize("variant", ["global", "smem", "stream", "grid"])
 @pytest.mark.parametrize("name", ["battery_wide", "battery_float", "battery_large_model"])
 def test_dp_kernel_variants_agree(gpu, variant, name, monkeypatch):
-    """Every K2 variant (rows in one CTA's SMEM, in cluster DSMEM, in global
-    memory) is bit-exact on the same instances (the host falls back where a
-    variant cannot hold a row)."""
+    """Every K2 variant (rows in one CTA's SMEM, in L2-resident global rows,
+    in global memory, over the whole GPU) is bit-exact on the same instances
+    (the host falls back where a variant cannot hold a row)."""
     if not (GOLDEN / f"{name}.npz").exists():
         pytest.skip("battery not generated")
     from paper_2410_10759_b200 import batch as B
@@ -229,35 +229,13 @@ def test_stream_cluster_sizes(gpu, cluster, monkeypatch):
         _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
 
 
-@pytest.mark.parametrize("cluster,cfg,bufs,occ", [("1", "0", "3", "1"), ("2", "0", "2", "1"), ("5", "0", "3", "1"),
-                                                  ("7", "1", "3", "1"), ("8", "0", "4", "1"), ("3", "1", "2", "1"),
-                                                  ("4", "2", "3", "2"), ("13", "2", "2", "2")])
-def test_own_kernel_geometries(gpu, cluster, cfg, bufs, occ, monkeypatch):
-    """The own-block kernel (rows in the cluster CTAs' shared memory, remote
-    windows over L2) at forced cluster sizes, both thread configurations and
-    2-4 global row buffers: many windows are remote or straddle a block edge."""
-    from paper_2410_10759_b200 import batch as B
-    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "own")
-    monkeypatch.setenv("SPLITPLAN_DP_CLUSTER", cluster)
-    monkeypatch.setenv("SPLITPLAN_OWN_CFG", cfg)
-    monkeypatch.setenv("SPLITPLAN_OWN_BUFS", bufs)
-    monkeypatch.setenv("SPLITPLAN_OWN_OCC", occ)
-    for name in ("battery_wide", "battery_large_model", "battery_acceptance"):
-        bat = Battery(name)
-        _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
-
-
-@pytest.mark.parametrize("inplace", ["1", "0"])
 @pytest.mark.parametrize("segment", ["0", "7", "1"])
-def test_grid_checkpoint_recompute(gpu, segment, inplace, monkeypatch):
+def test_grid_checkpoint_recompute(gpu, segment, monkeypatch):
     """The whole-GPU path for one huge instance, with the back-pointers kept
-    whole (segment 0) or recomputed from checkpoint rows every 7 / 1 stages;
-    one row buffer updated in place (where the shifts fit a one-neighbour
-    halo) or three buffers."""
+    whole (segment 0) or recomputed from checkpoint rows every 7 / 1 stages."""
     from paper_2410_10759_b200 import batch as B
     monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "grid")
     monkeypatch.setenv("SPLITPLAN_GRID_SEGMENT", segment)
-    monkeypatch.setenv("SPLITPLAN_GRID_INPLACE", inplace)
     for name in ("battery_wide", "battery_special"):
         bat = Battery(name)
         _compare(bat, "dp", B.plan_dp(_batch(bat)).to_host())
@@ -316,16 +294,83 @@ def test_full_size_batteries(gpu, name):
         _compare(bat, "greedy", B.plan_prefix(b, N.SP_GREEDY).to_host())
 
 
-@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0, 0]])
-def test_plan_dp_devices_partitions(gpu, devices, monkeypatch):
+@pytest.mark.parametrize("devices,segment", [([0, 0], "0"), ([0, 0, 0, 0], "0"), ([0] * 8, "0"),
+                                             ([0, 0], "13"), ([0, 0, 0], "1"), ([0] * 8, "29")])
+def test_plan_dp_devices_partitions(gpu, devices, segment, monkeypatch):
     """sp_plan_dp_devices: the capacity axis of whole-GPU instances split over
     a device list (here the one GPU listed several times: one launch per
-    partition, system-scope counters, the multi-device code path)."""
+    partition, system-scope counters, the multi-device code path).  Every
+    partition keeps its rows, checkpoints and back-pointers in its OWN
+    workspace allocation, and the backtrack hands (stage, column, side) from
+    partition to partition; with and without checkpoint / recompute."""
     from paper_2410_10759_b200 import batch as B
     monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "grid")
+    monkeypatch.setenv("SPLITPLAN_GRID_SEGMENT", segment)
     for name, must in (("battery_large_chain", False), ("battery_wide", True)):
         bat = Battery(name)
         _compare(bat, "dp", B.plan_dp(_batch(bat, with_must=must), devices=devices).to_host())
+
+
+def test_plan_dp_devices_minimum_partition_workspaces(gpu, monkeypatch):
+    """Partition workspaces of exactly the queried minimum (checkpoint /
+    recompute chosen by the library) give the same placements; one byte less
+    than what a partition needs is a clean SP_ERR_WORKSPACE."""
+    import ctypes as C
+    import torch
+    from paper_2410_10759_b200 import _native as N, batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "grid")
+    bat = Battery("battery_large_chain")
+    b = _batch(bat, with_must=False)
+    devices = [0, 0, 0]
+    arr = (C.c_int32 * 3)(*devices)
+    ws_min, pmin, pfull = C.c_size_t(0), C.c_size_t(0), C.c_size_t(0)
+    lib = N.library()
+    rc = N.with_workspace(lambda ws, nb: lib.sp_plan_dp_devices_workspace_bytes(
+        b.struct(), C.cast(arr, C.c_void_p), 3, C.byref(ws_min), C.byref(pmin), C.byref(pfull), ws, nb,
+        N.stream_ptr()))
+    assert rc == 0, lib.sp_last_error()
+    assert 0 < pmin.value <= pfull.value
+    for size, ok in ((pmin.value, True), (pfull.value, True), (pmin.value - 4096, False)):
+        parts = [torch.empty(size, dtype=torch.uint8, device="cuda") for _ in devices]
+        wptr = (C.c_void_p * 3)(*[t.data_ptr() for t in parts])
+        wlen = (C.c_size_t * 3)(*[size] * 3)
+        out = B.PolicyBatch.empty(b.n, b.total_layers, b.r.device)
+        ws = N.workspace(ws_min.value)
+        rc = lib.sp_plan_dp_devices(b.struct(), out.struct(), C.cast(arr, C.c_void_p), 3, N.ptr(ws), ws.numel(),
+                                    C.cast(wptr, C.c_void_p), C.cast(wlen, C.c_void_p), N.stream_ptr())
+        torch.cuda.synchronize()
+        if ok:
+            assert rc == 0, lib.sp_last_error()
+            _compare(bat, "dp", out.to_host())
+        else:
+            assert rc == N.SP_ERR_WORKSPACE, lib.sp_last_error()
+
+
+def test_exhaustive_rejects_long_instances(gpu):
+    """sp_plan_exhaustive checks L <= 24 itself (no 2^L overflow / index
+    overrun), whatever the Python wrapper knows about the lengths."""
+    from paper_2410_10759_b200 import _native as N, batch as B
+    L = 30
+    b = B.InstanceBatch.from_arrays([0, L], np.ones(L), np.ones(L), np.ones(L), np.ones(L), np.ones(L), [10], [1])
+    out = B.PolicyBatch.empty(1, L, b.r.device)
+    rc = N.library().sp_plan_exhaustive(b.struct(), out.struct(), N.stream_ptr())
+    assert rc == N.SP_ERR_UNSUPPORTED
+    b.n_layers_host = None  # the batched planner derives the lengths from the device offsets
+    from paper_2410_10759_b200.planner import plan_batch
+    with pytest.raises(ValueError, match="oracle limited to 24 layers"):
+        plan_batch("oracle", b)
+
+
+def test_build_dp_tables_checks_w_eff(gpu):
+    """sp_build_dp_tables refuses tables sized for another W_eff before writing."""
+    import torch
+    from paper_2410_10759_b200 import _native as N, batch as B
+    b = B.InstanceBatch.from_arrays([0, 3], [2, 2, 2], [1, 1, 1], [1, 1, 1], [1, 1, 1], [1.0, 2.0, 3.0], [5], [1])
+    C = torch.empty((4, 3), dtype=torch.float64, device="cuda")
+    S = torch.empty_like(C)
+    rc = N.with_workspace(lambda ws, nb: N.library().sp_build_dp_tables(b.struct(), 2, N.ptr(C), N.ptr(S), ws, nb,
+                                                                        N.stream_ptr()))
+    assert rc == N.SP_ERR_INVALID and b"does not match" in N.library().sp_last_error()
 
 
 def test_plan_dp_devices_rejects_bad_lists(gpu):
