@@ -152,7 +152,8 @@ VARIANTS = ["dp_stage_kernel<smem rows>", "dp_cluster_kernel<DSMEM rows>",
             "dp_stage_kernel<global rows>", "dp_coop_kernel<L2 rows>",
             "dp_stream_kernel<L2 rows, bulk-copy staged windows>",
             "dp_grid_kernel<one instance over the GPU>",
-            "dp_own_kernel<own block in SMEM, remote windows via L2>"]
+            "dp_own_kernel<own block in SMEM, remote windows via L2>",
+            "dp_steps_kernel<rows as breakpoint lists>"]
 NCU_SUMMARY = {0: "dp_smem_ncu_summary.json", 3: "dp_coop_ncu_summary.json",
                4: "dp_stream_ncu_summary.json"}
 

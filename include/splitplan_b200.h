@@ -82,6 +82,9 @@ size_t sp_last_required_workspace(void);
  * wave-path instance in ONE wave and kept every back-pointer stage of the
  * whole-GPU ones (no recompute); a caller growing its workspace uses it */
 size_t sp_last_full_workspace(void);
+/* after sp_plan_dp: instances whose rows outgrew the breakpoint lists and
+ * were re-solved on the dense kernels */
+int64_t sp_last_dense_fallbacks(void);
 
 /* Instrumentation (thread-local, off by default).  While enabled, every
  * DP-stage kernel launch is bracketed by CUDA events on its stream and every

@@ -98,6 +98,7 @@ SIGNATURES = {
     "sp_last_error": (C.c_char_p, []),
     "sp_last_required_workspace": (C.c_size_t, []),
     "sp_last_full_workspace": (C.c_size_t, []),
+    "sp_last_dense_fallbacks": (C.c_int64, []),
     "sp_profile_enable": (None, [C.c_int]),
     "sp_profile_collect": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                      C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -265,6 +266,7 @@ def grow_workspace_hint(full_bytes: int) -> None:
     dev = device()
     cur = _ws.get(dev.index)
     have = cur.numel() if cur is not None else 0
+    del cur  # no reference may keep the old buffer alive while it is replaced
     target = min(int(full_bytes), workspace_cap(dev), have + int(free_bytes(dev) * 0.9))
     if target <= have + (have >> 2):  # not worth a reallocation
         return
@@ -287,6 +289,7 @@ def with_workspace(fn, *args):
         need = int(library().sp_last_required_workspace())
         if need <= ws.numel():
             break
+        del ws  # released before the larger buffer is allocated
         ws = workspace(need + (1 << 20))
         rc = fn(*args, ptr(ws), C.c_size_t(ws.numel()))
     return rc

@@ -28,13 +28,22 @@ __device__ __forceinline__ double to_f64(int32_t v, double g) {
 }
 __device__ __forceinline__ double to_f64(double v, double) { return v; }
 
+// binary (Stein) gcd: shifts and subtractions, no 64-bit division
 __device__ __forceinline__ uint64_t gcd_u64(uint64_t a, uint64_t b) {
-  while (b) {
-    uint64_t t = a % b;
-    a = b;
-    b = t;
-  }
-  return a;
+  if (a == 0) return b;
+  if (b == 0) return a;
+  const int shift = __ffsll((long long)(a | b)) - 1;
+  a >>= __ffsll((long long)a) - 1;
+  do {
+    b >>= __ffsll((long long)b) - 1;
+    if (a > b) {
+      const uint64_t t = a;
+      a = b;
+      b = t;
+    }
+    b -= a;
+  } while (b);
+  return a << shift;
 }
 
 // ---------------------------------------------------------------------------
@@ -71,10 +80,17 @@ __global__ void weff_kernel(sp_instances in, int64_t* w_eff) {
 // ---------------------------------------------------------------------------
 // prep: W_eff, value domain, clamped shifts, scaled values
 
-__global__ void prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts, int64_t* rv, int2* reach) {
+// flag (optional): set to 1 for every instance (the breakpoint-list tier
+// clears it for the instances it solves).  steps_cols > 0: instances the
+// breakpoint-list tier takes (not NaN, narrower than steps_cols) get the
+// trivial frontier (0, 0) instead of the sequential recurrence -- only the
+// dense kernels use it, and it is exact to skip nothing.
+__global__ void __launch_bounds__(128) prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts, int64_t* rv,
+                                                   int2* reach, int32_t* flag, int64_t steps_cols = 0) {
   __shared__ int64_t sh64[32];
   __shared__ uint64_t shu[32];
   __shared__ int shi[32];
+  __shared__ StageShift tile[128];
   for (int64_t k = blockIdx.x; k < in.n; k += gridDim.x) {
     const int64_t lo = in.layer_off[k], hi = in.layer_off[k + 1];
     int64_t worst = 0;
@@ -93,11 +109,38 @@ __global__ void prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts,
         g = gcd_u64(g, v);
       }
     }
-    worst = block_reduce(worst, [](int64_t a, int64_t b) { return a + b; }, sh64);
-    finite = block_reduce(finite, [](int a, int b) { return a & b; }, shi);
-    integral = block_reduce(integral, [](int a, int b) { return a & b; }, shi);
-    isum = block_reduce(isum, [](uint64_t a, uint64_t b) { return min(a + b, (uint64_t)1 << 62); }, shu);
-    g = block_reduce(g, [](uint64_t a, uint64_t b) { return gcd_u64(a, b); }, shu);
+    {  // the five block reductions in one pass: warp shuffles, one barrier
+      const uint64_t sat = (uint64_t)1 << 62;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        worst += __shfl_xor_sync(0xffffffffu, worst, o);
+        finite &= __shfl_xor_sync(0xffffffffu, finite, o);
+        integral &= __shfl_xor_sync(0xffffffffu, integral, o);
+        isum = min(isum + __shfl_xor_sync(0xffffffffu, isum, o), sat);
+        g = gcd_u64(g, __shfl_xor_sync(0xffffffffu, g, o));
+      }
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+      if (lane == 0) {
+        sh64[wid] = worst;
+        shi[wid] = finite & integral ? 3 : (finite ? 1 : (integral ? 2 : 0));
+        shu[wid] = isum;
+        shu[16 + wid] = g;
+      }
+      __syncthreads();
+      worst = sh64[0];
+      int fi = shi[0];
+      isum = shu[0];
+      g = shu[16];
+      for (int w = 1; w < nw; ++w) {
+        worst += sh64[w];
+        fi &= shi[w];
+        isum = min(isum + shu[w], sat);
+        g = gcd_u64(g, shu[16 + w]);
+      }
+      finite = fi & 1;
+      integral = (fi >> 1) & 1;
+      __syncthreads();  // the scratch is reused by the next instance
+    }
     if (g == 0) g = 1;
     const int64_t W = min(in.budget[k], worst);
     int32_t mode;
@@ -113,41 +156,51 @@ __global__ void prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts,
       r.mode = mode;
       r.pad = 0;
       info[k] = r;
+      if (flag) flag[k] = 1;
     }
     const int64_t cap = min(W + 1, kMaxCols);
-    for (int64_t l = lo + threadIdx.x; l < hi; l += blockDim.x) {
-      const int64_t i = in.client_units[l], s = in.server_units[l];
-      const int64_t u = in.up_units[l], d = in.down_units[l];
-      StageShift sh;
-      sh.i = (int32_t)min(i, cap);
-      sh.id = (int32_t)min(i + d, cap);
-      sh.s = (int32_t)min(s, cap);
-      sh.su = (int32_t)min(s + u, cap);
-      shifts[l] = sh;
-      const double r = in.r[l];
-      if (mode == VM_INT32) {
-        rv[l] = (int64_t)((uint64_t)r / g);
-      } else {
-        rv[l] = __double_as_longlong(r);
-      }
-    }
     // reachable frontier: the first column of row k of C and of S that holds a
     // reachable value (rows are monotone in j; every column below it is
     // unreachable, NEG-like).  reach[lo + k] describes the row stage k reads.
-    // Not in the NaN domain, where "unreachable" cells may hold NaN.
-    __syncthreads();  // the block's clamped shifts are in global memory
-    if (threadIdx.x == 0 && reach) {
-      const bool sac = in.source_at_client[k] != 0;
-      int64_t mc = sac ? 0 : cap, ms = sac ? cap : 0;
-      for (int64_t l = lo; l < hi; ++l) {
-        reach[l] = mode == VM_F64_NAN ? make_int2(0, 0) : make_int2((int)min(mc, cap), (int)min(ms, cap));
-        const StageShift sh = shifts[l];
-        const int64_t nc = min(mc + sh.i, ms + sh.id), ns = min(ms + sh.s, mc + sh.su);
-        mc = min(nc, cap);
-        ms = min(ns, cap);
+    // Not in the NaN domain, where "unreachable" cells may hold NaN.  The
+    // recurrence is sequential: the block stages each tile of clamped shifts
+    // in shared memory and thread 0 walks it there.
+    const bool sac = in.source_at_client[k] != 0;
+    int64_t mc = sac ? 0 : cap, ms = sac ? cap : 0;
+    const bool trivial = mode == VM_F64_NAN || (steps_cols > 0 && W + 1 < steps_cols);
+    for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
+      const int64_t l = t0 + threadIdx.x;
+      if (l < hi) {
+        const int64_t i = in.client_units[l], s = in.server_units[l];
+        const int64_t u = in.up_units[l], d = in.down_units[l];
+        StageShift sh;
+        sh.i = (int32_t)min(i, cap);
+        sh.id = (int32_t)min(i + d, cap);
+        sh.s = (int32_t)min(s, cap);
+        sh.su = (int32_t)min(s + u, cap);
+        shifts[l] = sh;
+        tile[threadIdx.x] = sh;
+        if (trivial && reach) reach[l] = make_int2(0, 0);
+        const double r = in.r[l];
+        if (mode == VM_INT32) {
+          rv[l] = (int64_t)((uint64_t)r / g);
+        } else {
+          rv[l] = __double_as_longlong(r);
+        }
       }
+      __syncthreads();
+      if (threadIdx.x == 0 && reach && !trivial) {
+        const int cnt = (int)min((int64_t)blockDim.x, hi - t0);
+        for (int x = 0; x < cnt; ++x) {
+          reach[t0 + x] = make_int2((int)min(mc, cap), (int)min(ms, cap));
+          const StageShift sh = tile[x];
+          const int64_t nc = min(mc + sh.i, ms + sh.id), ns = min(ms + sh.s, mc + sh.su);
+          mc = min(nc, cap);
+          ms = min(ns, cap);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -158,11 +211,12 @@ __global__ void prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts,
 // once per layer k (planner.py:128-143):
 //   C_k[j] = r_k + max(C_{k-1}[j - i_k], S_{k-1}[j - i_k - d_k])
 //   S_k[j] =       max(S_{k-1}[j - s_k], C_{k-1}[j - s_k - u_k])
-// Three variants hold the rows in different places:
+// The dense variants hold the rows in different places:
 //   * dp_stage_kernel<ROWS_SMEM=true>   one CTA, rows in its SMEM
-//   * dp_cluster_kernel                 a thread-block cluster, rows split
-//                                       across the CTAs' distributed SMEM
 //   * dp_stage_kernel<ROWS_SMEM=false>  one CTA, rows in global memory
+//   * dp_stream_kernel (dp_stream.cuh)  a cluster, rows in L2-resident global memory
+//   * dp_grid_kernel (dp_grid.cuh)      the whole GPU / capacity partitions
+// (dp_steps.cuh holds the rows as breakpoint lists instead.)
 // Single-CTA variants update the rows IN PLACE, walking 32-aligned chunks of
 // CH = E*T columns from the top down: a chunk computes its new cells into
 // registers (its reads only touch columns <= its own, which no later chunk of
@@ -194,6 +248,7 @@ struct DpArgs {
   uint8_t* rows;
   double* tab_c;  // optional full-table output (build_dp_tables), n == 1
   double* tab_s;
+  int32_t* overflow;  // [n] breakpoint-list kernel: 1 = a row exceeded its capacity
 };
 
 __host__ __device__ inline int bp_words(int mode) { return mode == VM_F64_NAN ? 4 : 2; }

@@ -11,6 +11,7 @@ namespace {
 thread_local char g_err[1024] = "";
 thread_local size_t g_required_ws = 0;
 thread_local size_t g_full_ws = 0;
+thread_local int64_t g_steps_overflow = 0;
 
 struct DpRec {
   cudaEvent_t a, b;
@@ -46,6 +47,7 @@ int launch_check(const char* what) {
 
 void set_required_workspace(size_t bytes) { g_required_ws = bytes; }
 void set_full_workspace(size_t bytes) { g_full_ws = bytes; }
+void set_steps_overflow(int64_t n) { g_steps_overflow = n; }
 
 bool profiling() { return g_prof; }
 
@@ -98,5 +100,7 @@ const char* sp_last_error(void) { return g_err; }
 size_t sp_last_required_workspace(void) { return g_required_ws; }
 
 size_t sp_last_full_workspace(void) { return g_full_ws; }
+
+int64_t sp_last_dense_fallbacks(void) { return g_steps_overflow; }
 
 }  // extern "C"

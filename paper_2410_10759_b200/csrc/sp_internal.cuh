@@ -18,6 +18,7 @@ void set_error(int code, const char* fmt, ...);
 int check_cuda(cudaError_t err, const char* what);
 void set_required_workspace(size_t bytes);
 void set_full_workspace(size_t bytes);
+void set_steps_overflow(int64_t n);  // instances the last sp_plan_dp re-solved densely
 int launch_check(const char* what);  // also counts the launch when profiling
 
 // profiling (sp_abi.cu): events around DP-stage launches

@@ -8,6 +8,8 @@
 //                      windows)
 //   dp_grid.cuh        K2 for one huge instance (cfg5): dp_grid_kernel over
 //                      capacity partitions, checkpoint/backtrack kernels
+//   dp_steps.cuh       K2 / K3 on breakpoint lists (rows as step functions):
+//                      dp_steps_kernel, backtrack_steps_kernel
 //   this file          backtrack_kernel (K3: end-side choice + pointer walk +
 //                      _finish, planner.py:88-107, 146-202), prefix_kernel
 //                      (greedy / all-server / all-client, planner.py:205-225),
@@ -31,12 +33,14 @@ namespace {
 constexpr int kStageTile = 128;          // stage records staged in SMEM at a time
 constexpr size_t kSmemCap = 227 * 1024;  // sm_100a max dynamic SMEM per CTA
 constexpr int64_t kMaxCols = (int64_t(1) << 31) - 64;
+constexpr int64_t kGridMinColsSteps = (int64_t)1 << 22;  // == kGridMinCols: whole-GPU widths stay dense
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 #include "dp_core.cuh"
 #include "dp_stream.cuh"
 #include "dp_grid.cuh"
+#include "dp_steps.cuh"
 
 // ---------------------------------------------------------------------------
 // _finish over caller-supplied placements
@@ -356,7 +360,7 @@ size_t stage_bytes_mode(int mode) {
   return align_up(kStageTile * (sizeof(StageShift) + value_bytes(mode)), 16);
 }
 
-enum DpVariant { DPV_SMEM = 0, DPV_GLOBAL = 2, DPV_STREAM = 4 };
+enum DpVariant { DPV_SMEM = 0, DPV_GLOBAL = 2, DPV_STREAM = 4, DPV_STEPS = 7 };
 
 // ---- single-CTA kernels: T x E configurations ------------------------------
 
@@ -595,6 +599,53 @@ int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t
   return launch_stream_t<MODE, 256, 4, NS, 1, kStreamBufs>(a, n_items, geo, st);
 }
 
+// ---- breakpoint-list kernels ------------------------------------------------
+
+// tier geometry: lanes per instance and warps per block
+#ifndef SP_STEPS_G
+#define SP_STEPS_G 32
+#endif
+template <int CAP> constexpr int steps_group() { return CAP >= 1024 ? 32 : SP_STEPS_G; }
+template <int CAP> constexpr int steps_wpb() { return CAP >= 1024 ? 1 : 4; }
+size_t steps_smem(int mode, int cap) {
+  const int G = cap >= 1024 ? 32 : SP_STEPS_G, WPB = cap >= 1024 ? 1 : 4;
+  return (size_t)WPB * (32 / G) * 6 * (size_t)cap * (4 + value_bytes(mode));
+}
+
+template <int MODE, int CAP>
+int launch_steps_t(const StepsArgs& sa, cudaStream_t st) {
+  constexpr int G = steps_group<CAP>(), WPB = steps_wpb<CAP>(), PER_BLOCK = WPB * (32 / G);
+  auto kern = dp_steps_kernel<MODE, CAP, G, WPB>;
+  const size_t smem = steps_smem(MODE, CAP);
+  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                      "cudaFuncSetAttribute(dp_steps_kernel)");
+  if (rc) return rc;
+  kern<<<(unsigned)((sa.n_items + PER_BLOCK - 1) / PER_BLOCK), WPB * 32, smem, st>>>(sa);
+  return launch_check("dp_steps_kernel launch");
+}
+int launch_steps(int mode, int cap, const StepsArgs& sa, cudaStream_t st) {
+  if (sa.n_items == 0) return SP_OK;
+  if (cap == kStepsCap)
+    return mode == VM_INT32 ? launch_steps_t<VM_INT32, kStepsCap>(sa, st) : launch_steps_t<VM_F64, kStepsCap>(sa, st);
+  return mode == VM_INT32 ? launch_steps_t<VM_INT32, kStepsCapWide>(sa, st)
+                          : launch_steps_t<VM_F64, kStepsCapWide>(sa, st);
+}
+
+template <int CAP>
+int launch_backtrack_steps_t(const sp_instances& in, const StepsArgs& sa, int32_t* idx, const sp_policies& out,
+                             cudaStream_t st) {
+  constexpr int G = CAP >= 1024 ? 32 : 8, WPB = 4, PER_BLOCK = WPB * (32 / G);
+  backtrack_steps_kernel<CAP, G, WPB><<<(unsigned)((sa.n_items + PER_BLOCK - 1) / PER_BLOCK), WPB * 32, 0, st>>>(
+      in, sa, idx, out);
+  return launch_check("backtrack_steps_kernel launch");
+}
+int launch_backtrack_steps(int cap, const sp_instances& in, const StepsArgs& sa, int32_t* idx,
+                           const sp_policies& out, cudaStream_t st) {
+  if (sa.n_items == 0) return SP_OK;
+  return cap == kStepsCap ? launch_backtrack_steps_t<kStepsCap>(in, sa, idx, out, st)
+                          : launch_backtrack_steps_t<kStepsCapWide>(in, sa, idx, out, st);
+}
+
 int forced_variant() {
   const char* v = getenv("SPLITPLAN_DP_VARIANT");
   if (!v) return -1;
@@ -602,6 +653,7 @@ int forced_variant() {
   if (!strcmp(v, "global")) return DPV_GLOBAL;
   if (!strcmp(v, "stream")) return DPV_STREAM;
   if (!strcmp(v, "grid")) return 5;  // DPV_GRID
+  if (!strcmp(v, "steps")) return DPV_STEPS;
   return -1;
 }
 
@@ -609,7 +661,7 @@ int forced_variant() {
 // workspace / shared memory it needs.
 struct DpPlan {
   int variant = DPV_SMEM;
-  int cfg = 0;                  // single-CTA T x E configuration
+  int cfg = 0;                  // single-CTA T x E configuration; breakpoint-list capacity (DPV_STEPS)
   int threads = 0;
   StreamGeom sgeo{0, 0, 0, 0};  // stream
   size_t bp = 0, rows = 0, smem = 0;
@@ -621,8 +673,24 @@ struct DpPlan {
   }
 };
 
-DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) {
+// steps_eligible: the breakpoint-list kernels may take the instance (not for
+// full tables, not in the NaN domain, not at whole-GPU widths)
+bool steps_eligible(int mode, int64_t ncol, int force, bool tables) {
+  return !tables && mode != VM_F64_NAN && ncol < kGridMinColsSteps && (force < 0 || force == DPV_STEPS);
+}
+
+// `steps_cap` > 0: plan the breakpoint-list kernel with that capacity (the
+// caller checked steps_eligible); 0: a dense kernel.
+DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables, int steps_cap = 0) {
   DpPlan p;
+  if (steps_cap > 0) {
+    p.variant = DPV_STEPS;
+    p.cfg = steps_cap;
+    p.threads = (steps_cap >= 1024 ? 1 : 4) * 32;
+    p.smem = steps_smem(mode, steps_cap);
+    p.bp = align_up(steps_store_bytes((int)L, steps_cap), 256);
+    return p;
+  }
   const size_t vb = value_bytes(mode);
   p.cfg = single_cfg_for(ncol, (force == DPV_GLOBAL || tables) ? VM_F64 : mode);
   const size_t single_rows = single_row_bytes(mode, ncol, p.cfg);
@@ -656,6 +724,19 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables) 
 int launch_plan(int mode, const DpPlan& p, const DpArgs& a, int64_t n_items, cudaStream_t st) {
   if (n_items == 0) return SP_OK;
   switch (p.variant) {
+    case DPV_STEPS: {
+      StepsArgs sa = {};
+      sa.layer_off = a.layer_off;
+      sa.sac = a.sac;
+      sa.info = a.info;
+      sa.shifts = a.shifts;
+      sa.rv = a.rv;
+      sa.work = a.work;
+      sa.store = a.bp;
+      sa.overflow = a.overflow;
+      sa.n_items = n_items;
+      return launch_steps(mode, p.cfg, sa, st);
+    }
     case DPV_STREAM:
       switch (mode) {
         case VM_INT32: return launch_stream<VM_INT32>(a, n_items, p.sgeo, st);
@@ -681,6 +762,7 @@ int launch_plan(int mode, const DpPlan& p, const DpArgs& a, int64_t n_items, cud
 // read + write of both rows plus those bits
 double hbm_bytes_per_cell(int mode, int variant) {
   const double bits = bp_words(mode) * 4.0 / 32.0;
+  if (variant == DPV_STEPS) return 0.0;  // list bytes depend on the data, not the cells
   return variant == DPV_GLOBAL ? 4.0 * (double)value_bytes(mode) + bits : bits;
 }
 
@@ -1228,16 +1310,68 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   DpWork* work = (DpWork*)cv.take(sizeof(DpWork) * n);
   int2* reach = (int2*)cv.take(sizeof(int2) * total);
   int64_t* gstate = (int64_t*)cv.take(64);
+  int32_t* overflow = (int32_t*)cv.take(sizeof(int32_t) * n);
+  int32_t* flag = (int32_t*)cv.take(sizeof(int32_t) * n);
+  unsigned long long* solved = (unsigned long long*)cv.take(2 * sizeof(unsigned long long));
   const size_t fixed = align_up(cv.used, 256);
   if (!ws || fixed > ws_bytes) {
     set_required_workspace(fixed + (1 << 20));
     set_error(SP_ERR_WORKSPACE, "workspace %zu B < fixed part %zu B", ws_bytes, fixed);
     return SP_ERR_WORKSPACE;
   }
+  const int force = forced_variant();
+  const bool steps_ok = tab_c == nullptr && !q_min && (force < 0 || force == DPV_STEPS);
   const int grid = (int)std::min<int64_t>(n, 1 << 20);
-  prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv, reach);
+  const bool tier1_fits = steps_ok && out && fixed + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap) <= ws_bytes;
+  prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv, reach, steps_ok ? flag : nullptr,
+                                    tier1_fits ? kGridMinColsSteps : 0);
   int rc = launch_check("prep_kernel launch");
   if (rc) return rc;
+  uint8_t* dyn = (uint8_t*)ws + fixed;
+
+  // Tier 1, planned on the device: one warp per instance on breakpoint lists
+  // of kStepsCap breakpoints, every store at a position the kernel computes
+  // itself -- no host planning, one synchronisation for the whole batch.
+  // Instances it cannot take (NaN domain, whole-GPU width, more breakpoints)
+  // keep their flag and go through the host-planned tiers below.
+  bool tier1 = false;
+  if (tier1_fits) {
+    tier1 = true;
+    StepsArgs sa = {};
+    sa.layer_off = in->layer_off;
+    sa.sac = in->source_at_client;
+    sa.info = info;
+    sa.shifts = shifts;
+    sa.rv = rv;
+    sa.store = dyn;
+    sa.flag = flag;
+    sa.solved = solved;
+    sa.n_items = n;
+    sa.max_cols = kGridMinColsSteps;
+    rc = check_cuda(cudaMemsetAsync(solved, 0, 2 * sizeof(unsigned long long), st), "zero solved count");
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (!rc && profiling()) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, st);
+    }
+    if (!rc) rc = launch_steps(VM_INT32, kStepsCap, sa, st);
+    if (!rc) rc = launch_steps(VM_F64, kStepsCap, sa, st);
+    if (!rc && profiling()) cudaEventRecord(e1, st);
+    if (!rc) rc = launch_backtrack_steps(kStepsCap, *in, sa, idx, *out, st);
+    unsigned long long hsolved[2] = {0, 0};  // instances, DP cells
+    if (!rc)
+      rc = check_cuda(cudaMemcpyAsync(hsolved, solved, sizeof(hsolved), cudaMemcpyDeviceToHost, st),
+                      "copy solved count");
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync after breakpoint lists");
+    if (rc) return rc;
+    if (e1) prof_record_dp(e0, e1, (double)hsolved[1], 0.0, DPV_STEPS);
+    if (hsolved[0] == (unsigned long long)n) {
+      set_full_workspace(fixed + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap));
+      set_steps_overflow(0);
+      return SP_OK;
+    }
+  }
 
   std::vector<InstInfo> hinfo(n);
   std::vector<int64_t> hoff(n + 1);
@@ -1257,8 +1391,14 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     return SP_ERR_INVALID;
   }
   const size_t avail = ws_bytes - fixed;
-  uint8_t* dyn = (uint8_t*)ws + fixed;
-  const int force = forced_variant();
+  std::vector<int32_t> hflag;
+  if (tier1) {  // the instances tier 1 left: the next tiers take only them
+    hflag.resize(n);
+    rc = check_cuda(cudaMemcpyAsync(hflag.data(), flag, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st),
+                    "copy tier-1 flags");
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync");
+    if (rc) return rc;
+  }
   struct Item {
     int64_t inst, L, ncol;
     int mode;
@@ -1269,7 +1409,9 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   DpPlan cached;
   int cached_mode = -1;
   int64_t cached_ncol = -1, cached_L = -1;
+  int cached_cap = -1;
   for (int64_t k = 0; k < n; ++k) {
+    if (tier1 && !hflag[k]) continue;  // solved on breakpoint lists
     const int64_t ncol = hinfo[k].w_eff + 1;
     if (ncol > kMaxCols) {
       set_error(SP_ERR_UNSUPPORTED, "instance %lld: W_eff = %lld exceeds the supported 2^31 columns",
@@ -1281,11 +1423,20 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     it.L = hoff[k + 1] - hoff[k];
     it.ncol = ncol;
     it.mode = hinfo[k].mode;
-    if (it.mode != cached_mode || ncol != cached_ncol || it.L != cached_L) {
-      cached = plan_instance(it.mode, it.L, ncol, force, tab_c != nullptr);
+    // breakpoint lists first (tier 1 if it did not run, else the wide tier)
+    // (a tier whose store does not fit the workspace is skipped: the tiers are
+    // an optimisation, the dense kernels the guarantee)
+    int cap = steps_ok && steps_eligible(it.mode, ncol, force, tab_c != nullptr)
+                  ? (tier1 ? kStepsCapWide : kStepsCap)
+                  : 0;
+    if (cap == kStepsCap && align_up(steps_store_bytes((int)it.L, cap), 256) > avail) cap = kStepsCapWide;
+    if (cap == kStepsCapWide && align_up(steps_store_bytes((int)it.L, cap), 256) > avail) cap = 0;
+    if (it.mode != cached_mode || ncol != cached_ncol || it.L != cached_L || cap != cached_cap) {
+      cached = plan_instance(it.mode, it.L, ncol, force, tab_c != nullptr, cap);
       cached_mode = it.mode;
       cached_ncol = ncol;
       cached_L = it.L;
+      cached_cap = cap;
     }
     it.plan = cached;
     items.push_back(it);
@@ -1378,8 +1529,8 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   a.rows = dyn;
   a.tab_c = tab_c;
   a.tab_s = tab_s;
+  a.overflow = overflow;
 
-  size_t pos = 0;
   std::vector<DpWork> hwork;
   struct Group {
     int mode;
@@ -1388,6 +1539,8 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     std::vector<DpWork> items;
   };
   std::vector<Group> groups;
+  auto run_waves = [&](const std::vector<Item>& items) -> int {
+  size_t pos = 0;
   while (pos < items.size()) {
     // gather one wave that fits the workspace
     size_t end = pos, wave_bytes = 0;
@@ -1455,17 +1608,63 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       }
       first += cnt;
     }
-    if (out) {
-      const int64_t nw = (int64_t)hwork.size();
-      backtrack_kernel<<<(unsigned)((nw + 127) / 128), 128, 0, st>>>(*in, info, shifts, work, nw, dyn,
-                                                                      idx, *out);
-      rc = launch_check("backtrack_kernel launch");
-      if (rc) return rc;
+    if (out) {  // K3 per group: bit back-pointers or breakpoint lists
+      first = 0;
+      for (const Group& g : groups) {
+        const int64_t cnt = (int64_t)g.items.size();
+        if (g.plan.variant == DPV_STEPS) {
+          StepsArgs sa = {};
+          sa.layer_off = in->layer_off;
+          sa.info = info;
+          sa.shifts = shifts;
+          sa.rv = rv;
+          sa.work = work + first;
+          sa.store = dyn;
+          sa.overflow = overflow;
+          sa.n_items = cnt;
+          rc = launch_backtrack_steps(g.plan.cfg, *in, sa, idx, *out, st);
+        } else {
+          backtrack_kernel<<<(unsigned)((cnt + 127) / 128), 128, 0, st>>>(*in, info, shifts, work + first, cnt,
+                                                                            dyn, idx, *out);
+          rc = launch_check("backtrack_kernel launch");
+        }
+        if (rc) return rc;
+        first += cnt;
+      }
     }
     // the host work vector is reused next wave: the pageable H2D copy above is
     // synchronous with respect to the host buffer, so reuse is safe.
     pos = end;
   }
+  return SP_OK;
+  };
+  // instances whose rows outgrew the breakpoint lists move up a tier:
+  // kStepsCap -> kStepsCapWide -> the dense kernels
+  int64_t dense_fallbacks = 0;
+  while (!items.empty()) {
+    rc = run_waves(items);
+    if (rc) return rc;
+    bool any_steps = false;
+    for (const Item& it : items) any_steps |= it.plan.variant == DPV_STEPS;
+    if (!any_steps) break;
+    std::vector<int32_t> hover(n);
+    rc = check_cuda(cudaMemcpyAsync(hover.data(), overflow, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st),
+                    "copy overflow flags");
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync overflow flags");
+    if (rc) return rc;
+    std::vector<Item> redo;
+    for (const Item& it : items) {
+      if (it.plan.variant != DPV_STEPS || !hover[it.inst]) continue;
+      Item r = it;
+      int next = it.plan.cfg == kStepsCap ? kStepsCapWide : 0;
+      if (next && align_up(steps_store_bytes((int)it.L, next), 256) > avail) next = 0;
+      r.plan = plan_instance(it.mode, it.L, it.ncol, force == DPV_STEPS ? -1 : force, false, next);
+      dense_fallbacks += next == 0;
+      redo.push_back(r);
+    }
+    items.swap(redo);
+  }
+  set_steps_overflow(dense_fallbacks);
   return SP_OK;
 }
 
@@ -1632,7 +1831,7 @@ int sp_grid_plan_make(const sp_instances* in, int32_t nparts, int32_t ctas_per_p
     set_error(SP_ERR_WORKSPACE, "sp_grid_plan_make needs %zu B of scratch", align_up(cv.used, 256));
     return SP_ERR_WORKSPACE;
   }
-  prep_kernel<<<1, 128, 0, st>>>(*in, info, shifts, rv, reach);
+  prep_kernel<<<1, 128, 0, st>>>(*in, info, shifts, rv, reach, nullptr);
   rc = launch_check("prep_kernel launch");
   InstInfo hinfo;
   uint8_t sac = 0;
@@ -1706,7 +1905,7 @@ int sp_grid_part_prepare(const sp_grid_plan* plan, const sp_instances* in, void*
   cudaStream_t st = (cudaStream_t)stream;
   rc = check_cuda(cudaMemsetAsync(g.state(pw), 0, 128, st), "zero partition state");
   if (rc) return rc;
-  prep_kernel<<<1, 128, 0, st>>>(*in, g.info(pw), g.shifts(pw), g.rv(pw), g.reach(pw));
+  prep_kernel<<<1, 128, 0, st>>>(*in, g.info(pw), g.shifts(pw), g.rv(pw), g.reach(pw), nullptr);
   return launch_check("prep_kernel launch");
 }
 

@@ -14,7 +14,7 @@ HEADER = ROOT / "include" / "splitplan_b200.h"
 
 def declared_functions() -> list[str]:
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|void|size_t|const char\s*\*)\s*(sp_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|size_t|const char\s*\*)\s*(sp_\w+)\s*\(",
                                  text, flags=re.M)))
 
 

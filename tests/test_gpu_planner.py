@@ -397,11 +397,17 @@ def test_reachable_frontier_skips(gpu, variant, no_reach, monkeypatch):
         _compare(bat, "dp", B.plan_dp(_batch(bat, with_must=must)).to_host())
 
 
-def test_dp_workspace_query(gpu):
+@pytest.mark.parametrize("variant", ["stream", ""])
+def test_dp_workspace_query(gpu, variant, monkeypatch):
     """sp_plan_dp_workspace_bytes: plan_dp runs in exactly the reported minimum
-    workspace (bit-exact), and fails cleanly below it."""
+    workspace (bit-exact).  The minimum covers the dense kernels every
+    instance may fall back to; with the dense kernels forced, one page less
+    fails cleanly (by default the breakpoint lists may still fit: then the
+    result must be bit-exact)."""
     import torch
     from paper_2410_10759_b200 import _native as N, batch as B
+    if variant:
+        monkeypatch.setenv("SPLITPLAN_DP_VARIANT", variant)
     bat = Battery("battery_large_model")
     b = _batch(bat)
     mn, full = B.dp_workspace_bytes(b)
@@ -412,8 +418,73 @@ def test_dp_workspace_query(gpu):
         out = B.PolicyBatch.empty(b.n, b.total_layers, b.r.device)
         rc = lib.sp_plan_dp(b.struct(), out.struct(), N.ptr(ws), size, N.stream_ptr())
         torch.cuda.synchronize()
-        if ok:
+        if ok or (rc == 0 and not variant):
             assert rc == 0, N.library().sp_last_error()
             _compare(bat, "dp", out.to_host())
         else:
             assert rc == N.SP_ERR_WORKSPACE
+
+
+# ---------------------------------------------------------------------------
+# breakpoint lists (dp_steps.cuh): rows as step functions, stay_from back-pointers
+
+
+@pytest.mark.parametrize("name", BATTERIES + ["battery_large_model", "battery_large_chain"])
+def test_breakpoint_lists_match_reference(gpu, name, monkeypatch):
+    """The breakpoint-list tiers alone (instances they cannot hold fall back to
+    the dense kernels): bit-exact on every reference battery, including the
+    survey's fp-absorption vector and must_end_at."""
+    from paper_2410_10759_b200 import batch as B
+    monkeypatch.setenv("SPLITPLAN_DP_VARIANT", "steps")
+    bat = Battery(name)
+    _compare(bat, "dp", B.plan_dp(_batch(bat, with_must=name != "battery_large_chain")).to_host())
+
+
+def _dense_rows_instances(seed, n):
+    """Every third instance has random float r and shifts of 0..60 over 600
+    stages and 30,001 columns: rows of ~1,250 breakpoints, more than both
+    breakpoint tiers hold (dense fallback); the others have small integer r
+    (a few breakpoints, tier 1)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for t in range(n):
+        hard = t % 3 == 0
+        L, W, hi = (600, 30000, 60) if hard else (160, 3000, 400)
+        out.append(dict(i=rng.integers(0, hi, L), s=rng.integers(0, hi, L), u=rng.integers(0, hi, L),
+                        d=rng.integers(0, hi, L),
+                        r=(rng.random(L) * 50 if hard else rng.integers(0, 5, L).astype(float)),
+                        budget=int(W), sac=bool(t % 2)))
+    return out
+
+
+@pytest.mark.parametrize("ws_kind", ["large", "small"])
+def test_breakpoint_tiers_and_fallback(gpu, ws_kind, monkeypatch):
+    """Instances whose rows outgrow the tier-1 lists move to the wide tier and
+    then to the dense kernels (sp_last_dense_fallbacks counts the latter);
+    with a workspace too small for the device-planned tier everything runs in
+    host-planned waves.  Every result is bit-exact against the oracle."""
+    import torch
+    from paper_2410_10759_b200 import _native as N, batch as B
+    insts = _dense_rows_instances(17, 6)
+    off = np.zeros(len(insts) + 1, np.int64)
+    np.cumsum([len(x["r"]) for x in insts], out=off[1:])
+    cat = lambda k: np.concatenate([x[k] for x in insts])
+    b = B.InstanceBatch.from_arrays(off, cat("i"), cat("s"), cat("u"), cat("d"), cat("r"),
+                                    [x["budget"] for x in insts], [x["sac"] for x in insts])
+    lib = N.library()
+    if ws_kind == "large":
+        host = B.plan_dp(b).to_host()
+        assert lib.sp_last_dense_fallbacks() > 0, "expected some instances to outgrow the lists"
+    else:
+        mn, _full = B.dp_workspace_bytes(b)
+        ws = torch.empty(mn, dtype=torch.uint8, device=N.device())
+        out = B.PolicyBatch.empty(b.n, b.total_layers, b.r.device)
+        rc = lib.sp_plan_dp(b.struct(), out.struct(), N.ptr(ws), mn, N.stream_ptr())
+        assert rc == 0, lib.sp_last_error()
+        host = out.to_host()
+    for k, inst in enumerate(insts):
+        exp = O.plan_dp(inst)
+        got = dict(pi=host["pi"][off[k]:off[k + 1]], client_value=host["client_value"][k],
+                   server_load=host["server_load"][k], integer_latency=host["integer_latency"][k],
+                   feasible=host["feasible"][k])
+        assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{ws_kind}[{k}]")

@@ -32,6 +32,7 @@ def main():
     from paper_2410_10759_b200 import workloads as W
     from paper_2410_10759_b200.requests import Engine, RequestBatch
     lib = N.library()
+    N.workspace(int(float(os.environ.get("K2BENCH_WS_GB", "48")) * (1 << 30)))  # one wave from the first call
     req = RequestBatch.from_numpy(**W.cfg2(args.requests, 2000)[0]).to("cuda")
     layers = cm.build_preset("gpt2-24", 128).layers
     engine = Engine([layers])
