@@ -81,12 +81,13 @@ __global__ void weff_kernel(sp_instances in, int64_t* w_eff) {
 // prep: W_eff, value domain, clamped shifts, scaled values
 
 // flag (optional): set to 1 for every instance (the breakpoint-list tier
-// clears it for the instances it solves).  steps_cols > 0: instances the
-// breakpoint-list tier takes (not NaN, narrower than steps_cols) get the
-// trivial frontier (0, 0) instead of the sequential recurrence -- only the
-// dense kernels use it, and it is exact to skip nothing.
+// clears it for the instances it solves).  steps_hi > 0: instances the
+// breakpoint-list tier takes (not NaN, steps_lo[domain] <= W_eff + 1 <
+// steps_hi) get the trivial frontier (0, 0) instead of the sequential
+// recurrence -- only the dense kernels use it, and skipping nothing is exact.
 __global__ void __launch_bounds__(128) prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts, int64_t* rv,
-                                                   int2* reach, int32_t* flag, int64_t steps_cols = 0) {
+                                                   int2* reach, int32_t* flag, int64_t steps_hi = 0,
+                                                   int64_t steps_lo_i32 = 0, int64_t steps_lo_f64 = 0) {
   __shared__ int64_t sh64[32];
   __shared__ uint64_t shu[32];
   __shared__ int shi[32];
@@ -167,7 +168,8 @@ __global__ void __launch_bounds__(128) prep_kernel(sp_instances in, InstInfo* in
     // in shared memory and thread 0 walks it there.
     const bool sac = in.source_at_client[k] != 0;
     int64_t mc = sac ? 0 : cap, ms = sac ? cap : 0;
-    const bool trivial = mode == VM_F64_NAN || (steps_cols > 0 && W + 1 < steps_cols);
+    const bool trivial = mode == VM_F64_NAN ||
+                         (steps_hi > 0 && W + 1 < steps_hi && W + 1 >= (mode == VM_INT32 ? steps_lo_i32 : steps_lo_f64));
     for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
       const int64_t l = t0 + threadIdx.x;
       if (l < hi) {

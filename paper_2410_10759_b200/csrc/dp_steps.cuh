@@ -80,6 +80,7 @@ struct StepsArgs {
   int32_t* overflow;           // wave path: [n] 1 = a row exceeded CAP
   int64_t n_items;
   int64_t max_cols;            // device path: wider instances are left to the dense kernels
+  int64_t min_cols[2];         // device path, [int32, fp64 domain]: narrower ones too (one CTA's SMEM holds them)
 };
 
 template <int CAP>
@@ -229,7 +230,7 @@ __device__ __forceinline__ int steps_merge(const int32_t* ac, const V* av, int n
 // One group of G lanes per instance, WPB warps per block; rows double-buffered
 // in the group's shared memory, every row's (column, stay_from) written to the
 // instance's store.  Device path (a.work == null): group k takes instance k if
-// it is in this kernel's value domain and narrower than max_cols.
+// it is in this kernel's value domain and min_cols <= W_eff + 1 < max_cols.
 template <int MODE, int CAP, int G, int WPB>
 __global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
   using V = typename VT<MODE>::T;
@@ -243,7 +244,9 @@ __global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
   if (item >= a.n_items) return;  // whole groups leave together
   const int64_t inst = a.work ? a.work[item].inst : item;
   const InstInfo inf = a.info[inst];
-  if (!a.work && (inf.mode != MODE || inf.w_eff + 1 >= a.max_cols)) return;
+  if (!a.work && (inf.mode != MODE || inf.w_eff + 1 >= a.max_cols ||
+                  inf.w_eff + 1 < a.min_cols[MODE == VM_INT32 ? 0 : 1]))
+    return;
   unsigned char* ws = smem + (size_t)(warp * GPW + grp) * INST_BYTES;
   int32_t* rc = reinterpret_cast<int32_t*>(ws);    // [2][2][CAP]
   V* rvv = reinterpret_cast<V*>(ws + 4 * CAP * 4);  // [2][2][CAP]

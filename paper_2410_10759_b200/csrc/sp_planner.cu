@@ -673,10 +673,30 @@ struct DpPlan {
   }
 };
 
-// steps_eligible: the breakpoint-list kernels may take the instance (not for
-// full tables, not in the NaN domain, not at whole-GPU widths)
+// The widest row the single-CTA kernel holds in shared memory (it runs at
+// ~1e12 cells/s there, profiles/r01/single_e8): narrower rows stay on it.
+int64_t smem_max_cols(int mode) {
+  auto fits = [&](int64_t ncol) {
+    return single_row_bytes(mode, ncol, single_cfg_for(ncol, mode)) + stage_bytes_mode(mode) <= kSmemCap;
+  };
+  int64_t lo = 1, hi = (int64_t)1 << 20;  // fits(lo), !fits(hi)
+  while (hi - lo > 1) {
+    const int64_t m = (lo + hi) / 2;
+    if (fits(m)) lo = m;
+    else hi = m;
+  }
+  return lo;
+}
+// narrowest row the breakpoint lists take (all of them when forced)
+int64_t steps_min_cols(int mode, int force) { return force == DPV_STEPS ? 0 : smem_max_cols(mode) + 1; }
+
+// steps_eligible: the breakpoint-list kernels may take the instance: rows
+// wider than one SM's shared memory (where the dense alternative is the
+// L2-streaming kernel) and narrower than the whole-GPU path, not for full
+// tables, not in the NaN domain
 bool steps_eligible(int mode, int64_t ncol, int force, bool tables) {
-  return !tables && mode != VM_F64_NAN && ncol < kGridMinColsSteps && (force < 0 || force == DPV_STEPS);
+  return !tables && mode != VM_F64_NAN && ncol < kGridMinColsSteps && ncol >= steps_min_cols(mode, force) &&
+         (force < 0 || force == DPV_STEPS);
 }
 
 // `steps_cap` > 0: plan the breakpoint-list kernel with that capacity (the
@@ -1323,8 +1343,9 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   const bool steps_ok = tab_c == nullptr && !q_min && (force < 0 || force == DPV_STEPS);
   const int grid = (int)std::min<int64_t>(n, 1 << 20);
   const bool tier1_fits = steps_ok && out && fixed + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap) <= ws_bytes;
+  const int64_t lo_i32 = steps_min_cols(VM_INT32, force), lo_f64 = steps_min_cols(VM_F64, force);
   prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv, reach, steps_ok ? flag : nullptr,
-                                    tier1_fits ? kGridMinColsSteps : 0);
+                                    tier1_fits ? kGridMinColsSteps : 0, lo_i32, lo_f64);
   int rc = launch_check("prep_kernel launch");
   if (rc) return rc;
   uint8_t* dyn = (uint8_t*)ws + fixed;
@@ -1348,6 +1369,8 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     sa.solved = solved;
     sa.n_items = n;
     sa.max_cols = kGridMinColsSteps;
+    sa.min_cols[0] = lo_i32;
+    sa.min_cols[1] = lo_f64;
     rc = check_cuda(cudaMemsetAsync(solved, 0, 2 * sizeof(unsigned long long), st), "zero solved count");
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (!rc && profiling()) {

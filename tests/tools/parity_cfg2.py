@@ -2,7 +2,7 @@
 seed 2000) solved on the GPU exactly as bench.py does, and a sample of its
 placements recomputed by the oracle on every host core.
 
-    python tools/parity_cfg2.py [--sample 400]
+    python tests/tools/parity_cfg2.py [--sample 400]
 """
 import argparse
 import json
@@ -13,7 +13,7 @@ from pathlib import Path
 
 import numpy as np
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 
 
 def _oracle(args):

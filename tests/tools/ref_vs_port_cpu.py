@@ -2,7 +2,7 @@
 reference's profile -> build_problem -> plan_dp against the oracle port on the
 same cfg2 requests, one process each.  Run only where the reference exists.
 
-    PYTHONPATH=/root/reference/pkg/src python tools/ref_vs_port_cpu.py [--n 8]
+    PYTHONPATH=/root/reference/pkg/src python tests/tools/ref_vs_port_cpu.py [--n 8]
 """
 import argparse
 import json
@@ -10,7 +10,7 @@ import sys
 import time
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 
 
 def main():
