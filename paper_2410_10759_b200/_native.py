@@ -217,6 +217,7 @@ def to_dev(a, dtype, dev=None) -> torch.Tensor:
 
 
 _ws: dict[int, torch.Tensor] = {}
+_total_mem: dict[int, int] = {}
 _WS_MIN = 64 << 20
 _WS_ROUND = 64 << 20
 
@@ -233,8 +234,11 @@ def workspace_cap(dev=None) -> int:
     env = os.environ.get("SPLITPLAN_WS_GB")
     if env:
         return int(float(env) * (1 << 30))
-    _free, total = torch.cuda.mem_get_info(dev or device())
-    return int(total * 0.75)
+    d = dev or device()
+    key = d.index if d.index is not None else torch.cuda.current_device()
+    if key not in _total_mem:
+        _total_mem[key] = int(torch.cuda.get_device_properties(key).total_memory)
+    return int(_total_mem[key] * 0.75)
 
 
 def free_bytes(dev) -> int:
@@ -267,6 +271,8 @@ def grow_workspace_hint(full_bytes: int) -> None:
     cur = _ws.get(dev.index)
     have = cur.numel() if cur is not None else 0
     del cur  # no reference may keep the old buffer alive while it is replaced
+    if full_bytes <= have + (have >> 2):  # the common case: nothing to do, no driver query
+        return
     target = min(int(full_bytes), workspace_cap(dev), have + int(free_bytes(dev) * 0.9))
     if target <= have + (have >> 2):  # not worth a reallocation
         return
@@ -279,17 +285,28 @@ def release_workspace() -> None:
     torch.cuda.empty_cache()
 
 
+def _useful_size(need: int, full: int, have: int, dev) -> int:
+    """What to grow to: at least `need`; up to `full` (one wave, no recompute)
+    within the cap and the free memory."""
+    room = have + int(free_bytes(dev) * 0.9)
+    return max(int(need), min(int(full), workspace_cap(dev), room))
+
+
 def with_workspace(fn, *args):
-    """Call fn(*args, ws_ptr, ws_bytes), growing the workspace on SP_ERR_WORKSPACE."""
+    """Call fn(*args, ws_ptr, ws_bytes), growing the workspace on SP_ERR_WORKSPACE
+    (to what the call reports as useful, not just its minimum)."""
     ws = workspace()
     rc = fn(*args, ptr(ws), C.c_size_t(ws.numel()))
     for _ in range(8):  # each retry covers the largest instance seen failing so far
         if rc != SP_ERR_WORKSPACE:
             break
-        need = int(library().sp_last_required_workspace())
+        lib = library()
+        need = int(lib.sp_last_required_workspace())
         if need <= ws.numel():
             break
+        have = ws.numel()
+        target = _useful_size(need + (1 << 20), int(lib.sp_last_full_workspace()), have, ws.device)
         del ws  # released before the larger buffer is allocated
-        ws = workspace(need + (1 << 20))
+        ws = workspace(target)
         rc = fn(*args, ptr(ws), C.c_size_t(ws.numel()))
     return rc

@@ -76,7 +76,7 @@ struct StepsArgs {
   const DpWork* work;          // wave path: instance and store offset (bp_off) per item; null: item = instance
   uint8_t* store;              // workspace base of the stores
   int32_t* flag;               // [n] device path: cleared once the instance is solved here (prep sets it)
-  unsigned long long* solved;  // device path: [instances, DP cells] solved here
+  unsigned long long* solved;  // device path: [instances, DP cells, breakpoints stored, stages] solved here
   int32_t* overflow;           // wave path: [n] 1 = a row exceeded CAP
   int64_t n_items;
   int64_t max_cols;            // device path: wider instances are left to the dense kernels
@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
   __syncwarp(gmask);
   int buf = 0;
   bool over = false;
+  unsigned long long stored = (unsigned long long)(nC + nS);
   // stage records one stage ahead: their load latency overlaps the merges
   StageShift sh_next = a.shifts[lo];
   int64_t bits_next = a.rv[lo];
@@ -303,6 +304,7 @@ __global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
     }
     nC = nC2;
     nS = nS2;
+    stored += (unsigned long long)(nC + nS);
     buf = nb;
     if (g == 0) {
       g_cnt[r0] = nC;
@@ -323,6 +325,8 @@ __global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
       if (a.solved) {
         atomicAdd(a.solved, 1ull);
         atomicAdd(a.solved + 1, (unsigned long long)L * (unsigned long long)(W + 1));  // DP cells solved
+        atomicAdd(a.solved + 2, stored);
+        atomicAdd(a.solved + 3, (unsigned long long)L);
       }
     }
   }

@@ -1332,10 +1332,11 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   int64_t* gstate = (int64_t*)cv.take(64);
   int32_t* overflow = (int32_t*)cv.take(sizeof(int32_t) * n);
   int32_t* flag = (int32_t*)cv.take(sizeof(int32_t) * n);
-  unsigned long long* solved = (unsigned long long*)cv.take(2 * sizeof(unsigned long long));
+  unsigned long long* solved = (unsigned long long*)cv.take(4 * sizeof(unsigned long long));
   const size_t fixed = align_up(cv.used, 256);
   if (!ws || fixed > ws_bytes) {
     set_required_workspace(fixed + (1 << 20));
+    set_full_workspace(fixed + (1 << 20));  // unknown until the prep kernel has run
     set_error(SP_ERR_WORKSPACE, "workspace %zu B < fixed part %zu B", ws_bytes, fixed);
     return SP_ERR_WORKSPACE;
   }
@@ -1371,7 +1372,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     sa.max_cols = kGridMinColsSteps;
     sa.min_cols[0] = lo_i32;
     sa.min_cols[1] = lo_f64;
-    rc = check_cuda(cudaMemsetAsync(solved, 0, 2 * sizeof(unsigned long long), st), "zero solved count");
+    rc = check_cuda(cudaMemsetAsync(solved, 0, 4 * sizeof(unsigned long long), st), "zero solved count");
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (!rc && profiling()) {
       cudaEventCreate(&e0);
@@ -1382,13 +1383,20 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     if (!rc) rc = launch_steps(VM_F64, kStepsCap, sa, st);
     if (!rc && profiling()) cudaEventRecord(e1, st);
     if (!rc) rc = launch_backtrack_steps(kStepsCap, *in, sa, idx, *out, st);
-    unsigned long long hsolved[2] = {0, 0};  // instances, DP cells
+    unsigned long long hsolved[4] = {0, 0, 0, 0};  // instances, DP cells, breakpoints, stages
     if (!rc)
       rc = check_cuda(cudaMemcpyAsync(hsolved, solved, sizeof(hsolved), cudaMemcpyDeviceToHost, st),
                       "copy solved count");
     if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync after breakpoint lists");
     if (rc) return rc;
-    if (e1) prof_record_dp(e0, e1, (double)hsolved[1], 0.0, DPV_STEPS);
+    // algorithmic HBM bytes of the breakpoint-list kernel: the stage records it
+    // reads (16 B shifts + 8 B value per stage) and the store it writes (an
+    // 8-B {column, stay_from} per breakpoint, a 4-B count per row)
+    if (e1)
+      prof_record_dp(e0, e1, (double)hsolved[1],
+                     24.0 * (double)hsolved[3] + 8.0 * (double)hsolved[2] +
+                         8.0 * (double)(hsolved[3] + hsolved[0]),
+                     DPV_STEPS);
     if (hsolved[0] == (unsigned long long)n) {
       set_full_workspace(fixed + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap));
       set_steps_overflow(0);
@@ -1505,27 +1513,40 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   const int2* a_reach = env_int("SPLITPLAN_NO_REACH", 0) ? nullptr : reach;
   // instances too large for a wave (or wider than 4M columns) run alone over
   // the whole GPU (grid path, checkpointing if needed)
-  size_t grid_full = 0;
+  // The workspace that would run every wave-path instance in ONE wave and
+  // keep every back-pointer stage of the whole-GPU ones (reported whether or
+  // not this call succeeds: sp_last_full_workspace, so a caller growing its
+  // workspace after SP_ERR_WORKSPACE can grow straight to a useful size).
+  auto is_grid = [&](const Item& it) {
+    return tab_c == nullptr && (force == DPV_GRID || it.ncol >= kGridMinCols || it.plan.bp + it.plan.rows > avail);
+  };
+  {
+    size_t one = fixed, grid_full = 0;
+    for (const Item& it : items) {
+      if (!is_grid(it)) {
+        one += it.plan.bp + it.plan.rows;
+        continue;
+      }
+      if (dp) continue;  // partitions live in their own workspaces
+      const int np = std::max(1, std::min(kMaxParts, env_int("SPLITPLAN_GRID_PARTS", 1)));
+      int ms = 0;
+      if (np > 1) {
+        rc = read_max_shift(shifts + hoff[it.inst], (int)it.L, st, &ms);
+        if (rc) return rc;
+      }
+      size_t gmin = 0, gfull = 0;
+      grid_workspace_bytes(it.mode, it.L, it.ncol, np, np, ms, &gmin, &gfull);
+      grid_full = std::max(grid_full, fixed + (size_t)np * gfull);
+    }
+    set_full_workspace(std::max(one, grid_full));
+  }
   {
     std::vector<Item> rest;
     rest.reserve(items.size());
     for (const Item& it : items) {
-      const bool grid = tab_c == nullptr &&
-                        (force == DPV_GRID || it.ncol >= kGridMinCols || it.plan.bp + it.plan.rows > avail);
-      if (!grid) {
+      if (!is_grid(it)) {
         rest.push_back(it);
         continue;
-      }
-      if (!dp) {  // the workspace that keeps every back-pointer stage (no recompute)
-        const int np = std::max(1, std::min(kMaxParts, env_int("SPLITPLAN_GRID_PARTS", 1)));
-        int ms = 0;
-        if (np > 1) {
-          rc = read_max_shift(shifts + hoff[it.inst], (int)it.L, st, &ms);
-          if (rc) return rc;
-        }
-        size_t gmin = 0, gfull = 0;
-        grid_workspace_bytes(it.mode, it.L, it.ncol, np, np, ms, &gmin, &gfull);
-        grid_full = std::max(grid_full, fixed + (size_t)np * gfull);
       }
       rc = run_grid_instance(in, out, info, shifts, rv, a_reach, idx, gstate, it.inst, hoff[it.inst], (int)it.L,
                              it.ncol, it.mode, dyn, avail, st, dp);
@@ -1533,11 +1554,6 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       if (rc) return rc;
     }
     items.swap(rest);
-  }
-  {  // what one wave of every remaining instance would need (sp_last_full_workspace)
-    size_t one = fixed;
-    for (const Item& it : items) one += it.plan.bp + it.plan.rows;
-    set_full_workspace(std::max(one, grid_full));
   }
 
   DpArgs a;
