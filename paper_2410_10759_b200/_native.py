@@ -292,6 +292,16 @@ def _useful_size(need: int, full: int, have: int, dev) -> int:
     return max(int(need), min(int(full), workspace_cap(dev), room))
 
 
+def useful_size(need: int, full: int) -> int:
+    """The workspace to allocate for a call that needs `need` bytes and would
+    use `full` (one wave, no recompute) on the current device."""
+    dev = device()
+    cur = _ws.get(dev.index)
+    have = cur.numel() if cur is not None else 0
+    del cur
+    return _useful_size(need, full, have, dev)
+
+
 def with_workspace(fn, *args):
     """Call fn(*args, ws_ptr, ws_bytes), growing the workspace on SP_ERR_WORKSPACE
     (to what the call reports as useful, not just its minimum)."""

@@ -140,7 +140,17 @@ def plan_dp(batch: InstanceBatch, out: PolicyBatch | None = None, devices=None) 
             C.cast(wlen, C.c_void_p), N.stream_ptr()))
         N.check(rc, "sp_plan_dp_devices")
         return out
-    rc = N.with_workspace(lambda ws, nb: lib.sp_plan_dp(s, o, ws, nb, N.stream_ptr()))
+    ws = N.workspace()
+    rc = lib.sp_plan_dp(s, o, N.ptr(ws), ws.numel(), N.stream_ptr())
+    if rc == N.SP_ERR_WORKSPACE:
+        # size it from the query (prep only, no DP): the useful size at once,
+        # instead of running the batch in waves of a minimal workspace
+        del ws
+        mn, full = dp_workspace_bytes(batch)
+        N.workspace(N.useful_size(mn, full))
+        rc = N.with_workspace(lambda w, nb: lib.sp_plan_dp(s, o, w, nb, N.stream_ptr()))
+    else:
+        del ws
     N.check(rc, "sp_plan_dp")
     N.grow_workspace_hint(int(lib.sp_last_full_workspace()))
     return out

@@ -22,6 +22,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <type_traits>
 #include <vector>
 
@@ -599,6 +601,17 @@ int launch_stream(const DpArgs& a, int64_t n_items, StreamGeom geo, cudaStream_t
   return launch_stream_t<MODE, 256, 4, NS, 1, kStreamBufs>(a, n_items, geo, st);
 }
 
+// SPLITPLAN_TRACE=1: host-side phase timestamps of run_dp on stderr
+struct Trace {
+  bool on = env_int("SPLITPLAN_TRACE", 0) != 0;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void operator()(const char* what, long long x = -1) const {
+    if (!on) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[splitplan trace] %9.3f ms  %s %lld\n", ms, what, x);
+  }
+};
+
 // ---- breakpoint-list kernels ------------------------------------------------
 
 // tier geometry: lanes per instance and warps per block
@@ -694,9 +707,10 @@ int64_t steps_min_cols(int mode, int force) { return force == DPV_STEPS ? 0 : sm
 // wider than one SM's shared memory (where the dense alternative is the
 // L2-streaming kernel) and narrower than the whole-GPU path, not for full
 // tables, not in the NaN domain
-bool steps_eligible(int mode, int64_t ncol, int force, bool tables) {
-  return !tables && mode != VM_F64_NAN && ncol < kGridMinColsSteps && ncol >= steps_min_cols(mode, force) &&
-         (force < 0 || force == DPV_STEPS);
+// (lo_i32 / lo_f64: steps_min_cols of the two domains, computed once per call)
+bool steps_eligible(int mode, int64_t ncol, int force, bool tables, int64_t lo_i32, int64_t lo_f64) {
+  return !tables && mode != VM_F64_NAN && ncol < kGridMinColsSteps &&
+         ncol >= (mode == VM_INT32 ? lo_i32 : lo_f64) && (force < 0 || force == DPV_STEPS);
 }
 
 // `steps_cap` > 0: plan the breakpoint-list kernel with that capacity (the
@@ -1322,6 +1336,8 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
            int64_t w_eff_check = -1) {
   const int64_t n = in->n, total = in->total_layers;
   if (n == 0) return SP_OK;
+  const Trace trace;
+  trace("run_dp begin", n);
   Carve cv{(uint8_t*)ws, ws_bytes};
   InstInfo* info = (InstInfo*)cv.take(sizeof(InstInfo) * n);
   StageShift* shifts = (StageShift*)cv.take(sizeof(StageShift) * total);
@@ -1341,7 +1357,8 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     return SP_ERR_WORKSPACE;
   }
   const int force = forced_variant();
-  const bool steps_ok = tab_c == nullptr && !q_min && (force < 0 || force == DPV_STEPS);
+  const bool steps_allowed = tab_c == nullptr && (force < 0 || force == DPV_STEPS);
+  const bool steps_ok = steps_allowed && !q_min;
   const int grid = (int)std::min<int64_t>(n, 1 << 20);
   const bool tier1_fits = steps_ok && out && fixed + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap) <= ws_bytes;
   const int64_t lo_i32 = steps_min_cols(VM_INT32, force), lo_f64 = steps_min_cols(VM_F64, force);
@@ -1415,6 +1432,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   if (rc) return rc;
   rc = check_cuda(cudaStreamSynchronize(st), "sync after prep");
   if (rc) return rc;
+  trace("prep done, info on host");
 
   if (w_eff_check >= 0 && hinfo[0].w_eff != w_eff_check) {
     set_error(SP_ERR_INVALID, "w_eff = %lld does not match the instance's effective budget %lld",
@@ -1457,7 +1475,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     // breakpoint lists first (tier 1 if it did not run, else the wide tier)
     // (a tier whose store does not fit the workspace is skipped: the tiers are
     // an optimisation, the dense kernels the guarantee)
-    int cap = steps_ok && steps_eligible(it.mode, ncol, force, tab_c != nullptr)
+    int cap = steps_ok && steps_eligible(it.mode, ncol, force, tab_c != nullptr, lo_i32, lo_f64)
                   ? (tier1 ? kStepsCapWide : kStepsCap)
                   : 0;
     if (cap == kStepsCap && align_up(steps_store_bytes((int)it.L, cap), 256) > avail) cap = kStepsCapWide;
@@ -1483,9 +1501,17 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         for (int r = 0; r < dp->n; ++r) c += dp->dev[r] == dp->dev[p];
         per_dev = std::max(per_dev, c);
       }
+    size_t tier1 = 0;  // the device-planned breakpoint lists' store of the eligible instances
     for (const Item& it : items) {
       const bool grid = tab_c == nullptr && (force == DPV_GRID || it.ncol >= kGridMinCols);
       size_t imin = it.plan.bp + it.plan.rows, ifull = imin;
+      if (!grid && steps_allowed && steps_eligible(it.mode, it.ncol, force, false, lo_i32, lo_f64)) {
+        // the minimum stays the dense kernels' (every instance may fall back
+        // to them); the useful size is the breakpoint store
+        mn = std::max(mn, imin);
+        tier1 += (size_t)(it.L + 1) * steps_row_pair_bytes(kStepsCap);
+        continue;
+      }
       if (grid) {
         int ms = 0;
         if (nparts > 1) {
@@ -1505,7 +1531,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       full = grid ? std::max(full, ifull) : full + ifull;
     }
     *q_min = fixed + mn;
-    *q_full = fixed + std::max(full, mn);
+    *q_full = fixed + std::max(full + tier1, mn);
     if (q_part_min) *q_part_min = pmn;
     if (q_part_full) *q_part_full = pfull;
     return SP_OK;
@@ -1517,6 +1543,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   // keep every back-pointer stage of the whole-GPU ones (reported whether or
   // not this call succeeds: sp_last_full_workspace, so a caller growing its
   // workspace after SP_ERR_WORKSPACE can grow straight to a useful size).
+  trace("items planned", (long long)items.size());
   auto is_grid = [&](const Item& it) {
     return tab_c == nullptr && (force == DPV_GRID || it.ncol >= kGridMinCols || it.plan.bp + it.plan.rows > avail);
   };
@@ -1581,6 +1608,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   auto run_waves = [&](const std::vector<Item>& items) -> int {
   size_t pos = 0;
   while (pos < items.size()) {
+    trace("wave begin", (long long)pos);
     // gather one wave that fits the workspace
     size_t end = pos, wave_bytes = 0;
     while (end < items.size() && wave_bytes + items[end].plan.bp + items[end].plan.rows <= avail) {
@@ -1623,10 +1651,12 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     }
     for (const Group& g : groups)
       for (const DpWork& w : g.items) hwork.push_back(w);
+    trace("wave laid out", (long long)hwork.size());
     rc = check_cuda(cudaMemcpyAsync(work, hwork.data(), sizeof(DpWork) * hwork.size(),
                                     cudaMemcpyHostToDevice, st),
                     "upload work list");
     if (rc) return rc;
+    trace("work list uploaded");
     int64_t first = 0;
     for (const Group& g : groups) {
       const int64_t cnt = (int64_t)g.items.size();
@@ -1704,6 +1734,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     items.swap(redo);
   }
   set_steps_overflow(dense_fallbacks);
+  trace("run_dp end (launches queued)");
   return SP_OK;
 }
 
