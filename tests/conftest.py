@@ -19,6 +19,11 @@ GOLDEN = Path(__file__).resolve().parent / "golden"
 sys.path.insert(0, str(ROOT))
 
 
+# the reference's own suite is staged here by tests/tools/ref_tests.sh and run
+# separately (it imports `splitplan`); never collected by this suite
+collect_ignore = ["golden/_ref_tests", "golden/ref_shim", "tools"]
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
 
