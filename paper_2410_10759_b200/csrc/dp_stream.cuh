@@ -86,8 +86,12 @@ __device__ __forceinline__ uint32_t ld_cluster_relaxed(uint32_t addr) {
   asm volatile("ld.relaxed.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
+// Progress counters: published with a release reduction, polled by the other
+// CTAs of the cluster with relaxed loads (then an acquire fence) -- strong
+// operations of cluster scope on both sides, i.e. synchronisation, not a race.
+// (the counters only grow: a release max-reduction is the store)
 __device__ __forceinline__ void st_cluster_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.cluster.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+  asm volatile("red.release.cluster.shared::cta.max.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel_cluster() {
   asm volatile("fence.acq_rel.cluster;" ::: "memory");

@@ -167,8 +167,16 @@ class PlanProblem:
 
     @property
     def total_r(self) -> float:
-        from .evaluator import _total_r
-        return _total_r(self)
+        """np.sum(r) in numpy's pairwise order, computed on the device once per
+        r content (a cached value is reused while r's bytes are unchanged)."""
+        r = np.asarray(self.r, dtype=np.float64)
+        key = (id(self.r), hash(r.tobytes()))
+        cached = self.__dict__.get("_total_r_cache")
+        if cached is None or cached[0] != key:
+            from .evaluator import _total_r
+            cached = (key, _total_r(self))
+            self.__dict__["_total_r_cache"] = cached
+        return cached[1]
 
     @property
     def has_real_times(self) -> bool:

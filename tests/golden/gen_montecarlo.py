@@ -32,7 +32,10 @@ from splitplan.throughput_sim import (CapacityDeadlockError, SimConfig,  # noqa:
                                       capacity_for_requests, compare_variants,
                                       scenarios_from_cells)
 
-SIDS = [0, 17, 130, 255, 4095, 21845, 40000, 65535]
+# 8 hand-picked corners of the grid + 56 seeded draws: 64 scenarios, 4,096 requests
+SIDS = [0, 17, 130, 255, 4095, 21845, 40000, 65535] + sorted(
+    int(x) for x in __import__("numpy").random.default_rng(64).choice(
+        [x for x in range(65536) if x not in (0, 17, 130, 255, 4095, 21845, 40000, 65535)], 56, replace=False))
 OUT = Path(__file__).resolve().parent / "montecarlo.json"
 
 
