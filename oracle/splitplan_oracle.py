@@ -358,22 +358,40 @@ def plan_trivial(inst, side):
     raise ValueError(f"side must be 'all_server' or 'all_client', got {side!r}")
 
 
-def plan_exhaustive(inst):
-    """planner.py:228-268 -- every mask; ties go to the smallest mask (layer 1 = MSB)."""
+def plan_exhaustive(inst, chunk=1 << 16):
+    """planner.py:228-268 -- every mask in chunks of 65,536: latency as a float
+    sum, value = x @ r (numpy's BLAS dgemv: its summation order decides ties
+    under non-dyadic r), np.argmax inside a chunk (first max; a NaN value
+    wins), across chunks only a strictly greater value replaces the best."""
     L = len(inst["r"])
     if L > ORACLE_MAX_LAYERS:
         raise ValueError(f"oracle limited to {ORACLE_MAX_LAYERS} layers, got {L}")
-    best = None
-    for mask in range(1 << L):
-        pi = [(mask >> (L - 1 - k)) & 1 for k in range(L)]
-        if latency_units(pi, inst) > inst["budget"]:
-            continue
-        val = float(np.dot(np.array(pi, float), inst["r"]))
-        if best is None or val > best[0]:
-            best = (val, pi)
-    if best is None:
+    i, s = inst["i"].astype(float), inst["s"].astype(float)
+    u, d = inst["u"].astype(float), inst["d"].astype(float)
+    r = np.asarray(inst["r"], dtype=float)
+    x0 = 1.0 if inst["sac"] else 0.0
+    shifts = np.arange(L - 1, -1, -1, dtype=np.uint32)
+    best_value, best_mask = None, None
+    with np.errstate(invalid="ignore"):
+        for start in range(0, 1 << L, chunk):
+            masks = np.arange(start, min(start + chunk, 1 << L), dtype=np.uint32)
+            x = ((masks[:, None] >> shifts[None, :]) & 1).astype(float)
+            xprev = np.empty_like(x)
+            xprev[:, 0] = x0
+            xprev[:, 1:] = x[:, :-1]
+            lat = np.sum(x * (i + (1 - xprev) * d) + (1 - x) * (s + xprev * u), axis=1)
+            value = x @ r
+            ok = lat <= inst["budget"]
+            if not np.any(ok):
+                continue
+            value_ok = np.where(ok, value, NEG)
+            idx = int(np.argmax(value_ok))
+            if best_value is None or value_ok[idx] > best_value:
+                best_value, best_mask = float(value_ok[idx]), int(masks[idx])
+    if best_value is None:
         return infeasible(inst, "oracle")
-    return finish(np.array(best[1], np.int64), inst, "oracle")
+    pi = np.array([(best_mask >> int(sh)) & 1 for sh in shifts], np.int64)
+    return finish(pi, inst, "oracle")
 
 
 # ---------------------------------------------------------------------------

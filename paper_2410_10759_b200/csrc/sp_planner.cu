@@ -222,72 +222,108 @@ __global__ void prefix_kernel(sp_instances in, int32_t which, sp_policies out) {
 }
 
 // ---------------------------------------------------------------------------
-// exhaustive planner (plan_oracle): one CTA per instance, masks strided
+// exhaustive planner (plan_oracle, planner.py:228-268): one CTA per instance
+
+// value = x @ r (planner.py:253) exactly as numpy evaluates it on the host the
+// golden vectors come from: numpy hands the (masks x L) @ (L,) product to
+// OpenBLAS dgemv_t (0.3.30, the Haswell/SkylakeX micro-kernel), which sums
+// the first 4*floor(L/4) layers in four lane-strided accumulators (lane k
+// takes layers k, k+4, ... in order; x in {0, 1} makes each FMA an add),
+// reduces them as (a0 + a2) + (a1 + a3), then adds the last L mod 4 layers
+// summed left to right (a model checked against numpy on 51k masks, 0
+// mismatches; profiles/r02/oracle_blas_order.json).  0 * inf = NaN as in BLAS.
+__device__ double mask_value(const double* r, int L, uint32_t mask) {
+  const int m3 = L & 3, m1 = L - m3;
+  auto x = [&](int i) { return ((mask >> (L - 1 - i)) & 1u) ? 1.0 : 0.0; };  // layer 1 is the MSB
+  double y = 0.0;
+  if (m1) {
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = 0; i < m1; ++i) a[i & 3] = dadd(a[i & 3], dmul(x(i), r[i]));
+    y = dadd(y, dadd(dadd(a[0], a[2]), dadd(a[1], a[3])));
+  }
+  if (m3) {
+    double t = dmul(x(m1), r[m1]);
+    for (int i = m1 + 1; i < L; ++i) t = dadd(t, dmul(x(i), r[i]));
+    y = dadd(y, t);
+  }
+  return y;
+}
+
+struct MaskBest {
+  double v;
+  uint32_t m;
+  int found;
+};
+
+// np.argmax order inside one chunk of masks: NaN first, then the larger
+// value, ties to the smaller mask (the first index)
+__device__ __forceinline__ bool mask_better(const MaskBest& a, const MaskBest& b) {
+  if (!a.found) return false;
+  if (!b.found) return true;
+  const bool an = a.v != a.v, bn = b.v != b.v;
+  if (an || bn) return an && (!bn || a.m < b.m);
+  return a.v > b.v || (a.v == b.v && a.m < b.m);
+}
 
 __global__ void exhaustive_kernel(sp_instances in, sp_policies out) {
+  constexpr uint32_t kChunk = 1u << 16;  // planner.py:228 default chunk
   const int64_t inst = blockIdx.x;
   const int64_t lo = in.layer_off[inst];
   const int L = (int)(in.layer_off[inst + 1] - lo);
   const bool sac = in.source_at_client[inst] != 0;
   const int64_t budget = in.budget[inst];
+  const double* r = in.r + lo;
   __shared__ double s_val[32];
   __shared__ uint32_t s_mask[32];
   __shared__ int s_found[32];
-  double best_v = -INFINITY;
-  uint32_t best_m = 0xffffffffu;
-  int found = 0;
-  const uint32_t nmask = 1u << L;
-  for (uint32_t mask = threadIdx.x; mask < nmask; mask += blockDim.x) {
-    int64_t lat = 0;
-    double v = 0.0;
-    int prev = sac ? 1 : 0;
-    for (int k = 0; k < L; ++k) {
-      const int x = (mask >> (L - 1 - k)) & 1;  // layer 1 is the MSB
-      if (x) {
-        lat += in.client_units[lo + k] + (prev ? 0 : in.down_units[lo + k]);
-        v = dadd(v, in.r[lo + k]);
-      } else {
-        lat += in.server_units[lo + k] + (prev ? in.up_units[lo + k] : 0);
-      }
-      prev = x;
-    }
-    if (lat <= budget && (!found || v > best_v || (v == best_v && mask < best_m))) {
-      best_v = v;
-      best_m = mask;
-      found = 1;
-    }
-  }
-  // warp + block arg-reduction: larger value, then smaller mask
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, best_v, o);
-    const uint32_t om = __shfl_xor_sync(0xffffffffu, best_m, o);
-    const int of = __shfl_xor_sync(0xffffffffu, found, o);
-    if (of && (!found || ov > best_v || (ov == best_v && om < best_m))) {
-      best_v = ov;
-      best_m = om;
-      found = 1;
-    }
-  }
-  if (lane == 0) {
-    s_val[wid] = best_v;
-    s_mask[wid] = best_m;
-    s_found[wid] = found;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int nw = blockDim.x / 32;
-    for (int w = 1; w < nw; ++w) {
-      if (s_found[w] && (!found || s_val[w] > best_v || (s_val[w] == best_v && s_mask[w] < best_m))) {
-        best_v = s_val[w];
-        best_m = s_mask[w];
-        found = 1;
+  MaskBest best{-INFINITY, 0xffffffffu, 0};  // across chunks (thread 0)
+  const uint32_t nmask = 1u << L;
+  for (uint32_t start = 0; start < nmask; start += kChunk) {
+    const uint32_t stop = min(nmask, start + kChunk);
+    MaskBest cb{-INFINITY, 0xffffffffu, 0};
+    for (uint32_t mask = start + threadIdx.x; mask < stop; mask += blockDim.x) {
+      int64_t lat = 0;  // exact: the reference's float np.sum of integral terms (< 2^53)
+      int prev = sac ? 1 : 0;
+      for (int k = 0; k < L; ++k) {
+        const int xk = (mask >> (L - 1 - k)) & 1;
+        lat += xk ? in.client_units[lo + k] + (prev ? 0 : in.down_units[lo + k])
+                  : in.server_units[lo + k] + (prev ? in.up_units[lo + k] : 0);
+        prev = xk;
       }
+      if (lat > budget) continue;
+      const MaskBest c{mask_value(r, L, mask), mask, 1};
+      if (mask_better(c, cb)) cb = c;
     }
+    for (int o = 16; o > 0; o >>= 1) {
+      MaskBest other;
+      other.v = __shfl_xor_sync(0xffffffffu, cb.v, o);
+      other.m = __shfl_xor_sync(0xffffffffu, cb.m, o);
+      other.found = __shfl_xor_sync(0xffffffffu, cb.found, o);
+      if (mask_better(other, cb)) cb = other;
+    }
+    if (lane == 0) {
+      s_val[wid] = cb.v;
+      s_mask[wid] = cb.m;
+      s_found[wid] = cb.found;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x / 32); ++w) {
+        const MaskBest c{s_val[w], s_mask[w], s_found[w]};
+        if (mask_better(c, cb)) cb = c;
+      }
+      // across chunks the reference keeps a chunk's best only if strictly
+      // greater (a later NaN never replaces, planner.py:258-261)
+      if (cb.found && (!best.found || cb.v > best.v)) best = cb;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
     uint8_t* pi = out.pi + lo;
-    for (int k = 0; k < L; ++k) pi[k] = found ? (uint8_t)((best_m >> (L - 1 - k)) & 1) : 0;
-    int32_t idx[32];  // L <= 24 (planner.py:21 ORACLE_MAX_LAYERS)
-    finish_policy(in, inst, lo, L, idx, out, !found, false);
+    for (int k = 0; k < L; ++k) pi[k] = best.found ? (uint8_t)((best.m >> (L - 1 - k)) & 1) : 0;
+    int32_t idx[32];  // L <= 24 (planner.py:21 ORACLE_MAX_LAYERS; checked by sp_plan_exhaustive)
+    finish_policy(in, inst, lo, L, idx, out, !best.found, false);
     out.status[inst] = SP_OK;
   }
 }

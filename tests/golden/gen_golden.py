@@ -169,6 +169,8 @@ def gen_planner():
                                             source_at_client=bool(rng.integers(0, 2))))
     save_battery("battery_oracle_ties", probs, with_oracle=True)
 
+    gen_oracle_float()
+
     # medium integer battery: big W with many layers (exercises tiled rows)
     rng = np.random.default_rng(13)
     probs = []
@@ -182,6 +184,28 @@ def gen_planner():
                                             if t % 3 else rng.random(L) * 1e6,
                                             W, source_at_client=bool(t % 2)))
     save_battery("battery_wide", probs, planners=True)
+
+
+def gen_oracle_float():
+    """battery_oracle_float (see the comment below)."""
+    # oracle battery with decimal r (0.1 + 0.2 != 0.3): subsets whose sums tie
+    # in exact arithmetic differ by rounding, so the argmax depends on the
+    # order numpy's x @ r (BLAS dgemv) sums in (planner.py:253); L up to 20
+    # crosses the 65,536-mask chunks; a few r = inf (0 * inf = NaN values)
+    rng = np.random.default_rng(29)
+    vals = np.array([0.1, 0.2, 0.3, 0.7, 1.1, 0.05, 0.15, 2.2, 0.45, 3.3])
+    probs = []
+    for t in range(160):
+        L = int(rng.integers(1, 15)) if t < 140 else int(rng.integers(17, 21))
+        r = rng.choice(vals, L) * rng.choice([1.0, 1.0, 1.7], L)
+        if t % 53 == 52:
+            r[int(rng.integers(0, L))] = math.inf
+        i = rng.integers(0, 6, L)
+        probs.append(PlanProblem.from_costs(i, rng.integers(0, 6, L), rng.integers(0, 6, L),
+                                            rng.integers(0, 6, L), r, int(rng.integers(0, 4 * L + 8)),
+                                            source_at_client=bool(rng.integers(0, 2))))
+    save_battery("battery_oracle_float", probs, with_oracle=True, planners=False)
+
 
 
 def gen_tables():
@@ -412,6 +436,8 @@ if __name__ == "__main__":
     which = set(sys.argv[1:]) or {"planner", "tables", "cost", "units", "build", "sweep", "large"}
     if "planner" in which:
         gen_planner()
+    if "oracle_float" in which and "planner" not in which:
+        gen_oracle_float()
     if "tables" in which:
         gen_tables()
     if "cost" in which:

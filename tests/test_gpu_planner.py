@@ -63,7 +63,7 @@ def test_prefix_planners_match_reference(gpu, name):
         _compare(bat, planner, B.plan_prefix(b, code).to_host())
 
 
-@pytest.mark.parametrize("name", ["battery_acceptance", "battery_oracle_ties"])
+@pytest.mark.parametrize("name", ["battery_acceptance", "battery_oracle_ties", "battery_oracle_float"])
 def test_exhaustive_matches_reference(gpu, name):
     from paper_2410_10759_b200 import batch as B
     bat = Battery(name)

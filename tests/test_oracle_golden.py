@@ -35,7 +35,7 @@ def test_oracle_planners_match_reference(name):
 
 
 def test_oracle_exhaustive_matches_reference():
-    for name in ("battery_acceptance", "battery_oracle_ties"):
+    for name in ("battery_acceptance", "battery_oracle_ties", "battery_oracle_float"):
         bat = Battery(name)
         for k in range(0, bat.n, 3 if name == "battery_acceptance" else 1):
             inst = bat.inst(k)
@@ -153,7 +153,7 @@ def test_oracle_simulator_matches_reference():
 
 def test_golden_files_present():
     for f in ("battery_acceptance.npz", "battery_special.npz", "battery_float.npz",
-              "battery_oracle_ties.npz", "battery_wide.npz", "dp_tables.npz", "cost_model.json",
+              "battery_oracle_ties.npz", "battery_oracle_float.npz", "battery_wide.npz", "dp_tables.npz", "cost_model.json",
               "units.npz", "build_problem.json", "sweep_acceptance.csv", "sweep_small.csv",
               "sim.npz", "gen_golden.py"):
         assert (GOLDEN / f).exists(), f
