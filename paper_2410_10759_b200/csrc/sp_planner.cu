@@ -654,11 +654,14 @@ struct Trace {
 #ifndef SP_STEPS_G
 #define SP_STEPS_G 32
 #endif
+#ifndef SP_STEPS_WPB
+#define SP_STEPS_WPB 3
+#endif
 template <int CAP> constexpr int steps_group() { return CAP >= 1024 ? 32 : SP_STEPS_G; }
-template <int CAP> constexpr int steps_wpb() { return CAP >= 1024 ? 1 : 4; }
+template <int CAP> constexpr int steps_wpb() { return CAP >= 1024 ? 1 : SP_STEPS_WPB; }
 size_t steps_smem(int mode, int cap) {
-  const int G = cap >= 1024 ? 32 : SP_STEPS_G, WPB = cap >= 1024 ? 1 : 4;
-  return (size_t)WPB * (32 / G) * 6 * (size_t)cap * (4 + value_bytes(mode));
+  const int G = cap >= 1024 ? 32 : SP_STEPS_G, WPB = cap >= 1024 ? 1 : SP_STEPS_WPB;
+  return (size_t)WPB * (32 / G) * kStepsArrays * (size_t)cap * (4 + value_bytes(mode));
 }
 
 template <int MODE, int CAP>
