@@ -226,6 +226,14 @@ class ClockSampler:
             self.source = "nvidia-smi, 100 ms"
             self.thread = threading.Thread(target=self._smi_loop, daemon=True)
         self.thread.start()
+        # the sampler is live before the timed region opens; only samples
+        # taken inside the region are kept
+        t0 = time.perf_counter()
+        while not self.sm and time.perf_counter() - t0 < 2.0:
+            time.sleep(0.002)
+        self.sm.clear()
+        self.mx.clear()
+        self.reasons.clear()
         return self
 
     def __exit__(self, *exc):

@@ -227,140 +227,10 @@ __device__ __forceinline__ int steps_merge(const int32_t* ac, const V* av, int n
   return total > CAP ? -1 : total;
 }
 
-// The same merge without the scratch (2 x CAP events less shared memory per
-// instance, more resident warps): a first serial pass over the lane's part
-// only counts the kept events (and the first stay column before its first
-// kept event), a group scan places them, a second serial pass writes them;
-// a breakpoint whose segment continues into later lanes takes its stay
-// column from the first of them that sees one before its own first kept
-// event.
-template <int MODE, int G, int CAP, bool ADD, typename V>
-__device__ __forceinline__ int steps_merge_2p(const int32_t* ac, const V* av, int na, int ha, const int32_t* bc,
-                                              const V* bv, int nb, int hb, int W, V rk, int32_t* oc, V* ov,
-                                              int2* gent, int g, uint32_t gmask) {
-  const V NEG = VT<MODE>::neg();
-  constexpr int32_t COLM = 0x7fffffff;
-  {
-    int ca = 0, cb = 0;
-    const int nmax = max(na, nb);
-    for (int base = 0; base < nmax; base += G) {
-      const int x = base + g;
-      ca += __popc(__ballot_sync(gmask, x < na && ac[x] <= W - ha));
-      cb += __popc(__ballot_sync(gmask, x < nb && bc[x] <= W - hb));
-    }
-    na = ha > W ? 0 : ca;
-    nb = hb > W ? 0 : cb;
-  }
-  const int ne = na + nb;
-  int i0, j0;
-  {
-    const int d = (ne * g) / G;
-    int lo = max(0, d - nb), hi = min(d, na);
-    while (lo < hi) {
-      const int m = (lo + hi) >> 1;
-      if (ac[m] + ha <= bc[d - m - 1] + hb) lo = m + 1;
-      else hi = m;
-    }
-    i0 = lo;
-    j0 = d - lo;
-    if (i0 > 0 && j0 < nb && ac[i0 - 1] + ha == bc[j0] + hb) ++j0;
-  }
-  int i1 = __shfl_down_sync(gmask, i0, 1, G), j1 = __shfl_down_sync(gmask, j0, 1, G);
-  if (g == G - 1) {
-    i1 = na;
-    j1 = nb;
-  }
-  const V va0 = i0 > 0 ? av[i0 - 1] : NEG, vb0 = j0 > 0 ? bv[j0 - 1] : NEG;
-  V y0;
-  {
-    const V x = steps_max<MODE>(va0, vb0);
-    y0 = (ADD && x != NEG) ? steps_add<MODE>(x, rk) : x;
-  }
-  // one serial walk of the lane's part; `emit(col, y, keep, stay)` per event
-  auto walk = [&](auto&& emit) {
-    int i = i0, j = j0;
-    V va = va0, vb = vb0, prev = y0;
-    int cA = i < i1 ? ac[i] + ha : COLM, cB = j < j1 ? bc[j] + hb : COLM;
-    V nA = i < i1 ? av[i] : NEG, nB = j < j1 ? bv[j] : NEG;
-    while (i < i1 || j < j1) {
-      const bool tA = cA <= cB, tB = cB <= cA;
-      const int col = tA ? cA : cB;
-      if (tA) {
-        va = nA;
-        ++i;
-        cA = i < i1 ? ac[i] + ha : COLM;
-        nA = i < i1 ? av[i] : nA;
-      }
-      if (tB) {
-        vb = nB;
-        ++j;
-        cB = j < j1 ? bc[j] + hb : COLM;
-        nB = j < j1 ? bv[j] : nB;
-      }
-      const V x = steps_max<MODE>(va, vb);
-      const V y = ADD ? steps_add<MODE>(x, rk) : x;
-      const bool keep = prev == NEG ? y != NEG : y != prev;
-      const bool stay = va != NEG && (ADD ? steps_add<MODE>(va, rk) == y : va == y);
-      emit(col, y, keep, stay);
-      prev = y;
-    }
-  };
-  int nkeep = 0;
-  int32_t lead_stay = kNoStay;
-  walk([&](int col, V, bool keep, bool stay) {
-    if (keep) ++nkeep;
-    else if (nkeep == 0 && stay && lead_stay == kNoStay) lead_stay = col;
-  });
-  int pos = nkeep;
-#pragma unroll
-  for (int o = 1; o < G; o <<= 1) {
-    const int v = __shfl_up_sync(gmask, pos, o, G);
-    if (g >= o) pos += v;
-  }
-  const int total = __shfl_sync(gmask, pos, G - 1, G);
-  pos -= nkeep;
-  // the stay column of this lane's last breakpoint if its segment runs on:
-  // the first later lane that sees one before its own first kept event
-  int32_t inherit = kNoStay;
-  {
-    bool open = true;
-#pragma unroll
-    for (int o = 1; o < G; ++o) {
-      const int32_t ls = __shfl_down_sync(gmask, lead_stay, o, G);
-      const int nk = __shfl_down_sync(gmask, nkeep, o, G);
-      if (open && g + o < G) {
-        if (ls != kNoStay) {
-          inherit = ls;
-          open = false;
-        } else if (nk > 0) {
-          open = false;
-        }
-      }
-    }
-  }
-  if (total > CAP) return -1;
-  int w = pos - 1;  // slot of this lane's open breakpoint
-  int32_t open_stay = kNoStay;
-  walk([&](int col, V y, bool keep, bool stay) {
-    if (keep) {
-      if (w >= pos) gent[w] = make_int2(oc[w], open_stay);  // close the previous one
-      ++w;
-      oc[w] = col;
-      ov[w] = y;
-      open_stay = stay ? col : kNoStay;
-    } else if (stay && open_stay == kNoStay && w >= pos) {
-      open_stay = col;
-    }
-  });
-  if (w >= pos) gent[w] = make_int2(oc[w], open_stay != kNoStay ? open_stay : inherit);
-  __syncwarp(gmask);
-  return total;
-}
-
-#ifndef SP_STEPS_TWO_PASS
-#define SP_STEPS_TWO_PASS 0
-#endif
-constexpr int kStepsArrays = SP_STEPS_TWO_PASS ? 4 : 6;  // lists of CAP per instance in shared memory
+// lists of CAP entries per instance in shared memory: rows [2 bufs][C|S] +
+// the merge scratch [2 CAP].  (A two-pass merge without the scratch -- 4
+// lists, more resident warps -- measured slower: 2.43 vs 1.84 ms at CAP 256.)
+constexpr int kStepsArrays = 6;
 
 // One group of G lanes per instance, WPB warps per block; rows double-buffered
 // in the group's shared memory, every row's (column, stay_from) written to the
@@ -385,10 +255,8 @@ __global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
   unsigned char* ws = smem + (size_t)(warp * GPW + grp) * INST_BYTES;
   int32_t* rc = reinterpret_cast<int32_t*>(ws);    // [2][2][CAP]
   V* rvv = reinterpret_cast<V*>(ws + 4 * CAP * 4);  // [2][2][CAP]
-#if !SP_STEPS_TWO_PASS
   int32_t* ecs = reinterpret_cast<int32_t*>(ws + 4 * CAP * (4 + sizeof(V)));            // [2 CAP]
   V* eys = reinterpret_cast<V*>(ws + 4 * CAP * (4 + sizeof(V)) + 2 * CAP * 4);         // [2 CAP]
-#endif
   auto rcol = [&](int buf, int row) { return rc + (buf * 2 + row) * CAP; };
   auto rval = [&](int buf, int row) { return rvv + (buf * 2 + row) * CAP; };
 
@@ -429,21 +297,12 @@ __global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
     const V rk = MODE == VM_INT32 ? (V)(int32_t)bits : (V)__longlong_as_double(bits);
     const int nb = buf ^ 1;
     const size_t r0 = (size_t)(t + 1) * 2;
-#if SP_STEPS_TWO_PASS
-    const int nC2 = steps_merge_2p<MODE, G, CAP, true, V>(rcol(buf, 0), rval(buf, 0), nC, sh.i, rcol(buf, 1),
-                                                          rval(buf, 1), nS, sh.id, W, rk, rcol(nb, 0), rval(nb, 0),
-                                                          g_ent + r0 * CAP, g, gmask);
-    const int nS2 = steps_merge_2p<MODE, G, CAP, false, V>(rcol(buf, 1), rval(buf, 1), nS, sh.s, rcol(buf, 0),
-                                                           rval(buf, 0), nC, sh.su, W, rk, rcol(nb, 1), rval(nb, 1),
-                                                           g_ent + (r0 + 1) * CAP, g, gmask);
-#else
     const int nC2 = steps_merge<MODE, G, CAP, true, V>(rcol(buf, 0), rval(buf, 0), nC, sh.i, rcol(buf, 1),
                                                        rval(buf, 1), nS, sh.id, W, rk, ecs, eys, rcol(nb, 0),
                                                        rval(nb, 0), g_ent + r0 * CAP, g, gmask);
     const int nS2 = steps_merge<MODE, G, CAP, false, V>(rcol(buf, 1), rval(buf, 1), nS, sh.s, rcol(buf, 0),
                                                         rval(buf, 0), nC, sh.su, W, rk, ecs, eys, rcol(nb, 1),
                                                         rval(nb, 1), g_ent + (r0 + 1) * CAP, g, gmask);
-#endif
     if (nC2 < 0 || nS2 < 0) {
       over = true;
       break;
@@ -485,10 +344,13 @@ __global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
 // per round).  Device path: instances whose flag is still set are left
 // alone; wave path: overflowed ones.  Value-free: one launch serves every
 // value domain.
+constexpr int kBtSmemStages = 255;  // row counts of instances up to this many stages sit in shared memory
+
 template <int CAP, int G, int WPB>
 __global__ void __launch_bounds__(WPB * 32) backtrack_steps_kernel(sp_instances in, StepsArgs a,
                                                                    int32_t* idx_scratch, sp_policies out) {
   constexpr int GPW = 32 / G;
+  __shared__ int32_t scnt[WPB * GPW][2 * (kBtSmemStages + 1)];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / G, g = lane % G;
   const uint32_t gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
@@ -516,11 +378,19 @@ __global__ void __launch_bounds__(WPB * 32) backtrack_steps_kernel(sp_instances 
   const uint8_t* st = steps_store_of<CAP>(a, item, inst);
   const int32_t* g_cnt = reinterpret_cast<const int32_t*>(st);
   const int2* g_ent = reinterpret_cast<const int2*>(st + steps_cnt_bytes(L));
+  if (L <= kBtSmemStages) {  // the row counts once, instead of one dependent load per step
+    int32_t* sc = scnt[warp * GPW + grp];
+    for (int x = g; x < 2 * (L + 1); x += G) sc[x] = g_cnt[x];
+    __syncwarp(gmask);
+    g_cnt = sc;
+  }
   bool client = ec >= es;
   int64_t j = inf.w_eff;
   int32_t status = SP_OK;
+  StageShift sh_next = a.shifts[lo + L - 1];
   for (int k = L; k >= 1; --k) {
-    const StageShift sh = a.shifts[lo + k - 1];
+    const StageShift sh = sh_next;
+    if (k > 1) sh_next = a.shifts[lo + k - 2];
     const size_t r = (size_t)k * 2 + (client ? 0 : 1);
     const int2* ent = g_ent + r * CAP;
     // G-ary search for the number of breakpoints at or left of j
