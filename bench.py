@@ -436,10 +436,18 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # SPLITPLAN_BENCH_BACKEND=gloo: exercise the N > 1 path with every rank on
+    # the devices there are (a one-GPU box); the driver's runs use NCCL
+    backend = os.environ.get("SPLITPLAN_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2410_10759_b200 import _native as N
     from paper_2410_10759_b200 import batch as B
