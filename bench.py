@@ -295,6 +295,18 @@ class Profile:
         self.launches, self.variant = al.value, var.value
 
 
+def _l2_ceiling():
+    """Measured mixed-mode L2 throughput (GB/s) of the newest profiles/rNN/l2_ceiling run."""
+    for d in sorted((ROOT / "profiles").glob("r*"), reverse=True):
+        f = d / "l2_ceiling" / "l2_bandwidth.jsonl"
+        if f.exists():
+            vals = [json.loads(l)["total_GBps"] for l in f.read_text().splitlines()
+                    if l.strip() and json.loads(l).get("mode") == "mixed"]
+            if vals:
+                return max(vals), str(f.relative_to(ROOT))
+    return None, None
+
+
 def roofline(prof: Profile, step_ms_total: float) -> dict:
     peak, peak_kind = measured_peak_hbm()
     n = max(prof.n, 1)
@@ -324,7 +336,16 @@ def roofline(prof: Profile, step_ms_total: float) -> dict:
         out["note"] = ("breakpoint lists: the algorithmic bytes are the stage records read (24 B/stage) and the "
                        "breakpoints stored for the backtrack (8 B each + 4 B per row); the kernel is bound by "
                        "instruction issue and shared-memory latency of its merges, not by HBM (DESIGN.md 4)")
-    elif prof.variant in (4, 5):
+    if prof.variant == 4 and doc and rate:
+        # the rows live in L2: the L2 bytes per cell (ncu) against the L2
+        # ceiling measured with the kernel's own data path (tools/l2_bandwidth.cu)
+        l2doc, l2src = _l2_ceiling()
+        per_cell = doc["l2_read_bytes_per_cell"] + 8.0 + 0.25
+        if l2doc:
+            out["l2"] = {"bytes_per_cell": per_cell, "achieved_GBps": rate * per_cell / 1e9,
+                         "ceiling_GBps": l2doc, "ceiling_source": l2src,
+                         "frac": rate * per_cell / 1e9 / l2doc}
+    if prof.variant in (4, 5):
         out["note"] = ("dense L2-row kernel: algorithmic HBM bytes = the 2-bit packed back-pointers (0.25 B/cell); "
                        "the rows stay in L2; the survey's 33 B/cell row-streaming design would need "
                        f"{(rate or 0) * 33 / 1e9:.0f} GB/s for this rate")
