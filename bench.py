@@ -543,14 +543,24 @@ def main():
     prof_ms = p0.elapsed_time(p1)
 
     # ---- end-to-end timing (host buffers, copies inside) ------------------
-    for _ in range(2):  # warm the host -> device path (pinned staging, allocator)
-        step_e2e()
+    # warm the host <-> device path (pinned staging, allocator) holding the
+    # previous step's results while the next one runs, as the timed loop does
+    s, out = step_e2e()
+    for _ in range(max(args.warmup, 3)):
+        s, out = step_e2e()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    trace = os.environ.get("SPLITPLAN_BENCH_TRACE")
+    tw = []
     e0.record(stream)
     for _ in range(args.steps):
+        if trace:
+            tw.append(time.perf_counter())
         s, out = step_e2e()
     e1.record(stream)
+    if trace:
+        tw.append(time.perf_counter())
+        print("e2e step wall ms:", [round((b - a) * 1e3, 3) for a, b in zip(tw, tw[1:])], file=sys.stderr)
     barrier()
     e2e_ms = e0.elapsed_time(e1)
     d2h = sum(t.numel() * t.element_size() for t in out)
