@@ -1,4 +1,4 @@
-// K2 / K3 on breakpoint lists: the DP rows as monotone step functions.
+// K2 + K3 on breakpoint lists: the DP rows as monotone step functions.
 //
 // Fragment of sp_planner.cu: included there inside namespace sp::(anonymous),
 // after the declarations it uses; not a standalone header.
@@ -29,22 +29,35 @@
 // predecessor is non-decreasing, so the predicate is false on a prefix of the
 // segment and true on the rest: each breakpoint records `stay_from`, the
 // first column of its segment where it holds (kNoStay: nowhere), found during
-// the merge from the predecessor breakpoints the merge walks anyway.  The
+// the merge from the predecessor events the merge produces anyway.  The
 // backtrack then needs ONE lookup per stage -- the breakpoint of the current
 // row that covers j -- instead of re-deriving table values.
 //
-// Work decomposition: a group of G lanes per instance (G = 8: four instances
-// per warp; G = 32 for the wide tier).  A merge splits the merged order of
-// the two shifted lists into G equal diagonals (merge path: one binary search
-// per lane); each lane walks its part sequentially keeping the events whose
-// value differs from the previous one; a first pass counts them, a group scan
-// places them, a second pass writes them.
+// Work decomposition: one warp per instance; the two merges of a stage run
+// side by side, half-warp 0 building the C row and half-warp 1 the S row,
+// in lockstep (every ballot and shuffle is full-warp, every loop trip count
+// warp-uniform), so a stage costs one merge's latency chain.  A merge splits
+// the merged order of its two shifted lists into 16 equal diagonals (merge
+// path, one binary search per lane); each lane merges its part serially into
+// a scratch array at the merged positions -- every event carries the row
+// value after it and whether the stay predecessor reproduces it -- counting
+// the events it keeps (value differs from the previous slot's); a scan of
+// the counts places them, and each lane writes its kept breakpoints with
+// their stay_from.  The new row overwrites the old one (both merges have
+// finished reading the old rows by then), so shared memory holds
+// two rows and two scratch arrays per instance.
 //
-// Store of one instance (read by the backtrack): (L+1) rows x {C, S}, each a
-// count and CAP int2 {column, stay_from}, at a position the kernel computes
-// itself -- (layer_off[k] + k) * steps_row_pair_bytes(CAP) -- in the
-// device-planned tier (no host planning), or at DpWork::bp_off in the wave
-// path:   cnt int32[(L+1) * 2] (16-B aligned) | ent int2[(L+1) * 2][CAP]
+// The same warp then walks the instance back (end-side choice, planner.py:
+// 182-202; _backtrace, planner.py:146-179) through the rows it has just
+// stored -- row counts and the first 32 breakpoints of both candidate rows
+// are fetched one stage ahead -- and computes _finish (planner.py:88-101)
+// with the placement and the compacted r values in shared memory.
+//
+// Store of one instance (read by the walk): (L+1) rows x {C, S}, each a count
+// and CAP int2 {column, stay_from}, at a position the kernel computes itself
+// -- (layer_off[k] + k) * steps_row_pair_bytes(CAP) -- in the device-planned
+// tier (no host planning), or at DpWork::bp_off in the wave path:
+//   cnt int32[(L+1) * 2] (16-B aligned) | ent int2[(L+1) * 2][CAP]
 #pragma once
 
 constexpr int kStepsCap = 192;       // tier 1: every instance, device-planned, a warp each
@@ -78,9 +91,13 @@ struct StepsArgs {
   int32_t* flag;               // [n] device path: cleared once the instance is solved here (prep sets it)
   unsigned long long* solved;  // device path: [instances, DP cells, breakpoints stored, stages] solved here
   int32_t* overflow;           // wave path: [n] 1 = a row exceeded CAP
+  int32_t* idx;                // [total_layers] scratch of _finish for instances too long for shared memory
   int64_t n_items;
   int64_t max_cols;            // device path: wider instances are left to the dense kernels
   int64_t min_cols[2];         // device path, [int32, fp64 domain]: narrower ones too (one CTA's SMEM holds them)
+  int32_t walk;                // 1: walk back and finish every solved instance (the policies below)
+  sp_instances in;
+  sp_policies out;
 };
 
 template <int CAP>
@@ -89,176 +106,251 @@ __device__ __forceinline__ uint8_t* steps_store_of(const StepsArgs& a, int64_t i
                 : a.store + (size_t)(a.layer_off[inst] + inst) * steps_row_pair_bytes(CAP);
 }
 
-// first index in c[0, n) with c[idx] > x
-__device__ __forceinline__ int upper_bound_i32(const int32_t* c, int n, int32_t x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int m = (lo + hi) >> 1;
-    if (c[m] <= x) lo = m + 1;
-    else hi = m;
-  }
-  return lo;
-}
+constexpr uint32_t kFull = 0xffffffffu;
 
-// One merge by a group of G lanes (g: lane in the group, gmask: the group's
-// lanes): out = max(A shifted by ha, B shifted by hb) over columns <= W (+ r
-// when ADD: the C row), with the stay_from of every kept breakpoint (A is the
-// stay predecessor).  Writes the kept breakpoints to (oc, ov) in shared memory
-// and their (column, stay_from) to `gent` in the store.  Returns the count, or
-// -1 when it exceeds CAP.
-//   1. merge path: lane g takes diagonal [ne*g/G, ne*(g+1)/G) of the merged
-//      order (one binary search; an equal-column pair is never split);
-//   2. it merges its part serially into the scratch (ec, ey) at the merged
+// One merge by the 16 lanes of half-warp h (g: lane in the half), run by both
+// halves at once: out = max(A shifted by ha, B shifted by hb) over columns
+// <= W, plus rk (0 for the S row: the add is exact then) on reachable values,
+// with the stay_from of every kept breakpoint (A is the stay predecessor).
+// Writes the kept breakpoints to (oc, ov) in shared memory -- which may be
+// A's or B's storage: the old rows are dead once the merge phase is over --
+// and their (column, stay_from) to `gent` in the store.  Returns the count,
+// or -1 when it exceeds CAP.
+//   1. clip: only columns <= W - shift take part (usually the last one
+//      already fits; otherwise a ballot count over the sorted list);
+//   2. merge path: lane g takes diagonal [ne*g/16, ne*(g+1)/16) of the merged
+//      order (one binary search; an equal-column pair is never split), and
+//      merges its part serially into the scratch (ec, ey) at the merged
 //      positions -- every event carries the row value after it and whether
 //      the stay predecessor reproduces that value (bit 31 of the column);
-//      slots freed by merged equal-column pairs repeat the previous value;
-//   3. a ballot compaction keeps the events whose value differs from the
-//      previous slot's, and each kept event finds its segment's first stay
-//      column by scanning the (short) run of events up to the next kept one.
-template <int MODE, int G, int CAP, bool ADD, typename V>
-__device__ __forceinline__ int steps_merge(const int32_t* ac, const V* av, int na, int ha, const int32_t* bc,
-                                           const V* bv, int nb, int hb, int W, V rk, int32_t* ec, V* ey,
-                                           int32_t* oc, V* ov, int2* gent, int g, uint32_t gmask) {
+//      slots freed by merged equal-column pairs repeat the previous value.
+//      An event is kept iff its value differs from the previous slot's; the
+//      lane knows the value before its part, so it counts its own;
+//   3. a scan of the counts over the half places every lane's kept events;
+//   4. each lane re-reads its part and writes its kept breakpoints; a kept
+//      breakpoint's stay_from is the column of the first stay event from it
+//      up to the next kept one -- in the lane's own part, or in the first
+//      later part holding a kept or a stay event (one ballot).
+template <int MODE, int CAP, typename V>
+__device__ __forceinline__ int steps_merge_half(const int32_t* ac, const V* av, int na, int ha, const int32_t* bc,
+                                                const V* bv, int nb, int hb, int W, V rk, int32_t* ec, V* ey,
+                                                int32_t* oc, V* ov, int2* gent, int g, int h) {
   const V NEG = VT<MODE>::neg();
   constexpr int32_t STAY = (int32_t)0x80000000u;
   constexpr int32_t COLM = 0x7fffffff;
-  // columns <= W only: ballot counts over the sorted lists
+  const int hs = h << 4;
+  // 1. clip to columns <= W
+  if (ha > W) na = 0;
+  if (hb > W) nb = 0;
   {
-    int ca = 0, cb = 0;
-    const int nmax = max(na, nb);
-    for (int base = 0; base < nmax; base += G) {  // uniform trip count: every lane ballots
-      const int x = base + g;
-      ca += __popc(__ballot_sync(gmask, x < na && ac[x] <= W - ha));
-      cb += __popc(__ballot_sync(gmask, x < nb && bc[x] <= W - hb));
+    const bool needA = na > 0 && ac[na - 1] > W - ha;
+    const bool needB = nb > 0 && bc[nb - 1] > W - hb;
+    int trips = (needA || needB) ? (max(na, nb) + 15) >> 4 : 0;
+    trips = max(trips, __shfl_xor_sync(kFull, trips, 16));
+    if (trips) {
+      int ca = 0, cb = 0;
+      for (int t = 0; t < trips; ++t) {
+        const int x = (t << 4) + g;
+        const uint32_t ba = __ballot_sync(kFull, needA && x < na && ac[x] <= W - ha);
+        const uint32_t bb = __ballot_sync(kFull, needB && x < nb && bc[x] <= W - hb);
+        ca += __popc((ba >> hs) & 0xffffu);
+        cb += __popc((bb >> hs) & 0xffffu);
+      }
+      if (needA) na = ca;
+      if (needB) nb = cb;
     }
-    na = ha > W ? 0 : ca;
-    nb = hb > W ? 0 : cb;
   }
+  // 2. merge path + serial merge into the scratch; every lane knows the row
+  // value just before its part (y0), so it marks its own kept events
   const int ne = na + nb;
+  const int k0 = (ne * g) >> 4, kend = g == 15 ? ne : (ne * (g + 1)) >> 4;
   int i0, j0;
   {
-    const int d = (ne * g) / G;
-    int lo = max(0, d - nb), hi = min(d, na);
+    int lo = max(0, k0 - nb), hi = min(k0, na);
     while (lo < hi) {
       const int m = (lo + hi) >> 1;
-      if (ac[m] + ha <= bc[d - m - 1] + hb) lo = m + 1;
+      if (ac[m] + ha <= bc[k0 - m - 1] + hb) lo = m + 1;
       else hi = m;
     }
     i0 = lo;
-    j0 = d - lo;
+    j0 = k0 - lo;
     if (i0 > 0 && j0 < nb && ac[i0 - 1] + ha == bc[j0] + hb) ++j0;
   }
-  int i1 = __shfl_down_sync(gmask, i0, 1, G), j1 = __shfl_down_sync(gmask, j0, 1, G);
-  if (g == G - 1) {
+  int i1 = __shfl_down_sync(kFull, i0, 1, 16), j1 = __shfl_down_sync(kFull, j0, 1, 16);
+  if (g == 15) {
     i1 = na;
     j1 = nb;
   }
-  const int kend = g == G - 1 ? ne : (ne * (g + 1)) / G;
-  V va = i0 > 0 ? av[i0 - 1] : NEG, vb = j0 > 0 ? bv[j0 - 1] : NEG;
-  V y;
+  V y0;             // the row value just before this lane's part
+  int nk = 0;       // kept events in this lane's part
+  bool kept = false;
+  int32_t fs_pre = kNoStay;  // first stay event of this part before its first kept one
   {
-    const V x = steps_max<MODE>(va, vb);
-    y = (ADD && x != NEG) ? steps_add<MODE>(x, rk) : x;
-  }
-  int i = i0, j = j0, k = (ne * g) / G;
-  int cA = i < i1 ? ac[i] + ha : COLM, cB = j < j1 ? bc[j] + hb : COLM;
-  V nA = i < i1 ? av[i] : NEG, nB = j < j1 ? bv[j] : NEG;
-  while (i < i1 || j < j1) {
-    const bool tA = cA <= cB, tB = cB <= cA;
-    const int col = tA ? cA : cB;
-    if (tA) {
-      va = nA;
-      ++i;
-      cA = i < i1 ? ac[i] + ha : COLM;
-      nA = i < i1 ? av[i] : nA;
+    V va = i0 > 0 ? av[i0 - 1] : NEG, vb = j0 > 0 ? bv[j0 - 1] : NEG;
+    {
+      const V x = steps_max<MODE>(va, vb);
+      y0 = x != NEG ? steps_add<MODE>(x, rk) : x;
     }
-    if (tB) {
-      vb = nB;
-      ++j;
-      cB = j < j1 ? bc[j] + hb : COLM;
-      nB = j < j1 ? bv[j] : nB;
-    }
-    const V x = steps_max<MODE>(va, vb);
-    y = ADD ? steps_add<MODE>(x, rk) : x;
-    const bool stay = va != NEG && (ADD ? steps_add<MODE>(va, rk) == y : va == y);
-    ec[k] = stay ? (col | STAY) : col;
-    ey[k] = y;
-    ++k;
-  }
-  for (; k < kend; ++k) {  // freed by merged pairs: the value continues, no event
-    ec[k] = COLM;
-    ey[k] = y;
-  }
-  __syncwarp(gmask);
-  const uint32_t below = (1u << (threadIdx.x & 31)) - 1u;
-  int total = 0;
-  for (int base = 0; base < ne; base += G) {
-    const int e = base + g;
-    bool keep = false;
-    int32_t c = COLM;
-    V v = NEG;
-    if (e < ne) {
-      c = ec[e];
-      v = ey[e];
-      keep = e == 0 ? v != NEG : v != ey[e - 1];
-    }
-    const uint32_t m = __ballot_sync(gmask, keep);
-    const int pos = total + __popc(m & below);
-    if (keep && pos < CAP) {
-      const int col = c & COLM;
-      oc[pos] = col;
-      ov[pos] = v;
-      // first stay column of this breakpoint's segment: this event or a later
-      // one before the next kept event
-      int32_t sf = kNoStay;
-      for (int f = e; f < ne; ++f) {
-        const int32_t cf = ec[f];
-        if (f > e && ey[f] != ey[f - 1]) break;
-        if (cf & STAY) {
-          sf = cf & COLM;
-          break;
-        }
+    V y = y0;
+    int i = i0, j = j0, k = k0;
+    int cA = i < i1 ? ac[i] + ha : COLM, cB = j < j1 ? bc[j] + hb : COLM;
+    V nA = i < i1 ? av[i] : NEG, nB = j < j1 ? bv[j] : NEG;
+    while (i < i1 || j < j1) {
+      const bool tA = cA <= cB, tB = cB <= cA;
+      const int col = tA ? cA : cB;
+      if (tA) {
+        va = nA;
+        ++i;
+        cA = i < i1 ? ac[i] + ha : COLM;
+        nA = i < i1 ? av[i] : nA;
       }
-      gent[pos] = make_int2(col, sf);
+      if (tB) {
+        vb = nB;
+        ++j;
+        cB = j < j1 ? bc[j] + hb : COLM;
+        nB = j < j1 ? bv[j] : nB;
+      }
+      // after an event one side holds a breakpoint value: the max is reachable
+      const V yn = steps_add<MODE>(steps_max<MODE>(va, vb), rk);
+      const bool stay = va != NEG && steps_add<MODE>(va, rk) == yn;
+      const bool keep = yn != y;
+      if (!kept && !keep && stay && fs_pre == kNoStay) fs_pre = col;
+      kept |= keep;
+      nk += keep ? 1 : 0;
+      ec[k] = stay ? (col | STAY) : col;
+      ey[k] = yn;
+      y = yn;
+      ++k;
     }
-    total += __popc(m);
+    for (; k < kend; ++k) {  // freed by merged pairs: the value continues, no event
+      ec[k] = COLM;
+      ey[k] = y;
+    }
   }
-  __syncwarp(gmask);
+  // 3. output positions (a scan of the kept counts over the half) and the
+  // stay_from of a segment running past this lane's part: the first later
+  // lane with a kept event or an earlier stay event decides it
+  int incl = nk;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const int t = __shfl_up_sync(kFull, incl, o, 16);
+    if (g >= o) incl += t;
+  }
+  const int total = __shfl_sync(kFull, incl, hs + 15);
+  const uint32_t T = (__ballot_sync(kFull, kept || fs_pre != kNoStay) >> hs) & 0xffffu;
+  const uint32_t nxt = g == 15 ? 0u : (T >> (g + 1)) << (g + 1);
+  const int32_t tail_in = __shfl_sync(kFull, fs_pre, hs + (nxt ? __ffs(nxt) - 1 : g));
+  const int32_t tail_sf = nxt ? tail_in : kNoStay;
+  __syncwarp(kFull);  // both halves are done reading the old rows
+  // 4. this lane writes its kept breakpoints: the new row (over the old one)
+  // and (column, stay_from) to the store
+  {
+    int pos = incl - nk, open = -1;
+    int32_t ocol = 0;
+    V prev = y0;
+    for (int k = k0; k < kend; ++k) {
+      const int32_t c = ec[k];
+      const V v = ey[k];
+      const int32_t col = c & COLM;
+      if (v != prev) {
+        if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, kNoStay);
+        if (pos < CAP) {
+          oc[pos] = col;
+          ov[pos] = v;
+        }
+        open = pos;
+        ocol = col;
+        ++pos;
+      }
+      if (open >= 0 && (c & STAY)) {
+        if (open < CAP) gent[open] = make_int2(ocol, col);
+        open = -1;
+      }
+      prev = v;
+    }
+    if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, tail_sf);
+  }
+  __syncwarp(kFull);
   return total > CAP ? -1 : total;
 }
 
-// lists of CAP entries per instance in shared memory: rows [2 bufs][C|S] +
-// the merge scratch [2 CAP].  (A two-pass merge without the scratch -- 4
-// lists, more resident warps -- measured slower: 2.43 vs 1.84 ms at CAP 256.)
+// numpy-order _finish (planner.py:88-101) of a placement held in shared
+// memory by the whole warp: exact integer latency (any order), the placement
+// to global memory, r compacted into client / server order in `buf`, then the
+// two numpy pairwise sums (np_sum, one lane, shared-memory operands).
+__device__ __forceinline__ void finish_policy_warp(const sp_instances& in, int64_t inst, int64_t lo, int L,
+                                                   const uint8_t* pis, double* buf, const sp_policies& out,
+                                                   bool infeasible, int lane) {
+  const bool sac = in.source_at_client[inst] != 0;
+  const uint32_t below = (1u << lane) - 1u;
+  long long lat = 0;
+  int n1 = 0;
+  for (int base = 0; base < L; base += 32) {
+    const int k = base + lane;
+    const bool v = k < L;
+    const int x = v ? pis[k] : 0;
+    if (v) {
+      const int prev = k == 0 ? (sac ? 1 : 0) : pis[k - 1];
+      lat += x ? in.client_units[lo + k] + (prev == 0 ? in.down_units[lo + k] : 0)
+               : in.server_units[lo + k] + (prev == 1 ? in.up_units[lo + k] : 0);
+      out.pi[lo + k] = (uint8_t)x;
+    }
+    n1 += __popc(__ballot_sync(kFull, v && x));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lat += __shfl_xor_sync(kFull, lat, o);
+  int a = 0, b = n1;
+  for (int base = 0; base < L; base += 32) {
+    const int k = base + lane;
+    const bool v = k < L;
+    const int x = v ? pis[k] : 0;
+    const uint32_t bc = __ballot_sync(kFull, v && x), bs = __ballot_sync(kFull, v && !x);
+    if (v) buf[x ? a + __popc(bc & below) : b + __popc(bs & below)] = in.r[lo + k];
+    a += __popc(bc);
+    b += __popc(bs);
+  }
+  __syncwarp(kFull);
+  if (lane == 0) {
+    out.client_value[inst] = np_sum([&](int64_t m) { return buf[m]; }, n1);
+    out.server_load[inst] = np_sum([&](int64_t m) { return buf[n1 + m]; }, L - n1);
+    out.integer_latency[inst] = (int64_t)lat;
+    out.feasible[inst] = infeasible ? 0 : ((int64_t)lat <= in.budget[inst] ? 1 : 0);
+    out.status[inst] = SP_OK;
+  }
+}
+
+// lists of CAP entries per instance in shared memory: rows [C|S] + the two
+// merges' scratch [2][2 CAP]
 constexpr int kStepsArrays = 6;
 
-// One group of G lanes per instance, WPB warps per block; rows double-buffered
-// in the group's shared memory, every row's (column, stay_from) written to the
-// instance's store.  Device path (a.work == null): group k takes instance k if
-// it is in this kernel's value domain and min_cols <= W_eff + 1 < max_cols.
-template <int MODE, int CAP, int G, int WPB>
-__global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
+// One warp per instance, WPB warps per block: forward pass over the
+// breakpoint lists, every row's (column, stay_from) written to the
+// instance's store, then (a.walk) the walk back and _finish.  Device path
+// (a.work == null): warp k takes instance k if it is in this kernel's value
+// domain and min_cols <= W_eff + 1 < max_cols; an instance whose rows outgrow
+// CAP keeps its flag (device path) / gets its overflow bit (wave path) and
+// is left to the next tier.
+template <int MODE, int CAP, int WPB>
+__global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(StepsArgs a) {
   using V = typename VT<MODE>::T;
-  constexpr int GPW = 32 / G;                                        // groups (instances) per warp
-  constexpr size_t INST_BYTES = (size_t)kStepsArrays * CAP * (4 + sizeof(V));  // rows [2 bufs][C|S] (+ merge scratch)
+  constexpr size_t INST_BYTES = (size_t)kStepsArrays * CAP * (4 + sizeof(V));
+  constexpr size_t SCRATCH_BYTES = (size_t)4 * CAP * (4 + sizeof(V));
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane / G, g = lane % G;
-  const uint32_t gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
-  const int64_t item = ((int64_t)blockIdx.x * WPB + warp) * GPW + grp;
-  if (item >= a.n_items) return;  // whole groups leave together
+  const int h = lane >> 4, g = lane & 15;
+  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
+  if (item >= a.n_items) return;  // whole warps leave together
   const int64_t inst = a.work ? a.work[item].inst : item;
   const InstInfo inf = a.info[inst];
   if (!a.work && (inf.mode != MODE || inf.w_eff + 1 >= a.max_cols ||
                   inf.w_eff + 1 < a.min_cols[MODE == VM_INT32 ? 0 : 1]))
     return;
-  unsigned char* ws = smem + (size_t)(warp * GPW + grp) * INST_BYTES;
-  int32_t* rc = reinterpret_cast<int32_t*>(ws);    // [2][2][CAP]
-  V* rvv = reinterpret_cast<V*>(ws + 4 * CAP * 4);  // [2][2][CAP]
-  int32_t* ecs = reinterpret_cast<int32_t*>(ws + 4 * CAP * (4 + sizeof(V)));            // [2 CAP]
-  V* eys = reinterpret_cast<V*>(ws + 4 * CAP * (4 + sizeof(V)) + 2 * CAP * 4);         // [2 CAP]
-  auto rcol = [&](int buf, int row) { return rc + (buf * 2 + row) * CAP; };
-  auto rval = [&](int buf, int row) { return rvv + (buf * 2 + row) * CAP; };
+  unsigned char* ws = smem + (size_t)warp * INST_BYTES;
+  int32_t* rcol = reinterpret_cast<int32_t*>(ws);                 // [2 rows][CAP]
+  V* rval = reinterpret_cast<V*>(ws + 2 * CAP * 4);               // [2 rows][CAP]
+  unsigned char* scratch = ws + 2 * CAP * (4 + sizeof(V));
+  int32_t* ecs = reinterpret_cast<int32_t*>(scratch);             // [2 halves][2 CAP]
+  V* eys = reinterpret_cast<V*>(scratch + 4 * CAP * 4);           // [2 halves][2 CAP]
 
   const int64_t lo = a.layer_off[inst];
   const int L = (int)(a.layer_off[inst + 1] - lo);
@@ -269,21 +361,17 @@ __global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
   int2* g_ent = reinterpret_cast<int2*>(st + steps_cnt_bytes(L));
 
   // row 0: the origin side holds +0 everywhere, the other side nothing
-  int nC = sac ? 1 : 0, nS = sac ? 0 : 1;
+  int nMine = (h == 0) == sac ? 1 : 0;  // breakpoints of row h (C for h = 0)
+  int nOther = 1 - nMine;
   if (g == 0) {
-    rcol(0, 0)[0] = 0;
-    rval(0, 0)[0] = V(0);
-    rcol(0, 1)[0] = 0;
-    rval(0, 1)[0] = V(0);
-    g_cnt[0] = nC;
-    g_cnt[1] = nS;
-    g_ent[0] = make_int2(0, kNoStay);
-    g_ent[CAP] = make_int2(0, kNoStay);
+    rcol[h * CAP] = 0;
+    rval[h * CAP] = V(0);
+    g_cnt[h] = nMine;
+    g_ent[h * CAP] = make_int2(0, kNoStay);
   }
-  __syncwarp(gmask);
-  int buf = 0;
+  __syncwarp(kFull);
   bool over = false;
-  unsigned long long stored = (unsigned long long)(nC + nS);
+  unsigned long long stored = 1;
   // stage records one stage ahead: their load latency overlaps the merges
   StageShift sh_next = a.shifts[lo];
   int64_t bits_next = a.rv[lo];
@@ -294,140 +382,134 @@ __global__ void __launch_bounds__(WPB * 32) dp_steps_kernel(StepsArgs a) {
       sh_next = a.shifts[lo + t + 1];
       bits_next = a.rv[lo + t + 1];
     }
-    const V rk = MODE == VM_INT32 ? (V)(int32_t)bits : (V)__longlong_as_double(bits);
-    const int nb = buf ^ 1;
+    const V rk = h ? V(0) : (MODE == VM_INT32 ? (V)(int32_t)bits : (V)__longlong_as_double(bits));
     const size_t r0 = (size_t)(t + 1) * 2;
-    const int nC2 = steps_merge<MODE, G, CAP, true, V>(rcol(buf, 0), rval(buf, 0), nC, sh.i, rcol(buf, 1),
-                                                       rval(buf, 1), nS, sh.id, W, rk, ecs, eys, rcol(nb, 0),
-                                                       rval(nb, 0), g_ent + r0 * CAP, g, gmask);
-    const int nS2 = steps_merge<MODE, G, CAP, false, V>(rcol(buf, 1), rval(buf, 1), nS, sh.s, rcol(buf, 0),
-                                                        rval(buf, 0), nC, sh.su, W, rk, ecs, eys, rcol(nb, 1),
-                                                        rval(nb, 1), g_ent + (r0 + 1) * CAP, g, gmask);
-    if (nC2 < 0 || nS2 < 0) {
+    const int n2 = steps_merge_half<MODE, CAP, V>(
+        rcol + h * CAP, rval + h * CAP, nMine, h ? sh.s : sh.i, rcol + (1 - h) * CAP, rval + (1 - h) * CAP, nOther,
+        h ? sh.su : sh.id, W, rk, ecs + h * 2 * CAP, eys + h * 2 * CAP, rcol + h * CAP, rval + h * CAP,
+        g_ent + (r0 + h) * CAP, g, h);
+    const int n2o = __shfl_xor_sync(kFull, n2, 16);
+    if (n2 < 0 || n2o < 0) {
       over = true;
       break;
     }
-    nC = nC2;
-    nS = nS2;
-    stored += (unsigned long long)(nC + nS);
-    buf = nb;
-    if (g == 0) {
-      g_cnt[r0] = nC;
-      g_cnt[r0 + 1] = nS;
-    }
-    __syncwarp(gmask);
+    nMine = n2;
+    nOther = n2o;
+    stored += (unsigned long long)n2;  // this half's row (lane 0 reports half 0's; summed below)
+    if (g == 0) g_cnt[r0 + h] = n2;
+    __syncwarp(kFull);
   }
-  if (g == 0) {
-    if (a.overflow) a.overflow[inst] = over ? 1 : 0;
-    if (!over) {
-      // value at column W: the last breakpoint (every stored column is <= W)
-      const V NEG = VT<MODE>::neg();
-      const V ec_ = nC > 0 ? rval(buf, 0)[nC - 1] : NEG;
-      const V es_ = nS > 0 ? rval(buf, 1)[nS - 1] : NEG;
-      a.info[inst].end_c = to_f64(ec_, inf.scale);
-      a.info[inst].end_s = to_f64(es_, inf.scale);
-      if (a.flag) a.flag[inst] = 0;
-      if (a.solved) {
-        atomicAdd(a.solved, 1ull);
-        atomicAdd(a.solved + 1, (unsigned long long)L * (unsigned long long)(W + 1));  // DP cells solved
-        atomicAdd(a.solved + 2, stored);
-        atomicAdd(a.solved + 3, (unsigned long long)L);
-      }
+  stored += __shfl_xor_sync(kFull, stored, 16) - 1;  // both rows of every stage (+ the origin row)
+  const int nC = h == 0 ? nMine : nOther, nS = h == 0 ? nOther : nMine;
+  if (a.overflow && lane == 0) a.overflow[inst] = over ? 1 : 0;
+  if (over) return;
+  // value at column W: the last breakpoint (every stored column is <= W)
+  const V NEG = VT<MODE>::neg();
+  const double end_c = to_f64(nC > 0 ? rval[nC - 1] : NEG, inf.scale);
+  const double end_s = to_f64(nS > 0 ? rval[CAP + nS - 1] : NEG, inf.scale);
+  if (lane == 0) {
+    a.info[inst].end_c = end_c;
+    a.info[inst].end_s = end_s;
+    if (a.flag) a.flag[inst] = 0;
+    if (a.solved) {
+      atomicAdd(a.solved, 1ull);
+      atomicAdd(a.solved + 1, (unsigned long long)L * (unsigned long long)(W + 1));  // DP cells solved
+      atomicAdd(a.solved + 2, stored);
+      atomicAdd(a.solved + 3, (unsigned long long)L);
     }
   }
-}
+  if (!a.walk) return;
 
-// K3 on breakpoint lists: end-side argmax (planner.py:190-200) and the walk
-// of planner.py:146-179 -- per stage, the breakpoint of the current row that
-// covers j decides stay (j >= stay_from) or switch -- then _finish.  One group
-// of G lanes per instance; a lookup is a G-ary search (G independent loads
-// per round).  Device path: instances whose flag is still set are left
-// alone; wave path: overflowed ones.  Value-free: one launch serves every
-// value domain.
-constexpr int kBtSmemStages = 255;  // row counts of instances up to this many stages sit in shared memory
-
-template <int CAP, int G, int WPB>
-__global__ void __launch_bounds__(WPB * 32) backtrack_steps_kernel(sp_instances in, StepsArgs a,
-                                                                   int32_t* idx_scratch, sp_policies out) {
-  constexpr int GPW = 32 / G;
-  __shared__ int32_t scnt[WPB * GPW][2 * (kBtSmemStages + 1)];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane / G, g = lane % G;
-  const uint32_t gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
-  const int64_t item = ((int64_t)blockIdx.x * WPB + warp) * GPW + grp;
-  if (item >= a.n_items) return;
-  const int64_t inst = a.work ? a.work[item].inst : item;
-  if (a.work ? a.overflow[inst] != 0 : a.flag[inst] != 0) return;
-  const InstInfo inf = a.info[inst];
-  const int64_t lo = in.layer_off[inst];
-  const int L = (int)(in.layer_off[inst + 1] - lo);
-  double ec = inf.end_c, es = inf.end_s;
-  const int8_t must = in.must_end_at ? in.must_end_at[inst] : (int8_t)-1;
+  // ---- the walk back: end side (planner.py:182-202), _backtrace (146-179)
+  double ec = end_c, es = end_s;
+  const int8_t must = a.in.must_end_at ? a.in.must_end_at[inst] : (int8_t)-1;
   if (must == 1) es = -INFINITY;
   else if (must == 0) ec = -INFINITY;
   const double pmax = (es > ec) ? es : ec;  // Python builtin max(end_c, end_s)
-  uint8_t* pi = out.pi + lo;
-  if (pmax == -INFINITY) {  // _infeasible
-    if (g == 0) {
-      for (int k = 0; k < L; ++k) pi[k] = 0;
-      finish_policy(in, inst, lo, L, idx_scratch + lo, out, true, false);
-      out.status[inst] = SP_OK;
+  // the placement and the compacted r values of _finish live in the scratch
+  // when they fit (pi bytes, then L doubles)
+  const size_t pi_bytes = ((size_t)L + 15) & ~(size_t)15;
+  const bool in_smem = pi_bytes + (size_t)L * 8 <= SCRATCH_BYTES;
+  uint8_t* pis = in_smem ? scratch : a.out.pi + lo;
+  double* buf = reinterpret_cast<double*>(scratch + pi_bytes);
+  const bool infeasible = pmax == -INFINITY;
+  int32_t status = SP_OK;
+  if (infeasible) {  // _infeasible: all-server placement, feasible = False
+    for (int k = lane; k < L; k += 32) pis[k] = 0;
+  } else {
+    bool client = ec >= es;
+    int64_t j = inf.w_eff;
+    // row counts and the first 64 breakpoints of both rows, one stage ahead
+    const int2* ent_n = g_ent + (size_t)(2 * L) * CAP;
+    int2 cnt_n = *reinterpret_cast<const int2*>(g_cnt + 2 * L);
+    int2 eC0_n = ent_n[lane], eC1_n = ent_n[lane + 32], eS0_n = ent_n[CAP + lane], eS1_n = ent_n[CAP + lane + 32];
+    StageShift sh_n = a.shifts[lo + L - 1];
+    for (int k = L; k >= 1; --k) {
+      const int2 cnt = cnt_n, eC0 = eC0_n, eC1 = eC1_n, eS0 = eS0_n, eS1 = eS1_n;
+      const StageShift sh = sh_n;
+      if (k > 1) {
+        ent_n = g_ent + (size_t)(2 * (k - 1)) * CAP;
+        cnt_n = *reinterpret_cast<const int2*>(g_cnt + 2 * (k - 1));
+        eC0_n = ent_n[lane];
+        eC1_n = ent_n[lane + 32];
+        eS0_n = ent_n[CAP + lane];
+        eS1_n = ent_n[CAP + lane + 32];
+        sh_n = a.shifts[lo + k - 2];
+      }
+      const int n = client ? cnt.x : cnt.y;
+      int c;         // breakpoints at or left of j
+      int32_t sf;    // stay_from of the one covering j
+      if (n <= 64) {
+        const int2 e0 = client ? eC0 : eS0, e1 = client ? eC1 : eS1;
+        c = __popc(__ballot_sync(kFull, lane < n && e0.x <= j)) +
+            __popc(__ballot_sync(kFull, lane + 32 < n && e1.x <= j));
+        sf = __shfl_sync(kFull, c > 32 ? e1.y : e0.y, (c - 1) & 31);
+      } else {  // 32-ary search over the row in the store
+        const int2* ent = g_ent + (size_t)(2 * k + (client ? 0 : 1)) * CAP;
+        int lo_i = 0, hi_i = n;  // the count lies in [lo_i, hi_i]
+        while (lo_i < hi_i) {
+          const int span = hi_i - lo_i;
+          const int step = (span + 32) / 33;
+          const int p = lo_i + (lane + 1) * step - 1;
+          const bool valid = p < hi_i;
+          const int cc = __popc(__ballot_sync(kFull, valid && ent[p].x <= j));
+          const int nv = __popc(__ballot_sync(kFull, valid));
+          const int nlo = lo_i + cc * step;
+          hi_i = cc < nv ? lo_i + (cc + 1) * step - 1 : hi_i;
+          lo_i = nlo;
+        }
+        c = lo_i;
+        sf = c > 0 ? ent[c - 1].y : kNoStay;
+      }
+      if (c == 0) {  // j left of the row's first breakpoint: unreachable
+        status = SP_ERR_BACKTRACE;
+        break;
+      }
+      const bool stay = j >= sf;
+      if (lane == 0) pis[k - 1] = client ? 1 : 0;
+      if (client) {
+        j -= stay ? sh.i : sh.id;
+        client = stay;
+      } else {
+        j -= stay ? sh.s : sh.su;
+        client = !stay;
+      }
+      if (j < 0) {  // no predecessor reproduces the value (planner.py:168-169 / 177-178)
+        status = SP_ERR_BACKTRACE;
+        break;
+      }
     }
+  }
+  __syncwarp(kFull);
+  if (status != SP_OK) {
+    if (lane == 0) a.out.status[inst] = status;
     return;
   }
-  const uint8_t* st = steps_store_of<CAP>(a, item, inst);
-  const int32_t* g_cnt = reinterpret_cast<const int32_t*>(st);
-  const int2* g_ent = reinterpret_cast<const int2*>(st + steps_cnt_bytes(L));
-  if (L <= kBtSmemStages) {  // the row counts once, instead of one dependent load per step
-    int32_t* sc = scnt[warp * GPW + grp];
-    for (int x = g; x < 2 * (L + 1); x += G) sc[x] = g_cnt[x];
-    __syncwarp(gmask);
-    g_cnt = sc;
+  if (in_smem) {
+    finish_policy_warp(a.in, inst, lo, L, pis, buf, a.out, infeasible, lane);
+  } else if (lane == 0) {
+    sp_policies o = a.out;
+    finish_policy(a.in, inst, lo, L, a.idx + lo, o, infeasible, false);
+    a.out.status[inst] = SP_OK;
   }
-  bool client = ec >= es;
-  int64_t j = inf.w_eff;
-  int32_t status = SP_OK;
-  StageShift sh_next = a.shifts[lo + L - 1];
-  for (int k = L; k >= 1; --k) {
-    const StageShift sh = sh_next;
-    if (k > 1) sh_next = a.shifts[lo + k - 2];
-    const size_t r = (size_t)k * 2 + (client ? 0 : 1);
-    const int2* ent = g_ent + r * CAP;
-    // G-ary search for the number of breakpoints at or left of j
-    int lo_i = 0, hi_i = g_cnt[r];  // the count lies in [lo_i, hi_i]
-    while (lo_i < hi_i) {
-      const int span = hi_i - lo_i;
-      const int step = (span + G) / (G + 1);
-      const int p = lo_i + (g + 1) * step - 1;  // this lane's pivot
-      const bool valid = p < hi_i;
-      const int c = __popc(__ballot_sync(gmask, valid && ent[p].x <= j));  // pivots <= j: a prefix
-      const int nv = __popc(__ballot_sync(gmask, valid));
-      const int nlo = lo_i + c * step;
-      hi_i = c < nv ? lo_i + (c + 1) * step - 1 : hi_i;
-      lo_i = nlo;
-    }
-    if (lo_i == 0) {  // j left of the row's first breakpoint: unreachable
-      status = SP_ERR_BACKTRACE;
-      break;
-    }
-    const bool stay = j >= ent[lo_i - 1].y;
-    if (client) {
-      if (g == 0) pi[k - 1] = 1;
-      j -= stay ? sh.i : sh.id;
-      client = stay;
-    } else {
-      if (g == 0) pi[k - 1] = 0;
-      j -= stay ? sh.s : sh.su;
-      client = !stay;
-    }
-    if (j < 0) {  // no predecessor reproduces the value (planner.py:168-169 / 177-178)
-      status = SP_ERR_BACKTRACE;
-      break;
-    }
-  }
-  __syncwarp(gmask);
-  if (g != 0) return;
-  out.status[inst] = status;
-  if (status != SP_OK) return;
-  finish_policy(in, inst, lo, L, idx_scratch + lo, out, false, false);
 }

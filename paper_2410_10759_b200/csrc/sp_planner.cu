@@ -8,8 +8,8 @@
 //                      windows)
 //   dp_grid.cuh        K2 for one huge instance (cfg5): dp_grid_kernel over
 //                      capacity partitions, checkpoint/backtrack kernels
-//   dp_steps.cuh       K2 / K3 on breakpoint lists (rows as step functions):
-//                      dp_steps_kernel, backtrack_steps_kernel
+//   dp_steps.cuh       K2 + K3 on breakpoint lists (rows as step functions):
+//                      dp_steps_kernel (forward pass, walk back, _finish)
 //   this file          backtrack_kernel (K3: end-side choice + pointer walk +
 //                      _finish, planner.py:88-107, 146-202), prefix_kernel
 //                      (greedy / all-server / all-client, planner.py:205-225),
@@ -650,52 +650,39 @@ struct Trace {
 
 // ---- breakpoint-list kernels ------------------------------------------------
 
-// tier geometry: lanes per instance and warps per block
-#ifndef SP_STEPS_G
-#define SP_STEPS_G 32
-#endif
+// tier geometry: warps (instances) per block
 #ifndef SP_STEPS_WPB
 #define SP_STEPS_WPB 3
 #endif
-template <int CAP> constexpr int steps_group() { return CAP >= 1024 ? 32 : SP_STEPS_G; }
 template <int CAP> constexpr int steps_wpb() { return CAP >= 1024 ? 1 : SP_STEPS_WPB; }
 size_t steps_smem(int mode, int cap) {
-  const int G = cap >= 1024 ? 32 : SP_STEPS_G, WPB = cap >= 1024 ? 1 : SP_STEPS_WPB;
-  return (size_t)WPB * (32 / G) * kStepsArrays * (size_t)cap * (4 + value_bytes(mode));
+  const int WPB = cap >= 1024 ? 1 : SP_STEPS_WPB;
+  return (size_t)WPB * kStepsArrays * (size_t)cap * (4 + value_bytes(mode));
 }
 
 template <int MODE, int CAP>
 int launch_steps_t(const StepsArgs& sa, cudaStream_t st) {
-  constexpr int G = steps_group<CAP>(), WPB = steps_wpb<CAP>(), PER_BLOCK = WPB * (32 / G);
-  auto kern = dp_steps_kernel<MODE, CAP, G, WPB>;
+  constexpr int WPB = steps_wpb<CAP>();
+  auto kern = dp_steps_kernel<MODE, CAP, WPB>;
   const size_t smem = steps_smem(MODE, CAP);
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "cudaFuncSetAttribute(dp_steps_kernel)");
   if (rc) return rc;
-  kern<<<(unsigned)((sa.n_items + PER_BLOCK - 1) / PER_BLOCK), WPB * 32, smem, st>>>(sa);
+  kern<<<(unsigned)((sa.n_items + WPB - 1) / WPB), WPB * 32, smem, st>>>(sa);
   return launch_check("dp_steps_kernel launch");
 }
-int launch_steps(int mode, int cap, const StepsArgs& sa, cudaStream_t st) {
+// K2 + K3 on breakpoint lists; `out` null: forward pass only
+int launch_steps(int mode, int cap, StepsArgs sa, const sp_instances* in, const sp_policies* out, int32_t* idx,
+                 cudaStream_t st) {
   if (sa.n_items == 0) return SP_OK;
+  sa.walk = out ? 1 : 0;
+  if (in) sa.in = *in;
+  if (out) sa.out = *out;
+  sa.idx = idx;
   if (cap == kStepsCap)
     return mode == VM_INT32 ? launch_steps_t<VM_INT32, kStepsCap>(sa, st) : launch_steps_t<VM_F64, kStepsCap>(sa, st);
   return mode == VM_INT32 ? launch_steps_t<VM_INT32, kStepsCapWide>(sa, st)
                           : launch_steps_t<VM_F64, kStepsCapWide>(sa, st);
-}
-
-template <int CAP>
-int launch_backtrack_steps_t(const sp_instances& in, const StepsArgs& sa, int32_t* idx, const sp_policies& out,
-                             cudaStream_t st) {
-  constexpr int G = CAP >= 1024 ? 32 : 8, WPB = 4, PER_BLOCK = WPB * (32 / G);
-  backtrack_steps_kernel<CAP, G, WPB><<<(unsigned)((sa.n_items + PER_BLOCK - 1) / PER_BLOCK), WPB * 32, 0, st>>>(
-      in, sa, idx, out);
-  return launch_check("backtrack_steps_kernel launch");
-}
-int launch_backtrack_steps(int cap, const sp_instances& in, const StepsArgs& sa, int32_t* idx,
-                           const sp_policies& out, cudaStream_t st) {
-  if (sa.n_items == 0) return SP_OK;
-  return cap == kStepsCap ? launch_backtrack_steps_t<kStepsCap>(in, sa, idx, out, st)
-                          : launch_backtrack_steps_t<kStepsCapWide>(in, sa, idx, out, st);
 }
 
 int forced_variant() {
@@ -759,7 +746,7 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables, 
   if (steps_cap > 0) {
     p.variant = DPV_STEPS;
     p.cfg = steps_cap;
-    p.threads = (steps_cap >= 1024 ? 1 : 4) * 32;
+    p.threads = (steps_cap >= 1024 ? 1 : SP_STEPS_WPB) * 32;
     p.smem = steps_smem(mode, steps_cap);
     p.bp = align_up(steps_store_bytes((int)L, steps_cap), 256);
     return p;
@@ -794,7 +781,8 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables, 
   return p;
 }
 
-int launch_plan(int mode, const DpPlan& p, const DpArgs& a, int64_t n_items, cudaStream_t st) {
+int launch_plan(int mode, const DpPlan& p, const DpArgs& a, int64_t n_items, cudaStream_t st,
+                const sp_instances* in = nullptr, const sp_policies* out = nullptr, int32_t* idx = nullptr) {
   if (n_items == 0) return SP_OK;
   switch (p.variant) {
     case DPV_STEPS: {
@@ -808,7 +796,7 @@ int launch_plan(int mode, const DpPlan& p, const DpArgs& a, int64_t n_items, cud
       sa.store = a.bp;
       sa.overflow = a.overflow;
       sa.n_items = n_items;
-      return launch_steps(mode, p.cfg, sa, st);
+      return launch_steps(mode, p.cfg, sa, in, out, idx, st);
     }
     case DPV_STREAM:
       switch (mode) {
@@ -1435,10 +1423,9 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       cudaEventCreate(&e1);
       cudaEventRecord(e0, st);
     }
-    if (!rc) rc = launch_steps(VM_INT32, kStepsCap, sa, st);
-    if (!rc) rc = launch_steps(VM_F64, kStepsCap, sa, st);
+    if (!rc) rc = launch_steps(VM_INT32, kStepsCap, sa, in, out, idx, st);
+    if (!rc) rc = launch_steps(VM_F64, kStepsCap, sa, in, out, idx, st);
     if (!rc && profiling()) cudaEventRecord(e1, st);
-    if (!rc) rc = launch_backtrack_steps(kStepsCap, *in, sa, idx, *out, st);
     unsigned long long hsolved[4] = {0, 0, 0, 0};  // instances, DP cells, breakpoints, stages
     if (!rc)
       rc = check_cuda(cudaMemcpyAsync(hsolved, solved, sizeof(hsolved), cudaMemcpyDeviceToHost, st),
@@ -1707,7 +1694,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
       }
-      rc = launch_plan(g.mode, g.plan, ga, cnt, st);
+      rc = launch_plan(g.mode, g.plan, ga, cnt, st, in, out, idx);
       if (rc) return rc;
       if (profiling()) {
         cudaEventRecord(e1, st);
@@ -1716,27 +1703,16 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       }
       first += cnt;
     }
-    if (out) {  // K3 per group: bit back-pointers or breakpoint lists
+    if (out) {  // K3 per dense group (the breakpoint-list kernel walks its own instances back)
       first = 0;
       for (const Group& g : groups) {
         const int64_t cnt = (int64_t)g.items.size();
-        if (g.plan.variant == DPV_STEPS) {
-          StepsArgs sa = {};
-          sa.layer_off = in->layer_off;
-          sa.info = info;
-          sa.shifts = shifts;
-          sa.rv = rv;
-          sa.work = work + first;
-          sa.store = dyn;
-          sa.overflow = overflow;
-          sa.n_items = cnt;
-          rc = launch_backtrack_steps(g.plan.cfg, *in, sa, idx, *out, st);
-        } else {
+        if (g.plan.variant != DPV_STEPS) {
           backtrack_kernel<<<(unsigned)((cnt + 127) / 128), 128, 0, st>>>(*in, info, shifts, work + first, cnt,
                                                                             dyn, idx, *out);
           rc = launch_check("backtrack_kernel launch");
+          if (rc) return rc;
         }
-        if (rc) return rc;
         first += cnt;
       }
     }
