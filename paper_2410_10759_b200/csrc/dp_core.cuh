@@ -80,24 +80,25 @@ __global__ void weff_kernel(sp_instances in, int64_t* w_eff) {
 // ---------------------------------------------------------------------------
 // prep: W_eff, value domain, clamped shifts, scaled values
 
+// One warp per instance (four per 128-thread block), no block barriers.
 // flag (optional): set to 1 for every instance (the breakpoint-list tier
 // clears it for the instances it solves).  steps_hi > 0: instances the
 // breakpoint-list tier takes (not NaN, steps_lo[domain] <= W_eff + 1 <
 // steps_hi) get the trivial frontier (0, 0) instead of the sequential
 // recurrence -- only the dense kernels use it, and skipping nothing is exact.
-__global__ void __launch_bounds__(128) prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts, int64_t* rv,
-                                                   int2* reach, int32_t* flag, int64_t steps_hi = 0,
-                                                   int64_t steps_lo_i32 = 0, int64_t steps_lo_f64 = 0) {
-  __shared__ int64_t sh64[32];
-  __shared__ uint64_t shu[32];
-  __shared__ int shi[32];
-  __shared__ StageShift tile[128];
-  for (int64_t k = blockIdx.x; k < in.n; k += gridDim.x) {
+constexpr int kPrepWarps = 4;
+__global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(sp_instances in, InstInfo* info, StageShift* shifts,
+                                                               int64_t* rv, int2* reach, int32_t* flag,
+                                                               int64_t steps_hi = 0, int64_t steps_lo_i32 = 0,
+                                                               int64_t steps_lo_f64 = 0) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * kPrepWarps;
+  for (int64_t k = (int64_t)blockIdx.x * kPrepWarps + (threadIdx.x >> 5); k < in.n; k += nw) {
     const int64_t lo = in.layer_off[k], hi = in.layer_off[k + 1];
     int64_t worst = 0;
     int finite = 1, integral = 1;
     uint64_t isum = 0, g = 0;
-    for (int64_t l = lo + threadIdx.x; l < hi; l += blockDim.x) {
+    for (int64_t l = lo + lane; l < hi; l += 32) {
       worst += max(in.client_units[l] + in.down_units[l], in.server_units[l] + in.up_units[l]);
       const double r = in.r[l];
       if (!isfinite(r)) {
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(128) prep_kernel(sp_instances in, InstInfo* in
         g = gcd_u64(g, v);
       }
     }
-    {  // the five block reductions in one pass: warp shuffles, one barrier
+    {
       const uint64_t sat = (uint64_t)1 << 62;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -120,27 +121,6 @@ __global__ void __launch_bounds__(128) prep_kernel(sp_instances in, InstInfo* in
         isum = min(isum + __shfl_xor_sync(0xffffffffu, isum, o), sat);
         g = gcd_u64(g, __shfl_xor_sync(0xffffffffu, g, o));
       }
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-      if (lane == 0) {
-        sh64[wid] = worst;
-        shi[wid] = finite & integral ? 3 : (finite ? 1 : (integral ? 2 : 0));
-        shu[wid] = isum;
-        shu[16 + wid] = g;
-      }
-      __syncthreads();
-      worst = sh64[0];
-      int fi = shi[0];
-      isum = shu[0];
-      g = shu[16];
-      for (int w = 1; w < nw; ++w) {
-        worst += sh64[w];
-        fi &= shi[w];
-        isum = min(isum + shu[w], sat);
-        g = gcd_u64(g, shu[16 + w]);
-      }
-      finite = fi & 1;
-      integral = (fi >> 1) & 1;
-      __syncthreads();  // the scratch is reused by the next instance
     }
     if (g == 0) g = 1;
     const int64_t W = min(in.budget[k], worst);
@@ -148,7 +128,7 @@ __global__ void __launch_bounds__(128) prep_kernel(sp_instances in, InstInfo* in
     if (!finite) mode = VM_F64_NAN;
     else if (integral && isum < ((uint64_t)1 << 53) && isum / g <= (uint64_t)INT32_MAX) mode = VM_INT32;
     else mode = VM_F64;
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       InstInfo r;
       r.w_eff = W;
       r.scale = (double)g;
@@ -164,44 +144,42 @@ __global__ void __launch_bounds__(128) prep_kernel(sp_instances in, InstInfo* in
     // reachable value (rows are monotone in j; every column below it is
     // unreachable, NEG-like).  reach[lo + k] describes the row stage k reads.
     // Not in the NaN domain, where "unreachable" cells may hold NaN.  The
-    // recurrence is sequential: the block stages each tile of clamped shifts
-    // in shared memory and thread 0 walks it there.
+    // recurrence is sequential: every lane runs it over the warp's 32 stage
+    // records (shuffled in turn) and keeps the value of its own stage.
     const bool sac = in.source_at_client[k] != 0;
     int64_t mc = sac ? 0 : cap, ms = sac ? cap : 0;
     const bool trivial = mode == VM_F64_NAN ||
                          (steps_hi > 0 && W + 1 < steps_hi && W + 1 >= (mode == VM_INT32 ? steps_lo_i32 : steps_lo_f64));
-    for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
-      const int64_t l = t0 + threadIdx.x;
+    for (int64_t t0 = lo; t0 < hi; t0 += 32) {
+      const int64_t l = t0 + lane;
+      StageShift sh = {0, 0, 0, 0};
       if (l < hi) {
         const int64_t i = in.client_units[l], s = in.server_units[l];
         const int64_t u = in.up_units[l], d = in.down_units[l];
-        StageShift sh;
         sh.i = (int32_t)min(i, cap);
         sh.id = (int32_t)min(i + d, cap);
         sh.s = (int32_t)min(s, cap);
         sh.su = (int32_t)min(s + u, cap);
         shifts[l] = sh;
-        tile[threadIdx.x] = sh;
-        if (trivial && reach) reach[l] = make_int2(0, 0);
         const double r = in.r[l];
-        if (mode == VM_INT32) {
-          rv[l] = (int64_t)((uint64_t)r / g);
-        } else {
-          rv[l] = __double_as_longlong(r);
-        }
+        rv[l] = mode == VM_INT32 ? (int64_t)((uint64_t)r / g) : __double_as_longlong(r);
       }
-      __syncthreads();
-      if (threadIdx.x == 0 && reach && !trivial) {
-        const int cnt = (int)min((int64_t)blockDim.x, hi - t0);
-        for (int x = 0; x < cnt; ++x) {
-          reach[t0 + x] = make_int2((int)min(mc, cap), (int)min(ms, cap));
-          const StageShift sh = tile[x];
-          const int64_t nc = min(mc + sh.i, ms + sh.id), ns = min(ms + sh.s, mc + sh.su);
-          mc = min(nc, cap);
-          ms = min(ns, cap);
-        }
+      if (!reach) continue;
+      if (trivial) {
+        if (l < hi) reach[l] = make_int2(0, 0);
+        continue;
       }
-      __syncthreads();
+      const int cnt = (int)min((int64_t)32, hi - t0);
+      int2 mine = make_int2(0, 0);
+      for (int x = 0; x < cnt; ++x) {
+        const int32_t si = __shfl_sync(0xffffffffu, sh.i, x), sid = __shfl_sync(0xffffffffu, sh.id, x);
+        const int32_t ss = __shfl_sync(0xffffffffu, sh.s, x), ssu = __shfl_sync(0xffffffffu, sh.su, x);
+        if (lane == x) mine = make_int2((int)min(mc, cap), (int)min(ms, cap));
+        const int64_t nc = min(mc + si, ms + sid), ns = min(ms + ss, mc + ssu);
+        mc = min(nc, cap);
+        ms = min(ns, cap);
+      }
+      if (l < hi) reach[l] = mine;
     }
   }
 }

@@ -322,6 +322,26 @@ __device__ __forceinline__ void finish_policy_warp(const sp_instances& in, int64
 // lists of CAP entries per instance in shared memory: rows [C|S] + the two
 // merges' scratch [2][2 CAP]
 constexpr int kStepsArrays = 6;
+// the walk's ring: stages fetched ahead, and the bytes of one stage (stage
+// record 16 | row counts 8 | pad 8 | 64 breakpoints of C | 64 of S)
+constexpr int kWalkDepth = 6;
+constexpr size_t kWalkSlot = 32 + 2 * 64 * 8;
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // One warp per instance, WPB warps per block: forward pass over the
 // breakpoint lists, every row's (column, stay_from) written to the
@@ -334,7 +354,6 @@ template <int MODE, int CAP, int WPB>
 __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(StepsArgs a) {
   using V = typename VT<MODE>::T;
   constexpr size_t INST_BYTES = (size_t)kStepsArrays * CAP * (4 + sizeof(V));
-  constexpr size_t SCRATCH_BYTES = (size_t)4 * CAP * (4 + sizeof(V));
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = lane >> 4, g = lane & 15;
@@ -426,60 +445,85 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
   if (must == 1) es = -INFINITY;
   else if (must == 0) ec = -INFINITY;
   const double pmax = (es > ec) ? es : ec;  // Python builtin max(end_c, end_s)
-  // the placement and the compacted r values of _finish live in the scratch
-  // when they fit (pi bytes, then L doubles)
+  // The walk runs out of the warp's shared memory, free now: the placement
+  // (L bytes), then a ring of kWalkDepth stages fetched ahead with cp.async
+  // -- the stage record, the row counts and the first 64 breakpoints of both
+  // rows of a stage -- so the L2 latency of the store stays off the chain of
+  // dependent lookups; _finish then reuses the ring for the r values.
+  // Instances too long for that walk with plain loads, placement in global.
   const size_t pi_bytes = ((size_t)L + 15) & ~(size_t)15;
-  const bool in_smem = pi_bytes + (size_t)L * 8 <= SCRATCH_BYTES;
-  uint8_t* pis = in_smem ? scratch : a.out.pi + lo;
-  double* buf = reinterpret_cast<double*>(scratch + pi_bytes);
+  const bool ring = pi_bytes + (size_t)kWalkDepth * kWalkSlot <= INST_BYTES;
+  const bool fin_smem = pi_bytes + (size_t)L * 8 <= INST_BYTES;
+  uint8_t* pis = ring ? ws : a.out.pi + lo;
+  unsigned char* rbase = ws + pi_bytes;
   const bool infeasible = pmax == -INFINITY;
   int32_t status = SP_OK;
+  __syncwarp(kFull);  // every lane is done with the rows and the scratch
+  // one stage of the store into ring slot k % kWalkDepth (one commit group)
+  auto fetch = [&](int k) {
+    if (k >= 1) {
+      unsigned char* sl = rbase + (size_t)(k % kWalkDepth) * kWalkSlot;
+      const int2* er = g_ent + (size_t)(2 * k) * CAP;
+      cp_async8(sl + 32 + lane * 8, er + lane);
+      cp_async8(sl + 32 + (lane + 32) * 8, er + lane + 32);
+      cp_async8(sl + 32 + 512 + lane * 8, er + CAP + lane);
+      cp_async8(sl + 32 + 512 + (lane + 32) * 8, er + CAP + lane + 32);
+      if (lane == 0) cp_async16(sl, a.shifts + lo + k - 1);
+      if (lane == 1) cp_async8(sl + 16, g_cnt + 2 * k);
+    }
+    cp_async_commit();
+  };
+  // the breakpoints of row `ent` (n of them) at or left of j, and the
+  // stay_from of the last of them, with plain loads (32-ary search)
+  auto search = [&](const int2* ent, int n, int64_t j, int& c, int32_t& sf) {
+    int lo_i = 0, hi_i = n;  // the count lies in [lo_i, hi_i]
+    while (lo_i < hi_i) {
+      const int span = hi_i - lo_i;
+      const int step = (span + 32) / 33;
+      const int p = lo_i + (lane + 1) * step - 1;
+      const bool valid = p < hi_i;
+      const int cc = __popc(__ballot_sync(kFull, valid && ent[p].x <= j));
+      const int nv = __popc(__ballot_sync(kFull, valid));
+      const int nlo = lo_i + cc * step;
+      hi_i = cc < nv ? lo_i + (cc + 1) * step - 1 : hi_i;
+      lo_i = nlo;
+    }
+    c = lo_i;
+    sf = c > 0 ? ent[c - 1].y : kNoStay;
+  };
   if (infeasible) {  // _infeasible: all-server placement, feasible = False
     for (int k = lane; k < L; k += 32) pis[k] = 0;
   } else {
     bool client = ec >= es;
     int64_t j = inf.w_eff;
-    // row counts and the first 64 breakpoints of both rows, one stage ahead
-    const int2* ent_n = g_ent + (size_t)(2 * L) * CAP;
-    int2 cnt_n = *reinterpret_cast<const int2*>(g_cnt + 2 * L);
-    int2 eC0_n = ent_n[lane], eC1_n = ent_n[lane + 32], eS0_n = ent_n[CAP + lane], eS1_n = ent_n[CAP + lane + 32];
-    StageShift sh_n = a.shifts[lo + L - 1];
+    if (ring)
+      for (int d = 0; d < kWalkDepth; ++d) fetch(L - d);
     for (int k = L; k >= 1; --k) {
-      const int2 cnt = cnt_n, eC0 = eC0_n, eC1 = eC1_n, eS0 = eS0_n, eS1 = eS1_n;
-      const StageShift sh = sh_n;
-      if (k > 1) {
-        ent_n = g_ent + (size_t)(2 * (k - 1)) * CAP;
-        cnt_n = *reinterpret_cast<const int2*>(g_cnt + 2 * (k - 1));
-        eC0_n = ent_n[lane];
-        eC1_n = ent_n[lane + 32];
-        eS0_n = ent_n[CAP + lane];
-        eS1_n = ent_n[CAP + lane + 32];
-        sh_n = a.shifts[lo + k - 2];
-      }
-      const int n = client ? cnt.x : cnt.y;
-      int c;         // breakpoints at or left of j
-      int32_t sf;    // stay_from of the one covering j
-      if (n <= 64) {
-        const int2 e0 = client ? eC0 : eS0, e1 = client ? eC1 : eS1;
-        c = __popc(__ballot_sync(kFull, lane < n && e0.x <= j)) +
-            __popc(__ballot_sync(kFull, lane + 32 < n && e1.x <= j));
-        sf = __shfl_sync(kFull, c > 32 ? e1.y : e0.y, (c - 1) & 31);
-      } else {  // 32-ary search over the row in the store
-        const int2* ent = g_ent + (size_t)(2 * k + (client ? 0 : 1)) * CAP;
-        int lo_i = 0, hi_i = n;  // the count lies in [lo_i, hi_i]
-        while (lo_i < hi_i) {
-          const int span = hi_i - lo_i;
-          const int step = (span + 32) / 33;
-          const int p = lo_i + (lane + 1) * step - 1;
-          const bool valid = p < hi_i;
-          const int cc = __popc(__ballot_sync(kFull, valid && ent[p].x <= j));
-          const int nv = __popc(__ballot_sync(kFull, valid));
-          const int nlo = lo_i + cc * step;
-          hi_i = cc < nv ? lo_i + (cc + 1) * step - 1 : hi_i;
-          lo_i = nlo;
+      const size_t rr = (size_t)(2 * k + (client ? 0 : 1)) * CAP;
+      StageShift sh;
+      int n, c;
+      int32_t sf;  // stay_from of the breakpoint covering j
+      if (ring) {
+        cp_async_wait<kWalkDepth - 1>();
+        __syncwarp(kFull);
+        const unsigned char* sl = rbase + (size_t)(k % kWalkDepth) * kWalkSlot;
+        sh = *reinterpret_cast<const StageShift*>(sl);
+        n = reinterpret_cast<const int32_t*>(sl + 16)[client ? 0 : 1];
+        if (n <= 64) {
+          const int2* e = reinterpret_cast<const int2*>(sl + 32 + (client ? 0 : 512));
+          const int2 e0 = e[lane], e1 = e[lane + 32];
+          c = __popc(__ballot_sync(kFull, lane < n && e0.x <= j)) +
+              __popc(__ballot_sync(kFull, lane + 32 < n && e1.x <= j));
+          sf = __shfl_sync(kFull, c > 32 ? e1.y : e0.y, (c - 1) & 31);
+        } else {
+          search(g_ent + rr, n, j, c, sf);
         }
-        c = lo_i;
-        sf = c > 0 ? ent[c - 1].y : kNoStay;
+        __syncwarp(kFull);  // the slot is refilled next
+        fetch(k - kWalkDepth);
+      } else {
+        sh = a.shifts[lo + k - 1];
+        n = g_cnt[2 * k + (client ? 0 : 1)];
+        search(g_ent + rr, n, j, c, sf);
       }
       if (c == 0) {  // j left of the row's first breakpoint: unreachable
         status = SP_ERR_BACKTRACE;
@@ -499,15 +543,18 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
         break;
       }
     }
+    if (ring) cp_async_wait<0>();  // no copy may land after the ring is reused
   }
   __syncwarp(kFull);
   if (status != SP_OK) {
     if (lane == 0) a.out.status[inst] = status;
     return;
   }
-  if (in_smem) {
-    finish_policy_warp(a.in, inst, lo, L, pis, buf, a.out, infeasible, lane);
+  if (ring && fin_smem) {
+    finish_policy_warp(a.in, inst, lo, L, pis, reinterpret_cast<double*>(rbase), a.out, infeasible, lane);
   } else if (lane == 0) {
+    if (ring)
+      for (int k = 0; k < L; ++k) a.out.pi[lo + k] = pis[k];
     sp_policies o = a.out;
     finish_policy(a.in, inst, lo, L, a.idx + lo, o, infeasible, false);
     a.out.status[inst] = SP_OK;

@@ -227,7 +227,7 @@ __device__ void integerize_request(const Src& src, const sp_requests& req, int64
   }
 }
 
-__global__ void cost_table_kernel(sp_models M, sp_requests req, int32_t integerize, sp_cost_table out) {
+__global__ void __launch_bounds__(256, 3) cost_table_kernel(sp_models M, sp_requests req, int32_t integerize, sp_cost_table out) {
   const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (k >= req.n) return;
   const int32_t m = req.model ? req.model[k] : 0;

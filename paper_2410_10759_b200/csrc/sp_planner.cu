@@ -1386,7 +1386,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   const int force = forced_variant();
   const bool steps_allowed = tab_c == nullptr && (force < 0 || force == DPV_STEPS);
   const bool steps_ok = steps_allowed && !q_min;
-  const int grid = (int)std::min<int64_t>(n, 1 << 20);
+  const int grid = (int)std::min<int64_t>((n + kPrepWarps - 1) / kPrepWarps, 1 << 20);
   const bool tier1_fits = steps_ok && out && fixed + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap) <= ws_bytes;
   const int64_t lo_i32 = steps_min_cols(VM_INT32, force), lo_f64 = steps_min_cols(VM_F64, force);
   prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv, reach, steps_ok ? flag : nullptr,
