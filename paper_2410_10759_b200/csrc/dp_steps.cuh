@@ -193,28 +193,29 @@ __device__ __forceinline__ int steps_merge_half(const int32_t* ac, const V* av, 
     }
     V y = y0;
     int i = i0, j = j0, k = k0;
-    int cA = i < i1 ? ac[i] + ha : COLM, cB = j < j1 ? bc[j] + hb : COLM;
-    V nA = i < i1 ? av[i] : NEG, nB = j < j1 ? bv[j] : NEG;
-    while (i < i1 || j < j1) {
+    // branch-free: both lists are re-read at clamped positions every event
+    // (a column past the lane's range reads as COLM)
+    const int ilast = max(i1 - 1, 0), jlast = max(j1 - 1, 0);
+    int cA = i < i1 ? ac[min(i, ilast)] + ha : COLM, cB = j < j1 ? bc[min(j, jlast)] + hb : COLM;
+    V nA = av[min(i, ilast)], nB = bv[min(j, jlast)];
+    while (min(cA, cB) != COLM) {
       const bool tA = cA <= cB, tB = cB <= cA;
-      const int col = tA ? cA : cB;
-      if (tA) {
-        va = nA;
-        ++i;
-        cA = i < i1 ? ac[i] + ha : COLM;
-        nA = i < i1 ? av[i] : nA;
-      }
-      if (tB) {
-        vb = nB;
-        ++j;
-        cB = j < j1 ? bc[j] + hb : COLM;
-        nB = j < j1 ? bv[j] : nB;
-      }
+      const int col = min(cA, cB);
+      va = tA ? nA : va;
+      vb = tB ? nB : vb;
+      i += tA ? 1 : 0;
+      j += tB ? 1 : 0;
+      const int ii = min(i, ilast), jj = min(j, jlast);
+      const int32_t xa = ac[ii], xb = bc[jj];
+      nA = av[ii];
+      nB = bv[jj];
+      cA = i < i1 ? xa + ha : COLM;
+      cB = j < j1 ? xb + hb : COLM;
       // after an event one side holds a breakpoint value: the max is reachable
       const V yn = steps_add<MODE>(steps_max<MODE>(va, vb), rk);
       const bool stay = va != NEG && steps_add<MODE>(va, rk) == yn;
       const bool keep = yn != y;
-      if (!kept && !keep && stay && fs_pre == kNoStay) fs_pre = col;
+      fs_pre = (!kept && !keep && stay && fs_pre == kNoStay) ? col : fs_pre;
       kept |= keep;
       nk += keep ? 1 : 0;
       ec[k] = stay ? (col | STAY) : col;
@@ -246,29 +247,25 @@ __device__ __forceinline__ int steps_merge_half(const int32_t* ac, const V* av, 
   // and (column, stay_from) to the store
   {
     int pos = incl - nk, open = -1;
-    int32_t ocol = 0;
+    int32_t ocol = 0, osf = kNoStay;  // the open breakpoint: column, stay_from found so far
     V prev = y0;
     for (int k = k0; k < kend; ++k) {
       const int32_t c = ec[k];
       const V v = ey[k];
       const int32_t col = c & COLM;
-      if (v != prev) {
-        if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, kNoStay);
-        if (pos < CAP) {
-          oc[pos] = col;
-          ov[pos] = v;
-        }
+      if (v != prev) {  // kept: the previous open breakpoint is complete
+        if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf);
+        oc[pos] = col;  // (pos < 2 CAP: past CAP only on overflow, inside this warp's region)
+        ov[pos] = v;
         open = pos;
         ocol = col;
+        osf = kNoStay;
         ++pos;
       }
-      if (open >= 0 && (c & STAY)) {
-        if (open < CAP) gent[open] = make_int2(ocol, col);
-        open = -1;
-      }
+      osf = (c < 0 && osf == kNoStay) ? col : osf;  // bit 31: a stay event
       prev = v;
     }
-    if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, tail_sf);
+    if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf != kNoStay ? osf : tail_sf);
   }
   __syncwarp(kFull);
   return total > CAP ? -1 : total;
