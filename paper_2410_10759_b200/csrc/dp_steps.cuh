@@ -108,60 +108,58 @@ __device__ __forceinline__ uint8_t* steps_store_of(const StepsArgs& a, int64_t i
 
 constexpr uint32_t kFull = 0xffffffffu;
 
+// A breakpoint (or a merge event) in shared memory: column and row value
+// side by side, one 8-B (int32 domain) or 16-B (fp64) access.
+template <int MODE> struct Ent;
+template <> struct __align__(8) Ent<VM_INT32> {
+  int32_t c;
+  int32_t v;
+};
+template <> struct __align__(16) Ent<VM_F64> {
+  int32_t c;
+  int32_t pad;
+  double v;
+};
+template <int MODE, typename V>
+__device__ __forceinline__ Ent<MODE> mk_ent(int32_t c, V v) {
+  Ent<MODE> e;
+  e.c = c;
+  e.v = v;
+  return e;
+}
+
 // One merge by the 16 lanes of half-warp h (g: lane in the half), run by both
 // halves at once: out = max(A shifted by ha, B shifted by hb) over columns
 // <= W, plus rk (0 for the S row: the add is exact then) on reachable values,
 // with the stay_from of every kept breakpoint (A is the stay predecessor).
-// Writes the kept breakpoints to (oc, ov) in shared memory -- which may be
-// A's or B's storage: the old rows are dead once the merge phase is over --
-// and their (column, stay_from) to `gent` in the store.  Returns the count,
-// or -1 when it exceeds CAP.
-//   1. clip: only columns <= W - shift take part (usually the last one
-//      already fits; otherwise a ballot count over the sorted list);
-//   2. merge path: lane g takes diagonal [ne*g/16, ne*(g+1)/16) of the merged
+// na / nb: the breakpoints of A / B at columns <= W - ha / W - hb (counted
+// by the previous stage's write pass).  Writes the kept breakpoints to `out`
+// in shared memory -- this half's old row: the old rows are dead once the
+// merge phase is over -- and their (column, stay_from) to `gent` in the
+// store.  Returns the count (or -1 when it exceeds CAP) and, for the next
+// stage, the new row's breakpoints at columns <= t1 / <= t2 (cnt1 / cnt2).
+//   1. merge path: lane g takes diagonal [ne*g/16, ne*(g+1)/16) of the merged
 //      order (one binary search; an equal-column pair is never split), and
-//      merges its part serially into the scratch (ec, ey) at the merged
-//      positions -- every event carries the row value after it and whether
-//      the stay predecessor reproduces that value (bit 31 of the column);
-//      slots freed by merged equal-column pairs repeat the previous value.
-//      An event is kept iff its value differs from the previous slot's; the
-//      lane knows the value before its part, so it counts its own;
-//   3. a scan of the counts over the half places every lane's kept events;
-//   4. each lane re-reads its part and writes its kept breakpoints; a kept
+//      merges its part serially into the scratch at the merged positions --
+//      every event carries the row value after it and whether the stay
+//      predecessor reproduces that value (bit 31 of the column); slots freed
+//      by merged equal-column pairs repeat the previous value.  An event is
+//      kept iff its value differs from the previous slot's; the lane knows
+//      the value before its part, so it counts its own;
+//   2. a scan of the counts over the half places every lane's kept events;
+//   3. each lane re-reads its part and writes its kept breakpoints; a kept
 //      breakpoint's stay_from is the column of the first stay event from it
 //      up to the next kept one -- in the lane's own part, or in the first
 //      later part holding a kept or a stay event (one ballot).
 template <int MODE, int CAP, typename V>
-__device__ __forceinline__ int steps_merge_half(const int32_t* ac, const V* av, int na, int ha, const int32_t* bc,
-                                                const V* bv, int nb, int hb, int W, V rk, int32_t* ec, V* ey,
-                                                int32_t* oc, V* ov, int2* gent, int g, int h) {
+__device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int ha, const Ent<MODE>* B, int nb,
+                                                int hb, V rk, Ent<MODE>* ev, Ent<MODE>* out, int2* gent, int g,
+                                                int h, int t1, int t2, int& cnt1, int& cnt2) {
   const V NEG = VT<MODE>::neg();
   constexpr int32_t STAY = (int32_t)0x80000000u;
   constexpr int32_t COLM = 0x7fffffff;
   const int hs = h << 4;
-  // 1. clip to columns <= W
-  if (ha > W) na = 0;
-  if (hb > W) nb = 0;
-  {
-    const bool needA = na > 0 && ac[na - 1] > W - ha;
-    const bool needB = nb > 0 && bc[nb - 1] > W - hb;
-    int trips = (needA || needB) ? (max(na, nb) + 15) >> 4 : 0;
-    trips = max(trips, __shfl_xor_sync(kFull, trips, 16));
-    if (trips) {
-      int ca = 0, cb = 0;
-      for (int t = 0; t < trips; ++t) {
-        const int x = (t << 4) + g;
-        const uint32_t ba = __ballot_sync(kFull, needA && x < na && ac[x] <= W - ha);
-        const uint32_t bb = __ballot_sync(kFull, needB && x < nb && bc[x] <= W - hb);
-        ca += __popc((ba >> hs) & 0xffffu);
-        cb += __popc((bb >> hs) & 0xffffu);
-      }
-      if (needA) na = ca;
-      if (needB) nb = cb;
-    }
-  }
-  // 2. merge path + serial merge into the scratch; every lane knows the row
-  // value just before its part (y0), so it marks its own kept events
+  // 1. merge path + serial merge into the scratch
   const int ne = na + nb;
   const int k0 = (ne * g) >> 4, kend = g == 15 ? ne : (ne * (g + 1)) >> 4;
   int i0, j0;
@@ -169,12 +167,12 @@ __device__ __forceinline__ int steps_merge_half(const int32_t* ac, const V* av, 
     int lo = max(0, k0 - nb), hi = min(k0, na);
     while (lo < hi) {
       const int m = (lo + hi) >> 1;
-      if (ac[m] + ha <= bc[k0 - m - 1] + hb) lo = m + 1;
+      if (A[m].c + ha <= B[k0 - m - 1].c + hb) lo = m + 1;
       else hi = m;
     }
     i0 = lo;
     j0 = k0 - lo;
-    if (i0 > 0 && j0 < nb && ac[i0 - 1] + ha == bc[j0] + hb) ++j0;
+    if (i0 > 0 && j0 < nb && A[i0 - 1].c + ha == B[j0].c + hb) ++j0;
   }
   int i1 = __shfl_down_sync(kFull, i0, 1, 16), j1 = __shfl_down_sync(kFull, j0, 1, 16);
   if (g == 15) {
@@ -186,7 +184,7 @@ __device__ __forceinline__ int steps_merge_half(const int32_t* ac, const V* av, 
   bool kept = false;
   int32_t fs_pre = kNoStay;  // first stay event of this part before its first kept one
   {
-    V va = i0 > 0 ? av[i0 - 1] : NEG, vb = j0 > 0 ? bv[j0 - 1] : NEG;
+    V va = i0 > 0 ? A[i0 - 1].v : NEG, vb = j0 > 0 ? B[j0 - 1].v : NEG;
     {
       const V x = steps_max<MODE>(va, vb);
       y0 = x != NEG ? steps_add<MODE>(x, rk) : x;
@@ -194,23 +192,21 @@ __device__ __forceinline__ int steps_merge_half(const int32_t* ac, const V* av, 
     V y = y0;
     int i = i0, j = j0, k = k0;
     // branch-free: both lists are re-read at clamped positions every event
-    // (a column past the lane's range reads as COLM)
+    // (a position past the lane's range reads as column COLM)
     const int ilast = max(i1 - 1, 0), jlast = max(j1 - 1, 0);
-    int cA = i < i1 ? ac[min(i, ilast)] + ha : COLM, cB = j < j1 ? bc[min(j, jlast)] + hb : COLM;
-    V nA = av[min(i, ilast)], nB = bv[min(j, jlast)];
+    Ent<MODE> ea = A[min(i, ilast)], eb = B[min(j, jlast)];
+    int cA = i < i1 ? ea.c + ha : COLM, cB = j < j1 ? eb.c + hb : COLM;
     while (min(cA, cB) != COLM) {
       const bool tA = cA <= cB, tB = cB <= cA;
       const int col = min(cA, cB);
-      va = tA ? nA : va;
-      vb = tB ? nB : vb;
+      va = tA ? ea.v : va;
+      vb = tB ? eb.v : vb;
       i += tA ? 1 : 0;
       j += tB ? 1 : 0;
-      const int ii = min(i, ilast), jj = min(j, jlast);
-      const int32_t xa = ac[ii], xb = bc[jj];
-      nA = av[ii];
-      nB = bv[jj];
-      cA = i < i1 ? xa + ha : COLM;
-      cB = j < j1 ? xb + hb : COLM;
+      ea = A[min(i, ilast)];
+      eb = B[min(j, jlast)];
+      cA = i < i1 ? ea.c + ha : COLM;
+      cB = j < j1 ? eb.c + hb : COLM;
       // after an event one side holds a breakpoint value: the max is reachable
       const V yn = steps_add<MODE>(steps_max<MODE>(va, vb), rk);
       const bool stay = va != NEG && steps_add<MODE>(va, rk) == yn;
@@ -218,17 +214,13 @@ __device__ __forceinline__ int steps_merge_half(const int32_t* ac, const V* av, 
       fs_pre = (!kept && !keep && stay && fs_pre == kNoStay) ? col : fs_pre;
       kept |= keep;
       nk += keep ? 1 : 0;
-      ec[k] = stay ? (col | STAY) : col;
-      ey[k] = yn;
+      ev[k] = mk_ent<MODE>(stay ? (col | STAY) : col, yn);
       y = yn;
       ++k;
     }
-    for (; k < kend; ++k) {  // freed by merged pairs: the value continues, no event
-      ec[k] = COLM;
-      ey[k] = y;
-    }
+    for (; k < kend; ++k) ev[k] = mk_ent<MODE>(COLM, y);  // freed by merged pairs: no event
   }
-  // 3. output positions (a scan of the kept counts over the half) and the
+  // 2. output positions (a scan of the kept counts over the half) and the
   // stay_from of a segment running past this lane's part: the first later
   // lane with a kept event or an earlier stay event decides it
   int incl = nk;
@@ -243,30 +235,37 @@ __device__ __forceinline__ int steps_merge_half(const int32_t* ac, const V* av, 
   const int32_t tail_in = __shfl_sync(kFull, fs_pre, hs + (nxt ? __ffs(nxt) - 1 : g));
   const int32_t tail_sf = nxt ? tail_in : kNoStay;
   __syncwarp(kFull);  // both halves are done reading the old rows
-  // 4. this lane writes its kept breakpoints: the new row (over the old one)
-  // and (column, stay_from) to the store
+  // 3. this lane writes its kept breakpoints: the new row (over the old one)
+  // and (column, stay_from) to the store; it counts the ones at columns
+  // <= t1 / t2 for the next stage's clip
+  int c1 = 0, c2 = 0;
   {
     int pos = incl - nk, open = -1;
     int32_t ocol = 0, osf = kNoStay;  // the open breakpoint: column, stay_from found so far
     V prev = y0;
     for (int k = k0; k < kend; ++k) {
-      const int32_t c = ec[k];
-      const V v = ey[k];
-      const int32_t col = c & COLM;
-      if (v != prev) {  // kept: the previous open breakpoint is complete
+      const Ent<MODE> e = ev[k];
+      const int32_t col = e.c & COLM;
+      if (e.v != prev) {  // kept: the previous open breakpoint is complete
         if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf);
-        oc[pos] = col;  // (pos < 2 CAP: past CAP only on overflow, inside this warp's region)
-        ov[pos] = v;
+        out[pos] = mk_ent<MODE>(col, e.v);  // (pos < 2 CAP: past CAP only on overflow, inside this warp's region)
         open = pos;
         ocol = col;
         osf = kNoStay;
         ++pos;
+        c1 += col <= t1 ? 1 : 0;
+        c2 += col <= t2 ? 1 : 0;
       }
-      osf = (c < 0 && osf == kNoStay) ? col : osf;  // bit 31: a stay event
-      prev = v;
+      osf = (e.c < 0 && osf == kNoStay) ? col : osf;  // bit 31: a stay event
+      prev = e.v;
     }
     if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf != kNoStay ? osf : tail_sf);
   }
+  // the half's sums, both halves in one reduction each (counts < 2^16)
+  cnt1 = __reduce_add_sync(kFull, (uint32_t)c1 << hs);
+  cnt2 = __reduce_add_sync(kFull, (uint32_t)c2 << hs);
+  cnt1 = (int)(((uint32_t)cnt1 >> hs) & 0xffffu);
+  cnt2 = (int)(((uint32_t)cnt2 >> hs) & 0xffffu);
   __syncwarp(kFull);
   return total > CAP ? -1 : total;
 }
@@ -316,8 +315,8 @@ __device__ __forceinline__ void finish_policy_warp(const sp_instances& in, int64
   }
 }
 
-// lists of CAP entries per instance in shared memory: rows [C|S] + the two
-// merges' scratch [2][2 CAP]
+// entries per instance in shared memory: rows [C|S] + the two merges'
+// events [2][2 CAP]
 constexpr int kStepsArrays = 6;
 // the walk's ring: stages fetched ahead, and the bytes of one stage (stage
 // record 16 | row counts 8 | pad 8 | 64 breakpoints of C | 64 of S)
@@ -350,7 +349,8 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int MODE, int CAP, int WPB>
 __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(StepsArgs a) {
   using V = typename VT<MODE>::T;
-  constexpr size_t INST_BYTES = (size_t)kStepsArrays * CAP * (4 + sizeof(V));
+  using E = Ent<MODE>;
+  constexpr size_t INST_BYTES = (size_t)kStepsArrays * CAP * sizeof(E);
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = lane >> 4, g = lane & 15;
@@ -362,11 +362,8 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
                   inf.w_eff + 1 < a.min_cols[MODE == VM_INT32 ? 0 : 1]))
     return;
   unsigned char* ws = smem + (size_t)warp * INST_BYTES;
-  int32_t* rcol = reinterpret_cast<int32_t*>(ws);                 // [2 rows][CAP]
-  V* rval = reinterpret_cast<V*>(ws + 2 * CAP * 4);               // [2 rows][CAP]
-  unsigned char* scratch = ws + 2 * CAP * (4 + sizeof(V));
-  int32_t* ecs = reinterpret_cast<int32_t*>(scratch);             // [2 halves][2 CAP]
-  V* eys = reinterpret_cast<V*>(scratch + 4 * CAP * 4);           // [2 halves][2 CAP]
+  E* rows = reinterpret_cast<E*>(ws);              // [2 rows: C, S][CAP]
+  E* evs = rows + 2 * CAP;                         // [2 halves][2 CAP] merge events
 
   const int64_t lo = a.layer_off[inst];
   const int L = (int)(a.layer_off[inst + 1] - lo);
@@ -377,52 +374,61 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
   int2* g_ent = reinterpret_cast<int2*>(st + steps_cnt_bytes(L));
 
   // row 0: the origin side holds +0 everywhere, the other side nothing
-  int nMine = (h == 0) == sac ? 1 : 0;  // breakpoints of row h (C for h = 0)
-  int nOther = 1 - nMine;
+  const int n0 = (h == 0) == sac ? 1 : 0;  // breakpoints of row h (C for h = 0)
   if (g == 0) {
-    rcol[h * CAP] = 0;
-    rval[h * CAP] = V(0);
-    g_cnt[h] = nMine;
+    rows[h * CAP] = mk_ent<MODE>(0, V(0));
+    g_cnt[h] = n0;
     g_ent[h * CAP] = make_int2(0, kNoStay);
   }
   __syncwarp(kFull);
   bool over = false;
   unsigned long long stored = 1;
+  int nMine = n0;  // breakpoints of row h
   // stage records one stage ahead: their load latency overlaps the merges
-  StageShift sh_next = a.shifts[lo];
-  int64_t bits_next = a.rv[lo];
+  StageShift sh = a.shifts[lo];
+  int64_t bits = a.rv[lo];
+  // clipped counts of this stage's two lists (row 0: the one breakpoint at column 0)
+  int na = (n0 && (h ? sh.s : sh.i) <= W) ? 1 : 0;
+  int nb = (!n0 && (h ? sh.su : sh.id) <= W) ? 1 : 0;
   for (int t = 0; t < L; ++t) {
-    const StageShift sh = sh_next;
-    const int64_t bits = bits_next;
+    StageShift sh_next = sh;
+    int64_t bits_next = bits;
     if (t + 1 < L) {
       sh_next = a.shifts[lo + t + 1];
       bits_next = a.rv[lo + t + 1];
     }
     const V rk = h ? V(0) : (MODE == VM_INT32 ? (V)(int32_t)bits : (V)__longlong_as_double(bits));
     const size_t r0 = (size_t)(t + 1) * 2;
-    const int n2 = steps_merge_half<MODE, CAP, V>(
-        rcol + h * CAP, rval + h * CAP, nMine, h ? sh.s : sh.i, rcol + (1 - h) * CAP, rval + (1 - h) * CAP, nOther,
-        h ? sh.su : sh.id, W, rk, ecs + h * 2 * CAP, eys + h * 2 * CAP, rcol + h * CAP, rval + h * CAP,
-        g_ent + (r0 + h) * CAP, g, h);
+    // next stage's clip thresholds of the row this half builds: as its own
+    // merge's A (C: i, S: s) and as the other merge's B (C: s + u, S: i + d)
+    const int t1 = W - (h ? sh_next.s : sh_next.i), t2 = W - (h ? sh_next.id : sh_next.su);
+    int c1, c2;
+    const int n2 = steps_merge_half<MODE, CAP, V>(rows + h * CAP, na, h ? sh.s : sh.i, rows + (1 - h) * CAP, nb,
+                                                  h ? sh.su : sh.id, rk, evs + h * 2 * CAP, rows + h * CAP,
+                                                  g_ent + (r0 + h) * CAP, g, h, t1, t2, c1, c2);
     const int n2o = __shfl_xor_sync(kFull, n2, 16);
     if (n2 < 0 || n2o < 0) {
       over = true;
       break;
     }
     nMine = n2;
-    nOther = n2o;
-    stored += (unsigned long long)n2;  // this half's row (lane 0 reports half 0's; summed below)
+    na = c1;
+    nb = __shfl_xor_sync(kFull, c2, 16);
+    stored += (unsigned long long)n2;  // this half's row (summed over both halves below)
     if (g == 0) g_cnt[r0 + h] = n2;
+    sh = sh_next;
+    bits = bits_next;
     __syncwarp(kFull);
   }
   stored += __shfl_xor_sync(kFull, stored, 16) - 1;  // both rows of every stage (+ the origin row)
-  const int nC = h == 0 ? nMine : nOther, nS = h == 0 ? nOther : nMine;
+  const int nC = h == 0 ? nMine : __shfl_xor_sync(kFull, nMine, 16);
+  const int nS = h == 1 ? nMine : __shfl_xor_sync(kFull, nMine, 16);
   if (a.overflow && lane == 0) a.overflow[inst] = over ? 1 : 0;
   if (over) return;
   // value at column W: the last breakpoint (every stored column is <= W)
   const V NEG = VT<MODE>::neg();
-  const double end_c = to_f64(nC > 0 ? rval[nC - 1] : NEG, inf.scale);
-  const double end_s = to_f64(nS > 0 ? rval[CAP + nS - 1] : NEG, inf.scale);
+  const double end_c = to_f64(nC > 0 ? rows[nC - 1].v : NEG, inf.scale);
+  const double end_s = to_f64(nS > 0 ? rows[CAP + nS - 1].v : NEG, inf.scale);
   if (lane == 0) {
     a.info[inst].end_c = end_c;
     a.info[inst].end_s = end_s;
