@@ -108,8 +108,9 @@ int sp_effective_budget(const sp_instances* in, int64_t* w_eff, void* stream);
  * kernel over the integer budget axis, end-side argmax and back-pointer walk.
  * Replaces planner.py:182-202 `plan_dp` (with :128-143 `build_dp_tables`,
  * :146-179 `_backtrace`, :88-107 `_finish`/`_infeasible`).
- * `ws` is scratch of `ws_bytes` bytes (device); instances are processed in
- * waves that fit it.  SP_ERR_WORKSPACE if a single instance does not fit.
+ * `ws` is scratch of `ws_bytes` bytes (device, 256-byte aligned as cudaMalloc
+ * returns it; SP_ERR_INVALID otherwise); instances are processed in waves that
+ * fit it.  SP_ERR_WORKSPACE if a single instance does not fit.
  * Synchronises `stream` once (to size the waves) before returning. */
 int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes,
                void* stream);

@@ -57,15 +57,17 @@
 // and CAP int2 {column, stay_from}, at a position the kernel computes itself
 // -- (layer_off[k] + k) * steps_row_pair_bytes(CAP) -- in the device-planned
 // tier (no host planning), or at DpWork::bp_off in the wave path:
-//   cnt int32[(L+1) * 2] (16-B aligned) | ent int2[(L+1) * 2][CAP]
+//   cnt int32[(L+1) * 2] (padded to 16 B) | ent int2[(L+1) * 2][CAP]
 #pragma once
 
 constexpr int kStepsCap = 192;       // tier 1: every instance, device-planned, a warp each
 constexpr int kStepsCapWide = 1024;  // tier 2: instances tier 1 could not hold
 constexpr int32_t kNoStay = INT32_MAX;
 
-__host__ __device__ inline size_t steps_row_pair_bytes(int cap) { return 2 * (4 + (size_t)cap * 8); }
-__host__ __device__ inline size_t steps_cnt_bytes(int L) { return (size_t)(L + 1) * 8; }  // keeps int2 8-B aligned
+// sizes keep every store, and every row in it, 16-B aligned (the walk copies
+// breakpoint pairs with 16-B cp.async; CAP is even)
+__host__ __device__ inline size_t steps_row_pair_bytes(int cap) { return 16 + (size_t)cap * 16; }
+__host__ __device__ inline size_t steps_cnt_bytes(int L) { return ((size_t)(L + 1) * 8 + 15) & ~(size_t)15; }
 __host__ __device__ inline size_t steps_store_bytes(int L, int cap) {
   return steps_cnt_bytes(L) + (size_t)(L + 1) * 2 * cap * 8;
 }
@@ -320,7 +322,7 @@ __device__ __forceinline__ void finish_policy_warp(const sp_instances& in, int64
 constexpr int kStepsArrays = 6;
 // the walk's ring: stages fetched ahead, and the bytes of one stage (stage
 // record 16 | row counts 8 | pad 8 | 64 breakpoints of C | 64 of S)
-constexpr int kWalkDepth = 6;
+constexpr int kWalkDepth = 8;
 constexpr size_t kWalkSlot = 32 + 2 * 64 * 8;
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -465,12 +467,10 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
   // one stage of the store into ring slot k % kWalkDepth (one commit group)
   auto fetch = [&](int k) {
     if (k >= 1) {
-      unsigned char* sl = rbase + (size_t)(k % kWalkDepth) * kWalkSlot;
-      const int2* er = g_ent + (size_t)(2 * k) * CAP;
-      cp_async8(sl + 32 + lane * 8, er + lane);
-      cp_async8(sl + 32 + (lane + 32) * 8, er + lane + 32);
-      cp_async8(sl + 32 + 512 + lane * 8, er + CAP + lane);
-      cp_async8(sl + 32 + 512 + (lane + 32) * 8, er + CAP + lane + 32);
+      unsigned char* sl = rbase + (size_t)(k & (kWalkDepth - 1)) * kWalkSlot;
+      const int2* er = g_ent + (size_t)(2 * k) * CAP;  // 16-B aligned: CAP is even
+      cp_async16(sl + 32 + lane * 16, er + 2 * lane);
+      cp_async16(sl + 32 + 512 + lane * 16, er + CAP + 2 * lane);
       if (lane == 0) cp_async16(sl, a.shifts + lo + k - 1);
       if (lane == 1) cp_async8(sl + 16, g_cnt + 2 * k);
     }
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
   };
   // the breakpoints of row `ent` (n of them) at or left of j, and the
   // stay_from of the last of them, with plain loads (32-ary search)
-  auto search = [&](const int2* ent, int n, int64_t j, int& c, int32_t& sf) {
+  auto search = [&](const int2* ent, int n, int j, int& c, int32_t& sf) {
     int lo_i = 0, hi_i = n;  // the count lies in [lo_i, hi_i]
     while (lo_i < hi_i) {
       const int span = hi_i - lo_i;
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
     for (int k = lane; k < L; k += 32) pis[k] = 0;
   } else {
     bool client = ec >= es;
-    int64_t j = inf.w_eff;
+    int j = (int)inf.w_eff;
     if (ring)
       for (int d = 0; d < kWalkDepth; ++d) fetch(L - d);
     for (int k = L; k >= 1; --k) {
@@ -509,15 +509,14 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
       if (ring) {
         cp_async_wait<kWalkDepth - 1>();
         __syncwarp(kFull);
-        const unsigned char* sl = rbase + (size_t)(k % kWalkDepth) * kWalkSlot;
+        const unsigned char* sl = rbase + (size_t)(k & (kWalkDepth - 1)) * kWalkSlot;
         sh = *reinterpret_cast<const StageShift*>(sl);
         n = reinterpret_cast<const int32_t*>(sl + 16)[client ? 0 : 1];
-        if (n <= 64) {
-          const int2* e = reinterpret_cast<const int2*>(sl + 32 + (client ? 0 : 512));
-          const int2 e0 = e[lane], e1 = e[lane + 32];
-          c = __popc(__ballot_sync(kFull, lane < n && e0.x <= j)) +
-              __popc(__ballot_sync(kFull, lane + 32 < n && e1.x <= j));
-          sf = __shfl_sync(kFull, c > 32 ? e1.y : e0.y, (c - 1) & 31);
+        if (n <= 64) {  // lane l holds breakpoints 2l and 2l + 1
+          const int4 e = reinterpret_cast<const int4*>(sl + 32 + (client ? 0 : 512))[lane];
+          c = __popc(__ballot_sync(kFull, 2 * lane < n && e.x <= j)) +
+              __popc(__ballot_sync(kFull, 2 * lane + 1 < n && e.z <= j));
+          sf = __shfl_sync(kFull, ((c - 1) & 1) ? e.w : e.y, ((c - 1) >> 1) & 31);
         } else {
           search(g_ent + rr, n, j, c, sf);
         }

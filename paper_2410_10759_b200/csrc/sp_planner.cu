@@ -1365,6 +1365,10 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   if (n == 0) return SP_OK;
   const Trace trace;
   trace("run_dp begin", n);
+  if (ws && ((uintptr_t)ws & 255)) {
+    set_error(SP_ERR_INVALID, "workspace must be 256-byte aligned (cudaMalloc alignment)");
+    return SP_ERR_INVALID;
+  }
   Carve cv{(uint8_t*)ws, ws_bytes};
   InstInfo* info = (InstInfo*)cv.take(sizeof(InstInfo) * n);
   StageShift* shifts = (StageShift*)cv.take(sizeof(StageShift) * total);
