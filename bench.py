@@ -504,10 +504,7 @@ def main():
         r = host_req.to(dev, non_blocking=True)
         s = engine.solve(r, total_layers, off)
         pol = gather_policies(s.policies, s.layer_off)[0] if world > 1 else s.policies
-        out = (pol.pi.to("cpu", non_blocking=True), pol.client_value.to("cpu", non_blocking=True),
-               pol.server_load.to("cpu", non_blocking=True), pol.integer_latency.to("cpu", non_blocking=True),
-               pol.feasible.to("cpu", non_blocking=True))
-        return s, out
+        return s, pol.to_host_async()  # one packed device-to-host copy of the placements and records
 
     for _ in range(max(args.warmup, 3)):
         step_device()
@@ -563,7 +560,7 @@ def main():
         print("e2e step wall ms:", [round((b - a) * 1e3, 3) for a, b in zip(tw, tw[1:])], file=sys.stderr)
     barrier()
     e2e_ms = e0.elapsed_time(e1)
-    d2h = sum(t.numel() * t.element_size() for t in out)
+    d2h = out._buf.numel()
     del s
 
     t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=dev)
@@ -612,7 +609,7 @@ def main():
             "e2e": {"value": total_cells / (e2e_ms / args.steps / 1e3), "unit": "DP cells/s",
                     "scenarios_per_s": n * world / (e2e_ms / args.steps / 1e3),
                     "ms_per_step": e2e_ms / args.steps,
-                    "h2d_bytes_per_step": host_req.host_bytes(), "d2h_bytes_per_step": d2h},
+                    "h2d_bytes_per_step": host_req._buf.numel(), "d2h_bytes_per_step": d2h},
             "gpu_launches": int(prof.launches),
             "roofline": roofline(prof, prof_ms),
             "clocks": clk,

@@ -216,6 +216,29 @@ def to_dev(a, dtype, dev=None) -> torch.Tensor:
     return t.to(dev, non_blocking=False)
 
 
+def packed(specs, device=None, pin: bool = False, zero_prefix: int = 0):
+    """One allocation holding several typed arrays: `specs` is a list of
+    (name, numel, torch dtype); each array starts 256-B aligned.  Returns
+    (buffer, {name: view}).  The first `zero_prefix` arrays are zeroed with
+    one fill.  One copy per direction moves the whole set (the arrays stay
+    independent tensors for every consumer)."""
+    offs, o = [], 0
+    for _name, numel, dt in specs:
+        o = (o + 255) & ~255
+        offs.append(o)
+        o += int(numel) * dt.itemsize
+    if device is None or (isinstance(device, str) and device == "cpu"):
+        buf = torch.empty(max(o, 1), dtype=torch.uint8, pin_memory=pin)
+    else:
+        buf = torch.empty(max(o, 1), dtype=torch.uint8, device=device)
+    views = {name: buf[off:off + int(numel) * dt.itemsize].view(dt)
+             for (name, numel, dt), off in zip(specs, offs)}
+    if zero_prefix:
+        _name, numel, dt = specs[zero_prefix - 1]
+        buf[:offs[zero_prefix - 1] + int(numel) * dt.itemsize].zero_()
+    return buf, views
+
+
 _ws: dict[int, torch.Tensor] = {}
 _total_mem: dict[int, int] = {}
 _WS_MIN = 64 << 20

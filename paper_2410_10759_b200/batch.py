@@ -78,6 +78,12 @@ class InstanceBatch:
                                must)
 
 
+def _POLICY_LAYOUT(n: int, total: int):
+    # pi and status first: the two arrays zeroed up front
+    return [("pi", total, torch.uint8), ("status", n, torch.int32), ("client_value", n, torch.float64),
+            ("server_load", n, torch.float64), ("integer_latency", n, torch.int64), ("feasible", n, torch.uint8)]
+
+
 @dataclass
 class PolicyBatch:
     pi: torch.Tensor               # uint8 [T]
@@ -89,13 +95,34 @@ class PolicyBatch:
 
     @classmethod
     def empty(cls, n: int, total: int, dev=None) -> "PolicyBatch":
+        """One device allocation; pi and status zeroed (one fill)."""
         dev = dev or N.device()
-        return cls(torch.zeros(total, dtype=torch.uint8, device=dev),
-                   torch.empty(n, dtype=torch.float64, device=dev),
-                   torch.empty(n, dtype=torch.float64, device=dev),
-                   torch.empty(n, dtype=torch.int64, device=dev),
-                   torch.empty(n, dtype=torch.uint8, device=dev),
-                   torch.zeros(n, dtype=torch.int32, device=dev))
+        buf, v = N.packed(_POLICY_LAYOUT(n, total), dev, zero_prefix=2)
+        out = cls(v["pi"], v["client_value"], v["server_load"], v["integer_latency"], v["feasible"],
+                  v["status"])
+        out._buf = buf
+        return out
+
+    def to_host_async(self) -> "PolicyBatch":
+        """The results in pinned host memory: ONE device-to-host copy when the
+        batch owns a packed buffer (PolicyBatch.empty), stream-ordered; read
+        them after the stream (or the copy) has completed."""
+        buf = getattr(self, "_buf", None)
+        n, total = self.client_value.numel(), self.pi.numel()
+        hbuf, v = N.packed(_POLICY_LAYOUT(n, total), "cpu", pin=True)
+        if buf is not None and buf.numel() == hbuf.numel():
+            hbuf.copy_(buf, non_blocking=True)
+        else:
+            for k in v:
+                v[k].copy_(getattr(self, k), non_blocking=True)
+        out = PolicyBatch(v["pi"], v["client_value"], v["server_load"], v["integer_latency"], v["feasible"],
+                          v["status"])
+        out._buf = hbuf
+        return out
+
+    def nbytes(self) -> int:
+        return sum(getattr(self, k).numel() * getattr(self, k).element_size()
+                   for k in ("pi", "client_value", "server_load", "integer_latency", "feasible", "status"))
 
     def struct(self) -> N.SpPolicies:
         return N.SpPolicies(N.ptr(self.pi).value, N.ptr(self.client_value).value,

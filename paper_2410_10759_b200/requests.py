@@ -22,6 +22,11 @@ from .cost_model import encode_models
 _REQ_FIELDS = ("model", "seq_len", "client_fps", "server_fps", "uplink_bps", "downlink_bps",
                "propagation_s", "deadline_s", "unit_s", "flags")
 _REQ_DTYPES = dict(model=np.int32, seq_len=np.int64, flags=np.uint8)
+_REQ_TORCH = {np.int32: torch.int32, np.int64: torch.int64, np.uint8: torch.uint8, np.float64: torch.float64}
+
+
+def _req_layout(n: int):
+    return [(f, n, _REQ_TORCH[_REQ_DTYPES.get(f, np.float64)]) for f in _REQ_FIELDS]
 
 
 @dataclass
@@ -45,16 +50,26 @@ class RequestBatch:
 
     @classmethod
     def from_numpy(cls, pin: bool = False, **arrays) -> "RequestBatch":
-        ts = {}
+        """Host batch; every field in ONE (optionally pinned) buffer, so that
+        `to(device)` is a single host-to-device copy."""
+        n = len(arrays["model"])
+        buf, v = N.packed(_req_layout(n), "cpu", pin=pin)
         for f in _REQ_FIELDS:
-            a = np.ascontiguousarray(arrays[f], dtype=_REQ_DTYPES.get(f, np.float64))
-            t = torch.from_numpy(a)
-            ts[f] = t.pin_memory() if pin else t
-        return cls(**ts)
+            v[f].copy_(torch.from_numpy(np.ascontiguousarray(arrays[f], dtype=_REQ_DTYPES.get(f, np.float64))))
+        out = cls(**v)
+        out._buf = buf
+        return out
 
     def to(self, device, non_blocking: bool = False) -> "RequestBatch":
-        return RequestBatch(**{f: getattr(self, f).to(device, non_blocking=non_blocking)
-                               for f in _REQ_FIELDS})
+        buf = getattr(self, "_buf", None)
+        if buf is None:
+            return RequestBatch(**{f: getattr(self, f).to(device, non_blocking=non_blocking)
+                                   for f in _REQ_FIELDS})
+        dbuf, v = N.packed(_req_layout(self.n), device)
+        dbuf.copy_(buf, non_blocking=non_blocking)
+        out = RequestBatch(**v)
+        out._buf = dbuf
+        return out
 
     def host_bytes(self) -> int:
         return sum(getattr(self, f).numel() * getattr(self, f).element_size() for f in _REQ_FIELDS)
@@ -121,5 +136,5 @@ class Engine:
         # a request whose cost table failed (NaN / inf / negative / overflowing
         # times: the reference raises and records an error cell) is never a
         # feasible placement; its status word says why
-        pol.feasible.mul_((status == 0).to(torch.uint8))
+        torch.mul(pol.feasible, status == 0, out=pol.feasible)
         return Solved(inst.layer_off, inst, pol, status, f["cs"], f["ss"], f["up"], f["dn"])

@@ -40,10 +40,7 @@ def main():
     def step_e2e():
         r = host_req.to(dev, non_blocking=True)
         s = eng.solve(r, total, off)
-        pol = s.policies
-        return (pol.pi.to("cpu", non_blocking=True), pol.client_value.to("cpu", non_blocking=True),
-                pol.server_load.to("cpu", non_blocking=True), pol.integer_latency.to("cpu", non_blocking=True),
-                pol.feasible.to("cpu", non_blocking=True))
+        return s.policies.to_host_async()
 
     for _ in range(5):
         step_e2e()
