@@ -30,9 +30,11 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 3  /* 2: + sp_plan_dp_devices, sp_plan_dp_workspace_bytes;
+#define SP_ABI_VERSION 4  /* 2: + sp_plan_dp_devices, sp_plan_dp_workspace_bytes;
                              3: per-partition workspaces, sp_grid_* (one process per
-                                device), sp_ipc_*, sp_last_full_workspace */
+                                device), sp_ipc_*, sp_last_full_workspace;
+                             4: sp_plan_dp_async / sp_plan_dp_finish; 256-B aligned
+                                workspaces */
 
 enum sp_status {
   SP_OK = 0,
@@ -114,6 +116,24 @@ int sp_effective_budget(const sp_instances* in, int64_t* w_eff, void* stream);
  * Synchronises `stream` once (to size the waves) before returning. */
 int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes,
                void* stream);
+
+/* sp_plan_dp in two halves, so that a caller can queue the next batch while
+ * this one runs (no stream synchronisation in the first half).
+ * sp_plan_dp_async enqueues the device-planned tier (prep, breakpoint lists,
+ * walk back, _finish) on `stream` and returns; `pending` is caller-owned
+ * PINNED host memory of SP_PENDING_BYTES bytes (8-B aligned) that receives
+ * the tier's counters.  When the tier cannot take the batch (workspace,
+ * widths) the call runs to completion like sp_plan_dp.  sp_plan_dp_finish
+ * waits for the counters (not for the whole stream) and runs the
+ * host-planned tiers for the instances left; `in`, `out`, `ws` and
+ * `ws_bytes` must be those of the async call, and `ws` untouched in between.
+ * The policies are final once sp_plan_dp_finish returned SP_OK and the
+ * stream has reached that point. */
+#define SP_PENDING_BYTES 64
+int sp_plan_dp_async(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes, void* stream,
+                     void* pending);
+int sp_plan_dp_finish(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes, void* stream,
+                      void* pending);
 
 /* Workspace sizes for sp_plan_dp on these instances (the `*_workspace_bytes`
  * query of SURVEY.md 8b): min_bytes runs every instance (in waves; whole-GPU

@@ -92,6 +92,8 @@ class SpSimOut(C.Structure):
                 ("mean_wait_ms", P), ("status", P), ("deadlock_req", P)]
 
 
+SP_PENDING_BYTES = 64  # include/splitplan_b200.h
+
 # name -> (restype, argtypes); the full list the header declares
 SIGNATURES = {
     "sp_abi_version": (C.c_int, []),
@@ -105,6 +107,8 @@ SIGNATURES = {
                                      C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "sp_effective_budget": (C.c_int, [C.POINTER(SpInstances), P, P]),
     "sp_plan_dp": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_size_t, P]),
+    "sp_plan_dp_async": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_size_t, P, P]),
+    "sp_plan_dp_finish": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_size_t, P, P]),
     "sp_plan_dp_devices": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_int32, P,
                                      C.c_size_t, P, P, P]),
     "sp_plan_dp_devices_workspace_bytes": (C.c_int, [C.POINTER(SpInstances), P, C.c_int32,

@@ -103,13 +103,21 @@ class PolicyBatch:
         out._buf = buf
         return out
 
-    def to_host_async(self) -> "PolicyBatch":
+    def to_host_async(self, into: "PolicyBatch | None" = None) -> "PolicyBatch":
         """The results in pinned host memory: ONE device-to-host copy when the
         batch owns a packed buffer (PolicyBatch.empty), stream-ordered; read
-        them after the stream (or the copy) has completed."""
+        them after the stream (or the copy) has completed.  `into`: a host
+        batch of the same shape from an earlier call, reused (a caller
+        streaming many batches keeps a few and avoids pinned allocations)."""
         buf = getattr(self, "_buf", None)
         n, total = self.client_value.numel(), self.pi.numel()
-        hbuf, v = N.packed(_POLICY_LAYOUT(n, total), "cpu", pin=True)
+        if into is not None and getattr(into, "_buf", None) is not None and into.pi.numel() == total \
+                and into.client_value.numel() == n:
+            hbuf = into._buf
+            v = {k: getattr(into, k) for k in ("pi", "client_value", "server_load", "integer_latency",
+                                               "feasible", "status")}
+        else:
+            hbuf, v = N.packed(_POLICY_LAYOUT(n, total), "cpu", pin=True)
         if buf is not None and buf.numel() == hbuf.numel():
             hbuf.copy_(buf, non_blocking=True)
         else:
@@ -181,6 +189,44 @@ def plan_dp(batch: InstanceBatch, out: PolicyBatch | None = None, devices=None) 
     N.check(rc, "sp_plan_dp")
     N.grow_workspace_hint(int(lib.sp_last_full_workspace()))
     return out
+
+
+class PendingPlan:
+    """An sp_plan_dp_async call in flight: `finish()` waits for its
+    device-planned tier (not for the whole stream), runs the host-planned
+    tiers for what it left and returns the policies.  The workspace must not
+    be reused before finish()."""
+
+    def __init__(self, batch, out, ws, pend, s, o, done: bool):
+        self.batch, self.out, self.ws, self.pend, self.s, self.o = batch, out, ws, pend, s, o
+        self.done = done
+
+    def finish(self) -> PolicyBatch:
+        if not self.done:
+            rc = N.library().sp_plan_dp_finish(self.s, self.o, N.ptr(self.ws), self.ws.numel(), N.stream_ptr(),
+                                               N.ptr(self.pend))
+            self.done = True
+            N.check(rc, "sp_plan_dp_finish")
+        return self.out
+
+
+def plan_dp_async(batch: InstanceBatch, out: PolicyBatch | None = None,
+                  ws: torch.Tensor | None = None) -> PendingPlan:
+    """plan_dp without a stream synchronisation: the batch's device-planned
+    tier is queued and the call returns (sp_plan_dp_async); PendingPlan.finish()
+    completes it.  `ws`: this call's workspace (distinct per call in flight),
+    else the shared cached one.  Falls back to plan_dp when the tier cannot
+    take the batch in `ws`."""
+    out = out or PolicyBatch.empty(batch.n, batch.total_layers, batch.r.device)
+    ws = N.workspace() if ws is None else ws
+    pend = torch.empty(N.SP_PENDING_BYTES, dtype=torch.uint8, pin_memory=True)
+    s, o = batch.struct(), out.struct()
+    rc = N.library().sp_plan_dp_async(s, o, N.ptr(ws), ws.numel(), N.stream_ptr(), N.ptr(pend))
+    if rc == N.SP_ERR_WORKSPACE:
+        plan_dp(batch, out)
+        return PendingPlan(batch, out, ws, pend, s, o, True)
+    N.check(rc, "sp_plan_dp_async")
+    return PendingPlan(batch, out, ws, pend, s, o, False)
 
 
 def partition_workspaces(batch: InstanceBatch, devices) -> list[torch.Tensor]:

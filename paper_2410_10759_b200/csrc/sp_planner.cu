@@ -1357,10 +1357,23 @@ void grid_workspace_bytes(int mode, int64_t L, int64_t ncol, int nparts, int per
 // q_part_full those of each partition workspace when `dp` is set).
 // `w_eff_check` >= 0: build_dp_tables' caller-sized tables, checked against
 // the instance's W_eff before anything is written.
+// Pending state of sp_plan_dp_async / sp_plan_dp_finish, in the caller's
+// pinned host buffer of SP_PENDING_BYTES bytes.
+struct PendingRec {
+  unsigned long long solved[4];  // tier 1's counters, copied there by the stream
+  cudaEvent_t ev;                // recorded after that copy
+  int32_t mode;                  // 0: nothing pending (the call ran to completion), 1: tier 1 in flight
+  int32_t pad;
+};
+static_assert(sizeof(PendingRec) <= SP_PENDING_BYTES, "pending record");
+
+// `begin`: enqueue tier 1 and return (its counters land in begin->solved);
+// `resume`: the second half of such a call -- nothing is launched again, the
+// counters are waited for and the host-planned tiers run for what is left.
 int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_s, void* ws,
            size_t ws_bytes, cudaStream_t st, size_t* q_min = nullptr, size_t* q_full = nullptr,
            const DevPlan* dp = nullptr, size_t* q_part_min = nullptr, size_t* q_part_full = nullptr,
-           int64_t w_eff_check = -1) {
+           int64_t w_eff_check = -1, PendingRec* begin = nullptr, PendingRec* resume = nullptr) {
   const int64_t n = in->n, total = in->total_layers;
   if (n == 0) return SP_OK;
   const Trace trace;
@@ -1393,10 +1406,13 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   const int grid = (int)std::min<int64_t>((n + kPrepWarps - 1) / kPrepWarps, 1 << 20);
   const bool tier1_fits = steps_ok && out && fixed + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap) <= ws_bytes;
   const int64_t lo_i32 = steps_min_cols(VM_INT32, force), lo_f64 = steps_min_cols(VM_F64, force);
-  prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv, reach, steps_ok ? flag : nullptr,
-                                    tier1_fits ? kGridMinColsSteps : 0, lo_i32, lo_f64);
-  int rc = launch_check("prep_kernel launch");
-  if (rc) return rc;
+  int rc = SP_OK;
+  if (!resume) {
+    prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv, reach, steps_ok ? flag : nullptr,
+                                      tier1_fits ? kGridMinColsSteps : 0, lo_i32, lo_f64);
+    rc = launch_check("prep_kernel launch");
+    if (rc) return rc;
+  }
   uint8_t* dyn = (uint8_t*)ws + fixed;
 
   // Tier 1, planned on the device: one warp per instance on breakpoint lists
@@ -1420,22 +1436,39 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     sa.max_cols = kGridMinColsSteps;
     sa.min_cols[0] = lo_i32;
     sa.min_cols[1] = lo_f64;
-    rc = check_cuda(cudaMemsetAsync(solved, 0, 4 * sizeof(unsigned long long), st), "zero solved count");
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (!rc && profiling()) {
-      cudaEventCreate(&e0);
-      cudaEventCreate(&e1);
-      cudaEventRecord(e0, st);
-    }
-    if (!rc) rc = launch_steps(VM_INT32, kStepsCap, sa, in, out, idx, st);
-    if (!rc) rc = launch_steps(VM_F64, kStepsCap, sa, in, out, idx, st);
-    if (!rc && profiling()) cudaEventRecord(e1, st);
     unsigned long long hsolved[4] = {0, 0, 0, 0};  // instances, DP cells, breakpoints, stages
-    if (!rc)
-      rc = check_cuda(cudaMemcpyAsync(hsolved, solved, sizeof(hsolved), cudaMemcpyDeviceToHost, st),
-                      "copy solved count");
-    if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync after breakpoint lists");
-    if (rc) return rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (resume) {
+      rc = check_cuda(cudaEventSynchronize(resume->ev), "wait for tier 1");
+      cudaEventDestroy(resume->ev);
+      resume->ev = nullptr;
+      resume->mode = 0;
+      if (rc) return rc;
+      memcpy(hsolved, resume->solved, sizeof(hsolved));
+    } else {
+      rc = check_cuda(cudaMemsetAsync(solved, 0, 4 * sizeof(unsigned long long), st), "zero solved count");
+      if (!rc && profiling() && !begin) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+      }
+      if (!rc) rc = launch_steps(VM_INT32, kStepsCap, sa, in, out, idx, st);
+      if (!rc) rc = launch_steps(VM_F64, kStepsCap, sa, in, out, idx, st);
+      if (!rc && e1) cudaEventRecord(e1, st);
+      if (!rc && begin) {  // asynchronous: the counters travel to the caller's pinned buffer
+        rc = check_cuda(cudaMemcpyAsync(begin->solved, solved, sizeof(hsolved), cudaMemcpyDeviceToHost, st),
+                        "copy solved count");
+        if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&begin->ev, cudaEventDisableTiming), "event");
+        if (!rc) rc = check_cuda(cudaEventRecord(begin->ev, st), "record tier 1");
+        if (!rc) begin->mode = 1;
+        return rc;
+      }
+      if (!rc)
+        rc = check_cuda(cudaMemcpyAsync(hsolved, solved, sizeof(hsolved), cudaMemcpyDeviceToHost, st),
+                        "copy solved count");
+      if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync after breakpoint lists");
+      if (rc) return rc;
+    }
     // algorithmic HBM bytes of the breakpoint-list kernel: the stage records it
     // reads (16 B shifts + 8 B value per stage) and the store it writes (an
     // 8-B {column, stay_from} per breakpoint, a 4-B count per row)
@@ -1783,6 +1816,42 @@ int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_byt
   rc = validate_out(out);
   if (rc) return rc;
   return run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int sp_plan_dp_async(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes, void* stream,
+                     void* pending) {
+  int rc = validate(in);
+  if (rc) return rc;
+  rc = validate_out(out);
+  if (rc) return rc;
+  if (!pending || ((uintptr_t)pending & 7)) {
+    set_error(SP_ERR_INVALID, "sp_plan_dp_async: pending must be an 8-B aligned pinned host buffer");
+    return SP_ERR_INVALID;
+  }
+  PendingRec* p = (PendingRec*)pending;
+  memset(p, 0, sizeof(PendingRec));
+  // runs to completion (mode stays 0) unless tier 1 took the batch
+  return run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr, nullptr, nullptr,
+                nullptr, -1, p, nullptr);
+}
+
+int sp_plan_dp_finish(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes, void* stream,
+                      void* pending) {
+  if (!pending) {
+    set_error(SP_ERR_INVALID, "sp_plan_dp_finish: null pending");
+    return SP_ERR_INVALID;
+  }
+  PendingRec* p = (PendingRec*)pending;
+  if (p->mode != 1) return SP_OK;  // the async call completed the batch itself
+  int rc = validate(in);
+  if (!rc) rc = validate_out(out);
+  if (rc) {
+    cudaEventDestroy(p->ev);
+    p->mode = 0;
+    return rc;
+  }
+  return run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr, nullptr, nullptr,
+                nullptr, -1, nullptr, p);
 }
 
 int sp_plan_dp_workspace_bytes(const sp_instances* in, size_t* min_bytes, size_t* full_bytes, void* ws,

@@ -126,6 +126,17 @@ class Engine:
         inst = B.InstanceBatch(off, i["i"], i["s"], i["u"], i["d"], f["r"], budget, sac)
         return inst, status, f
 
+    def solve_async(self, req: RequestBatch, total_layers: int | None = None, off: torch.Tensor | None = None,
+                    ws: torch.Tensor | None = None) -> "PendingSolve":
+        """`solve` without a stream synchronisation (sp_plan_dp_async): the
+        whole chain is queued and the call returns; PendingSolve.result()
+        completes it.  A caller pipelines batches by queueing the next one
+        before collecting this one, each in flight with its own workspace."""
+        if total_layers is None:
+            total_layers = int(self.n_layers[req.model.cpu().numpy()].sum())
+        inst, status, f = self.cost_table(req, total_layers, off)
+        return PendingSolve(B.plan_dp_async(inst, ws=ws), inst, status, f)
+
     def solve(self, req: RequestBatch, total_layers: int | None = None,
               off: torch.Tensor | None = None) -> Solved:
         """K1 cost table + DP placement for every request (one stream)."""
@@ -138,3 +149,16 @@ class Engine:
         # feasible placement; its status word says why
         torch.mul(pol.feasible, status == 0, out=pol.feasible)
         return Solved(inst.layer_off, inst, pol, status, f["cs"], f["ss"], f["up"], f["dn"])
+
+
+class PendingSolve:
+    """An Engine.solve_async call in flight."""
+
+    def __init__(self, pending: B.PendingPlan, inst: B.InstanceBatch, status: torch.Tensor, f: dict):
+        self.pending, self.inst, self.status, self.f = pending, inst, status, f
+
+    def result(self) -> Solved:
+        pol = self.pending.finish()
+        torch.mul(pol.feasible, self.status == 0, out=pol.feasible)
+        f = self.f
+        return Solved(self.inst.layer_off, self.inst, pol, self.status, f["cs"], f["ss"], f["up"], f["dn"])

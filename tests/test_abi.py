@@ -39,7 +39,7 @@ def test_library_exports_every_declared_symbol():
 def test_library_is_sm100a_and_abi_version():
     from paper_2410_10759_b200 import _native
     from paper_2410_10759_b200._build import LIB
-    assert _native.library().sp_abi_version() == 3
+    assert _native.library().sp_abi_version() == 4
     out = subprocess.run(["cuobjdump", "--list-elf", str(LIB)], capture_output=True, text=True)
     assert "sm_100a" in out.stdout, out.stdout
 

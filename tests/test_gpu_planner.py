@@ -488,3 +488,69 @@ def test_breakpoint_tiers_and_fallback(gpu, ws_kind, monkeypatch):
                    server_load=host["server_load"][k], integer_latency=host["integer_latency"][k],
                    feasible=host["feasible"][k])
         assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{ws_kind}[{k}]")
+
+
+# ---------------------------------------------------------------------------
+# sp_plan_dp_async / sp_plan_dp_finish
+
+
+@pytest.mark.parametrize("name", BATTERIES + ["battery_large_model"])
+def test_plan_dp_async_matches_reference(gpu, name):
+    """The two-half call gives the reference's results on every battery (the
+    batteries mix instances tier 1 solves with ones the host-planned tiers
+    take in finish())."""
+    from paper_2410_10759_b200 import batch as B
+    bat = Battery(name)
+    pend = B.plan_dp_async(_batch(bat))
+    _compare(bat, "dp", pend.finish().to_host())
+
+
+def test_plan_dp_async_fallbacks_and_two_in_flight(gpu):
+    """Two batches in flight on one stream with their own workspaces, the
+    second queued before the first is finished; the batches need the wide
+    tier and the dense kernels (run by finish()).  Bit-exact vs the oracle."""
+    import torch
+    from paper_2410_10759_b200 import _native as N, batch as B
+    sets = [_dense_rows_instances(17, 6), _dense_rows_instances(23, 5)]
+    batches, offs = [], []
+    for insts in sets:
+        off = np.zeros(len(insts) + 1, np.int64)
+        np.cumsum([len(x["r"]) for x in insts], out=off[1:])
+        cat = lambda k: np.concatenate([x[k] for x in insts])
+        batches.append(B.InstanceBatch.from_arrays(off, cat("i"), cat("s"), cat("u"), cat("d"), cat("r"),
+                                                   [x["budget"] for x in insts], [x["sac"] for x in insts]))
+        offs.append(off)
+    _mn, full = B.dp_workspace_bytes(batches[0])
+    big = max(full, B.dp_workspace_bytes(batches[1])[1])
+    ws = [torch.empty(big, dtype=torch.uint8, device=N.device()) for _ in range(2)]
+    p0 = B.plan_dp_async(batches[0], ws=ws[0])
+    p1 = B.plan_dp_async(batches[1], ws=ws[1])
+    hosts = [p0.finish().to_host(), p1.finish().to_host()]
+    for insts, off, host in zip(sets, offs, hosts):
+        for k, inst in enumerate(insts):
+            exp = O.plan_dp(inst)
+            got = dict(pi=host["pi"][off[k]:off[k + 1]], client_value=host["client_value"][k],
+                       server_load=host["server_load"][k], integer_latency=host["integer_latency"][k],
+                       feasible=host["feasible"][k])
+            assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"async[{k}]")
+
+
+def test_engine_solve_async_pipelined(gpu):
+    """Engine.solve_async with two batches in flight gives exactly Engine.solve's results."""
+    import torch
+    from paper_2410_10759_b200 import _native as N, cost_model as cm, workloads as W
+    from paper_2410_10759_b200.requests import Engine, RequestBatch
+    eng = Engine([cm.build_preset("gpt2-24", 128).layers])
+    reqs = [RequestBatch.from_numpy(**W.cfg2(300, seed)[0]).to(N.device()) for seed in (5, 6, 7)]
+    ref = [eng.solve(r).policies.to_host() for r in reqs]
+    ws = [torch.empty(512 << 20, dtype=torch.uint8, device=N.device()) for _ in range(2)]
+    prev, got = None, []
+    for k, r in enumerate(reqs + [None]):
+        cur = eng.solve_async(r, ws=ws[k & 1]) if r is not None else None
+        if prev is not None:
+            got.append(prev.result().policies.to_host_async())
+        prev = cur
+    torch.cuda.synchronize()
+    for a, b in zip(ref, got):
+        for key in ("pi", "client_value", "server_load", "integer_latency", "feasible", "status"):
+            np.testing.assert_array_equal(a[key], getattr(b, key).numpy(), err_msg=key)

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--requests", type=int, default=10_000)
     ap.add_argument("--blocks", type=int, default=0, help="N blocks of 20 device / e2e steps, with SM clocks")
     ap.add_argument("--plain", action="store_true", help="no profiler: CUDA-event times of device and e2e steps")
+    ap.add_argument("--pipelined", action="store_true", help="e2e steps as bench.py times them (solve_async)")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile, record_function
@@ -37,10 +38,26 @@ def main():
     off = eng.layer_offsets(dev_req)
     total = args.requests * len(layers)
 
+    from paper_2410_10759_b200 import _native as N
+    state = {"prev": None, "k": 0, "ws": None, "out": [None, None, None]}
+
     def step_e2e():
-        r = host_req.to(dev, non_blocking=True)
-        s = eng.solve(r, total, off)
-        return s.policies.to_host_async()
+        if not args.pipelined:
+            r = host_req.to(dev, non_blocking=True)
+            s = eng.solve(r, total, off)
+            return s.policies.to_host_async()
+        # bench.py's timed loop: queue step k, then collect step k - 1
+        if state["ws"] is None:
+            eng.solve(dev_req, total, off)  # sizes the cached workspace for the batch
+            state["ws"] = [N.workspace(), torch.empty_like(N.workspace())]
+        k = state["k"]
+        cur = eng.solve_async(host_req.to(dev, non_blocking=True), total, off, ws=state["ws"][k & 1])
+        out = None
+        if state["prev"] is not None:
+            s = state["prev"].result()
+            out = state["out"][k % 3] = s.policies.to_host_async(into=state["out"][k % 3])
+        state["prev"], state["k"] = cur, k + 1
+        return out
 
     for _ in range(5):
         step_e2e()
