@@ -49,8 +49,8 @@
 //
 // The same warp then walks the instance back (end-side choice, planner.py:
 // 182-202; _backtrace, planner.py:146-179) through the rows it has just
-// stored -- row counts and the first 32 breakpoints of both candidate rows
-// are fetched one stage ahead -- and computes _finish (planner.py:88-101)
+// stored -- the stage records and the breakpoints of both candidate rows are
+// fetched kWalkDepth stages ahead -- and computes _finish (planner.py:88-101)
 // with the placement and the compacted r values in shared memory.
 //
 // Store of one instance (read by the walk): (L+1) rows x {C, S}, each a count
@@ -321,7 +321,7 @@ __device__ __forceinline__ void finish_policy_warp(const sp_instances& in, int64
 // events [2][2 CAP]
 constexpr int kStepsArrays = 6;
 // the walk's ring: stages fetched ahead, and the bytes of one stage (stage
-// record 16 | row counts 8 | pad 8 | 64 breakpoints of C | 64 of S)
+// record 16 | pad 16 | up to 64 breakpoints of C | up to 64 of S)
 constexpr int kWalkDepth = 8;
 constexpr size_t kWalkSlot = 32 + 2 * 64 * 8;
 
@@ -456,23 +456,31 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
   // rows of a stage -- so the L2 latency of the store stays off the chain of
   // dependent lookups; _finish then reuses the ring for the r values.
   // Instances too long for that walk with plain loads, placement in global.
+  // The row counts of every stage are copied into shared memory first (the
+  // forward pass left them in the store, L2-hot), so each stage's fetch copies
+  // only the breakpoints its rows hold.
+  using CntT = typename std::conditional<(CAP < 256), uint8_t, uint16_t>::type;
   const size_t pi_bytes = ((size_t)L + 15) & ~(size_t)15;
-  const bool ring = pi_bytes + (size_t)kWalkDepth * kWalkSlot <= INST_BYTES;
-  const bool fin_smem = pi_bytes + (size_t)L * 8 <= INST_BYTES;
+  const size_t cnt_bytes = ((size_t)(L + 1) * 2 * sizeof(CntT) + 15) & ~(size_t)15;
+  const bool ring = pi_bytes + cnt_bytes + (size_t)kWalkDepth * kWalkSlot <= INST_BYTES;
+  const bool fin_smem = pi_bytes + cnt_bytes + (size_t)L * 8 <= INST_BYTES;
   uint8_t* pis = ring ? ws : a.out.pi + lo;
-  unsigned char* rbase = ws + pi_bytes;
+  CntT* cnts = reinterpret_cast<CntT*>(ws + pi_bytes);
+  unsigned char* rbase = ws + pi_bytes + cnt_bytes;
   const bool infeasible = pmax == -INFINITY;
   int32_t status = SP_OK;
   __syncwarp(kFull);  // every lane is done with the rows and the scratch
   // one stage of the store into ring slot k % kWalkDepth (one commit group)
+  // (only breakpoint pairs holding a breakpoint; a row of more than 64 is
+  // searched in the store instead)
   auto fetch = [&](int k) {
     if (k >= 1) {
       unsigned char* sl = rbase + (size_t)(k & (kWalkDepth - 1)) * kWalkSlot;
       const int2* er = g_ent + (size_t)(2 * k) * CAP;  // 16-B aligned: CAP is even
-      cp_async16(sl + 32 + lane * 16, er + 2 * lane);
-      cp_async16(sl + 32 + 512 + lane * 16, er + CAP + 2 * lane);
+      const int fc = cnts[2 * k], fs = cnts[2 * k + 1];
+      if (fc <= 64 && 2 * lane < fc) cp_async16(sl + 32 + lane * 16, er + 2 * lane);
+      if (fs <= 64 && 2 * lane < fs) cp_async16(sl + 32 + 512 + lane * 16, er + CAP + 2 * lane);
       if (lane == 0) cp_async16(sl, a.shifts + lo + k - 1);
-      if (lane == 1) cp_async8(sl + 16, g_cnt + 2 * k);
     }
     cp_async_commit();
   };
@@ -499,8 +507,11 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
   } else {
     bool client = ec >= es;
     int j = (int)inf.w_eff;
-    if (ring)
+    if (ring) {
+      for (int k = lane; k < 2 * (L + 1); k += 32) cnts[k] = (CntT)g_cnt[k];
+      __syncwarp(kFull);
       for (int d = 0; d < kWalkDepth; ++d) fetch(L - d);
+    }
     for (int k = L; k >= 1; --k) {
       const size_t rr = (size_t)(2 * k + (client ? 0 : 1)) * CAP;
       StageShift sh;
@@ -511,7 +522,7 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
         __syncwarp(kFull);
         const unsigned char* sl = rbase + (size_t)(k & (kWalkDepth - 1)) * kWalkSlot;
         sh = *reinterpret_cast<const StageShift*>(sl);
-        n = reinterpret_cast<const int32_t*>(sl + 16)[client ? 0 : 1];
+        n = cnts[2 * k + (client ? 0 : 1)];
         if (n <= 64) {  // lane l holds breakpoints 2l and 2l + 1
           const int4 e = reinterpret_cast<const int4*>(sl + 32 + (client ? 0 : 512))[lane];
           c = __popc(__ballot_sync(kFull, 2 * lane < n && e.x <= j)) +
