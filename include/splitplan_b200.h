@@ -409,6 +409,23 @@ size_t sp_sim_workspace_bytes(const sp_sim_batch* b);
 int sp_sim_replay(const sp_sim_batch* b, sp_sim_out* out, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* Arrival skeletons, one per seed, drawn by numpy's default_rng(seed) stream
+ * bit for bit (PCG64 seeded through SeedSequence, numpy's ziggurat
+ * exponential, Lemire bounded integers).  Replaces throughput_sim.py:179-186
+ * `_skeleton` for a batch of runs:
+ *   g = default_rng(seeds[r])
+ *   arrival_ms[r, :] = np.cumsum(g.exponential(scale, horizon))
+ *   choice[r, :]     = g.integers(0, choice_hi[r] - choice_lo[r], horizon) + choice_lo[r]
+ *   exec_count[r, :] = g.integers(1, exec_max + 1, horizon)
+ * Outputs are row-major [n, horizon].  seeds[r] >= 0; 1 <= choice_hi[r] -
+ * choice_lo[r] <= 2^32 and the rows < 2^31; 1 <= exec_max < 2^31.  status[r]
+ * (optional): SP_OK, or SP_ERR_INVALID for a run whose range is empty (numpy
+ * raises ValueError there; nothing is written for it). */
+int sp_sim_skeletons(const int64_t* seeds, const int64_t* choice_lo, const int64_t* choice_hi,
+                     int64_t n, int64_t horizon, double scale, int64_t exec_max,
+                     double* arrival_ms, int32_t* choice, int32_t* exec_count, int32_t* status,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -142,6 +142,7 @@ SIGNATURES = {
     "sp_segment_sum": (C.c_int, [P, P, C.c_int64, P, P]),
     "sp_sim_workspace_bytes": (C.c_size_t, [C.POINTER(SpSimBatch)]),
     "sp_sim_replay": (C.c_int, [C.POINTER(SpSimBatch), C.POINTER(SpSimOut), P, C.c_size_t, P]),
+    "sp_sim_skeletons": (C.c_int, [P, P, P, C.c_int64, C.c_int64, C.c_double, C.c_int64, P, P, P, P, P]),
 }
 
 _lib = None

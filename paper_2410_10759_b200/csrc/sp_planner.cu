@@ -781,6 +781,160 @@ DpPlan plan_instance(int mode, int64_t L, int64_t ncol, int force, bool tables, 
   return p;
 }
 
+// ---- tier 0: the SMEM kernel's instances, planned on the device -------------
+//
+// Rows narrow enough for one CTA's shared memory run on dp_stage_kernel<SMEM>
+// (~1e12 cells/s).  A batch of millions of them (configs[3]: 4.2M requests)
+// used to be planned instance by instance on the host; tier 0 plans them on
+// the device instead: t0_count_kernel classifies every instance by launch
+// configuration (value domain x T x E, the default rule of single_cfg_for)
+// and counts instances, cells and back-pointer bytes per class; after the one
+// synchronisation the call makes anyway, t0_scatter_kernel writes each
+// instance's work item into its class's segment of the work list and carves
+// its back-pointer table out of the workspace with a warp-aggregated bump
+// allocator; then one dp_stage_kernel and one backtrack_kernel per non-empty
+// class.  Placement order is irrelevant to the results (each instance's table
+// is its own).
+constexpr int kT0Classes = 11;  // int32: cfg 4, 5, 3; fp64 and NaN domain: cfg 0-3
+constexpr int kT0Block = 256;   // instances per counting block (the unit waves are cut at)
+struct T0Stats {                // global: [max_ncol | class cursors | bump]
+  unsigned long long max_ncol[kT0Classes];
+  unsigned long long cursor[kT0Classes];
+  unsigned long long bump;
+};
+struct T0Block {  // per counting block
+  uint32_t count[kT0Classes];
+  uint32_t pad;
+  unsigned long long bytes;  // back-pointer bytes (each table 256-B aligned)
+  unsigned long long cells[kT0Classes];
+};
+struct T0Seg {  // a wave's class segments in the work list
+  unsigned long long off[kT0Classes];
+};
+__host__ __device__ inline int t0_class_mode(int c) { return c < 3 ? VM_INT32 : (c < 7 ? VM_F64 : VM_F64_NAN); }
+__host__ __device__ inline int t0_class_cfg(int c) {
+  return c < 3 ? (c == 0 ? 4 : (c == 1 ? 5 : 3)) : (c < 7 ? c - 3 : c - 7);
+}
+// single_cfg_for without the environment overrides (tier 0 is off when one is set)
+__host__ __device__ inline int t0_cfg_of(int64_t ncol, int mode) {
+  if (mode == VM_INT32 && ncol <= 12288) return 128 * 8 * 4 >= ncol ? 4 : 5;
+  if (ncol <= 64 * 4 * 4) return 0;
+  if (ncol <= 128 * 4 * 4) return 1;
+  if (ncol <= 256 * 4 * 4) return 2;
+  return 3;
+}
+__host__ __device__ inline int t0_class_of(int64_t ncol, int mode) {
+  const int cfg = t0_cfg_of(ncol, mode);
+  if (mode == VM_INT32) return cfg == 4 ? 0 : (cfg == 5 ? 1 : 2);
+  return (mode == VM_F64 ? 3 : 7) + cfg;
+}
+__host__ __device__ inline int64_t t0_ch(int cfg) {
+  constexpr int T[] = {64, 128, 256, 512, 128, 256}, E[] = {4, 4, 4, 4, 8, 8};
+  return (int64_t)T[cfg] * E[cfg];
+}
+__host__ __device__ inline int64_t t0_row_words(int mode, int cfg, int64_t ncol) {
+  const int64_t ch = t0_ch(cfg), cols = (ncol + ch - 1) / ch * ch;
+  return (cols + 31) / 32 * bp_words(mode);
+}
+// class and back-pointer bytes of instance k (class -1: not tier 0)
+__device__ __forceinline__ int t0_classify(const sp_instances& in, const InstInfo* info, const int32_t* flag,
+                                           int64_t max_i32, int64_t max_f64, int64_t k, int64_t& ncol,
+                                           unsigned long long& bytes, unsigned long long& cells) {
+  const InstInfo inf = info[k];
+  ncol = inf.w_eff + 1;
+  const int64_t L = in.layer_off[k + 1] - in.layer_off[k];
+  bytes = cells = 0;
+  if ((flag && !flag[k]) || L <= 0 || ncol > (inf.mode == VM_INT32 ? max_i32 : max_f64)) return -1;
+  const int c = t0_class_of(ncol, inf.mode);
+  bytes = align_up((size_t)L * (size_t)t0_row_words(inf.mode, t0_class_cfg(c), ncol) * 4, 256);
+  cells = (unsigned long long)L * (unsigned long long)ncol;
+  return c;
+}
+
+// one thread per instance: per-block class counts, cells and back-pointer
+// bytes (the host cuts waves at block boundaries), global widest row per class
+__global__ void __launch_bounds__(kT0Block) t0_count_kernel(sp_instances in, const InstInfo* info,
+                                                            const int32_t* flag, int64_t max_i32, int64_t max_f64,
+                                                            uint8_t* cls, T0Stats* stats, T0Block* blocks) {
+  __shared__ uint32_t s_cnt[kT0Classes];
+  __shared__ unsigned long long s_cells[kT0Classes], s_max[kT0Classes], s_bytes;
+  if (threadIdx.x < kT0Classes) {
+    s_cnt[threadIdx.x] = 0;
+    s_cells[threadIdx.x] = 0;
+    s_max[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) s_bytes = 0;
+  __syncthreads();
+  const int64_t k = (int64_t)blockIdx.x * kT0Block + threadIdx.x;
+  if (k < in.n) {
+    int64_t ncol;
+    unsigned long long bytes, cells;
+    const int c = t0_classify(in, info, flag, max_i32, max_f64, k, ncol, bytes, cells);
+    cls[k] = c < 0 ? 255 : (uint8_t)c;
+    if (c >= 0) {
+      atomicAdd(&s_cnt[c], 1u);
+      atomicAdd(&s_cells[c], cells);
+      atomicMax(&s_max[c], (unsigned long long)ncol);
+      atomicAdd(&s_bytes, bytes);
+    }
+  }
+  __syncthreads();
+  T0Block& b = blocks[blockIdx.x];
+  if (threadIdx.x < kT0Classes) {
+    b.count[threadIdx.x] = s_cnt[threadIdx.x];
+    b.cells[threadIdx.x] = s_cells[threadIdx.x];
+    if (s_max[threadIdx.x]) atomicMax(&stats->max_ncol[threadIdx.x], s_max[threadIdx.x]);
+  }
+  if (threadIdx.x == 0) {
+    b.pad = 0;
+    b.bytes = s_bytes;
+  }
+}
+
+// one wave (counting blocks [b0, b0 + gridDim.x)): the work items into their
+// class segments, back-pointer tables carved from `bump` (warp-aggregated),
+// the instances' flags cleared (solved here)
+__global__ void __launch_bounds__(kT0Block) t0_scatter_kernel(sp_instances in, const InstInfo* info,
+                                                              const uint8_t* cls, int64_t b0, T0Seg seg,
+                                                              T0Stats* stats, DpWork* work, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (b0 + blockIdx.x) * kT0Block + threadIdx.x;
+  const int c = k < in.n && cls[k] != 255 ? (int)cls[k] : -1;
+  unsigned long long bytes = 0;
+  int64_t ncol = 0;
+  int mode = 0;
+  if (c >= 0) {
+    const InstInfo inf = info[k];
+    ncol = inf.w_eff + 1;
+    mode = inf.mode;
+    const int64_t L = in.layer_off[k + 1] - in.layer_off[k];
+    bytes = align_up((size_t)L * (size_t)t0_row_words(mode, t0_class_cfg(c), ncol) * 4, 256);
+  }
+  unsigned long long incl = bytes;  // exclusive scan of the warp's bytes + one bump
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  unsigned long long wbase = 0;
+  if (lane == 31 && incl) wbase = atomicAdd(&stats->bump, incl);
+  wbase = __shfl_sync(0xffffffffu, wbase, 31);
+  const unsigned peers = __match_any_sync(0xffffffffu, c);  // one cursor increment per class in the warp
+  const int leader = __ffs(peers) - 1;
+  unsigned long long pbase = 0;
+  if (c >= 0 && lane == leader) pbase = atomicAdd(&stats->cursor[c], (unsigned long long)__popc(peers));
+  pbase = __shfl_sync(peers, pbase, leader);
+  if (c >= 0) {
+    DpWork w;
+    w.inst = k;
+    w.bp_off = (int64_t)(wbase + incl - bytes);
+    w.row_off = -1;
+    w.bp_row_words = t0_row_words(mode, t0_class_cfg(c), ncol);
+    work[seg.off[c] + pbase + __popc(peers & ((1u << lane) - 1u))] = w;
+    if (flag) flag[k] = 0;
+  }
+}
+
 int launch_plan(int mode, const DpPlan& p, const DpArgs& a, int64_t n_items, cudaStream_t st,
                 const sp_instances* in = nullptr, const sp_policies* out = nullptr, int32_t* idx = nullptr) {
   if (n_items == 0) return SP_OK;
@@ -1393,6 +1547,10 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   int32_t* overflow = (int32_t*)cv.take(sizeof(int32_t) * n);
   int32_t* flag = (int32_t*)cv.take(sizeof(int32_t) * n);
   unsigned long long* solved = (unsigned long long*)cv.take(4 * sizeof(unsigned long long));
+  const int64_t t0_nblk = (n + kT0Block - 1) / kT0Block;
+  T0Stats* t0s = (T0Stats*)cv.take(sizeof(T0Stats));
+  T0Block* t0blk = (T0Block*)cv.take(sizeof(T0Block) * t0_nblk);
+  uint8_t* t0cls = (uint8_t*)cv.take(n);
   const size_t fixed = align_up(cv.used, 256);
   if (!ws || fixed > ws_bytes) {
     set_required_workspace(fixed + (1 << 20));
@@ -1406,14 +1564,41 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   const int grid = (int)std::min<int64_t>((n + kPrepWarps - 1) / kPrepWarps, 1 << 20);
   const bool tier1_fits = steps_ok && out && fixed + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap) <= ws_bytes;
   const int64_t lo_i32 = steps_min_cols(VM_INT32, force), lo_f64 = steps_min_cols(VM_F64, force);
+  // tier 0 (the SMEM kernel's instances, planned on the device): the default
+  // kernel choice only (no forced variant or configuration), not for the
+  // workspace query, full tables, or the first half of an asynchronous call
+  const bool t0_allowed = out && tab_c == nullptr && !q_min && force < 0 && !getenv("SPLITPLAN_DP_THREADS") &&
+                          !getenv("SPLITPLAN_DP_SINGLE_E") && env_int("SPLITPLAN_NO_TIER0", 0) == 0;
+  const bool t0_ok = t0_allowed && !begin;
   int rc = SP_OK;
   if (!resume) {
-    prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv, reach, steps_ok ? flag : nullptr,
+    prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv, reach, (steps_ok || t0_allowed) ? flag : nullptr,
                                       tier1_fits ? kGridMinColsSteps : 0, lo_i32, lo_f64);
     rc = launch_check("prep_kernel launch");
     if (rc) return rc;
   }
   uint8_t* dyn = (uint8_t*)ws + fixed;
+  if (t0_ok) {  // classify and count (the totals travel with the next synchronisation)
+    rc = check_cuda(cudaMemsetAsync(t0s, 0, sizeof(T0Stats), st), "zero tier-0 counters");
+    if (rc) return rc;
+    t0_count_kernel<<<(unsigned)t0_nblk, kT0Block, 0, st>>>(*in, info, (steps_ok || t0_allowed) ? flag : nullptr,
+                                                           smem_max_cols(VM_INT32), smem_max_cols(VM_F64), t0cls,
+                                                           t0s, t0blk);
+    rc = launch_check("t0_count_kernel launch");
+    if (rc) return rc;
+  }
+  T0Stats ht0 = {};
+  std::vector<T0Block> hblk;
+  bool ht0_valid = false;
+  auto copy_t0 = [&]() -> int {  // queue the tier-0 counts' copy (the caller synchronises)
+    hblk.resize((size_t)t0_nblk);
+    int r = check_cuda(cudaMemcpyAsync(&ht0, t0s, sizeof(T0Stats), cudaMemcpyDeviceToHost, st), "copy tier-0 max");
+    if (!r)
+      r = check_cuda(cudaMemcpyAsync(hblk.data(), t0blk, sizeof(T0Block) * t0_nblk, cudaMemcpyDeviceToHost, st),
+                     "copy tier-0 counts");
+    ht0_valid = true;
+    return r;
+  };
 
   // Tier 1, planned on the device: one warp per instance on breakpoint lists
   // of kStepsCap breakpoints, every store at a position the kernel computes
@@ -1421,6 +1606,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   // Instances it cannot take (NaN domain, whole-GPU width, more breakpoints)
   // keep their flag and go through the host-planned tiers below.
   bool tier1 = false;
+  unsigned long long tier1_solved = 0;
   if (tier1_fits) {
     tier1 = true;
     StepsArgs sa = {};
@@ -1466,6 +1652,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       if (!rc)
         rc = check_cuda(cudaMemcpyAsync(hsolved, solved, sizeof(hsolved), cudaMemcpyDeviceToHost, st),
                         "copy solved count");
+      if (!rc && t0_ok) rc = copy_t0();
       if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync after breakpoint lists");
       if (rc) return rc;
     }
@@ -1477,11 +1664,108 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
                      24.0 * (double)hsolved[3] + 8.0 * (double)hsolved[2] +
                          8.0 * (double)(hsolved[3] + hsolved[0]),
                      DPV_STEPS);
-    if (hsolved[0] == (unsigned long long)n) {
-      set_full_workspace(fixed + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap));
-      set_steps_overflow(0);
-      return SP_OK;
+    tier1_solved = hsolved[0];
+  }
+
+  // Tier 0: every instance of the SMEM kernel's range, in waves of whole
+  // counting blocks whose back-pointer tables fit after tier 1's store
+  unsigned long long t0_taken = 0;
+  size_t t0_peak = 0;
+  const size_t region0 = tier1 ? align_up((size_t)(total + n) * steps_row_pair_bytes(kStepsCap), 256) : 0;
+  if (t0_ok) {
+    if (!ht0_valid) {
+      rc = copy_t0();
+      if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync after tier-0 count");
+      if (rc) return rc;
     }
+    uint8_t* base0 = dyn + region0;
+    const size_t avail0 = ws_bytes > fixed + region0 ? ws_bytes - fixed - region0 : 0;
+    bool fits = true;
+    unsigned long long cnt = 0;
+    for (const T0Block& b : hblk) {
+      fits &= b.bytes <= avail0;
+      for (int c = 0; c < kT0Classes; ++c) cnt += b.count[c];
+    }
+    if (cnt > 0 && fits) {
+      DpArgs a0 = {};
+      a0.layer_off = in->layer_off;
+      a0.sac = in->source_at_client;
+      a0.info = info;
+      a0.shifts = shifts;
+      a0.rv = rv;
+      a0.bp = base0;
+      a0.rows = base0;
+      int64_t b_lo = 0;
+      while (b_lo < t0_nblk) {
+        // one wave: whole blocks while their tables fit
+        int64_t b_hi = b_lo;
+        size_t wbytes = 0;
+        unsigned long long wcnt[kT0Classes] = {}, wcells[kT0Classes] = {};
+        while (b_hi < t0_nblk && wbytes + hblk[b_hi].bytes <= avail0) {
+          wbytes += hblk[b_hi].bytes;
+          for (int c = 0; c < kT0Classes; ++c) {
+            wcnt[c] += hblk[b_hi].count[c];
+            wcells[c] += hblk[b_hi].cells[c];
+          }
+          ++b_hi;
+        }
+        T0Seg seg;
+        unsigned long long acc = 0;
+        for (int c = 0; c < kT0Classes; ++c) {
+          seg.off[c] = acc;
+          acc += wcnt[c];
+        }
+        t0_peak = std::max(t0_peak, wbytes);
+        if (acc) {
+          rc = check_cuda(cudaMemsetAsync(&t0s->cursor, 0, sizeof(unsigned long long) * (kT0Classes + 1), st),
+                          "zero tier-0 cursors");
+          if (rc) return rc;
+          t0_scatter_kernel<<<(unsigned)(b_hi - b_lo), kT0Block, 0, st>>>(*in, info, t0cls, b_lo, seg, t0s, work,
+                                                                          flag);
+          rc = launch_check("t0_scatter_kernel launch");
+          if (rc) return rc;
+          for (int c = 0; c < kT0Classes; ++c) {
+            const unsigned long long m = wcnt[c];
+            if (!m) continue;
+            const int mode = t0_class_mode(c), cfg = t0_class_cfg(c);
+            DpArgs ga = a0;
+            ga.work = work + seg.off[c];
+            const size_t smem = stage_bytes_mode(mode) + single_row_bytes(mode, (int64_t)ht0.max_ncol[c], cfg);
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (profiling()) {
+              cudaEventCreate(&e0);
+              cudaEventCreate(&e1);
+              cudaEventRecord(e0, st);
+            }
+            switch (mode) {
+              case VM_INT32: rc = launch_single<VM_INT32, true>(ga, (int64_t)m, cfg, smem, st); break;
+              case VM_F64: rc = launch_single<VM_F64, true>(ga, (int64_t)m, cfg, smem, st); break;
+              default: rc = launch_single<VM_F64_NAN, true>(ga, (int64_t)m, cfg, smem, st); break;
+            }
+            if (rc) return rc;
+            if (profiling()) {
+              cudaEventRecord(e1, st);
+              prof_record_dp(e0, e1, (double)wcells[c], (double)wcells[c] * hbm_bytes_per_cell(mode, DPV_SMEM),
+                             DPV_SMEM);
+            }
+            backtrack_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(*in, info, shifts, work + seg.off[c],
+                                                                          (int64_t)m, base0, idx, *out);
+            rc = launch_check("backtrack_kernel launch");
+            if (rc) return rc;
+          }
+        }
+        trace("tier-0 wave", (long long)acc);
+        b_lo = b_hi;
+      }
+      t0_taken = cnt;
+    }
+  }
+  if (tier1_solved + t0_taken == (unsigned long long)n) {
+    unsigned long long t0_all = 0;
+    for (const T0Block& b : hblk) t0_all += b.bytes;
+    set_full_workspace(fixed + region0 + (size_t)t0_all);
+    set_steps_overflow(0);
+    return SP_OK;
   }
 
   std::vector<InstInfo> hinfo(n);
@@ -1504,7 +1788,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   }
   const size_t avail = ws_bytes - fixed;
   std::vector<int32_t> hflag;
-  if (tier1) {  // the instances tier 1 left: the next tiers take only them
+  if (tier1 || t0_taken) {  // the instances tiers 1 and 0 left: the next tiers take only them
     hflag.resize(n);
     rc = check_cuda(cudaMemcpyAsync(hflag.data(), flag, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st),
                     "copy tier-1 flags");
@@ -1523,7 +1807,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   int64_t cached_ncol = -1, cached_L = -1;
   int cached_cap = -1;
   for (int64_t k = 0; k < n; ++k) {
-    if (tier1 && !hflag[k]) continue;  // solved on breakpoint lists
+    if (!hflag.empty() && !hflag[k]) continue;  // solved by tier 1 (breakpoint lists) or tier 0
     const int64_t ncol = hinfo[k].w_eff + 1;
     if (ncol > kMaxCols) {
       set_error(SP_ERR_UNSUPPORTED, "instance %lld: W_eff = %lld exceeds the supported 2^31 columns",

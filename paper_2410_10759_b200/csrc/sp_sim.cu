@@ -10,6 +10,7 @@
 #include <algorithm>
 
 #include "sp_internal.cuh"
+#include "np_random.cuh"
 
 namespace sp {
 namespace {
@@ -130,6 +131,36 @@ __global__ void sim_replay_kernel(sp_sim_batch b, sp_sim_out o, HeapEntry* heap_
   }
 }
 
+// One thread per skeleton: numpy's default_rng(seed) draws in numpy's order
+// (np_random.cuh; throughput_sim.py:179-186): the exponential inter-arrival
+// gaps summed left to right (np.cumsum), then the table-row picks, then the
+// execution counts.  The three phases draw from the same stream, so a thread
+// generates its skeleton start to end.
+__global__ void skeleton_kernel(const int64_t* seeds, const int64_t* lo, const int64_t* hi, int64_t n,
+                                int64_t horizon, double scale, int64_t exec_max, double* arrival_ms,
+                                int32_t* choice, int32_t* exec_count, int32_t* status) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t a = lo[r], span = hi[r] - a;
+  if (span < 1) {
+    if (status) status[r] = SP_ERR_INVALID;
+    return;
+  }
+  nprand::Pcg64 g = nprand::pcg64_from_seed((uint64_t)seeds[r]);
+  double* arr = arrival_ms + r * horizon;
+  double run = 0.0;
+  for (int64_t k = 0; k < horizon; ++k) {
+    const double e = dmul(scale, nprand::standard_exponential(g));
+    run = k == 0 ? e : dadd(run, e);
+    arr[k] = run;
+  }
+  int32_t* ch = choice + r * horizon;
+  for (int64_t k = 0; k < horizon; ++k) ch[k] = (int32_t)(nprand::integers(g, 0, span) + a);
+  int32_t* ex = exec_count + r * horizon;
+  for (int64_t k = 0; k < horizon; ++k) ex[k] = (int32_t)nprand::integers(g, 1, exec_max + 1);
+  if (status) status[r] = SP_OK;
+}
+
 __global__ void segment_sum_kernel(const double* x, const int64_t* off, int64_t n_seg, double* out) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_seg) return;
@@ -153,6 +184,21 @@ int sp_segment_sum(const double* x, const int64_t* seg_off, int64_t n_seg, doubl
   segment_sum_kernel<<<(unsigned)((n_seg + 127) / 128), 128, 0, (cudaStream_t)stream>>>(x, seg_off, n_seg,
                                                                                        out);
   return launch_check("segment_sum_kernel launch");
+}
+
+int sp_sim_skeletons(const int64_t* seeds, const int64_t* choice_lo, const int64_t* choice_hi, int64_t n,
+                     int64_t horizon, double scale, int64_t exec_max, double* arrival_ms, int32_t* choice,
+                     int32_t* exec_count, int32_t* status, void* stream) {
+  if (n < 0 || horizon < 0 || exec_max < 1 || exec_max >= ((int64_t)1 << 31) ||
+      (n > 0 && (!seeds || !choice_lo || !choice_hi)) ||
+      (n > 0 && horizon > 0 && (!arrival_ms || !choice || !exec_count))) {
+    set_error(SP_ERR_INVALID, "sp_sim_skeletons: bad arguments");
+    return SP_ERR_INVALID;
+  }
+  if (n == 0) return SP_OK;
+  skeleton_kernel<<<(unsigned)((n + 63) / 64), 64, 0, (cudaStream_t)stream>>>(
+      seeds, choice_lo, choice_hi, n, horizon, scale, exec_max, arrival_ms, choice, exec_count, status);
+  return launch_check("skeleton_kernel launch");
 }
 
 size_t sp_sim_workspace_bytes(const sp_sim_batch* b) {

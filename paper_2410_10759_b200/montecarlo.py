@@ -11,10 +11,12 @@ demand variants over one seeded arrival skeleton (`compare_variants`,
 
     K1 cost table + prep + K2 + K3   every request of every scenario (dp)
     prefix kernel                    greedy and all_server on the same instances
+    skeleton kernel                  one seeded arrival skeleton per scenario
+                                     (numpy's default_rng stream, bit for bit)
     K4 replay                        3 runs per scenario in one launch
 
-with the table bookkeeping (filter, coordinate sort, normalisation) and the
-numpy PCG64 skeletons on the host, exactly as the reference computes them.
+with the table bookkeeping (filter, coordinate sort, normalisation) on the
+host and the device, exactly as the reference computes them.
 Scenarios are independent, so `run(..., group=...)` shards them over ranks
 and gathers the per-scenario records once at the end.
 """
@@ -30,7 +32,7 @@ from . import _native as N
 from . import batch as B
 from . import workloads as W
 from .requests import Engine, RequestBatch
-from .throughput_sim import VARIANTS, replay_arrays
+from .throughput_sim import VARIANTS, replay_arrays, skeletons_device
 
 BETA_PER_MS = 0.057
 HORIZON = 2000
@@ -128,81 +130,6 @@ def segment_means(values: np.ndarray, row_off: np.ndarray) -> np.ndarray:
         return sums / np.diff(row_off).astype(np.float64)
 
 
-def _skeleton_rows(sids, a, b, beta_per_ms, horizon, arr, gidx, execs, lo, hi):
-    """Seeded skeletons of rows [lo, hi) (numpy PCG64, throughput_sim.py:179-186)."""
-    for r in range(lo, hi):
-        g = np.random.default_rng(int(sids[r]))
-        arr[r] = np.cumsum(g.exponential(scale=1.0 / beta_per_ms, size=horizon))
-        gidx[r] = g.integers(0, b[r] - a[r], size=horizon) + a[r]
-        execs[r] = g.integers(1, EXEC_MAX + 1, size=horizon)
-
-
-def _skeleton_job(job):
-    from multiprocessing import shared_memory
-    names, n, horizon, sids, a, b, beta_per_ms, lo, hi = job
-    shms = [shared_memory.SharedMemory(name=x) for x in names]
-    try:
-        arr = np.ndarray((n, horizon), np.float64, buffer=shms[0].buf)
-        gidx = np.ndarray((n, horizon), np.int64, buffer=shms[1].buf)
-        execs = np.ndarray((n, horizon), np.int64, buffer=shms[2].buf)
-        _skeleton_rows(sids, a, b, beta_per_ms, horizon, arr, gidx, execs, lo, hi)
-        del arr, gidx, execs
-    finally:
-        for x in shms:
-            x.close()
-
-
-_POOL = None
-
-
-def _pool(procs: int):
-    """Forked worker processes for the skeletons, kept for the process's
-    lifetime (numpy only: the workers never touch CUDA)."""
-    global _POOL
-    if _POOL is None or _POOL[1] != procs:
-        import atexit
-        from multiprocessing import get_context
-        if _POOL is not None:
-            _POOL[0].terminate()
-        _POOL = (get_context("fork").Pool(procs), procs)
-        atexit.register(_POOL[0].terminate)
-    return _POOL[0]
-
-
-def skeletons(sids, a, b, beta_per_ms, horizon, procs=None):
-    """Arrival skeletons of scenarios `sids` (tables rows [a, b)): arrivals,
-    global table-row indices and execution counts, [n, horizon] each.
-
-    Bit-identical to the reference's per-scenario `default_rng(seed)` draws.
-    numpy's generator holds the GIL for part of every call, so large grids are
-    generated by forked worker processes writing into shared memory."""
-    import os
-    n = len(sids)
-    procs = procs or int(os.environ.get("SPLITPLAN_SKELETON_PROCS", "0")) or min(32, os.cpu_count() or 1)
-    if n < 1024 or procs <= 1:
-        arr = np.empty((n, horizon))
-        gidx = np.empty((n, horizon), np.int64)
-        execs = np.empty((n, horizon), np.int64)
-        _skeleton_rows(sids, a, b, beta_per_ms, horizon, arr, gidx, execs, 0, n)
-        return arr, gidx, execs
-    from multiprocessing import shared_memory
-    shms = [shared_memory.SharedMemory(create=True, size=max(1, n * horizon * 8)) for _ in range(3)]
-    try:
-        names = [x.name for x in shms]
-        step = (n + procs - 1) // procs
-        jobs = [(names, n, horizon, sids, a, b, beta_per_ms, lo, min(n, lo + step))
-                for lo in range(0, n, step)]
-        _pool(procs).map(_skeleton_job, jobs, chunksize=1)
-        arr = np.ndarray((n, horizon), np.float64, buffer=shms[0].buf).copy()
-        gidx = np.ndarray((n, horizon), np.int64, buffer=shms[1].buf).copy()
-        execs = np.ndarray((n, horizon), np.int64, buffer=shms[2].buf).copy()
-        return arr, gidx, execs
-    finally:
-        for x in shms:
-            x.close()
-            x.unlink()
-
-
 def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORIZON,
         omega_requests: float = OMEGA_REQUESTS, group=None) -> MonteCarloResult:
     """The cfg4 sweep over `scenario_ids` (default: all 65,536), sharded over
@@ -240,15 +167,15 @@ def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORI
     for blk in range(0, len(sim), SIM_BLOCK):
         ids = sim[blk:blk + SIM_BLOCK]
         n = len(ids)
-        arrivals, gidx, execs = skeletons(sids[ids], row_off[ids], row_off[ids + 1], beta_per_ms, horizon)
-        arr_d = torch.from_numpy(arrivals).pin_memory().to(dev, non_blocking=True)
-        gidx_d = torch.from_numpy(gidx.astype(np.int32)).pin_memory().to(dev, non_blocking=True).long()
-        ex_d = torch.from_numpy(execs.astype(np.int8)).pin_memory().to(dev, non_blocking=True)
+        # the seeded skeletons, drawn on the device (numpy's stream bit for bit)
+        arr_d, gidx_d, ex_d = skeletons_device(sids[ids], row_off[ids], row_off[ids + 1], horizon, beta_per_ms,
+                                               EXEC_MAX)
+        gidx_d = gidx_d.long()
         arr3 = arr_d[:, None, :].expand(n, 3, horizon).reshape(-1)
         dur3 = (dl_ms_d[gidx_d] * ex_d.to(torch.float64))[:, None, :].expand(n, 3, horizon).reshape(-1)
         dem3 = demand_d[gidx_d].permute(0, 2, 1).reshape(-1)
         roff = np.arange(3 * n + 1, dtype=np.int64) * horizon
-        o = replay_arrays(roff, arr3, dem3, dur3, np.repeat(capacity[ids], 3))
+        o = replay_arrays(roff, arr3, dem3, dur3, np.repeat(capacity[ids], 3), per_request=False)
         max_w[ids] = o["mx"][:3 * n].cpu().numpy().reshape(-1, 3)
         mean_w[ids] = o["mean"][:3 * n].cpu().numpy().reshape(-1, 3)
         status[ids] = o["st"][:3 * n].cpu().numpy().reshape(-1, 3)
@@ -282,4 +209,4 @@ def _gather(local, sids, bounds, group) -> MonteCarloResult:
                             int(st[0]), float(st[1]))
 
 
-__all__ = ["MonteCarloResult", "run", "skeletons", "solve_requests", "scenario_tables", "VARIANTS"]
+__all__ = ["MonteCarloResult", "run", "solve_requests", "scenario_tables", "VARIANTS"]

@@ -189,6 +189,28 @@ def _skeleton(config: SimConfig):
     return arrivals, idx, execs
 
 
+def skeletons_device(seeds, choice_lo, choice_hi, horizon: int, beta_per_ms: float,
+                     exec_count_max: int = 10) -> tuple:
+    """`_skeleton` of many seeded runs at once on the GPU (sp_sim_skeletons:
+    numpy's default_rng(seed) stream bit for bit, one thread per run).  Run r
+    picks table rows in [choice_lo[r], choice_hi[r]).  Returns device tensors
+    [n, horizon]: arrivals (float64), rows (int32), execution counts (int32)."""
+    dev = N.device()
+    seeds_d = N.to_dev(np.asarray(seeds, dtype=np.int64), torch.int64, dev)
+    lo_d = N.to_dev(np.asarray(choice_lo, dtype=np.int64), torch.int64, dev)
+    hi_d = N.to_dev(np.asarray(choice_hi, dtype=np.int64), torch.int64, dev)
+    n = seeds_d.numel()
+    if bool(((hi_d - lo_d) < 1).any()) or bool((seeds_d < 0).any()):
+        raise ValueError("skeletons need non-negative seeds and non-empty scenario ranges")
+    arr = torch.empty((n, horizon), dtype=torch.float64, device=dev)
+    rows = torch.empty((n, horizon), dtype=torch.int32, device=dev)
+    execs = torch.empty((n, horizon), dtype=torch.int32, device=dev)
+    N.check(N.library().sp_sim_skeletons(N.ptr(seeds_d), N.ptr(lo_d), N.ptr(hi_d), n, int(horizon),
+                                         1.0 / beta_per_ms, int(exec_count_max), N.ptr(arr), N.ptr(rows),
+                                         N.ptr(execs), None, N.stream_ptr()), "sp_sim_skeletons")
+    return arr, rows, execs
+
+
 def _project(config: SimConfig, arrivals, idx, execs, variant: str) -> Stream:
     dem = np.array([s.demand(variant) for s in config.scenarios])
     dl = np.array([s.deadline_s * 1000.0 for s in config.scenarios])
@@ -205,11 +227,12 @@ def generate_stream(config: SimConfig) -> Stream:
 # replay on the GPU
 
 
-def replay_arrays(run_off, arrival_ms, demand, duration_ms, capacity) -> dict:
+def replay_arrays(run_off, arrival_ms, demand, duration_ms, capacity, per_request: bool = True) -> dict:
     """K4 over independent runs given as CSR arrays (host numpy or device
     tensors): run k replays requests [run_off[k], run_off[k+1]) against
     capacity[k].  Returns the device outputs: admit / wait / cumulative wait
-    per request, max / mean wait, status and the deadlocked request per run."""
+    per request (wait / cumulative only with `per_request`), max / mean wait,
+    status and the deadlocked request per run."""
     dev = N.device()
     t = dict(off=N.to_dev(run_off, torch.int64, dev), arr=N.to_dev(arrival_ms, torch.float64, dev),
              dem=N.to_dev(demand, torch.float64, dev), dur=N.to_dev(duration_ms, torch.float64, dev),
@@ -217,15 +240,16 @@ def replay_arrays(run_off, arrival_ms, demand, duration_ms, capacity) -> dict:
     nr = t["off"].numel() - 1
     total = t["arr"].numel()
     o = dict(admit=torch.empty(max(total, 1), dtype=torch.float64, device=dev),
-             wait=torch.empty(max(total, 1), dtype=torch.float64, device=dev),
-             cum=torch.empty(max(total, 1), dtype=torch.float64, device=dev),
              mx=torch.empty(max(nr, 1), dtype=torch.float64, device=dev),
              mean=torch.empty(max(nr, 1), dtype=torch.float64, device=dev),
              st=torch.zeros(max(nr, 1), dtype=torch.int32, device=dev),
              dead=torch.empty(max(nr, 1), dtype=torch.int64, device=dev))
+    if per_request:
+        o["wait"] = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+        o["cum"] = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
     b = N.SpSimBatch(nr, total, *[N.ptr(t[k]).value for k in ("off", "arr", "dem", "dur", "cap")])
-    so = N.SpSimOut(*[N.ptr(o[k]).value for k in ("admit", "wait", "cum", "mx", "mean", "st",
-                                                   "dead")])
+    so = N.SpSimOut(*[N.ptr(o[k]).value if k in o else None for k in ("admit", "wait", "cum", "mx", "mean",
+                                                                       "st", "dead")])
     lib = N.library()
     need = int(lib.sp_sim_workspace_bytes(b))
     ws = N.workspace(need)

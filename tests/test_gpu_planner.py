@@ -554,3 +554,62 @@ def test_engine_solve_async_pipelined(gpu):
     for a, b in zip(ref, got):
         for key in ("pi", "client_value", "server_load", "integer_latency", "feasible", "status"):
             np.testing.assert_array_equal(a[key], getattr(b, key).numpy(), err_msg=key)
+
+
+# ---------------------------------------------------------------------------
+# tier 0: the SMEM kernel's instances planned on the device
+
+
+def _tier0_instances(seed, n):
+    """Narrow instances over the tier-0 classes: integral r (int32 domain) at
+    widths in all three int32 configurations, float r (fp64 domain) at the
+    four fp64 widths (the NaN domain's narrow instances are in the inf-r
+    batteries)."""
+    rng = np.random.default_rng(seed)
+    w_int, w_f64 = [300, 1500, 3000, 6000, 14000], [300, 700, 1500, 2500, 6000, 11000]
+    out = []
+    for t in range(n):
+        kind = t % 5
+        widths = w_int if kind < 3 else w_f64
+        W = widths[(t // 5) % len(widths)] + int(rng.integers(0, 200))
+        L = int(rng.integers(4, 24))
+        hi = max(2, W // 6)
+        r = rng.integers(0, 9, L).astype(float) if kind < 3 else rng.random(L) * 7
+        out.append(dict(i=rng.integers(0, hi, L), s=rng.integers(0, hi, L), u=rng.integers(0, hi, L),
+                        d=rng.integers(0, hi, L), r=r, budget=int(W), sac=bool(t % 2)))
+    return out
+
+
+@pytest.mark.parametrize("waves", ["one", "several"])
+def test_tier0_device_planned_waves(gpu, waves, capfd, monkeypatch):
+    """1,300 narrow instances (six counting blocks) over every tier-0 class,
+    run by the device-planned SMEM tier in one wave, and in several waves of
+    a workspace holding about a third of their back-pointer tables; every
+    placement bit-exact against the oracle."""
+    import torch
+    from paper_2410_10759_b200 import _native as N, batch as B
+    insts = _tier0_instances(29, 1300)
+    off = np.zeros(len(insts) + 1, np.int64)
+    np.cumsum([len(x["r"]) for x in insts], out=off[1:])
+    cat = lambda k: np.concatenate([x[k] for x in insts])
+    b = B.InstanceBatch.from_arrays(off, cat("i"), cat("s"), cat("u"), cat("d"), cat("r"),
+                                    [x["budget"] for x in insts], [x["sac"] for x in insts])
+    lib = N.library()
+    mn, full = B.dp_workspace_bytes(b)
+    size = full + (1 << 20) if waves == "one" else mn + (full - mn) // 3
+    ws = torch.empty(size, dtype=torch.uint8, device=N.device())
+    out = B.PolicyBatch.empty(b.n, b.total_layers, b.r.device)
+    monkeypatch.setenv("SPLITPLAN_TRACE", "1")
+    rc = lib.sp_plan_dp(b.struct(), out.struct(), N.ptr(ws), size, N.stream_ptr())
+    assert rc == 0, lib.sp_last_error()
+    host = out.to_host()
+    err = capfd.readouterr().err
+    n_waves = err.count("tier-0 wave")
+    assert n_waves == 1 if waves == "one" else n_waves >= 2, err[-2000:]
+    assert "items planned" not in err  # nothing left for the host-planned tiers
+    for k, inst in enumerate(insts):
+        exp = O.plan_dp(inst)
+        got = dict(pi=host["pi"][off[k]:off[k + 1]], client_value=host["client_value"][k],
+                   server_load=host["server_load"][k], integer_latency=host["integer_latency"][k],
+                   feasible=host["feasible"][k])
+        assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"tier0 {waves}[{k}]")

@@ -56,29 +56,6 @@ def test_cfg4_grid():
     assert set(np.unique(req["model"])) <= {0, 1, 2}
 
 
-def test_cfg4_skeletons_match_reference_draws():
-    """The Monte-Carlo skeletons (forked workers into shared memory, or inline)
-    are the reference's per-scenario default_rng(seed) draws, bit for bit
-    (throughput_sim.py:179-186)."""
-    from paper_2410_10759_b200 import montecarlo as MC
-    n, horizon, beta = 1100, 300, MC.BETA_PER_MS
-    sids = np.arange(n) * 3 + 11
-    a = np.arange(n) * 64
-    b = a + np.random.default_rng(1).integers(1, 64, n)
-    inline = MC.skeletons(sids, a, b, beta, horizon, procs=1)
-    forked = MC.skeletons(sids, a, b, beta, horizon, procs=3)
-    for x, y in zip(inline, forked):
-        assert np.array_equal(x, y)
-    for r in (0, 517, n - 1):
-        g = np.random.default_rng(int(sids[r]))
-        arr = np.cumsum(g.exponential(scale=1.0 / beta, size=horizon))
-        idx = g.integers(0, b[r] - a[r], size=horizon)
-        ex = g.integers(1, MC.EXEC_MAX + 1, size=horizon)
-        assert np.array_equal(inline[0][r], arr)
-        assert np.array_equal(inline[1][r], idx + a[r])
-        assert np.array_equal(inline[2][r], ex)
-
-
 def test_lexsort_device_equals_numpy():
     """The Monte-Carlo table sort (successive stable sorts, here on the CPU
     device) is np.lexsort's permutation, ties and float keys included."""

@@ -19,5 +19,5 @@ if __name__ == "__main__":
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     print(json.dumps({"scenarios": n, "wall_s": dt, "scenarios_per_s": n / dt, "cpus": os.cpu_count(),
-                      "skeleton_procs": os.environ.get("SPLITPLAN_SKELETON_PROCS", "auto"),
+                      "skeletons": "device",
                       "requests": r.requests, "dp_cells": r.dp_cells}))

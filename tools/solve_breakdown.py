@@ -1,6 +1,7 @@
 """Where the time of one Engine.solve goes (device kernels vs host planning).
 
     python tools/solve_breakdown.py --config cfg3 --n 1000000
+    python tools/solve_breakdown.py --config cfg4 --n 65536     (scenarios)
 
 Runs a warm-up solve (the workspace grows to its useful size), then one
 timed solve with the library's per-launch DP profile, CUDA events around the
@@ -26,7 +27,11 @@ def main():
     from paper_2410_10759_b200 import batch as B
     from paper_2410_10759_b200 import workloads as W
     from paper_2410_10759_b200.requests import Engine, RequestBatch
-    req, layers = getattr(W, args.config)(args.n)
+    if args.config == "cfg4":  # n scenarios of 64 requests each
+        import numpy as np
+        req, layers, _ = W.cfg4(np.arange(args.n))
+    else:
+        req, layers = getattr(W, args.config)(args.n)
     eng = Engine(layers)
     dev = RequestBatch.from_numpy(**req).to(N.device())
     total = int(eng.n_layers[req["model"]].sum())
