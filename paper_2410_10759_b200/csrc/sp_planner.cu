@@ -1567,9 +1567,11 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   // tier 0 (the SMEM kernel's instances, planned on the device): the default
   // kernel choice only (no forced variant or configuration), not for the
   // workspace query, full tables, or the first half of an asynchronous call
-  const bool t0_allowed = out && tab_c == nullptr && !q_min && force < 0 && !getenv("SPLITPLAN_DP_THREADS") &&
+  // (the workspace query counts its instances the same way, to size it)
+  const bool t0_allowed = (out || q_min) && tab_c == nullptr && force < 0 && !getenv("SPLITPLAN_DP_THREADS") &&
                           !getenv("SPLITPLAN_DP_SINGLE_E") && env_int("SPLITPLAN_NO_TIER0", 0) == 0;
-  const bool t0_ok = t0_allowed && !begin;
+  const bool t0_count = t0_allowed && !begin;  // classify and count
+  const bool t0_ok = t0_count && !q_min;        // and run
   int rc = SP_OK;
   if (!resume) {
     prep_kernel<<<grid, 128, 0, st>>>(*in, info, shifts, rv, reach, (steps_ok || t0_allowed) ? flag : nullptr,
@@ -1578,7 +1580,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     if (rc) return rc;
   }
   uint8_t* dyn = (uint8_t*)ws + fixed;
-  if (t0_ok) {  // classify and count (the totals travel with the next synchronisation)
+  if (t0_count) {  // classify and count (the totals travel with the next synchronisation)
     rc = check_cuda(cudaMemsetAsync(t0s, 0, sizeof(T0Stats), st), "zero tier-0 counters");
     if (rc) return rc;
     t0_count_kernel<<<(unsigned)t0_nblk, kT0Block, 0, st>>>(*in, info, (steps_ok || t0_allowed) ? flag : nullptr,
@@ -1672,12 +1674,17 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   unsigned long long t0_taken = 0;
   size_t t0_peak = 0;
   const size_t region0 = tier1 ? align_up((size_t)(total + n) * steps_row_pair_bytes(kStepsCap), 256) : 0;
-  if (t0_ok) {
-    if (!ht0_valid) {
-      rc = copy_t0();
-      if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync after tier-0 count");
-      if (rc) return rc;
+  std::vector<uint8_t> hcls;  // the query: tier-0 classes (255: a host-planned tier's instance)
+  if (t0_count && !ht0_valid) {
+    rc = copy_t0();
+    if (!rc && q_min) {
+      hcls.resize(n);
+      rc = check_cuda(cudaMemcpyAsync(hcls.data(), t0cls, n, cudaMemcpyDeviceToHost, st), "copy tier-0 classes");
     }
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync after tier-0 count");
+    if (rc) return rc;
+  }
+  if (t0_ok) {
     uint8_t* base0 = dyn + region0;
     const size_t avail0 = ws_bytes > fixed + region0 ? ws_bytes - fixed - region0 : 0;
     bool fits = true;
@@ -1760,6 +1767,21 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       t0_taken = cnt;
     }
   }
+  if (q_min && !hcls.empty()) {  // the query, every instance in tier 0: no host planning
+    unsigned long long cnt = 0, all = 0, mx = 0;
+    for (const T0Block& b : hblk) {
+      for (int c = 0; c < kT0Classes; ++c) cnt += b.count[c];
+      all += b.bytes;
+      mx = std::max(mx, b.bytes);
+    }
+    if (cnt == (unsigned long long)n) {
+      *q_min = fixed + (size_t)mx;
+      *q_full = fixed + (size_t)all;
+      if (q_part_min) *q_part_min = 0;
+      if (q_part_full) *q_part_full = 0;
+      return SP_OK;
+    }
+  }
   if (tier1_solved + t0_taken == (unsigned long long)n) {
     unsigned long long t0_all = 0;
     for (const T0Block& b : hblk) t0_all += b.bytes;
@@ -1808,6 +1830,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   int cached_cap = -1;
   for (int64_t k = 0; k < n; ++k) {
     if (!hflag.empty() && !hflag[k]) continue;  // solved by tier 1 (breakpoint lists) or tier 0
+    if (!hcls.empty() && hcls[k] != 255) continue;  // the query: tier 0's (sized below)
     const int64_t ncol = hinfo[k].w_eff + 1;
     if (ncol > kMaxCols) {
       set_error(SP_ERR_UNSUPPORTED, "instance %lld: W_eff = %lld exceeds the supported 2^31 columns",
@@ -1877,8 +1900,13 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       mn = std::max(mn, imin);
       full = grid ? std::max(full, ifull) : full + ifull;
     }
+    size_t t0_all = 0;  // tier 0: its tables in one wave (useful), one counting block's (minimum)
+    for (const T0Block& b : hblk) {
+      t0_all += b.bytes;
+      mn = std::max(mn, (size_t)b.bytes);
+    }
     *q_min = fixed + mn;
-    *q_full = fixed + std::max(full + tier1, mn);
+    *q_full = fixed + std::max(full + tier1 + t0_all, mn);
     if (q_part_min) *q_part_min = pmn;
     if (q_part_full) *q_part_full = pfull;
     return SP_OK;

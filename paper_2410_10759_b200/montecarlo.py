@@ -54,7 +54,8 @@ class MonteCarloResult:
 
 
 def solve_requests(req: dict, layer_lists) -> dict:
-    """dp / greedy / all_server server loads and feasibility for every request."""
+    """dp / greedy / all_server server loads and feasibility for every request
+    (device tensors)."""
     eng = Engine(layer_lists)
     sol = eng.solve(RequestBatch.from_numpy(**req).to(N.device()))
     out = {"dp": sol.policies}
@@ -62,11 +63,9 @@ def solve_requests(req: dict, layer_lists) -> dict:
     out["all_server"] = B.plan_prefix(sol.instances, N.SP_ALL_SERVER)
     w_eff = B.effective_budget(sol.instances)
     lens = (sol.layer_off[1:] - sol.layer_off[:-1]).to(torch.float64)
-    cells = float((lens * (w_eff + 1).to(torch.float64)).sum().item())
-    valid = (sol.status == 0).cpu().numpy()  # cost-table errors are error cells, never kept
-    host = {k: dict(load=v.server_load.cpu().numpy(), ok=v.feasible.cpu().numpy().astype(bool) & valid)
-            for k, v in out.items()}
-    host["cells"] = cells
+    valid = sol.status == 0  # cost-table errors are error cells, never kept
+    host = {k: dict(load=v.server_load, ok=(v.feasible != 0) & valid) for k, v in out.items()}
+    host["cells"] = (lens * (w_eff + 1).to(torch.float64)).sum()
     return host
 
 
@@ -74,60 +73,72 @@ def scenario_tables(req: dict, off: np.ndarray, model_names, solved: dict):
     """Per scenario, the reference's scenario table: coordinates whose dp,
     greedy and all_server rows are feasible, sorted by (model, seq_len,
     deadline, up, down), one row per coordinate, demands normalised by the
-    mean nosplit load (throughput_sim.py:133-163).
+    mean nosplit load (throughput_sim.py:133-163).  On the device.
 
-    Returns CSR offsets over rows, the per-row demands [rows, 3] and deadlines."""
+    Returns CSR offsets over rows (host), the per-row demands [rows, 3] and
+    deadlines (device)."""
+    dev = N.device()
     # rank of each request's model name in sorted name order (the reference
     # sorts coordinates by name): a per-model lookup, not a sort of strings
     uniq = sorted(set(model_names))
-    rank_of = np.array([uniq.index(x) for x in model_names], dtype=np.int64)
-    name_rank = rank_of[np.asarray(req["model"])]
+    rank_of = torch.tensor([uniq.index(x) for x in model_names], dtype=torch.int64, device=dev)
+    col = lambda k, dt: torch.from_numpy(np.ascontiguousarray(req[k], dtype=dt)).to(dev)
+    name_rank = rank_of[col("model", np.int64)]
+    seq, dl, up, down = (col("seq_len", np.int64), col("deadline_s", np.float64), col("uplink_bps", np.float64),
+                         col("downlink_bps", np.float64))
     S = len(off) - 1
-    scen = np.repeat(np.arange(S), np.diff(off))
+    counts = torch.from_numpy(np.diff(off)).to(dev)
+    scen = torch.repeat_interleave(torch.arange(S, device=dev), counts)
     keep = solved["dp"]["ok"] & solved["greedy"]["ok"] & solved["all_server"]["ok"]
-    order = lexsort_device((req["downlink_bps"], req["uplink_bps"], req["deadline_s"], req["seq_len"],
-                            name_rank, scen))
+    order = lexsort_tensors((down, up, dl, seq, name_rank, scen))
     order = order[keep[order]]
     # identical coordinates collapse to one row (a dict keyed by coordinate)
-    key = np.stack([scen[order], name_rank[order], req["seq_len"][order]]).T
-    fkey = np.stack([req["deadline_s"][order], req["uplink_bps"][order],
-                     req["downlink_bps"][order]]).T
-    dup = np.zeros(order.size, dtype=bool)
-    if order.size > 1:
-        dup[1:] = np.all(key[1:] == key[:-1], axis=1) & np.all(fkey[1:] == fkey[:-1], axis=1)
+    dup = torch.zeros(order.numel(), dtype=torch.bool, device=dev)
+    if order.numel() > 1:
+        same = torch.ones(order.numel() - 1, dtype=torch.bool, device=dev)
+        for k in (scen, name_rank, seq, dl, up, down):
+            v = k[order]
+            same &= v[1:] == v[:-1]
+        dup[1:] = same
     order = order[~dup]
     rows_scen = scen[order]
-    row_off = np.zeros(S + 1, dtype=np.int64)
-    np.cumsum(np.bincount(rows_scen, minlength=S), out=row_off[1:])
-    loads = np.stack([solved["dp"]["load"][order], solved["greedy"]["load"][order],
-                      solved["all_server"]["load"][order]], axis=1)
-    norm = segment_means(loads[:, 2], row_off)  # throughput_sim.py:156, numpy-order np.mean
+    row_off = torch.zeros(S + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(torch.bincount(rows_scen, minlength=S), 0, out=row_off[1:])
+    loads = torch.stack([solved["dp"]["load"][order], solved["greedy"]["load"][order],
+                         solved["all_server"]["load"][order]], dim=1)
+    norm = segment_means_device(loads[:, 2].contiguous(), row_off)  # throughput_sim.py:156, numpy-order np.mean
     demand = loads / norm[rows_scen][:, None]
-    return row_off, demand, req["deadline_s"][order]
+    return row_off.cpu().numpy(), demand, dl[order]
+
+
+def lexsort_tensors(keys) -> torch.Tensor:
+    """np.lexsort(keys) (last key primary) of device tensors as successive
+    stable sorts, least significant key first -- the same permutation."""
+    idx = torch.arange(keys[0].numel(), device=keys[0].device)
+    for k in keys:
+        idx = idx[torch.sort(k[idx], stable=True).indices]
+    return idx
 
 
 def lexsort_device(keys, device=None) -> np.ndarray:
-    """np.lexsort(keys) (last key primary) as successive stable sorts on the
-    device, least significant key first -- the same permutation."""
+    """np.lexsort of host arrays, computed on the device."""
     dev = device or N.device()
-    n = len(keys[0])
-    idx = torch.arange(n, device=dev)
-    for k in keys:
-        kt = torch.from_numpy(np.ascontiguousarray(k)).to(dev)
-        idx = idx[torch.sort(kt[idx], stable=True).indices]
-    return idx.cpu().numpy()
+    return lexsort_tensors([torch.from_numpy(np.ascontiguousarray(k)).to(dev) for k in keys]).cpu().numpy()
+
+
+def segment_means_device(values: torch.Tensor, row_off: torch.Tensor) -> torch.Tensor:
+    """np.mean of every CSR segment in numpy's summation order (sp_segment_sum,
+    then / n); NaN for empty segments."""
+    from .evaluator import segment_sums
+    return segment_sums(values, row_off) / (row_off[1:] - row_off[:-1]).to(torch.float64)
 
 
 def segment_means(values: np.ndarray, row_off: np.ndarray) -> np.ndarray:
-    """np.mean of every CSR segment in numpy's summation order (sp_segment_sum
-    on the device, then / n); NaN for empty segments."""
-    from .evaluator import segment_sums
+    """segment_means_device of host arrays."""
     dev = N.device()
     x = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(dev)
     off = torch.from_numpy(np.ascontiguousarray(row_off, dtype=np.int64)).to(dev)
-    sums = segment_sums(x, off).cpu().numpy()
-    with np.errstate(invalid="ignore", divide="ignore"):
-        return sums / np.diff(row_off).astype(np.float64)
+    return segment_means_device(x, off).cpu().numpy()
 
 
 def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORIZON,
@@ -147,13 +158,14 @@ def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORI
 
     req, layer_lists, off = W.cfg4(sids)
     solved = solve_requests(req, layer_lists)
-    row_off, demand, deadline_s = scenario_tables(req, off, W.CFG4_MODELS, solved)
+    row_off, demand_d, dl_d = scenario_tables(req, off, W.CFG4_MODELS, solved)
     S = len(sids)
     sizes = np.diff(row_off)
     capacity = np.zeros(S)
     sim = np.flatnonzero(sizes > 0)
     # throughput_sim.py:172-176: omega x numpy-order mean of the nosplit demands
-    capacity[sim] = float(omega_requests) * segment_means(demand[:, 2], row_off)[sim]
+    mean_ns = segment_means_device(demand_d[:, 2].contiguous(), torch.from_numpy(row_off).to(demand_d.device))
+    capacity[sim] = float(omega_requests) * mean_ns.cpu().numpy()[sim]
 
     max_w = np.zeros((S, 3))
     mean_w = np.zeros((S, 3))
@@ -162,8 +174,7 @@ def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORI
     # the scenario tables live on the device; each run's demand / duration
     # columns are gathered there from the skeleton's table-row indices
     # (throughput_sim.py:189-198: duration = deadline x execution count)
-    demand_d = torch.from_numpy(np.ascontiguousarray(demand)).to(dev)
-    dl_ms_d = torch.from_numpy(deadline_s * 1000.0).to(dev)
+    dl_ms_d = dl_d * 1000.0
     for blk in range(0, len(sim), SIM_BLOCK):
         ids = sim[blk:blk + SIM_BLOCK]
         n = len(ids)
@@ -181,7 +192,7 @@ def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORI
         status[ids] = o["st"][:3 * n].cpu().numpy().reshape(-1, 3)
         del o, arr3, dur3, dem3, arr_d, gidx_d, ex_d
     return MonteCarloResult(sids, sizes, capacity, max_w, mean_w, status, int(off[-1]),
-                            solved["cells"])
+                            float(solved["cells"].item()))
 
 
 def _gather(local, sids, bounds, group) -> MonteCarloResult:

@@ -57,6 +57,31 @@ def _total_flops(layers, seq_len: int) -> int:
     return sum(cm.flop_of_layer(l, int(seq_len)) for l in layers)
 
 
+def _total_flops_many(layers, seqs) -> np.ndarray:
+    """float(_total_flops(layers, s)) for every s in `seqs`: the closed forms
+    of cost_model.flop_of_layer in exact int64 arithmetic (every term and sum
+    stays far below 2^63 for these models), one numpy pass per layer; models
+    with custom (possibly float) entries take the scalar path."""
+    seqs = np.asarray(seqs, dtype=np.int64)
+    if any(l.kind is cm.LayerKind.CUSTOM for l in layers):
+        return np.array([_total_flops(layers, int(x)) for x in seqs], dtype=float)
+    tot = np.zeros(seqs.shape, dtype=np.int64)
+    for l in layers:
+        s, d = np.maximum(1, seqs // l.seq_divisor), int(l.hidden_dim)
+        k = l.kind
+        if k is cm.LayerKind.ATTENTION:
+            tot += 8 * s * d * d + 4 * s * s * d + cm.SOFTMAX_FLOPS_PER_SCORE * s * s * int(l.heads)
+        elif k is cm.LayerKind.FEED_FORWARD:
+            tot += 4 * s * d * int(l.ffn_dim)
+        elif k is cm.LayerKind.LAYER_NORM:
+            tot += 5 * s * d
+        elif k is cm.LayerKind.EMBEDDING:
+            tot += 2 * s * d
+        else:  # classifier
+            tot += 2 * s * d * int(l.out_dim)
+    return tot.astype(np.float64)
+
+
 def _requests(model, seq, cfps, sfps, up, down, deadline, unit, flags=SOURCE_CLIENT) -> dict:
     n = len(seq)
     full = lambda v: np.full(n, v, dtype=np.float64) if np.isscalar(v) else np.asarray(v, np.float64)
@@ -129,17 +154,11 @@ def cfg4_scenario(sid: int) -> tuple[int, int, int]:
     return (sid // 16) % 16, sid % 16, sid // 256
 
 
-def _cfg4_mix(mix: int, layer_lists, flop_cache: dict):
+def _cfg4_mix(mix: int):
     rng = np.random.default_rng(1_000_003 * mix + 4)
     m = rng.integers(0, len(CFG4_MODELS), CFG4_REQUESTS)
     s = np.rint(2.0 ** rng.uniform(7, 12, CFG4_REQUESTS)).astype(np.int64)
-    f = np.empty(CFG4_REQUESTS)
-    for k, (mi, si) in enumerate(zip(m, s)):
-        key = (int(mi), int(si))
-        if key not in flop_cache:
-            flop_cache[key] = _total_flops(layer_lists[mi], si)
-        f[k] = flop_cache[key]
-    return m, s, f
+    return m, s
 
 
 def cfg4(scenarios=None) -> tuple[dict, list, np.ndarray]:
@@ -153,11 +172,16 @@ def cfg4(scenarios=None) -> tuple[dict, list, np.ndarray]:
     sids = np.arange(16 * 16 * CFG4_MIXES) if scenarios is None else np.asarray(scenarios, dtype=np.int64)
     layer_lists = [model_layers(m) for m in CFG4_MODELS]
     a, b, mix = (sids // 16) % 16, sids % 16, sids // 256
-    cache: dict = {}
-    mixes = {int(x): _cfg4_mix(int(x), layer_lists, cache) for x in np.unique(mix)}
-    M = np.stack([mixes[int(x)][0] for x in mix])
-    S = np.stack([mixes[int(x)][1] for x in mix])
-    F = np.stack([mixes[int(x)][2] for x in mix])
+    uniq, inv = np.unique(mix, return_inverse=True)
+    drawn = [_cfg4_mix(int(x)) for x in uniq]
+    um, us = np.stack([d[0] for d in drawn]), np.stack([d[1] for d in drawn])
+    # total FLOPs of every (model, seq) pair the mixes draw, once per pair
+    uf = np.empty(um.shape)
+    for mi in range(len(CFG4_MODELS)):
+        sel = um == mi
+        vals, back = np.unique(us[sel], return_inverse=True)
+        uf[sel] = _total_flops_many(layer_lists[mi], vals)[back]
+    M, S, F = um[inv], us[inv], uf[inv]
     dl = CFG4_SCALES[a][:, None] * F / cfps
     bw = np.repeat(CFG4_BANDWIDTHS[b], CFG4_REQUESTS)
     off = np.arange(len(sids) + 1, dtype=np.int64) * CFG4_REQUESTS
