@@ -510,14 +510,16 @@ def main():
     # its own workspace) before step k is collected (PendingSolve.result), so
     # the host's launch work overlaps the device's; every step still solves
     # its whole batch and is collected inside the timed region.
-    ws_pair = []
+    # two pipeline slots (workspace, cost table, policies), allocated once:
+    # no allocation inside the timed loops
+    slots = []
 
     def run_device(steps: int):
-        if not ws_pair:
-            ws_pair.extend([N.workspace(), torch.empty_like(N.workspace())])
+        if not slots:
+            slots.extend(engine.solve_slot(n, total_layers, N.workspace().numel()) for _ in range(2))
         prev = None
         for k in range(steps + 1):
-            cur = engine.solve_async(dev_req, total_layers, off, ws=ws_pair[k & 1]) if k < steps else None
+            cur = engine.solve_async(dev_req, total_layers, off, slot=slots[k & 1]) if k < steps else None
             if prev is not None:
                 s = prev.result()
                 if world > 1:
@@ -526,20 +528,33 @@ def main():
 
     host_out = [None, None, None]  # pinned result buffers, reused round-robin
 
+    phase_log = [] if os.environ.get("SPLITPLAN_BENCH_TRACE") == "phases" else None
+
+    req_dev = [None, None]  # the device copies of the request parameters, one per slot
+
     def run_e2e(steps: int):
-        if not ws_pair:
-            ws_pair.extend([N.workspace(), torch.empty_like(N.workspace())])
+        if not slots:
+            slots.extend(engine.solve_slot(n, total_layers, N.workspace().numel()) for _ in range(2))
         prev, s, out = None, None, None
         for k in range(steps + 1):
+            t = [time.perf_counter()]
             cur = None
             if k < steps:
-                cur = engine.solve_async(host_req.to(dev, non_blocking=True), total_layers, off,
-                                         ws=ws_pair[k & 1])
+                if req_dev[k & 1] is None:
+                    req_dev[k & 1] = host_req.to(dev, non_blocking=True)
+                else:  # the same single host-to-device copy into the slot's buffer
+                    req_dev[k & 1]._buf.copy_(host_req._buf, non_blocking=True)
+                cur = engine.solve_async(req_dev[k & 1], total_layers, off, slot=slots[k & 1])
+            t.append(time.perf_counter())
             if prev is not None:
                 s = prev.result()
+                t.append(time.perf_counter())
                 pol = gather_policies(s.policies, s.layer_off)[0] if world > 1 else s.policies
                 # one packed device-to-host copy of the placements and records
                 out = host_out[k % 3] = pol.to_host_async(into=host_out[k % 3])
+            t.append(time.perf_counter())
+            if phase_log is not None:
+                phase_log.append([round((b - a) * 1e3, 3) for a, b in zip(t, t[1:])])
             prev = cur
         return s, out
 
@@ -586,16 +601,18 @@ def main():
     trace = os.environ.get("SPLITPLAN_BENCH_TRACE")
     tw = []
     e0.record(stream)
-    if trace:
+    if trace and phase_log is None:
         for _ in range(args.steps):
             tw.append(time.perf_counter())
             s, out = step_e2e()
     else:
         s, out = run_e2e(args.steps)
     e1.record(stream)
-    if trace:
+    if trace and phase_log is None:
         tw.append(time.perf_counter())
         print("e2e step wall ms:", [round((b - a) * 1e3, 3) for a, b in zip(tw, tw[1:])], file=sys.stderr)
+    if phase_log is not None:
+        print("e2e phases ms (queue, result, copy):", phase_log, file=sys.stderr)
     barrier()
     e2e_ms = e0.elapsed_time(e1)
     d2h = out._buf.numel()

@@ -206,8 +206,18 @@ class PendingPlan:
             rc = N.library().sp_plan_dp_finish(self.s, self.o, N.ptr(self.ws), self.ws.numel(), N.stream_ptr(),
                                                N.ptr(self.pend))
             self.done = True
+            _PEND_FREE.append(self.pend)  # its record is consumed: reusable
             N.check(rc, "sp_plan_dp_finish")
         return self.out
+
+
+# pinned pending records of sp_plan_dp_async, reused: a pinned allocation
+# inside a pipelined loop can stall the host for milliseconds (page pinning)
+_PEND_FREE: list = []
+
+
+def _pending_record() -> torch.Tensor:
+    return _PEND_FREE.pop() if _PEND_FREE else torch.empty(N.SP_PENDING_BYTES, dtype=torch.uint8, pin_memory=True)
 
 
 def plan_dp_async(batch: InstanceBatch, out: PolicyBatch | None = None,
@@ -219,12 +229,13 @@ def plan_dp_async(batch: InstanceBatch, out: PolicyBatch | None = None,
     take the batch in `ws`."""
     out = out or PolicyBatch.empty(batch.n, batch.total_layers, batch.r.device)
     ws = N.workspace() if ws is None else ws
-    pend = torch.empty(N.SP_PENDING_BYTES, dtype=torch.uint8, pin_memory=True)
+    pend = _pending_record()
     s, o = batch.struct(), out.struct()
     rc = N.library().sp_plan_dp_async(s, o, N.ptr(ws), ws.numel(), N.stream_ptr(), N.ptr(pend))
     if rc == N.SP_ERR_WORKSPACE:
+        _PEND_FREE.append(pend)
         plan_dp(batch, out)
-        return PendingPlan(batch, out, ws, pend, s, o, True)
+        return PendingPlan(batch, out, ws, _pending_record(), s, o, True)
     N.check(rc, "sp_plan_dp_async")
     return PendingPlan(batch, out, ws, pend, s, o, False)
 

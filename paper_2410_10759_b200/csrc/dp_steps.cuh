@@ -55,8 +55,10 @@
 //
 // Store of one instance (read by the walk): (L+1) rows x {C, S}, each a count
 // and CAP int2 {column, stay_from}, at a position the kernel computes itself
-// -- (layer_off[k] + k) * steps_row_pair_bytes(CAP) -- in the device-planned
-// tier (no host planning), or at DpWork::bp_off in the wave path:
+// -- (layer_off[k] + k - pos0) * steps_row_pair_bytes(CAP) -- in the
+// device-planned tier (no host planning; a batch whose stores do not fit the
+// workspace runs in waves of consecutive instances), or at DpWork::bp_off in
+// the host-planned path:
 //   cnt int32[(L+1) * 2] (padded to 16 B) | ent int2[(L+1) * 2][CAP]
 #pragma once
 
@@ -95,6 +97,8 @@ struct StepsArgs {
   int32_t* overflow;           // wave path: [n] 1 = a row exceeded CAP
   int32_t* idx;                // [total_layers] scratch of _finish for instances too long for shared memory
   int64_t n_items;
+  int64_t item0, pos0;         // device path: instances [item0, item0 + n_items); store of instance k at
+                               // (layer_off[k] + k - pos0) row pairs (pos0 = layer_off[item0] + item0)
   int64_t max_cols;            // device path: wider instances are left to the dense kernels
   int64_t min_cols[2];         // device path, [int32, fp64 domain]: narrower ones too (one CTA's SMEM holds them)
   int32_t walk;                // 1: walk back and finish every solved instance (the policies below)
@@ -105,7 +109,7 @@ struct StepsArgs {
 template <int CAP>
 __device__ __forceinline__ uint8_t* steps_store_of(const StepsArgs& a, int64_t item, int64_t inst) {
   return a.work ? a.store + a.work[item].bp_off
-                : a.store + (size_t)(a.layer_off[inst] + inst) * steps_row_pair_bytes(CAP);
+                : a.store + (size_t)(a.layer_off[inst] + inst - a.pos0) * steps_row_pair_bytes(CAP);
 }
 
 constexpr uint32_t kFull = 0xffffffffu;
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
   const int h = lane >> 4, g = lane & 15;
   const int64_t item = (int64_t)blockIdx.x * WPB + warp;
   if (item >= a.n_items) return;  // whole warps leave together
-  const int64_t inst = a.work ? a.work[item].inst : item;
+  const int64_t inst = a.work ? a.work[item].inst : a.item0 + item;
   const InstInfo inf = a.info[inst];
   if (!a.work && (inf.mode != MODE || inf.w_eff + 1 >= a.max_cols ||
                   inf.w_eff + 1 < a.min_cols[MODE == VM_INT32 ? 0 : 1]))

@@ -34,13 +34,17 @@
 #include <stdint.h>
 #include <math.h>
 
+// (SP_DT: functions that read the ziggurat tables -- device-only under nvcc,
+// where the tables live in device memory)
 #ifdef __CUDACC__
 #define SP_HD __host__ __device__ __forceinline__
+#define SP_DT __device__ __forceinline__
 #ifndef SP_ZIG_QUAL
 #define SP_ZIG_QUAL __device__ const
 #endif
 #else
 #define SP_HD inline
+#define SP_DT inline
 #ifndef SP_ZIG_QUAL
 #define SP_ZIG_QUAL static const
 #endif
@@ -269,7 +273,7 @@ SP_HD double glibc_log1p(double x) {
 // ---------------------------------------------------------------------------
 // distributions (numpy/random/src/distributions/distributions.c)
 
-SP_HD double standard_exponential(Pcg64& g) {
+SP_DT double standard_exponential(Pcg64& g) {
   for (;;) {
     uint64_t ri = next_u64(g);
     ri >>= 3;

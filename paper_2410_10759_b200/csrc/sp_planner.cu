@@ -727,7 +727,16 @@ int64_t smem_max_cols(int mode) {
   return lo;
 }
 // narrowest row the breakpoint lists take (all of them when forced)
-int64_t steps_min_cols(int mode, int force) { return force == DPV_STEPS ? 0 : smem_max_cols(mode) + 1; }
+// (rows of a few thousand columns already take ~30x fewer breakpoints than
+// columns on model-derived instances: the lists beat the SMEM kernel there,
+// profiles/r02/tier0/; SPLITPLAN_STEPS_MIN_COLS moves the threshold)
+constexpr int64_t kStepsMinCols = 1024;
+int64_t steps_min_cols(int mode, int force) {
+  (void)mode;
+  if (force == DPV_STEPS) return 0;
+  const int v = env_int("SPLITPLAN_STEPS_MIN_COLS", -1);
+  return v >= 0 ? v : kStepsMinCols;
+}
 
 // steps_eligible: the breakpoint-list kernels may take the instance: rows
 // wider than one SM's shared memory (where the dense alternative is the
@@ -837,14 +846,17 @@ __host__ __device__ inline int64_t t0_row_words(int mode, int cfg, int64_t ncol)
   return (cols + 31) / 32 * bp_words(mode);
 }
 // class and back-pointer bytes of instance k (class -1: not tier 0)
+// (skip: the query's stand-in for tier 1's flags -- rows in [skip[mode], skip[2])
+// outside the NaN domain are tier 1's)
 __device__ __forceinline__ int t0_classify(const sp_instances& in, const InstInfo* info, const int32_t* flag,
-                                           int64_t max_i32, int64_t max_f64, int64_t k, int64_t& ncol,
-                                           unsigned long long& bytes, unsigned long long& cells) {
+                                           int64_t max_i32, int64_t max_f64, const int64_t* skip, int64_t k,
+                                           int64_t& ncol, unsigned long long& bytes, unsigned long long& cells) {
   const InstInfo inf = info[k];
   ncol = inf.w_eff + 1;
   const int64_t L = in.layer_off[k + 1] - in.layer_off[k];
   bytes = cells = 0;
   if ((flag && !flag[k]) || L <= 0 || ncol > (inf.mode == VM_INT32 ? max_i32 : max_f64)) return -1;
+  if (inf.mode != VM_F64_NAN && ncol < skip[2] && ncol >= skip[inf.mode == VM_INT32 ? 0 : 1]) return -1;
   const int c = t0_class_of(ncol, inf.mode);
   bytes = align_up((size_t)L * (size_t)t0_row_words(inf.mode, t0_class_cfg(c), ncol) * 4, 256);
   cells = (unsigned long long)L * (unsigned long long)ncol;
@@ -853,9 +865,13 @@ __device__ __forceinline__ int t0_classify(const sp_instances& in, const InstInf
 
 // one thread per instance: per-block class counts, cells and back-pointer
 // bytes (the host cuts waves at block boundaries), global widest row per class
+struct T0Skip {
+  int64_t v[3];  // [lo int32, lo fp64, hi]; hi = 0: nothing skipped
+};
 __global__ void __launch_bounds__(kT0Block) t0_count_kernel(sp_instances in, const InstInfo* info,
                                                             const int32_t* flag, int64_t max_i32, int64_t max_f64,
-                                                            uint8_t* cls, T0Stats* stats, T0Block* blocks) {
+                                                            T0Skip skip, uint8_t* cls, T0Stats* stats,
+                                                            T0Block* blocks) {
   __shared__ uint32_t s_cnt[kT0Classes];
   __shared__ unsigned long long s_cells[kT0Classes], s_max[kT0Classes], s_bytes;
   if (threadIdx.x < kT0Classes) {
@@ -869,7 +885,7 @@ __global__ void __launch_bounds__(kT0Block) t0_count_kernel(sp_instances in, con
   if (k < in.n) {
     int64_t ncol;
     unsigned long long bytes, cells;
-    const int c = t0_classify(in, info, flag, max_i32, max_f64, k, ncol, bytes, cells);
+    const int c = t0_classify(in, info, flag, max_i32, max_f64, skip.v, k, ncol, bytes, cells);
     cls[k] = c < 0 ? 255 : (uint8_t)c;
     if (c >= 0) {
       atomicAdd(&s_cnt[c], 1u);
@@ -1562,7 +1578,12 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   const bool steps_allowed = tab_c == nullptr && (force < 0 || force == DPV_STEPS);
   const bool steps_ok = steps_allowed && !q_min;
   const int grid = (int)std::min<int64_t>((n + kPrepWarps - 1) / kPrepWarps, 1 << 20);
-  const bool tier1_fits = steps_ok && out && fixed + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap) <= ws_bytes;
+  // tier 1 in one launch when every instance's store fits the workspace, else
+  // (not in an asynchronous call) in waves of consecutive instances
+  const size_t rpb = steps_row_pair_bytes(kStepsCap);
+  const bool tier1_one = steps_ok && out && fixed + (size_t)(total + n) * rpb <= ws_bytes;
+  const bool tier1_fits = tier1_one || (steps_ok && out && !begin && !resume && fixed + 64 * rpb <= ws_bytes &&
+                                        env_int("SPLITPLAN_NO_TIER1_WAVES", 0) == 0);
   const int64_t lo_i32 = steps_min_cols(VM_INT32, force), lo_f64 = steps_min_cols(VM_F64, force);
   // tier 0 (the SMEM kernel's instances, planned on the device): the default
   // kernel choice only (no forced variant or configuration), not for the
@@ -1580,15 +1601,21 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     if (rc) return rc;
   }
   uint8_t* dyn = (uint8_t*)ws + fixed;
-  if (t0_count) {  // classify and count (the totals travel with the next synchronisation)
-    rc = check_cuda(cudaMemsetAsync(t0s, 0, sizeof(T0Stats), st), "zero tier-0 counters");
-    if (rc) return rc;
+  // tier-0 classification and counts, queued after tier 1 (the instances it
+  // left keep their flag); the totals travel with the next synchronisation
+  bool t0_counted = false;
+  auto launch_t0_count = [&]() -> int {
+    if (!t0_count || t0_counted) return SP_OK;
+    t0_counted = true;
+    int r = check_cuda(cudaMemsetAsync(t0s, 0, sizeof(T0Stats), st), "zero tier-0 counters");
+    if (r) return r;
+    T0Skip skip = {{0, 0, 0}};
+    if (q_min && steps_allowed) skip = T0Skip{{lo_i32, lo_f64, kGridMinColsSteps}};
     t0_count_kernel<<<(unsigned)t0_nblk, kT0Block, 0, st>>>(*in, info, (steps_ok || t0_allowed) ? flag : nullptr,
-                                                           smem_max_cols(VM_INT32), smem_max_cols(VM_F64), t0cls,
-                                                           t0s, t0blk);
-    rc = launch_check("t0_count_kernel launch");
-    if (rc) return rc;
-  }
+                                                           smem_max_cols(VM_INT32), smem_max_cols(VM_F64), skip,
+                                                           t0cls, t0s, t0blk);
+    return launch_check("t0_count_kernel launch");
+  };
   T0Stats ht0 = {};
   std::vector<T0Block> hblk;
   bool ht0_valid = false;
@@ -1640,8 +1667,37 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
       }
-      if (!rc) rc = launch_steps(VM_INT32, kStepsCap, sa, in, out, idx, st);
-      if (!rc) rc = launch_steps(VM_F64, kStepsCap, sa, in, out, idx, st);
+      if (tier1_one) {
+        sa.item0 = 0;
+        sa.pos0 = 0;
+        if (!rc) rc = launch_steps(VM_INT32, kStepsCap, sa, in, out, idx, st);
+        if (!rc) rc = launch_steps(VM_F64, kStepsCap, sa, in, out, idx, st);
+      } else if (!rc) {
+        // waves: consecutive instances whose stores fit (an instance alone too
+        // large for the workspace keeps its flag for the next tiers)
+        std::vector<int64_t> ho(n + 1);
+        rc = check_cuda(cudaMemcpyAsync(ho.data(), in->layer_off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost,
+                                        st),
+                        "copy layer offsets");
+        if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync for tier-1 waves");
+        const size_t avail1 = ws_bytes - fixed;
+        int64_t i0 = 0;
+        while (!rc && i0 < n) {
+          int64_t i1 = i0;
+          while (i1 < n && (size_t)(ho[i1 + 1] - ho[i0] + (i1 + 1 - i0)) * rpb <= avail1) ++i1;
+          if (i1 == i0) {
+            ++i0;
+            continue;
+          }
+          sa.item0 = i0;
+          sa.pos0 = ho[i0] + i0;
+          sa.n_items = i1 - i0;
+          rc = launch_steps(VM_INT32, kStepsCap, sa, in, out, idx, st);
+          if (!rc) rc = launch_steps(VM_F64, kStepsCap, sa, in, out, idx, st);
+          trace("tier-1 wave", (long long)(i1 - i0));
+          i0 = i1;
+        }
+      }
       if (!rc && e1) cudaEventRecord(e1, st);
       if (!rc && begin) {  // asynchronous: the counters travel to the caller's pinned buffer
         rc = check_cuda(cudaMemcpyAsync(begin->solved, solved, sizeof(hsolved), cudaMemcpyDeviceToHost, st),
@@ -1654,6 +1710,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       if (!rc)
         rc = check_cuda(cudaMemcpyAsync(hsolved, solved, sizeof(hsolved), cudaMemcpyDeviceToHost, st),
                         "copy solved count");
+      if (!rc) rc = launch_t0_count();
       if (!rc && t0_ok) rc = copy_t0();
       if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync after breakpoint lists");
       if (rc) return rc;
@@ -1673,10 +1730,12 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   // counting blocks whose back-pointer tables fit after tier 1's store
   unsigned long long t0_taken = 0;
   size_t t0_peak = 0;
-  const size_t region0 = tier1 ? align_up((size_t)(total + n) * steps_row_pair_bytes(kStepsCap), 256) : 0;
+  // (tier 1's stores are dead once its kernels are: their walk is fused)
+  const size_t region0 = 0;
   std::vector<uint8_t> hcls;  // the query: tier-0 classes (255: a host-planned tier's instance)
-  if (t0_count && !ht0_valid) {
-    rc = copy_t0();
+  if (t0_count && !ht0_valid && tier1_solved < (unsigned long long)n) {
+    rc = launch_t0_count();
+    if (!rc) rc = copy_t0();
     if (!rc && q_min) {
       hcls.resize(n);
       rc = check_cuda(cudaMemcpyAsync(hcls.data(), t0cls, n, cudaMemcpyDeviceToHost, st), "copy tier-0 classes");
@@ -1684,7 +1743,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
     if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync after tier-0 count");
     if (rc) return rc;
   }
-  if (t0_ok) {
+  if (t0_ok && ht0_valid) {
     uint8_t* base0 = dyn + region0;
     const size_t avail0 = ws_bytes > fixed + region0 ? ws_bytes - fixed - region0 : 0;
     bool fits = true;
@@ -1785,7 +1844,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   if (tier1_solved + t0_taken == (unsigned long long)n) {
     unsigned long long t0_all = 0;
     for (const T0Block& b : hblk) t0_all += b.bytes;
-    set_full_workspace(fixed + region0 + (size_t)t0_all);
+    set_full_workspace(fixed + std::max((size_t)t0_all, tier1 ? (size_t)(total + n) * rpb : (size_t)0));
     set_steps_overflow(0);
     return SP_OK;
   }
@@ -1906,7 +1965,7 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       mn = std::max(mn, (size_t)b.bytes);
     }
     *q_min = fixed + mn;
-    *q_full = fixed + std::max(full + tier1 + t0_all, mn);
+    *q_full = fixed + std::max(std::max(full, tier1), std::max((size_t)t0_all, mn));
     if (q_part_min) *q_part_min = pmn;
     if (q_part_full) *q_part_full = pfull;
     return SP_OK;

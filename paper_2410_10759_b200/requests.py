@@ -106,16 +106,23 @@ class Engine:
                                                      N.stream_ptr()), "sp_request_layer_offsets")
         return off
 
-    def cost_table(self, req: RequestBatch, total_layers: int, off: torch.Tensor | None = None):
-        dev = self.device
+    def cost_buffers(self, n: int, total_layers: int) -> dict:
+        """The cost table's outputs for n requests / total_layers entries in
+        ONE device allocation (views by name); reusable across calls."""
+        T = int(total_layers)
+        spec = [(k, T, torch.float64) for k in ("r", "cs", "ss", "up", "dn")]
+        spec += [(k, T, torch.int64) for k in ("i", "s", "u", "d")]
+        spec += [("budget", n, torch.int64), ("sac", n, torch.uint8), ("status", n, torch.int32)]
+        return N.packed(spec, self.device)[1]
+
+    def cost_table(self, req: RequestBatch, total_layers: int, off: torch.Tensor | None = None,
+                   bufs: dict | None = None):
         off = self.layer_offsets(req) if off is None else off
         T = int(total_layers)
-        f = {k: torch.empty(T, dtype=torch.float64, device=dev)
-             for k in ("r", "cs", "ss", "up", "dn")}
-        i = {k: torch.empty(T, dtype=torch.int64, device=dev) for k in ("i", "s", "u", "d")}
-        budget = torch.empty(req.n, dtype=torch.int64, device=dev)
-        sac = torch.empty(req.n, dtype=torch.uint8, device=dev)
-        status = torch.empty(req.n, dtype=torch.int32, device=dev)
+        v = bufs if bufs is not None else self.cost_buffers(req.n, T)
+        f = {k: v[k] for k in ("r", "cs", "ss", "up", "dn")}
+        i = {k: v[k] for k in ("i", "s", "u", "d")}
+        budget, sac, status = v["budget"], v["sac"], v["status"]
         tab = N.SpCostTable(N.ptr(off).value, T, N.ptr(f["r"]).value, N.ptr(f["cs"]).value, None,
                             None, N.ptr(f["ss"]).value, N.ptr(f["up"]).value, N.ptr(f["dn"]).value,
                             N.ptr(i["i"]).value, N.ptr(i["s"]).value, N.ptr(i["u"]).value,
@@ -126,16 +133,27 @@ class Engine:
         inst = B.InstanceBatch(off, i["i"], i["s"], i["u"], i["d"], f["r"], budget, sac)
         return inst, status, f
 
+    def solve_slot(self, n: int, total_layers: int, ws_bytes: int) -> dict:
+        """Everything one solve_async call writes -- workspace, cost table,
+        policies -- allocated once, for a pipelined caller to reuse (no
+        allocation inside its loop)."""
+        return dict(ws=torch.empty(ws_bytes, dtype=torch.uint8, device=self.device),
+                    cost=self.cost_buffers(n, total_layers),
+                    pol=B.PolicyBatch.empty(n, int(total_layers), self.device))
+
     def solve_async(self, req: RequestBatch, total_layers: int | None = None, off: torch.Tensor | None = None,
-                    ws: torch.Tensor | None = None) -> "PendingSolve":
+                    ws: torch.Tensor | None = None, slot: dict | None = None) -> "PendingSolve":
         """`solve` without a stream synchronisation (sp_plan_dp_async): the
         whole chain is queued and the call returns; PendingSolve.result()
         completes it.  A caller pipelines batches by queueing the next one
-        before collecting this one, each in flight with its own workspace."""
+        before collecting this one, each in flight with its own workspace --
+        or its own `slot` (solve_slot: workspace and every output reused; the
+        results of a slot are valid until the slot is queued again)."""
         if total_layers is None:
             total_layers = int(self.n_layers[req.model.cpu().numpy()].sum())
-        inst, status, f = self.cost_table(req, total_layers, off)
-        return PendingSolve(B.plan_dp_async(inst, ws=ws), inst, status, f)
+        inst, status, f = self.cost_table(req, total_layers, off, bufs=slot["cost"] if slot else None)
+        pend = B.plan_dp_async(inst, out=slot["pol"] if slot else None, ws=slot["ws"] if slot else ws)
+        return PendingSolve(pend, inst, status, f)
 
     def solve(self, req: RequestBatch, total_layers: int | None = None,
               off: torch.Tensor | None = None) -> Solved:

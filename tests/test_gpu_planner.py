@@ -580,12 +580,14 @@ def _tier0_instances(seed, n):
     return out
 
 
-@pytest.mark.parametrize("waves", ["one", "several"])
-def test_tier0_device_planned_waves(gpu, waves, capfd, monkeypatch):
-    """1,300 narrow instances (six counting blocks) over every tier-0 class,
-    run by the device-planned SMEM tier in one wave, and in several waves of
-    a workspace holding about a third of their back-pointer tables; every
-    placement bit-exact against the oracle."""
+@pytest.mark.parametrize("case", ["tier0_one", "tier0_several", "tier1_several"])
+def test_device_planned_tiers_in_waves(gpu, case, capfd, monkeypatch):
+    """1,300 narrow instances (six counting blocks) over every tier-0 class:
+    the device-planned SMEM tier (breakpoint lists held back) in one wave and
+    in several waves of a workspace holding about a third of their
+    back-pointer tables; and the default split -- tier 1 (breakpoint lists)
+    in waves of consecutive instances, tier 0 for the narrowest rows.  Every
+    placement bit-exact against the oracle, nothing left to host planning."""
     import torch
     from paper_2410_10759_b200 import _native as N, batch as B
     insts = _tier0_instances(29, 1300)
@@ -595,8 +597,11 @@ def test_tier0_device_planned_waves(gpu, waves, capfd, monkeypatch):
     b = B.InstanceBatch.from_arrays(off, cat("i"), cat("s"), cat("u"), cat("d"), cat("r"),
                                     [x["budget"] for x in insts], [x["sac"] for x in insts])
     lib = N.library()
+    if case.startswith("tier0"):  # breakpoint lists held back
+        monkeypatch.setenv("SPLITPLAN_STEPS_MIN_COLS", str(1 << 30))
+        monkeypatch.setenv("SPLITPLAN_NO_TIER1_WAVES", "1")
     mn, full = B.dp_workspace_bytes(b)
-    size = full + (1 << 20) if waves == "one" else mn + (full - mn) // 3
+    size = full + (1 << 20) if case == "tier0_one" else mn + (full - mn) // 3
     ws = torch.empty(size, dtype=torch.uint8, device=N.device())
     out = B.PolicyBatch.empty(b.n, b.total_layers, b.r.device)
     monkeypatch.setenv("SPLITPLAN_TRACE", "1")
@@ -604,12 +609,17 @@ def test_tier0_device_planned_waves(gpu, waves, capfd, monkeypatch):
     assert rc == 0, lib.sp_last_error()
     host = out.to_host()
     err = capfd.readouterr().err
-    n_waves = err.count("tier-0 wave")
-    assert n_waves == 1 if waves == "one" else n_waves >= 2, err[-2000:]
+    t0, t1 = err.count("tier-0 wave"), err.count("tier-1 wave")
+    if case == "tier0_one":
+        assert t0 == 1 and t1 == 0, err[-2000:]
+    elif case == "tier0_several":
+        assert t0 >= 2 and t1 == 0, err[-2000:]
+    else:
+        assert t1 >= 2 and t0 >= 1, err[-2000:]
     assert "items planned" not in err  # nothing left for the host-planned tiers
     for k, inst in enumerate(insts):
         exp = O.plan_dp(inst)
         got = dict(pi=host["pi"][off[k]:off[k + 1]], client_value=host["client_value"][k],
                    server_load=host["server_load"][k], integer_latency=host["integer_latency"][k],
                    feasible=host["feasible"][k])
-        assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"tier0 {waves}[{k}]")
+        assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{case}[{k}]")
