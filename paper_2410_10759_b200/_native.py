@@ -159,7 +159,9 @@ def library() -> C.CDLL:
             if not Path(LIB).exists():
                 raise RuntimeError(f"splitplan-b200 CUDA library missing at {LIB}; "
                                    "run __graft_entry__.build() first")
-            lib = C.CDLL(str(LIB))
+            # SPLITPLAN_LIB: an alternative build of the same library (A/B
+            # measurements of compile-time variants; tools only)
+            lib = C.CDLL(os.environ.get("SPLITPLAN_LIB") or str(LIB))
             for name, (res, args) in SIGNATURES.items():
                 fn = getattr(lib, name, None)
                 if fn is None:
@@ -242,6 +244,31 @@ def packed(specs, device=None, pin: bool = False, zero_prefix: int = 0):
         _name, numel, dt = specs[zero_prefix - 1]
         buf[:offs[zero_prefix - 1] + int(numel) * dt.itemsize].zero_()
     return buf, views
+
+
+def packed_upload(specs, arrays: dict, device) -> dict:
+    """Host arrays -> device views of ONE allocation, with ONE host-to-device
+    copy (a call with a handful of small arrays costs one copy instead of one
+    per array).  `specs` as for `packed`; `arrays[name]` array-likes."""
+    offs, o = [], 0
+    for _name, numel, dt in specs:
+        o = (o + 255) & ~255
+        offs.append(o)
+        o += int(numel) * dt.itemsize
+    h = np.empty(max(o, 1), dtype=np.uint8)  # staged with numpy: a few us per array
+    for (name, numel, dt), off in zip(specs, offs):
+        src = arrays[name]
+        if isinstance(src, torch.Tensor):
+            src = src.cpu().numpy()
+        h[off:off + int(numel) * dt.itemsize].view(_NP_OF[dt])[:] = src
+    dbuf = torch.from_numpy(h).to(device)
+    out = {name: dbuf[off:off + int(numel) * dt.itemsize].view(dt) for (name, numel, dt), off in zip(specs, offs)}
+    out["_buf"] = dbuf
+    return out
+
+
+_NP_OF = {torch.int64: np.int64, torch.int32: np.int32, torch.float64: np.float64, torch.uint8: np.uint8,
+          torch.int8: np.int8}
 
 
 _ws: dict[int, torch.Tensor] = {}

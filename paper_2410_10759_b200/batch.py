@@ -50,14 +50,26 @@ class InstanceBatch:
 
     @classmethod
     def from_arrays(cls, layer_off, i, s, u, d, r, budget, sac, must=None) -> "InstanceBatch":
+        """Host arrays -> one device allocation, one host-to-device copy."""
         dev = N.device()
         lo = np.asarray(layer_off, dtype=np.int64)
-        return cls(N.to_dev(lo, torch.int64, dev), N.to_dev(i, torch.int64, dev),
-                   N.to_dev(s, torch.int64, dev), N.to_dev(u, torch.int64, dev),
-                   N.to_dev(d, torch.int64, dev), N.to_dev(r, torch.float64, dev),
-                   N.to_dev(budget, torch.int64, dev), N.to_dev(sac, torch.uint8, dev),
-                   None if must is None else N.to_dev(must, torch.int8, dev),
-                   np.diff(lo))
+        n, T = lo.size - 1, int(lo[-1]) if lo.size else 0
+        spec = [("layer_off", n + 1, torch.int64)] + [(k, T, torch.int64) for k in ("i", "s", "u", "d")]
+        spec += [("r", T, torch.float64), ("budget", n, torch.int64), ("sac", n, torch.uint8)]
+        arrays = dict(layer_off=lo, i=np.asarray(i, np.int64), s=np.asarray(s, np.int64),
+                      u=np.asarray(u, np.int64), d=np.asarray(d, np.int64), r=np.asarray(r, np.float64),
+                      budget=np.asarray(budget, np.int64), sac=np.asarray(sac, np.uint8))
+        if must is not None:
+            spec.append(("must", n, torch.int8))
+            arrays["must"] = np.asarray(must, np.int8)
+        for name, numel, _dt in spec:
+            if np.size(arrays[name]) != numel:
+                raise ValueError(f"{name}: {np.size(arrays[name])} values, expected {numel}")
+        v = N.packed_upload(spec, arrays, dev)
+        out = cls(v["layer_off"], v["i"], v["s"], v["u"], v["d"], v["r"], v["budget"], v["sac"],
+                  v.get("must"), np.diff(lo))
+        out._buf = v["_buf"]
+        return out
 
     @classmethod
     def from_problems(cls, problems, must_end_at=None) -> "InstanceBatch":
@@ -138,6 +150,15 @@ class PolicyBatch:
                             N.ptr(self.feasible).value, N.ptr(self.status).value)
 
     def to_host(self) -> dict:
+        buf = getattr(self, "_buf", None)
+        if buf is not None and buf.device.type != "cpu":  # one device-to-host copy
+            hbuf = buf.cpu()
+            base = buf.data_ptr()
+            view = lambda t: hbuf[t.data_ptr() - base: t.data_ptr() - base + t.numel() * t.element_size()] \
+                .view(t.dtype).numpy()
+            return dict(pi=view(self.pi), client_value=view(self.client_value), server_load=view(self.server_load),
+                        integer_latency=view(self.integer_latency), feasible=view(self.feasible).astype(bool),
+                        status=view(self.status))
         return dict(pi=self.pi.cpu().numpy(), client_value=self.client_value.cpu().numpy(),
                     server_load=self.server_load.cpu().numpy(),
                     integer_latency=self.integer_latency.cpu().numpy(),

@@ -322,11 +322,21 @@ __device__ __forceinline__ void finish_policy_warp(const sp_instances& in, int64
 }
 
 // entries per instance in shared memory: rows [C|S] + the two merges'
-// events [2][2 CAP]
-constexpr int kStepsArrays = 6;
+// events [2][EV x CAP] (EV = 2 holds any merge of two rows of CAP; EV = 1
+// halves the footprint, a merge of more than CAP events overflows to the next
+// tier; the wide tier keeps 2)
+#ifndef SP_STEPS_EV
+#define SP_STEPS_EV 2
+#endif
+#ifndef SP_STEPS_MINB
+#define SP_STEPS_MINB 8
+#endif
+template <int CAP> __host__ __device__ constexpr int steps_ev() { return CAP >= 1024 ? 2 : SP_STEPS_EV; }
+template <int CAP> __host__ __device__ constexpr int steps_arrays() { return 2 + 2 * steps_ev<CAP>(); }
+__host__ __device__ inline int steps_arrays_rt(int cap) { return 2 + 2 * (cap >= 1024 ? 2 : SP_STEPS_EV); }
 // the walk's ring: stages fetched ahead, and the bytes of one stage (stage
 // record 16 | pad 16 | up to 64 breakpoints of C | up to 64 of S)
-constexpr int kWalkDepth = 8;
+template <int CAP> __host__ __device__ constexpr int walk_depth() { return steps_arrays<CAP>() >= 6 ? 8 : 4; }
 constexpr size_t kWalkSlot = 32 + 2 * 64 * 8;
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -353,10 +363,12 @@ __device__ __forceinline__ void cp_async_wait() {
 // CAP keeps its flag (device path) / gets its overflow bit (wave path) and
 // is left to the next tier.
 template <int MODE, int CAP, int WPB>
-__global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(StepsArgs a) {
+__global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : SP_STEPS_MINB) dp_steps_kernel(StepsArgs a) {
   using V = typename VT<MODE>::T;
   using E = Ent<MODE>;
-  constexpr size_t INST_BYTES = (size_t)kStepsArrays * CAP * sizeof(E);
+  constexpr size_t INST_BYTES = (size_t)steps_arrays<CAP>() * CAP * sizeof(E);
+  constexpr int EVC = steps_ev<CAP>() * CAP;  // merge events per half
+  constexpr int kWalkDepth = walk_depth<CAP>();
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = lane >> 4, g = lane & 15;
@@ -369,7 +381,7 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
     return;
   unsigned char* ws = smem + (size_t)warp * INST_BYTES;
   E* rows = reinterpret_cast<E*>(ws);              // [2 rows: C, S][CAP]
-  E* evs = rows + 2 * CAP;                         // [2 halves][2 CAP] merge events
+  E* evs = rows + 2 * CAP;                         // [2 halves][EVC] merge events
 
   const int64_t lo = a.layer_off[inst];
   const int L = (int)(a.layer_off[inst + 1] - lo);
@@ -408,9 +420,13 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : 8) dp_steps_kernel(St
     // next stage's clip thresholds of the row this half builds: as its own
     // merge's A (C: i, S: s) and as the other merge's B (C: s + u, S: i + d)
     const int t1 = W - (h ? sh_next.s : sh_next.i), t2 = W - (h ? sh_next.id : sh_next.su);
+    if (EVC < 2 * CAP && __any_sync(kFull, na + nb > EVC)) {  // more events than the scratch holds
+      over = true;
+      break;
+    }
     int c1, c2;
     const int n2 = steps_merge_half<MODE, CAP, V>(rows + h * CAP, na, h ? sh.s : sh.i, rows + (1 - h) * CAP, nb,
-                                                  h ? sh.su : sh.id, rk, evs + h * 2 * CAP, rows + h * CAP,
+                                                  h ? sh.su : sh.id, rk, evs + h * EVC, rows + h * CAP,
                                                   g_ent + (r0 + h) * CAP, g, h, t1, t2, c1, c2);
     const int n2o = __shfl_xor_sync(kFull, n2, 16);
     if (n2 < 0 || n2o < 0) {

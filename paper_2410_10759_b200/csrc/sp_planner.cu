@@ -657,7 +657,8 @@ struct Trace {
 template <int CAP> constexpr int steps_wpb() { return CAP >= 1024 ? 1 : SP_STEPS_WPB; }
 size_t steps_smem(int mode, int cap) {
   const int WPB = cap >= 1024 ? 1 : SP_STEPS_WPB;
-  return (size_t)WPB * kStepsArrays * (size_t)cap * (mode == VM_INT32 ? sizeof(Ent<VM_INT32>) : sizeof(Ent<VM_F64>));
+  return (size_t)WPB * steps_arrays_rt(cap) * (size_t)cap *
+         (mode == VM_INT32 ? sizeof(Ent<VM_INT32>) : sizeof(Ent<VM_F64>));
 }
 
 template <int MODE, int CAP>
