@@ -732,15 +732,21 @@ def run_reference(args, rank: int, world: int):
     """The reference arm: the oracle port of the reference path (profile ->
     build_problem -> plan_dp) on every host core, rank 0 only.  The process
     pool is created before the timed steps; each step is a bounded sample of
-    about 1.5 s of wall time on all cores."""
+    about 2.5 s of wall time on all cores (>= 8 requests per worker)."""
     if rank != 0:
         return
     req_np = cfg2_requests(args.requests, args.seed * 1000)
     procs = max(1, min(os.cpu_count() or 1, 128))
     pool = CpuPool(procs)
     try:
-        _cells, dt = pool.run(_cpu_jobs(req_np, range(procs)))  # fork + first touch, untimed
-        per = args.cpu_sample or min(int(max(procs, math.ceil(procs * 1.5 / max(dt, 1e-3)))), args.requests)
+        pool.run(_cpu_jobs(req_np, range(procs)))  # fork + first touch, untimed
+        # calibration on warm workers: two requests each; a step then gives every
+        # worker >= 8 requests (about 2.5 s), so the slowest worker's tail is a
+        # small part of the step (with ~5 per worker the arm read half the rate
+        # of cpu_baseline on the same box)
+        _cells, dt = pool.run(_cpu_jobs(req_np, np.arange(2 * procs) % args.requests))
+        per_worker = max(8, int(round(2.5 / max(dt / 2, 1e-3))))
+        per = args.cpu_sample or min(procs * per_worker, args.requests)
         times, cells_tot = [], 0.0
         for s in range(args.warmup + args.steps):
             idx = (np.arange(per) + s * per) % args.requests

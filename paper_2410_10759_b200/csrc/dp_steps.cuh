@@ -146,10 +146,10 @@ __device__ __forceinline__ Ent<MODE> mk_ent(int32_t c, V v) {
 // stage, the new row's breakpoints at columns <= t1 / <= t2 (cnt1 / cnt2).
 //   1. merge path: lane g takes diagonal [ne*g/16, ne*(g+1)/16) of the merged
 //      order (one binary search; an equal-column pair is never split), and
-//      merges its part serially into the scratch at the merged positions --
-//      every event carries the row value after it and whether the stay
-//      predecessor reproduces that value (bit 31 of the column); slots freed
-//      by merged equal-column pairs repeat the previous value.  An event is
+//      merges its part serially into its region of the scratch (from its
+//      diagonal's start) -- every event carries the row value after it and
+//      whether the stay predecessor reproduces that value (bit 31 of the
+//      column); a merged equal-column pair is one event.  An event is
 //      kept iff its value differs from the previous slot's; the lane knows
 //      the value before its part, so it counts its own;
 //   2. a scan of the counts over the half places every lane's kept events;
@@ -167,7 +167,7 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
   const int hs = h << 4;
   // 1. merge path + serial merge into the scratch
   const int ne = na + nb;
-  const int k0 = (ne * g) >> 4, kend = g == 15 ? ne : (ne * (g + 1)) >> 4;
+  const int k0 = (ne * g) >> 4;
   int i0, j0;
   {
     int lo = max(0, k0 - nb), hi = min(k0, na);
@@ -187,6 +187,7 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
   }
   V y0;             // the row value just before this lane's part
   int nk = 0;       // kept events in this lane's part
+  int kev;          // end of this lane's events in the scratch (k0 + events)
   bool kept = false;
   int32_t fs_pre = kNoStay;  // first stay event of this part before its first kept one
   {
@@ -224,7 +225,7 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
       y = yn;
       ++k;
     }
-    for (; k < kend; ++k) ev[k] = mk_ent<MODE>(COLM, y);  // freed by merged pairs: no event
+    kev = k;  // (a merged equal-column pair is one event: fewer events than merged positions)
   }
   // 2. output positions (a scan of the kept counts over the half) and the
   // stay_from of a segment running past this lane's part: the first later
@@ -249,7 +250,7 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
     int pos = incl - nk, open = -1;
     int32_t ocol = 0, osf = kNoStay;  // the open breakpoint: column, stay_from found so far
     V prev = y0;
-    for (int k = k0; k < kend; ++k) {
+    for (int k = k0; k < kev; ++k) {
       const Ent<MODE> e = ev[k];
       const int32_t col = e.c & COLM;
       if (e.v != prev) {  // kept: the previous open breakpoint is complete
