@@ -728,10 +728,11 @@ int64_t smem_max_cols(int mode) {
   return lo;
 }
 // narrowest row the breakpoint lists take (all of them when forced)
-// (rows of a few thousand columns already take ~30x fewer breakpoints than
-// columns on model-derived instances: the lists beat the SMEM kernel there,
-// profiles/r02/tier0/; SPLITPLAN_STEPS_MIN_COLS moves the threshold)
-constexpr int64_t kStepsMinCols = 1024;
+// (rows of any width: on model-derived instances the lists beat the SMEM
+// kernel down to the narrowest rows -- cfg4 solve 349 ms at a 1,024-column
+// threshold, 221 ms at 32, profiles/r02/tier0/threshold.md -- and a row of at
+// most CAP columns cannot overflow them; SPLITPLAN_STEPS_MIN_COLS moves it)
+constexpr int64_t kStepsMinCols = 0;
 int64_t steps_min_cols(int mode, int force) {
   (void)mode;
   if (force == DPV_STEPS) return 0;
