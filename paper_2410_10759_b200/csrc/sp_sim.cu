@@ -6,7 +6,8 @@
 // of arrivals, so only the in-service min-heap needs storage: a per-run
 // binary heap of (finish_ms, seq, request) in the caller's workspace, keyed
 // lexicographically on (finish, seq) exactly like the reference's heapq
-// tuples (seq is unique, so the pop order is fully determined).
+// tuples (seq is unique, so the pop order is fully determined; any heap
+// arity gives it -- this one is 4-ary).
 #include <algorithm>
 
 #include "sp_internal.cuh"
@@ -25,10 +26,14 @@ __device__ __forceinline__ bool less(const HeapEntry& a, const HeapEntry& b) {
   return a.finish < b.finish || (a.finish == b.finish && a.seq < b.seq);
 }
 
+// 4-ary heap: half the depth of a binary one; a node's four children are
+// adjacent (one or two 32-B sectors), loaded back to back before comparing,
+// so a sift-down level costs one memory latency.  Keys are unique (seq), so
+// every valid heap pops the same order.
 __device__ void heap_push(HeapEntry* h, int64_t& size, HeapEntry e) {
   int64_t c = size++;
   while (c > 0) {
-    const int64_t p = (c - 1) >> 1;
+    const int64_t p = (c - 1) >> 2;
     const HeapEntry pe = h[p];
     if (!less(e, pe)) break;
     h[c] = pe;
@@ -42,19 +47,18 @@ __device__ HeapEntry heap_pop(HeapEntry* h, int64_t& size) {
   const HeapEntry last = h[--size];
   int64_t c = 0;
   while (true) {
-    int64_t l = 2 * c + 1;
-    if (l >= size) break;
-    HeapEntry le = h[l];
-    if (l + 1 < size) {
-      const HeapEntry re = h[l + 1];
-      if (less(re, le)) {
-        le = re;
-        ++l;
-      }
-    }
-    if (!less(le, last)) break;
-    h[c] = le;
-    c = l;
+    const int64_t f = 4 * c + 1;
+    if (f >= size) break;
+    HeapEntry ch[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ch[q] = h[min(f + q, size - 1)];  // (past the end: a copy of the last child)
+    int best = 0;
+#pragma unroll
+    for (int q = 1; q < 4; ++q)
+      if (less(ch[q], ch[best])) best = q;
+    if (!less(ch[best], last)) break;
+    h[c] = ch[best];
+    c = f + best;
   }
   if (size > 0) h[c] = last;
   return top;
