@@ -34,7 +34,7 @@ extern "C" {
                              3: per-partition workspaces, sp_grid_* (one process per
                                 device), sp_ipc_*, sp_last_full_workspace;
                              4: sp_plan_dp_async / sp_plan_dp_finish; 256-B aligned
-                                workspaces */
+                                workspaces; sp_plan_dp_onewave_bytes */
 
 enum sp_status {
   SP_OK = 0,
@@ -144,6 +144,12 @@ int sp_plan_dp_finish(const sp_instances* in, sp_policies* out, void* ws, size_t
  * sp_last_required_workspace().  Synchronises `stream`; launches no DP. */
 int sp_plan_dp_workspace_bytes(const sp_instances* in, size_t* min_bytes, size_t* full_bytes, void* ws,
                                size_t ws_bytes, void* stream);
+
+/* Host arithmetic only (no device work): the workspace with which sp_plan_dp
+ * runs the device-planned breakpoint-list tier of n instances of total_layers
+ * stages in ONE wave (fixed part + every instance's store).  A caller sizing
+ * its workspace ahead of a call uses it to avoid many small waves. */
+size_t sp_plan_dp_onewave_bytes(int64_t n, int64_t total_layers);
 
 /* sp_plan_dp with the capacity axis of huge instances split over devices
  * (SURVEY.md 8(e), cfg5).  Instances that take the whole-GPU path (>= 4M

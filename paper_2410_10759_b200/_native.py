@@ -143,6 +143,7 @@ SIGNATURES = {
     "sp_sim_workspace_bytes": (C.c_size_t, [C.POINTER(SpSimBatch)]),
     "sp_sim_replay": (C.c_int, [C.POINTER(SpSimBatch), C.POINTER(SpSimOut), P, C.c_size_t, P]),
     "sp_sim_skeletons": (C.c_int, [P, P, P, C.c_int64, C.c_int64, C.c_double, C.c_int64, P, P, P, P, P]),
+    "sp_plan_dp_onewave_bytes": (C.c_size_t, [C.c_int64, C.c_int64]),
 }
 
 _lib = None

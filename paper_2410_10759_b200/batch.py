@@ -196,6 +196,10 @@ def plan_dp(batch: InstanceBatch, out: PolicyBatch | None = None, devices=None) 
             C.cast(wlen, C.c_void_p), N.stream_ptr()))
         N.check(rc, "sp_plan_dp_devices")
         return out
+    # grow the cached workspace ahead of the call to what runs the
+    # device-planned tier in one wave (host arithmetic; within the cap and the
+    # free memory), instead of many small waves in a first call
+    N.grow_workspace_hint(int(lib.sp_plan_dp_onewave_bytes(batch.n, batch.total_layers)))
     ws = N.workspace()
     rc = lib.sp_plan_dp(s, o, N.ptr(ws), ws.numel(), N.stream_ptr())
     if rc == N.SP_ERR_WORKSPACE:

@@ -1889,6 +1889,11 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
   int cached_mode = -1;
   int64_t cached_ncol = -1, cached_L = -1;
   int cached_cap = -1;
+  // the query's tier-1 instances are sized in O(1) each: their stores summed,
+  // the dense fallback's minimum bounded by the widest and longest per domain
+  // (both monotone in L and W_eff), instead of a launch plan per instance
+  size_t q_tier1 = 0;
+  int64_t q_maxL[3] = {0, 0, 0}, q_maxcol[3] = {0, 0, 0};
   for (int64_t k = 0; k < n; ++k) {
     if (!hflag.empty() && !hflag[k]) continue;  // solved by tier 1 (breakpoint lists) or tier 0
     if (!hcls.empty() && hcls[k] != 255) continue;  // the query: tier 0's (sized below)
@@ -1897,6 +1902,15 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       set_error(SP_ERR_UNSUPPORTED, "instance %lld: W_eff = %lld exceeds the supported 2^31 columns",
                 (long long)k, (long long)hinfo[k].w_eff);
       return SP_ERR_UNSUPPORTED;
+    }
+    if (q_min && steps_allowed && ncol < kGridMinCols && force != DPV_GRID &&
+        steps_eligible(hinfo[k].mode, ncol, force, false, lo_i32, lo_f64)) {
+      const int64_t L = hoff[k + 1] - hoff[k];
+      const int m = hinfo[k].mode;
+      q_tier1 += (size_t)(L + 1) * rpb;
+      q_maxL[m] = std::max(q_maxL[m], L);
+      q_maxcol[m] = std::max(q_maxcol[m], ncol);
+      continue;
     }
     Item it;
     it.inst = k;
@@ -1961,6 +1975,12 @@ int run_dp(const sp_instances* in, sp_policies* out, double* tab_c, double* tab_
       mn = std::max(mn, imin);
       full = grid ? std::max(full, ifull) : full + ifull;
     }
+    tier1 += q_tier1;
+    for (int m = 0; m < 3; ++m)
+      if (q_maxL[m] > 0) {  // the dense kernels' need of any tier-1 instance that overflows
+        const DpPlan p = plan_instance(m, q_maxL[m], q_maxcol[m], force, false, 0);
+        mn = std::max(mn, p.bp + p.rows);
+      }
     size_t t0_all = 0;  // tier 0: its tables in one wave (useful), one counting block's (minimum)
     for (const T0Block& b : hblk) {
       t0_all += b.bytes;
@@ -2225,6 +2245,25 @@ int sp_plan_dp_finish(const sp_instances* in, sp_policies* out, void* ws, size_t
   }
   return run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr, nullptr, nullptr,
                 nullptr, -1, nullptr, p);
+}
+
+size_t sp_plan_dp_onewave_bytes(int64_t n, int64_t total) {
+  if (n <= 0 || total < 0) return 0;
+  Carve cv{nullptr, 0};  // run_dp's fixed part, laid out the same way
+  cv.take(sizeof(InstInfo) * n);
+  cv.take(sizeof(StageShift) * total);
+  cv.take(sizeof(int64_t) * total);
+  cv.take(sizeof(int32_t) * total);
+  cv.take(sizeof(DpWork) * n);
+  cv.take(sizeof(int2) * total);
+  cv.take(64);
+  cv.take(sizeof(int32_t) * n);
+  cv.take(sizeof(int32_t) * n);
+  cv.take(4 * sizeof(unsigned long long));
+  cv.take(sizeof(T0Stats));
+  cv.take(sizeof(T0Block) * ((n + kT0Block - 1) / kT0Block));
+  cv.take(n);
+  return align_up(cv.used, 256) + (size_t)(total + n) * steps_row_pair_bytes(kStepsCap);
 }
 
 int sp_plan_dp_workspace_bytes(const sp_instances* in, size_t* min_bytes, size_t* full_bytes, void* ws,
