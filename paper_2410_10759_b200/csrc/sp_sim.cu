@@ -42,9 +42,11 @@ __device__ void heap_push(HeapEntry* h, int64_t& size, HeapEntry e) {
   h[c] = e;
 }
 
-__device__ HeapEntry heap_pop(HeapEntry* h, int64_t& size) {
+// (root_finish: the new root's finish time after the pop, INFINITY if empty)
+__device__ HeapEntry heap_pop(HeapEntry* h, int64_t& size, double& root_finish) {
   const HeapEntry top = h[0];
   const HeapEntry last = h[--size];
+  root_finish = size > 0 ? last.finish : INFINITY;
   int64_t c = 0;
   while (true) {
     const int64_t f = 4 * c + 1;
@@ -57,6 +59,7 @@ __device__ HeapEntry heap_pop(HeapEntry* h, int64_t& size) {
     for (int q = 1; q < 4; ++q)
       if (less(ch[q], ch[best])) best = q;
     if (!less(ch[best], last)) break;
+    if (c == 0) root_finish = ch[best].finish;
     h[c] = ch[best];
     c = f + best;
   }
@@ -81,20 +84,26 @@ __global__ void sim_replay_kernel(sp_sim_batch b, sp_sim_out o, HeapEntry* heap_
   int32_t seq = 0;
   int32_t status = SP_OK;
   int64_t dead = -1;
-  for (int64_t k = 0; k < n; ++k) admit[k] = 0.0;
+  // the heap's root finish, the next arrival and the FIFO head's demand stay
+  // in registers: every global access is divergent across a warp's runs (one
+  // run per lane), so the replay is bound by load instructions, not math.
+  // (admit needs no initialisation: a run that completes admits every
+  // request; a deadlocked run's admit times are not reported)
+  double top_f = INFINITY;
+  double t_arr = n > 0 ? arr[0] : INFINITY;
+  double need = n > 0 ? dem[0] : 0.0;  // dem[head]
   while (next < n || hsize > 0) {
-    const double t_arr = next < n ? arr[next] : INFINITY;
     double now;
-    if (hsize > 0 && h[0].finish <= t_arr) {  // completions before equal-time arrivals
-      const HeapEntry e = heap_pop(h, hsize);
+    if (top_f <= t_arr) {  // completions before equal-time arrivals (top_f is INFINITY when empty)
+      const HeapEntry e = heap_pop(h, hsize, top_f);
       now = e.finish;
       free_cap = dadd(free_cap, dem[e.req]);
     } else {
       now = t_arr;
       ++next;
+      t_arr = next < n ? arr[next] : INFINITY;
     }
     while (head < next) {
-      const double need = dem[head];
       if (need <= dadd(free_cap, eps)) {
         admit[head] = now;
         free_cap = dadd(free_cap, -need);
@@ -103,7 +112,9 @@ __global__ void sim_replay_kernel(sp_sim_batch b, sp_sim_out o, HeapEntry* heap_
         e.seq = seq++;
         e.req = (int32_t)head;
         heap_push(h, hsize, e);
+        top_f = e.finish < top_f ? e.finish : top_f;  // the root is the minimum finish
         ++head;
+        if (head < n) need = dem[head];
       } else {
         if (need > dadd(cap, eps)) {
           status = SP_ERR_DEADLOCK;
@@ -119,20 +130,31 @@ __global__ void sim_replay_kernel(sp_sim_batch b, sp_sim_out o, HeapEntry* heap_
   if (status != SP_OK) return;
   // waits, max, numpy-order mean, sequential cumsum (throughput_sim.py:122-130, 247)
   double mx = -INFINITY, run_sum = 0.0;
-  for (int64_t k = 0; k < n; ++k) {
-    const double w = dadd(admit[k], -arr[k]);
-    if (o.wait_ms) o.wait_ms[lo + k] = w;
-    if (o.cum_wait_ms) {
-      run_sum = (k == 0) ? w : dadd(run_sum, w);
-      o.cum_wait_ms[lo + k] = run_sum;
+  const bool per_request = o.wait_ms || o.cum_wait_ms;
+  if (per_request || !o.mean_wait_ms) {
+    for (int64_t k = 0; k < n; ++k) {
+      const double w = dadd(admit[k], -arr[k]);
+      if (o.wait_ms) o.wait_ms[lo + k] = w;
+      if (o.cum_wait_ms) {
+        run_sum = (k == 0) ? w : dadd(run_sum, w);
+        o.cum_wait_ms[lo + k] = run_sum;
+      }
+      mx = (w > mx || w != w) ? w : mx;
     }
-    mx = (w > mx || w != w) ? w : mx;
   }
-  if (o.max_wait_ms) o.max_wait_ms[run] = n ? mx : 0.0;
   if (o.mean_wait_ms) {
-    const double s = np_sum([&](int64_t k) { return dadd(admit[k], -arr[k]); }, n);
+    // (without per-request outputs the max rides along the sum's single pass:
+    // np_sum reads every element exactly once)
+    const double s = np_sum(
+        [&](int64_t k) {
+          const double w = dadd(admit[k], -arr[k]);
+          if (!per_request) mx = (w > mx || w != w) ? w : mx;
+          return w;
+        },
+        n);
     o.mean_wait_ms[run] = n ? ddiv(s, (double)n) : 0.0;
   }
+  if (o.max_wait_ms) o.max_wait_ms[run] = n ? mx : 0.0;
 }
 
 // One thread per skeleton: numpy's default_rng(seed) draws in numpy's order
