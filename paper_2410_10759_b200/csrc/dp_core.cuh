@@ -29,6 +29,25 @@ __device__ __forceinline__ double to_f64(int32_t v, double g) {
 __device__ __forceinline__ double to_f64(double v, double) { return v; }
 
 // binary (Stein) gcd: shifts and subtractions, no 64-bit division
+// exact remainder of integral doubles 0 <= v, 0 < d < 2^53: q = floor(v / d)
+// may be one off, v - q*d is an integer below 2d in magnitude and the fma
+// computes it exactly; one correction step fixes q
+__device__ __forceinline__ double rem_exact(double v, double d) {
+  const double q = floor(__ddiv_rn(v, d));
+  double r = __fma_rn(-q, d, v);
+  if (r < 0.0) r = __dadd_rn(r, d);
+  else if (r >= d) r = __dadd_rn(r, -d);
+  return r;
+}
+__device__ __forceinline__ double gcd_f64(double a, double b) {
+  while (b != 0.0) {
+    const double t = rem_exact(a, b);
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
 __device__ __forceinline__ uint64_t gcd_u64(uint64_t a, uint64_t b) {
   if (a == 0) return b;
   if (b == 0) return a;
@@ -97,7 +116,7 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(sp_instances in, 
     const int64_t lo = in.layer_off[k], hi = in.layer_off[k + 1];
     int64_t worst = 0;
     int finite = 1, integral = 1;
-    uint64_t isum = 0, g = 0;
+    uint64_t isum = 0, orv = 0;
     for (int64_t l = lo + lane; l < hi; l += 32) {
       worst += max(in.client_units[l] + in.down_units[l], in.server_units[l] + in.up_units[l]);
       const double r = in.r[l];
@@ -108,7 +127,7 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(sp_instances in, 
       } else {
         const uint64_t v = (uint64_t)r;  // r >= 0 (problem.py:151-153)
         isum = min(isum + v, (uint64_t)1 << 62);
-        g = gcd_u64(g, v);
+        orv |= v;
       }
     }
     {
@@ -119,10 +138,24 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(sp_instances in, 
         finite &= __shfl_xor_sync(0xffffffffu, finite, o);
         integral &= __shfl_xor_sync(0xffffffffu, integral, o);
         isum = min(isum + __shfl_xor_sync(0xffffffffu, isum, o), sat);
-        g = gcd_u64(g, __shfl_xor_sync(0xffffffffu, g, o));
+        orv |= __shfl_xor_sync(0xffffffffu, orv, o);
       }
     }
-    if (g == 0) g = 1;
+    // The int32 domain stores r / g for any common divisor g (the values are
+    // g * v exactly either way); the largest power of two dividing every r
+    // (the lowest set bit of their OR) usually leaves the sums in range
+    // (model FLOP counts carry large powers of two), and only when it does
+    // not is the exact gcd computed -- a second pass of binary gcds.
+    uint64_t g = orv ? (orv & (~orv + 1)) : 1;
+    if (finite && integral && isum < ((uint64_t)1 << 53) && isum / g > (uint64_t)INT32_MAX) {
+      // Euclid on exact doubles (every r < 2^53): once the running gcd has
+      // settled, each further r costs one exact remainder
+      double gg = 0.0;
+      for (int64_t l = lo + lane; l < hi; l += 32) gg = gcd_f64(gg, in.r[l]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gg = gcd_f64(gg, __shfl_xor_sync(0xffffffffu, gg, o));
+      g = gg > 0.0 ? (uint64_t)gg : 1;
+    }
     const int64_t W = min(in.budget[k], worst);
     int32_t mode;
     if (!finite) mode = VM_F64_NAN;
@@ -162,7 +195,8 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(sp_instances in, 
         sh.su = (int32_t)min(s + u, cap);
         shifts[l] = sh;
         const double r = in.r[l];
-        rv[l] = mode == VM_INT32 ? (int64_t)((uint64_t)r / g) : __double_as_longlong(r);
+        // (g divides r and the quotient is below 2^31: the fp64 division is exact)
+        rv[l] = mode == VM_INT32 ? (int64_t)__ddiv_rn(r, (double)g) : __double_as_longlong(r);
       }
       if (!reach) continue;
       if (trivial) {
