@@ -24,8 +24,9 @@ struct LayerCost {
 };
 
 __device__ inline int64_t eff_seq(int64_t seq_len, int64_t div) {
-  // cost_model.py:137-138 (positive operands: floor division)
-  return max((int64_t)1, seq_len / div);
+  // cost_model.py:137-138 (positive operands: floor division; the common
+  // divisor 1 skips the 64-bit division routine)
+  return max((int64_t)1, div == 1 ? seq_len : seq_len / div);
 }
 
 __device__ inline double poly(const double* c, double s) {
