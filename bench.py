@@ -660,6 +660,9 @@ def main():
                       "(CUDA-event timing, no flush needed)" % (prof.bytes / max(prof.n, 1) / 1e9),
                 "parallelism": f"request-sharded dp{world}",
                 "collective": "none in the solve; one all_gather of result records per step when N > 1",
+                "scenario": "scenarios_per_s counts solved requests: one (model, seq_len, link, deadline) "
+                            "placement problem, a run_sweep cell of the reference (evaluator.py:211-226); the "
+                            "Monte-Carlo grid's scenarios/s (configs[3]) is configs.cfg4.scenarios_per_s",
             },
             "scenarios_per_s": n * world / (step_ms / 1e3),
             "e2e": {"value": total_cells / (e2e_ms / args.steps / 1e3), "unit": "DP cells/s",

@@ -53,3 +53,26 @@ def test_error_state_without_gpu_calls():
     assert b"null instance batch" in lib.sp_last_error()
     rc = lib.sp_to_units(None, 1, ctypes.c_double(1e-3), 0, None, None, None)
     assert rc == _native.SP_ERR_INVALID
+
+
+def test_onewave_bytes_is_host_arithmetic():
+    """sp_plan_dp_onewave_bytes needs no device: the fixed part plus one
+    breakpoint store (2 rows x (8 + 8 x 192) bytes) per stage and instance."""
+    from paper_2410_10759_b200 import _native
+    lib = _native.library()
+    assert lib.sp_plan_dp_onewave_bytes(0, 0) == 0
+    a = lib.sp_plan_dp_onewave_bytes(10_000, 980_000)
+    b = lib.sp_plan_dp_onewave_bytes(20_000, 1_960_000)
+    assert a >= (980_000 + 10_000) * 2 * (8 + 8 * 192)
+    assert a % 256 == 0 and b > 1.9 * a
+
+
+def test_skeleton_arguments_validated_without_gpu():
+    from paper_2410_10759_b200 import _native
+    lib = _native.library()
+    rc = lib.sp_sim_skeletons(None, None, None, 4, 10, ctypes.c_double(1.0), 10, None, None, None, None, None)
+    assert rc == _native.SP_ERR_INVALID
+    rc = lib.sp_sim_skeletons(None, None, None, 0, 10, ctypes.c_double(1.0), 0, None, None, None, None, None)
+    assert rc == _native.SP_ERR_INVALID  # exec_max < 1
+    assert lib.sp_sim_skeletons(None, None, None, 0, 10, ctypes.c_double(1.0), 10, None, None, None, None,
+                                None) == 0
