@@ -406,7 +406,7 @@ typedef struct sp_sim_out {
 int sp_segment_sum(const double* x, const int64_t* seg_off, int64_t n_seg, double* out,
                    void* stream);
 
-/* Heap workspace the replay needs (16 bytes per request). */
+/* Heap workspace the replay needs (16 bytes per request + 128 per run). */
 size_t sp_sim_workspace_bytes(const sp_sim_batch* b);
 
 /* K4: FIFO admission with a completion min-heap keyed (finish, seq), one

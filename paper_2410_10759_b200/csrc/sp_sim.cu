@@ -43,6 +43,11 @@ __device__ void heap_push(HeapEntry* h, int64_t& size, HeapEntry e) {
 }
 
 // (root_finish: the new root's finish time after the pop, INFINITY if empty)
+// A node's four children h[4c+1 .. 4c+4] are one 64-B aligned group (the
+// run's heap starts 3 entries into a 64-B aligned block): two 256-bit loads.
+struct __align__(32) EntryPair {
+  HeapEntry a, b;
+};
 __device__ HeapEntry heap_pop(HeapEntry* h, int64_t& size, double& root_finish) {
   const HeapEntry top = h[0];
   const HeapEntry last = h[--size];
@@ -51,13 +56,14 @@ __device__ HeapEntry heap_pop(HeapEntry* h, int64_t& size, double& root_finish) 
   while (true) {
     const int64_t f = 4 * c + 1;
     if (f >= size) break;
-    HeapEntry ch[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) ch[q] = h[min(f + q, size - 1)];  // (past the end: a copy of the last child)
+    const EntryPair* g = reinterpret_cast<const EntryPair*>(h + f);
+    const EntryPair p0 = g[0], p1 = g[1];
+    const HeapEntry ch[4] = {p0.a, p0.b, p1.a, p1.b};
+    const int nv = (int)min((int64_t)4, size - f);  // children past the end are not in the heap
     int best = 0;
 #pragma unroll
     for (int q = 1; q < 4; ++q)
-      if (less(ch[q], ch[best])) best = q;
+      if (q < nv && less(ch[q], ch[best])) best = q;
     if (!less(ch[best], last)) break;
     if (c == 0) root_finish = ch[best].finish;
     h[c] = ch[best];
@@ -76,7 +82,9 @@ __global__ void sim_replay_kernel(sp_sim_batch b, sp_sim_out o, HeapEntry* heap_
   const double* dem = b.demand + lo;
   const double* dur = b.duration_ms + lo;
   double* admit = o.admit_ms + lo;
-  HeapEntry* h = heap_ws + lo;  // a run never holds more than n in service
+  // a run never holds more than n in service; its heap starts 3 entries into
+  // a 64-B aligned block (children groups aligned), 8 spare entries per run
+  HeapEntry* h = heap_ws + (((lo + 8 * run) + 3) & ~(int64_t)3) + 3;
   const double cap = b.capacity[run];
   const double eps = dmul(1e-9, cap);
   double free_cap = cap;
@@ -229,7 +237,7 @@ int sp_sim_skeletons(const int64_t* seeds, const int64_t* choice_lo, const int64
 
 size_t sp_sim_workspace_bytes(const sp_sim_batch* b) {
   if (!b) return 0;
-  return sizeof(HeapEntry) * (size_t)std::max<int64_t>(1, b->total_requests);
+  return sizeof(HeapEntry) * (size_t)std::max<int64_t>(1, b->total_requests + 8 * b->n_runs + 8);
 }
 
 int sp_sim_replay(const sp_sim_batch* b, sp_sim_out* o, void* ws, size_t ws_bytes, void* stream) {
