@@ -56,10 +56,16 @@ __device__ HeapEntry heap_pop(HeapEntry* h, int64_t& size, double& root_finish) 
   while (true) {
     const int64_t f = 4 * c + 1;
     if (f >= size) break;
-    const EntryPair* g = reinterpret_cast<const EntryPair*>(h + f);
-    const EntryPair p0 = g[0], p1 = g[1];
-    const HeapEntry ch[4] = {p0.a, p0.b, p1.a, p1.b};
     const int nv = (int)min((int64_t)4, size - f);  // children past the end are not in the heap
+    HeapEntry ch[4];
+    if (nv == 4) {
+      const EntryPair* g = reinterpret_cast<const EntryPair*>(h + f);
+      const EntryPair p0 = g[0], p1 = g[1];
+      ch[0] = p0.a, ch[1] = p0.b, ch[2] = p1.a, ch[3] = p1.b;
+    } else {  // the last, partial group: only entries of the heap are read
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ch[q] = h[f + min(q, nv - 1)];
+    }
     int best = 0;
 #pragma unroll
     for (int q = 1; q < 4; ++q)

@@ -13,7 +13,8 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
-CASES = ("smem", "stream", "grid", "grid_parts", "grid_devices", "steps", "steps_wide", "prefix", "sim", "cost")
+CASES = ("smem", "stream", "grid", "grid_parts", "grid_devices", "steps", "steps_wide", "prefix", "sim", "cost",
+         "tier0", "tier1_waves", "async", "skeleton", "montecarlo")
 
 
 def instances(seed, n, L, W, hi, float_r=False):
@@ -49,6 +50,33 @@ def main():
         os.environ.update(SPLITPLAN_DP_VARIANT="grid", SPLITPLAN_GRID_SEGMENT="5")
         b = instances(4, 1, 16, 20000, 400)
         p = B.plan_dp(b, devices=[torch.cuda.current_device()] * 2)
+    elif c == "tier0":  # the device-planned SMEM tier: classes of both domains, NaN domain
+        os.environ["SPLITPLAN_STEPS_MIN_COLS"] = str(1 << 30)
+        b = instances(7, 40, 10, 700, 120, float_r=False)
+        p = B.plan_dp(b)
+        b2 = instances(8, 40, 10, 3000, 500, float_r=True)
+        p = B.plan_dp(b2)
+    elif c == "tier1_waves":  # breakpoint lists in waves of a small workspace
+        b = instances(9, 64, 12, 2000, 300)
+        mn, full = B.dp_workspace_bytes(b)
+        size = mn + (full - mn) // 4
+        ws = torch.empty(size, dtype=torch.uint8, device=N.device())
+        p = B.PolicyBatch.empty(b.n, b.total_layers, b.r.device)
+        assert N.library().sp_plan_dp(b.struct(), p.struct(), N.ptr(ws), size, N.stream_ptr()) == 0
+    elif c == "async":
+        b = instances(10, 16, 12, 5000, 400)
+        p = B.plan_dp_async(b).finish()
+    elif c == "skeleton":
+        from paper_2410_10759_b200.throughput_sim import skeletons_device
+        arr, rows, ex = skeletons_device(np.arange(64), np.zeros(64, np.int64), np.arange(64) % 7 + 1, 500, 0.057)
+        torch.cuda.synchronize()
+        print("skeleton ok", float(arr[:, -1].sum()))
+        return
+    elif c == "montecarlo":
+        from paper_2410_10759_b200 import montecarlo as MC
+        res = MC.run(np.arange(0, 4096, 257), horizon=300)
+        print("montecarlo ok", int((res.status == 0).sum()))
+        return
     elif c == "prefix":
         b = instances(5, 4, 20, 3000, 400)
         p = B.plan_prefix(b, N.SP_GREEDY)
