@@ -107,9 +107,11 @@ class PolicyBatch:
 
     @classmethod
     def empty(cls, n: int, total: int, dev=None) -> "PolicyBatch":
-        """One device allocation; pi and status zeroed (one fill)."""
+        """One device allocation, zeroed with one fill (pi and status must
+        start at zero; the alignment gaps are zeroed too, so the one-copy
+        to_host reads no uninitialised bytes)."""
         dev = dev or N.device()
-        buf, v = N.packed(_POLICY_LAYOUT(n, total), dev, zero_prefix=2)
+        buf, v = N.packed(_POLICY_LAYOUT(n, total), dev, zero_prefix=len(_POLICY_LAYOUT(0, 0)))
         out = cls(v["pi"], v["client_value"], v["server_load"], v["integer_latency"], v["feasible"],
                   v["status"])
         out._buf = buf

@@ -326,18 +326,23 @@ __device__ __forceinline__ void finish_policy_warp(const sp_instances& in, int64
 // events [2][EV x CAP] (EV = 2 holds any merge of two rows of CAP; EV = 1
 // halves the footprint, a merge of more than CAP events overflows to the next
 // tier; the wide tier keeps 2)
-#ifndef SP_STEPS_EV
-#define SP_STEPS_EV 2
+#ifndef SP_STEPS_EV2
+#define SP_STEPS_EV2 4  // twice the events scratch per half, in units of CAP (4: 2 CAP)
 #endif
 #ifndef SP_STEPS_MINB
 #define SP_STEPS_MINB 8
 #endif
-template <int CAP> __host__ __device__ constexpr int steps_ev() { return CAP >= 1024 ? 2 : SP_STEPS_EV; }
-template <int CAP> __host__ __device__ constexpr int steps_arrays() { return 2 + 2 * steps_ev<CAP>(); }
-__host__ __device__ inline int steps_arrays_rt(int cap) { return 2 + 2 * (cap >= 1024 ? 2 : SP_STEPS_EV); }
-// the walk's ring: stages fetched ahead, and the bytes of one stage (stage
-// record 16 | pad 16 | up to 64 breakpoints of C | up to 64 of S)
-template <int CAP> __host__ __device__ constexpr int walk_depth() { return steps_arrays<CAP>() >= 6 ? 8 : 4; }
+template <int CAP> __host__ __device__ constexpr int steps_ev2() { return CAP >= 1024 ? 4 : SP_STEPS_EV2; }
+// entries per instance: 2 rows + 2 halves x EV2/2 x CAP events
+template <int CAP> __host__ __device__ constexpr int steps_arrays() { return 2 + steps_ev2<CAP>(); }
+__host__ __device__ inline int steps_arrays_rt(int cap) { return 2 + (cap >= 1024 ? 4 : SP_STEPS_EV2); }
+template <int CAP, typename E> __host__ __device__ constexpr int walk_depth() {
+  // as many prefetched stages (at most 8) as the instance's shared memory holds
+  // next to the placement and the row counts of a 128-stage instance
+  return (int)(((size_t)steps_arrays<CAP>() * CAP * sizeof(E) - 128 - 272) / (32 + 2 * 64 * 8)) >= 8
+             ? 8
+             : (int)(((size_t)steps_arrays<CAP>() * CAP * sizeof(E) - 128 - 272) / (32 + 2 * 64 * 8));
+}
 constexpr size_t kWalkSlot = 32 + 2 * 64 * 8;
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -368,8 +373,8 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : SP_STEPS_MINB) dp_ste
   using V = typename VT<MODE>::T;
   using E = Ent<MODE>;
   constexpr size_t INST_BYTES = (size_t)steps_arrays<CAP>() * CAP * sizeof(E);
-  constexpr int EVC = steps_ev<CAP>() * CAP;  // merge events per half
-  constexpr int kWalkDepth = walk_depth<CAP>();
+  constexpr int EVC = steps_ev2<CAP>() * CAP / 2;  // merge events per half
+  constexpr int kWalkDepth = walk_depth<CAP, E>();
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = lane >> 4, g = lane & 15;
@@ -496,11 +501,14 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : SP_STEPS_MINB) dp_ste
   // searched in the store instead)
   auto fetch = [&](int k) {
     if (k >= 1) {
-      unsigned char* sl = rbase + (size_t)(k & (kWalkDepth - 1)) * kWalkSlot;
+      unsigned char* sl = rbase + (size_t)(k % kWalkDepth) * kWalkSlot;
       const int2* er = g_ent + (size_t)(2 * k) * CAP;  // 16-B aligned: CAP is even
       const int fc = cnts[2 * k], fs = cnts[2 * k + 1];
-      if (fc <= 64 && 2 * lane < fc) cp_async16(sl + 32 + lane * 16, er + 2 * lane);
-      if (fs <= 64 && 2 * lane < fs) cp_async16(sl + 32 + 512 + lane * 16, er + CAP + 2 * lane);
+      // (a row of odd count: its last breakpoint alone, never the unwritten slot after it)
+      if (fc <= 64 && 2 * lane + 1 < fc) cp_async16(sl + 32 + lane * 16, er + 2 * lane);
+      else if (fc <= 64 && 2 * lane < fc) cp_async8(sl + 32 + lane * 16, er + 2 * lane);
+      if (fs <= 64 && 2 * lane + 1 < fs) cp_async16(sl + 32 + 512 + lane * 16, er + CAP + 2 * lane);
+      else if (fs <= 64 && 2 * lane < fs) cp_async8(sl + 32 + 512 + lane * 16, er + CAP + 2 * lane);
       if (lane == 0) cp_async16(sl, a.shifts + lo + k - 1);
     }
     cp_async_commit();
@@ -541,7 +549,7 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : SP_STEPS_MINB) dp_ste
       if (ring) {
         cp_async_wait<kWalkDepth - 1>();
         __syncwarp(kFull);
-        const unsigned char* sl = rbase + (size_t)(k & (kWalkDepth - 1)) * kWalkSlot;
+        const unsigned char* sl = rbase + (size_t)(k % kWalkDepth) * kWalkSlot;
         sh = *reinterpret_cast<const StageShift*>(sl);
         n = cnts[2 * k + (client ? 0 : 1)];
         if (n <= 64) {  // lane l holds breakpoints 2l and 2l + 1
