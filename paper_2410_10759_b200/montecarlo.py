@@ -53,11 +53,11 @@ class MonteCarloResult:
     dp_cells: float            # DP cells solved
 
 
-def solve_requests(req: dict, layer_lists) -> dict:
+def solve_requests(req, layer_lists) -> dict:
     """dp / greedy / all_server server loads and feasibility for every request
-    (device tensors)."""
+    (device tensors); `req` a host dict of arrays or a device RequestBatch."""
     eng = Engine(layer_lists)
-    sol = eng.solve(RequestBatch.from_numpy(**req).to(N.device()))
+    sol = eng.solve(req if isinstance(req, RequestBatch) else RequestBatch.from_numpy(**req).to(N.device()))
     out = {"dp": sol.policies}
     out["greedy"] = B.plan_prefix(sol.instances, N.SP_GREEDY)
     out["all_server"] = B.plan_prefix(sol.instances, N.SP_ALL_SERVER)
@@ -82,7 +82,10 @@ def scenario_tables(req: dict, off: np.ndarray, model_names, solved: dict):
     # sorts coordinates by name): a per-model lookup, not a sort of strings
     uniq = sorted(set(model_names))
     rank_of = torch.tensor([uniq.index(x) for x in model_names], dtype=torch.int64, device=dev)
-    col = lambda k, dt: torch.from_numpy(np.ascontiguousarray(req[k], dtype=dt)).to(dev)
+    if isinstance(req, RequestBatch):  # already on the device
+        col = lambda k, dt: getattr(req, k).to(dev, {np.int64: torch.int64, np.float64: torch.float64}[dt])
+    else:
+        col = lambda k, dt: torch.from_numpy(np.ascontiguousarray(req[k], dtype=dt)).to(dev)
     name_rank = rank_of[col("model", np.int64)]
     seq, dl, up, down = (col("seq_len", np.int64), col("deadline_s", np.float64), col("uplink_bps", np.float64),
                          col("downlink_bps", np.float64))
@@ -156,7 +159,7 @@ def run(scenario_ids=None, beta_per_ms: float = BETA_PER_MS, horizon: int = HORI
             if b[rank + 1] > b[rank] else None
         return _gather(local, sids, b, group)
 
-    req, layer_lists, off = W.cfg4(sids)
+    req, layer_lists, off = W.cfg4_device(sids, N.device())  # the grid expanded on the device
     solved = solve_requests(req, layer_lists)
     row_off, demand_d, dl_d = scenario_tables(req, off, W.CFG4_MODELS, solved)
     S = len(sids)

@@ -189,6 +189,51 @@ def cfg4(scenarios=None) -> tuple[dict, list, np.ndarray]:
             off)
 
 
+def cfg4_device(scenarios, device):
+    """cfg4 built on `device`: the 256 workload mixes are drawn on the host
+    (numpy, as `cfg4`), the grid's 4.2M requests are expanded from them on the
+    device -- the same values bit for bit (the deadline is the same IEEE
+    product and quotient).  Returns (RequestBatch on `device`, model layer
+    lists, scenario offsets [S+1] on the host)."""
+    import torch
+    from . import _native as N
+    from .requests import RequestBatch, _req_layout
+    cfps, sfps = calibrated_rates()
+    sids = np.asarray(scenarios, dtype=np.int64)
+    layer_lists = [model_layers(m) for m in CFG4_MODELS]
+    a, b, mix = (sids // 16) % 16, sids % 16, sids // 256
+    uniq, inv = np.unique(mix, return_inverse=True)
+    drawn = [_cfg4_mix(int(x)) for x in uniq]
+    um, us = np.stack([d[0] for d in drawn]), np.stack([d[1] for d in drawn])
+    uf = np.empty(um.shape)
+    for mi in range(len(CFG4_MODELS)):
+        sel = um == mi
+        vals, back = np.unique(us[sel], return_inverse=True)
+        uf[sel] = _total_flops_many(layer_lists[mi], vals)[back]
+    dev = torch.device(device)
+    t = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x)).to(dev, dt)
+    inv_d = t(inv.astype(np.int64), torch.int64)
+    n = len(sids) * CFG4_REQUESTS
+    _buf, v = N.packed(_req_layout(n), dev)
+    v["model"].view(-1, CFG4_REQUESTS).copy_(t(um, torch.int32)[inv_d])
+    v["seq_len"].view(-1, CFG4_REQUESTS).copy_(t(us, torch.int64)[inv_d])
+    # (the divisor as a device tensor: PyTorch's CUDA division by a Python
+    # scalar multiplies by its reciprocal, which is not numpy's quotient)
+    prod = t(CFG4_SCALES, torch.float64)[t(a, torch.int64)][:, None] * t(uf, torch.float64)[inv_d]
+    torch.div(prod, torch.full((1, 1), cfps, dtype=torch.float64, device=dev).expand_as(prod),
+              out=v["deadline_s"].view(-1, CFG4_REQUESTS))
+    bw = t(CFG4_BANDWIDTHS, torch.float64)[t(b, torch.int64)][:, None].expand(-1, CFG4_REQUESTS)
+    v["uplink_bps"].view(-1, CFG4_REQUESTS).copy_(bw)
+    v["downlink_bps"].view(-1, CFG4_REQUESTS).copy_(bw)
+    for k, val in (("client_fps", cfps), ("server_fps", sfps), ("propagation_s", PROP_S), ("unit_s", 1e-3),
+                   ("flags", SOURCE_CLIENT)):
+        v[k].fill_(val)
+    req = RequestBatch(**v)
+    req._buf = _buf
+    off = np.arange(len(sids) + 1, dtype=np.int64) * CFG4_REQUESTS
+    return req, layer_lists, off
+
+
 def cfg5(L: int = 100_000, W: int = 10_000_000, seed: int = 5) -> dict:
     """configs[4]: one huge chain via PlanProblem.from_costs (problem.py:179-185):
     i, s, u, d ~ U{0..200}, r ~ U{0..100} (integral floats), source at the

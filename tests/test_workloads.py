@@ -66,3 +66,17 @@ def test_lexsort_device_equals_numpy():
     keys = (rng.choice([3e7, 1e8, 1e9], n), rng.choice([3e7, 2e8], n), rng.random(n).round(2),
             rng.integers(128, 4096, n), rng.integers(0, 3, n), np.repeat(np.arange(n // 64 + 1), 64)[:n])
     assert np.array_equal(np.lexsort(keys), MC.lexsort_device(keys, device=torch.device("cpu")))
+
+
+def test_cfg4_device_expansion_is_bitwise_cfg4():
+    """The Monte-Carlo grid expanded on a device (here the CPU device) equals
+    the host generator field by field, bit for bit."""
+    import torch  # noqa: F401
+    sids = np.arange(0, 65536, 97)
+    req, _l, off = W.cfg4(sids)
+    rb, _l2, off2 = W.cfg4_device(sids, "cpu")
+    assert np.array_equal(off, off2)
+    for k, v in req.items():
+        a, b = np.asarray(v), getattr(rb, k).numpy()
+        assert a.dtype == b.dtype, k
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), k
