@@ -227,12 +227,15 @@ class PendingPlan:
     def __init__(self, batch, out, ws, pend, s, o, done: bool):
         self.batch, self.out, self.ws, self.pend, self.s, self.o = batch, out, ws, pend, s, o
         self.done = done
+        self.launched_more = False  # finish() queued kernels (instances the device-planned tier left)
 
     def finish(self) -> PolicyBatch:
         if not self.done:
             rc = N.library().sp_plan_dp_finish(self.s, self.o, N.ptr(self.ws), self.ws.numel(), N.stream_ptr(),
                                                N.ptr(self.pend))
             self.done = True
+            # the record's first word: instances the device-planned tier solved
+            self.launched_more = int(self.pend[:8].view(torch.int64)[0]) < self.batch.n
             _PEND_FREE.append(self.pend)  # its record is consumed: reusable
             N.check(rc, "sp_plan_dp_finish")
         return self.out

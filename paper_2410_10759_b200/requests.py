@@ -135,11 +135,36 @@ class Engine:
 
     def solve_slot(self, n: int, total_layers: int, ws_bytes: int) -> dict:
         """Everything one solve_async call writes -- workspace, cost table,
-        policies -- allocated once, for a pipelined caller to reuse (no
-        allocation inside its loop)."""
+        policies, the device copy of host request parameters -- allocated
+        once, for a pipelined caller to reuse (no allocation inside its loop)."""
+        buf, v = N.packed(_req_layout(n), self.device)
+        req = RequestBatch(**v)
+        req._buf = buf
         return dict(ws=torch.empty(ws_bytes, dtype=torch.uint8, device=self.device),
                     cost=self.cost_buffers(n, total_layers),
-                    pol=B.PolicyBatch.empty(n, int(total_layers), self.device))
+                    pol=B.PolicyBatch.empty(n, int(total_layers), self.device), req=req,
+                    k1_done=None, d2h_done=None)
+
+    def copy_stream(self) -> torch.cuda.Stream:
+        """The engine's stream for host <-> device copies of pipelined calls:
+        a step's request upload and its results' download overlap the
+        neighbouring steps' kernels."""
+        if getattr(self, "_copies", None) is None:
+            self._copies = torch.cuda.Stream(self.device)
+        return self._copies
+
+    def _upload(self, host_req: RequestBatch, slot: dict) -> RequestBatch:
+        """Host (pinned, packed) request parameters into the slot's device
+        buffer on the copy stream, once the slot's previous cost table has
+        read it; the compute stream waits for the copy."""
+        cs, cur = self.copy_stream(), torch.cuda.current_stream(self.device)
+        dreq = slot["req"]
+        if slot["k1_done"] is not None:
+            cs.wait_event(slot["k1_done"])
+        with torch.cuda.stream(cs):
+            dreq._buf.copy_(host_req._buf, non_blocking=True)
+        cur.wait_stream(cs)
+        return dreq
 
     def solve_async(self, req: RequestBatch, total_layers: int | None = None, off: torch.Tensor | None = None,
                     ws: torch.Tensor | None = None, slot: dict | None = None) -> "PendingSolve":
@@ -151,9 +176,25 @@ class Engine:
         results of a slot are valid until the slot is queued again)."""
         if total_layers is None:
             total_layers = int(self.n_layers[req.model.cpu().numpy()].sum())
+        if slot is not None and req.model.device.type == "cpu":  # host parameters: uploaded on the copy stream
+            req = self._upload(req, slot)
         inst, status, f = self.cost_table(req, total_layers, off, bufs=slot["cost"] if slot else None)
+        if slot is not None:
+            cur = torch.cuda.current_stream(self.device)
+            slot["k1_done"] = torch.cuda.Event()
+            slot["k1_done"].record(cur)
+            if slot["d2h_done"] is not None:  # the slot's previous results have been copied out
+                cur.wait_event(slot["d2h_done"])
         pend = B.plan_dp_async(inst, out=slot["pol"] if slot else None, ws=slot["ws"] if slot else ws)
-        return PendingSolve(pend, inst, status, f)
+        ps = PendingSolve(pend, inst, status, f, self, slot)
+        if slot is not None:
+            # the feasibility mask and the results' ready event are queued now,
+            # right behind this batch's kernels -- not behind the next batch's,
+            # which a pipelined caller queues before collecting this one
+            torch.mul(pend.out.feasible, status == 0, out=pend.out.feasible)
+            ps.ready = torch.cuda.Event()
+            ps.ready.record(torch.cuda.current_stream(self.device))
+        return ps
 
     def solve(self, req: RequestBatch, total_layers: int | None = None,
               off: torch.Tensor | None = None) -> Solved:
@@ -172,11 +213,38 @@ class Engine:
 class PendingSolve:
     """An Engine.solve_async call in flight."""
 
-    def __init__(self, pending: B.PendingPlan, inst: B.InstanceBatch, status: torch.Tensor, f: dict):
+    def __init__(self, pending: B.PendingPlan, inst: B.InstanceBatch, status: torch.Tensor, f: dict,
+                 engine: "Engine | None" = None, slot: dict | None = None):
         self.pending, self.inst, self.status, self.f = pending, inst, status, f
+        self.engine, self.slot = engine, slot
+        self.ready = None  # recorded behind the batch's kernels (slot calls)
 
     def result(self) -> Solved:
         pol = self.pending.finish()
-        torch.mul(pol.feasible, self.status == 0, out=pol.feasible)
+        if self.ready is None or self.pending.launched_more:
+            # (again after the kernels finish() queued: the mask is idempotent)
+            torch.mul(pol.feasible, self.status == 0, out=pol.feasible)
+            if self.ready is not None:
+                self.ready.record(torch.cuda.current_stream(self.engine.device))
         f = self.f
         return Solved(self.inst.layer_off, self.inst, pol, self.status, f["cs"], f["ss"], f["up"], f["dn"])
+
+    def result_to_host(self, into: B.PolicyBatch | None = None):
+        """result(), then the policies copied to pinned host memory on the
+        engine's copy stream (overlapping the next step's kernels).  Returns
+        (Solved, host PolicyBatch, event): read the host batch after the event."""
+        s = self.result()
+        eng = self.engine
+        cs, cur = eng.copy_stream(), torch.cuda.current_stream(eng.device)
+        ready = self.ready
+        if ready is None:
+            ready = torch.cuda.Event()
+            ready.record(cur)
+        cs.wait_event(ready)
+        with torch.cuda.stream(cs):
+            host = s.policies.to_host_async(into=into)
+        done = torch.cuda.Event()
+        done.record(cs)
+        if self.slot is not None:
+            self.slot["d2h_done"] = done
+        return s, host, done

@@ -623,3 +623,29 @@ def test_device_planned_tiers_in_waves(gpu, case, capfd, monkeypatch):
                    server_load=host["server_load"][k], integer_latency=host["integer_latency"][k],
                    feasible=host["feasible"][k])
         assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"{case}[{k}]")
+
+
+def test_engine_pipelined_host_requests_and_results(gpu):
+    """The pipelined public path bench.py's e2e leg times: host request
+    parameters uploaded into reused slots on the engine's copy stream,
+    results copied out there (result_to_host), three batches through two
+    slots -- exactly Engine.solve's results."""
+    import torch
+    from paper_2410_10759_b200 import _native as N, cost_model as cm, workloads as W
+    from paper_2410_10759_b200.requests import Engine, RequestBatch
+    eng = Engine([cm.build_preset("gpt2-24", 128).layers])
+    hosts = [RequestBatch.from_numpy(pin=True, **W.cfg2(400, seed)[0]) for seed in (11, 12, 13, 14)]
+    ref = [eng.solve(h.to(N.device())).policies.to_host() for h in hosts]
+    total = 400 * 98
+    slots = [eng.solve_slot(400, total, 512 << 20) for _ in range(2)]
+    prev, got = None, []
+    for k, h in enumerate(hosts + [None]):
+        cur = eng.solve_async(h, total, slot=slots[k & 1]) if h is not None else None
+        if prev is not None:
+            _s, host, done = prev.result_to_host()
+            got.append((host, done))
+        prev = cur
+    for (host, done), r in zip(got, ref):
+        done.synchronize()
+        for key in ("pi", "client_value", "server_load", "integer_latency", "feasible", "status"):
+            np.testing.assert_array_equal(r[key], getattr(host, key).numpy().astype(r[key].dtype), err_msg=key)
