@@ -307,6 +307,14 @@ def _l2_ceiling():
     return None, None
 
 
+_CLOCK_HINT = [None]
+
+
+def clock_mhz_hint():
+    """The median SM clock the timed region ran at (set once it is sampled)."""
+    return _CLOCK_HINT[0]
+
+
 def roofline(prof: Profile, step_ms_total: float) -> dict:
     peak, peak_kind = measured_peak_hbm()
     n = max(prof.n, 1)
@@ -334,8 +342,18 @@ def roofline(prof: Profile, step_ms_total: float) -> dict:
                                               "lts_throughput_pct", "dram_bytes_per_cell", "warp_inst_per_cell")}
     if prof.variant == 7:
         out["note"] = ("breakpoint lists: the algorithmic bytes are the stage records read (24 B/stage) and the "
-                       "breakpoints stored for the backtrack (8 B each + 4 B per row); the kernel is bound by "
-                       "instruction issue and shared-memory latency of its merges, not by HBM (DESIGN.md 4)")
+                       "breakpoints stored for the backtrack (8 B each + 8 B per row pair); the kernel is bound by "
+                       "instruction issue of its merges, not by HBM (DESIGN.md 4)")
+        if doc and doc.get("warp_inst_per_cell") and avg_ms > 0:
+            # the binding resource: warp-instruction issue, 4 schedulers x 148
+            # SMs x one instruction per clock (the SM clock sampled in the run)
+            inst = doc["warp_inst_per_cell"] * cells_per_launch
+            clk = (clock_mhz_hint() or 1965.0) * 1e6
+            peak_issue = 148 * 4 * clk
+            out["issue"] = {"bound": "warp-instruction issue", "achieved": inst / (avg_ms / 1e3),
+                            "peak": peak_issue, "unit": "warp-inst/s",
+                            "frac": inst / (avg_ms / 1e3) / peak_issue,
+                            "warp_inst_per_launch": inst, "source": src}
     if prof.variant == 4 and doc and rate:
         # the rows live in L2: the L2 bytes per cell (ncu) against the L2
         # ceiling measured with the kernel's own data path (tools/l2_bandwidth.cu)
@@ -582,6 +600,7 @@ def main():
         barrier()
     dev_ms = ev0.elapsed_time(ev1)
     clk = clocks.summary()
+    _CLOCK_HINT[0] = clk.get("sm_mhz") if isinstance(clk, dict) else None
 
     # ---- kernel accounting (a separate, instrumented pass) ----------------
     barrier()
