@@ -649,3 +649,40 @@ def test_engine_pipelined_host_requests_and_results(gpu):
         done.synchronize()
         for key in ("pi", "client_value", "server_load", "integer_latency", "feasible", "status"):
             np.testing.assert_array_equal(r[key], getattr(host, key).numpy().astype(r[key].dtype), err_msg=key)
+
+
+def test_tier1_waves_skip_an_instance_too_large_for_a_wave(gpu, capfd, monkeypatch):
+    """With the minimum workspace, a 1,500-stage instance's breakpoint store
+    (1,501 x 3 KB) exceeds what a wave may use: tier 1 runs the small ones in
+    waves and leaves it, flagged, to the dense kernels (tier 0).  All
+    placements bit-exact against the oracle."""
+    import torch
+    from paper_2410_10759_b200 import _native as N, batch as B
+    rng = np.random.default_rng(41)
+    insts = []
+    for t in range(40):
+        L, W = (1500, 600) if t == 17 else (12, 900)
+        insts.append(dict(i=rng.integers(0, 60, L), s=rng.integers(0, 60, L), u=rng.integers(0, 60, L),
+                          d=rng.integers(0, 60, L), r=rng.integers(0, 9, L).astype(float), budget=W,
+                          sac=bool(t % 2)))
+    off = np.zeros(len(insts) + 1, np.int64)
+    np.cumsum([len(x["r"]) for x in insts], out=off[1:])
+    cat = lambda k: np.concatenate([x[k] for x in insts])
+    b = B.InstanceBatch.from_arrays(off, cat("i"), cat("s"), cat("u"), cat("d"), cat("r"),
+                                    [x["budget"] for x in insts], [x["sac"] for x in insts])
+    mn, _full = B.dp_workspace_bytes(b)
+    lib = N.library()
+    ws = torch.empty(mn, dtype=torch.uint8, device=N.device())
+    out = B.PolicyBatch.empty(b.n, b.total_layers, b.r.device)
+    monkeypatch.setenv("SPLITPLAN_TRACE", "1")
+    rc = lib.sp_plan_dp(b.struct(), out.struct(), N.ptr(ws), mn, N.stream_ptr())
+    assert rc == 0, lib.sp_last_error()
+    err = capfd.readouterr().err
+    assert "tier-1 wave" in err and ("tier-0 wave 1" in err or "items planned" in err), err[-1500:]
+    host = out.to_host()
+    for k, inst in enumerate(insts):
+        exp = O.plan_dp(inst)
+        got = dict(pi=host["pi"][off[k]:off[k + 1]], client_value=host["client_value"][k],
+                   server_load=host["server_load"][k], integer_latency=host["integer_latency"][k],
+                   feasible=host["feasible"][k])
+        assert_policy(got, dict(exp, pi=tuple(exp["pi"])), f"big[{k}]")
