@@ -203,9 +203,15 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
     const int ilast = max(i1 - 1, 0), jlast = max(j1 - 1, 0);
     Ent<MODE> ea = A[min(i, ilast)], eb = B[min(j, jlast)];
     int cA = i < i1 ? ea.c + ha : COLM, cB = j < j1 ? eb.c + hb : COLM;
-    while (min(cA, cB) != COLM) {
-      const bool tA = cA <= cB, tB = cB <= cA;
+    // warp-uniform trip count (the most merged positions of any lane; an
+    // event consumes one or two) with every update predicated: no divergent
+    // loop to reconverge
+    const int kend = g == 15 ? ne : (ne * (g + 1)) >> 4;
+    const int trips = (int)__reduce_max_sync(kFull, (uint32_t)(kend - k0));
+    for (int it = 0; it < trips; ++it) {
       const int col = min(cA, cB);
+      const bool act = col != COLM;
+      const bool tA = act && cA <= cB, tB = act && cB <= cA;
       va = tA ? ea.v : va;
       vb = tB ? eb.v : vb;
       i += tA ? 1 : 0;
@@ -217,13 +223,13 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
       // after an event one side holds a breakpoint value: the max is reachable
       const V yn = steps_add<MODE>(steps_max<MODE>(va, vb), rk);
       const bool stay = va != NEG && steps_add<MODE>(va, rk) == yn;
-      const bool keep = yn != y;
-      fs_pre = (!kept && !keep && stay && fs_pre == kNoStay) ? col : fs_pre;
+      const bool keep = act && yn != y;
+      fs_pre = (act && !kept && !keep && stay && fs_pre == kNoStay) ? col : fs_pre;
       kept |= keep;
       nk += keep ? 1 : 0;
-      ev[k] = mk_ent<MODE>(stay ? (col | STAY) : col, yn);
-      y = yn;
-      ++k;
+      if (act) ev[k] = mk_ent<MODE>(stay ? (col | STAY) : col, yn);
+      y = act ? yn : y;
+      k += act ? 1 : 0;
     }
     kev = k;  // (a merged equal-column pair is one event: fewer events than merged positions)
   }
@@ -250,21 +256,24 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
     int pos = incl - nk, open = -1;
     int32_t ocol = 0, osf = kNoStay;  // the open breakpoint: column, stay_from found so far
     V prev = y0;
-    for (int k = k0; k < kev; ++k) {
-      const Ent<MODE> e = ev[k];
+    // (warp-uniform trip count, every update predicated)
+    const int nev = kev - k0;
+    const int trips = (int)__reduce_max_sync(kFull, (uint32_t)nev);
+    for (int it = 0; it < trips; ++it) {
+      const bool act = it < nev;
+      const Ent<MODE> e = ev[k0 + min(it, max(nev - 1, 0))];
       const int32_t col = e.c & COLM;
-      if (e.v != prev) {  // kept: the previous open breakpoint is complete
-        if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf);
-        out[pos] = mk_ent<MODE>(col, e.v);  // (pos < 2 CAP: past CAP only on overflow, inside this warp's region)
-        open = pos;
-        ocol = col;
-        osf = kNoStay;
-        ++pos;
-        c1 += col <= t1 ? 1 : 0;
-        c2 += col <= t2 ? 1 : 0;
-      }
-      osf = (e.c < 0 && osf == kNoStay) ? col : osf;  // bit 31: a stay event
-      prev = e.v;
+      const bool keep = act && e.v != prev;  // kept: the previous open breakpoint is complete
+      if (keep && open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf);
+      if (keep) out[pos] = mk_ent<MODE>(col, e.v);  // (pos < 2 CAP: past CAP only on overflow, inside this warp's region)
+      open = keep ? pos : open;
+      ocol = keep ? col : ocol;
+      osf = keep ? kNoStay : osf;
+      pos += keep ? 1 : 0;
+      c1 += (keep && col <= t1) ? 1 : 0;
+      c2 += (keep && col <= t2) ? 1 : 0;
+      osf = (act && e.c < 0 && osf == kNoStay) ? col : osf;  // bit 31: a stay event
+      prev = act ? e.v : prev;
     }
     if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf != kNoStay ? osf : tail_sf);
   }
