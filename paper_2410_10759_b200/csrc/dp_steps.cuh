@@ -203,15 +203,9 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
     const int ilast = max(i1 - 1, 0), jlast = max(j1 - 1, 0);
     Ent<MODE> ea = A[min(i, ilast)], eb = B[min(j, jlast)];
     int cA = i < i1 ? ea.c + ha : COLM, cB = j < j1 ? eb.c + hb : COLM;
-    // warp-uniform trip count (the most merged positions of any lane; an
-    // event consumes one or two) with every update predicated: no divergent
-    // loop to reconverge
-    const int kend = g == 15 ? ne : (ne * (g + 1)) >> 4;
-    const int trips = (int)__reduce_max_sync(kFull, (uint32_t)(kend - k0));
-    for (int it = 0; it < trips; ++it) {
+    while (min(cA, cB) != COLM) {
+      const bool tA = cA <= cB, tB = cB <= cA;
       const int col = min(cA, cB);
-      const bool act = col != COLM;
-      const bool tA = act && cA <= cB, tB = act && cB <= cA;
       va = tA ? ea.v : va;
       vb = tB ? eb.v : vb;
       i += tA ? 1 : 0;
@@ -223,13 +217,13 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
       // after an event one side holds a breakpoint value: the max is reachable
       const V yn = steps_add<MODE>(steps_max<MODE>(va, vb), rk);
       const bool stay = va != NEG && steps_add<MODE>(va, rk) == yn;
-      const bool keep = act && yn != y;
-      fs_pre = (act && !kept && !keep && stay && fs_pre == kNoStay) ? col : fs_pre;
+      const bool keep = yn != y;
+      fs_pre = (!kept && !keep && stay && fs_pre == kNoStay) ? col : fs_pre;
       kept |= keep;
       nk += keep ? 1 : 0;
-      if (act) ev[k] = mk_ent<MODE>(stay ? (col | STAY) : col, yn);
-      y = act ? yn : y;
-      k += act ? 1 : 0;
+      ev[k] = mk_ent<MODE>(stay ? (col | STAY) : col, yn);
+      y = yn;
+      ++k;
     }
     kev = k;  // (a merged equal-column pair is one event: fewer events than merged positions)
   }
