@@ -348,14 +348,16 @@ template <int CAP, typename E> __host__ __device__ constexpr int walk_depth() {
 }
 constexpr size_t kWalkSlot = 32 + 2 * 64 * 8;
 
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src)
-               : "memory");
-}
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                "l"(src)
+               : "memory");
+}
+// 16-B slot, `bytes` (0, 8 or 16) of them copied, the rest zero-filled: one
+// instruction for every lane instead of a divergent choice of copy sizes
+__device__ __forceinline__ void cp_async16_part(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -508,10 +510,10 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : SP_STEPS_MINB) dp_ste
       const int2* er = g_ent + (size_t)(2 * k) * CAP;  // 16-B aligned: CAP is even
       const int fc = cnts[2 * k], fs = cnts[2 * k + 1];
       // (a row of odd count: its last breakpoint alone, never the unwritten slot after it)
-      if (fc <= 64 && 2 * lane + 1 < fc) cp_async16(sl + 32 + lane * 16, er + 2 * lane);
-      else if (fc <= 64 && 2 * lane < fc) cp_async8(sl + 32 + lane * 16, er + 2 * lane);
-      if (fs <= 64 && 2 * lane + 1 < fs) cp_async16(sl + 32 + 512 + lane * 16, er + CAP + 2 * lane);
-      else if (fs <= 64 && 2 * lane < fs) cp_async8(sl + 32 + 512 + lane * 16, er + CAP + 2 * lane);
+      const int bc = fc <= 64 ? 8 * min(max(fc - 2 * lane, 0), 2) : 0;
+      const int bs = fs <= 64 ? 8 * min(max(fs - 2 * lane, 0), 2) : 0;
+      cp_async16_part(sl + 32 + lane * 16, er + 2 * lane, bc);
+      cp_async16_part(sl + 32 + 512 + lane * 16, er + CAP + 2 * lane, bs);
       if (lane == 0) cp_async16(sl, a.shifts + lo + k - 1);
     }
     cp_async_commit();
