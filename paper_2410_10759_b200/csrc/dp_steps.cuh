@@ -271,6 +271,9 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
     }
     if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf != kNoStay ? osf : tail_sf);
   }
+  // a row of odd count gets a padding entry, so the walk's 16-B pair copies
+  // only ever read written memory
+  if (g == 15 && (total & 1) && total < CAP) gent[total] = make_int2(COLM, kNoStay);
   // the half's sums, both halves in one reduction each (counts < 2^16)
   cnt1 = __reduce_add_sync(kFull, (uint32_t)c1 << hs);
   cnt2 = __reduce_add_sync(kFull, (uint32_t)c2 << hs);
@@ -408,6 +411,7 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : SP_STEPS_MINB) dp_ste
     rows[h * CAP] = mk_ent<MODE>(0, V(0));
     g_cnt[h] = n0;
     g_ent[h * CAP] = make_int2(0, kNoStay);
+    g_ent[h * CAP + 1] = make_int2(0x7fffffff, kNoStay);  // the pair's padding entry
   }
   __syncwarp(kFull);
   bool over = false;
@@ -510,10 +514,12 @@ __global__ void __launch_bounds__(WPB * 32, WPB == 1 ? 1 : SP_STEPS_MINB) dp_ste
       const int2* er = g_ent + (size_t)(2 * k) * CAP;  // 16-B aligned: CAP is even
       const int fc = cnts[2 * k], fs = cnts[2 * k + 1];
       // (a row of odd count: its last breakpoint alone, never the unwritten slot after it)
-      const int bc = fc <= 64 ? 8 * min(max(fc - 2 * lane, 0), 2) : 0;
-      const int bs = fs <= 64 ? 8 * min(max(fs - 2 * lane, 0), 2) : 0;
-      cp_async16_part(sl + 32 + lane * 16, er + 2 * lane, bc);
-      cp_async16_part(sl + 32 + 512 + lane * 16, er + CAP + 2 * lane, bs);
+      // (rows of odd count carry a padding entry: whole pairs; a lane with
+      // nothing to copy points at the always-written row counts)
+      const bool pc = fc <= 64 && 2 * lane < fc, ps = fs <= 64 && 2 * lane < fs;
+      cp_async16_part(sl + 32 + lane * 16, pc ? (const void*)(er + 2 * lane) : (const void*)g_cnt, pc ? 16 : 0);
+      cp_async16_part(sl + 32 + 512 + lane * 16, ps ? (const void*)(er + CAP + 2 * lane) : (const void*)g_cnt,
+                      ps ? 16 : 0);
       if (lane == 0) cp_async16(sl, a.shifts + lo + k - 1);
     }
     cp_async_commit();
