@@ -105,6 +105,10 @@ class CpuPool:
 
     def __init__(self, procs: int):
         from multiprocessing import get_context
+        # one thread per worker process (no BLAS / OpenMP oversubscription of
+        # the host cores the pool already covers)
+        for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ.setdefault(k, "1")
         self.procs = procs
         self.pool = get_context("fork").Pool(procs) if procs > 1 else None
 
