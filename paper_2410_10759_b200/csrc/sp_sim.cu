@@ -57,23 +57,27 @@ __device__ HeapEntry heap_pop(HeapEntry* h, int64_t& size, double& root_finish) 
     const int64_t f = 4 * c + 1;
     if (f >= size) break;
     const int nv = (int)min((int64_t)4, size - f);  // children past the end are not in the heap
-    HeapEntry ch[4];
+    HeapEntry c0, c1, c2, c3;
     if (nv == 4) {
       const EntryPair* g = reinterpret_cast<const EntryPair*>(h + f);
       const EntryPair p0 = g[0], p1 = g[1];
-      ch[0] = p0.a, ch[1] = p0.b, ch[2] = p1.a, ch[3] = p1.b;
+      c0 = p0.a, c1 = p0.b, c2 = p1.a, c3 = p1.b;
     } else {  // the last, partial group: only entries of the heap are read
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ch[q] = h[f + min(q, nv - 1)];
+      c0 = h[f];
+      c1 = h[f + min(1, nv - 1)];
+      c2 = h[f + min(2, nv - 1)];
+      c3 = h[f + min(3, nv - 1)];
     }
-    int best = 0;
-#pragma unroll
-    for (int q = 1; q < 4; ++q)
-      if (q < nv && less(ch[q], ch[best])) best = q;
-    if (!less(ch[best], last)) break;
-    if (c == 0) root_finish = ch[best].finish;
-    h[c] = ch[best];
-    c = f + best;
+    // the minimum child by selects (no indexed array: it would live in local memory)
+    HeapEntry best = c0;
+    int bi = 0;
+    if (nv > 1 && less(c1, best)) best = c1, bi = 1;
+    if (nv > 2 && less(c2, best)) best = c2, bi = 2;
+    if (nv > 3 && less(c3, best)) best = c3, bi = 3;
+    if (!less(best, last)) break;
+    if (c == 0) root_finish = best.finish;
+    h[c] = best;
+    c = f + bi;
   }
   if (size > 0) h[c] = last;
   return top;
