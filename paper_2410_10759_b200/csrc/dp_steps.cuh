@@ -35,8 +35,8 @@
 //
 // Work decomposition: one warp per instance; the two merges of a stage run
 // side by side, half-warp 0 building the C row and half-warp 1 the S row,
-// in lockstep (every ballot and shuffle is full-warp, every loop trip count
-// warp-uniform), so a stage costs one merge's latency chain.  A merge splits
+// in lockstep (every ballot and shuffle is full-warp), so a stage costs one
+// merge's latency chain.  A merge splits
 // the merged order of its two shifted lists into 16 equal diagonals (merge
 // path, one binary search per lane); each lane merges its part serially into
 // a scratch array at the merged positions -- every event carries the row
@@ -50,8 +50,10 @@
 // The same warp then walks the instance back (end-side choice, planner.py:
 // 182-202; _backtrace, planner.py:146-179) through the rows it has just
 // stored -- the stage records and the breakpoints of both candidate rows are
-// fetched kWalkDepth stages ahead -- and computes _finish (planner.py:88-101)
-// with the placement and the compacted r values in shared memory.
+// fetched kWalkDepth stages ahead, as whole 16-B breakpoint pairs (a row of
+// odd count carries a written padding entry) -- and computes _finish
+// (planner.py:88-101) with the placement and the compacted r values in shared
+// memory.
 //
 // Store of one instance (read by the walk): (L+1) rows x {C, S}, each a count
 // and CAP int2 {column, stay_from}, at a position the kernel computes itself
@@ -153,10 +155,12 @@ __device__ __forceinline__ Ent<MODE> mk_ent(int32_t c, V v) {
 //      kept iff its value differs from the previous slot's; the lane knows
 //      the value before its part, so it counts its own;
 //   2. a scan of the counts over the half places every lane's kept events;
-//   3. each lane re-reads its part and writes its kept breakpoints; a kept
-//      breakpoint's stay_from is the column of the first stay event from it
-//      up to the next kept one -- in the lane's own part, or in the first
-//      later part holding a kept or a stay event (one ballot).
+//   3. each lane re-reads its part and writes its kept breakpoints (a
+//      warp-uniform trip count with predicated updates: the data-dependent
+//      loop's reconvergence cost 8 % of the kernel); a kept breakpoint's
+//      stay_from is the column of the first stay event from it up to the
+//      next kept one -- in the lane's own part, or in the first later part
+//      holding a kept or a stay event (one ballot).
 template <int MODE, int CAP, typename V>
 __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int ha, const Ent<MODE>* B, int nb,
                                                 int hb, V rk, Ent<MODE>* ev, Ent<MODE>* out, int2* gent, int g,
