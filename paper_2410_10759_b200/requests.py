@@ -159,6 +159,8 @@ class Engine:
         read it; the compute stream waits for the copy."""
         cs, cur = self.copy_stream(), torch.cuda.current_stream(self.device)
         dreq = slot["req"]
+        if getattr(host_req, "_buf", None) is None:  # not packed: pack it (one copy still)
+            host_req = RequestBatch.from_numpy(**{f: getattr(host_req, f).numpy() for f in _REQ_FIELDS})
         if slot["k1_done"] is not None:
             cs.wait_event(slot["k1_done"])
         with torch.cuda.stream(cs):
@@ -176,8 +178,11 @@ class Engine:
         results of a slot are valid until the slot is queued again)."""
         if total_layers is None:
             total_layers = int(self.n_layers[req.model.cpu().numpy()].sum())
-        if slot is not None and req.model.device.type == "cpu":  # host parameters: uploaded on the copy stream
-            req = self._upload(req, slot)
+        if req.model.device.type == "cpu":  # host parameters
+            if slot is not None:  # uploaded on the copy stream into the slot
+                req = self._upload(req, slot)
+            else:
+                req = req.to(self.device, non_blocking=True)
         inst, status, f = self.cost_table(req, total_layers, off, bufs=slot["cost"] if slot else None)
         if slot is not None:
             cur = torch.cuda.current_stream(self.device)
