@@ -204,6 +204,8 @@ class Engine:
     def solve(self, req: RequestBatch, total_layers: int | None = None,
               off: torch.Tensor | None = None) -> Solved:
         """K1 cost table + DP placement for every request (one stream)."""
+        if req.model.device.type == "cpu":  # host parameters: one copy to the device
+            req = req.to(self.device)
         if total_layers is None:
             total_layers = int(self.n_layers[req.model.cpu().numpy()].sum())
         inst, status, f = self.cost_table(req, total_layers, off)
