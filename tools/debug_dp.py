@@ -25,7 +25,7 @@ def main():
     for p, r in zip(probs, rows):
         prof = cm.profile(cm.build_preset(r["model"], r["seq_len"]), client, server, r["metric"])
         p.r = np.array([x.r for x in prof])
-    for variant in ("auto", "smem", "cluster", "global"):
+    for variant in ("auto", "smem", "global", "stream", "steps"):
         os.environ["SPLITPLAN_DP_VARIANT"] = variant
         b = B.InstanceBatch.from_problems(probs)
         h = B.plan_dp(b).to_host()

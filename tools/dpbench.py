@@ -51,7 +51,7 @@ def main():
     from paper_2410_10759_b200 import _native as N
     from paper_2410_10759_b200 import batch as B
     lib = N.library()
-    names = ["smem", "cluster", "global", "coop", "stream", "grid", "own"]
+    names = {0: "smem", 2: "global", 4: "stream", 5: "grid", 7: "steps"}
     for W in [int(w) for w in args.W.split(",")]:
         n = args.n or max(148, int(1.2e10 / (args.L * (W + 1))))
         b = B.InstanceBatch.from_arrays(*make(n, args.L, W, 1, args.r))
@@ -67,7 +67,7 @@ def main():
         lib.sp_profile_collect(C.byref(ms), C.byref(nl), C.byref(cells), C.byref(byts), C.byref(al),
                                C.byref(var))
         lib.sp_profile_enable(0)
-        print(json.dumps({"W": W, "L": args.L, "n": n, "variant": names[var.value],
+        print(json.dumps({"W": W, "L": args.L, "n": n, "variant": names.get(var.value, str(var.value)),
                           "cells_per_s": cells.value / (ms.value / 1e3),
                           "kernel_ms": ms.value / max(nl.value, 1), "launches": nl.value,
                           "hbm_GBps_algorithmic": byts.value / (ms.value / 1e3) / 1e9}), flush=True)
