@@ -145,6 +145,19 @@ int sp_plan_dp_finish(const sp_instances* in, sp_policies* out, void* ws, size_t
 int sp_plan_dp_workspace_bytes(const sp_instances* in, size_t* min_bytes, size_t* full_bytes, void* ws,
                                size_t ws_bytes, void* stream);
 
+/* sp_plan_dp with HOST pointers in `in` and `out` (the scalar drop-in calls:
+ * planner.plan_dp on one problem, planner.py:182-202).  Each side's arrays
+ * are expected packed in one host buffer (alignment gaps allowed): the
+ * instances travel in one host-to-device copy, the policies back in one
+ * device-to-host copy, both through the front of `ws`; then the stream is
+ * synchronised.  SP_ERR_UNSUPPORTED when a side spans more than 64 MB. */
+int sp_plan_dp_host(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes, void* stream);
+
+/* sp_plan_prefix with host pointers, the same way (planner.plan_greedy /
+ * plan_trivial on one problem, planner.py:205-225). */
+int sp_plan_prefix_host(const sp_instances* in, int32_t which, sp_policies* out, void* ws, size_t ws_bytes,
+                        void* stream);
+
 /* Host arithmetic only (no device work): the workspace with which sp_plan_dp
  * runs the device-planned breakpoint-list tier of n instances of total_layers
  * stages in ONE wave (fixed part + every instance's store).  A caller sizing

@@ -144,6 +144,9 @@ SIGNATURES = {
     "sp_sim_replay": (C.c_int, [C.POINTER(SpSimBatch), C.POINTER(SpSimOut), P, C.c_size_t, P]),
     "sp_sim_skeletons": (C.c_int, [P, P, P, C.c_int64, C.c_int64, C.c_double, C.c_int64, P, P, P, P, P]),
     "sp_plan_dp_onewave_bytes": (C.c_size_t, [C.c_int64, C.c_int64]),
+    "sp_plan_dp_host": (C.c_int, [C.POINTER(SpInstances), C.POINTER(SpPolicies), P, C.c_size_t, P]),
+    "sp_plan_prefix_host": (C.c_int, [C.POINTER(SpInstances), C.c_int32, C.POINTER(SpPolicies), P, C.c_size_t,
+                                      P]),
 }
 
 _lib = None

@@ -250,6 +250,54 @@ def _pending_record() -> torch.Tensor:
     return _PEND_FREE.pop() if _PEND_FREE else torch.empty(N.SP_PENDING_BYTES, dtype=torch.uint8, pin_memory=True)
 
 
+def _host_packed(specs, arrays: dict | None = None):
+    """One host (numpy) buffer holding typed arrays at 256-B aligned offsets:
+    (buffer, {name: numpy view}); `arrays` fills them."""
+    offs, o = [], 0
+    for _name, numel, dt in specs:
+        o = (o + 255) & ~255
+        offs.append(o)
+        o += int(numel) * dt.itemsize
+    h = np.zeros(max(o, 1), dtype=np.uint8)
+    views = {name: h[off:off + int(numel) * dt.itemsize].view(N._NP_OF[dt])
+             for (name, numel, dt), off in zip(specs, offs)}
+    if arrays:
+        for name, v in views.items():
+            v[:] = arrays[name]
+    return h, views
+
+
+def plan_dp_host(layer_off, i, s, u, d, r, budget, sac, must=None, prefix: int | None = None) -> dict:
+    """plan_dp (or, with `prefix` = SP_GREEDY / SP_ALL_SERVER / SP_ALL_CLIENT,
+    plan_prefix) of a few host instances in one library call
+    (sp_plan_dp_host / sp_plan_prefix_host): the instances packed into one
+    host buffer go in with one copy, the policies come back with one copy --
+    the scalar drop-in's path.  Returns the host results (to_host's dict)."""
+    lo = np.asarray(layer_off, dtype=np.int64)
+    n, T = lo.size - 1, int(lo[-1]) if lo.size else 0
+    spec = [("layer_off", n + 1, torch.int64)] + [(k, T, torch.int64) for k in ("i", "s", "u", "d")]
+    spec += [("r", T, torch.float64), ("budget", n, torch.int64), ("sac", n, torch.uint8)]
+    arrays = dict(layer_off=lo, i=i, s=s, u=u, d=d, r=r, budget=budget, sac=sac)
+    if must is not None:
+        spec.append(("must", n, torch.int8))
+        arrays["must"] = must
+    hin, v = _host_packed(spec, arrays)
+    hout, o = _host_packed(_POLICY_LAYOUT(n, T))
+    addr = lambda a: a.ctypes.data
+    ins = N.SpInstances(n, T, *[addr(v[k]) for k in ("layer_off", "i", "s", "u", "d", "r", "budget", "sac")],
+                        addr(v["must"]) if must is not None else None)
+    outs = N.SpPolicies(addr(o["pi"]), addr(o["client_value"]), addr(o["server_load"]),
+                        addr(o["integer_latency"]), addr(o["feasible"]), addr(o["status"]))
+    lib = N.library()
+    if prefix is None:
+        rc = N.with_workspace(lambda ws, nb: lib.sp_plan_dp_host(ins, outs, ws, nb, N.stream_ptr()))
+    else:
+        rc = N.with_workspace(lambda ws, nb: lib.sp_plan_prefix_host(ins, prefix, outs, ws, nb, N.stream_ptr()))
+    N.check(rc, "sp_plan_dp_host" if prefix is None else "sp_plan_prefix_host")
+    return dict(pi=o["pi"], client_value=o["client_value"], server_load=o["server_load"],
+                integer_latency=o["integer_latency"], feasible=o["feasible"].astype(bool), status=o["status"])
+
+
 def plan_dp_async(batch: InstanceBatch, out: PolicyBatch | None = None,
                   ws: torch.Tensor | None = None) -> PendingPlan:
     """plan_dp without a stream synchronisation: the batch's device-planned

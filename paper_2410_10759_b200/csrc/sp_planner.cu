@@ -2211,6 +2211,110 @@ int sp_plan_dp(const sp_instances* in, sp_policies* out, void* ws, size_t ws_byt
   return run_dp(in, out, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+}  // extern "C"
+
+// The host-pointer entry points: both sides' (packed) host arrays copied
+// through the front of `ws`, `run(device instances, device policies, rest of
+// ws, its bytes, stream)` in between, then a stream synchronisation.
+template <typename Run>
+static int with_host_copies(const char* what, const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes,
+                            void* stream, Run run) {
+  int rc = validate(in);
+  if (rc) return rc;
+  rc = validate_out(out);
+  if (rc) return rc;
+  const int64_t n = in->n, T = in->total_layers;
+  if (n == 0) return SP_OK;
+  struct Field {
+    const void* p;
+    size_t bytes;
+  };
+  const Field fin[] = {{in->layer_off, 8 * (size_t)(n + 1)}, {in->client_units, 8 * (size_t)T},
+                       {in->server_units, 8 * (size_t)T},   {in->up_units, 8 * (size_t)T},
+                       {in->down_units, 8 * (size_t)T},     {in->r, 8 * (size_t)T},
+                       {in->budget, 8 * (size_t)n},         {in->source_at_client, (size_t)n},
+                       {in->must_end_at, in->must_end_at ? (size_t)n : 0}};
+  const Field fout[] = {{out->pi, (size_t)T},         {out->client_value, 8 * (size_t)n},
+                        {out->server_load, 8 * (size_t)n}, {out->integer_latency, 8 * (size_t)n},
+                        {out->feasible, (size_t)n},   {out->status, 4 * (size_t)n}};
+  // each side's fields as one span of host memory (callers pack them): one
+  // copy in, one copy out
+  auto span = [](const Field* f, int k, uintptr_t& lo, uintptr_t& hi) {
+    lo = UINTPTR_MAX;
+    hi = 0;
+    for (int i = 0; i < k; ++i)
+      if (f[i].p && f[i].bytes) {
+        lo = std::min(lo, (uintptr_t)f[i].p);
+        hi = std::max(hi, (uintptr_t)f[i].p + f[i].bytes);
+      }
+  };
+  uintptr_t ilo, ihi, olo, ohi;
+  span(fin, 9, ilo, ihi);
+  span(fout, 6, olo, ohi);
+  const size_t in_bytes = ihi - ilo, out_bytes = ohi - olo;
+  const size_t head = align_up(in_bytes, 256) + align_up(out_bytes, 256);
+  if (in_bytes > ((size_t)64 << 20) || out_bytes > ((size_t)64 << 20)) {
+    set_error(SP_ERR_UNSUPPORTED, "%s: the host arrays must be packed (spans of %zu / %zu B)", what,
+              in_bytes, out_bytes);
+    return SP_ERR_UNSUPPORTED;
+  }
+  if (!ws || ws_bytes < head) {
+    set_required_workspace(head + (1 << 20));
+    set_error(SP_ERR_WORKSPACE, "%s needs %zu B for the copies", what, head);
+    return SP_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* din = (uint8_t*)ws;
+  uint8_t* dout = din + align_up(in_bytes, 256);
+  auto dev = [](const void* p, uintptr_t lo, uint8_t* base) -> void* {
+    return p ? (void*)(base + ((uintptr_t)p - lo)) : nullptr;
+  };
+  rc = check_cuda(cudaMemcpyAsync(din, (const void*)ilo, in_bytes, cudaMemcpyHostToDevice, st), "copy instances in");
+  if (!rc) rc = check_cuda(cudaMemsetAsync(dout, 0, out_bytes, st), "zero policies");
+  if (rc) return rc;
+  sp_instances di = *in;
+  di.layer_off = (const int64_t*)dev(in->layer_off, ilo, din);
+  di.client_units = (const int64_t*)dev(in->client_units, ilo, din);
+  di.server_units = (const int64_t*)dev(in->server_units, ilo, din);
+  di.up_units = (const int64_t*)dev(in->up_units, ilo, din);
+  di.down_units = (const int64_t*)dev(in->down_units, ilo, din);
+  di.r = (const double*)dev(in->r, ilo, din);
+  di.budget = (const int64_t*)dev(in->budget, ilo, din);
+  di.source_at_client = (const uint8_t*)dev(in->source_at_client, ilo, din);
+  di.must_end_at = (const int8_t*)dev(in->must_end_at, ilo, din);
+  sp_policies dp_ = *out;
+  dp_.pi = (uint8_t*)dev(out->pi, olo, dout);
+  dp_.client_value = (double*)dev(out->client_value, olo, dout);
+  dp_.server_load = (double*)dev(out->server_load, olo, dout);
+  dp_.integer_latency = (int64_t*)dev(out->integer_latency, olo, dout);
+  dp_.feasible = (uint8_t*)dev(out->feasible, olo, dout);
+  dp_.status = (int32_t*)dev(out->status, olo, dout);
+  rc = run(&di, &dp_, (uint8_t*)ws + head, ws_bytes - head, st);
+  if (rc == SP_ERR_WORKSPACE) set_required_workspace(head + sp_last_required_workspace());
+  if (rc) return rc;
+  rc = check_cuda(cudaMemcpyAsync((void*)olo, dout, out_bytes, cudaMemcpyDeviceToHost, st), "copy policies out");
+  if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "sync");
+  return rc;
+}
+
+
+extern "C" {
+
+int sp_plan_dp_host(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes, void* stream) {
+  return with_host_copies("sp_plan_dp_host", in, out, ws, ws_bytes, stream,
+                          [](const sp_instances* di, sp_policies* dout, void* w, size_t wb, cudaStream_t st) {
+                            return run_dp(di, dout, nullptr, nullptr, w, wb, st);
+                          });
+}
+
+int sp_plan_prefix_host(const sp_instances* in, int32_t which, sp_policies* out, void* ws, size_t ws_bytes,
+                        void* stream) {
+  return with_host_copies("sp_plan_prefix_host", in, out, ws, ws_bytes, stream,
+                          [which](const sp_instances* di, sp_policies* dout, void*, size_t, cudaStream_t st) {
+                            return sp_plan_prefix(di, which, dout, st);
+                          });
+}
+
 int sp_plan_dp_async(const sp_instances* in, sp_policies* out, void* ws, size_t ws_bytes, void* stream,
                      void* pending) {
   int rc = validate(in);

@@ -105,13 +105,30 @@ def plan_many(name: str, problems: Sequence[PlanProblem],
     if must_end_at is not None:
         for m in must_end_at:
             _check_must(m)
-    batch = B.InstanceBatch.from_problems(problems, must_end_at)
     key = name.replace("-", "_")
-    res = plan_batch(name, batch)
     label = key if key in PLANNER_NAMES else name
     off = np.zeros(len(problems) + 1, dtype=np.int64)
     np.cumsum([p.n_layers for p in problems], out=off[1:])
+    prefix = {"greedy": N.SP_GREEDY, "all_server": N.SP_ALL_SERVER, "all_client": N.SP_ALL_CLIENT}.get(key)
+    if (key == "dp" or prefix is not None) and len(problems) <= SCALAR_BATCH and int(off[-1]) <= SCALAR_LAYERS:
+        # a few problems (the scalar drop-in calls): one library call, host
+        # arrays in and out (sp_plan_dp_host / sp_plan_prefix_host)
+        cat = lambda f: np.concatenate([np.asarray(getattr(p, f)) for p in problems])
+        must = None if must_end_at is None else \
+            np.array([-1 if m is None else (1 if m == "client" else 0) for m in must_end_at], dtype=np.int8)
+        host = B.plan_dp_host(off, cat("client_units"), cat("server_units"), cat("up_units"), cat("down_units"),
+                              cat("r"), [p.budget for p in problems], [p.source_at_client for p in problems],
+                              must, prefix=prefix)
+        return _policies(label, host, off)
+    batch = B.InstanceBatch.from_problems(problems, must_end_at)
+    res = plan_batch(name, batch)
     return _policies(label, res.to_host(), off)
+
+
+# problems per call (and their layers) below which plan_many("dp") takes the
+# one-call host path
+SCALAR_BATCH = 64
+SCALAR_LAYERS = 1 << 16
 
 
 def plan_dp(problem: PlanProblem, must_end_at: str | None = None) -> PlacementPolicy:
