@@ -167,8 +167,9 @@ def cpu_baseline(req_np: dict, seconds: float = 12.0) -> dict:
 
 class ClockSampler:
     """SM clocks and throttle reasons sampled DURING a timed region: NVML
-    polled every ~5 ms on a thread (a cfg2 step takes a few ms, too short for
-    nvidia-smi's loop), nvidia-smi -lms 100 if NVML is unavailable."""
+    polled every ~2 ms on a thread plus one sample taken as the region closes
+    (a cfg2 step takes about a millisecond, too short for nvidia-smi's loop),
+    nvidia-smi -lms 100 if NVML is unavailable."""
 
     REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
                ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -179,21 +180,31 @@ class ClockSampler:
         self.index = index
         self.sm: list[float] = []
         self.mx: list[float] = []
+        self.max_mhz = None
         self.reasons: set[str] = set()
         self.stop = threading.Event()
         self.source = "none"
+        self._nv = None
 
-    def _nvml_loop(self, nv, h):
-        bits = [(name, getattr(nv, attr, 0)) for name, attr in self.REASONS]
-        while not self.stop.is_set():
-            try:
-                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
-                self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.reasons.update(name for name, b in bits if b and r & b)
-            except Exception:
-                break
-            time.sleep(0.005)
+    def _nvml_sample(self) -> bool:
+        nv, h = self._nv
+        try:
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.reasons.update(name for name, b in self._bits if b and r & b)
+        except Exception:
+            return False
+        return True
+
+    def _nvml_loop(self):
+        while not self.stop.is_set() and self._nvml_sample():
+            time.sleep(0.002)
+
+    def sample_now(self):
+        """One synchronous sample, taken while the last timed launches still run
+        (a short timed region can end between two polls of the thread)."""
+        if self._nv is not None:
+            self._nvml_sample()
 
     def _smi_loop(self):
         fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -224,8 +235,11 @@ class ClockSampler:
             import pynvml as nv
             nv.nvmlInit()
             h = nv.nvmlDeviceGetHandleByIndex(self.index)
-            self.source = "nvml, 5 ms"
-            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._nv = (nv, h)
+            self._bits = [(name, getattr(nv, attr, 0)) for name, attr in self.REASONS]
+            self.source = "nvml, 2 ms + one sample at the end of the region"
+            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
         except Exception:
             self.source = "nvidia-smi, 100 ms"
             self.thread = threading.Thread(target=self._smi_loop, daemon=True)
@@ -246,7 +260,7 @@ class ClockSampler:
 
     def summary(self) -> dict:
         return {"sm_mhz": float(np.median(self.sm)) if self.sm else None,
-                "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
+                "sm_max_mhz": max(self.mx) if self.mx else self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(self.sm), "source": self.source}
 
 
@@ -605,6 +619,7 @@ def main():
         ev0.record(stream)
         run_device(args.steps)
         ev1.record(stream)
+        clocks.sample_now()
         barrier()
     dev_ms = ev0.elapsed_time(ev1)
     clk = clocks.summary()
