@@ -36,3 +36,31 @@ def test_reference_arm_under_torchrun_world2():
         assert k in d
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
     assert d["value"] > 0
+
+
+def test_clock_sampler_samples_short_regions(monkeypatch):
+    """bench.ClockSampler keeps only samples taken inside the timed region and
+    always has at least the one taken as the region closes (a 20-step cfg2
+    region lasts ~20 ms); throttle reasons map from NVML's bit mask."""
+    import types
+
+    nv = types.ModuleType("pynvml")
+    nv.NVML_CLOCK_SM = 0
+    nv.nvmlInit = lambda: None
+    nv.nvmlDeviceGetHandleByIndex = lambda i: i
+    nv.nvmlDeviceGetClockInfo = lambda h, c: 1965
+    nv.nvmlDeviceGetMaxClockInfo = lambda h, c: 1965
+    nv.nvmlDeviceGetCurrentClocksEventReasons = lambda h: 0x4
+    nv.nvmlClocksEventReasonSwPowerCap = 0x4
+    nv.nvmlClocksEventReasonHwSlowdown = 0x8
+    monkeypatch.setitem(sys.modules, "pynvml", nv)
+    sys.path.insert(0, str(ROOT))
+    try:
+        import bench
+    finally:
+        sys.path.remove(str(ROOT))
+    with bench.ClockSampler(0) as clocks:
+        clocks.sample_now()
+    s = clocks.summary()
+    assert s["samples"] >= 1 and s["sm_mhz"] == 1965.0 and s["sm_max_mhz"] == 1965.0
+    assert s["reasons"] == ["sw_power_cap"]
