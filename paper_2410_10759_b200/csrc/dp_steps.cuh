@@ -192,8 +192,6 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
   V y0;             // the row value just before this lane's part
   int nk = 0;       // kept events in this lane's part
   int kev;          // end of this lane's events in the scratch (k0 + events)
-  bool kept = false;
-  int32_t fs_pre = kNoStay;  // first stay event of this part before its first kept one
   {
     V va = i0 > 0 ? A[i0 - 1].v : NEG, vb = j0 > 0 ? B[j0 - 1].v : NEG;
     {
@@ -222,8 +220,6 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
       const V yn = steps_add<MODE>(steps_max<MODE>(va, vb), rk);
       const bool stay = va != NEG && steps_add<MODE>(va, rk) == yn;
       const bool keep = yn != y;
-      fs_pre = (!kept && !keep && stay && fs_pre == kNoStay) ? col : fs_pre;
-      kept |= keep;
       nk += keep ? 1 : 0;
       ev[k] = mk_ent<MODE>(stay ? (col | STAY) : col, yn);
       y = yn;
@@ -231,9 +227,7 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
     }
     kev = k;  // (a merged equal-column pair is one event: fewer events than merged positions)
   }
-  // 2. output positions (a scan of the kept counts over the half) and the
-  // stay_from of a segment running past this lane's part: the first later
-  // lane with a kept event or an earlier stay event decides it
+  // 2. output positions (a scan of the kept counts over the half)
   int incl = nk;
 #pragma unroll
   for (int o = 1; o < 16; o <<= 1) {
@@ -241,10 +235,6 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
     if (g >= o) incl += t;
   }
   const int total = __shfl_sync(kFull, incl, hs + 15);
-  const uint32_t T = (__ballot_sync(kFull, kept || fs_pre != kNoStay) >> hs) & 0xffffu;
-  const uint32_t nxt = g == 15 ? 0u : (T >> (g + 1)) << (g + 1);
-  const int32_t tail_in = __shfl_sync(kFull, fs_pre, hs + (nxt ? __ffs(nxt) - 1 : g));
-  const int32_t tail_sf = nxt ? tail_in : kNoStay;
   __syncwarp(kFull);  // both halves are done reading the old rows
   // 3. this lane writes its kept breakpoints: the new row (over the old one)
   // and (column, stay_from) to the store; it counts the ones at columns
@@ -253,6 +243,7 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
   {
     int pos = incl - nk, open = -1;
     int32_t ocol = 0, osf = kNoStay;  // the open breakpoint: column, stay_from found so far
+    int32_t fs_pre = kNoStay;  // first stay event of this part before its first kept one
     V prev = y0;
     // (warp-uniform trip count, every update predicated)
     const int nev = kev - k0;
@@ -264,6 +255,7 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
       const bool keep = act && e.v != prev;  // kept: the previous open breakpoint is complete
       if (keep && open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf);
       if (keep) out[pos] = mk_ent<MODE>(col, e.v);  // (pos < 2 CAP: past CAP only on overflow, inside this warp's region)
+      fs_pre = (keep && open < 0) ? osf : fs_pre;
       open = keep ? pos : open;
       ocol = keep ? col : ocol;
       osf = keep ? kNoStay : osf;
@@ -273,6 +265,13 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
       osf = (act && e.c < 0 && osf == kNoStay) ? col : osf;  // bit 31: a stay event
       prev = act ? e.v : prev;
     }
+    if (open < 0) fs_pre = osf;
+    // the stay_from of a segment running past this lane's part: the first
+    // later lane with a kept event or an earlier stay event decides it
+    const uint32_t T = (__ballot_sync(kFull, nk > 0 || fs_pre != kNoStay) >> hs) & 0xffffu;
+    const uint32_t nxt = g == 15 ? 0u : (T >> (g + 1)) << (g + 1);
+    const int32_t tail_in = __shfl_sync(kFull, fs_pre, hs + (nxt ? __ffs(nxt) - 1 : g));
+    const int32_t tail_sf = nxt ? tail_in : kNoStay;
     if (open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf != kNoStay ? osf : tail_sf);
   }
   // a row of odd count gets a padding entry, so the walk's 16-B pair copies
