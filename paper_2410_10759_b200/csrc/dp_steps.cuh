@@ -218,7 +218,8 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
       cB = j < j1 ? eb.c + hb : COLM;
       // after an event one side holds a breakpoint value: the max is reachable
       const V yn = steps_add<MODE>(steps_max<MODE>(va, vb), rk);
-      const bool stay = va != NEG && steps_add<MODE>(va, rk) == yn;
+      // (int32: the add is exact, so va + rk == max(va, vb) + rk iff va >= vb)
+      const bool stay = va != NEG && (MODE == VM_INT32 ? va >= vb : steps_add<MODE>(va, rk) == yn);
       const bool keep = yn != y;
       nk += keep ? 1 : 0;
       ev[k] = mk_ent<MODE>(stay ? (col | STAY) : col, yn);
@@ -253,7 +254,7 @@ __device__ __forceinline__ int steps_merge_half(const Ent<MODE>* A, int na, int 
       const Ent<MODE> e = ev[k0 + min(it, max(nev - 1, 0))];
       const int32_t col = e.c & COLM;
       const bool keep = act && e.v != prev;  // kept: the previous open breakpoint is complete
-      if (keep && open >= 0 && open < CAP) gent[open] = make_int2(ocol, osf);
+      if (keep && (unsigned)open < (unsigned)CAP) gent[open] = make_int2(ocol, osf);
       if (keep) out[pos] = mk_ent<MODE>(col, e.v);  // (pos < 2 CAP: past CAP only on overflow, inside this warp's region)
       fs_pre = (keep && open < 0) ? osf : fs_pre;
       open = keep ? pos : open;
